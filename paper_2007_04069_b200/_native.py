@@ -1,0 +1,212 @@
+"""ctypes binding of the C-ABI engine (`include/autoplan_b200.h`).
+
+The engine has no CPU fallback: importing this module succeeds on a CPU-only
+machine (so the package and its host logic can be used and tested), but any
+compute call raises `EngineUnavailable` unless the in-tree
+`libautoplan_b200.so` is built and a CUDA device is present.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "libautoplan_b200.so"
+
+AP_OK = 0
+AP_ERR_INVALID = -1
+AP_ERR_CUDA = -2
+AP_ERR_UNSUPPORTED = -3
+AP_ERR_INFEASIBLE = -4
+
+OUTCOME_COMPLETE = 0
+OUTCOME_INCOMPLETE = 1
+OUTCOME_CONFLICT = 2
+
+
+class EngineUnavailable(RuntimeError):
+    """The CUDA engine cannot run here (library missing or no GPU)."""
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code: int, message: str):
+        super().__init__(f"[{code}] {message}")
+        self.code = code
+
+
+class GraphDesc(ctypes.Structure):
+    _fields_ = [
+        ("num_instructions", ctypes.c_int32),
+        ("opcode", ctypes.c_void_p),
+        ("rank", ctypes.c_void_p),
+        ("dims_offset", ctypes.c_void_p),
+        ("dims", ctypes.c_void_p),
+        ("operand_offset", ctypes.c_void_p),
+        ("operands", ctypes.c_void_p),
+        ("gte_element", ctypes.c_void_p),
+    ]
+
+
+class GraphInfo(ctypes.Structure):
+    _fields_ = [
+        ("num_slots", ctypes.c_int64),
+        ("num_classes", ctypes.c_int32),
+        ("num_links", ctypes.c_int32),
+        ("num_implications", ctypes.c_int64),
+        ("num_forced", ctypes.c_int32),
+    ]
+
+
+# every symbol the header declares: name -> (restype, argtypes)
+_VP = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I32 = ctypes.c_int32
+SIGNATURES: dict[str, tuple] = {
+    "ap_graph_create": (ctypes.c_int, [ctypes.POINTER(GraphDesc), ctypes.POINTER(_VP)]),
+    "ap_graph_destroy": (ctypes.c_int, [_VP]),
+    "ap_graph_get_info": (ctypes.c_int, [_VP, ctypes.POINTER(GraphInfo)]),
+    "ap_graph_export": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP]),
+    "ap_decision_create": (ctypes.c_int, [_VP, _VP, _VP, _I32, ctypes.POINTER(_VP)]),
+    "ap_decision_destroy": (ctypes.c_int, [_VP]),
+    "ap_propagate_batch": (ctypes.c_int, [_VP, _VP, _VP, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _VP, _VP]),
+    "ap_propagate_trace": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "ap_last_error": (ctypes.c_char_p, []),
+    "ap_version": (ctypes.c_char_p, []),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library(path: Path | str = LIB_PATH):
+    """Load the engine library and bind its C-ABI signatures (no GPU needed)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not Path(path).exists():
+                raise EngineUnavailable(
+                    f"{path} is not built; run `python -m paper_2007_04069_b200.build` (nvcc, sm_100a)"
+                )
+            lib = ctypes.CDLL(str(path))
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def require_device():
+    """The library plus a CUDA device, or EngineUnavailable."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise EngineUnavailable("no CUDA device: the B200 engine has no CPU fallback")
+    return load_library()
+
+
+def check(rc: int) -> None:
+    if rc != AP_OK:
+        msg = _lib.ap_last_error().decode(errors="replace") if _lib is not None else "unknown"
+        raise NativeError(rc, msg)
+
+
+def ptr(a) -> ctypes.c_void_p | None:
+    """Raw pointer of a numpy array or torch tensor (None passes through)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return ctypes.c_void_p(a.ctypes.data)
+    return ctypes.c_void_p(a.data_ptr())
+
+
+def stream_handle(stream=None) -> ctypes.c_void_p:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+class DeviceGraph:
+    """Per-graph engine tables (ap_graph_t).
+
+    The rule compile runs on the host at construction (so `export()` works
+    without a GPU); the tables are uploaded to `device_index` on first use.
+    """
+
+    def __init__(self, flat, device_index: int | None = None):
+        lib = load_library()
+        self.flat = flat
+        self.device_index = device_index
+        self._keep = [
+            np.ascontiguousarray(a) if a.size else np.zeros(1, dtype=a.dtype)
+            for a in (flat.opcode, flat.rank, flat.dims_offset, flat.dims, flat.operand_offset, flat.operands,
+                      flat.gte_element)
+        ]
+        desc = GraphDesc(flat.num_instructions, *[a.ctypes.data for a in self._keep])
+        handle = ctypes.c_void_p()
+        check(lib.ap_graph_create(ctypes.byref(desc), ctypes.byref(handle)))
+        self.handle = handle
+        info = GraphInfo()
+        check(lib.ap_graph_get_info(handle, ctypes.byref(info)))
+        self.num_slots = int(info.num_slots)
+        self.num_classes = int(info.num_classes)
+        self.num_links = int(info.num_links)
+        self.num_implications = int(info.num_implications)
+        self.num_forced = int(info.num_forced)
+        self._decisions: dict[tuple, DeviceDecision] = {}
+
+    def export(self) -> dict[str, np.ndarray]:
+        """Host copies of the compiled tables (tests / tooling)."""
+        cls = np.empty(max(self.num_slots, 1), dtype=np.int32)
+        forced = np.empty(max(self.num_classes, 1), dtype=np.uint8)
+        off = np.empty(self.num_classes + 1, dtype=np.int32)
+        tgt = np.empty(max(self.num_implications, 1), dtype=np.int32)
+        check(_lib.ap_graph_export(self.handle, ptr(cls), ptr(forced), ptr(off), ptr(tgt)))
+        return {
+            "class_of_slot": cls[: self.num_slots],
+            "class_forced": forced[: self.num_classes],
+            "imp_offset": off,
+            "imp_target": tgt[: self.num_implications],
+        }
+
+    def decision(self, slots: np.ndarray, is_candidate: np.ndarray) -> "DeviceDecision":
+        key = (slots.tobytes(), is_candidate.tobytes())
+        dec = self._decisions.get(key)
+        if dec is None:
+            dec = DeviceDecision(self, slots, is_candidate)
+            self._decisions[key] = dec
+        return dec
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and _lib is not None:
+            for d in self.__dict__.get("_decisions", {}).values():
+                d.close()
+            _lib.ap_graph_destroy(h)
+            self.handle = None
+
+
+class DeviceDecision:
+    """A decision set (ap_decision_t): seed / candidate slot positions."""
+
+    def __init__(self, graph: DeviceGraph, slots: np.ndarray, is_candidate: np.ndarray):
+        self.graph = graph
+        self.slots = np.ascontiguousarray(slots, dtype=np.int64)
+        self.is_candidate = np.ascontiguousarray(is_candidate, dtype=np.uint8)
+        self.n = int(self.slots.shape[0])
+        handle = ctypes.c_void_p()
+        check(_lib.ap_decision_create(graph.handle, ptr(self.slots) if self.n else None,
+                                      ptr(self.is_candidate) if self.n else None, self.n, ctypes.byref(handle)))
+        self.handle = handle
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and _lib is not None:
+            _lib.ap_decision_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        self.close()

@@ -1,0 +1,110 @@
+// Internal structures of the B200 plan-exploration engine (not part of the C-ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/autoplan_b200.h"
+
+namespace apb {
+
+void set_error(const std::string& msg);
+int cuda_fail(cudaError_t err, const char* what);
+
+#define AP_CUDA_CHECK(expr)                                   \
+  do {                                                        \
+    cudaError_t _e = (expr);                                  \
+    if (_e != cudaSuccess) return ::apb::cuda_fail(_e, #expr); \
+  } while (0)
+
+// Device buffer owned by a handle.
+template <typename T>
+struct DevBuf {
+  T* ptr = nullptr;
+  size_t n = 0;
+  int upload(const std::vector<T>& host) {
+    n = host.size();
+    if (n == 0) return AP_OK;
+    AP_CUDA_CHECK(cudaMalloc(&ptr, n * sizeof(T)));
+    AP_CUDA_CHECK(cudaMemcpy(ptr, host.data(), n * sizeof(T), cudaMemcpyHostToDevice));
+    return AP_OK;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    n = 0;
+  }
+};
+
+// One compiled rule of the reference sweep (sharding.py:155-202), kept only for
+// the exact-order trace kernel.  Program words: kind, site, then operands.
+enum RuleKind : int32_t { RULE_LINK = 0, RULE_DOT = 1, RULE_REDUCE = 2 };
+
+struct GraphTables {
+  // host copies
+  int32_t num_instr = 0;
+  int64_t num_slots = 0;
+  int32_t num_classes = 0;
+  int32_t num_links = 0;
+  std::vector<int64_t> slot_base;     // [N+1]
+  std::vector<int32_t> slot_owner;    // [S] position owning the slot
+  std::vector<int32_t> class_of_slot; // [S]
+  std::vector<uint8_t> slot_forced;   // [S] directly forced replicated
+  std::vector<uint8_t> class_forced;  // [C]
+  std::vector<int32_t> imp_offset;    // [C+1]
+  std::vector<uint16_t> imp_target;   // [T]
+  std::vector<int32_t> program;       // trace program (reference sweep order)
+  std::vector<int32_t> forced_list;   // forced slots in reference order
+
+  // device copies
+  DevBuf<uint16_t> d_slot_class;
+  DevBuf<uint8_t> d_class_forced;
+  DevBuf<int32_t> d_imp_offset;
+  DevBuf<uint16_t> d_imp_target;
+  DevBuf<int32_t> d_program;
+  DevBuf<int32_t> d_forced_list;
+  DevBuf<int64_t> d_slot_base;
+  DevBuf<int32_t> d_slot_owner;
+  int device = 0;
+  bool uploaded = false;
+};
+
+struct DecisionTables {
+  int32_t n = 0;
+  std::vector<int64_t> slots;
+  std::vector<uint16_t> dec_class;
+  std::vector<uint8_t> dec_flags;     // bit0 candidate, bit1 slot directly forced
+  std::vector<int32_t> first_same;    // [n] first position on the same tensor (U-seed pin rule)
+  DevBuf<uint16_t> d_dec_class;
+  DevBuf<uint8_t> d_dec_flags;
+  DevBuf<int32_t> d_first_same;
+  DevBuf<int64_t> d_slots;
+  const GraphTables* graph = nullptr;
+  bool uploaded = false;
+};
+
+int build_graph(const ap_graph_desc* desc, GraphTables* g);
+int ensure_graph_on_device(GraphTables* g);
+int ensure_decision_on_device(DecisionTables* d);
+int build_decision(const GraphTables* g, const int64_t* slots, const uint8_t* is_cand, int32_t n,
+                   DecisionTables* d);
+
+int launch_propagate(const GraphTables* g, const DecisionTables* d, const int8_t* seeds, int64_t batch,
+                     int64_t seed_stride, int8_t* slots_out, int64_t slots_stride, int8_t* cand_out,
+                     int64_t cand_stride, uint8_t* outcome, int32_t* counts, cudaStream_t stream);
+
+int run_trace(const GraphTables* g, const DecisionTables* d, const int8_t* seeds_host, const int8_t* init_host,
+              int8_t* slots_host,
+              int32_t* outcome_host, int32_t* site_out, cudaStream_t stream);
+
+}  // namespace apb
+
+struct ap_graph {
+  apb::GraphTables t;
+};
+struct ap_decision {
+  apb::DecisionTables t;
+};

@@ -1,0 +1,455 @@
+// K1 — batched sharding propagation on sm_100a.
+//
+// Replaces PropagationEngine.run (reference sharding.py:210-248) for a batch
+// of seed vectors.  One warp owns one plan at a time (persistent grid,
+// warp-strided over the batch).  Per plan:
+//   1. seed pass      lanes stride the decision positions; a P (R) seed marks
+//                     its link class in the warp's P (R) flag row (benign
+//                     same-value byte stores, no atomics);
+//   2. implications   lanes stride the classes; every P class marks its
+//                     implication targets R;
+//   3. class pass     status per class (P wins), conflict = any(P and R),
+//                     warp vote;
+//   4. candidates     per-position status, decided / newly counts (warp
+//                     reductions), optional per-position output;
+//   5. slots          16 slots per lane-iteration: two 16-byte class-id
+//                     loads, 16 table lookups, one 16-byte store.
+// Graph tables (slot->class, implication CSR, forced flags) are staged in
+// shared memory once per CTA when they fit, else read through L1/L2.
+#include <algorithm>
+
+#include "engine.h"
+
+namespace apb {
+namespace {
+
+constexpr int kWarps = 8;
+constexpr int kThreads = kWarps * 32;
+constexpr unsigned kFull = 0xffffffffu;
+
+struct PropParams {
+  const uint16_t* slot_class;
+  const uint8_t* class_forced;
+  const int32_t* imp_offset;
+  const uint16_t* imp_target;
+  const uint16_t* dec_class;
+  const uint8_t* dec_flags;
+  const int32_t* first_same;
+  int64_t S;
+  int32_t C, Cp, D, T, ncand;
+  const int8_t* seeds;
+  int64_t seed_stride, batch;
+  int8_t* slots_out;
+  int64_t slots_stride;
+  int8_t* cand_out;
+  int64_t cand_stride;
+  uint8_t* outcome;
+  int32_t* counts;
+  int stage_tables;  // copy tables to shared memory
+  // byte offsets of the staged tables inside dynamic shared memory
+  int off_slot_class, off_dec_class, off_dec_flags, off_forced, off_imp_off, off_imp_tgt, off_first_same,
+      off_scratch;
+};
+
+__host__ __device__ inline int64_t align16(int64_t x) { return (x + 15) & ~int64_t(15); }
+
+__device__ inline void copy_to_smem(uint8_t* dst, const void* src, int64_t bytes) {
+  const uint8_t* s = reinterpret_cast<const uint8_t*>(src);
+  for (int64_t i = threadIdx.x; i < bytes; i += blockDim.x) dst[i] = s[i];
+}
+
+__device__ inline uint32_t pack4(const int8_t* table, uint32_t c01, uint32_t c23) {
+  const uint32_t s0 = (uint8_t)table[c01 & 0xffffu];
+  const uint32_t s1 = (uint8_t)table[c01 >> 16];
+  const uint32_t s2 = (uint8_t)table[c23 & 0xffffu];
+  const uint32_t s3 = (uint8_t)table[c23 >> 16];
+  return s0 | (s1 << 8) | (s2 << 16) | (s3 << 24);
+}
+
+template <bool kVecSlots>
+__global__ void __launch_bounds__(kThreads) propagate_kernel(PropParams p) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  const uint16_t* slot_class = p.slot_class;
+  const uint16_t* dec_class = p.dec_class;
+  const uint8_t* dec_flags = p.dec_flags;
+  const uint8_t* class_forced = p.class_forced;
+  const int32_t* imp_offset = p.imp_offset;
+  const uint16_t* imp_target = p.imp_target;
+  const int32_t* first_same = p.first_same;
+  if (p.stage_tables) {
+    copy_to_smem(smem + p.off_slot_class, p.slot_class, p.S * 2);
+    copy_to_smem(smem + p.off_dec_class, p.dec_class, (int64_t)p.D * 2);
+    copy_to_smem(smem + p.off_dec_flags, p.dec_flags, p.D);
+    copy_to_smem(smem + p.off_forced, p.class_forced, p.C);
+    copy_to_smem(smem + p.off_imp_off, p.imp_offset, (int64_t)(p.C + 1) * 4);
+    copy_to_smem(smem + p.off_imp_tgt, p.imp_target, (int64_t)p.T * 2);
+    copy_to_smem(smem + p.off_first_same, p.first_same, (int64_t)p.D * 4);
+    __syncthreads();
+    slot_class = reinterpret_cast<const uint16_t*>(smem + p.off_slot_class);
+    dec_class = reinterpret_cast<const uint16_t*>(smem + p.off_dec_class);
+    dec_flags = smem + p.off_dec_flags;
+    class_forced = smem + p.off_forced;
+    imp_offset = reinterpret_cast<const int32_t*>(smem + p.off_imp_off);
+    imp_target = reinterpret_cast<const uint16_t*>(smem + p.off_imp_tgt);
+    first_same = reinterpret_cast<const int32_t*>(smem + p.off_first_same);
+  }
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  uint8_t* flagP = smem + p.off_scratch + (int64_t)warp * 3 * p.Cp;
+  uint8_t* flagR = flagP + p.Cp;
+  int8_t* table = reinterpret_cast<int8_t*>(flagR + p.Cp);
+
+  const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+  for (int64_t b = (int64_t)blockIdx.x * kWarps + warp; b < p.batch; b += nwarps) {
+    // 0. clear the flag rows (Cp is a multiple of 16)
+    for (int i = lane; i < (2 * p.Cp) / 16; i += 32) reinterpret_cast<uint4*>(flagP)[i] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+
+    // 1. seeds
+    const int8_t* srow = p.seeds + b * p.seed_stride;
+    bool conflict = false;
+    for (int j = lane; j < p.D; j += 32) {
+      const int v = srow[j];
+      if (v == 1) {
+        flagP[dec_class[j]] = 1;
+      } else if (v == 0) {
+        flagR[dec_class[j]] = 1;
+      } else if (v == 2) {
+        // an UNDECIDED seed conflicts iff its slot is already decided when it
+        // is applied: forced replicated, or pinned by an earlier P seed on the
+        // same tensor (sharding.py:116-118, 219-229)
+        if (dec_flags[j] & 2) conflict = true;
+        for (int k = first_same[j]; k < j; ++k)
+          if (srow[k] == 1) conflict = true;
+      }
+    }
+    __syncwarp();
+
+    // 2. implications of partitioned classes
+    for (int c = lane; c < p.C; c += 32) {
+      if (flagP[c]) {
+        const int e = imp_offset[c + 1];
+        for (int k = imp_offset[c]; k < e; ++k) flagR[imp_target[k]] = 1;
+      }
+    }
+    __syncwarp();
+
+    // 3. class statuses
+    for (int c = lane; c < p.C; c += 32) {
+      const bool isP = flagP[c] != 0;
+      const bool isR = (flagR[c] | class_forced[c]) != 0;
+      conflict |= isP && isR;
+      table[c] = isP ? 1 : (isR ? 0 : -1);
+    }
+    conflict = __any_sync(kFull, conflict);
+    __syncwarp();
+
+    // 4. candidate positions
+    int dP = 0, dR = 0, nP = 0, nR = 0;
+    int8_t* crow = p.cand_out ? p.cand_out + b * p.cand_stride : nullptr;
+    for (int j = lane; j < p.D; j += 32) {
+      const int s = table[dec_class[j]];
+      if (crow) crow[j] = (int8_t)s;
+      if (dec_flags[j] & 1) {
+        const bool seeded = srow[j] != -1;
+        dP += (s == 1);
+        dR += (s == 0);
+        nP += (s == 1) && !seeded;
+        nR += (s == 0) && !seeded;
+      }
+    }
+    dP = __reduce_add_sync(kFull, dP);
+    dR = __reduce_add_sync(kFull, dR);
+    nP = __reduce_add_sync(kFull, nP);
+    nR = __reduce_add_sync(kFull, nR);
+
+    // 5. all slots
+    if (p.slots_out) {
+      int8_t* orow = p.slots_out + b * p.slots_stride;
+      const int64_t full = p.S / 16;
+      if (kVecSlots) {
+        for (int64_t k = lane; k < full; k += 32) {
+          const uint4 ca = reinterpret_cast<const uint4*>(slot_class)[2 * k];
+          const uint4 cb = reinterpret_cast<const uint4*>(slot_class)[2 * k + 1];
+          uint4 o;
+          o.x = pack4(table, ca.x, ca.y);
+          o.y = pack4(table, ca.z, ca.w);
+          o.z = pack4(table, cb.x, cb.y);
+          o.w = pack4(table, cb.z, cb.w);
+          reinterpret_cast<uint4*>(orow)[k] = o;
+        }
+        for (int64_t s = full * 16 + lane; s < p.S; s += 32) orow[s] = table[slot_class[s]];
+      } else {
+        for (int64_t s = lane; s < p.S; s += 32) orow[s] = table[slot_class[s]];
+      }
+    }
+    if (lane == 0) {
+      p.outcome[b] = conflict ? AP_OUTCOME_CONFLICT
+                              : ((dP + dR == p.ncand) ? AP_OUTCOME_COMPLETE : AP_OUTCOME_INCOMPLETE);
+      if (p.counts) {
+        int4 cv = conflict ? make_int4(0, 0, 0, 0) : make_int4(dP, dR, nP, nR);
+        reinterpret_cast<int4*>(p.counts)[b] = cv;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// ---- exact-order replay (one thread) --------------------------------------
+
+struct TraceState {
+  int8_t* st;
+  const int64_t* base;
+  const int32_t* owner;
+  int conflict_site;
+};
+
+__device__ inline int tr_set(TraceState& t, int64_t s, int v, int site) {
+  const int cur = t.st[s];
+  if (cur == v) return 0;
+  if (cur != -1) {
+    t.conflict_site = site;
+    return -1;
+  }
+  if (v == 1) {
+    const int32_t o = t.owner[s];
+    const int64_t lo = t.base[o], hi = t.base[o + 1];
+    for (int64_t k = lo; k < hi; ++k)
+      if (t.st[k] == 1) {
+        t.conflict_site = site;
+        return -1;
+      }
+    t.st[s] = 1;
+    for (int64_t k = lo; k < hi; ++k)
+      if (t.st[k] == -1) t.st[k] = 0;
+  } else {
+    t.st[s] = (int8_t)v;
+  }
+  return 1;
+}
+
+__device__ inline int tr_link(TraceState& t, int64_t a, int64_t b, int site) {
+  const int va = t.st[a], vb = t.st[b];
+  if (va == vb) return 0;
+  if (va == -1) return tr_set(t, a, vb, site);
+  if (vb == -1) return tr_set(t, b, va, site);
+  t.conflict_site = site;
+  return -1;
+}
+
+#define TR(expr)              \
+  do {                        \
+    const int _r = (expr);    \
+    if (_r < 0) return -1;    \
+    changed |= _r;            \
+  } while (0)
+
+__global__ void trace_kernel(const int32_t* prog, int64_t prog_len, const int32_t* forced, int64_t nforced,
+                             const int64_t* dec_slots, const int8_t* seeds, int32_t D, int8_t* st,
+                             const int64_t* base, const int32_t* owner, int64_t S, int64_t cap, bool has_init,
+                             int32_t* result) {
+  TraceState t{st, base, owner, -1};
+  if (!has_init)
+    for (int64_t s = 0; s < S; ++s) st[s] = -1;
+  int status = 0;  // 0 fixed point, 1 conflict, 2 cap exceeded
+  for (int64_t i = 0; i < nforced && status == 0; ++i)
+    if (tr_set(t, forced[i], 0, owner[forced[i]]) < 0) status = 1;
+  for (int32_t j = 0; j < D && status == 0; ++j) {
+    const int v = seeds[j];
+    if (v == -1) continue;
+    const int64_t s = dec_slots[j];
+    if (tr_set(t, s, v == 2 ? -1 : v, owner[s]) < 0) status = 1;
+  }
+  auto sweep = [&](void) -> int {
+    int changed = 0;
+    int64_t pc = 0;
+    while (pc < prog_len) {
+      const int kind = prog[pc], site = prog[pc + 1];
+      if (kind == RULE_LINK) {
+        TR(tr_link(t, prog[pc + 2], prog[pc + 3], site));
+        pc += 4;
+      } else if (kind == RULE_DOT) {
+        const int64_t a = base[prog[pc + 2]], b = base[prog[pc + 3]], c = base[prog[pc + 4]];
+        TR(tr_link(t, a + 0, c + 0, site));
+        TR(tr_link(t, b + 1, c + 1, site));
+        TR(tr_link(t, a + 1, b + 0, site));
+        if (st[a] == 1 || st[c] == 1) {
+          TR(tr_set(t, b + 0, 0, site));
+          TR(tr_set(t, b + 1, 0, site));
+        }
+        if (st[b + 1] == 1 || st[c + 1] == 1) {
+          TR(tr_set(t, a + 0, 0, site));
+          TR(tr_set(t, a + 1, 0, site));
+        }
+        if (st[a + 1] == 1 || st[b] == 1) {
+          TR(tr_set(t, c + 0, 0, site));
+          TR(tr_set(t, c + 1, 0, site));
+        }
+        pc += 5;
+      } else {
+        const int32_t a = prog[pc + 2], out = prog[pc + 3], nr = prog[pc + 4];
+        const int32_t* red = prog + pc + 5;
+        bool anyP = false;
+        for (int k = 0; k < nr; ++k) anyP |= st[base[a] + red[k]] == 1;
+        if (anyP)
+          for (int64_t s = base[out]; s < base[out + 1]; ++s) TR(tr_set(t, s, 0, site));
+        bool outP = false;
+        for (int64_t s = base[out]; s < base[out + 1]; ++s) outP |= st[s] == 1;
+        if (outP)
+          for (int k = 0; k < nr; ++k) TR(tr_set(t, base[a] + red[k], 0, site));
+        pc += 5 + nr;
+      }
+    }
+    return changed;
+  };
+  if (status == 0) {
+    status = 2;
+    for (int64_t it = 0; it < cap; ++it) {
+      const int r = sweep();
+      if (r < 0) {
+        status = 1;
+        break;
+      }
+      if (r == 0) {
+        status = 0;
+        break;
+      }
+    }
+  }
+  result[0] = status;
+  result[1] = t.conflict_site;
+}
+
+int g_num_sms = -1;
+
+}  // namespace
+
+int launch_propagate(const GraphTables* g, const DecisionTables* d, const int8_t* seeds, int64_t batch,
+                     int64_t seed_stride, int8_t* slots_out, int64_t slots_stride, int8_t* cand_out,
+                     int64_t cand_stride, uint8_t* outcome, int32_t* counts, cudaStream_t stream) {
+  if (batch < 0 || (batch > 0 && (!seeds || !outcome)) || seed_stride < d->n ||
+      (slots_out && slots_stride < g->num_slots) || (cand_out && cand_stride < d->n)) {
+    set_error("ap_propagate_batch: bad arguments (null buffer or stride smaller than row)");
+    return AP_ERR_INVALID;
+  }
+  if (d->graph != g) {
+    set_error("ap_propagate_batch: decision set belongs to another graph");
+    return AP_ERR_INVALID;
+  }
+  if (batch == 0) return AP_OK;
+  PropParams p{};
+  p.slot_class = g->d_slot_class.ptr;
+  p.class_forced = g->d_class_forced.ptr;
+  p.imp_offset = g->d_imp_offset.ptr;
+  p.imp_target = g->d_imp_target.ptr;
+  p.dec_class = d->d_dec_class.ptr;
+  p.dec_flags = d->d_dec_flags.ptr;
+  p.first_same = d->d_first_same.ptr;
+  p.S = g->num_slots;
+  p.C = g->num_classes;
+  p.Cp = (int32_t)align16(std::max(g->num_classes, 1));
+  p.D = d->n;
+  p.T = (int32_t)g->imp_target.size();
+  int ncand = 0;
+  for (uint8_t f : d->dec_flags) ncand += f & 1;
+  p.ncand = ncand;
+  p.seeds = seeds;
+  p.seed_stride = seed_stride;
+  p.batch = batch;
+  p.slots_out = slots_out;
+  p.slots_stride = slots_stride;
+  p.cand_out = cand_out;
+  p.cand_stride = cand_stride;
+  p.outcome = outcome;
+  p.counts = counts;
+
+  int64_t off = 0;
+  auto place = [&](int64_t bytes) {
+    const int64_t o = off;
+    off += align16(bytes);
+    return (int)o;
+  };
+  p.off_slot_class = place(p.S * 2);
+  p.off_dec_class = place((int64_t)p.D * 2);
+  p.off_dec_flags = place(p.D);
+  p.off_forced = place(p.C);
+  p.off_imp_off = place((int64_t)(p.C + 1) * 4);
+  p.off_imp_tgt = place((int64_t)p.T * 2);
+  p.off_first_same = place((int64_t)p.D * 4);
+  const int64_t tables_bytes = off;
+  const int64_t scratch_bytes = (int64_t)kWarps * 3 * p.Cp;
+  const int64_t kSmemCap = 200 * 1024;
+  int64_t smem = tables_bytes + scratch_bytes;
+  p.stage_tables = 1;
+  if (smem > kSmemCap) {
+    p.stage_tables = 0;
+    smem = scratch_bytes;
+    p.off_scratch = 0;
+    if (smem > kSmemCap) {
+      set_error("ap_propagate_batch: too many link classes for the per-warp shared-memory scratch");
+      return AP_ERR_UNSUPPORTED;
+    }
+  } else {
+    p.off_scratch = (int)tables_bytes;
+  }
+  const bool vec = slots_out && (slots_stride % 16 == 0) && ((reinterpret_cast<uintptr_t>(slots_out) & 15) == 0);
+  auto kern = vec ? propagate_kernel<true> : propagate_kernel<false>;
+  AP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (g_num_sms < 0) {
+    int dev = 0;
+    AP_CUDA_CHECK(cudaGetDevice(&dev));
+    AP_CUDA_CHECK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  int per_sm = 0;
+  AP_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, (size_t)smem));
+  per_sm = std::max(per_sm, 1);
+  const int64_t want = (batch + kWarps - 1) / kWarps;
+  const int grid = (int)std::min<int64_t>(want, (int64_t)g_num_sms * per_sm);
+  kern<<<grid, kThreads, (size_t)smem, stream>>>(p);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int run_trace(const GraphTables* g, const DecisionTables* d, const int8_t* seeds_host, const int8_t* init_host,
+              int8_t* slots_host, int32_t* outcome_host, int32_t* site_out, cudaStream_t stream) {
+  const int64_t S = g->num_slots;
+  int8_t* d_seeds = nullptr;
+  int8_t* d_state = nullptr;
+  int32_t* d_res = nullptr;
+  AP_CUDA_CHECK(cudaMalloc(&d_seeds, std::max<int64_t>(d->n, 1)));
+  AP_CUDA_CHECK(cudaMalloc(&d_state, std::max<int64_t>(S, 1)));
+  AP_CUDA_CHECK(cudaMalloc(&d_res, 2 * sizeof(int32_t)));
+  if (d->n) AP_CUDA_CHECK(cudaMemcpyAsync(d_seeds, seeds_host, d->n, cudaMemcpyHostToDevice, stream));
+  if (init_host && S) AP_CUDA_CHECK(cudaMemcpyAsync(d_state, init_host, S, cudaMemcpyHostToDevice, stream));
+  int max_rank = 1;
+  for (int32_t q = 0; q < g->num_instr; ++q)
+    max_rank = std::max<int>(max_rank, (int)(g->slot_base[q + 1] - g->slot_base[q]));
+  const int64_t cap = std::max<int64_t>(2, (int64_t)g->num_instr * max_rank + 2);  // sharding.py:251-252
+  trace_kernel<<<1, 1, 0, stream>>>(g->d_program.ptr, (int64_t)g->program.size(), g->d_forced_list.ptr,
+                                    (int64_t)g->forced_list.size(), d->d_slots.ptr, d_seeds, d->n, d_state,
+                                    g->d_slot_base.ptr, g->d_slot_owner.ptr, S, cap, init_host != nullptr, d_res);
+  AP_CUDA_CHECK(cudaGetLastError());
+  int32_t res[2];
+  AP_CUDA_CHECK(cudaMemcpyAsync(res, d_res, sizeof(res), cudaMemcpyDeviceToHost, stream));
+  if (S) AP_CUDA_CHECK(cudaMemcpyAsync(slots_host, d_state, S, cudaMemcpyDeviceToHost, stream));
+  AP_CUDA_CHECK(cudaStreamSynchronize(stream));
+  cudaFree(d_seeds);
+  cudaFree(d_state);
+  cudaFree(d_res);
+  if (res[0] == 2) {
+    set_error("sharding propagation failed to reach a fixed point");
+    return AP_ERR_UNSUPPORTED;
+  }
+  *site_out = res[1];
+  if (res[0] == 1) {
+    *outcome_host = AP_OUTCOME_CONFLICT;
+  } else {
+    bool complete = true;
+    for (int32_t j = 0; j < d->n; ++j)
+      if ((d->dec_flags[j] & 1) && slots_host[d->slots[j]] == -1) complete = false;
+    *outcome_host = complete ? AP_OUTCOME_COMPLETE : AP_OUTCOME_INCOMPLETE;
+  }
+  return AP_OK;
+}
+
+}  // namespace apb
