@@ -1,6 +1,7 @@
 // C-ABI entry points (include/autoplan_b200.h): argument checks, handle
 // lifetime and the thread-local error string.
 #include <cstdio>
+#include <cstdlib>
 #include <new>
 #include <string>
 
@@ -28,6 +29,10 @@ static void release_graph(GraphTables* t) {
   t->d_forced_list.release();
   t->d_slot_base.release();
   t->d_slot_owner.release();
+  t->d_slot_desc.release();
+  t->d_slot_cls8.release();
+  t->d_imp_offset16.release();
+  t->d_imp_target8.release();
 }
 
 static void release_decision(DecisionTables* t) {
@@ -35,6 +40,10 @@ static void release_decision(DecisionTables* t) {
   t->d_dec_flags.release();
   t->d_first_same.release();
   t->d_slots.release();
+  t->d_dec_desc.release();
+  t->d_dec_masks.release();
+  t->d_dec_cls8.release();
+  t->d_class_ncand.release();
 }
 
 }  // namespace apb
@@ -145,6 +154,14 @@ int ap_propagate_batch(ap_graph_t g, ap_decision_t d, const int8_t* seeds_dev, i
   int rc = apb::ensure_graph_on_device(&g->t);
   if (rc == AP_OK) rc = apb::ensure_decision_on_device(&d->t);
   if (rc != AP_OK) return rc;
+  // descriptor-driven fast kernel when the graph / strides allow it, else the
+  // generic kernel (AP_PROPAGATE_GENERIC=1 forces the generic one, for tests)
+  const char* force = std::getenv("AP_PROPAGATE_GENERIC");
+  if (!(force && force[0] == '1') && batch > 0) {
+    rc = apb::launch_propagate_fast(&g->t, &d->t, seeds_dev, batch, seed_stride, slots_dev, slots_stride, cand_dev,
+                                    cand_stride, outcome_dev, counts_dev, static_cast<cudaStream_t>(stream));
+    if (rc != AP_ERR_UNSUPPORTED) return rc;
+  }
   return apb::launch_propagate(&g->t, &d->t, seeds_dev, batch, seed_stride, slots_dev, slots_stride, cand_dev,
                                cand_stride, outcome_dev, counts_dev, static_cast<cudaStream_t>(stream));
 }

@@ -59,7 +59,18 @@ struct GraphTables {
   std::vector<int32_t> program;       // trace program (reference sweep order)
   std::vector<int32_t> forced_list;   // forced slots in reference order
 
+  // fast-kernel tables (only when num_classes <= kMaxFastClasses)
+  bool fast = false;
+  std::vector<uint32_t> slot_desc;    // [nq_s * 4] chunk descriptors (see propagate_fast.cu)
+  std::vector<uint8_t> slot_cls8;     // [nq_s * 16] class id per slot, 0xFF padding
+  std::vector<uint16_t> imp_offset16; // [C+1]
+  std::vector<uint8_t> imp_target8;   // [T]
+
   // device copies
+  DevBuf<uint32_t> d_slot_desc;
+  DevBuf<uint8_t> d_slot_cls8;
+  DevBuf<uint16_t> d_imp_offset16;
+  DevBuf<uint8_t> d_imp_target8;
   DevBuf<uint16_t> d_slot_class;
   DevBuf<uint8_t> d_class_forced;
   DevBuf<int32_t> d_imp_offset;
@@ -78,6 +89,17 @@ struct DecisionTables {
   std::vector<uint16_t> dec_class;
   std::vector<uint8_t> dec_flags;     // bit0 candidate, bit1 slot directly forced
   std::vector<int32_t> first_same;    // [n] first position on the same tensor (U-seed pin rule)
+  // fast-kernel tables
+  bool fast = false;
+  int32_t ncand = 0;
+  std::vector<uint32_t> dec_desc;     // [nq_d * 8] chunk descriptors
+  std::vector<uint32_t> dec_masks;    // [nq_d] valid | candidate << 16 (permuted bit order)
+  std::vector<uint8_t> dec_cls8;      // [nq_d * 16]
+  std::vector<uint16_t> class_ncand;  // [C] candidate positions per class
+  DevBuf<uint32_t> d_dec_desc;
+  DevBuf<uint32_t> d_dec_masks;
+  DevBuf<uint8_t> d_dec_cls8;
+  DevBuf<uint16_t> d_class_ncand;
   DevBuf<uint16_t> d_dec_class;
   DevBuf<uint8_t> d_dec_flags;
   DevBuf<int32_t> d_first_same;
@@ -91,6 +113,16 @@ int ensure_graph_on_device(GraphTables* g);
 int ensure_decision_on_device(DecisionTables* d);
 int build_decision(const GraphTables* g, const int64_t* slots, const uint8_t* is_cand, int32_t n,
                    DecisionTables* d);
+
+constexpr int kMaxFastClasses = 255;  // class 255 is the padding marker of the fast tables
+constexpr int kFastMaxChunks = 8;     // decision positions <= 32 lanes * 8 chunks * 16
+
+void build_fast_graph(GraphTables* g);
+void build_fast_decision(const GraphTables* g, DecisionTables* d);
+// Returns AP_ERR_UNSUPPORTED (without setting an error) when the fast path does not apply.
+int launch_propagate_fast(const GraphTables* g, const DecisionTables* d, const int8_t* seeds, int64_t batch,
+                          int64_t seed_stride, int8_t* slots_out, int64_t slots_stride, int8_t* cand_out,
+                          int64_t cand_stride, uint8_t* outcome, int32_t* counts, cudaStream_t stream);
 
 int launch_propagate(const GraphTables* g, const DecisionTables* d, const int8_t* seeds, int64_t batch,
                      int64_t seed_stride, int8_t* slots_out, int64_t slots_stride, int8_t* cand_out,

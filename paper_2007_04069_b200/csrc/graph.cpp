@@ -294,7 +294,7 @@ int build_graph(const ap_graph_desc* desc, GraphTables* g) {
     for (int32_t t : v) g->imp_target.push_back((uint16_t)t);
     g->imp_offset[c + 1] = (int32_t)g->imp_target.size();
   }
-
+  build_fast_graph(g);
   return AP_OK;
 }
 
@@ -321,6 +321,14 @@ int ensure_graph_on_device(GraphTables* g) {
   if ((rc = g->d_forced_list.upload(g->forced_list)) != AP_OK) return rc;
   if ((rc = g->d_slot_base.upload(g->slot_base)) != AP_OK) return rc;
   if ((rc = g->d_slot_owner.upload(g->slot_owner)) != AP_OK) return rc;
+  if (g->fast) {
+    if ((rc = g->d_slot_desc.upload(g->slot_desc)) != AP_OK) return rc;
+    if ((rc = g->d_slot_cls8.upload(g->slot_cls8)) != AP_OK) return rc;
+    if ((rc = g->d_imp_offset16.upload(g->imp_offset16)) != AP_OK) return rc;
+    std::vector<uint8_t> tgt = g->imp_target8;
+    if (tgt.empty()) tgt.push_back(0);
+    if ((rc = g->d_imp_target8.upload(tgt)) != AP_OK) return rc;
+  }
   g->uploaded = true;
   return AP_OK;
 }
@@ -332,6 +340,12 @@ int ensure_decision_on_device(DecisionTables* d) {
   if ((rc = d->d_dec_flags.upload(d->dec_flags)) != AP_OK) return rc;
   if ((rc = d->d_first_same.upload(d->first_same)) != AP_OK) return rc;
   if ((rc = d->d_slots.upload(d->slots)) != AP_OK) return rc;
+  if (d->fast) {
+    if ((rc = d->d_dec_desc.upload(d->dec_desc)) != AP_OK) return rc;
+    if ((rc = d->d_dec_masks.upload(d->dec_masks)) != AP_OK) return rc;
+    if ((rc = d->d_dec_cls8.upload(d->dec_cls8)) != AP_OK) return rc;
+    if ((rc = d->d_class_ncand.upload(d->class_ncand)) != AP_OK) return rc;
+  }
   d->uploaded = true;
   return AP_OK;
 }
@@ -359,6 +373,7 @@ int build_decision(const GraphTables* g, const int64_t* slots, const uint8_t* is
     const bool same = i > 0 && g->slot_owner[slots[i - 1]] == g->slot_owner[s];
     d->first_same[i] = same ? d->first_same[i - 1] : i;
   }
+  build_fast_decision(g, d);
   return AP_OK;
 }
 

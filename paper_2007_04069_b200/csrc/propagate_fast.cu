@@ -1,0 +1,560 @@
+// K1 fast path — descriptor-driven batched propagation (graphs with <= 255
+// link classes, 16-byte aligned seed / output rows).
+//
+// Same closure as propagate.cu (see graph.cpp header), restructured so the
+// per-plan instruction count scales with the number of 16-wide chunks instead
+// of the number of slots:
+//
+// * slot chunk descriptor (static per graph, 16 B): the <= 8 distinct link
+//   classes of 16 consecutive slots plus four PRMT selectors.  Emitting 16
+//   slot statuses = <= 8 shared-memory table lookups, 3-6 PRMT to pack the
+//   looked-up statuses into an 8-byte table, 4 PRMT with the selectors, one
+//   16-byte store.  (BERT-48: every chunk has <= 4 distinct classes.)
+// * decision chunk descriptor (static per decision set, 32 B): the chunk's
+//   <= 8 local classes, one 16-bit position mask per local class and the
+//   selectors for per-candidate output.  The seed pass turns 16 seed bytes
+//   into P / R / U position masks with 3 LOP3 per word, then marks the
+//   local class flags with one AND per class.
+// * counts: decided P/R = sum over classes of (#candidates in class), newly =
+//   decided - seeded (popcounts of the P/R masks); UNDECIDED seeds take a
+//   per-position slow path.
+// * the next plan's seed chunks are prefetched into registers while the
+//   current plan is evaluated.
+// Bit order of the 16-bit position masks: position t = 4*i + b (word i, byte b)
+// is bit 8*b + i, which is what OR-ing (word_i & 0x01010101) << i produces.
+#include <algorithm>
+#include <cstring>
+#include <set>
+
+#include "engine.h"
+
+namespace apb {
+namespace {
+
+constexpr int kWarpsF = 8;
+constexpr int kThreadsF = kWarpsF * 32;
+constexpr unsigned kFullMask = 0xffffffffu;
+constexpr uint32_t kOnes = 0x01010101u;
+constexpr int kScratchPerWarp = 768;  // flagP[256] flagR[256] table[256]
+
+inline int perm_bit(int t) { return 8 * (t & 3) + (t >> 2); }
+
+// Local classes of one 16-wide chunk, first-appearance order.  Returns false
+// when the chunk has more than 8 distinct classes.
+bool local_classes(const int32_t* cls, int count, std::vector<int>* uniq, int local[16]) {
+  uniq->clear();
+  for (int t = 0; t < 16; ++t) {
+    const int c = t < count ? cls[t] : cls[0];
+    auto it = std::find(uniq->begin(), uniq->end(), c);
+    if (it == uniq->end()) {
+      if (uniq->size() == 8) return false;
+      uniq->push_back(c);
+      local[t] = (int)uniq->size() - 1;
+    } else {
+      local[t] = (int)(it - uniq->begin());
+    }
+  }
+  return true;
+}
+
+void pack_classes(const std::vector<int>& uniq, uint32_t* w0, uint32_t* w1) {
+  uint8_t b[8];
+  for (int j = 0; j < 8; ++j) b[j] = j < (int)uniq.size() ? (uint8_t)uniq[j] : 0xFF;
+  std::memcpy(w0, b, 4);
+  std::memcpy(w1, b + 4, 4);
+  if (uniq.size() <= 4) *w1 = 0xFFFFFFFFu;  // marker: four lookups suffice
+}
+
+void pack_selectors(const int local[16], uint32_t* z, uint32_t* w) {
+  uint32_t sel[4];
+  for (int j = 0; j < 4; ++j) {
+    sel[j] = 0;
+    for (int b = 0; b < 4; ++b) sel[j] |= (uint32_t)local[4 * j + b] << (4 * b);
+  }
+  *z = sel[0] | (sel[1] << 16);
+  *w = sel[2] | (sel[3] << 16);
+}
+
+}  // namespace
+
+void build_fast_graph(GraphTables* g) {
+  g->fast = g->num_classes <= kMaxFastClasses;
+  if (!g->fast) return;
+  const int64_t S = g->num_slots;
+  const int64_t nq = (S + 15) / 16;
+  g->slot_desc.assign(nq * 4, 0);
+  g->slot_cls8.assign(nq * 16, 0xFF);
+  std::vector<int> uniq;
+  int local[16];
+  for (int64_t q = 0; q < nq; ++q) {
+    const int count = (int)std::min<int64_t>(16, S - 16 * q);
+    for (int t = 0; t < count; ++t) g->slot_cls8[16 * q + t] = (uint8_t)g->class_of_slot[16 * q + t];
+    uint32_t* d = &g->slot_desc[4 * q];
+    if (!local_classes(&g->class_of_slot[16 * q], count, &uniq, local)) {
+      d[0] = 0xFFFFFFFFu;  // fallback: per-slot lookups through slot_cls8
+      continue;
+    }
+    pack_classes(uniq, &d[0], &d[1]);
+    pack_selectors(local, &d[2], &d[3]);
+  }
+  const int C = g->num_classes;
+  g->imp_offset16.assign(C + 1, 0);
+  g->imp_target8.assign(g->imp_target.size(), 0);
+  for (int c = 0; c <= C; ++c) g->imp_offset16[c] = (uint16_t)g->imp_offset[c];
+  for (size_t k = 0; k < g->imp_target.size(); ++k) g->imp_target8[k] = (uint8_t)g->imp_target[k];
+  if (g->imp_target.size() > 65535) g->fast = false;
+}
+
+void build_fast_decision(const GraphTables* g, DecisionTables* d) {
+  d->fast = g->fast && d->n <= 32 * kFastMaxChunks * 16 && d->n < 65536;
+  if (!d->fast) return;
+  const int n = d->n;
+  const int nq = (n + 15) / 16;
+  d->dec_desc.assign((size_t)nq * 8, 0);
+  d->dec_masks.assign(nq, 0);
+  d->dec_cls8.assign((size_t)nq * 16, 0xFF);
+  d->class_ncand.assign(256, 0);
+  d->ncand = 0;
+  std::vector<int32_t> cls(n);
+  for (int i = 0; i < n; ++i) {
+    cls[i] = g->class_of_slot[d->slots[i]];
+    d->dec_cls8[i] = (uint8_t)cls[i];
+    if (d->dec_flags[i] & 1) {
+      d->class_ncand[cls[i]]++;
+      d->ncand++;
+    }
+  }
+  std::vector<int> uniq;
+  int local[16];
+  for (int q = 0; q < nq; ++q) {
+    const int count = std::min(16, n - 16 * q);
+    uint32_t valid = 0, cand = 0;
+    for (int t = 0; t < count; ++t) {
+      valid |= 1u << perm_bit(t);
+      if (d->dec_flags[16 * q + t] & 1) cand |= 1u << perm_bit(t);
+    }
+    d->dec_masks[q] = valid | (cand << 16);
+    uint32_t* w = &d->dec_desc[(size_t)8 * q];
+    if (!local_classes(&cls[16 * q], count, &uniq, local)) {
+      w[0] = 0xFFFFFFFFu;  // fallback chunk
+      continue;
+    }
+    pack_classes(uniq, &w[0], &w[1]);
+    uint32_t m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int t = 0; t < count; ++t) m[local[t]] |= 1u << perm_bit(t);
+    w[2] = m[0] | (m[1] << 16);
+    w[3] = m[2] | (m[3] << 16);
+    w[4] = m[4] | (m[5] << 16);
+    w[5] = m[6] | (m[7] << 16);
+    pack_selectors(local, &w[6], &w[7]);
+  }
+}
+
+namespace {
+
+struct FastParams {
+  const uint4* slot_desc;
+  const uint8_t* slot_cls8;
+  const uint4* dec_desc;
+  const uint32_t* dec_masks;
+  const uint8_t* dec_cls8;
+  const uint8_t* forced;
+  const uint16_t* ncand;
+  const uint16_t* imp_off;
+  const uint8_t* imp_tgt;
+  const uint8_t* dec_flags;   // global, slow path only
+  const int32_t* first_same;  // global, slow path only
+  int32_t nq_s, nq_d, C, D, T, any_slot_fallback, ncand_total;
+  int64_t S;
+  const int8_t* seeds;
+  int64_t seed_stride, batch;
+  int8_t* slots_out;
+  int64_t slots_stride;
+  int8_t* cand_out;
+  int64_t cand_stride;
+  int cand_vec;
+  uint8_t* outcome;
+  int32_t* counts;
+  int off_slot_desc, off_slot_cls8, off_dec_desc, off_dec_masks, off_dec_cls8, off_forced, off_ncand, off_imp_off,
+      off_imp_tgt, off_scratch;
+};
+
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts_u8(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void stg_stream(void* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// address of byte `k` of packed class word `w` inside a 256-aligned table at `base`
+#define TBL_ADDR(w, base, k) __byte_perm((w), (base), 0x7650 + (k))
+
+// Status table of up to 8 local classes as two words (bytes = int8 statuses).
+__device__ __forceinline__ void local_table(uint32_t c03, uint32_t c47, uint32_t tb, uint32_t* lo, uint32_t* hi) {
+  const uint32_t s0 = lds_u8(TBL_ADDR(c03, tb, 0));
+  const uint32_t s1 = lds_u8(TBL_ADDR(c03, tb, 1));
+  const uint32_t s2 = lds_u8(TBL_ADDR(c03, tb, 2));
+  const uint32_t s3 = lds_u8(TBL_ADDR(c03, tb, 3));
+  *lo = __byte_perm(__byte_perm(s0, s1, 0x0040), __byte_perm(s2, s3, 0x0040), 0x5410);
+  if (c47 == 0xFFFFFFFFu) {
+    *hi = *lo;
+  } else {
+    const uint32_t s4 = lds_u8(TBL_ADDR(c47, tb, 0));
+    const uint32_t s5 = lds_u8(TBL_ADDR(c47, tb, 1));
+    const uint32_t s6 = lds_u8(TBL_ADDR(c47, tb, 2));
+    const uint32_t s7 = lds_u8(TBL_ADDR(c47, tb, 3));
+    *hi = __byte_perm(__byte_perm(s4, s5, 0x0040), __byte_perm(s6, s7, 0x0040), 0x5410);
+  }
+}
+
+__device__ __forceinline__ uint4 select16(uint32_t lo, uint32_t hi, uint32_t z, uint32_t w) {
+  uint4 o;
+  o.x = __byte_perm(lo, hi, z & 0xFFFF);
+  o.y = __byte_perm(lo, hi, z >> 16);
+  o.z = __byte_perm(lo, hi, w & 0xFFFF);
+  o.w = __byte_perm(lo, hi, w >> 16);
+  return o;
+}
+
+// P / R / U position masks of one 16-byte seed chunk (permuted bit order)
+__device__ __forceinline__ void seed_masks(uint4 s, uint32_t* xp, uint32_t* xr, uint32_t* xu) {
+  const uint32_t w[4] = {s.x, s.y, s.z, s.w};
+  uint32_t p = 0, r = 0, u = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t a = w[i], b = w[i] >> 1;
+    p |= ((a & ~b) & kOnes) << i;   // byte == 1 (bit0 set, bit1 clear)
+    r |= ((~a & ~b) & kOnes) << i;  // byte == 0
+    u |= ((~a & b) & kOnes) << i;   // byte == 2
+  }
+  *xp = p;
+  *xr = r;
+  *xu = u;
+}
+
+template <int MAXCH>
+__global__ void __launch_bounds__(kThreadsF) propagate_fast_kernel(FastParams p) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  // stage the static tables
+  auto stage = [&](int off, const void* src, int64_t bytes) {
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    uint4* d = reinterpret_cast<uint4*>(smem + off);
+    const int64_t n16 = bytes / 16;
+    for (int64_t i = threadIdx.x; i < n16; i += blockDim.x) d[i] = s[i];
+    const uint8_t* sb = reinterpret_cast<const uint8_t*>(src);
+    for (int64_t i = n16 * 16 + threadIdx.x; i < bytes; i += blockDim.x) smem[off + i] = sb[i];
+  };
+  stage(p.off_slot_desc, p.slot_desc, (int64_t)p.nq_s * 16);
+  if (p.any_slot_fallback) stage(p.off_slot_cls8, p.slot_cls8, (int64_t)p.nq_s * 16);
+  stage(p.off_dec_desc, p.dec_desc, (int64_t)p.nq_d * 32);
+  stage(p.off_dec_masks, p.dec_masks, (int64_t)p.nq_d * 4);
+  stage(p.off_dec_cls8, p.dec_cls8, (int64_t)p.nq_d * 16);
+  stage(p.off_forced, p.forced, p.C);
+  stage(p.off_ncand, p.ncand, 512);
+  stage(p.off_imp_off, p.imp_off, (int64_t)(p.C + 1) * 2);
+  stage(p.off_imp_tgt, p.imp_tgt, p.T);
+  __syncthreads();
+
+  const uint4* slot_desc = reinterpret_cast<const uint4*>(smem + p.off_slot_desc);
+  const uint8_t* slot_cls8 = smem + p.off_slot_cls8;
+  const uint4* dec_desc = reinterpret_cast<const uint4*>(smem + p.off_dec_desc);
+  const uint32_t* dec_masks = reinterpret_cast<const uint32_t*>(smem + p.off_dec_masks);
+  const uint8_t* dec_cls8 = smem + p.off_dec_cls8;
+  const uint8_t* forced = smem + p.off_forced;
+  const uint16_t* ncand = reinterpret_cast<const uint16_t*>(smem + p.off_ncand);
+  const uint16_t* imp_off = reinterpret_cast<const uint16_t*>(smem + p.off_imp_off);
+  const uint8_t* imp_tgt = smem + p.off_imp_tgt;
+
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  // per-warp scratch, 256-aligned in the shared window so table / flag
+  // addresses are base | class (one PRMT each)
+  const uint32_t smem_sa = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t scratch_sa = (smem_sa + (uint32_t)p.off_scratch + 255u) & ~255u;
+  uint8_t* scratch = smem + (scratch_sa - smem_sa) + warp * kScratchPerWarp;
+  uint8_t* flagP = scratch;
+  uint8_t* flagR = scratch + 256;
+  int8_t* table = reinterpret_cast<int8_t*>(scratch + 512);
+  const uint32_t fb = (uint32_t)__cvta_generic_to_shared(flagP);  // flagR = fb + 256
+  const uint32_t tb = fb + 512;
+
+  const int64_t nwarps = (int64_t)gridDim.x * kWarpsF;
+  int64_t b = (int64_t)blockIdx.x * kWarpsF + warp;
+  uint4 cur[MAXCH];
+#pragma unroll
+  for (int i = 0; i < MAXCH; ++i) {
+    const int q = lane + 32 * i;
+    cur[i] = (b < p.batch && q < p.nq_d) ? ldg_stream(p.seeds + b * p.seed_stride + 16 * q) : make_uint4(0, 0, 0, 0);
+  }
+
+  for (; b < p.batch; b += nwarps) {
+    // 0. clear flags (512 bytes: one 16-byte store per lane)
+    reinterpret_cast<uint4*>(scratch)[lane] = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+
+    // 1. seed pass
+    int nPs = 0, nRs = 0;
+    uint32_t anyU = 0;
+#pragma unroll
+    for (int i = 0; i < MAXCH; ++i) {
+      const int q = lane + 32 * i;
+      if (q < p.nq_d) {
+        uint32_t xp, xr, xu;
+        seed_masks(cur[i], &xp, &xr, &xu);
+        const uint32_t vm = dec_masks[q];
+        const uint32_t valid = vm & 0xFFFF, cand = vm >> 16;
+        xp &= valid;
+        xr &= valid;
+        anyU |= xu & valid;
+        nPs += __popc(xp & cand);
+        nRs += __popc(xr & cand);
+        const uint4 d0 = dec_desc[2 * q];
+        if ((d0.x & 0xFF) != 0xFF) {
+          const uint32_t mw[4] = {d0.z, d0.w, 0, 0};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t m = (j & 1) ? (mw[j >> 1] >> 16) : (mw[j >> 1] & 0xFFFF);
+            const uint32_t a = TBL_ADDR(d0.x, fb, j);
+            if (xp & m) sts_u8(a, 1);
+            if (xr & m) sts_u8(a + 256, 1);
+          }
+          if (d0.y != 0xFFFFFFFFu) {
+            const uint4 d1 = dec_desc[2 * q + 1];
+            const uint32_t mw2[2] = {d1.x, d1.y};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint32_t m = (j & 1) ? (mw2[j >> 1] >> 16) : (mw2[j >> 1] & 0xFFFF);
+              const uint32_t a = TBL_ADDR(d0.y, fb, j);
+              if (xp & m) sts_u8(a, 1);
+              if (xr & m) sts_u8(a + 256, 1);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            const uint32_t bit = 1u << (8 * (t & 3) + (t >> 2));
+            const uint32_t c = dec_cls8[16 * q + t];
+            if (xp & bit) flagP[c] = 1;
+            if (xr & bit) flagR[c] = 1;
+          }
+        }
+      }
+    }
+    const bool hasU = __any_sync(kFullMask, anyU != 0);
+    __syncwarp();
+
+    // prefetch the next plan's seeds while this one is evaluated
+    const int64_t bn = b + nwarps;
+#pragma unroll
+    for (int i = 0; i < MAXCH; ++i) {
+      const int q = lane + 32 * i;
+      if (bn < p.batch && q < p.nq_d) cur[i] = ldg_stream(p.seeds + bn * p.seed_stride + 16 * q);
+    }
+
+    // 2. implications of partitioned classes
+    for (int c = lane; c < p.C; c += 32) {
+      if (flagP[c]) {
+        const int e = imp_off[c + 1];
+        for (int k = imp_off[c]; k < e; ++k) flagR[imp_tgt[k]] = 1;
+      }
+    }
+    __syncwarp();
+
+    // 3. class statuses, conflict and decided counts
+    bool conflict = false;
+    uint32_t dPR = 0;  // decided P | decided R << 16
+    for (int c = lane; c < p.C; c += 32) {
+      const bool isP = flagP[c] != 0;
+      const bool isR = (flagR[c] | forced[c]) != 0;
+      conflict |= isP && isR;
+      table[c] = isP ? 1 : (isR ? 0 : -1);
+      const uint32_t nc = ncand[c];
+      dPR += isP ? nc : (isR ? (nc << 16) : 0u);
+    }
+    conflict = __any_sync(kFullMask, conflict);
+    dPR = __reduce_add_sync(kFullMask, dPR);
+    uint32_t sPR = __reduce_add_sync(kFullMask, (uint32_t)nPs | ((uint32_t)nRs << 16));
+    __syncwarp();
+
+    int dP = dPR & 0xFFFF, dR = dPR >> 16;
+    int nP = dP - (int)(sPR & 0xFFFF), nR = dR - (int)(sPR >> 16);
+    if (hasU) {
+      // UNDECIDED seeds: conflict rule and exact per-position newly counts
+      const int8_t* srow = p.seeds + b * p.seed_stride;
+      bool uconf = false;
+      int np = 0, nr = 0;
+      for (int j = lane; j < p.D; j += 32) {
+        const int v = srow[j];
+        if (v == 2) {
+          if (p.dec_flags[j] & 2) uconf = true;
+          for (int k = p.first_same[j]; k < j; ++k)
+            if (srow[k] == 1) uconf = true;
+        }
+        if ((p.dec_flags[j] & 1) && v == -1) {
+          const int s = table[dec_cls8[j]];
+          np += s == 1;
+          nr += s == 0;
+        }
+      }
+      conflict |= __any_sync(kFullMask, uconf);
+      nP = __reduce_add_sync(kFullMask, np);
+      nR = __reduce_add_sync(kFullMask, nr);
+    }
+
+    // 4. per-candidate statuses
+    if (p.cand_out) {
+      int8_t* crow = p.cand_out + b * p.cand_stride;
+      for (int q = lane; q < p.nq_d; q += 32) {
+        const uint4 d0 = dec_desc[2 * q];
+        if (p.cand_vec && (d0.x & 0xFF) != 0xFF) {
+          const uint4 d1 = dec_desc[2 * q + 1];
+          uint32_t lo, hi;
+          local_table(d0.x, d0.y, tb, &lo, &hi);
+          const uint4 o = select16(lo, hi, d1.z, d1.w);
+          if (16 * q + 16 <= p.D) {
+            reinterpret_cast<uint4*>(crow)[q] = o;
+          } else {
+            const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
+            for (int t = 0; 16 * q + t < p.D; ++t) crow[16 * q + t] = (int8_t)(ow[t >> 2] >> (8 * (t & 3)));
+          }
+        } else {
+          for (int t = 0; t < 16 && 16 * q + t < p.D; ++t) crow[16 * q + t] = table[dec_cls8[16 * q + t]];
+        }
+      }
+    }
+
+    // 5. all slot statuses
+    if (p.slots_out) {
+      int8_t* orow = p.slots_out + b * p.slots_stride;
+      for (int q = lane; q < p.nq_s; q += 32) {
+        const uint4 d = slot_desc[q];
+        uint4 o;
+        if ((d.x & 0xFF) != 0xFF) {
+          uint32_t lo, hi;
+          local_table(d.x, d.y, tb, &lo, &hi);
+          o = select16(lo, hi, d.z, d.w);
+        } else {
+          uint32_t ow[4] = {0, 0, 0, 0};
+          for (int t = 0; t < 16; ++t) ow[t >> 2] |= (uint32_t)(uint8_t)table[slot_cls8[16 * q + t]] << (8 * (t & 3));
+          o = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+        }
+        stg_stream(orow + 16 * q, o);
+      }
+    }
+    if (lane == 0) {
+      // complete iff every candidate is decided (sharding.py:246-247)
+      p.outcome[b] = conflict ? AP_OUTCOME_CONFLICT
+                              : ((dP + dR == p.ncand_total) ? AP_OUTCOME_COMPLETE : AP_OUTCOME_INCOMPLETE);
+      if (p.counts)
+        reinterpret_cast<int4*>(p.counts)[b] = conflict ? make_int4(0, 0, 0, 0) : make_int4(dP, dR, nP, nR);
+    }
+    __syncwarp();
+  }
+}
+
+template <int MAXCH>
+int launch_fast_t(const FastParams& p, int64_t smem, cudaStream_t stream) {
+  static int num_sms = -1;
+  auto kern = propagate_fast_kernel<MAXCH>;
+  AP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (num_sms < 0) {
+    int dev = 0;
+    AP_CUDA_CHECK(cudaGetDevice(&dev));
+    AP_CUDA_CHECK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  int per_sm = 0;
+  AP_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreadsF, (size_t)smem));
+  per_sm = std::max(per_sm, 1);
+  const int64_t want = (p.batch + kWarpsF - 1) / kWarpsF;
+  const int grid = (int)std::min<int64_t>(want, (int64_t)num_sms * per_sm);
+  kern<<<grid, kThreadsF, (size_t)smem, stream>>>(p);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+inline int64_t a16(int64_t x) { return (x + 15) & ~int64_t(15); }
+
+}  // namespace
+
+int launch_propagate_fast(const GraphTables* g, const DecisionTables* d, const int8_t* seeds, int64_t batch,
+                          int64_t seed_stride, int8_t* slots_out, int64_t slots_stride, int8_t* cand_out,
+                          int64_t cand_stride, uint8_t* outcome, int32_t* counts, cudaStream_t stream) {
+  if (!g->fast || !d->fast || d->n == 0) return AP_ERR_UNSUPPORTED;
+  const int nq_d = (d->n + 15) / 16;
+  const int64_t nq_s = (g->num_slots + 15) / 16;
+  auto aligned = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
+  if (seed_stride % 16 || !aligned(seeds) || seed_stride < 16 * nq_d) return AP_ERR_UNSUPPORTED;
+  if (slots_out && (slots_stride % 16 || !aligned(slots_out) || slots_stride < 16 * nq_s)) return AP_ERR_UNSUPPORTED;
+  FastParams p{};
+  p.slot_desc = reinterpret_cast<const uint4*>(g->d_slot_desc.ptr);
+  p.slot_cls8 = g->d_slot_cls8.ptr;
+  p.dec_desc = reinterpret_cast<const uint4*>(d->d_dec_desc.ptr);
+  p.dec_masks = d->d_dec_masks.ptr;
+  p.dec_cls8 = d->d_dec_cls8.ptr;
+  p.forced = g->d_class_forced.ptr;
+  p.ncand = d->d_class_ncand.ptr;
+  p.imp_off = g->d_imp_offset16.ptr;
+  p.imp_tgt = g->d_imp_target8.ptr;
+  p.dec_flags = d->d_dec_flags.ptr;
+  p.first_same = d->d_first_same.ptr;
+  p.nq_s = (int32_t)nq_s;
+  p.nq_d = nq_d;
+  p.C = g->num_classes;
+  p.D = d->n;
+  p.T = (int32_t)g->imp_target8.size();
+  p.any_slot_fallback = 0;
+  for (int64_t q = 0; q < nq_s; ++q)
+    if ((g->slot_desc[4 * q] & 0xFF) == 0xFF) p.any_slot_fallback = 1;
+  p.ncand_total = d->ncand;
+  p.S = g->num_slots;
+  p.seeds = seeds;
+  p.seed_stride = seed_stride;
+  p.batch = batch;
+  p.slots_out = slots_out;
+  p.slots_stride = slots_stride;
+  p.cand_out = cand_out;
+  p.cand_stride = cand_stride;
+  p.cand_vec = cand_out && cand_stride % 16 == 0 && aligned(cand_out);
+  p.outcome = outcome;
+  p.counts = counts;
+  int64_t off = 0;
+  auto place = [&](int64_t bytes) {
+    const int64_t o = off;
+    off += a16(bytes);
+    return (int)o;
+  };
+  p.off_slot_desc = place(nq_s * 16);
+  p.off_slot_cls8 = p.any_slot_fallback ? place(nq_s * 16) : 0;
+  p.off_dec_desc = place((int64_t)nq_d * 32);
+  p.off_dec_masks = place((int64_t)nq_d * 4);
+  p.off_dec_cls8 = place((int64_t)nq_d * 16);
+  p.off_forced = place(256);
+  p.off_ncand = place(512);
+  p.off_imp_off = place((int64_t)(p.C + 1) * 2);
+  p.off_imp_tgt = place(std::max(p.T, 1));
+  p.off_scratch = (int)off;
+  const int64_t smem = off + 256 + (int64_t)kWarpsF * kScratchPerWarp;
+  if (smem > 200 * 1024) return AP_ERR_UNSUPPORTED;
+  const int chunks = (nq_d + 31) / 32;
+  if (chunks <= 1) return launch_fast_t<1>(p, smem, stream);
+  if (chunks <= 2) return launch_fast_t<2>(p, smem, stream);
+  if (chunks <= 3) return launch_fast_t<3>(p, smem, stream);
+  if (chunks <= 4) return launch_fast_t<4>(p, smem, stream);
+  if (chunks <= 8) return launch_fast_t<8>(p, smem, stream);
+  return AP_ERR_UNSUPPORTED;
+}
+
+}  // namespace apb

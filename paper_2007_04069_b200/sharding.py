@@ -65,6 +65,11 @@ SEED_NONE = -1
 SEED_UNDECIDED = 2
 
 
+def pad16(n: int) -> int:
+    """Row stride (bytes) of seed / status rows: 16-byte multiple for vector loads and stores."""
+    return max(16, (n + 15) // 16 * 16)
+
+
 @dataclass(frozen=True)
 class ShardingSpec:
     """Per-dim statuses of one tensor, optionally with its extents."""
@@ -274,17 +279,17 @@ class PropagationEngine:
         dev, dec, pos, cand_slots = self._decision_for(cand, ((t, d) for t, d, _ in applied))
         # seeds after a seeding conflict are never applied (nor validated) by
         # the reference; the conflicting seed itself is the last applied one
-        row = np.full(max(dec.n, 1), SEED_NONE, dtype=np.int8)
+        row = np.full(pad16(dec.n), SEED_NONE, dtype=np.int8)
         for t, d, v in applied:
             row[pos[eng.slot(t, d)]] = SEED_UNDECIDED if v == _U else v
         seeded_slots = {eng.slot(t, d) for t, d, _ in applied}
         with torch.cuda.device(dev.device_index):
             seeds_d = torch.from_numpy(row).cuda().view(1, -1)
-            slots_d = torch.empty((1, max(eng.num_slots, 1)), dtype=torch.int8, device="cuda")
+            slots_d = torch.empty((1, self.slots_stride), dtype=torch.int8, device="cuda")
             outcome_d = torch.empty(1, dtype=torch.uint8, device="cuda")
             lib = _native.require_device()
             _native.check(
-                lib.ap_propagate_batch(dev.handle, dec.handle, _native.ptr(seeds_d), 1, max(dec.n, 1),
+                lib.ap_propagate_batch(dev.handle, dec.handle, _native.ptr(seeds_d), 1, len(row),
                                        _native.ptr(slots_d), slots_d.shape[1], None, 0, _native.ptr(outcome_d),
                                        None, _native.stream_handle())
             )
@@ -340,7 +345,7 @@ class PropagationEngine:
         b = seeds.shape[0]
         _native.check(
             lib.ap_propagate_batch(
-                dev.handle, dec.handle, _native.ptr(seeds), b, seeds.stride(0) if b else max(dec.n, 1),
+                dev.handle, dec.handle, _native.ptr(seeds), b, seeds.stride(0) if b else pad16(dec.n),
                 _native.ptr(slots), 0 if slots is None else slots.stride(0),
                 _native.ptr(statuses), 0 if statuses is None else statuses.stride(0),
                 _native.ptr(outcome), _native.ptr(counts), _native.stream_handle(stream),
@@ -372,7 +377,7 @@ class PropagationEngine:
             dev_bufs = []
             for _ in range(2):
                 d = {
-                    "seeds": torch.empty((chunk, max(n, 1)), dtype=torch.int8, device="cuda"),
+                    "seeds": torch.empty((chunk, pad16(n)), dtype=torch.int8, device="cuda")[:, :n],
                     "outcome": torch.empty(chunk, dtype=torch.uint8, device="cuda"),
                     "counts": torch.empty((chunk, 4), dtype=torch.int32, device="cuda"),
                 }
@@ -425,20 +430,24 @@ class PropagationEngine:
                 perm = torch.empty(dec.n, dtype=torch.long)
                 perm[torch.from_numpy(order)] = torch.arange(len(order))
                 s = s[:, perm.cuda()]
-            s = s.contiguous()
             b = s.shape[0]
+            row = pad16(dec.n)
+            if s.stride(0) != row or s.stride(1) != 1 or s.data_ptr() % 16:
+                padded = torch.empty((b, row), dtype=torch.int8, device="cuda")
+                padded[:, : dec.n].copy_(s)
+                s = padded[:, : dec.n]
             out = {
                 "outcome": torch.empty(b, dtype=torch.uint8, device="cuda"),
                 "counts": torch.empty((b, 4), dtype=torch.int32, device="cuda"),
             }
-            cand_t = torch.empty((b, max(dec.n, 1)), dtype=torch.int8, device="cuda") if want_statuses else None
+            cand_t = torch.empty((b, row), dtype=torch.int8, device="cuda") if want_statuses else None
             slots_t = None
             if want_slots:
                 stride = (eng.num_slots + 15) // 16 * 16 or 16
                 slots_t = torch.empty((b, stride), dtype=torch.int8, device="cuda")
             lib = _native.require_device()
             _native.check(
-                lib.ap_propagate_batch(dev.handle, dec.handle, _native.ptr(s), b, max(s.shape[1], 1),
+                lib.ap_propagate_batch(dev.handle, dec.handle, _native.ptr(s), b, row,
                                        _native.ptr(slots_t), 0 if slots_t is None else slots_t.shape[1],
                                        _native.ptr(cand_t), 0 if cand_t is None else cand_t.shape[1],
                                        _native.ptr(out["outcome"]), _native.ptr(out["counts"]),

@@ -43,7 +43,8 @@ def prefix_seed_batch(order, start: int, count: int, seed: int = BATCH_SEED, dev
 
     order_t = torch.as_tensor(np.asarray(order, dtype=np.int64), device=device)
     n = int(order_t.numel())
-    out = torch.empty((count, n), dtype=torch.int8, device=device)
+    # rows padded to a 16-byte stride (the fast kernel's vector loads); the view hides the pad
+    out = torch.full((count, max(16, (n + 15) // 16 * 16)), -1, dtype=torch.int8, device=device)[:, :n]
     pos = torch.arange(n, dtype=torch.int64, device=device)
     s0 = mix32(torch.tensor(seed & _M32, dtype=torch.int64))
     s1 = mix32(s0 ^ 0x5BD1E995)

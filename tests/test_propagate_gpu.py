@@ -156,6 +156,31 @@ def test_full_size_batch_against_oracle(cuda, name):
     assert ok.sum() > 0
 
 
+@pytest.mark.parametrize("name", ["bert48", "t5_large", "vgg19", "mlp2"])
+def test_fast_and_generic_kernels_agree(cuda, name, monkeypatch):
+    """Descriptor-driven fast kernel vs the generic kernel: identical outputs incl. conflict rows."""
+    g = graphs.generate(name)
+    dims = decision_dims(g, g.trainable_variables)
+    n = len(dims)
+    rng = np.random.default_rng(11)
+    seeds = np.concatenate([
+        random_prefix_seeds(rng, n, 300, rng.permutation(n)),
+        np.where(rng.random((40, n)) < 0.05, rng.integers(0, 3, size=(40, n)), -1).astype(np.int8),
+    ])
+    eng = PropagationEngine(g, dims)
+    fast = eng.run_batch(torch.from_numpy(seeds), want_slots=True)
+    monkeypatch.setenv("AP_PROPAGATE_GENERIC", "1")
+    generic = eng.run_batch(torch.from_numpy(seeds), want_slots=True)
+    for key in ("outcome", "counts", "statuses", "slots"):
+        assert torch.equal(fast[key], generic[key]), key
+
+
+@pytest.mark.parametrize("name", ["t5_block", "attention_block", "bert_base", "random_042"])
+def test_generic_kernel_matches_reference(cuda, name, monkeypatch):
+    monkeypatch.setenv("AP_PROPAGATE_GENERIC", "1")
+    test_batch_kernel_matches_reference(cuda, name)
+
+
 def test_properties_at_scale(cuda):
     """Size-independent properties: idempotence, monotonicity, order independence."""
     g = graphs.bert48()
