@@ -21,7 +21,8 @@
 // * the next plan's seed chunks are prefetched into registers while the
 //   current plan is evaluated.
 // Bit order of the 16-bit position masks: position t = 4*i + b (word i, byte b)
-// is bit 8*b + i, which is what OR-ing (word_i & 0x01010101) << i produces.
+// is bit 4*b + i: OR-ing (word_i & 0x01010101) << i puts it at 8*b + i, and
+// `squeeze` packs those nibbles into 16 bits.
 #include <algorithm>
 #include <cstring>
 #include <set>
@@ -37,7 +38,8 @@ constexpr unsigned kFullMask = 0xffffffffu;
 constexpr uint32_t kOnes = 0x01010101u;
 constexpr int kScratchPerWarp = 768;  // flagP[256] flagR[256] table[256]
 
-inline int perm_bit(int t) { return 8 * (t & 3) + (t >> 2); }
+// 16-bit position mask bit of chunk position t = 4*i + b (word i, byte b)
+inline int perm_bit(int t) { return 4 * (t & 3) + (t >> 2); }
 
 // Local classes of one 16-wide chunk, first-appearance order.  Returns false
 // when the chunk has more than 8 distinct classes.
@@ -229,7 +231,13 @@ __device__ __forceinline__ uint4 select16(uint32_t lo, uint32_t hi, uint32_t z, 
   return o;
 }
 
-// P / R / U position masks of one 16-byte seed chunk (permuted bit order)
+// Squeeze bits {8b + i : b, i < 4} into bits {4b + i}: one shift-or and one PRMT.
+__device__ __forceinline__ uint32_t squeeze(uint32_t x) {
+  const uint32_t y = x | (x >> 4);
+  return __byte_perm(y, 0u, 0x4420);
+}
+
+// P / R / U position masks of one 16-byte seed chunk (bit 4*b + i for word i, byte b)
 __device__ __forceinline__ void seed_masks(uint4 s, uint32_t* xp, uint32_t* xr, uint32_t* xu) {
   const uint32_t w[4] = {s.x, s.y, s.z, s.w};
   uint32_t p = 0, r = 0, u = 0;
@@ -240,9 +248,9 @@ __device__ __forceinline__ void seed_masks(uint4 s, uint32_t* xp, uint32_t* xr, 
     r |= ((~a & ~b) & kOnes) << i;  // byte == 0
     u |= ((~a & b) & kOnes) << i;   // byte == 2
   }
-  *xp = p;
-  *xr = r;
-  *xu = u;
+  *xp = squeeze(p);
+  *xr = squeeze(r);
+  *xu = squeeze(u);
 }
 
 template <int MAXCH>
@@ -345,7 +353,7 @@ __global__ void __launch_bounds__(kThreadsF) propagate_fast_kernel(FastParams p)
         } else {
 #pragma unroll
           for (int t = 0; t < 16; ++t) {
-            const uint32_t bit = 1u << (8 * (t & 3) + (t >> 2));
+            const uint32_t bit = 1u << (4 * (t & 3) + (t >> 2));
             const uint32_t c = dec_cls8[16 * q + t];
             if (xp & bit) flagP[c] = 1;
             if (xr & bit) flagR[c] = 1;
