@@ -31,8 +31,8 @@ static void release_graph(GraphTables* t) {
   t->d_slot_owner.release();
   t->d_slot_desc.release();
   t->d_slot_cls8.release();
-  t->d_imp_offset16.release();
-  t->d_imp_target8.release();
+  t->d_imp_bits.release();
+  t->d_forced_bits.release();
 }
 
 static void release_decision(DecisionTables* t) {

@@ -63,14 +63,16 @@ struct GraphTables {
   bool fast = false;
   std::vector<uint32_t> slot_desc;    // [nq_s * 4] chunk descriptors (see propagate_fast.cu)
   std::vector<uint8_t> slot_cls8;     // [nq_s * 16] class id per slot, 0xFF padding
-  std::vector<uint16_t> imp_offset16; // [C+1]
-  std::vector<uint8_t> imp_target8;   // [T]
+  std::vector<uint32_t> imp_bits;     // [C * 8] 256-bit implication row per class
+  std::vector<uint32_t> forced_bits;  // [8] forced-replicated classes
+  bool slot_all_k4 = false;           // every slot chunk has <= 4 classes, none falls back
+  int32_t slot_fallback_chunks = 0;
 
   // device copies
   DevBuf<uint32_t> d_slot_desc;
   DevBuf<uint8_t> d_slot_cls8;
-  DevBuf<uint16_t> d_imp_offset16;
-  DevBuf<uint8_t> d_imp_target8;
+  DevBuf<uint32_t> d_imp_bits;
+  DevBuf<uint32_t> d_forced_bits;
   DevBuf<uint16_t> d_slot_class;
   DevBuf<uint8_t> d_class_forced;
   DevBuf<int32_t> d_imp_offset;

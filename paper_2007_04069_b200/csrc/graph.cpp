@@ -324,10 +324,8 @@ int ensure_graph_on_device(GraphTables* g) {
   if (g->fast) {
     if ((rc = g->d_slot_desc.upload(g->slot_desc)) != AP_OK) return rc;
     if ((rc = g->d_slot_cls8.upload(g->slot_cls8)) != AP_OK) return rc;
-    if ((rc = g->d_imp_offset16.upload(g->imp_offset16)) != AP_OK) return rc;
-    std::vector<uint8_t> tgt = g->imp_target8;
-    if (tgt.empty()) tgt.push_back(0);
-    if ((rc = g->d_imp_target8.upload(tgt)) != AP_OK) return rc;
+    if ((rc = g->d_imp_bits.upload(g->imp_bits)) != AP_OK) return rc;
+    if ((rc = g->d_forced_bits.upload(g->forced_bits)) != AP_OK) return rc;
   }
   g->uploaded = true;
   return AP_OK;

@@ -99,12 +99,26 @@ void build_fast_graph(GraphTables* g) {
     pack_classes(uniq, &d[0], &d[1]);
     pack_selectors(local, &d[2], &d[3]);
   }
+  g->slot_fallback_chunks = 0;
+  g->slot_all_k4 = true;
+  for (int64_t q = 0; q < nq; ++q) {
+    if ((g->slot_desc[4 * q] & 0xFF) == 0xFF) {
+      g->slot_fallback_chunks++;
+      g->slot_all_k4 = false;
+    } else if (g->slot_desc[4 * q + 1] != 0xFFFFFFFFu) {
+      g->slot_all_k4 = false;
+    }
+  }
   const int C = g->num_classes;
-  g->imp_offset16.assign(C + 1, 0);
-  g->imp_target8.assign(g->imp_target.size(), 0);
-  for (int c = 0; c <= C; ++c) g->imp_offset16[c] = (uint16_t)g->imp_offset[c];
-  for (size_t k = 0; k < g->imp_target.size(); ++k) g->imp_target8[k] = (uint8_t)g->imp_target[k];
-  if (g->imp_target.size() > 65535) g->fast = false;
+  g->imp_bits.assign((size_t)std::max(C, 1) * 8, 0);
+  g->forced_bits.assign(8, 0);
+  for (int c = 0; c < C; ++c) {
+    for (int k = g->imp_offset[c]; k < g->imp_offset[c + 1]; ++k) {
+      const int t = g->imp_target[k];
+      g->imp_bits[(size_t)8 * c + (t >> 5)] |= 1u << (t & 31);
+    }
+    if (g->class_forced[c]) g->forced_bits[c >> 5] |= 1u << (c & 31);
+  }
 }
 
 void build_fast_decision(const GraphTables* g, DecisionTables* d) {
@@ -160,13 +174,12 @@ struct FastParams {
   const uint4* dec_desc;
   const uint32_t* dec_masks;
   const uint8_t* dec_cls8;
-  const uint8_t* forced;
-  const uint16_t* ncand;
-  const uint16_t* imp_off;
-  const uint8_t* imp_tgt;
-  const uint8_t* dec_flags;   // global, slow path only
-  const int32_t* first_same;  // global, slow path only
-  int32_t nq_s, nq_d, C, D, T, any_slot_fallback, ncand_total;
+  const uint32_t* forced_bits;  // [8]
+  const uint16_t* ncand;        // [256]
+  const uint32_t* imp_bits;     // [C * 8]
+  const uint8_t* dec_flags;     // global, slow path only
+  const int32_t* first_same;    // global, slow path only
+  int32_t nq_s, nq_d, C, D, any_slot_fallback, slot_all_k4, ncand_total;
   int64_t S;
   const int8_t* seeds;
   int64_t seed_stride, batch;
@@ -177,8 +190,7 @@ struct FastParams {
   int cand_vec;
   uint8_t* outcome;
   int32_t* counts;
-  int off_slot_desc, off_slot_cls8, off_dec_desc, off_dec_masks, off_dec_cls8, off_forced, off_ncand, off_imp_off,
-      off_imp_tgt, off_scratch;
+  int off_slot_desc, off_slot_cls8, off_dec_desc, off_dec_masks, off_dec_cls8, off_ncand, off_imp_bits, off_scratch;
 };
 
 __device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
@@ -222,13 +234,23 @@ __device__ __forceinline__ void local_table(uint32_t c03, uint32_t c47, uint32_t
   }
 }
 
+// PRMT reads only selector bits [15:0], so the high half-word needs no mask.
 __device__ __forceinline__ uint4 select16(uint32_t lo, uint32_t hi, uint32_t z, uint32_t w) {
   uint4 o;
-  o.x = __byte_perm(lo, hi, z & 0xFFFF);
+  o.x = __byte_perm(lo, hi, z);
   o.y = __byte_perm(lo, hi, z >> 16);
-  o.z = __byte_perm(lo, hi, w & 0xFFFF);
+  o.z = __byte_perm(lo, hi, w);
   o.w = __byte_perm(lo, hi, w >> 16);
   return o;
+}
+
+// Status word of 4 local classes (k <= 4 chunks).
+__device__ __forceinline__ uint32_t local_table4(uint32_t c03, uint32_t tb) {
+  const uint32_t s0 = lds_u8(TBL_ADDR(c03, tb, 0));
+  const uint32_t s1 = lds_u8(TBL_ADDR(c03, tb, 1));
+  const uint32_t s2 = lds_u8(TBL_ADDR(c03, tb, 2));
+  const uint32_t s3 = lds_u8(TBL_ADDR(c03, tb, 3));
+  return __byte_perm(__byte_perm(s0, s1, 0x0040), __byte_perm(s2, s3, 0x0040), 0x5410);
 }
 
 // Squeeze bits {8b + i : b, i < 4} into bits {4b + i}: one shift-or and one PRMT.
@@ -270,10 +292,8 @@ __global__ void __launch_bounds__(kThreadsF) propagate_fast_kernel(FastParams p)
   stage(p.off_dec_desc, p.dec_desc, (int64_t)p.nq_d * 32);
   stage(p.off_dec_masks, p.dec_masks, (int64_t)p.nq_d * 4);
   stage(p.off_dec_cls8, p.dec_cls8, (int64_t)p.nq_d * 16);
-  stage(p.off_forced, p.forced, p.C);
   stage(p.off_ncand, p.ncand, 512);
-  stage(p.off_imp_off, p.imp_off, (int64_t)(p.C + 1) * 2);
-  stage(p.off_imp_tgt, p.imp_tgt, p.T);
+  stage(p.off_imp_bits, p.imp_bits, (int64_t)p.C * 32);
   __syncthreads();
 
   const uint4* slot_desc = reinterpret_cast<const uint4*>(smem + p.off_slot_desc);
@@ -281,10 +301,11 @@ __global__ void __launch_bounds__(kThreadsF) propagate_fast_kernel(FastParams p)
   const uint4* dec_desc = reinterpret_cast<const uint4*>(smem + p.off_dec_desc);
   const uint32_t* dec_masks = reinterpret_cast<const uint32_t*>(smem + p.off_dec_masks);
   const uint8_t* dec_cls8 = smem + p.off_dec_cls8;
-  const uint8_t* forced = smem + p.off_forced;
   const uint16_t* ncand = reinterpret_cast<const uint16_t*>(smem + p.off_ncand);
-  const uint16_t* imp_off = reinterpret_cast<const uint16_t*>(smem + p.off_imp_off);
-  const uint8_t* imp_tgt = smem + p.off_imp_tgt;
+  const uint4* imp_bits = reinterpret_cast<const uint4*>(smem + p.off_imp_bits);
+  uint32_t forced_bits[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) forced_bits[k] = p.forced_bits[k];
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -372,27 +393,52 @@ __global__ void __launch_bounds__(kThreadsF) propagate_fast_kernel(FastParams p)
       if (bn < p.batch && q < p.nq_d) cur[i] = ldg_stream(p.seeds + bn * p.seed_stride + 16 * q);
     }
 
-    // 2. implications of partitioned classes
-    for (int c = lane; c < p.C; c += 32) {
-      if (flagP[c]) {
-        const int e = imp_off[c + 1];
-        for (int k = imp_off[c]; k < e; ++k) flagR[imp_tgt[k]] = 1;
+    // 2. class bitsets: word k holds classes 32k..32k+31 (flags beyond C stay 0)
+    uint32_t Pw[8], Rw[8], acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      acc[k] = 0;
+      if (32 * k < p.C) {
+        Pw[k] = __ballot_sync(kFullMask, flagP[32 * k + lane] != 0);
+        Rw[k] = __ballot_sync(kFullMask, flagR[32 * k + lane] != 0) | forced_bits[k];
+      } else {
+        Pw[k] = Rw[k] = 0;
       }
     }
-    __syncwarp();
-
-    // 3. class statuses, conflict and decided counts
-    bool conflict = false;
-    uint32_t dPR = 0;  // decided P | decided R << 16
-    for (int c = lane; c < p.C; c += 32) {
-      const bool isP = flagP[c] != 0;
-      const bool isR = (flagR[c] | forced[c]) != 0;
-      conflict |= isP && isR;
-      table[c] = isP ? 1 : (isR ? 0 : -1);
-      const uint32_t nc = ncand[c];
-      dPR += isP ? nc : (isR ? (nc << 16) : 0u);
+    // 3. implications: each lane ORs the 256-bit rows of its own partitioned
+    //    classes, then one warp OR-reduction per word
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if ((Pw[k] >> lane) & 1u) {
+        const uint4* row = imp_bits + 2 * (32 * k + lane);
+        const uint4 a = row[0], c = row[1];
+        acc[0] |= a.x; acc[1] |= a.y; acc[2] |= a.z; acc[3] |= a.w;
+        acc[4] |= c.x; acc[5] |= c.y; acc[6] |= c.z; acc[7] |= c.w;
+      }
     }
-    conflict = __any_sync(kFullMask, conflict);
+    uint32_t clash = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (32 * k < p.C) {
+        Rw[k] |= __reduce_or_sync(kFullMask, acc[k]);
+        clash |= Pw[k] & Rw[k];
+      }
+    }
+    bool conflict = clash != 0;  // warp-uniform
+
+    // 4. class status table and decided counts (lane-owned classes)
+    uint32_t dPR = 0;  // decided P | decided R << 16
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (32 * k < p.C) {
+        const int c = 32 * k + lane;
+        const bool isP = (Pw[k] >> lane) & 1u;
+        const bool isR = (Rw[k] >> lane) & 1u;
+        table[c] = isP ? 1 : (isR ? 0 : -1);
+        const uint32_t nc = ncand[c];
+        dPR += isP ? nc : (isR ? (nc << 16) : 0u);
+      }
+    }
     dPR = __reduce_add_sync(kFullMask, dPR);
     uint32_t sPR = __reduce_add_sync(kFullMask, (uint32_t)nPs | ((uint32_t)nRs << 16));
     __syncwarp();
@@ -445,7 +491,16 @@ __global__ void __launch_bounds__(kThreadsF) propagate_fast_kernel(FastParams p)
     }
 
     // 5. all slot statuses
-    if (p.slots_out) {
+    if (p.slots_out && p.slot_all_k4) {
+      // common case (BERT-48): branch-free, four lookups per 16 slots
+      int8_t* orow = p.slots_out + b * p.slots_stride + 16 * lane;
+      const uint4* dq = slot_desc + lane;
+      for (int q = lane; q < p.nq_s; q += 32, dq += 32, orow += 512) {
+        const uint4 d = *dq;
+        const uint32_t lo = local_table4(d.x, tb);
+        stg_stream(orow, select16(lo, lo, d.z, d.w));
+      }
+    } else if (p.slots_out) {
       int8_t* orow = p.slots_out + b * p.slots_stride;
       for (int q = lane; q < p.nq_s; q += 32) {
         const uint4 d = slot_desc[q];
@@ -512,20 +567,17 @@ int launch_propagate_fast(const GraphTables* g, const DecisionTables* d, const i
   p.dec_desc = reinterpret_cast<const uint4*>(d->d_dec_desc.ptr);
   p.dec_masks = d->d_dec_masks.ptr;
   p.dec_cls8 = d->d_dec_cls8.ptr;
-  p.forced = g->d_class_forced.ptr;
+  p.forced_bits = g->d_forced_bits.ptr;
   p.ncand = d->d_class_ncand.ptr;
-  p.imp_off = g->d_imp_offset16.ptr;
-  p.imp_tgt = g->d_imp_target8.ptr;
+  p.imp_bits = g->d_imp_bits.ptr;
   p.dec_flags = d->d_dec_flags.ptr;
   p.first_same = d->d_first_same.ptr;
   p.nq_s = (int32_t)nq_s;
   p.nq_d = nq_d;
   p.C = g->num_classes;
   p.D = d->n;
-  p.T = (int32_t)g->imp_target8.size();
-  p.any_slot_fallback = 0;
-  for (int64_t q = 0; q < nq_s; ++q)
-    if ((g->slot_desc[4 * q] & 0xFF) == 0xFF) p.any_slot_fallback = 1;
+  p.any_slot_fallback = g->slot_fallback_chunks > 0;
+  p.slot_all_k4 = g->slot_all_k4;
   p.ncand_total = d->ncand;
   p.S = g->num_slots;
   p.seeds = seeds;
@@ -549,10 +601,8 @@ int launch_propagate_fast(const GraphTables* g, const DecisionTables* d, const i
   p.off_dec_desc = place((int64_t)nq_d * 32);
   p.off_dec_masks = place((int64_t)nq_d * 4);
   p.off_dec_cls8 = place((int64_t)nq_d * 16);
-  p.off_forced = place(256);
   p.off_ncand = place(512);
-  p.off_imp_off = place((int64_t)(p.C + 1) * 2);
-  p.off_imp_tgt = place(std::max(p.T, 1));
+  p.off_imp_bits = place((int64_t)std::max(p.C, 1) * 32);
   p.off_scratch = (int)off;
   const int64_t smem = off + 256 + (int64_t)kWarpsF * kScratchPerWarp;
   if (smem > 200 * 1024) return AP_ERR_UNSUPPORTED;
