@@ -149,7 +149,7 @@ def ncu_traffic(kernel: str):
         return None
     data = json.loads(p.read_text())
     k = data.get("kernels", {}).get(kernel)
-    return None if k is None else k.get("dram_bytes_per_launch")
+    return None if k is None else k.get("dram_bytes_per_plan")
 
 
 # -- CPU baselines (reference planner) ----------------------------------------------
@@ -386,7 +386,8 @@ def run_ours(args):
     bytes_per_plan = n + S + 1 + 16
     achieved = B * bytes_per_plan / per_launch_s / 1e9
     peak, peak_src = measured_peak_hbm()
-    traffic = ncu_traffic("propagate_kernel")
+    traffic_per_plan = ncu_traffic("propagate_kernel")
+    traffic = None if traffic_per_plan is None else traffic_per_plan * B
     value = world * B * args.steps / (max_ms / 1e3)
     line = {
         "metric": METRIC,
