@@ -128,6 +128,93 @@ int ap_propagate_trace(ap_graph_t g, ap_decision_t d, const int8_t* seeds_host,
                        const int8_t* init_state_host, int8_t* slots_host, int32_t* outcome_host,
                        int32_t* conflict_site_out, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Pipeline cost model (reference pipecost.py, topology.py, envs.py:276-404).
+ * All fp64 arithmetic reproduces the reference's evaluation order bit for
+ * bit: naive sequential stage sums (pipecost.py:99-102), CPython 3.12's
+ * compensated sum() (pipecost.py:173-174, 225), left-to-right products and
+ * quotients, first-wins max/min.
+ * ------------------------------------------------------------------------- */
+
+typedef struct ap_pipe* ap_pipe_t;
+
+typedef struct ap_topology {
+  int32_t num_servers;
+  int32_t gpus_per_server;
+  double intra_bw;   /* bytes/s inside a server (topology.py:18) */
+  double inter_bw;   /* bytes/s between servers (topology.py:19) */
+} ap_topology;
+
+/* The forward instruction order of a graph (forward_subgraph, ir.py:464-470)
+ * with what the cost model reads from it.  Positions index that order. */
+typedef struct ap_pipe_desc {
+  int32_t num_forward;
+  const double* cost_ms;         /* [F] compute_cost_ms or 0.0 */
+  const int64_t* out_bytes;      /* [F] output byte size */
+  const int32_t* last_use;       /* [F] largest forward-consumer position, -1 if none */
+  int32_t num_vars;
+  const int32_t* var_anchor;     /* [V] first forward-consumer position, else own position, else -1 */
+  const int64_t* var_bytes;      /* [V] in trainable_ids() order */
+} ap_pipe_desc;
+
+/* Replaces the per-graph work inside stage_metrics / candidate_pivots
+ * (pipecost.py:72-141, 279-336): crossing-activation bytes per cut,
+ * parameter-ownership prefixes, the naive cost prefix. */
+int ap_pipe_create(const ap_pipe_desc* desc, ap_pipe_t* out);
+int ap_pipe_destroy(ap_pipe_t p);
+
+/* candidate_pivots pruning mask (pipecost.py:279-336) on the device:
+ * allowed_dev [F-1] uint8 = position kept as a K-stage pivot candidate. */
+int ap_pipe_candidates(ap_pipe_t p, const ap_topology* topo, int32_t num_stages, int32_t radius,
+                       uint8_t* allowed_dev, void* stream);
+
+/* Batched stage_metrics (pipecost.py:72-141): pivots_dev [B, P] strictly
+ * increasing forward positions -> per stage (P+1 stages) compute_ms,
+ * activation_bytes, param_bytes (fp64) and num_variables (int32). */
+int ap_pipe_metrics(ap_pipe_t p, const int32_t* pivots_dev, int64_t batch, int32_t num_pivots,
+                    double backward_multiplier, double* compute_dev, double* act_dev, double* param_dev,
+                    int32_t* nvars_dev, void* stream);
+
+/* Batched proportional_device_cuts + pipeline_length + memory_feasible
+ * (pipecost.py:144-252) from per-stage metrics [B, K].  cuts_dev [B, K-1]:
+ * if `given_cuts` is non-zero they are inputs, else they are written with
+ * the proportional allocation.  mem_per_device < 0 disables the memory
+ * check (feasible = 1); optimizer_multiplier is memory_feasible's (4.0).
+ * python_floats != 0: the metrics are Python floats and builtin sum() is
+ * CPython's compensated float sum; 0: they are numpy float64 scalars (as
+ * PipeInferEnv.decode_metrics returns) and sum() is a naive left fold.
+ * length_dev [B] fp64, feasible_dev [B] uint8 (nullable). */
+int ap_pipe_length(const ap_topology* topo, int32_t num_stages, int32_t micro_batches, int64_t batch,
+                   const double* compute_dev, const double* act_dev, const double* param_dev, int32_t* cuts_dev,
+                   int32_t given_cuts, double mem_per_device, double optimizer_multiplier, int32_t python_floats,
+                   double* length_dev, uint8_t* feasible_dev, void* stream);
+
+/* PipeTrainEnv._state for `num_envs` states at once (envs.py:371-404): for
+ * every allowed candidate pivot of each state, the slowest stage allreduce,
+ * the slowest boundary transfer and the compute balance of the plan
+ * applied + [candidate], block-normalised, plus the one-hot of the applied
+ * picks.  cand_pos_dev [C] candidate positions (ascending); applied_dev
+ * [E, max_applied] candidate *indices* (-1 padded); mask_dev [E, C];
+ * state_dev [E, 4C] fp64. */
+int ap_pipe_train_state(ap_pipe_t p, const ap_topology* topo, const int32_t* cand_pos_dev, int32_t num_cand,
+                        const int32_t* applied_dev, int32_t max_applied, const uint8_t* mask_dev, int64_t num_envs,
+                        double backward_multiplier, double* state_dev, void* stream);
+
+/* PP-infer terminal evaluation on coarsened arrays (envs.py:593-616):
+ * decode_metrics + pipeline_length on the normalised topology for B
+ * (boundaries, cuts) points.  arrays_dev = [3 * G] fp64 (C*, A*, W*). */
+int ap_infer_length(const double* arrays_dev, int32_t granularity, const ap_topology* topo_normalized,
+                    int32_t num_stages, int32_t micro_batches, const int32_t* boundaries_dev,
+                    const int32_t* cuts_dev, int64_t batch, double* length_dev, void* stream);
+
+/* Exhaustive PP-infer search over per-slot bands (helpers.py:156-230 space,
+ * env-path arithmetic): lexicographic first-wins argmin.  band_* are host
+ * CSR lists of allowed values per pick (K-1 picks each).  Synchronises. */
+int ap_infer_search(const double* arrays_dev, int32_t granularity, const ap_topology* topo_normalized,
+                    int32_t num_stages, int32_t micro_batches, const int32_t* band_b, const int32_t* band_b_off,
+                    const int32_t* band_c, const int32_t* band_c_off, int32_t* best_boundaries,
+                    int32_t* best_cuts, double* best_length, int64_t* points_evaluated, void* stream);
+
 const char* ap_last_error(void);
 const char* ap_version(void);
 

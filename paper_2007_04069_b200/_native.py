@@ -60,10 +60,37 @@ class GraphInfo(ctypes.Structure):
     ]
 
 
+class Topology(ctypes.Structure):
+    _fields_ = [
+        ("num_servers", ctypes.c_int32),
+        ("gpus_per_server", ctypes.c_int32),
+        ("intra_bw", ctypes.c_double),
+        ("inter_bw", ctypes.c_double),
+    ]
+
+    @classmethod
+    def of(cls, topo) -> "Topology":
+        return cls(int(topo.num_servers), int(topo.gpus_per_server), float(topo.intra_bw), float(topo.inter_bw))
+
+
+class PipeDesc(ctypes.Structure):
+    _fields_ = [
+        ("num_forward", ctypes.c_int32),
+        ("cost_ms", ctypes.c_void_p),
+        ("out_bytes", ctypes.c_void_p),
+        ("last_use", ctypes.c_void_p),
+        ("num_vars", ctypes.c_int32),
+        ("var_anchor", ctypes.c_void_p),
+        ("var_bytes", ctypes.c_void_p),
+    ]
+
+
 # every symbol the header declares: name -> (restype, argtypes)
 _VP = ctypes.c_void_p
 _I64 = ctypes.c_int64
 _I32 = ctypes.c_int32
+_F64 = ctypes.c_double
+_TOPO = ctypes.POINTER(Topology)
 SIGNATURES: dict[str, tuple] = {
     "ap_graph_create": (ctypes.c_int, [ctypes.POINTER(GraphDesc), ctypes.POINTER(_VP)]),
     "ap_graph_destroy": (ctypes.c_int, [_VP]),
@@ -73,6 +100,15 @@ SIGNATURES: dict[str, tuple] = {
     "ap_decision_destroy": (ctypes.c_int, [_VP]),
     "ap_propagate_batch": (ctypes.c_int, [_VP, _VP, _VP, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _VP, _VP]),
     "ap_propagate_trace": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "ap_pipe_create": (ctypes.c_int, [ctypes.POINTER(PipeDesc), ctypes.POINTER(_VP)]),
+    "ap_pipe_destroy": (ctypes.c_int, [_VP]),
+    "ap_pipe_candidates": (ctypes.c_int, [_VP, _TOPO, _I32, _I32, _VP, _VP]),
+    "ap_pipe_metrics": (ctypes.c_int, [_VP, _VP, _I64, _I32, _F64, _VP, _VP, _VP, _VP, _VP]),
+    "ap_pipe_length": (ctypes.c_int, [_TOPO, _I32, _I32, _I64, _VP, _VP, _VP, _VP, _I32, _F64, _F64, _I32, _VP, _VP,
+                                      _VP]),
+    "ap_pipe_train_state": (ctypes.c_int, [_VP, _TOPO, _VP, _I32, _VP, _I32, _VP, _I64, _F64, _VP, _VP]),
+    "ap_infer_length": (ctypes.c_int, [_VP, _I32, _TOPO, _I32, _I32, _VP, _VP, _I64, _VP, _VP]),
+    "ap_infer_search": (ctypes.c_int, [_VP, _I32, _TOPO, _I32, _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "ap_last_error": (ctypes.c_char_p, []),
     "ap_version": (ctypes.c_char_p, []),
 }

@@ -1,0 +1,758 @@
+// K2 / K3 — pipeline cost model on the device, bit-exact with the reference.
+//
+// Reference: pipecost.py:72-336 (stage_metrics, pipeline_length,
+// memory_feasible, proportional_device_counts/cuts, candidate_pivots),
+// topology.py:121-148 (transfer / ring allreduce), envs.py:371-404
+// (PipeTrainEnv._state), envs.py:593-616 (PipeInferEnv decode + length).
+//
+// Bit parity rules (SURVEY §7 hard part 1), all enforced here:
+//  * this file is compiled with -fmad=false: every + and * rounds on its own;
+//  * stage compute sums are naive sequential sums starting at each stage's
+//    first instruction (never prefix differences);
+//  * CPython >= 3.12 builtin sum() over floats is Neumaier-compensated
+//    (py_sum below), e.g. pipeline_length's sum(times) and the total of
+//    proportional_device_counts;
+//  * byte counts are integers (exact in int64, converted once);
+//  * expressions keep Python's left-to-right association, ties in max/min
+//    and in the largest-remainder sort resolve to the lowest index.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "engine.h"
+
+namespace apb {
+namespace {
+
+constexpr int kMaxStages = 32;
+
+struct Topo {
+  int32_t g;  // gpus per server
+  int32_t d;  // devices
+  double intra, inter;
+};
+
+__host__ __device__ inline double bw(const Topo& t, int a, int b) { return (a / t.g == b / t.g) ? t.intra : t.inter; }
+
+// CPython 3.12 builtin sum() of floats (Python/bltinmodule.c, Neumaier)
+__host__ __device__ inline double py_sum(const double* x, int n) {
+  if (n <= 0) return 0.0;
+  double total = x[0];
+  double c = 0.0;
+  for (int i = 1; i < n; ++i) {
+    const double v = x[i];
+    const double t = total + v;
+    if (fabs(total) >= fabs(v))
+      c += (total - t) + v;
+    else
+      c += (v - t) + total;
+    total = t;
+  }
+  if (c != 0.0 && isfinite(c)) total += c;
+  return total;
+}
+
+// proportional_device_counts (pipecost.py:207-237)
+__host__ __device__ inline void proportional_counts(const double* comp, int k, int d, int* counts) {
+  const double total = py_sum(comp, k);
+  double q[kMaxStages];
+  int sum = 0;
+  for (int i = 0; i < k; ++i) {
+    q[i] = total <= 0.0 ? (double)d / (double)k : ((double)d * comp[i]) / total;
+    counts[i] = (int)(long long)q[i];
+    sum += counts[i];
+  }
+  const int rem = d - sum;
+  int add[kMaxStages];
+  for (int i = 0; i < k; ++i) {
+    const double fi = q[i] - (double)counts[i];
+    int rank = 0;
+    for (int j = 0; j < k; ++j) {
+      const double fj = q[j] - (double)counts[j];
+      rank += (fj > fi) || (fj == fi && j < i);
+    }
+    add[i] = rank < rem;
+  }
+  for (int i = 0; i < k; ++i) counts[i] += add[i];
+  for (;;) {  // starvation fix: no stage keeps zero devices
+    int poorest = -1;
+    for (int i = 0; i < k; ++i)
+      if (counts[i] == 0) {
+        poorest = i;
+        break;
+      }
+    if (poorest < 0) break;
+    int richest = 0;
+    for (int i = 1; i < k; ++i)
+      if (counts[i] > counts[richest]) richest = i;
+    counts[richest] -= 1;
+    counts[poorest] = 1;
+  }
+}
+
+// ring allreduce over devices [start, end) (topology.py:131-148)
+__host__ __device__ inline double allreduce(const Topo& t, double bytes, int start, int end) {
+  const int n = end - start;
+  if (n <= 1 || bytes == 0.0) return 0.0;
+  double slow = INFINITY;
+  for (int i = 0; i < n; ++i) {
+    const double b = bw(t, start + i, start + (i + 1) % n);
+    if (b < slow) slow = b;
+  }
+  return ((2.0 * (double)(n - 1)) / (double)n) * bytes / slow;
+}
+
+// transfer between consecutive groups (topology.py:121-128)
+__host__ __device__ inline double transfer(const Topo& t, double bytes, int src, int dst) {
+  if (src == dst) return 0.0;
+  return bytes / bw(t, src, dst);
+}
+
+__host__ __device__ inline void groups_from_counts(const int* counts, int k, int* start, int* end) {
+  int acc = 0;
+  for (int s = 0; s < k; ++s) {
+    start[s] = acc;
+    acc += counts[s];
+    end[s] = acc;
+  }
+}
+
+// builtin sum() over numpy float64 scalars: not PyFloat_CheckExact, so CPython
+// takes its generic PyNumber_Add path — a plain left-to-right sum
+__host__ __device__ inline double naive_sum(const double* x, int n) {
+  double total = 0.0;
+  for (int i = 0; i < n; ++i) total = (i == 0) ? x[0] : total + x[i];
+  return total;
+}
+
+// pipeline_length (pipecost.py:144-176) for groups [start, end).  `exact_floats`
+// selects CPython's compensated float sum (metrics are Python floats, as from
+// stage_metrics) or the naive generic sum (numpy scalars, as from
+// PipeInferEnv.decode_metrics, envs.py:608-615).
+__host__ __device__ inline double pipeline_len(const Topo& t, int k, int m, const double* comp, const double* act,
+                                               const double* param, const int* start, const int* end,
+                                               bool exact_floats = true) {
+  double times[kMaxStages], trans[kMaxStages], red_max = 0.0, t_max = 0.0;
+  for (int s = 0; s < k; ++s) {
+    times[s] = (comp[s] / 1000.0) / (double)(end[s] - start[s]);
+    if (s == 0 || times[s] > t_max) t_max = times[s];
+    const double r = allreduce(t, param[s], start[s], end[s]);
+    if (s == 0 || r > red_max) red_max = r;
+  }
+  for (int s = 0; s + 1 < k; ++s) trans[s] = transfer(t, act[s], end[s] - 1, start[s + 1]);
+  double len = (double)(m - 1) * t_max;
+  len = len + (exact_floats ? py_sum(times, k) : naive_sum(times, k));
+  len = len + (exact_floats ? py_sum(trans, k - 1) : naive_sum(trans, k - 1));
+  len = len + red_max;
+  return len;
+}
+
+// memory_feasible (pipecost.py:179-204)
+__host__ __device__ inline bool memory_ok(int k, int m, const double* act, const double* param, const int* start,
+                                          const int* end, double mem, double opt) {
+  for (int s = 0; s < k; ++s) {
+    const double n = (double)(end[s] - start[s]);
+    const double act_in = s > 0 ? act[s - 1] : 0.0;
+    const double ws = ((double)m * (act_in + act[s])) / n;
+    if ((param[s] / n) * opt + ws > mem) return false;
+  }
+  return true;
+}
+
+struct PipeDev {
+  int32_t F;
+  const double* cost;
+  const int64_t* crossing;
+  const int64_t* wprefix;
+  const int32_t* vprefix;
+  int64_t wtotal;
+  int32_t vtotal;
+};
+
+// stage_metrics for sorted cut positions cuts[0..P-1] (pipecost.py:72-141).
+// Costs are read through `cost` (shared or global memory).
+__device__ inline void stage_metrics_dev(const PipeDev& pd, const double* cost, const int* cuts, int P, double scale,
+                                         double* comp, double* act, double* param, int* nvars) {
+  int s = 0;
+  double acc = 0.0;
+  for (int i = 0; i < pd.F; ++i) {
+    if (s < P && i > cuts[s]) {
+      comp[s] = acc;
+      ++s;
+      acc = 0.0;
+    }
+    acc = acc + cost[i];
+  }
+  comp[s] = acc;
+  for (++s; s <= P; ++s) comp[s] = 0.0;
+  int64_t wprev = 0;
+  int32_t vprev = 0;
+  for (int k = 0; k <= P; ++k) {
+    const int64_t w = k < P ? pd.wprefix[cuts[k]] : pd.wtotal;
+    const int32_t v = k < P ? pd.vprefix[cuts[k]] : pd.vtotal;
+    comp[k] = comp[k] * scale;
+    act[k] = k < P ? (double)pd.crossing[cuts[k]] : 0.0;
+    param[k] = (double)(w - wprev);
+    if (nvars) nvars[k] = v - vprev;
+    wprev = w;
+    vprev = v;
+  }
+}
+
+__global__ void metrics_kernel(PipeDev pd, const int32_t* pivots, int64_t batch, int P, double scale, double* comp,
+                               double* act, double* param, int32_t* nvars) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < batch; b += (int64_t)gridDim.x * blockDim.x) {
+    int cuts[kMaxStages];
+    for (int k = 0; k < P; ++k) cuts[k] = pivots[b * P + k];
+    double c[kMaxStages], a[kMaxStages], w[kMaxStages];
+    int v[kMaxStages];
+    stage_metrics_dev(pd, pd.cost, cuts, P, scale, c, a, w, v);
+    for (int k = 0; k <= P; ++k) {
+      comp[b * (P + 1) + k] = c[k];
+      act[b * (P + 1) + k] = a[k];
+      param[b * (P + 1) + k] = w[k];
+      if (nvars) nvars[b * (P + 1) + k] = v[k];
+    }
+  }
+}
+
+__global__ void length_kernel(Topo t, int K, int M, int64_t batch, const double* comp, const double* act,
+                              const double* param, int32_t* cuts, int given, double mem, double opt, int exact,
+                              double* len, uint8_t* feas) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < batch; b += (int64_t)gridDim.x * blockDim.x) {
+    const double* c = comp + b * K;
+    const double* a = act + b * K;
+    const double* w = param + b * K;
+    int counts[kMaxStages], start[kMaxStages], end[kMaxStages];
+    if (given) {
+      int prev = 0;
+      for (int s = 0; s < K; ++s) {
+        const int e = s + 1 < K ? cuts[b * (K - 1) + s] : t.d;
+        counts[s] = e - prev;
+        prev = e;
+      }
+    } else {
+      proportional_counts(c, K, t.d, counts);
+    }
+    groups_from_counts(counts, K, start, end);
+    if (!given)
+      for (int s = 0; s + 1 < K; ++s) cuts[b * (K - 1) + s] = end[s];
+    len[b] = pipeline_len(t, K, M, c, a, w, start, end, exact != 0);
+    if (feas) feas[b] = mem < 0.0 ? 1 : (memory_ok(K, M, a, w, start, end, mem, opt) ? 1 : 0);
+  }
+}
+
+// candidate_pivots (pipecost.py:279-336): position i survives when the two-stage
+// proportional device cut lies in the allowed set and trainables sit on both sides
+__global__ void candidates_kernel(int F, const double* prefix, double total, const int32_t* cp_prefix, int32_t cp_total,
+                                  Topo t, int radius, uint8_t* allowed) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < F - 1; i += gridDim.x * blockDim.x) {
+    double two[2] = {prefix[i], total - prefix[i]};
+    int counts[2];
+    proportional_counts(two, 2, t.d, counts);
+    const int cut = counts[0];
+    bool ok = false;
+    for (int mm = t.g; mm < t.d; mm += t.g) {  // allowed_device_cuts (pipecost.py:255-268)
+      const int lo = mm - radius > 1 ? mm - radius : 1;
+      const int hi = mm + radius < t.d - 1 ? mm + radius : t.d - 1;
+      if (cut >= lo && cut <= hi) ok = true;
+    }
+    if (ok && cp_total > 0) {
+      const int before = cp_prefix[i];
+      if (before == 0 || before == cp_total) ok = false;
+    }
+    allowed[i] = ok ? 1 : 0;
+  }
+}
+
+// PipeTrainEnv._state raw features: one thread per (env, candidate)
+__global__ void train_cand_kernel(PipeDev pd, Topo t, const int32_t* cand_pos, int C, const int32_t* applied, int A,
+                                  const uint8_t* mask, int64_t E, double scale, double* state) {
+  extern __shared__ double s_cost[];
+  for (int i = threadIdx.x; i < pd.F; i += blockDim.x) s_cost[i] = pd.cost[i];
+  __syncthreads();
+  const int64_t total = E * (int64_t)C;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = idx / C;
+    const int i = (int)(idx % C);
+    double* st = state + e * 4 * (int64_t)C;
+    const bool allowed = mask[e * C + i] != 0;
+    if (!allowed) {
+      st[i] = 0.0;
+      st[C + i] = 0.0;
+      st[2 * C + i] = 0.0;
+      continue;
+    }
+    int cuts[kMaxStages];
+    int P = 0;
+    for (int k = 0; k < A; ++k) {
+      const int a = applied[e * A + k];
+      if (a >= 0) cuts[P++] = cand_pos[a];
+    }
+    cuts[P++] = cand_pos[i];
+    const int K = P + 1;
+    double c[kMaxStages], a[kMaxStages], w[kMaxStages];
+    stage_metrics_dev(pd, s_cost, cuts, P, scale, c, a, w, nullptr);
+    int counts[kMaxStages], start[kMaxStages], end[kMaxStages];
+    proportional_counts(c, K, t.d, counts);
+    groups_from_counts(counts, K, start, end);
+    double red = 0.0, tra = 0.0, top = c[0], bot = c[0];
+    for (int s = 0; s < K; ++s) {
+      const double r = allreduce(t, w[s], start[s], end[s]);
+      if (s == 0 || r > red) red = r;
+      if (c[s] > top) top = c[s];
+      if (c[s] < bot) bot = c[s];
+    }
+    for (int s = 0; s + 1 < K; ++s) {
+      const double x = transfer(t, a[s], end[s] - 1, start[s + 1]);
+      if (s == 0 || x > tra) tra = x;
+    }
+    st[i] = red;
+    st[C + i] = tra;
+    st[2 * C + i] = top > 0.0 ? bot / top : 1.0;
+  }
+}
+
+// block normalisation and one-hot (envs.py:398-404): one CTA per env
+__global__ void train_norm_kernel(int C, const int32_t* applied, int A, int64_t E, double* state) {
+  __shared__ double s_max[2][32];
+  for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+    double* st = state + e * 4 * (int64_t)C;
+    double mr = 0.0, mt = 0.0;
+    for (int i = threadIdx.x; i < C; i += blockDim.x) {
+      mr = fmax(mr, st[i]);
+      mt = fmax(mt, st[C + i]);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      mr = fmax(mr, __shfl_xor_sync(0xffffffffu, mr, o));
+      mt = fmax(mt, __shfl_xor_sync(0xffffffffu, mt, o));
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+      s_max[0][w] = mr;
+      s_max[1][w] = mt;
+    }
+    __syncthreads();
+    mr = 0.0;
+    mt = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+      mr = fmax(mr, s_max[0][k]);
+      mt = fmax(mt, s_max[1][k]);
+    }
+    for (int i = threadIdx.x; i < C; i += blockDim.x) {
+      if (mr > 0.0) st[i] = st[i] / mr;
+      if (mt > 0.0) st[C + i] = st[C + i] / mt;
+      st[3 * C + i] = 0.0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int k = 0; k < A; ++k) {
+        const int a = applied[e * A + k];
+        if (a >= 0) st[3 * C + a] = 1.0;
+      }
+    __syncthreads();
+  }
+}
+
+// PP-infer decode_metrics + pipeline_length (envs.py:593-616, 585)
+__device__ inline double infer_point(const double* arr, int G, const Topo& t, int K, int M, const int* bnd,
+                                     const int* cut) {
+  const double* cc = arr;
+  const double* aa = arr + G;
+  const double* ww = arr + 2 * G;
+  double comp[kMaxStages], act[kMaxStages], par[kMaxStages];
+  int start[kMaxStages], end[kMaxStages];
+  int lo = 0;
+  for (int s = 0; s < K; ++s) {
+    const int hi = s + 1 < K ? bnd[s] : G;
+    const double c = cc[hi - 1] - (lo > 0 ? cc[lo - 1] : 0.0);
+    const double w = ww[hi - 1] - (lo > 0 ? ww[lo - 1] : 0.0);
+    comp[s] = c * 1000.0;
+    par[s] = w;
+    act[s] = hi < G ? aa[hi - 1] : 0.0;
+    lo = hi;
+  }
+  int prev = 0;
+  for (int s = 0; s < K; ++s) {
+    start[s] = prev;
+    end[s] = s + 1 < K ? cut[s] : t.d;
+    prev = end[s];
+  }
+  return pipeline_len(t, K, M, comp, act, par, start, end, /*exact_floats=*/false);
+}
+
+__global__ void infer_kernel(const double* arr, int G, Topo t, int K, int M, const int32_t* bnd, const int32_t* cut,
+                             int64_t batch, double* len) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < batch; b += (int64_t)gridDim.x * blockDim.x) {
+    int bb[kMaxStages], cc[kMaxStages];
+    for (int s = 0; s + 1 < K; ++s) {
+      bb[s] = bnd[b * (K - 1) + s];
+      cc[s] = cut[b * (K - 1) + s];
+    }
+    len[b] = infer_point(arr, G, t, K, M, bb, cc);
+  }
+}
+
+// exhaustive search: every (b-combo, c-combo), first-wins argmin per block
+__global__ void infer_search_kernel(const double* arr, int G, Topo t, int K, int M, const int32_t* bcomb, int64_t nb,
+                                    const int32_t* ccomb, int64_t nc, double* blk_len, int64_t* blk_idx) {
+  __shared__ double s_len[256];
+  __shared__ int64_t s_idx[256];
+  double best = INFINITY;
+  int64_t best_i = INT64_MAX;
+  const int64_t total = nb * nc;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t ib = idx / nc, ic = idx % nc;
+    int bb[kMaxStages], cc[kMaxStages];
+    for (int s = 0; s + 1 < K; ++s) {
+      bb[s] = bcomb[ib * (K - 1) + s];
+      cc[s] = ccomb[ic * (K - 1) + s];
+    }
+    double l = infer_point(arr, G, t, K, M, bb, cc);
+    if (l < 1e-12) l = 1e-12;  // _MIN_LENGTH (envs.py:53, 584)
+    if (l < best || (l == best && idx < best_i)) {
+      best = l;
+      best_i = idx;
+    }
+  }
+  s_len[threadIdx.x] = best;
+  s_idx[threadIdx.x] = best_i;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      const double l2 = s_len[threadIdx.x + o];
+      const int64_t i2 = s_idx[threadIdx.x + o];
+      if (l2 < s_len[threadIdx.x] || (l2 == s_len[threadIdx.x] && i2 < s_idx[threadIdx.x])) {
+        s_len[threadIdx.x] = l2;
+        s_idx[threadIdx.x] = i2;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    blk_len[blockIdx.x] = s_len[0];
+    blk_idx[blockIdx.x] = s_idx[0];
+  }
+}
+
+Topo make_topo(const ap_topology* t) { return Topo{t->gpus_per_server, t->num_servers * t->gpus_per_server, t->intra_bw, t->inter_bw}; }
+
+int check_topo(const ap_topology* t, int stages) {
+  if (!t || t->num_servers < 1 || t->gpus_per_server < 1 || !(t->intra_bw > 0) || !(t->inter_bw > 0)) {
+    set_error("invalid topology");
+    return AP_ERR_INVALID;
+  }
+  if (stages > kMaxStages || stages < 1) {
+    set_error("stage count outside [1, 32]");
+    return AP_ERR_UNSUPPORTED;
+  }
+  return AP_OK;
+}
+
+int grid_for(int64_t n, int threads) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, 148 * 16)); }
+
+}  // namespace
+}  // namespace apb
+
+using namespace apb;
+
+struct ap_pipe {
+  int32_t F = 0;
+  std::vector<double> cost, prefix;
+  std::vector<int64_t> crossing, wprefix;
+  std::vector<int32_t> vprefix, cp_prefix;
+  int64_t wtotal = 0;
+  int32_t vtotal = 0, cp_total = 0;
+  double total = 0.0;
+  DevBuf<double> d_cost, d_prefix;
+  DevBuf<int64_t> d_crossing, d_wprefix;
+  DevBuf<int32_t> d_vprefix, d_cp_prefix;
+  bool uploaded = false;
+  int device = 0;
+
+  int ensure() {
+    int cur = 0;
+    AP_CUDA_CHECK(cudaGetDevice(&cur));
+    if (uploaded) {
+      if (cur != device) {
+        set_error("pipe handle used on another device");
+        return AP_ERR_INVALID;
+      }
+      return AP_OK;
+    }
+    device = cur;
+    int rc;
+    if ((rc = d_cost.upload(cost)) != AP_OK) return rc;
+    if ((rc = d_prefix.upload(prefix)) != AP_OK) return rc;
+    if ((rc = d_crossing.upload(crossing)) != AP_OK) return rc;
+    if ((rc = d_wprefix.upload(wprefix)) != AP_OK) return rc;
+    if ((rc = d_vprefix.upload(vprefix)) != AP_OK) return rc;
+    if ((rc = d_cp_prefix.upload(cp_prefix)) != AP_OK) return rc;
+    uploaded = true;
+    return AP_OK;
+  }
+  PipeDev dev() const {
+    return PipeDev{F, d_cost.ptr, d_crossing.ptr, d_wprefix.ptr, d_vprefix.ptr, wtotal, vtotal};
+  }
+  void release() {
+    d_cost.release();
+    d_prefix.release();
+    d_crossing.release();
+    d_wprefix.release();
+    d_vprefix.release();
+    d_cp_prefix.release();
+  }
+};
+
+extern "C" {
+
+int ap_pipe_create(const ap_pipe_desc* desc, ap_pipe_t* out) {
+  if (!desc || !out || desc->num_forward < 1 || desc->num_vars < 0 || !desc->cost_ms || !desc->out_bytes ||
+      !desc->last_use || (desc->num_vars > 0 && (!desc->var_anchor || !desc->var_bytes))) {
+    set_error("ap_pipe_create: bad descriptor");
+    return AP_ERR_INVALID;
+  }
+  ap_pipe* p = new ap_pipe();
+  const int F = desc->num_forward;
+  p->F = F;
+  p->cost.assign(desc->cost_ms, desc->cost_ms + F);
+  // naive running prefix, exactly the reference's `acc += c` (pipecost.py:298-304)
+  p->prefix.resize(F);
+  double acc = 0.0;
+  for (int i = 0; i < F; ++i) {
+    acc += p->cost[i];
+    p->prefix[i] = acc;
+  }
+  p->total = acc;
+  // activation bytes crossing a cut after position c (pipecost.py:104-115):
+  // tensor i crosses every cut in [i, last_use[i])
+  std::vector<int64_t> diff(F + 1, 0);
+  for (int i = 0; i < F; ++i) {
+    const int lu = desc->last_use[i];
+    if (lu > i) {
+      diff[i] += desc->out_bytes[i];
+      diff[lu] -= desc->out_bytes[i];
+    }
+  }
+  p->crossing.resize(F);
+  int64_t run = 0;
+  for (int i = 0; i < F; ++i) p->crossing[i] = (run += diff[i]);
+  // parameter ownership (pipecost.py:117-130): anchor -1 = stage 0 always
+  std::vector<int64_t> wb(F + 1, 0);
+  std::vector<int32_t> vb(F + 1, 0), cb(F + 1, 0);
+  for (int v = 0; v < desc->num_vars; ++v) {
+    const int a = desc->var_anchor[v];
+    if (a >= F) {
+      delete p;
+      set_error("ap_pipe_create: var anchor out of range");
+      return AP_ERR_INVALID;
+    }
+    wb[a < 0 ? 0 : a] += desc->var_bytes[v];
+    vb[a < 0 ? 0 : a] += 1;
+    p->wtotal += desc->var_bytes[v];
+    p->vtotal += 1;
+    if (a >= 0) {  // candidate_pivots only sees anchored variables (pipecost.py:309-319)
+      cb[a] += 1;
+      p->cp_total += 1;
+    }
+  }
+  p->wprefix.resize(F);
+  p->vprefix.resize(F);
+  p->cp_prefix.resize(F);
+  int64_t w = 0;
+  int32_t vv = 0, cc = 0;
+  for (int i = 0; i < F; ++i) {
+    p->wprefix[i] = (w += wb[i]);
+    p->vprefix[i] = (vv += vb[i]);
+    p->cp_prefix[i] = (cc += cb[i]);
+  }
+  *out = p;
+  return AP_OK;
+}
+
+int ap_pipe_destroy(ap_pipe_t p) {
+  if (p) {
+    p->release();
+    delete p;
+  }
+  return AP_OK;
+}
+
+int ap_pipe_candidates(ap_pipe_t p, const ap_topology* topo, int32_t num_stages, int32_t radius, uint8_t* allowed,
+                       void* stream) {
+  int rc = check_topo(topo, 2);
+  if (rc != AP_OK) return rc;
+  if (!p || !allowed || radius < 0) {
+    set_error("ap_pipe_candidates: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  if ((rc = p->ensure()) != AP_OK) return rc;
+  (void)num_stages;
+  const Topo t = make_topo(topo);
+  candidates_kernel<<<grid_for(p->F, 256), 256, 0, (cudaStream_t)stream>>>(p->F, p->d_prefix.ptr, p->total,
+                                                                          p->d_cp_prefix.ptr, p->cp_total, t, radius,
+                                                                          allowed);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_pipe_metrics(ap_pipe_t p, const int32_t* pivots, int64_t batch, int32_t P, double bwm, double* comp,
+                    double* act, double* param, int32_t* nvars, void* stream) {
+  if (!p || batch < 0 || P < 0 || P + 1 > kMaxStages || (batch && (!comp || !act || !param || (P && !pivots)))) {
+    set_error("ap_pipe_metrics: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  int rc = p->ensure();
+  if (rc != AP_OK) return rc;
+  if (batch == 0) return AP_OK;
+  metrics_kernel<<<grid_for(batch, 128), 128, 0, (cudaStream_t)stream>>>(p->dev(), pivots, batch, P, 1.0 + bwm, comp,
+                                                                         act, param, nvars);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_pipe_length(const ap_topology* topo, int32_t K, int32_t M, int64_t batch, const double* comp,
+                   const double* act, const double* param, int32_t* cuts, int32_t given, double mem, double opt,
+                   int32_t python_floats, double* len, uint8_t* feas, void* stream) {
+  int rc = check_topo(topo, K);
+  if (rc != AP_OK) return rc;
+  if (batch < 0 || M < 1 || K > topo->num_servers * topo->gpus_per_server ||
+      (batch && (!comp || !act || !param || !len || (K > 1 && !cuts)))) {
+    set_error("ap_pipe_length: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  if (batch == 0) return AP_OK;
+  length_kernel<<<grid_for(batch, 128), 128, 0, (cudaStream_t)stream>>>(make_topo(topo), K, M, batch, comp, act, param,
+                                                                         cuts, given, mem, opt, python_floats, len,
+                                                                         feas);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_pipe_train_state(ap_pipe_t p, const ap_topology* topo, const int32_t* cand_pos, int32_t C,
+                        const int32_t* applied, int32_t A, const uint8_t* mask, int64_t E, double bwm, double* state,
+                        void* stream) {
+  int rc = check_topo(topo, A + 2);
+  if (rc != AP_OK) return rc;
+  if (!p || C < 1 || A < 0 || E < 0 || (E && (!cand_pos || !mask || !state || (A && !applied)))) {
+    set_error("ap_pipe_train_state: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  if ((rc = p->ensure()) != AP_OK) return rc;
+  if (E == 0) return AP_OK;
+  const size_t smem = (size_t)p->F * sizeof(double);
+  if (smem > 200 * 1024) {
+    set_error("ap_pipe_train_state: forward graph too long for the shared-memory cost cache");
+    return AP_ERR_UNSUPPORTED;
+  }
+  AP_CUDA_CHECK(cudaFuncSetAttribute(train_cand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const Topo t = make_topo(topo);
+  train_cand_kernel<<<grid_for(E * (int64_t)C, 128), 128, smem, (cudaStream_t)stream>>>(p->dev(), t, cand_pos, C,
+                                                                                        applied, A, mask, E, 1.0 + bwm,
+                                                                                        state);
+  AP_CUDA_CHECK(cudaGetLastError());
+  train_norm_kernel<<<(int)std::min<int64_t>(E, 148 * 8), 256, 0, (cudaStream_t)stream>>>(C, applied, A, E, state);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_infer_length(const double* arrays, int32_t G, const ap_topology* topo, int32_t K, int32_t M,
+                    const int32_t* bnd, const int32_t* cut, int64_t batch, double* len, void* stream) {
+  int rc = check_topo(topo, K);
+  if (rc != AP_OK) return rc;
+  if (!arrays || G < 2 || batch < 0 || (batch && (!len || (K > 1 && (!bnd || !cut))))) {
+    set_error("ap_infer_length: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  if (batch == 0) return AP_OK;
+  infer_kernel<<<grid_for(batch, 128), 128, 0, (cudaStream_t)stream>>>(arrays, G, make_topo(topo), K, M, bnd, cut,
+                                                                        batch, len);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// strictly increasing combinations of one value per pick, lexicographic
+void combos(const int32_t* vals, const int32_t* off, int picks, std::vector<int32_t>* out) {
+  std::vector<int> idx(picks, 0);
+  std::vector<int32_t> cur(picks);
+  out->clear();
+  for (int s = 0; s < picks; ++s)
+    if (off[s + 1] == off[s]) return;
+  for (;;) {
+    bool ok = true;
+    for (int s = 0; s < picks; ++s) {
+      cur[s] = vals[off[s] + idx[s]];
+      if (s > 0 && cur[s] <= cur[s - 1]) ok = false;
+    }
+    if (ok) out->insert(out->end(), cur.begin(), cur.end());
+    int s = picks - 1;
+    while (s >= 0 && ++idx[s] == off[s + 1] - off[s]) idx[s--] = 0;
+    if (s < 0) return;
+  }
+}
+
+}  // namespace
+
+extern "C" int ap_infer_search(const double* arrays, int32_t G, const ap_topology* topo, int32_t K, int32_t M,
+                               const int32_t* band_b, const int32_t* band_b_off, const int32_t* band_c,
+                               const int32_t* band_c_off, int32_t* best_b, int32_t* best_c, double* best_len,
+                               int64_t* evaluated, void* stream) {
+  int rc = check_topo(topo, K);
+  if (rc != AP_OK) return rc;
+  if (K < 2 || !arrays || !band_b || !band_b_off || !band_c || !band_c_off || !best_b || !best_c || !best_len) {
+    set_error("ap_infer_search: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  const int picks = K - 1;
+  std::vector<int32_t> bc, cc;
+  combos(band_b, band_b_off, picks, &bc);
+  combos(band_c, band_c_off, picks, &cc);
+  const int64_t nb = (int64_t)bc.size() / picks, nc = (int64_t)cc.size() / picks;
+  if (evaluated) *evaluated = nb * nc;
+  if (nb == 0 || nc == 0) {
+    set_error("ap_infer_search: empty search space");
+    return AP_ERR_INFEASIBLE;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  int32_t *d_b = nullptr, *d_c = nullptr;
+  double* d_len = nullptr;
+  int64_t* d_idx = nullptr;
+  const int blocks = (int)std::min<int64_t>((nb * nc + 255) / 256, 148 * 8);
+  AP_CUDA_CHECK(cudaMalloc(&d_b, bc.size() * sizeof(int32_t)));
+  AP_CUDA_CHECK(cudaMalloc(&d_c, cc.size() * sizeof(int32_t)));
+  AP_CUDA_CHECK(cudaMalloc(&d_len, blocks * sizeof(double)));
+  AP_CUDA_CHECK(cudaMalloc(&d_idx, blocks * sizeof(int64_t)));
+  AP_CUDA_CHECK(cudaMemcpyAsync(d_b, bc.data(), bc.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  AP_CUDA_CHECK(cudaMemcpyAsync(d_c, cc.data(), cc.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  infer_search_kernel<<<blocks, 256, 0, s>>>(arrays, G, make_topo(topo), K, M, d_b, nb, d_c, nc, d_len, d_idx);
+  AP_CUDA_CHECK(cudaGetLastError());
+  std::vector<double> hl(blocks);
+  std::vector<int64_t> hi(blocks);
+  AP_CUDA_CHECK(cudaMemcpyAsync(hl.data(), d_len, blocks * sizeof(double), cudaMemcpyDeviceToHost, s));
+  AP_CUDA_CHECK(cudaMemcpyAsync(hi.data(), d_idx, blocks * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  AP_CUDA_CHECK(cudaStreamSynchronize(s));
+  cudaFree(d_b);
+  cudaFree(d_c);
+  cudaFree(d_len);
+  cudaFree(d_idx);
+  double bl = INFINITY;
+  int64_t bi = INT64_MAX;
+  for (int k = 0; k < blocks; ++k)
+    if (hl[k] < bl || (hl[k] == bl && hi[k] < bi)) {
+      bl = hl[k];
+      bi = hi[k];
+    }
+  const int64_t ib = bi / nc, ic = bi % nc;
+  for (int s2 = 0; s2 < picks; ++s2) {
+    best_b[s2] = bc[ib * picks + s2];
+    best_c[s2] = cc[ic * picks + s2];
+  }
+  *best_len = bl;
+  return AP_OK;
+}
