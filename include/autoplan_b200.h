@@ -215,6 +215,20 @@ int ap_infer_search(const double* arrays_dev, int32_t granularity, const ap_topo
                     const int32_t* band_c, const int32_t* band_c_off, int32_t* best_boundaries,
                     int32_t* best_cuts, double* best_length, int64_t* points_evaluated, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * DQN (reference agent.py).  The Q-network's dense contractions run on the
+ * tcgen05 tensor cores; everything else of the learner stays device-resident.
+ * ------------------------------------------------------------------------- */
+
+/* C[M,N] = op(A)[M,K] * op(B)[K,N] (+ bias[N]) (ReLU), fp32 in/out.
+ * op(A)[m,k] = transA ? A[k*lda+m] : A[m*lda+k]; op(B)[k,n] = transB ?
+ * B[n*ldb+k] : B[k*ldb+n].  precision 3 = 3xTF32 split (fp32-accurate),
+ * 1 = plain TF32.  Replaces the numpy matmuls of QNetwork.forward_cached /
+ * backward (agent.py:93-136). */
+int ap_gemm_tf32(const float* A, int64_t lda, int32_t transA, const float* B, int64_t ldb, int32_t transB,
+                 float* C, int64_t ldc, int32_t M, int32_t N, int32_t K, const float* bias, int32_t relu,
+                 int32_t precision, void* stream);
+
 const char* ap_last_error(void);
 const char* ap_version(void);
 

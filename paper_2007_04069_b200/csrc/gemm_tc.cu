@@ -1,0 +1,274 @@
+// tcgen05 tensor-core GEMM for the Q-network (sm_100a).
+//
+//   C[M,N] = op(A)[M,K] * op(B)[K,N]  (+ bias[n]) (ReLU)
+//
+// kind::tf32 MMAs (M=128 per CTA, N <= 256), fp32 accumulators in TMEM.
+// Precision 3 ("3xTF32") splits both operands into a TF32 head and a
+// remainder while staging (x = hi + lo, hi = x with the low 13 mantissa bits
+// cleared) and issues hi*hi + hi*lo + lo*hi per K step: products carry ~fp32
+// accuracy, which is what lets the Q-network agree with the fp64 reference
+// within an fp32 tolerance.  Precision 1 is plain TF32.
+//
+// Structure (one CTA = 4 warps = 128 TMEM lanes per output tile):
+//  * all threads stage a BK=32 slice of A and B into shared memory in the
+//    canonical K-major no-swizzle UMMA layout (8-row x 16-byte core matrices:
+//    LBO = 128 B along K, SBO = 1024 B along M/N), transposing on the fly when
+//    the global operand is M/N-contiguous; two stages double-buffer the loads
+//    against the asynchronous MMAs;
+//  * thread 0 issues the tcgen05.mma chain of the slice and commits it to the
+//    stage's mbarrier; a stage is refilled only after its mbarrier phase flips;
+//  * epilogue: each warp tcgen05.ld's its 32 TMEM lanes (rows), applies bias
+//    and ReLU, and stores fp32 rows.
+#include <algorithm>
+
+#include "engine.h"
+
+namespace apb {
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBK = 32;
+constexpr int kTileRowBytes = kBK * 4;  // one row of a K-slice: 128 B = 8 core-matrix columns
+
+struct GemmArgs {
+  const float* A;
+  int64_t lda;
+  int transA;
+  const float* B;
+  int64_t ldb;
+  int transB;
+  float* C;
+  int64_t ldc;
+  int M, N, K;
+  const float* bias;
+  int relu;
+  int precision;
+  int bn;  // N tile (multiple of 16, <= 256)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// byte offset of element (r, k) inside a [rows x 32] K-major canonical tile
+__device__ __forceinline__ uint32_t tile_off(int r, int k) {
+  return (uint32_t)((r >> 3) * 1024 + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4);
+}
+
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((128 >> 4) & 0x3FFF) << 16;   // leading byte offset: next 16-byte K chunk
+  d |= (uint64_t)((1024 >> 4) & 0x3FFF) << 32;  // stride byte offset: next 8-row group
+  d |= (uint64_t)1 << 46;                         // descriptor version (sm_100)
+  return d;                                       // base offset 0, SWIZZLE_NONE
+}
+
+__device__ __forceinline__ uint32_t make_idesc(int m, int n) {
+  uint32_t d = 0;
+  d |= 1u << 4;              // D format f32
+  d |= 2u << 7;              // A format tf32
+  d |= 2u << 10;             // B format tf32
+  d |= (uint32_t)(n >> 3) << 17;
+  d |= (uint32_t)(m >> 4) << 24;
+  return d;                  // K-major A and B, no negate
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+      "@!done bra WAIT_%=;\n\t}\n" ::"r"(mbar),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void split_tf32(float x, float* hi, float* lo) {
+  const float h = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+  *hi = h;
+  *lo = x - h;
+}
+
+// Stage rows [r0, r0+rows) x K-slice [k0, k0+32) of op(X) into hi/lo tiles.
+// op(X)[r, k] = trans ? X[k*ld + r] : X[r*ld + k]
+__device__ void stage_tile(const float* X, int64_t ld, int trans, int rows_total, int K, int r0, int k0, int rows,
+                           uint8_t* hi, uint8_t* lo, bool split) {
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  if (!trans) {
+    // K contiguous: each thread moves 4 consecutive k of one row
+    const int groups = rows * (kBK / 4);
+    for (int g = tid; g < groups; g += nthr) {
+      const int r = g / (kBK / 4), kq = (g % (kBK / 4)) * 4;
+      const int gr = r0 + r, gk = k0 + kq;
+      float v[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) v[t] = (gr < rows_total && gk + t < K) ? X[(int64_t)gr * ld + gk + t] : 0.0f;
+      float4 h, l;
+      if (split) {
+        split_tf32(v[0], &h.x, &l.x);
+        split_tf32(v[1], &h.y, &l.y);
+        split_tf32(v[2], &h.z, &l.z);
+        split_tf32(v[3], &h.w, &l.w);
+      } else {
+        h = make_float4(v[0], v[1], v[2], v[3]);
+      }
+      const uint32_t off = tile_off(r, kq);
+      *reinterpret_cast<float4*>(hi + off) = h;
+      if (split) *reinterpret_cast<float4*>(lo + off) = l;
+    }
+  } else {
+    // rows contiguous: consecutive threads read consecutive rows of one k
+    const int total = rows * kBK;
+    for (int g = tid; g < total; g += nthr) {
+      const int k = g / rows, r = g % rows;
+      const int gr = r0 + r, gk = k0 + k;
+      const float x = (gr < rows_total && gk < K) ? X[(int64_t)gk * ld + gr] : 0.0f;
+      const uint32_t off = tile_off(r, k);
+      if (split) {
+        float h, l;
+        split_tf32(x, &h, &l);
+        *reinterpret_cast<float*>(hi + off) = h;
+        *reinterpret_cast<float*>(lo + off) = l;
+      } else {
+        *reinterpret_cast<float*>(hi + off) = x;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128, 1) gemm_tf32_kernel(GemmArgs g) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ uint32_t tmem_slot;
+
+  const int bn = g.bn;
+  const bool split = g.precision == 3;
+  const int m0 = blockIdx.x * kBM;
+  const int n0 = blockIdx.y * bn;
+  const int a_bytes = kBM * kTileRowBytes;  // 16 KB
+  const int b_bytes = bn * kTileRowBytes;
+  const int stage_bytes = (a_bytes + b_bytes) * (split ? 2 : 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  int cols = 32;
+  while (cols < bn) cols <<= 1;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
+                 "r"(cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_slot;
+  const uint32_t idesc = make_idesc(kBM, bn);
+
+  const int nk = (g.K + kBK - 1) / kBK;
+  for (int kt = 0; kt < nk; ++kt) {
+    const int buf = kt & 1;
+    if (kt >= 2) mbar_wait(smem_u32(&mbar[buf]), ((kt - 2) >> 1) & 1);
+    uint8_t* base = smem + buf * stage_bytes;
+    uint8_t* a_hi = base;
+    uint8_t* b_hi = base + a_bytes;
+    uint8_t* a_lo = base + a_bytes + b_bytes;
+    uint8_t* b_lo = a_lo + a_bytes;
+    stage_tile(g.A, g.lda, g.transA, g.M, g.K, m0, kt * kBK, kBM, a_hi, a_lo, split);
+    stage_tile(g.B, g.ldb, !g.transB, g.N, g.K, n0, kt * kBK, bn, b_hi, b_lo, split);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int ks = 0; ks < kBK / 8; ++ks) {
+        const uint32_t koff = ks * 256;  // two 16-byte K chunks per MMA (K = 8 tf32)
+        const uint64_t ah = make_desc(smem_u32(a_hi) + koff), bh = make_desc(smem_u32(b_hi) + koff);
+        mma_tf32(tmem, ah, bh, idesc, (kt | ks) != 0);
+        if (split) {
+          const uint64_t al = make_desc(smem_u32(a_lo) + koff), bl = make_desc(smem_u32(b_lo) + koff);
+          mma_tf32(tmem, ah, bl, idesc, 1);
+          mma_tf32(tmem, al, bh, idesc, 1);
+        }
+      }
+      mma_commit(smem_u32(&mbar[buf]));
+    }
+  }
+  mbar_wait(smem_u32(&mbar[(nk - 1) & 1]), ((nk - 1) >> 1) & 1);
+  asm volatile("tcgen05.fence::after_thread_sync;");
+
+  // epilogue: warp w owns TMEM lanes / tile rows [32w, 32w+32)
+  const int row = m0 + warp * 32 + lane;
+  for (int c0 = 0; c0 < bn; c0 += 16) {
+    uint32_t v[16];
+    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (row < g.M) {
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const int col = n0 + c0 + t;
+        if (col < g.N) {
+          float x = __uint_as_float(v[t]);
+          if (g.bias) x += g.bias[col];
+          if (g.relu) x = fmaxf(x, 0.0f);
+          g.C[(int64_t)row * g.ldc + col] = x;
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(cols));
+}
+
+}  // namespace
+
+int launch_gemm_tf32(const float* A, int64_t lda, int transA, const float* B, int64_t ldb, int transB, float* C,
+                     int64_t ldc, int M, int N, int K, const float* bias, int relu, int precision,
+                     cudaStream_t stream) {
+  if (M <= 0 || N <= 0 || K <= 0) return AP_OK;
+  GemmArgs g{A, lda, transA, B, ldb, transB, C, ldc, M, N, K, bias, relu, precision == 3 ? 3 : 1, 0};
+  // widest N tile up to 256 that covers N with the fewest tiles (multiple of 16)
+  const int tiles = (N + 255) / 256;
+  int bn = (N + tiles - 1) / tiles;
+  bn = (bn + 15) / 16 * 16;
+  g.bn = bn;
+  const int stage = (kBM + bn) * kTileRowBytes * (g.precision == 3 ? 2 : 1);
+  const int smem = 2 * stage;
+  AP_CUDA_CHECK(cudaFuncSetAttribute(gemm_tf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  dim3 grid((M + kBM - 1) / kBM, (N + bn - 1) / bn);
+  gemm_tf32_kernel<<<grid, 128, smem, stream>>>(g);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+}  // namespace apb
+
+extern "C" int ap_gemm_tf32(const float* A, int64_t lda, int32_t transA, const float* B, int64_t ldb, int32_t transB,
+                            float* C, int64_t ldc, int32_t M, int32_t N, int32_t K, const float* bias, int32_t relu,
+                            int32_t precision, void* stream) {
+  if (!A || !B || !C || M < 0 || N < 0 || K < 0) {
+    apb::set_error("ap_gemm_tf32: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  return apb::launch_gemm_tf32(A, lda, transA, B, ldb, transB, C, ldc, M, N, K, bias, relu, precision,
+                               static_cast<cudaStream_t>(stream));
+}

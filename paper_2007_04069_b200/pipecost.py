@@ -168,7 +168,8 @@ def pipeline_length_batch(topo, compute, act, param, micro_batches: int, cuts=No
     """
     import torch
 
-    compute = compute.contiguous()
+    # keep every contiguous temporary alive until the launch is enqueued
+    compute, act, param = compute.contiguous(), act.contiguous(), param.contiguous()
     b, k = compute.shape
     given = cuts is not None
     if given:
@@ -180,8 +181,7 @@ def pipeline_length_batch(topo, compute, act, param, micro_batches: int, cuts=No
     lib = _native.require_device()
     topo_c = _native.Topology.of(topo)
     _native.check(lib.ap_pipe_length(ctypes.byref(topo_c), k, int(micro_batches), b, _native.ptr(compute),
-                                     _native.ptr(act.contiguous()), _native.ptr(param.contiguous()),
-                                     _native.ptr(cuts_t), int(given),
+                                     _native.ptr(act), _native.ptr(param), _native.ptr(cuts_t), int(given),
                                      -1.0 if mem_per_device is None else float(mem_per_device),
                                      float(optimizer_multiplier), int(bool(python_floats)), _native.ptr(length),
                                      _native.ptr(feas), _native.stream_handle()))

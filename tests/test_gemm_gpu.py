@@ -1,0 +1,57 @@
+"""tcgen05 GEMM numerics against a plain PyTorch fp64 reference of the same op."""
+
+import pytest
+import torch
+
+from paper_2007_04069_b200.tc import gemm
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [
+    (64, 256, 1060),   # Q-net layer 0 forward, batch 64, BERT-48 OPP state
+    (64, 256, 256),    # layer 1
+    (64, 3, 256),      # dueling heads (V + 2 advantages)
+    (1060, 256, 64),   # dW0 = x^T dz
+    (300, 40, 77),     # ragged everything
+    (4096, 256, 1060), # batched act over 4096 envs
+    (128, 2193, 256),  # PP-train advantage head (2192 actions + value)
+]
+
+
+def ref(a, b, ta, tb, bias, relu):
+    x = (a.t() if ta else a).double() @ (b.t() if tb else b).double()
+    if bias is not None:
+        x = x + bias.double()
+    if relu:
+        x = x.clamp_min(0.0)
+    return x
+
+
+@pytest.mark.parametrize("m,n,k", SHAPES)
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True)])
+def test_gemm_3xtf32_matches_fp64(cuda, m, n, k, ta, tb):
+    g = torch.Generator(device="cuda").manual_seed(m * 7 + n * 3 + k)
+    a = torch.randn((k, m) if ta else (m, k), device="cuda", generator=g)
+    b = torch.randn((n, k) if tb else (k, n), device="cuda", generator=g)
+    bias = torch.randn(n, device="cuda", generator=g)
+    out = gemm(a, b, trans_a=ta, trans_b=tb, bias=bias, relu=True, precision=3)
+    r = ref(a, b, ta, tb, bias, True)
+    err = (out.double() - r).abs().max().item()
+    scale = (a.abs().double().t() if not ta else a.abs().double()).shape  # noqa: F841
+    # fp32-level tolerance: |err| <= 1e-5 * sqrt(k) * |a||b| typical magnitude
+    tol = 2e-5 * (k ** 0.5) * 4.0
+    assert err < tol, (err, tol)
+
+
+@pytest.mark.parametrize("m,n,k", SHAPES[:4])
+def test_gemm_tf32_is_tf32_accurate(cuda, m, n, k):
+    g = torch.Generator(device="cuda").manual_seed(1)
+    a = torch.randn((m, k), device="cuda", generator=g)
+    b = torch.randn((k, n), device="cuda", generator=g)
+    out = gemm(a, b, precision=1)
+    r = ref(a, b, False, False, None, False)
+    rel = ((out.double() - r).abs().max() / r.abs().max()).item()
+    assert rel < 5e-3
+    out3 = gemm(a, b, precision=3)
+    rel3 = ((out3.double() - r).abs().max() / r.abs().max()).item()
+    assert rel3 < 1e-5 and rel3 < rel
