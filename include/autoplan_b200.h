@@ -229,6 +229,44 @@ int ap_gemm_tf32(const float* A, int64_t lda, int32_t transA, const float* B, in
                  float* C, int64_t ldc, int32_t M, int32_t N, int32_t K, const float* bias, int32_t relu,
                  int32_t precision, void* stream);
 
+/* Dueling combine Q = V + A - mean(A) from fused head outputs z = [V, A]
+ * (agent.py:104-109).  z [B, 1+A] (row stride ldz), q [B, A]. */
+int ap_dqn_dueling(const float* z, int64_t ldz, float* q, int64_t ldq, int32_t B, int32_t A, void* stream);
+
+/* Masked argmax per row, ties to the lowest index (agent.py:147-152); with
+ * epsilon > 0, epsilon-greedy with a counter-based RNG keyed by `seed`
+ * (throughput mode; parity mode draws with numpy on the host). */
+int ap_dqn_act(const float* q, int64_t ldq, const uint8_t* mask, int64_t ldm, int32_t E, int32_t A, float epsilon,
+               uint64_t seed, int32_t* actions, void* stream);
+
+/* Double-DQN TD error, per-row Huber loss contributions w*huber(td) (loss_rows
+ * [B]; the loss is their mean) and the gradient w.r.t. z = [V, A]
+ * (agent.py:258-299, 114-118). */
+int ap_dqn_td(const float* q, const float* online_next, const float* target_next, int64_t ldq, const int32_t* actions,
+              const float* rewards, const uint8_t* done, const uint8_t* next_mask, int64_t ldm, const float* weights,
+              int32_t B, int32_t A, float gamma, float huber_delta, float* dz, int64_t ldz, float* td,
+              float* loss_rows, void* stream);
+
+/* dh[i] = 0 where h[i] <= 0 (ReLU backward, agent.py:132). */
+int ap_dqn_relu_backward(float* dh, const float* h, int64_t n, void* stream);
+/* out[c] = sum_r x[r*ld + c] (bias gradients, agent.py:118,134). */
+int ap_dqn_colsum(const float* x, int64_t ld, int32_t rows, int32_t cols, float* out, void* stream);
+/* Adam over a flat parameter buffer (agent.py:240-250); correct1/2 = 1 - beta^t. */
+int ap_dqn_adam(float* params, const float* grads, float* m, float* v, int64_t n, float lr, float beta1, float beta2,
+                float eps, float correct1, float correct2, void* stream);
+
+/* Prioritized replay sample for B caller-drawn uniforms (agent.py:207-223):
+ * p**alpha, numpy pairwise sum, sequential cumsum / cdf[-1],
+ * searchsorted(side='right'), IS weights (n*p)**-beta / max.  fp64.
+ * scratch: 2*n + B doubles. */
+int ap_per_sample(const double* priorities, int32_t n, double alpha, double beta, const double* uniforms, int32_t B,
+                  double* scratch, int32_t* indices, float* weights, void* stream);
+/* priorities[idx] = |td| + 1e-6, last duplicate wins (agent.py:225-226). */
+int ap_per_update(double* priorities, const int32_t* indices, const float* td, int32_t B, void* stream);
+/* dst[b, :] = src[idx[b], :] (replay minibatch gather). */
+int ap_gather_rows(const float* src, int64_t lds, const int32_t* idx, int32_t B, int32_t cols, float* dst,
+                   int64_t ldd, void* stream);
+
 const char* ap_last_error(void);
 const char* ap_version(void);
 

@@ -111,6 +111,17 @@ SIGNATURES: dict[str, tuple] = {
     "ap_infer_search": (ctypes.c_int, [_VP, _I32, _TOPO, _I32, _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "ap_gemm_tf32": (ctypes.c_int, [_VP, _I64, _I32, _VP, _I64, _I32, _VP, _I64, _I32, _I32, _I32, _VP, _I32, _I32,
                                     _VP]),
+    "ap_dqn_dueling": (ctypes.c_int, [_VP, _I64, _VP, _I64, _I32, _I32, _VP]),
+    "ap_dqn_act": (ctypes.c_int, [_VP, _I64, _VP, _I64, _I32, _I32, ctypes.c_float, ctypes.c_uint64, _VP, _VP]),
+    "ap_dqn_td": (ctypes.c_int, [_VP, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _I64, _VP, _I32, _I32, ctypes.c_float,
+                                 ctypes.c_float, _VP, _I64, _VP, _VP, _VP]),
+    "ap_dqn_relu_backward": (ctypes.c_int, [_VP, _VP, _I64, _VP]),
+    "ap_dqn_colsum": (ctypes.c_int, [_VP, _I64, _I32, _I32, _VP, _VP]),
+    "ap_dqn_adam": (ctypes.c_int, [_VP, _VP, _VP, _VP, _I64, ctypes.c_float, ctypes.c_float, ctypes.c_float,
+                                   ctypes.c_float, ctypes.c_float, ctypes.c_float, _VP]),
+    "ap_per_sample": (ctypes.c_int, [_VP, _I32, _F64, _F64, _VP, _I32, _VP, _VP, _VP, _VP]),
+    "ap_per_update": (ctypes.c_int, [_VP, _VP, _VP, _I32, _VP]),
+    "ap_gather_rows": (ctypes.c_int, [_VP, _I64, _VP, _I32, _I32, _VP, _I64, _VP]),
     "ap_last_error": (ctypes.c_char_p, []),
     "ap_version": (ctypes.c_char_p, []),
 }

@@ -1,0 +1,549 @@
+"""Dueling double DQN with prioritized replay, device-resident.
+
+Same public surface as reference `autoplan.agent` (`pkg/src/autoplan/agent.py:21-392`):
+`AgentConfig`, `epsilon_at`, `QNetwork`, `masked_argmax`, `act`,
+`Transition`, `PrioritizedReplayBuffer`, `AdamOptimizer`, `huber`,
+`train_step`, `DqnAgent` (act / observe / learn / save / load), and the
+same `.npz` checkpoint layout.
+
+Where it runs:
+* Q-network forward / backward contractions: tcgen05 tensor-core GEMMs
+  (3xTF32, fp32-accurate) with bias + ReLU fused into the GEMM epilogue;
+* dueling combine, TD / Huber / head gradients, ReLU backward, bias
+  gradients, Adam, PER sampling and priority updates: fused kernels
+  (`csrc/dqn.cu`);
+* replay ring, both networks, Adam moments and priorities live in HBM;
+  the target sync is a device copy.
+Random draws come from the same `numpy.random.Generator` stream as the
+reference (network init, epsilon-greedy, the uniforms behind `rng.choice`),
+so with identical inputs the agent takes the same decisions; Q-values agree
+with the fp64 reference within fp32 tolerance.
+"""
+
+from __future__ import annotations
+
+import json
+from dataclasses import asdict, dataclass
+from typing import Sequence
+
+import numpy as np
+
+from . import _native
+from .tc import gemm
+
+
+class CheckpointError(Exception):
+    """A checkpoint file does not match the expected layout."""
+
+
+class DivergenceError(Exception):
+    """Training produced a non-finite loss."""
+
+
+@dataclass(frozen=True)
+class AgentConfig:
+    gamma: float = 0.6
+    lr: float = 0.001
+    batch_size: int = 64
+    buffer_capacity: int = 2000
+    per_alpha: float = 0.2
+    per_beta: float = 0.6
+    target_sync_every: int = 100
+    epsilon_start: float = 1.0
+    epsilon_final: float = 0.1
+    epsilon_decay_iters: int = 2000
+    hidden: tuple[int, ...] = (256, 256)
+    huber_delta: float = 1.0
+    adam_beta1: float = 0.9
+    adam_beta2: float = 0.999
+    adam_eps: float = 1e-8
+
+
+def epsilon_at(iteration: int, config: AgentConfig) -> float:
+    """Linear decay from epsilon_start to epsilon_final (agent.py:50-55)."""
+    if config.epsilon_decay_iters <= 0:
+        return config.epsilon_final
+    frac = min(1.0, max(0.0, iteration / config.epsilon_decay_iters))
+    return config.epsilon_start + (config.epsilon_final - config.epsilon_start) * frac
+
+
+def _stream():
+    return _native.stream_handle()
+
+
+class QNetwork:
+    """Dueling MLP on the device: ReLU trunk, value head, advantage head.
+
+    Parameters live in one flat fp32 buffer (views: w_i [fan_in, width],
+    b_i, then the fused head wh = [wv | wa] [width, 1 + A] and bh).
+    """
+
+    def __init__(self, state_dim: int, num_actions: int, hidden: Sequence[int] = (256, 256),
+                 rng: np.random.Generator | None = None, _init: bool = True):
+        if state_dim < 1 or num_actions < 1:
+            raise ValueError("state_dim and num_actions must be positive")
+        if not hidden:
+            raise ValueError("the trunk needs at least one hidden layer")
+        import torch
+
+        self.state_dim = state_dim
+        self.num_actions = num_actions
+        self.hidden = tuple(hidden)
+        shapes = []
+        fan_in = state_dim
+        for i, width in enumerate(self.hidden):
+            shapes += [(f"w{i}", (fan_in, width)), (f"b{i}", (width,))]
+            fan_in = width
+        shapes += [("wh", (fan_in, 1 + num_actions)), ("bh", (1 + num_actions,))]
+        self._shapes = shapes
+        total = sum(int(np.prod(s)) for _, s in shapes)
+        self.flat = torch.zeros(total, dtype=torch.float32, device="cuda")
+        self.grad = torch.zeros(total, dtype=torch.float32, device="cuda")
+        self.views: dict[str, "torch.Tensor"] = {}
+        self.grads: dict[str, "torch.Tensor"] = {}
+        off = 0
+        for name, shape in shapes:
+            n = int(np.prod(shape))
+            self.views[name] = self.flat[off: off + n].view(shape)
+            self.grads[name] = self.grad[off: off + n].view(shape)
+            off += n
+        if _init:
+            rng = rng or np.random.default_rng(0)
+            params = {}
+            fan_in = state_dim
+            for i, width in enumerate(self.hidden):
+                params[f"w{i}"] = self._init(rng, fan_in, width)
+                params[f"b{i}"] = self._init(rng, fan_in, width, bias=True)
+                fan_in = width
+            params["wv"] = self._init(rng, fan_in, 1)
+            params["bv"] = self._init(rng, fan_in, 1, bias=True)
+            params["wa"] = self._init(rng, fan_in, num_actions)
+            params["ba"] = self._init(rng, fan_in, num_actions, bias=True)
+            self.load_params(params)
+
+    @staticmethod
+    def _init(rng, fan_in: int, width: int, bias: bool = False) -> np.ndarray:
+        """Same draws as the reference initializer (agent.py:87-91)."""
+        bound = 1.0 / np.sqrt(fan_in)
+        return rng.uniform(-bound, bound, size=(width,) if bias else (fan_in, width)).astype(np.float64)
+
+    # -- reference-layout parameter access -------------------------------------------
+
+    @property
+    def params(self) -> dict[str, np.ndarray]:
+        """Host fp64 copies in the reference layout (w*, b*, wv, bv, wa, ba)."""
+        out = {}
+        for i in range(len(self.hidden)):
+            out[f"w{i}"] = self.views[f"w{i}"].double().cpu().numpy()
+            out[f"b{i}"] = self.views[f"b{i}"].double().cpu().numpy()
+        wh = self.views["wh"].double().cpu().numpy()
+        bh = self.views["bh"].double().cpu().numpy()
+        out["wv"], out["wa"] = wh[:, :1].copy(), wh[:, 1:].copy()
+        out["bv"], out["ba"] = bh[:1].copy(), bh[1:].copy()
+        return out
+
+    def load_params(self, params: dict[str, np.ndarray]) -> None:
+        import torch
+
+        for i in range(len(self.hidden)):
+            self.views[f"w{i}"].copy_(torch.from_numpy(np.asarray(params[f"w{i}"])))
+            self.views[f"b{i}"].copy_(torch.from_numpy(np.asarray(params[f"b{i}"])))
+        wh = np.concatenate([np.asarray(params["wv"]), np.asarray(params["wa"])], axis=1)
+        bh = np.concatenate([np.asarray(params["bv"]), np.asarray(params["ba"])])
+        self.views["wh"].copy_(torch.from_numpy(wh))
+        self.views["bh"].copy_(torch.from_numpy(bh))
+
+    # -- compute ----------------------------------------------------------------------
+
+    def forward_device(self, x, cache: bool = False):
+        """Q [B, A] for device states x [B, state_dim] fp32 (and the activations when cache)."""
+        import torch
+
+        acts = [x]
+        h = x
+        for i in range(len(self.hidden)):
+            h = gemm(h, self.views[f"w{i}"], bias=self.views[f"b{i}"], relu=True)
+            acts.append(h)
+        z = gemm(h, self.views["wh"], bias=self.views["bh"])
+        b = x.shape[0]
+        q = torch.empty((b, self.num_actions), dtype=torch.float32, device="cuda")
+        lib = _native.require_device()
+        _native.check(lib.ap_dqn_dueling(_native.ptr(z), z.stride(0), _native.ptr(q), q.stride(0), b,
+                                         self.num_actions, _stream()))
+        return (q, acts) if cache else q
+
+    def forward(self, states) -> np.ndarray:
+        import torch
+
+        x = torch.as_tensor(np.atleast_2d(np.asarray(states, dtype=np.float64)), dtype=torch.float32).cuda()
+        if x.shape[1] != self.state_dim:
+            raise ValueError(f"expected state dim {self.state_dim}, got {x.shape[1]}")
+        return self.forward_device(x).double().cpu().numpy()
+
+    def backward_device(self, acts, dz) -> None:
+        """Gradients into self.grad from dLoss/dz (z = [V, A] head outputs)."""
+        lib = _native.require_device()
+        h = acts[-1]
+        b = dz.shape[0]
+        gemm(h, dz, trans_a=True, out=self.grads["wh"])
+        _native.check(lib.ap_dqn_colsum(_native.ptr(dz), dz.stride(0), b, dz.shape[1], _native.ptr(self.grads["bh"]),
+                                        _stream()))
+        dh = gemm(dz, self.views["wh"], trans_b=True)
+        for i in range(len(self.hidden) - 1, -1, -1):
+            _native.check(lib.ap_dqn_relu_backward(_native.ptr(dh), _native.ptr(acts[i + 1]), dh.numel(), _stream()))
+            gemm(acts[i], dh, trans_a=True, out=self.grads[f"w{i}"])
+            _native.check(lib.ap_dqn_colsum(_native.ptr(dh), dh.stride(0), b, dh.shape[1],
+                                            _native.ptr(self.grads[f"b{i}"]), _stream()))
+            if i > 0:
+                dh = gemm(dh, self.views[f"w{i}"], trans_b=True)
+
+    def forward_cached(self, states):
+        import torch
+
+        x = torch.as_tensor(np.atleast_2d(np.asarray(states, dtype=np.float64)), dtype=torch.float32).cuda()
+        q, acts = self.forward_device(x, cache=True)
+        return q.double().cpu().numpy(), {"acts": acts}
+
+    def backward(self, cache: dict, dq: np.ndarray) -> dict[str, np.ndarray]:
+        """Reference-layout gradients for dLoss/dQ (agent.py:111-136)."""
+        import torch
+
+        dq = np.asarray(dq, dtype=np.float64)
+        dz = np.concatenate([dq.sum(axis=1, keepdims=True), dq - dq.sum(axis=1, keepdims=True) / self.num_actions],
+                            axis=1)
+        self.backward_device(cache["acts"], torch.from_numpy(dz).float().cuda().contiguous())
+        out = {}
+        for i in range(len(self.hidden)):
+            out[f"w{i}"] = self.grads[f"w{i}"].double().cpu().numpy()
+            out[f"b{i}"] = self.grads[f"b{i}"].double().cpu().numpy()
+        gh = self.grads["wh"].double().cpu().numpy()
+        gb = self.grads["bh"].double().cpu().numpy()
+        out["wv"], out["wa"], out["bv"], out["ba"] = gh[:, :1], gh[:, 1:], gb[:1], gb[1:]
+        return out
+
+    def copy_from(self, other: "QNetwork") -> None:
+        self.flat.copy_(other.flat)
+
+    def clone(self) -> "QNetwork":
+        twin = QNetwork(self.state_dim, self.num_actions, self.hidden, _init=False)
+        twin.copy_from(self)
+        return twin
+
+
+def sync_target(net: QNetwork, target_net: QNetwork) -> None:
+    """Hard device copy of the online parameters (agent.py:142-144)."""
+    target_net.copy_from(net)
+
+
+def masked_argmax(q: np.ndarray, mask: np.ndarray) -> int:
+    """Highest allowed Q, ties to the lowest index (agent.py:147-152)."""
+    if not mask.any():
+        raise ValueError("no action is allowed")
+    return int(np.argmax(np.where(mask, q, -np.inf)))
+
+
+def act(net: QNetwork, state: np.ndarray, mask: np.ndarray, epsilon: float, rng: np.random.Generator) -> int:
+    """Epsilon-greedy over the allowed set (agent.py:155-170), same draw order as the reference."""
+    import torch
+
+    mask = np.asarray(mask, dtype=bool)
+    if not mask.any():
+        raise ValueError("no action is allowed")
+    if rng.random() < epsilon:
+        allowed = np.flatnonzero(mask)
+        return int(allowed[rng.integers(len(allowed))])
+    x = torch.as_tensor(np.asarray(state, dtype=np.float64), dtype=torch.float32).cuda().view(1, -1)
+    q = net.forward_device(x)
+    m = torch.from_numpy(mask.astype(np.uint8)).cuda().view(1, -1)
+    out = torch.empty(1, dtype=torch.int32, device="cuda")
+    lib = _native.require_device()
+    _native.check(lib.ap_dqn_act(_native.ptr(q), q.stride(0), _native.ptr(m), m.stride(0), 1, net.num_actions, 0.0, 0,
+                                 _native.ptr(out), _stream()))
+    return int(out.item())
+
+
+@dataclass(frozen=True)
+class Transition:
+    state: np.ndarray
+    action: int
+    reward: float
+    next_state: np.ndarray
+    done: bool
+    next_mask: np.ndarray
+
+
+class PrioritizedReplayBuffer:
+    """Device ring buffer with proportional prioritized sampling (agent.py:183-226)."""
+
+    def __init__(self, capacity: int = 2000, state_dim: int | None = None, num_actions: int | None = None):
+        if capacity < 1:
+            raise ValueError("capacity must be positive")
+        self.capacity = capacity
+        self.state_dim = state_dim
+        self.num_actions = num_actions
+        self._size = 0
+        self._next = 0
+        self._store = None
+
+    def _alloc(self, state_dim: int, num_actions: int) -> None:
+        import torch
+
+        c = self.capacity
+        dev = "cuda"
+        self.state_dim, self.num_actions = state_dim, num_actions
+        self._store = {
+            "states": torch.zeros((c, state_dim), dtype=torch.float32, device=dev),
+            "next_states": torch.zeros((c, state_dim), dtype=torch.float32, device=dev),
+            "actions": torch.zeros(c, dtype=torch.int32, device=dev),
+            "rewards": torch.zeros(c, dtype=torch.float32, device=dev),
+            "done": torch.zeros(c, dtype=torch.uint8, device=dev),
+            "next_mask": torch.zeros((c, num_actions), dtype=torch.uint8, device=dev),
+            "priorities": torch.zeros(c, dtype=torch.float64, device=dev),
+            "scratch": torch.zeros(2 * c + 1024, dtype=torch.float64, device=dev),
+        }
+
+    def __len__(self) -> int:
+        return self._size
+
+    @property
+    def store(self):
+        return self._store
+
+    def push(self, t: Transition) -> None:
+        """Insert with the current maximum priority (agent.py:197-205)."""
+        import torch
+
+        if self._store is None:
+            self._alloc(len(t.state), len(t.next_mask))
+        s = self._store
+        k = self._next
+        s["states"][k].copy_(torch.as_tensor(np.asarray(t.state, np.float64), dtype=torch.float32))
+        s["next_states"][k].copy_(torch.as_tensor(np.asarray(t.next_state, np.float64), dtype=torch.float32))
+        s["actions"][k] = int(t.action)
+        s["rewards"][k] = float(t.reward)
+        s["done"][k] = int(bool(t.done))
+        s["next_mask"][k].copy_(torch.as_tensor(np.asarray(t.next_mask, dtype=np.uint8)))
+        self.push_priority(k)
+        self._size = min(self._size + 1, self.capacity)
+        self._next = (k + 1) % self.capacity
+
+    def push_priority(self, slot: int) -> None:
+        pr = self._store["priorities"]
+        if self._size:
+            pr[slot] = pr[: self._size].max()  # device-side, no sync
+        else:
+            pr[slot] = 1.0
+
+    def sample_device(self, batch_size: int, alpha: float, beta: float, uniforms):
+        """Indices [B] int32 and IS weights [B] fp32 on the device for the given uniforms."""
+        import torch
+
+        n = self._size
+        if n < batch_size:
+            raise ValueError("not enough transitions to sample a batch")
+        s = self._store
+        u = torch.as_tensor(uniforms, dtype=torch.float64).cuda()
+        idx = torch.empty(batch_size, dtype=torch.int32, device="cuda")
+        w = torch.empty(batch_size, dtype=torch.float32, device="cuda")
+        if s["scratch"].numel() < 2 * n + batch_size:
+            s["scratch"] = torch.zeros(2 * n + batch_size, dtype=torch.float64, device="cuda")
+        lib = _native.require_device()
+        _native.check(lib.ap_per_sample(_native.ptr(s["priorities"]), n, float(alpha), float(beta), _native.ptr(u),
+                                        batch_size, _native.ptr(s["scratch"]), _native.ptr(idx), _native.ptr(w),
+                                        _stream()))
+        return idx, w
+
+    def sample(self, batch_size: int, alpha: float, beta: float, rng: np.random.Generator):
+        """(indices, None, weights) on the host; draws rng.random(B) exactly like rng.choice would."""
+        u = rng.random(batch_size)
+        idx, w = self.sample_device(batch_size, alpha, beta, u)
+        return idx.cpu().numpy().astype(np.int64), None, w.double().cpu().numpy()
+
+    def update_priorities_device(self, indices, td) -> None:
+        lib = _native.require_device()
+        _native.check(lib.ap_per_update(_native.ptr(self._store["priorities"]), _native.ptr(indices), _native.ptr(td),
+                                        int(indices.numel()), _stream()))
+
+    @property
+    def priorities(self) -> np.ndarray:
+        return self._store["priorities"][: self._size].cpu().numpy()
+
+
+class AdamOptimizer:
+    """Adam with bias correction over the network's flat buffer (agent.py:229-250)."""
+
+    def __init__(self, net: QNetwork, config: AgentConfig):
+        import torch
+
+        self.net = net
+        self.lr = config.lr
+        self.beta1 = config.adam_beta1
+        self.beta2 = config.adam_beta2
+        self.eps = config.adam_eps
+        self.t = 0
+        self.m = torch.zeros_like(net.flat)
+        self.v = torch.zeros_like(net.flat)
+
+    def step(self) -> None:
+        self.t += 1
+        c1 = 1.0 - self.beta1 ** self.t
+        c2 = 1.0 - self.beta2 ** self.t
+        lib = _native.require_device()
+        _native.check(lib.ap_dqn_adam(_native.ptr(self.net.flat), _native.ptr(self.net.grad), _native.ptr(self.m),
+                                      _native.ptr(self.v), self.net.flat.numel(), self.lr, self.beta1, self.beta2,
+                                      self.eps, c1, c2, _stream()))
+
+
+def huber(x: np.ndarray, delta: float) -> np.ndarray:
+    ax = np.abs(x)
+    return np.where(ax <= delta, 0.5 * x ** 2, delta * (ax - 0.5 * delta))
+
+
+class _Batch:
+    """Preallocated device minibatch buffers for one (B, state_dim, A)."""
+
+    def __init__(self, b: int, s: int, a: int):
+        import torch
+
+        self.states = torch.empty((b, s), dtype=torch.float32, device="cuda")
+        self.next_states = torch.empty((b, s), dtype=torch.float32, device="cuda")
+        self.dz = torch.empty((b, 1 + a), dtype=torch.float32, device="cuda")
+        self.td = torch.empty(b, dtype=torch.float32, device="cuda")
+        self.loss_rows = torch.empty(b, dtype=torch.float32, device="cuda")
+        self.loss = torch.empty(1, dtype=torch.float32, device="cuda")
+
+
+def train_step_device(net: QNetwork, target_net: QNetwork, buffer: PrioritizedReplayBuffer, config: AgentConfig,
+                      optimizer: AdamOptimizer, uniforms, batch: _Batch | None = None):
+    """One double-DQN update, all on the device; returns the loss as a device scalar (agent.py:258-299)."""
+    lib = _native.require_device()
+    b = config.batch_size
+    s = buffer.store
+    batch = batch or _Batch(b, net.state_dim, net.num_actions)
+    idx, weights = buffer.sample_device(b, config.per_alpha, config.per_beta, uniforms)
+    for src, dst in ((s["states"], batch.states), (s["next_states"], batch.next_states)):
+        _native.check(lib.ap_gather_rows(_native.ptr(src), src.stride(0), _native.ptr(idx), b, src.shape[1],
+                                         _native.ptr(dst), dst.stride(0), _stream()))
+    il = idx.long()
+    actions = s["actions"][il]
+    rewards = s["rewards"][il]
+    done = s["done"][il]
+    masks = s["next_mask"][il].contiguous()
+    online_next = net.forward_device(batch.next_states)
+    target_next = target_net.forward_device(batch.next_states)
+    q_all, acts = net.forward_device(batch.states, cache=True)
+    _native.check(lib.ap_dqn_td(_native.ptr(q_all), _native.ptr(online_next), _native.ptr(target_next),
+                                q_all.stride(0), _native.ptr(actions), _native.ptr(rewards), _native.ptr(done),
+                                _native.ptr(masks), masks.stride(0), _native.ptr(weights), b, net.num_actions,
+                                float(config.gamma), float(config.huber_delta), _native.ptr(batch.dz),
+                                batch.dz.stride(0), _native.ptr(batch.td), _native.ptr(batch.loss_rows), _stream()))
+    net.backward_device(acts, batch.dz)
+    optimizer.step()
+    buffer.update_priorities_device(idx, batch.td)
+    _native.check(lib.ap_dqn_colsum(_native.ptr(batch.loss_rows), 1, b, 1, _native.ptr(batch.loss), _stream()))
+    return batch.loss
+
+
+def train_step(net, target_net, buffer, config, optimizer, rng) -> float:
+    """Reference signature: draws the sampling uniforms from `rng`, returns the loss."""
+    loss = train_step_device(net, target_net, buffer, config, optimizer, rng.random(config.batch_size))
+    return float(loss.item()) / config.batch_size
+
+
+class DqnAgent:
+    """Network, target, replay buffer and Adam together (agent.py:302-392)."""
+
+    def __init__(self, config: AgentConfig, state_dim: int, num_actions: int, seed: int = 0):
+        self.config = config
+        self.rng = np.random.default_rng(seed)
+        self.net = QNetwork(state_dim, num_actions, config.hidden, self.rng)
+        self.target = self.net.clone()
+        self.buffer = PrioritizedReplayBuffer(config.buffer_capacity, state_dim, num_actions)
+        self.optimizer = AdamOptimizer(self.net, config)
+        self.train_steps = 0
+        self._batch = None
+
+    @property
+    def epsilon(self) -> float:
+        return epsilon_at(self.train_steps, self.config)
+
+    def act(self, state: np.ndarray, mask: np.ndarray, greedy: bool = False) -> int:
+        return act(self.net, state, mask, 0.0 if greedy else self.epsilon, self.rng)
+
+    def observe(self, transition: Transition) -> None:
+        self.buffer.push(transition)
+
+    def learn(self) -> float | None:
+        if len(self.buffer) < self.config.batch_size:
+            return None
+        if self._batch is None:
+            self._batch = _Batch(self.config.batch_size, self.net.state_dim, self.net.num_actions)
+        loss_t = train_step_device(self.net, self.target, self.buffer, self.config, self.optimizer,
+                                   self.rng.random(self.config.batch_size), self._batch)
+        loss = float(loss_t.item()) / self.config.batch_size
+        if not np.isfinite(loss):
+            raise DivergenceError(f"training loss diverged to {loss}")
+        self.train_steps += 1
+        if self.train_steps % self.config.target_sync_every == 0:
+            sync_target(self.net, self.target)
+        return loss
+
+    # -- checkpoints (reference .npz layout, agent.py:341-392) ----------------------
+
+    def save(self, path: str) -> None:
+        arrays = {f"net.{k}": v for k, v in self.net.params.items()}
+        arrays.update({f"target.{k}": v for k, v in self.target.params.items()})
+        for slot, buf in (("m", self.optimizer.m), ("v", self.optimizer.v)):
+            tmp = QNetwork(self.net.state_dim, self.net.num_actions, self.net.hidden, _init=False)
+            tmp.flat.copy_(buf)
+            arrays.update({f"adam.{slot}.{k}": v for k, v in tmp.params.items()})
+        header = {
+            "version": 1,
+            "config": asdict(self.config),
+            "state_dim": self.net.state_dim,
+            "num_actions": self.net.num_actions,
+            "train_steps": self.train_steps,
+            "adam_t": self.optimizer.t,
+            "rng_state": self.rng.bit_generator.state,
+        }
+        with open(path, "wb") as fh:
+            np.savez(fh, header=np.frombuffer(json.dumps(header).encode(), dtype=np.uint8), **arrays)
+
+    @classmethod
+    def load(cls, path: str) -> "DqnAgent":
+        try:
+            with np.load(path) as blob:
+                header = json.loads(bytes(blob["header"]).decode())
+                arrays = {k: blob[k] for k in blob.files if k != "header"}
+        except (OSError, KeyError, ValueError, json.JSONDecodeError) as exc:
+            raise CheckpointError(f"cannot read checkpoint {path}: {exc}") from exc
+        if header.get("version") != 1:
+            raise CheckpointError(f"unsupported checkpoint version {header.get('version')}")
+        raw = dict(header["config"])
+        raw["hidden"] = tuple(raw["hidden"])
+        config = AgentConfig(**raw)
+        agent = cls(config, header["state_dim"], header["num_actions"])
+        expected = agent.net.params
+        for scope, net in (("net", agent.net), ("target", agent.target)):
+            params = {}
+            for key, ref in expected.items():
+                stored = arrays.get(f"{scope}.{key}")
+                if stored is None or stored.shape != ref.shape:
+                    raise CheckpointError(f"checkpoint parameter {scope}.{key} is missing or has the wrong shape")
+                params[key] = stored.astype(np.float64)
+            net.load_params(params)
+        for slot, buf in (("m", agent.optimizer.m), ("v", agent.optimizer.v)):
+            params = {}
+            for key, ref in expected.items():
+                stored = arrays.get(f"adam.{slot}.{key}")
+                if stored is None or stored.shape != ref.shape:
+                    raise CheckpointError(f"checkpoint slot adam.{slot}.{key} is missing or malformed")
+                params[key] = stored.astype(np.float64)
+            tmp = QNetwork(header["state_dim"], header["num_actions"], config.hidden, _init=False)
+            tmp.load_params(params)
+            buf.copy_(tmp.flat)
+        agent.train_steps = int(header["train_steps"])
+        agent.optimizer.t = int(header["adam_t"])
+        agent.rng = np.random.default_rng()
+        agent.rng.bit_generator.state = header["rng_state"]
+        return agent

@@ -1,0 +1,406 @@
+// DQN learner kernels (reference agent.py:58-337), device-resident.
+//
+// The Q-network GEMMs run on the tensor cores (gemm_tc.cu); these kernels are
+// the non-GEMM parts, each fused to one pass:
+//   dueling combine          Q = V + A - mean(A)                (agent.py:104-109)
+//   masked argmax / act      ties to the lowest index           (agent.py:147-170)
+//   TD + Huber + head grads  double-DQN target, IS weights,     (agent.py:258-299)
+//                            dQ folded straight into dV / dA    (agent.py:114-118)
+//   ReLU backward, column sums (bias grads)                     (agent.py:119-136)
+//   Adam with bias correction over one flat parameter buffer    (agent.py:229-250)
+//   PER: priority**alpha, numpy pairwise sum, sequential cumsum,
+//        searchsorted(side='right'), IS weights; last-write-wins
+//        priority scatter                                        (agent.py:183-226)
+// PER arithmetic is fp64 and follows numpy's evaluation order so the sampled
+// indices match the reference for the same uniforms.
+#include <cmath>
+
+#include "engine.h"
+
+namespace apb {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__global__ void dueling_kernel(const float* z, int64_t ldz, float* q, int64_t ldq, int B, int A) {
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= B) return;
+  const float* row = z + (int64_t)b * ldz;
+  float s = 0.0f;
+  for (int j = lane; j < A; j += 32) s += row[1 + j];
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  const float mean = s / (float)A;
+  const float v = row[0];
+  for (int j = lane; j < A; j += 32) q[(int64_t)b * ldq + j] = v + row[1 + j] - mean;
+}
+
+// masked argmax (ties -> lowest index); eps-greedy with a counter-based hash
+// when eps > 0 (throughput mode; parity mode draws on the host)
+__device__ inline uint32_t hash32(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdULL;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ULL;
+  x ^= x >> 33;
+  return (uint32_t)x;
+}
+
+__global__ void act_kernel(const float* q, int64_t ldq, const uint8_t* mask, int64_t ldm, int E, int A, float eps,
+                           uint64_t seed, int32_t* out) {
+  const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (e >= E) return;
+  const uint8_t* m = mask + (int64_t)e * ldm;
+  int count = 0;
+  float best = -INFINITY;
+  int best_j = 0x7fffffff;
+  for (int j = lane; j < A; j += 32) {
+    if (!m[j]) continue;
+    ++count;
+    const float v = q[(int64_t)e * ldq + j];
+    if (v > best || (v == best && j < best_j)) {
+      best = v;
+      best_j = j;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    const float ov = __shfl_xor_sync(kFull, best, o);
+    const int oj = __shfl_xor_sync(kFull, best_j, o);
+    if (ov > best || (ov == best && oj < best_j)) {
+      best = ov;
+      best_j = oj;
+    }
+    count += __shfl_xor_sync(kFull, count, o);
+  }
+  int action = best_j == 0x7fffffff ? -1 : best_j;
+  if (eps > 0.0f && count > 0) {
+    const uint32_t r0 = hash32(seed * 0x9E3779B97F4A7C15ULL + (uint64_t)e * 2 + 0);
+    if ((float)(r0 >> 8) * (1.0f / 16777216.0f) < eps) {
+      const int pick = (int)(hash32(seed * 0x9E3779B97F4A7C15ULL + (uint64_t)e * 2 + 1) % (uint32_t)count);
+      // the pick-th allowed action
+      int seen = 0;
+      action = -1;
+      for (int base = 0; base < A && action < 0; base += 32) {
+        const int j = base + lane;
+        const bool ok = j < A && m[j];
+        const unsigned bal = __ballot_sync(kFull, ok);
+        const int n = __popc(bal);
+        if (pick < seen + n) {
+          unsigned bits = bal;
+          for (int k = 0; k < pick - seen; ++k) bits &= bits - 1;
+          action = base + __ffs(bits) - 1;
+        }
+        seen += n;
+      }
+    }
+  }
+  if (lane == 0) out[e] = action;
+}
+
+// Double-DQN TD error, Huber-weighted loss and the gradient w.r.t. the fused
+// head outputs z = [V, A_0..A_{n-1}] (agent.py:258-299, 114-118).
+__global__ void td_kernel(const float* q, const float* online_next, const float* target_next, int64_t ldq,
+                          const int32_t* actions, const float* rewards, const uint8_t* done, const uint8_t* next_mask,
+                          int64_t ldm, const float* weights, int B, int A, float gamma, float delta, float* dz,
+                          int64_t ldz, float* td_out, float* loss_out) {
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= B) return;
+  const uint8_t* m = next_mask + (int64_t)b * ldm;
+  // best next action by the online net over the (safe) next mask
+  bool any = false;
+  float best = -INFINITY;
+  int best_j = 0x7fffffff;
+  for (int j = lane; j < A; j += 32) {
+    if (!m[j]) continue;
+    any = true;
+    const float v = online_next[(int64_t)b * ldq + j];
+    if (v > best || (v == best && j < best_j)) {
+      best = v;
+      best_j = j;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    const float ov = __shfl_xor_sync(kFull, best, o);
+    const int oj = __shfl_xor_sync(kFull, best_j, o);
+    if (ov > best || (ov == best && oj < best_j)) {
+      best = ov;
+      best_j = oj;
+    }
+  }
+  any = __any_sync(kFull, any);
+  const int a_next = any ? best_j : 0;  // empty mask: action 0 is "safe", bootstrap zeroed below
+  const float d = (done[b] || !any) ? 1.0f : 0.0f;
+  const float target = rewards[b] + gamma * (1.0f - d) * target_next[(int64_t)b * ldq + a_next];
+  const int a = actions[b];
+  const float td = q[(int64_t)b * ldq + a] - target;
+  const float w = weights[b];
+  const float ad = fabsf(td);
+  const float hub = ad <= delta ? 0.5f * td * td : delta * (ad - 0.5f * delta);
+  const float g = w * fminf(fmaxf(td, -delta), delta) / (float)B;
+  for (int j = lane; j <= A; j += 32) {
+    float v;
+    if (j == 0)
+      v = g;  // dV = sum_j dQ_j
+    else
+      v = ((j - 1) == a ? g : 0.0f) - g / (float)A;  // dA_j = dQ_j - sum(dQ)/A
+    dz[(int64_t)b * ldz + j] = v;
+  }
+  if (lane == 0) {
+    td_out[b] = td;
+    loss_out[b] = w * hub;  // loss = mean over rows, reduced deterministically by the caller
+  }
+}
+
+__global__ void relu_bwd_kernel(float* dh, const float* h, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (!(h[i] > 0.0f)) dh[i] = 0.0f;
+}
+
+__global__ void colsum_kernel(const float* x, int64_t ld, int rows, int cols, float* out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  float s = 0.0f;
+  for (int r = 0; r < rows; ++r) s += x[(int64_t)r * ld + c];
+  out[c] = s;
+}
+
+__global__ void adam_kernel(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
+                            float eps, float c1, float c2) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    const float mi = b1 * m[i] + (1.0f - b1) * gi;
+    const float vi = b2 * v[i] + (1.0f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    p[i] -= lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+  }
+}
+
+// numpy pairwise summation of a block of <= 128 doubles
+// (numpy/_core/src/umath/loops_utils.h.src, PW_BLOCKSIZE = 128)
+__device__ double pairwise_leaf(const double* x, int64_t m) {
+  if (m < 8) {
+    double v = -0.0;  // numpy starts from -0.0 to preserve -0.0 sums
+    for (int64_t i = 0; i < m; ++i) v += x[i];
+    return v;
+  }
+  double r[8];
+  for (int k = 0; k < 8; ++k) r[k] = x[k];
+  int64_t i;
+  for (i = 8; i < m - (m % 8); i += 8)
+    for (int k = 0; k < 8; ++k) r[k] += x[i + k];
+  double v = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (; i < m; ++i) v += x[i];
+  return v;
+}
+
+// the recursion sum(a, n) = sum(a, n2) + sum(a + n2, n - n2), n2 = n/2 rounded
+// down to a multiple of 8, evaluated with an explicit post-order stack
+__device__ double pairwise_sum(const double* a, int64_t n) {
+  struct Frame {
+    int64_t off, n;
+    int state;
+    double left;
+  };
+  Frame fr[64];
+  int top = 0;
+  fr[0] = {0, n, 0, 0.0};
+  double ret = 0.0;
+  while (top >= 0) {
+    Frame& f = fr[top];
+    if (f.n <= 128) {
+      ret = pairwise_leaf(a + f.off, f.n);
+      --top;
+      continue;
+    }
+    int64_t n2 = f.n / 2;
+    n2 -= n2 % 8;
+    if (f.state == 0) {
+      f.state = 1;
+      fr[top + 1] = {f.off, n2, 0, 0.0};
+      ++top;
+    } else if (f.state == 1) {
+      f.left = ret;
+      f.state = 2;
+      fr[top + 1] = {f.off + n2, f.n - n2, 0, 0.0};
+      ++top;
+    } else {
+      ret = f.left + ret;
+      --top;
+    }
+  }
+  return ret;
+}
+
+// one CTA: PER sample (agent.py:207-223) for B uniforms drawn by the caller
+__global__ void per_sample_kernel(const double* prio, int n, double alpha, double beta, const double* uniforms, int B,
+                                  double* scaled, double* cdf, int32_t* idx_out, float* w_out) {
+  __shared__ double s_total, s_last, s_wmax;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) scaled[i] = pow(prio[i], alpha);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double total = pairwise_sum(scaled, n);
+    s_total = total;
+    // probs = scaled / total; cdf = probs.cumsum(); cdf /= cdf[-1]
+    double acc = 0.0;
+    for (int i = 0; i < n; ++i) {
+      acc = (i == 0) ? scaled[0] / total : acc + scaled[i] / total;
+      cdf[i] = acc;
+    }
+    s_last = acc;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) cdf[i] = cdf[i] / s_last;
+  __syncthreads();
+  double wloc = 0.0;
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    const double u = uniforms[b];
+    int lo = 0, hi = n;  // first index with cdf > u (searchsorted side='right')
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (cdf[mid] <= u)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    idx_out[b] = lo;
+    const double p = scaled[lo] / s_total;
+    const double w = pow((double)n * p, -beta);
+    cdf[n + b] = w;
+    wloc = fmax(wloc, w);
+  }
+  // max over B weights
+  __shared__ double s_w[32];
+  for (int o = 16; o; o >>= 1) wloc = fmax(wloc, __shfl_xor_sync(kFull, wloc, o));
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = wloc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) m = fmax(m, s_w[k]);
+    s_wmax = m;
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < B; b += blockDim.x) w_out[b] = (float)(cdf[n + b] / s_wmax);
+}
+
+// priorities[idx] = |td| + 1e-6, duplicates: the last occurrence wins (agent.py:226)
+__global__ void per_update_kernel(double* prio, const int32_t* idx, const float* td, int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  for (int k = b + 1; k < B; ++k)
+    if (idx[k] == idx[b]) return;
+  prio[idx[b]] = fabs((double)td[b]) + 1e-6;
+}
+
+__global__ void gather_rows_kernel(const float* src, int64_t lds, const int32_t* idx, int B, int cols, float* dst,
+                                   int64_t ldd) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)B * cols;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(i / cols), c = (int)(i % cols);
+    dst[(int64_t)b * ldd + c] = src[(int64_t)idx[b] * lds + c];
+  }
+}
+
+int blocks_for(int64_t n, int t) { return (int)std::min<int64_t>((n + t - 1) / t, 148 * 32); }
+
+}  // namespace
+}  // namespace apb
+
+using namespace apb;
+
+extern "C" {
+
+int ap_dqn_dueling(const float* z, int64_t ldz, float* q, int64_t ldq, int32_t B, int32_t A, void* stream) {
+  if (!z || !q || B < 0 || A < 1) {
+    set_error("ap_dqn_dueling: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  if (B == 0) return AP_OK;
+  dueling_kernel<<<(B + 7) / 8, 256, 0, (cudaStream_t)stream>>>(z, ldz, q, ldq, B, A);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_dqn_act(const float* q, int64_t ldq, const uint8_t* mask, int64_t ldm, int32_t E, int32_t A, float epsilon,
+               uint64_t seed, int32_t* actions, void* stream) {
+  if (!q || !mask || !actions || E < 0 || A < 1) {
+    set_error("ap_dqn_act: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  if (E == 0) return AP_OK;
+  act_kernel<<<(E + 7) / 8, 256, 0, (cudaStream_t)stream>>>(q, ldq, mask, ldm, E, A, epsilon, seed, actions);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_dqn_td(const float* q, const float* online_next, const float* target_next, int64_t ldq, const int32_t* actions,
+              const float* rewards, const uint8_t* done, const uint8_t* next_mask, int64_t ldm, const float* weights,
+              int32_t B, int32_t A, float gamma, float huber_delta, float* dz, int64_t ldz, float* td, float* loss,
+              void* stream) {
+  if (!q || !online_next || !target_next || !actions || !rewards || !done || !next_mask || !weights || !dz || !td ||
+      !loss || B < 1 || A < 1) {
+    set_error("ap_dqn_td: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  td_kernel<<<(B + 7) / 8, 256, 0, (cudaStream_t)stream>>>(q, online_next, target_next, ldq, actions, rewards, done,
+                                                           next_mask, ldm, weights, B, A, gamma, huber_delta, dz, ldz,
+                                                           td, loss);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_dqn_relu_backward(float* dh, const float* h, int64_t n, void* stream) {
+  if (n <= 0) return AP_OK;
+  relu_bwd_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(dh, h, n);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_dqn_colsum(const float* x, int64_t ld, int32_t rows, int32_t cols, float* out, void* stream) {
+  if (cols <= 0) return AP_OK;
+  colsum_kernel<<<(cols + 127) / 128, 128, 0, (cudaStream_t)stream>>>(x, ld, rows, cols, out);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_dqn_adam(float* params, const float* grads, float* m, float* v, int64_t n, float lr, float beta1, float beta2,
+                float eps, float correct1, float correct2, void* stream) {
+  if (n <= 0) return AP_OK;
+  adam_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(params, grads, m, v, n, lr, beta1, beta2, eps,
+                                                                     correct1, correct2);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_per_sample(const double* priorities, int32_t n, double alpha, double beta, const double* uniforms, int32_t B,
+                  double* scratch, int32_t* indices, float* weights, void* stream) {
+  if (!priorities || !uniforms || !scratch || !indices || !weights || n < 1 || B < 1) {
+    set_error("ap_per_sample: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  // scratch: [n] scaled + [n + B] cdf / weights
+  per_sample_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(priorities, n, alpha, beta, uniforms, B, scratch,
+                                                         scratch + n, indices, weights);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_per_update(double* priorities, const int32_t* indices, const float* td, int32_t B, void* stream) {
+  if (B <= 0) return AP_OK;
+  per_update_kernel<<<(B + 127) / 128, 128, 0, (cudaStream_t)stream>>>(priorities, indices, td, B);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_gather_rows(const float* src, int64_t lds, const int32_t* idx, int32_t B, int32_t cols, float* dst,
+                   int64_t ldd, void* stream) {
+  if (B <= 0 || cols <= 0) return AP_OK;
+  gather_rows_kernel<<<blocks_for((int64_t)B * cols, 256), 256, 0, (cudaStream_t)stream>>>(src, lds, idx, B, cols, dst,
+                                                                                         ldd);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+}  // extern "C"
