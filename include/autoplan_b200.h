@@ -267,6 +267,36 @@ int ap_per_update(double* priorities, const int32_t* indices, const float* td, i
 int ap_gather_rows(const float* src, int64_t lds, const int32_t* idx, int32_t B, int32_t cols, float* dst,
                    int64_t ldd, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Vectorised episode driver (device-resident train_partition, cli.py:193-248)
+ * ------------------------------------------------------------------------- */
+
+/* seeds[e, position[e]] = P (action 0) or R (action 1) (envs.py:137-144). */
+int ap_vec_apply(int8_t* seeds, int64_t ld, const int32_t* position, const int32_t* actions, int32_t E, void* stream);
+
+/* After ap_propagate_batch over the E seed rows: rewards (0.4 newP + 0.1 newR
+ * or -1 on conflict), done flags, next decision positions (first undecided dim
+ * in `order`), next states [E, n+1], next masks, episode bookkeeping and
+ * auto-reset of finished envs (envs.py:103-177, 207-221). */
+int ap_vec_post(int32_t E, int32_t n, int64_t ld, int8_t* seeds, const int8_t* status, const uint8_t* outcome,
+                const int32_t* counts, int32_t* prev_counts, int32_t* position, const int32_t* order, float* cur_state,
+                int64_t lds, float* next_state, float* rewards, uint8_t* done, uint8_t* next_mask, int32_t A,
+                float* ep_return, float* finished_return, int32_t* finished_partitions, int32_t* episodes_done,
+                void* stream);
+
+/* E transitions into the device replay ring at slots (slot0 + e) % cap with
+ * the running max priority (agent.py:197-205). */
+int ap_per_push(int32_t E, int32_t S, int32_t A, int64_t slot0, int64_t cap, const float* states,
+                const float* next_states, int64_t lds, const int32_t* actions, const float* rewards,
+                const uint8_t* done, const uint8_t* masks, float* r_states, float* r_next, int32_t* r_actions,
+                float* r_rewards, uint8_t* r_done, uint8_t* r_masks, double* r_prio, const double* max_prio,
+                void* stream);
+
+/* Throughput-mode PER sample (parallel scan; not numpy-ordered) that also
+ * refreshes the running max priority.  cdf_scratch: n doubles. */
+int ap_per_sample_fast(const double* priorities, int32_t n, double alpha, double beta, const float* uniforms, int32_t B,
+                       double* cdf_scratch, int32_t* indices, float* weights, double* max_priority, void* stream);
+
 const char* ap_last_error(void);
 const char* ap_version(void);
 

@@ -1,0 +1,236 @@
+// Vectorised OPP / ADP episode driver on the device.
+//
+// E partition-search environments (reference PartitionSearchEnv,
+// envs.py:69-230) step in lockstep without host round trips:
+//   vec_apply   seeds[e, position[e]] = P or R from the chosen action
+//   (K1)        batched propagation of all E seed rows
+//   vec_post    reward 0.4*newP + 0.1*newR or -1 on conflict, done flags,
+//               next decision position (first undecided dim in the linkage
+//               order), next-state vectors, auto-reset of finished episodes
+//   per_push    transitions into the device replay ring at max priority
+// plus a throughput-mode PER sampler (parallel CTA scan; the parity sampler
+// in dqn.cu keeps numpy's sequential order).
+#include <cmath>
+
+#include "engine.h"
+
+namespace apb {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+__global__ void vec_apply_kernel(int8_t* seeds, int64_t ld, const int32_t* position, const int32_t* actions, int E) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  seeds[(int64_t)e * ld + position[e]] = actions[e] == 0 ? 1 : 0;  // ACTION_PARTITION -> P (envs.py:45-48,137-142)
+}
+
+// one warp per env
+__global__ void vec_post_kernel(int E, int n, int64_t ld, int8_t* seeds, const int8_t* status,
+                                const uint8_t* outcome, const int32_t* counts, int32_t* prev_counts, int32_t* position,
+                                const int32_t* order, float* cur_state, int64_t lds, float* next_state,
+                                float* rewards, uint8_t* done, uint8_t* next_mask, int A, float* ep_return,
+                                float* finished_return, int32_t* finished_partitions, int32_t* episodes_done) {
+  const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (e >= E) return;
+  const int8_t* st = status + (int64_t)e * ld;
+  float* cs = cur_state + (int64_t)e * lds;
+  float* ns = next_state + (int64_t)e * lds;
+  const int oc = outcome[e];
+  float reward;
+  bool fin;
+  if (oc == AP_OUTCOME_CONFLICT) {
+    reward = -1.0f;
+    fin = true;
+    for (int j = lane; j <= n; j += 32) ns[j] = cs[j];  // state unchanged (envs.py:147-149)
+  } else {
+    const int dP = counts[(int64_t)e * 4 + 0], dR = counts[(int64_t)e * 4 + 1];
+    reward = 0.4f * (float)(dP - prev_counts[2 * e]) + 0.1f * (float)(dR - prev_counts[2 * e + 1]);
+    fin = oc == AP_OUTCOME_COMPLETE;
+    // next position: first undecided dim in linkage order (envs.py:207-211)
+    int pos = -1;
+    for (int base = 0; base < n && pos < 0; base += 32) {
+      const int j = base + lane;
+      const bool und = j < n && st[order[j]] == -1;
+      const unsigned bal = __ballot_sync(kFull, und);
+      if (bal) pos = order[base + __ffs(bal) - 1];
+    }
+    for (int j = lane; j < n; j += 32) ns[j] = (float)st[j];
+    if (lane == 0) {
+      ns[n] = pos < 0 ? 1.0f : (float)pos / (float)n;
+      prev_counts[2 * e] = dP;
+      prev_counts[2 * e + 1] = dR;
+      position[e] = pos < 0 ? 0 : pos;
+    }
+    // keep the decided statuses as the env's new state
+    for (int j = lane; j <= n; j += 32) cs[j] = ns[j];
+    if (fin && lane == 0) finished_partitions[e] = dP;
+  }
+  if (lane == 0) {
+    rewards[e] = reward;
+    done[e] = fin ? 1 : 0;
+    ep_return[e] += reward;
+    if (fin) {
+      finished_return[e] = ep_return[e];
+      if (oc == AP_OUTCOME_CONFLICT) finished_partitions[e] = -1;
+      episodes_done[e] += 1;
+    }
+  }
+  for (int j = lane; j < A; j += 32) next_mask[(int64_t)e * A + j] = fin ? 0 : 1;
+  if (fin) {  // auto-reset for the next step (envs.py:103-108)
+    int8_t* sd = seeds + (int64_t)e * ld;
+    for (int j = lane; j < n; j += 32) {
+      sd[j] = -1;
+      cs[j] = -1.0f;
+    }
+    if (lane == 0) {
+      const int first = order[0];
+      cs[n] = (float)first / (float)n;
+      position[e] = first;
+      prev_counts[2 * e] = 0;
+      prev_counts[2 * e + 1] = 0;
+      ep_return[e] = 0.0f;
+    }
+  }
+}
+
+__global__ void per_push_kernel(int E, int S, int A, int64_t slot0, int64_t cap, const float* states,
+                                const float* next_states, int64_t lds, const int32_t* actions, const float* rewards,
+                                const uint8_t* done, const uint8_t* masks, float* r_states, float* r_next,
+                                int32_t* r_actions, float* r_rewards, uint8_t* r_done, uint8_t* r_masks,
+                                double* r_prio, const double* max_prio) {
+  const int e = blockIdx.x;
+  const int64_t slot = (slot0 + e) % cap;
+  for (int j = threadIdx.x; j < S; j += blockDim.x) {
+    r_states[slot * S + j] = states[(int64_t)e * lds + j];
+    r_next[slot * S + j] = next_states[(int64_t)e * lds + j];
+  }
+  for (int j = threadIdx.x; j < A; j += blockDim.x) r_masks[slot * A + j] = masks[(int64_t)e * A + j];
+  if (threadIdx.x == 0) {
+    r_actions[slot] = actions[e];
+    r_rewards[slot] = rewards[e];
+    r_done[slot] = done[e];
+    r_prio[slot] = *max_prio;
+  }
+}
+
+// throughput-mode PER sample: priorities**alpha, CTA-parallel scan, searchsorted,
+// IS weights; also refreshes the running max priority used by per_push
+__global__ void per_sample_fast_kernel(const double* prio, int n, double alpha, double beta, const float* uniforms,
+                                       int B, double* cdf, int32_t* idx_out, float* w_out, double* max_prio) {
+  __shared__ double part[1024];
+  __shared__ double pmax[1024];
+  const int t = threadIdx.x, T = blockDim.x;
+  const int per = (n + T - 1) / T;
+  const int lo = t * per, hi = min(n, lo + per);
+  double acc = 0.0, mx = 0.0;
+  for (int i = lo; i < hi; ++i) {
+    const double v = pow(prio[i], alpha);
+    acc += v;
+    cdf[i] = acc;
+    mx = fmax(mx, prio[i]);
+  }
+  part[t] = acc;
+  pmax[t] = mx;
+  __syncthreads();
+  if (t == 0) {
+    double run = 0.0, m = 0.0;
+    for (int k = 0; k < T; ++k) {
+      const double v = part[k];
+      part[k] = run;
+      run += v;
+      m = fmax(m, pmax[k]);
+    }
+    pmax[0] = run;
+    *max_prio = m;
+  }
+  __syncthreads();
+  const double total = pmax[0];
+  for (int i = lo; i < hi; ++i) cdf[i] += part[t];
+  __syncthreads();
+  for (int b = t; b < B; b += T) {
+    const double u = (double)uniforms[b] * total;
+    int l = 0, h = n;
+    while (l < h) {
+      const int mid = (l + h) >> 1;
+      if (cdf[mid] <= u)
+        l = mid + 1;
+      else
+        h = mid;
+    }
+    if (l >= n) l = n - 1;
+    idx_out[b] = l;
+    const double p = (cdf[l] - (l ? cdf[l - 1] : 0.0)) / total;
+    w_out[b] = (float)pow((double)n * p, -beta);
+  }
+  __syncthreads();
+  // normalise by the batch maximum
+  float wm = 0.0f;
+  for (int b = t; b < B; b += T) wm = fmaxf(wm, w_out[b]);
+  for (int o = 16; o; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(kFull, wm, o));
+  __shared__ float s_w[32];
+  if ((t & 31) == 0) s_w[t >> 5] = wm;
+  __syncthreads();
+  if (t == 0) {
+    float m = 0.0f;
+    for (int k = 0; k < (T >> 5); ++k) m = fmaxf(m, s_w[k]);
+    s_w[0] = m;
+  }
+  __syncthreads();
+  for (int b = t; b < B; b += T) w_out[b] /= s_w[0];
+}
+
+}  // namespace
+}  // namespace apb
+
+using namespace apb;
+
+extern "C" {
+
+int ap_vec_apply(int8_t* seeds, int64_t ld, const int32_t* position, const int32_t* actions, int32_t E, void* stream) {
+  if (E <= 0) return AP_OK;
+  vec_apply_kernel<<<(E + 255) / 256, 256, 0, (cudaStream_t)stream>>>(seeds, ld, position, actions, E);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_vec_post(int32_t E, int32_t n, int64_t ld, int8_t* seeds, const int8_t* status, const uint8_t* outcome,
+                const int32_t* counts, int32_t* prev_counts, int32_t* position, const int32_t* order, float* cur_state,
+                int64_t lds, float* next_state, float* rewards, uint8_t* done, uint8_t* next_mask, int32_t A,
+                float* ep_return, float* finished_return, int32_t* finished_partitions, int32_t* episodes_done,
+                void* stream) {
+  if (E <= 0) return AP_OK;
+  vec_post_kernel<<<(E + 7) / 8, 256, 0, (cudaStream_t)stream>>>(
+      E, n, ld, seeds, status, outcome, counts, prev_counts, position, order, cur_state, lds, next_state, rewards, done,
+      next_mask, A, ep_return, finished_return, finished_partitions, episodes_done);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_per_push(int32_t E, int32_t S, int32_t A, int64_t slot0, int64_t cap, const float* states,
+                const float* next_states, int64_t lds, const int32_t* actions, const float* rewards,
+                const uint8_t* done, const uint8_t* masks, float* r_states, float* r_next, int32_t* r_actions,
+                float* r_rewards, uint8_t* r_done, uint8_t* r_masks, double* r_prio, const double* max_prio,
+                void* stream) {
+  if (E <= 0) return AP_OK;
+  per_push_kernel<<<E, 128, 0, (cudaStream_t)stream>>>(E, S, A, slot0, cap, states, next_states, lds, actions, rewards,
+                                                       done, masks, r_states, r_next, r_actions, r_rewards, r_done,
+                                                       r_masks, r_prio, max_prio);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_per_sample_fast(const double* priorities, int32_t n, double alpha, double beta, const float* uniforms, int32_t B,
+                       double* cdf_scratch, int32_t* indices, float* weights, double* max_priority, void* stream) {
+  if (n < 1 || B < 1) {
+    set_error("ap_per_sample_fast: empty buffer or batch");
+    return AP_ERR_INVALID;
+  }
+  per_sample_fast_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(priorities, n, alpha, beta, uniforms, B, cdf_scratch,
+                                                               indices, weights, max_priority);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+}  // extern "C"

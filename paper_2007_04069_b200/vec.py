@@ -1,0 +1,228 @@
+"""Device-resident vectorised search: E partition envs + a DQN learner, no host sync.
+
+Throughput mode of the reference episode loop (`cli.py:193-248`): every
+vector step does, for all E environments at once,
+
+    act     Q over the E current states (tcgen05 GEMMs, M = E) + epsilon-greedy
+    step    seed the chosen dims, batched propagation (K1), rewards / done /
+            next positions / auto-reset (ap_vec_post)
+    observe E transitions into the device replay ring
+    learn   `learn_steps` double-DQN updates of batch `batch_size`
+
+so the learn : env-step ratio is learn_steps : E (stated in every report).
+Under torch.distributed each rank runs its own envs and learner replica;
+the Q-gradient is all-reduced over NCCL before every Adam step, so replicas
+stay identical (data-parallel DQN).  Parity with the reference's single
+learner is a 1-GPU, E = 1 property of `search.train_partition`; this driver
+is for throughput.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native
+from .agent import AdamOptimizer, AgentConfig, QNetwork, _Batch, epsilon_at, sync_target
+from .ir import decision_dims
+from .linkage import extract_linkage_groups, sorted_decision_order
+from .sharding import PropagationEngine, pad16
+
+
+def _s():
+    return _native.stream_handle()
+
+
+class VecPartitionEnv:
+    """E OPP (or ADP) environments stepping in lockstep on the device."""
+
+    def __init__(self, graph, E: int, task: str = "opp"):
+        import torch
+
+        if task == "opp":
+            dims = decision_dims(graph, graph.trainable_variables)
+            order = sorted_decision_order(extract_linkage_groups(graph, dims))
+        else:
+            from .envs import adp_candidates
+
+            dims = decision_dims(graph, [graph.instruction(i).name for i in adp_candidates(graph)])
+            order = list(dims)
+        self.dims = dims
+        self.E = E
+        self.n = n = len(dims)
+        self.state_dim = n + 1
+        self.num_actions = 2
+        self.engine = PropagationEngine(graph, dims)
+        self.engine.prepare()
+        idx = {d: k for k, d in enumerate(dims)}
+        self.order = torch.tensor([idx[d] for d in order], dtype=torch.int32, device="cuda")
+        ld = pad16(n)
+        dev = "cuda"
+        self.seeds_full = torch.full((E, ld), -1, dtype=torch.int8, device=dev)
+        self.seeds = self.seeds_full[:, :n]
+        self.status = torch.empty((E, ld), dtype=torch.int8, device=dev)
+        self.outcome = torch.empty(E, dtype=torch.uint8, device=dev)
+        self.counts = torch.empty((E, 4), dtype=torch.int32, device=dev)
+        self.prev_counts = torch.zeros((E, 2), dtype=torch.int32, device=dev)
+        first = int(self.order[0].item())
+        self.position = torch.full((E,), first, dtype=torch.int32, device=dev)
+        self.cur_state = torch.full((E, self.state_dim), -1.0, dtype=torch.float32, device=dev)
+        self.cur_state[:, n] = first / n
+        self.next_state = torch.empty_like(self.cur_state)
+        self.obs = torch.empty_like(self.cur_state)
+        self.rewards = torch.empty(E, dtype=torch.float32, device=dev)
+        self.done = torch.empty(E, dtype=torch.uint8, device=dev)
+        self.next_mask = torch.empty((E, 2), dtype=torch.uint8, device=dev)
+        self.mask = torch.ones((E, 2), dtype=torch.uint8, device=dev)
+        self.ep_return = torch.zeros(E, dtype=torch.float32, device=dev)
+        self.finished_return = torch.zeros(E, dtype=torch.float32, device=dev)
+        self.finished_partitions = torch.full((E,), -1, dtype=torch.int32, device=dev)
+        self.episodes_done = torch.zeros(E, dtype=torch.int32, device=dev)
+
+    def step(self, actions) -> None:
+        """Apply actions [E] int32 (device); fills rewards / done / next_state / next_mask."""
+        lib = _native.require_device()
+        P = _native.ptr
+        self.obs.copy_(self.cur_state)
+        _native.check(lib.ap_vec_apply(P(self.seeds_full), self.seeds_full.stride(0), P(self.position), P(actions),
+                                       self.E, _s()))
+        self.engine.launch(self.seeds, self.outcome, self.counts, None, self.status)
+        _native.check(lib.ap_vec_post(self.E, self.n, self.seeds_full.stride(0), P(self.seeds_full), P(self.status),
+                                      P(self.outcome), P(self.counts), P(self.prev_counts), P(self.position),
+                                      P(self.order), P(self.cur_state), self.cur_state.stride(0), P(self.next_state),
+                                      P(self.rewards), P(self.done), P(self.next_mask), 2, P(self.ep_return),
+                                      P(self.finished_return), P(self.finished_partitions), P(self.episodes_done),
+                                      _s()))
+
+
+class VecDqnTrainer:
+    """Batched acting + device replay + (data-parallel) DQN learner over a VecPartitionEnv."""
+
+    def __init__(self, env: VecPartitionEnv, config: AgentConfig, capacity: int, seed: int = 0,
+                 learn_steps: int = 1, process_group=None):
+        import torch
+
+        self.env = env
+        self.config = config
+        self.capacity = capacity
+        self.learn_steps = learn_steps
+        self.pg = process_group
+        rng = np.random.default_rng(seed)
+        self.net = QNetwork(env.state_dim, env.num_actions, config.hidden, rng)
+        if process_group is not None:  # identical replicas: broadcast rank 0's init
+            import torch.distributed as dist
+
+            dist.broadcast(self.net.flat, src=0, group=process_group)
+        self.target = self.net.clone()
+        self.opt = AdamOptimizer(self.net, config)
+        S, A, dev = env.state_dim, env.num_actions, "cuda"
+        self.ring = {
+            "states": torch.zeros((capacity, S), dtype=torch.float32, device=dev),
+            "next_states": torch.zeros((capacity, S), dtype=torch.float32, device=dev),
+            "actions": torch.zeros(capacity, dtype=torch.int32, device=dev),
+            "rewards": torch.zeros(capacity, dtype=torch.float32, device=dev),
+            "done": torch.zeros(capacity, dtype=torch.uint8, device=dev),
+            "next_mask": torch.zeros((capacity, A), dtype=torch.uint8, device=dev),
+            "priorities": torch.zeros(capacity, dtype=torch.float64, device=dev),
+            "cdf": torch.zeros(capacity, dtype=torch.float64, device=dev),
+        }
+        self.max_prio = torch.ones(1, dtype=torch.float64, device=dev)
+        self.size = 0
+        self.slot = 0
+        self.actions = torch.empty(env.E, dtype=torch.int32, device=dev)
+        self.batch = _Batch(config.batch_size, S, A)
+        self.idx = torch.empty(config.batch_size, dtype=torch.int32, device=dev)
+        self.weights = torch.empty(config.batch_size, dtype=torch.float32, device=dev)
+        self.uniforms = torch.empty(config.batch_size, dtype=torch.float32, device=dev)
+        self.gen = torch.Generator(device=dev)
+        self.gen.manual_seed(seed)
+        self.train_steps = 0
+        self.vector_steps = 0
+        self.launches = 0
+
+    # -- one vector step -------------------------------------------------------------
+
+    def act(self) -> None:
+        lib = _native.require_device()
+        env = self.env
+        q = self.net.forward_device(env.cur_state)
+        eps = epsilon_at(self.train_steps, self.config)
+        _native.check(lib.ap_dqn_act(_native.ptr(q), q.stride(0), _native.ptr(env.mask), env.mask.stride(0), env.E,
+                                     env.num_actions, float(eps), self.vector_steps + 1, _native.ptr(self.actions),
+                                     _s()))
+        self.launches += 4  # 3 GEMMs + act
+
+    def observe(self) -> None:
+        lib = _native.require_device()
+        env, r = self.env, self.ring
+        P = _native.ptr
+        _native.check(lib.ap_per_push(env.E, env.state_dim, env.num_actions, self.slot, self.capacity, P(env.obs),
+                                      P(env.next_state), env.obs.stride(0), P(self.actions), P(env.rewards),
+                                      P(env.done), P(env.next_mask), P(r["states"]), P(r["next_states"]),
+                                      P(r["actions"]), P(r["rewards"]), P(r["done"]), P(r["next_mask"]),
+                                      P(r["priorities"]), P(self.max_prio), _s()))
+        self.slot = (self.slot + env.E) % self.capacity
+        self.size = min(self.size + env.E, self.capacity)
+        self.launches += 1
+
+    def learn(self) -> None:
+        import torch
+
+        cfg, r, b = self.config, self.ring, self.batch
+        B = cfg.batch_size
+        if self.size < B:
+            return
+        lib = _native.require_device()
+        P = _native.ptr
+        torch.rand(B, generator=self.gen, device="cuda", out=self.uniforms)
+        _native.check(lib.ap_per_sample_fast(P(r["priorities"]), self.size, cfg.per_alpha, cfg.per_beta,
+                                             P(self.uniforms), B, P(r["cdf"]), P(self.idx), P(self.weights),
+                                             P(self.max_prio), _s()))
+        for src, dst in ((r["states"], b.states), (r["next_states"], b.next_states)):
+            _native.check(lib.ap_gather_rows(P(src), src.stride(0), P(self.idx), B, src.shape[1], P(dst),
+                                             dst.stride(0), _s()))
+        il = self.idx.long()
+        actions, rewards, done = r["actions"][il], r["rewards"][il], r["done"][il]
+        masks = r["next_mask"][il]
+        online_next = self.net.forward_device(b.next_states)
+        target_next = self.target.forward_device(b.next_states)
+        q_all, acts = self.net.forward_device(b.states, cache=True)
+        _native.check(lib.ap_dqn_td(P(q_all), P(online_next), P(target_next), q_all.stride(0), P(actions), P(rewards),
+                                    P(done), P(masks), masks.stride(0), P(self.weights), B, self.env.num_actions,
+                                    float(cfg.gamma), float(cfg.huber_delta), P(b.dz), b.dz.stride(0), P(b.td),
+                                    P(b.loss_rows), _s()))
+        self.net.backward_device(acts, b.dz)
+        if self.pg is not None:  # data-parallel learners: average the Q-gradient over NVLink
+            import torch.distributed as dist
+
+            dist.all_reduce(self.net.grad, op=dist.ReduceOp.AVG, group=self.pg)
+        self.opt.step()
+        _native.check(lib.ap_per_update(P(r["priorities"]), P(self.idx), P(b.td), B, _s()))
+        self.train_steps += 1
+        if self.train_steps % cfg.target_sync_every == 0:
+            sync_target(self.net, self.target)
+        self.launches += 2 + 2 + 9 + 1 + 9 + 1 + 1
+
+    def step(self) -> None:
+        self.act()
+        self.env.step(self.actions)
+        self.launches += 3
+        self.observe()
+        for _ in range(self.learn_steps):
+            self.learn()
+        self.vector_steps += 1
+
+    # -- reporting ---------------------------------------------------------------------
+
+    def best_plan(self):
+        """(partitions, return, env index) of the best finished episode seen on this rank."""
+        parts = self.env.finished_partitions
+        ret = self.env.finished_return
+        key = parts.double() * 1e6 + ret.double()
+        k = int(torch_argmax(key))
+        return int(parts[k].item()), float(ret[k].item()), k
+
+
+def torch_argmax(x):
+    import torch
+
+    return torch.argmax(x).item()
