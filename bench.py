@@ -47,6 +47,12 @@ def parse_args():
     p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--cpu-seconds", type=float, default=15.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-secondary", action="store_true", help="skip the DQN / PP-train / PP-infer figures")
+    p.add_argument("--dqn-envs", type=int, default=4096)
+    p.add_argument("--dqn-learn-steps", type=int, default=4)
+    p.add_argument("--dqn-steps", type=int, default=30)
+    p.add_argument("--pp-envs", type=int, default=64)
+    p.add_argument("--single-steps", type=int, default=300)
     return p.parse_args()
 
 
@@ -378,6 +384,15 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_single(g, dims, order, args.cpu_seconds)
 
+    secondary = {}
+    if not args.no_secondary:
+        want_cpu = rank == 0 and world == 1 and not args.no_cpu_baseline
+        secondary["dqn_env_steps_per_s"] = bench_dqn_vec(args, g, world, rank)
+        secondary["pp_train_candidates_per_s"] = bench_pp_train(args, world, want_cpu)
+        secondary["pp_infer_points_per_s"] = bench_pp_infer(args, world, want_cpu)
+        if rank == 0 and world == 1:
+            secondary["dqn_env_steps_per_s_single_env"] = bench_dqn_single(args, g, dims, groups, want_cpu)
+
     if world > 1:
         dist.destroy_process_group()
     if rank != 0:
@@ -428,8 +443,279 @@ def run_ours(args):
         },
         "gpu_launches": args.steps,
         "clocks": clock_info,
+        "secondary": secondary,
     }
     print(json.dumps(line), flush=True)
+
+
+# -- secondary metrics (DQN env-steps/s, PP-train and PP-infer plan evaluation) ----------
+
+
+def _max_over_ranks(x: float, world: int) -> float:
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def bench_dqn_vec(args, g, world, rank):
+    """Throughput-mode DQN: E envs per GPU, batched act / step / observe, L learn steps (batch 64) per vector step."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2007_04069_b200.agent import AgentConfig
+    from paper_2007_04069_b200.vec import VecDqnTrainer, VecPartitionEnv
+
+    E, L = args.dqn_envs, args.dqn_learn_steps
+    env = VecPartitionEnv(g, E)
+    cfg = AgentConfig(lr=0.0005, epsilon_decay_iters=2000)
+    pg = dist.group.WORLD if world > 1 else None
+    tr = VecDqnTrainer(env, cfg, capacity=max(4 * E, 4096), seed=rank, learn_steps=L, process_group=pg)
+    for _ in range(5):
+        tr.step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = tr.launches
+    s.record()
+    for _ in range(args.dqn_steps):
+        tr.step()
+    e.record()
+    torch.cuda.synchronize()
+    ms = _max_over_ranks(s.elapsed_time(e), world)
+    # tensor-pipe figure for the batched act forward (the dominant GEMMs)
+    x = env.cur_state
+    for _ in range(3):
+        tr.net.forward_device(x)
+    s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s2.record()
+    for _ in range(10):
+        tr.net.forward_device(x)
+    e2.record()
+    torch.cuda.synchronize()
+    fwd_s = s2.elapsed_time(e2) / 1e3 / 10
+    S, H = env.state_dim, cfg.hidden[0]
+    flops = 2.0 * E * (S * H + H * H + H * 3) * 3  # 3xTF32: three tensor-core passes
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    tf32_peak = peaks.get("bf16_tflops", 1590.0) / 2.0
+    return {
+        "value": world * E * args.dqn_steps / (ms / 1e3),
+        "unit": "env-steps/s",
+        "config": {"graph": "bert48", "task": "opp", "envs_per_gpu": E, "learn_steps_per_vector_step": L,
+                   "learn_batch": cfg.batch_size, "learn_to_env_step_ratio": f"{L}:{E}",
+                   "hidden": list(cfg.hidden), "state_dim": S, "replay_capacity": tr.capacity,
+                   "parallelism": f"data-parallel DQN x{world}, NCCL allreduce of Q-gradients" if world > 1 else "1 GPU",
+                   "vector_steps": args.dqn_steps},
+        "ms_per_vector_step": ms / args.dqn_steps,
+        "gpu_launches_per_vector_step": (tr.launches - launches0) / args.dqn_steps,
+        "act_forward_tensor": {"bound": "tensor", "achieved": flops / fwd_s / 1e12, "unit": "TFLOP/s",
+                               "peak": tf32_peak, "peak_source": "half of measured bf16 (dense TF32 = bf16/2)",
+                               "frac": flops / fwd_s / 1e12 / tf32_peak, "gemm_m": E,
+                               "note": "3 GEMMs M=E K=state_dim/256 N=256/3, 3xTF32"},
+    }
+
+
+def bench_pp_train(args, world, want_cpu):
+    """PP-train candidate plans/s: PipeTrainEnv._state over all allowed pivots of E random partial plans."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    from paper_2007_04069_b200 import _native
+    from paper_2007_04069_b200.envs import PipeTrainEnv
+    from paper_2007_04069_b200.topology import DeviceTopology
+
+    g, _ = workload_setup(args.workload)
+    topo = DeviceTopology(2, 4)
+    K = 4
+    env = PipeTrainEnv(g, topo, K, radius=3)
+    C = env.num_actions
+    E = args.pp_envs
+    rng = np.random.default_rng(7)
+    applied = np.full((E, K - 2), -1, dtype=np.int32)
+    mask = np.zeros((E, C), dtype=np.uint8)
+    for e in range(E):
+        k = int(rng.integers(0, K - 1))  # 0..K-2 picks so far
+        picks = np.sort(rng.choice(C - (K - 1), size=k, replace=False)) if k else np.zeros(0, int)
+        applied[e, :k] = picks
+        last = picks[-1] if k else -1
+        remaining = (K - 1) - k
+        mask[e, last + 1: C - remaining + 1] = 1
+    d_cand = torch.from_numpy(env._cand_pos).cuda()
+    d_app = torch.from_numpy(applied).cuda()
+    d_mask = torch.from_numpy(mask).cuda()
+    state = torch.empty((E, 4 * C), dtype=torch.float64, device="cuda")
+    lib = _native.require_device()
+    topo_c = _native.Topology.of(topo)
+
+    def run():
+        _native.check(lib.ap_pipe_train_state(env._model.handle, ctypes.byref(topo_c), _native.ptr(d_cand), C,
+                                              _native.ptr(d_app), K - 2, _native.ptr(d_mask), E, 2.0,
+                                              _native.ptr(state), _native.stream_handle()))
+
+    for _ in range(2):
+        run()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters = 5
+    s.record()
+    for _ in range(iters):
+        run()
+    e.record()
+    torch.cuda.synchronize()
+    ms = _max_over_ranks(s.elapsed_time(e), world)
+    evaluated = int(mask.sum())
+    out = {"value": world * evaluated * iters / (ms / 1e3), "unit": "candidate plans/s",
+           "config": {"graph": args.workload, "topology": "2x4", "stages": K, "radius": 3, "candidates": C,
+                      "env_states_per_launch": E, "allowed_candidates_per_launch": evaluated},
+           "ms_per_launch": ms / iters,
+           "bound": "fp64 add latency (N_f sequential adds per candidate)"}
+    if want_cpu:
+        out["cpu_baseline"] = cpu_pp_train(g, topo, K, env, applied, mask)
+    return out
+
+
+def cpu_pp_train(g, topo, K, env, applied, mask):
+    """The reference PipeTrainEnv._state (one core) on the first partial plan of the same batch."""
+    try:
+        rir, _ = _ref_import()
+        from autoplan.envs import PipeTrainEnv as RefEnv
+        from autoplan.topology import DeviceTopology as RefTopo
+    except ImportError:
+        return None
+    rg = rir.graph_from_dict(g.to_dict())
+    renv = RefEnv(rg, RefTopo(topo.num_servers, topo.gpus_per_server), K, radius=3)
+    renv.reset()
+    k = int((applied[0] >= 0).sum())
+    renv._applied = [int(x) for x in applied[0, :k]]
+    t0 = time.perf_counter()
+    renv._state()
+    dt = time.perf_counter() - t0
+    n = int(renv.action_mask().sum())
+    return {"value": n / dt, "unit": "candidate plans/s", "cores": 1, "kind": "reference",
+            "sample": f"one PipeTrainEnv._state call ({n} allowed candidates, {dt:.1f} s)"}
+
+
+def bench_pp_infer(args, world, want_cpu):
+    """PP-infer (boundaries, cuts) points/s: the exhaustive search over the full configC K=4 space."""
+    import torch
+
+    from paper_2007_04069_b200.dataproc import generate_environment
+    from paper_2007_04069_b200.envs import PipeInferEnv, brute_force_plan
+    from paper_2007_04069_b200.topology import PRESETS
+
+    arrays = generate_environment("uniform", 1280, 0)
+    env = PipeInferEnv(arrays, PRESETS["configc"], 4)
+    brute_force_plan(env)  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    bb, cc, length, points = brute_force_plan(env)
+    dt = _max_over_ranks(time.perf_counter() - t0, world)
+    out = {"value": world * points / dt, "unit": "points/s",
+           "config": {"profile": "generate_environment(uniform, 1280, 0)", "topology": "configc", "stages": 4,
+                      "points_per_search": points, "best": {"boundaries": bb, "cuts": cc, "length": length}},
+           "seconds_per_search": dt}
+    if want_cpu:
+        try:
+            _ref_import()
+            from autoplan.envs import PipeInferEnv as RefEnv
+            from autoplan.pipecost import PipelinePlan, pipeline_length
+            from autoplan.topology import PRESETS as RP
+
+            renv = RefEnv(arrays, RP["configc"], 4)
+            import itertools
+
+            combos = itertools.product(itertools.combinations(range(1, 128), 3), itertools.combinations(range(1, 32), 3))
+            n, t0 = 0, time.perf_counter()
+            for b, c in combos:
+                pipeline_length(PipelinePlan(b, c, 1), renv.decode_metrics(b), renv.topo_norm)
+                n += 1
+                if n % 256 == 0 and time.perf_counter() - t0 > 3.0:
+                    break
+            out["cpu_baseline"] = {"value": n / (time.perf_counter() - t0), "unit": "points/s", "cores": 1,
+                                   "kind": "reference", "sample": f"first {n} points of the same space"}
+        except ImportError:
+            pass
+    return out
+
+
+def bench_dqn_single(args, g, dims, groups, want_cpu):
+    """Reference-semantics loop (one env, act / step / observe / learn per step, batch 64) on BERT-48 OPP."""
+    import torch
+
+    from paper_2007_04069_b200.agent import AgentConfig, DqnAgent, Transition
+    from paper_2007_04069_b200.envs import OppEnv
+
+    env = OppEnv(g, groups=groups)
+    cfg = AgentConfig(lr=0.0005, epsilon_decay_iters=2000)
+    agent = DqnAgent(cfg, env.state_dim, env.num_actions, 0)
+
+    def run(steps):
+        done = 0
+        state = env.reset()
+        while done < steps:
+            if env.done:
+                state = env.reset()
+            a = agent.act(state, env.action_mask())
+            r = env.step(a)
+            agent.observe(Transition(state, a, r.reward, r.next_state, r.done, env.action_mask()))
+            agent.learn()
+            state = r.next_state
+            done += 1
+
+    run(80)  # fill past the first batch
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    run(args.single_steps)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    out = {"value": args.single_steps / dt, "unit": "env-steps/s",
+           "config": {"graph": args.workload, "task": "opp", "envs": 1, "learn_batch": 64,
+                      "learn_to_env_step_ratio": "1:1", "semantics": "reference train_partition loop"}}
+    if want_cpu:
+        out["cpu_baseline"] = cpu_dqn_single(g, dims, groups, args.cpu_seconds)
+    return out
+
+
+def cpu_dqn_single(g, dims, groups, seconds):
+    try:
+        rir, rsh = _ref_import()
+        from autoplan.agent import AgentConfig as RA
+        from autoplan.agent import DqnAgent as RD
+        from autoplan.agent import Transition as RT
+        from autoplan.envs import OppEnv as RO
+        from autoplan.linkage import LinkageGroup as RL
+    except ImportError:
+        return None
+    rg = rir.graph_from_dict(g.to_dict())
+    rdims = {(d.instruction_id, d.dim): rir.DimIndex(d.flat_index, d.instruction_id, d.dim) for d in dims}
+    rgroups = {}
+    for (d, st), grp in groups.items():  # same groups, as reference objects (skips its 18 s extraction)
+        key = (rdims[(d.instruction_id, d.dim)], rsh.DimStatus(int(st)))
+        rgroups[key] = RL(key, tuple((rdims[(x.instruction_id, x.dim)], rsh.DimStatus(int(s))) for x, s in grp.implied),
+                          grp.infeasible)
+    env = RO(rg, groups=rgroups)
+    agent = RD(RA(lr=0.0005, epsilon_decay_iters=2000), env.state_dim, env.num_actions, 0)
+    n, t0 = 0, time.perf_counter()
+    state = env.reset()
+    while time.perf_counter() - t0 < seconds:
+        if env.done:
+            state = env.reset()
+        a = agent.act(state, env.action_mask())
+        r = env.step(a)
+        agent.observe(RT(state, a, r.reward, r.next_state, r.done, env.action_mask()))
+        agent.learn()
+        state = r.next_state
+        n += 1
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "env-steps/s", "cores": 1, "kind": "reference",
+            "sample": f"{n} reference train_partition steps on BERT-48 OPP ({dt:.1f} s; includes the first, "
+                      f"learn-free steps)"}
 
 
 def main():

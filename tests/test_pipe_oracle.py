@@ -46,6 +46,15 @@ def test_oracle_stage_metrics_and_length(name):
             assert po.memory_feasible(m, cuts, M, topo, mem) == bool(d["metric_feas"][r])
 
 
+@pytest.mark.parametrize("dist,seed", [("uniform", 11), ("normal", 12), ("binomial", 13)])
+def test_dataproc_matches_reference_arrays(dist, seed):
+    from paper_2007_04069_b200.dataproc import generate_environment
+
+    d = load("infer", f"gen_{dist}_configa")
+    arr = generate_environment(dist, 1280, seed)
+    np.testing.assert_array_equal(np.concatenate([arr.c, arr.a, arr.w]), d["arrays"])
+
+
 @pytest.mark.parametrize("name", INFERS)
 def test_oracle_infer_lengths(name):
     d = load("infer", name)
