@@ -43,6 +43,25 @@ def test_gemm_3xtf32_matches_fp64(cuda, m, n, k, ta, tb):
     assert err < tol, (err, tol)
 
 
+@pytest.mark.parametrize("m,n,k", SHAPES + [(64, 1060, 256), (257, 33, 1060)])
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
+def test_pipelined_kernel_matches_simple_kernel(cuda, m, n, k, ta, tb, monkeypatch):
+    """cp.async / split-K kernel (gemm_tc2.cu) vs the simple kernel (gemm_tc.cu), both vs fp64."""
+    g = torch.Generator(device="cuda").manual_seed(m + n + k)
+    a = torch.randn((k, m) if ta else (m, k), device="cuda", generator=g)
+    b = torch.randn((n, k) if tb else (k, n), device="cuda", generator=g)
+    for prec in (1, 3):
+        fast = gemm(a, b, trans_a=ta, trans_b=tb, precision=prec)
+        monkeypatch.setenv("AP_GEMM_V1", "1")
+        slow = gemm(a, b, trans_a=ta, trans_b=tb, precision=prec)
+        monkeypatch.delenv("AP_GEMM_V1")
+        r = ref(a, b, ta, tb, None, False)
+        scale = r.abs().max().item()
+        tol = (1e-5 if prec == 3 else 5e-3) * scale
+        assert (fast.double() - r).abs().max().item() < tol
+        assert (slow.double() - r).abs().max().item() < tol
+
+
 @pytest.mark.parametrize("m,n,k", SHAPES[:4])
 def test_gemm_tf32_is_tf32_accurate(cuda, m, n, k):
     g = torch.Generator(device="cuda").manual_seed(1)
