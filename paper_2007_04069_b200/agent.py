@@ -107,6 +107,11 @@ class QNetwork:
             self.views[name] = self.flat[off: off + n].view(shape)
             self.grads[name] = self.grad[off: off + n].view(shape)
             off += n
+        # [out, in] copies of every weight: the forward GEMMs then read both
+        # operands K-major (the pipelined tcgen05 kernel); refreshed whenever
+        # the parameters change
+        self.wt = {name: torch.empty((s[1], s[0]), dtype=torch.float32, device="cuda")
+                   for name, s in shapes if len(s) == 2}
         if _init:
             rng = rng or np.random.default_rng(0)
             params = {}
@@ -152,6 +157,11 @@ class QNetwork:
         bh = np.concatenate([np.asarray(params["bv"]), np.asarray(params["ba"])])
         self.views["wh"].copy_(torch.from_numpy(wh))
         self.views["bh"].copy_(torch.from_numpy(bh))
+        self.refresh_transposed()
+
+    def refresh_transposed(self) -> None:
+        for name, t in self.wt.items():
+            t.copy_(self.views[name].t())
 
     # -- compute ----------------------------------------------------------------------
 
@@ -162,9 +172,9 @@ class QNetwork:
         acts = [x]
         h = x
         for i in range(len(self.hidden)):
-            h = gemm(h, self.views[f"w{i}"], bias=self.views[f"b{i}"], relu=True)
+            h = gemm(h, self.wt[f"w{i}"], trans_b=True, bias=self.views[f"b{i}"], relu=True)
             acts.append(h)
-        z = gemm(h, self.views["wh"], bias=self.views["bh"])
+        z = gemm(h, self.wt["wh"], trans_b=True, bias=self.views["bh"])
         b = x.shape[0]
         q = torch.empty((b, self.num_actions), dtype=torch.float32, device="cuda")
         lib = _native.require_device()
@@ -223,6 +233,7 @@ class QNetwork:
 
     def copy_from(self, other: "QNetwork") -> None:
         self.flat.copy_(other.flat)
+        self.refresh_transposed()
 
     def clone(self) -> "QNetwork":
         twin = QNetwork(self.state_dim, self.num_actions, self.hidden, _init=False)
@@ -392,6 +403,7 @@ class AdamOptimizer:
         _native.check(lib.ap_dqn_adam(_native.ptr(self.net.flat), _native.ptr(self.net.grad), _native.ptr(self.m),
                                       _native.ptr(self.v), self.net.flat.numel(), self.lr, self.beta1, self.beta2,
                                       self.eps, c1, c2, _stream()))
+        self.net.refresh_transposed()
 
 
 def huber(x: np.ndarray, delta: float) -> np.ndarray:

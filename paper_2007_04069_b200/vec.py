@@ -112,6 +112,7 @@ class VecDqnTrainer:
             import torch.distributed as dist
 
             dist.broadcast(self.net.flat, src=0, group=process_group)
+            self.net.refresh_transposed()
         self.target = self.net.clone()
         self.opt = AdamOptimizer(self.net, config)
         S, A, dev = env.state_dim, env.num_actions, "cuda"
