@@ -292,10 +292,15 @@ int ap_per_push(int32_t E, int32_t S, int32_t A, int64_t slot0, int64_t cap, con
                 float* r_rewards, uint8_t* r_done, uint8_t* r_masks, double* r_prio, const double* max_prio,
                 void* stream);
 
-/* Throughput-mode PER sample (parallel scan; not numpy-ordered) that also
- * refreshes the running max priority.  cdf_scratch: n doubles. */
-int ap_per_sample_fast(const double* priorities, int32_t n, double alpha, double beta, const float* uniforms, int32_t B,
-                       double* cdf_scratch, int32_t* indices, float* weights, double* max_priority, void* stream);
+/* Throughput-mode PER sample (parallel scan; not numpy-ordered) over
+ * priorities already raised to alpha; also refreshes the running max (in the
+ * same scaled domain) that ap_per_push assigns.  cdf_scratch: n doubles. */
+int ap_per_sample_fast(const double* scaled_priorities, int32_t n, double alpha, double beta, const float* uniforms,
+                       int32_t B, double* cdf_scratch, int32_t* indices, float* weights, double* max_priority,
+                       void* stream);
+/* scaled[idx] = (|td| + 1e-6)**alpha, last duplicate wins (throughput mode). */
+int ap_per_update_scaled(double* scaled, const int32_t* indices, const float* td, int32_t B, double alpha,
+                         void* stream);
 
 const char* ap_last_error(void);
 const char* ap_version(void);

@@ -128,6 +128,7 @@ SIGNATURES: dict[str, tuple] = {
     "ap_per_push": (ctypes.c_int, [_I32, _I32, _I32, _I64, _I64, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
                                    _VP, _VP, _VP, _VP, _VP]),
     "ap_per_sample_fast": (ctypes.c_int, [_VP, _I32, _F64, _F64, _VP, _I32, _VP, _VP, _VP, _VP, _VP]),
+    "ap_per_update_scaled": (ctypes.c_int, [_VP, _VP, _VP, _I32, _F64, _VP]),
     "ap_last_error": (ctypes.c_char_p, []),
     "ap_version": (ctypes.c_char_p, []),
 }

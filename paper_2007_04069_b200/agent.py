@@ -195,13 +195,15 @@ class QNetwork:
         lib = _native.require_device()
         h = acts[-1]
         b = dz.shape[0]
-        gemm(h, dz, trans_a=True, out=self.grads["wh"])
+        # weight gradients as K-major GEMMs (contraction over the batch):
+        # dW = h^T dz  ->  A = h^T [in, B], B-operand = dz^T [out, B]
+        gemm(h.t().contiguous(), dz.t().contiguous(), trans_b=True, out=self.grads["wh"])
         _native.check(lib.ap_dqn_colsum(_native.ptr(dz), dz.stride(0), b, dz.shape[1], _native.ptr(self.grads["bh"]),
                                         _stream()))
         dh = gemm(dz, self.views["wh"], trans_b=True)
         for i in range(len(self.hidden) - 1, -1, -1):
             _native.check(lib.ap_dqn_relu_backward(_native.ptr(dh), _native.ptr(acts[i + 1]), dh.numel(), _stream()))
-            gemm(acts[i], dh, trans_a=True, out=self.grads[f"w{i}"])
+            gemm(acts[i].t().contiguous(), dh.t().contiguous(), trans_b=True, out=self.grads[f"w{i}"])
             _native.check(lib.ap_dqn_colsum(_native.ptr(dh), dh.stride(0), b, dh.shape[1],
                                             _native.ptr(self.grads[f"b{i}"]), _stream()))
             if i > 0:

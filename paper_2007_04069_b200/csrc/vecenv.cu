@@ -125,11 +125,12 @@ __global__ void per_sample_fast_kernel(const double* prio, int n, double alpha, 
   const int per = (n + T - 1) / T;
   const int lo = t * per, hi = min(n, lo + per);
   double acc = 0.0, mx = 0.0;
+  (void)alpha;  // `prio` already holds priority**alpha (kept scaled by ap_per_update_scaled)
   for (int i = lo; i < hi; ++i) {
-    const double v = pow(prio[i], alpha);
+    const double v = prio[i];
     acc += v;
     cdf[i] = acc;
-    mx = fmax(mx, prio[i]);
+    mx = fmax(mx, v);
   }
   part[t] = acc;
   pmax[t] = mx;
@@ -181,6 +182,15 @@ __global__ void per_sample_fast_kernel(const double* prio, int n, double alpha, 
   for (int b = t; b < B; b += T) w_out[b] /= s_w[0];
 }
 
+// scaled[idx] = (|td| + 1e-6)**alpha, last duplicate wins
+__global__ void per_update_scaled_kernel(double* scaled, const int32_t* idx, const float* td, int B, double alpha) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  for (int k = b + 1; k < B; ++k)
+    if (idx[k] == idx[b]) return;
+  scaled[idx[b]] = pow(fabs((double)td[b]) + 1e-6, alpha);
+}
+
 }  // namespace
 }  // namespace apb
 
@@ -229,6 +239,14 @@ int ap_per_sample_fast(const double* priorities, int32_t n, double alpha, double
   }
   per_sample_fast_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(priorities, n, alpha, beta, uniforms, B, cdf_scratch,
                                                                indices, weights, max_priority);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_per_update_scaled(double* scaled, const int32_t* indices, const float* td, int32_t B, double alpha,
+                         void* stream) {
+  if (B <= 0) return AP_OK;
+  per_update_scaled_kernel<<<(B + 127) / 128, 128, 0, (cudaStream_t)stream>>>(scaled, indices, td, B, alpha);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }

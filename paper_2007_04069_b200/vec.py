@@ -197,7 +197,8 @@ class VecDqnTrainer:
 
             dist.all_reduce(self.net.grad, op=dist.ReduceOp.AVG, group=self.pg)
         self.opt.step()
-        _native.check(lib.ap_per_update(P(r["priorities"]), P(self.idx), P(b.td), B, _s()))
+        _native.check(lib.ap_per_update_scaled(P(r["priorities"]), P(self.idx), P(b.td), B, float(cfg.per_alpha),
+                                               _s()))
         self.train_steps += 1
         if self.train_steps % cfg.target_sync_every == 0:
             sync_target(self.net, self.target)
