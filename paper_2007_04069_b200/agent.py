@@ -89,6 +89,7 @@ class QNetwork:
         self.state_dim = state_dim
         self.num_actions = num_actions
         self.hidden = tuple(hidden)
+        self.precision = 3  # 3xTF32 (fp32-accurate); the throughput trainer may set 1 (TF32)
         shapes = []
         fan_in = state_dim
         for i, width in enumerate(self.hidden):
@@ -172,9 +173,9 @@ class QNetwork:
         acts = [x]
         h = x
         for i in range(len(self.hidden)):
-            h = gemm(h, self.wt[f"w{i}"], trans_b=True, bias=self.views[f"b{i}"], relu=True)
+            h = gemm(h, self.wt[f"w{i}"], trans_b=True, bias=self.views[f"b{i}"], relu=True, precision=self.precision)
             acts.append(h)
-        z = gemm(h, self.wt["wh"], trans_b=True, bias=self.views["bh"])
+        z = gemm(h, self.wt["wh"], trans_b=True, bias=self.views["bh"], precision=self.precision)
         b = x.shape[0]
         q = torch.empty((b, self.num_actions), dtype=torch.float32, device="cuda")
         lib = _native.require_device()
@@ -197,17 +198,18 @@ class QNetwork:
         b = dz.shape[0]
         # weight gradients as K-major GEMMs (contraction over the batch):
         # dW = h^T dz  ->  A = h^T [in, B], B-operand = dz^T [out, B]
-        gemm(h.t().contiguous(), dz.t().contiguous(), trans_b=True, out=self.grads["wh"])
+        gemm(h.t().contiguous(), dz.t().contiguous(), trans_b=True, out=self.grads["wh"], precision=self.precision)
         _native.check(lib.ap_dqn_colsum(_native.ptr(dz), dz.stride(0), b, dz.shape[1], _native.ptr(self.grads["bh"]),
                                         _stream()))
-        dh = gemm(dz, self.views["wh"], trans_b=True)
+        dh = gemm(dz, self.views["wh"], trans_b=True, precision=self.precision)
         for i in range(len(self.hidden) - 1, -1, -1):
             _native.check(lib.ap_dqn_relu_backward(_native.ptr(dh), _native.ptr(acts[i + 1]), dh.numel(), _stream()))
-            gemm(acts[i].t().contiguous(), dh.t().contiguous(), trans_b=True, out=self.grads[f"w{i}"])
+            gemm(acts[i].t().contiguous(), dh.t().contiguous(), trans_b=True, out=self.grads[f"w{i}"],
+                 precision=self.precision)
             _native.check(lib.ap_dqn_colsum(_native.ptr(dh), dh.stride(0), b, dh.shape[1],
                                             _native.ptr(self.grads[f"b{i}"]), _stream()))
             if i > 0:
-                dh = gemm(dh, self.views[f"w{i}"], trans_b=True)
+                dh = gemm(dh, self.views[f"w{i}"], trans_b=True, precision=self.precision)
 
     def forward_cached(self, states):
         import torch
@@ -239,6 +241,7 @@ class QNetwork:
 
     def clone(self) -> "QNetwork":
         twin = QNetwork(self.state_dim, self.num_actions, self.hidden, _init=False)
+        twin.precision = self.precision
         twin.copy_from(self)
         return twin
 

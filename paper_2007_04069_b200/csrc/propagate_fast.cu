@@ -234,13 +234,20 @@ __device__ __forceinline__ void local_table(uint32_t c03, uint32_t c47, uint32_t
   }
 }
 
-// PRMT reads only selector bits [15:0], so the high half-word needs no mask.
+// raw PRMT: the selectors are stored with clear mode bits, so skip the
+// 0x7777 masking __byte_perm adds; PRMT reads only selector bits [15:0]
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(s));
+  return d;
+}
+
 __device__ __forceinline__ uint4 select16(uint32_t lo, uint32_t hi, uint32_t z, uint32_t w) {
   uint4 o;
-  o.x = __byte_perm(lo, hi, z);
-  o.y = __byte_perm(lo, hi, z >> 16);
-  o.z = __byte_perm(lo, hi, w);
-  o.w = __byte_perm(lo, hi, w >> 16);
+  o.x = prmt(lo, hi, z);
+  o.y = prmt(lo, hi, z >> 16);
+  o.z = prmt(lo, hi, w);
+  o.w = prmt(lo, hi, w >> 16);
   return o;
 }
 
@@ -250,13 +257,13 @@ __device__ __forceinline__ uint32_t local_table4(uint32_t c03, uint32_t tb) {
   const uint32_t s1 = lds_u8(TBL_ADDR(c03, tb, 1));
   const uint32_t s2 = lds_u8(TBL_ADDR(c03, tb, 2));
   const uint32_t s3 = lds_u8(TBL_ADDR(c03, tb, 3));
-  return __byte_perm(__byte_perm(s0, s1, 0x0040), __byte_perm(s2, s3, 0x0040), 0x5410);
+  return prmt(prmt(s0, s1, 0x0040), prmt(s2, s3, 0x0040), 0x5410);
 }
 
 // Squeeze bits {8b + i : b, i < 4} into bits {4b + i}: one shift-or and one PRMT.
 __device__ __forceinline__ uint32_t squeeze(uint32_t x) {
   const uint32_t y = x | (x >> 4);
-  return __byte_perm(y, 0u, 0x4420);
+  return prmt(y, 0u, 0x4420);
 }
 
 // P / R / U position masks of one 16-byte seed chunk (bit 4*b + i for word i, byte b)
@@ -275,7 +282,8 @@ __device__ __forceinline__ void seed_masks(uint4 s, uint32_t* xp, uint32_t* xr, 
   *xu = squeeze(u);
 }
 
-template <int MAXCH>
+// MAXCH: 16-byte seed chunks per lane; NW: 32-bit class words (classes <= 32*NW)
+template <int MAXCH, int NW>
 __global__ void __launch_bounds__(kThreadsF) propagate_fast_kernel(FastParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
   // stage the static tables
@@ -303,9 +311,9 @@ __global__ void __launch_bounds__(kThreadsF) propagate_fast_kernel(FastParams p)
   const uint8_t* dec_cls8 = smem + p.off_dec_cls8;
   const uint16_t* ncand = reinterpret_cast<const uint16_t*>(smem + p.off_ncand);
   const uint4* imp_bits = reinterpret_cast<const uint4*>(smem + p.off_imp_bits);
-  uint32_t forced_bits[8];
+  uint32_t forced_bits[NW];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) forced_bits[k] = p.forced_bits[k];
+  for (int k = 0; k < NW; ++k) forced_bits[k] = p.forced_bits[k];
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -394,50 +402,52 @@ __global__ void __launch_bounds__(kThreadsF) propagate_fast_kernel(FastParams p)
     }
 
     // 2. class bitsets: word k holds classes 32k..32k+31 (flags beyond C stay 0)
-    uint32_t Pw[8], Rw[8], acc[8];
+    uint32_t Pw[NW], Rw[NW], acc[NW];
+    uint32_t myP = 0;  // bit k: this lane's class 32k+lane is partitioned
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < NW; ++k) {
       acc[k] = 0;
-      if (32 * k < p.C) {
-        Pw[k] = __ballot_sync(kFullMask, flagP[32 * k + lane] != 0);
-        Rw[k] = __ballot_sync(kFullMask, flagR[32 * k + lane] != 0) | forced_bits[k];
-      } else {
-        Pw[k] = Rw[k] = 0;
-      }
+      Pw[k] = __ballot_sync(kFullMask, flagP[32 * k + lane] != 0);
+      Rw[k] = __ballot_sync(kFullMask, flagR[32 * k + lane] != 0) | forced_bits[k];
+      myP |= ((Pw[k] >> lane) & 1u) << k;
     }
-    // 3. implications: each lane ORs the 256-bit rows of its own partitioned
-    //    classes, then one warp OR-reduction per word
+    // 3. implications: each lane ORs the rows of its own partitioned classes
+    //    (rows are 8 words apart, only the first NW matter), then one warp
+    //    OR-reduction per word
+    while (myP) {
+      const int k = __ffs(myP) - 1;
+      myP &= myP - 1;
+      const uint32_t* row = reinterpret_cast<const uint32_t*>(imp_bits + 2 * (32 * k + lane));
+      if (NW <= 4) {
+        const uint4 a = *reinterpret_cast<const uint4*>(row);
+        const uint32_t aw[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      if ((Pw[k] >> lane) & 1u) {
-        const uint4* row = imp_bits + 2 * (32 * k + lane);
-        const uint4 a = row[0], c = row[1];
-        acc[0] |= a.x; acc[1] |= a.y; acc[2] |= a.z; acc[3] |= a.w;
-        acc[4] |= c.x; acc[5] |= c.y; acc[6] |= c.z; acc[7] |= c.w;
+        for (int w = 0; w < NW; ++w) acc[w] |= aw[w];
+      } else {
+        const uint4 a = *reinterpret_cast<const uint4*>(row), c = *reinterpret_cast<const uint4*>(row + 4);
+        const uint32_t aw[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+#pragma unroll
+        for (int w = 0; w < NW; ++w) acc[w] |= aw[w];
       }
     }
     uint32_t clash = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      if (32 * k < p.C) {
-        Rw[k] |= __reduce_or_sync(kFullMask, acc[k]);
-        clash |= Pw[k] & Rw[k];
-      }
+    for (int k = 0; k < NW; ++k) {
+      Rw[k] |= __reduce_or_sync(kFullMask, acc[k]);
+      clash |= Pw[k] & Rw[k];
     }
     bool conflict = clash != 0;  // warp-uniform
 
     // 4. class status table and decided counts (lane-owned classes)
     uint32_t dPR = 0;  // decided P | decided R << 16
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      if (32 * k < p.C) {
-        const int c = 32 * k + lane;
-        const bool isP = (Pw[k] >> lane) & 1u;
-        const bool isR = (Rw[k] >> lane) & 1u;
-        table[c] = isP ? 1 : (isR ? 0 : -1);
-        const uint32_t nc = ncand[c];
-        dPR += isP ? nc : (isR ? (nc << 16) : 0u);
-      }
+    for (int k = 0; k < NW; ++k) {
+      const int c = 32 * k + lane;
+      const bool isP = (Pw[k] >> lane) & 1u;
+      const bool isR = (Rw[k] >> lane) & 1u;
+      table[c] = isP ? 1 : (isR ? 0 : -1);
+      const uint32_t nc = ncand[c];
+      dPR += isP ? nc : (isR ? (nc << 16) : 0u);
     }
     dPR = __reduce_add_sync(kFullMask, dPR);
     uint32_t sPR = __reduce_add_sync(kFullMask, (uint32_t)nPs | ((uint32_t)nRs << 16));
@@ -528,10 +538,10 @@ __global__ void __launch_bounds__(kThreadsF) propagate_fast_kernel(FastParams p)
   }
 }
 
-template <int MAXCH>
+template <int MAXCH, int NW>
 int launch_fast_t(const FastParams& p, int64_t smem, cudaStream_t stream) {
   static int num_sms = -1;
-  auto kern = propagate_fast_kernel<MAXCH>;
+  auto kern = propagate_fast_kernel<MAXCH, NW>;
   AP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (num_sms < 0) {
     int dev = 0;
@@ -549,6 +559,20 @@ int launch_fast_t(const FastParams& p, int64_t smem, cudaStream_t stream) {
 }
 
 inline int64_t a16(int64_t x) { return (x + 15) & ~int64_t(15); }
+
+template <int MAXCH>
+int dispatch_nw(int nw, const FastParams& p, int64_t smem, cudaStream_t stream) {
+  switch (nw <= 1 ? 1 : nw) {
+    case 1: return launch_fast_t<MAXCH, 1>(p, smem, stream);
+    case 2: return launch_fast_t<MAXCH, 2>(p, smem, stream);
+    case 3: return launch_fast_t<MAXCH, 3>(p, smem, stream);
+    case 4: return launch_fast_t<MAXCH, 4>(p, smem, stream);
+    case 5: return launch_fast_t<MAXCH, 5>(p, smem, stream);
+    case 6: return launch_fast_t<MAXCH, 6>(p, smem, stream);
+    case 7: return launch_fast_t<MAXCH, 7>(p, smem, stream);
+    default: return launch_fast_t<MAXCH, 8>(p, smem, stream);
+  }
+}
 
 }  // namespace
 
@@ -607,11 +631,12 @@ int launch_propagate_fast(const GraphTables* g, const DecisionTables* d, const i
   const int64_t smem = off + 256 + (int64_t)kWarpsF * kScratchPerWarp;
   if (smem > 200 * 1024) return AP_ERR_UNSUPPORTED;
   const int chunks = (nq_d + 31) / 32;
-  if (chunks <= 1) return launch_fast_t<1>(p, smem, stream);
-  if (chunks <= 2) return launch_fast_t<2>(p, smem, stream);
-  if (chunks <= 3) return launch_fast_t<3>(p, smem, stream);
-  if (chunks <= 4) return launch_fast_t<4>(p, smem, stream);
-  if (chunks <= 8) return launch_fast_t<8>(p, smem, stream);
+  const int nw = (p.C + 31) / 32;
+  if (chunks <= 1) return dispatch_nw<1>(nw, p, smem, stream);
+  if (chunks <= 2) return dispatch_nw<2>(nw, p, smem, stream);
+  if (chunks <= 3) return dispatch_nw<3>(nw, p, smem, stream);
+  if (chunks <= 4) return dispatch_nw<4>(nw, p, smem, stream);
+  if (chunks <= 8) return dispatch_nw<8>(nw, p, smem, stream);
   return AP_ERR_UNSUPPORTED;
 }
 

@@ -98,7 +98,7 @@ class VecDqnTrainer:
     """Batched acting + device replay + (data-parallel) DQN learner over a VecPartitionEnv."""
 
     def __init__(self, env: VecPartitionEnv, config: AgentConfig, capacity: int, seed: int = 0,
-                 learn_steps: int = 1, process_group=None):
+                 learn_steps: int = 1, process_group=None, precision: int = 1):
         import torch
 
         self.env = env
@@ -108,6 +108,7 @@ class VecDqnTrainer:
         self.pg = process_group
         rng = np.random.default_rng(seed)
         self.net = QNetwork(env.state_dim, env.num_actions, config.hidden, rng)
+        self.net.precision = precision  # TF32 tensor cores by default in throughput mode
         if process_group is not None:  # identical replicas: broadcast rank 0's init
             import torch.distributed as dist
 
