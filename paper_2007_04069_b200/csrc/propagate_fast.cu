@@ -502,13 +502,16 @@ __global__ void __launch_bounds__(kThreadsF) propagate_fast_kernel(FastParams p)
     if (p.slots_out) {
       int8_t* orow = p.slots_out + b * p.slots_stride + 32 * lane;
       const uint4* dq = slot_desc + 2 * lane;
-      if (p.slot_all_k4) {
-        // common case (BERT-48): branch-free, four lookups per 32 slots
+      if (!p.any_slot_fallback) {
+        // common case: four lookups per 32 slots; the rare 5..8-class chunk
+        // takes a short divergent detour for its second status word
         for (int q = lane; q < p.nq_s; q += 32, dq += 64, orow += 1024) {
           const uint4 d0 = dq[0], d1 = dq[1];
           const uint32_t lo = local_table4(d0.x, tb);
-          stg_stream(orow, select16(lo, lo, d0.z, d0.w));
-          stg_stream(orow + 16, select16(lo, lo, d1.x, d1.y));
+          uint32_t hi = lo;
+          if (d0.y != 0xFFFFFFFFu) hi = local_table4(d0.y, tb);
+          stg_stream(orow, select16(lo, hi, d0.z, d0.w));
+          stg_stream(orow + 16, select16(lo, hi, d1.x, d1.y));
         }
       } else {
         for (int q = lane; q < p.nq_s; q += 32, dq += 64, orow += 1024) {
