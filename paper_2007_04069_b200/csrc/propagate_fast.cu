@@ -41,11 +41,11 @@ constexpr int kScratchPerWarp = 768;  // flagP[256] flagR[256] table[256]
 // 16-bit position mask bit of chunk position t = 4*i + b (word i, byte b)
 inline int perm_bit(int t) { return 4 * (t & 3) + (t >> 2); }
 
-// Local classes of one `width`-wide chunk, first-appearance order.  Returns
-// false when the chunk has more than 8 distinct classes.
-bool local_classes(const int32_t* cls, int count, std::vector<int>* uniq, int* local, int width = 16) {
+// Local classes of one 16-wide chunk, first-appearance order.  Returns false
+// when the chunk has more than 8 distinct classes.
+bool local_classes(const int32_t* cls, int count, std::vector<int>* uniq, int local[16]) {
   uniq->clear();
-  for (int t = 0; t < width; ++t) {
+  for (int t = 0; t < 16; ++t) {
     const int c = t < count ? cls[t] : cls[0];
     auto it = std::find(uniq->begin(), uniq->end(), c);
     if (it == uniq->end()) {
@@ -82,30 +82,32 @@ void pack_selectors(const int local[16], uint32_t* z, uint32_t* w) {
 void build_fast_graph(GraphTables* g) {
   g->fast = g->num_classes <= kMaxFastClasses;
   if (!g->fast) return;
-  // 32-slot chunks: 8-word descriptor = classes 0-3, classes 4-7 (or the
-  // four-class marker), 8 PRMT selectors (two 16-bit halves per word), pad
   const int64_t S = g->num_slots;
-  const int64_t nq = (S + 31) / 32;
-  g->slot_desc.assign(nq * 8, 0);
-  g->slot_cls8.assign(nq * 32, 0xFF);
+  const int64_t nq = (S + 15) / 16;
+  g->slot_desc.assign(nq * 4, 0);
+  g->slot_cls8.assign(nq * 16, 0xFF);
   std::vector<int> uniq;
-  int local[32];
+  int local[16];
+  for (int64_t q = 0; q < nq; ++q) {
+    const int count = (int)std::min<int64_t>(16, S - 16 * q);
+    for (int t = 0; t < count; ++t) g->slot_cls8[16 * q + t] = (uint8_t)g->class_of_slot[16 * q + t];
+    uint32_t* d = &g->slot_desc[4 * q];
+    if (!local_classes(&g->class_of_slot[16 * q], count, &uniq, local)) {
+      d[0] = 0xFFFFFFFFu;  // fallback: per-slot lookups through slot_cls8
+      continue;
+    }
+    pack_classes(uniq, &d[0], &d[1]);
+    pack_selectors(local, &d[2], &d[3]);
+  }
   g->slot_fallback_chunks = 0;
   g->slot_all_k4 = true;
   for (int64_t q = 0; q < nq; ++q) {
-    const int count = (int)std::min<int64_t>(32, S - 32 * q);
-    for (int t = 0; t < count; ++t) g->slot_cls8[32 * q + t] = (uint8_t)g->class_of_slot[32 * q + t];
-    uint32_t* d = &g->slot_desc[8 * q];
-    if (!local_classes(&g->class_of_slot[32 * q], count, &uniq, local, 32)) {
-      d[0] = 0xFFFFFFFFu;  // fallback: per-slot lookups through slot_cls8
+    if ((g->slot_desc[4 * q] & 0xFF) == 0xFF) {
       g->slot_fallback_chunks++;
       g->slot_all_k4 = false;
-      continue;
+    } else if (g->slot_desc[4 * q + 1] != 0xFFFFFFFFu) {
+      g->slot_all_k4 = false;
     }
-    if (uniq.size() > 4) g->slot_all_k4 = false;
-    pack_classes(uniq, &d[0], &d[1]);
-    pack_selectors(local, &d[2], &d[3]);
-    pack_selectors(local + 16, &d[4], &d[5]);
   }
   const int C = g->num_classes;
   g->imp_bits.assign((size_t)std::max(C, 1) * 8, 0);
@@ -293,8 +295,8 @@ __global__ void __launch_bounds__(kThreadsF) propagate_fast_kernel(FastParams p)
     const uint8_t* sb = reinterpret_cast<const uint8_t*>(src);
     for (int64_t i = n16 * 16 + threadIdx.x; i < bytes; i += blockDim.x) smem[off + i] = sb[i];
   };
-  stage(p.off_slot_desc, p.slot_desc, (int64_t)p.nq_s * 32);
-  if (p.any_slot_fallback) stage(p.off_slot_cls8, p.slot_cls8, (int64_t)p.nq_s * 32);
+  stage(p.off_slot_desc, p.slot_desc, (int64_t)p.nq_s * 16);
+  if (p.any_slot_fallback) stage(p.off_slot_cls8, p.slot_cls8, (int64_t)p.nq_s * 16);
   stage(p.off_dec_desc, p.dec_desc, (int64_t)p.nq_d * 32);
   stage(p.off_dec_masks, p.dec_masks, (int64_t)p.nq_d * 4);
   stage(p.off_dec_cls8, p.dec_cls8, (int64_t)p.nq_d * 16);
@@ -498,37 +500,31 @@ __global__ void __launch_bounds__(kThreadsF) propagate_fast_kernel(FastParams p)
       }
     }
 
-    // 5. all slot statuses, 32 per lane-iteration (two 16-byte stores)
-    if (p.slots_out) {
-      int8_t* orow = p.slots_out + b * p.slots_stride + 32 * lane;
-      const uint4* dq = slot_desc + 2 * lane;
-      if (!p.any_slot_fallback) {
-        // common case: four lookups per 32 slots; the rare 5..8-class chunk
-        // takes a short divergent detour for its second status word
-        for (int q = lane; q < p.nq_s; q += 32, dq += 64, orow += 1024) {
-          const uint4 d0 = dq[0], d1 = dq[1];
-          const uint32_t lo = local_table4(d0.x, tb);
-          uint32_t hi = lo;
-          if (d0.y != 0xFFFFFFFFu) hi = local_table4(d0.y, tb);
-          stg_stream(orow, select16(lo, hi, d0.z, d0.w));
-          stg_stream(orow + 16, select16(lo, hi, d1.x, d1.y));
+    // 5. all slot statuses
+    if (p.slots_out && p.slot_all_k4) {
+      // common case (BERT-48): branch-free, four lookups per 16 slots
+      int8_t* orow = p.slots_out + b * p.slots_stride + 16 * lane;
+      const uint4* dq = slot_desc + lane;
+      for (int q = lane; q < p.nq_s; q += 32, dq += 32, orow += 512) {
+        const uint4 d = *dq;
+        const uint32_t lo = local_table4(d.x, tb);
+        stg_stream(orow, select16(lo, lo, d.z, d.w));
+      }
+    } else if (p.slots_out) {
+      int8_t* orow = p.slots_out + b * p.slots_stride;
+      for (int q = lane; q < p.nq_s; q += 32) {
+        const uint4 d = slot_desc[q];
+        uint4 o;
+        if ((d.x & 0xFF) != 0xFF) {
+          uint32_t lo, hi;
+          local_table(d.x, d.y, tb, &lo, &hi);
+          o = select16(lo, hi, d.z, d.w);
+        } else {
+          uint32_t ow[4] = {0, 0, 0, 0};
+          for (int t = 0; t < 16; ++t) ow[t >> 2] |= (uint32_t)(uint8_t)table[slot_cls8[16 * q + t]] << (8 * (t & 3));
+          o = make_uint4(ow[0], ow[1], ow[2], ow[3]);
         }
-      } else {
-        for (int q = lane; q < p.nq_s; q += 32, dq += 64, orow += 1024) {
-          const uint4 d0 = dq[0], d1 = dq[1];
-          if ((d0.x & 0xFF) != 0xFF) {
-            uint32_t lo, hi;
-            local_table(d0.x, d0.y, tb, &lo, &hi);
-            stg_stream(orow, select16(lo, hi, d0.z, d0.w));
-            stg_stream(orow + 16, select16(lo, hi, d1.x, d1.y));
-          } else {
-            uint32_t ow[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            for (int t = 0; t < 32; ++t)
-              ow[t >> 2] |= (uint32_t)(uint8_t)table[slot_cls8[32 * q + t]] << (8 * (t & 3));
-            stg_stream(orow, make_uint4(ow[0], ow[1], ow[2], ow[3]));
-            stg_stream(orow + 16, make_uint4(ow[4], ow[5], ow[6], ow[7]));
-          }
-        }
+        stg_stream(orow + 16 * q, o);
       }
     }
     if (lane == 0) {
@@ -585,10 +581,10 @@ int launch_propagate_fast(const GraphTables* g, const DecisionTables* d, const i
                           int64_t cand_stride, uint8_t* outcome, int32_t* counts, cudaStream_t stream) {
   if (!g->fast || !d->fast || d->n == 0) return AP_ERR_UNSUPPORTED;
   const int nq_d = (d->n + 15) / 16;
-  const int64_t nq_s = (g->num_slots + 31) / 32;  // 32-slot chunks
+  const int64_t nq_s = (g->num_slots + 15) / 16;
   auto aligned = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
   if (seed_stride % 16 || !aligned(seeds) || seed_stride < 16 * nq_d) return AP_ERR_UNSUPPORTED;
-  if (slots_out && (slots_stride % 16 || !aligned(slots_out) || slots_stride < 32 * nq_s)) return AP_ERR_UNSUPPORTED;
+  if (slots_out && (slots_stride % 16 || !aligned(slots_out) || slots_stride < 16 * nq_s)) return AP_ERR_UNSUPPORTED;
   FastParams p{};
   p.slot_desc = reinterpret_cast<const uint4*>(g->d_slot_desc.ptr);
   p.slot_cls8 = g->d_slot_cls8.ptr;
@@ -624,8 +620,8 @@ int launch_propagate_fast(const GraphTables* g, const DecisionTables* d, const i
     off += a16(bytes);
     return (int)o;
   };
-  p.off_slot_desc = place(nq_s * 32);
-  p.off_slot_cls8 = p.any_slot_fallback ? place(nq_s * 32) : 0;
+  p.off_slot_desc = place(nq_s * 16);
+  p.off_slot_cls8 = p.any_slot_fallback ? place(nq_s * 16) : 0;
   p.off_dec_desc = place((int64_t)nq_d * 32);
   p.off_dec_masks = place((int64_t)nq_d * 4);
   p.off_dec_cls8 = place((int64_t)nq_d * 16);

@@ -330,8 +330,8 @@ class PropagationEngine:
 
     @property
     def slots_stride(self) -> int:
-        """Row stride of slot outputs: |S| rounded up to 32 bytes (the fast kernel's 32-slot stores)."""
-        return max(32, (self._eng.num_slots + 31) // 32 * 32)
+        """Row stride of slot outputs: |S| rounded up to 16 bytes (vectorised stores)."""
+        return max(16, (self._eng.num_slots + 15) // 16 * 16)
 
     def launch(self, seeds, outcome, counts=None, slots=None, statuses=None, stream=None) -> None:
         """Raw stream-ordered launch on preallocated device tensors (no allocation, no sync).
@@ -443,7 +443,7 @@ class PropagationEngine:
             cand_t = torch.empty((b, row), dtype=torch.int8, device="cuda") if want_statuses else None
             slots_t = None
             if want_slots:
-                stride = self.slots_stride
+                stride = (eng.num_slots + 15) // 16 * 16 or 16
                 slots_t = torch.empty((b, stride), dtype=torch.int8, device="cuda")
             lib = _native.require_device()
             _native.check(
