@@ -331,10 +331,9 @@ __global__ void __launch_bounds__(kThreadsF) propagate_fast_kernel(FastParams p)
   const int64_t nwarps = (int64_t)gridDim.x * kWarpsF;
   int64_t b = (int64_t)blockIdx.x * kWarpsF + warp;
   uint4 cur[MAXCH];
+  if (b < p.batch) {
 #pragma unroll
-  for (int i = 0; i < MAXCH; ++i) {
-    const int q = lane + 32 * i;
-    cur[i] = (b < p.batch && q < p.nq_d) ? ldg_stream(p.seeds + b * p.seed_stride + 16 * q) : make_uint4(0, 0, 0, 0);
+    for (int i = 0; i < MAXCH; ++i) cur[i] = ldg_stream(p.seeds + b * p.seed_stride + 16 * min(lane + 32 * i, p.nq_d - 1));
   }
 
   for (; b < p.batch; b += nwarps) {
@@ -393,12 +392,16 @@ __global__ void __launch_bounds__(kThreadsF) propagate_fast_kernel(FastParams p)
     const bool hasU = __any_sync(kFullMask, anyU != 0);
     __syncwarp();
 
-    // prefetch the next plan's seeds while this one is evaluated
-    const int64_t bn = b + nwarps;
+    // prefetch the next plan's seeds while this one is evaluated.  The loads
+    // are unconditional (addresses clamped into the batch) so they land in
+    // cur[] directly; a guarded load compiles to load-to-temp + predicated
+    // move, which waits out the DRAM latency right here.
+    const int64_t bn = b + nwarps < p.batch ? b + nwarps : b;
+    const int8_t* nrow = p.seeds + bn * p.seed_stride;
 #pragma unroll
     for (int i = 0; i < MAXCH; ++i) {
-      const int q = lane + 32 * i;
-      if (bn < p.batch && q < p.nq_d) cur[i] = ldg_stream(p.seeds + bn * p.seed_stride + 16 * q);
+      const int q = min(lane + 32 * i, p.nq_d - 1);
+      cur[i] = ldg_stream(nrow + 16 * q);
     }
 
     // 2. class bitsets: word k holds classes 32k..32k+31 (flags beyond C stay 0)
