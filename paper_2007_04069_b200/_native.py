@@ -9,12 +9,14 @@ compute call raises `EngineUnavailable` unless the in-tree
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "libautoplan_b200.so"
+# AP_LIB_PATH: developer override to A/B an alternative build of the same engine
+LIB_PATH = Path(os.environ.get("AP_LIB_PATH") or Path(__file__).resolve().parent / "libautoplan_b200.so")
 
 AP_OK = 0
 AP_ERR_INVALID = -1

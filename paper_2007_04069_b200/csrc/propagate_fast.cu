@@ -32,7 +32,16 @@
 namespace apb {
 namespace {
 
-constexpr int kWarpsF = 8;
+#ifndef AP_K1_MIN_BLOCKS
+#define AP_K1_MIN_BLOCKS 2
+#endif
+#ifndef AP_K1_MAX_CTAS_PER_SM
+#define AP_K1_MAX_CTAS_PER_SM 0  // 0: as many as fit
+#endif
+#ifndef AP_K1_WARPS
+#define AP_K1_WARPS 12  // 12 warps x 2 CTAs per SM: measured best on B200 (BERT-48)
+#endif
+constexpr int kWarpsF = AP_K1_WARPS;
 constexpr int kThreadsF = kWarpsF * 32;
 constexpr unsigned kFullMask = 0xffffffffu;
 constexpr uint32_t kOnes = 0x01010101u;
@@ -213,6 +222,14 @@ __device__ __forceinline__ void stg_stream(void* p, uint4 v) {
                : "memory");
 }
 
+// predicated streaming store: one @p STG, no branch around it
+__device__ __forceinline__ void stg_stream_if(void* p, uint4 v, int pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t@q st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};\n\t}" ::"l"(p),
+      "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(pred)
+      : "memory");
+}
+
 // address of byte `k` of packed class word `w` inside a 256-aligned table at `base`
 #define TBL_ADDR(w, base, k) __byte_perm((w), (base), 0x7650 + (k))
 
@@ -284,7 +301,7 @@ __device__ __forceinline__ void seed_masks(uint4 s, uint32_t* xp, uint32_t* xr, 
 
 // MAXCH: 16-byte seed chunks per lane; NW: 32-bit class words (classes <= 32*NW)
 template <int MAXCH, int NW>
-__global__ void __launch_bounds__(kThreadsF) propagate_fast_kernel(FastParams p) {
+__global__ void __launch_bounds__(kThreadsF, AP_K1_MIN_BLOCKS) propagate_fast_kernel(FastParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
   // stage the static tables
   auto stage = [&](int off, const void* src, int64_t bytes) {
@@ -506,12 +523,17 @@ __global__ void __launch_bounds__(kThreadsF) propagate_fast_kernel(FastParams p)
     // 5. all slot statuses
     if (p.slots_out && p.slot_all_k4) {
       // common case (BERT-48): branch-free, four lookups per 16 slots
+      // warp-uniform trip count: a per-lane `q < nq_s` bound diverges in the
+      // last round and runs the unrolled body's remainder paths back to back
       int8_t* orow = p.slots_out + b * p.slots_stride + 16 * lane;
-      const uint4* dq = slot_desc + lane;
-      for (int q = lane; q < p.nq_s; q += 32, dq += 32, orow += 512) {
-        const uint4 d = *dq;
+      const int rounds = (p.nq_s + 31) >> 5;
+      const int last = p.nq_s - 1;
+#pragma unroll 4
+      for (int it = 0; it < rounds; ++it) {
+        const int q = lane + 32 * it;
+        const uint4 d = slot_desc[min(q, last)];
         const uint32_t lo = local_table4(d.x, tb);
-        stg_stream(orow, select16(lo, lo, d.z, d.w));
+        stg_stream_if(orow + 512 * it, select16(lo, lo, d.z, d.w), q <= last);
       }
     } else if (p.slots_out) {
       int8_t* orow = p.slots_out + b * p.slots_stride;
@@ -553,6 +575,7 @@ int launch_fast_t(const FastParams& p, int64_t smem, cudaStream_t stream) {
   }
   int per_sm = 0;
   AP_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreadsF, (size_t)smem));
+  if (AP_K1_MAX_CTAS_PER_SM > 0) per_sm = std::min(per_sm, AP_K1_MAX_CTAS_PER_SM);
   per_sm = std::max(per_sm, 1);
   const int64_t want = (p.batch + kWarpsF - 1) / kWarpsF;
   const int grid = (int)std::min<int64_t>(want, (int64_t)num_sms * per_sm);
