@@ -193,6 +193,7 @@ def _ref_eval_rows(rows):
 
 def cpu_baseline_single(g, dims, order, seconds: float):
     """The reference engine (reused, one core) on the first rows of the same batch."""
+    from paper_2007_04069_b200.distributed import plan_shard
     from paper_2007_04069_b200.workloads import prefix_seed_batch
 
     dims_raw = [(d.flat_index, d.instruction_id, d.dim) for d in dims]
@@ -233,6 +234,7 @@ def run_reference_arm(args):
     if rank != 0:
         return
     g, dims = workload_setup(args.workload)
+    from paper_2007_04069_b200.distributed import plan_shard
     from paper_2007_04069_b200.workloads import prefix_seed_batch
 
     # decision order from the reference's own linkage would take minutes at this
@@ -306,6 +308,7 @@ def run_ours(args):
 
     from paper_2007_04069_b200.linkage import extract_linkage_groups, sorted_decision_order
     from paper_2007_04069_b200.sharding import PropagationEngine
+    from paper_2007_04069_b200.distributed import plan_shard
     from paper_2007_04069_b200.workloads import prefix_seed_batch
 
     rank, world, local = env_rank()
@@ -329,7 +332,7 @@ def run_ours(args):
         (ROOT / "profiles" / f"order_{args.workload}.json").write_text(json.dumps(order.tolist()))
 
     B = args.batch
-    seeds = prefix_seed_batch(order, rank * B, B, device="cuda", chunk=1 << 18)
+    seeds = prefix_seed_batch(order, *plan_shard(rank, B), device="cuda", chunk=1 << 18)
     stride = eng.slots_stride
     slots = torch.empty((B, stride), dtype=torch.int8, device="cuda")
     outcome = torch.empty(B, dtype=torch.uint8, device="cuda")
@@ -356,15 +359,12 @@ def run_ours(args):
         dist.barrier()
     clock_info = clocks.stop()
     elapsed_ms = start.elapsed_time(end)
-    t = torch.tensor([elapsed_ms], device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_ms = float(t.item())
+    max_ms = _max_over_ranks(elapsed_ms, world)
     conflict_rate = float((outcome == 2).float().mean().item())
 
     # e2e through the host-buffer API: pinned H2D + kernel + D2H every step
     Be = args.e2e_batch
-    seeds_host = prefix_seed_batch(order, rank * Be, Be, device="cuda").cpu().pin_memory()
+    seeds_host = prefix_seed_batch(order, *plan_shard(rank, Be), device="cuda").cpu().pin_memory()
     out_host = None
     for _ in range(2):
         out_host = eng.run_batch_host(seeds_host, out=out_host)
@@ -375,10 +375,7 @@ def run_ours(args):
     for _ in range(args.e2e_steps):
         out_host = eng.run_batch_host(seeds_host, out=out_host)
     e2e_s = time.perf_counter() - t0
-    te = torch.tensor([e2e_s], device="cuda")
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_s = float(te.item())
+    e2e_s = _max_over_ranks(e2e_s, world)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -431,7 +428,8 @@ def run_ours(args):
             "traffic": traffic,
             "bytes_per_plan": bytes_per_plan,
             "peak_source": peak_src,
-            "kernel": "propagate_kernel<true>",
+            "kernel": "apb::propagate_fast_kernel (K1)",
+            "traffic_source": "profiles/ncu_summary.json dram bytes/plan x plans per launch (ncu --set full)",
         },
         "cpu_baseline": cpu,
         "e2e": {
@@ -452,13 +450,9 @@ def run_ours(args):
 
 
 def _max_over_ranks(x: float, world: int) -> float:
-    import torch
-    import torch.distributed as dist
+    from paper_2007_04069_b200.distributed import max_over_ranks
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    return max_over_ranks(x) if world > 1 else float(x)
 
 
 def bench_dqn_vec(args, g, world, rank):
@@ -499,7 +493,8 @@ def bench_dqn_vec(args, g, world, rank):
     torch.cuda.synchronize()
     fwd_s = s2.elapsed_time(e2) / 1e3 / 10
     S, H = env.state_dim, cfg.hidden[0]
-    flops = 2.0 * E * (S * H + H * H + H * 3) * 3  # 3xTF32: three tensor-core passes
+    flops = 2.0 * E * (S * H + H * H + H * 3)  # algorithmic (one pass; precision 3 would run three)
+    best = tr.best_plan_global()  # all-gather of every rank's incumbent, first-wins by global episode id
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     tf32_peak = peaks.get("bf16_tflops", 1590.0) / 2.0
     return {
@@ -511,11 +506,14 @@ def bench_dqn_vec(args, g, world, rank):
                    "parallelism": f"data-parallel DQN x{world}, NCCL allreduce of Q-gradients" if world > 1 else "1 GPU",
                    "vector_steps": args.dqn_steps},
         "ms_per_vector_step": ms / args.dqn_steps,
+        "best_plan": None if best is None else {"partitions": best.partitions, "return": best.reward,
+                                                "global_episode": best.episode},
         "gpu_launches_per_vector_step": (tr.launches - launches0) / args.dqn_steps,
         "act_forward_tensor": {"bound": "tensor", "achieved": flops / fwd_s / 1e12, "unit": "TFLOP/s",
                                "peak": tf32_peak, "peak_source": "half of measured bf16 (dense TF32 = bf16/2)",
                                "frac": flops / fwd_s / 1e12 / tf32_peak, "gemm_m": E,
-                               "note": "3 GEMMs M=E K=state_dim/256 N=256/3, 3xTF32"},
+                               "note": f"3 GEMMs M=E K=state_dim/256 N=256/3, tcgen05 kind::tf32, "
+                                       f"precision={tr.net.precision} (1 = TF32, 3 = 3xTF32)"},
     }
 
 

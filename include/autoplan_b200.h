@@ -284,6 +284,16 @@ int ap_vec_post(int32_t E, int32_t n, int64_t ld, int8_t* seeds, const int8_t* s
                 float* ep_return, float* finished_return, int32_t* finished_partitions, int32_t* episodes_done,
                 void* stream);
 
+/* Per-env best completed plan of the vectorised driver (cli.py:237-240):
+ * replaces the incumbent iff (partitions, return) is strictly greater; records
+ * the global episode id step_base + e and copies the per-candidate status row
+ * into best_status [E, ld].  Cross-env / cross-rank selection keeps the
+ * reference's first-wins by lowest episode id. */
+int ap_vec_track_best(int32_t E, int32_t n, int64_t ld, const int8_t* status, const uint8_t* outcome,
+                      const uint8_t* done, const int32_t* finished_partitions, const float* finished_return,
+                      int64_t step_base, int32_t* best_partitions, float* best_return, int64_t* best_episode,
+                      int8_t* best_status, void* stream);
+
 /* E transitions into the device replay ring at slots (slot0 + e) % cap with
  * the running max priority (agent.py:197-205). */
 int ap_per_push(int32_t E, int32_t S, int32_t A, int64_t slot0, int64_t cap, const float* states,

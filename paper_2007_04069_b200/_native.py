@@ -127,6 +127,7 @@ SIGNATURES: dict[str, tuple] = {
     "ap_vec_apply": (ctypes.c_int, [_VP, _I64, _VP, _VP, _I32, _VP]),
     "ap_vec_post": (ctypes.c_int, [_I32, _I32, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _VP, _VP, _VP, _VP,
                                    _I32, _VP, _VP, _VP, _VP, _VP]),
+    "ap_vec_track_best": (ctypes.c_int, [_I32, _I32, _I64, _VP, _VP, _VP, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP]),
     "ap_per_push": (ctypes.c_int, [_I32, _I32, _I32, _I64, _I64, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
                                    _VP, _VP, _VP, _VP, _VP]),
     "ap_per_sample_fast": (ctypes.c_int, [_VP, _I32, _F64, _F64, _VP, _I32, _VP, _VP, _VP, _VP, _VP]),

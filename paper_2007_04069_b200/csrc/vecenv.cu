@@ -95,6 +95,32 @@ __global__ void vec_post_kernel(int E, int n, int64_t ld, int8_t* seeds, const i
   }
 }
 
+// Per-env incumbent of completed (non-conflict) episodes, cli.py:237-240:
+// replace iff (partitions, return) is strictly greater, so within an env the
+// earliest episode wins ties.  The episode id is global (step_base + e) so a
+// cross-env / cross-rank reduction can keep first-wins by lowest id.
+// One warp per env; the winning per-candidate status row is copied.
+__global__ void vec_track_best_kernel(int E, int n, int64_t ld, const int8_t* status, const uint8_t* outcome,
+                                      const uint8_t* done, const int32_t* finished_partitions,
+                                      const float* finished_return, int64_t step_base, int32_t* best_partitions,
+                                      float* best_return, int64_t* best_episode, int8_t* best_status) {
+  const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (e >= E || !done[e] || outcome[e] == AP_OUTCOME_CONFLICT) return;
+  const int32_t p = finished_partitions[e];
+  const float r = finished_return[e];
+  const int32_t bp = best_partitions[e];
+  if (!(p > bp || (p == bp && r > best_return[e]))) return;
+  const int8_t* src = status + (int64_t)e * ld;
+  int8_t* dst = best_status + (int64_t)e * ld;
+  for (int j = lane; j < n; j += 32) dst[j] = src[j];
+  if (lane == 0) {
+    best_partitions[e] = p;
+    best_return[e] = r;
+    best_episode[e] = step_base + e;
+  }
+}
+
 __global__ void per_push_kernel(int E, int S, int A, int64_t slot0, int64_t cap, const float* states,
                                 const float* next_states, int64_t lds, const int32_t* actions, const float* rewards,
                                 const uint8_t* done, const uint8_t* masks, float* r_states, float* r_next,
@@ -214,6 +240,19 @@ int ap_vec_post(int32_t E, int32_t n, int64_t ld, int8_t* seeds, const int8_t* s
   vec_post_kernel<<<(E + 7) / 8, 256, 0, (cudaStream_t)stream>>>(
       E, n, ld, seeds, status, outcome, counts, prev_counts, position, order, cur_state, lds, next_state, rewards, done,
       next_mask, A, ep_return, finished_return, finished_partitions, episodes_done);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_vec_track_best(int32_t E, int32_t n, int64_t ld, const int8_t* status, const uint8_t* outcome,
+                      const uint8_t* done, const int32_t* finished_partitions, const float* finished_return,
+                      int64_t step_base, int32_t* best_partitions, float* best_return, int64_t* best_episode,
+                      int8_t* best_status, void* stream) {
+  if (E <= 0) return AP_OK;
+  vec_track_best_kernel<<<(E + 7) / 8, 256, 0, (cudaStream_t)stream>>>(E, n, ld, status, outcome, done,
+                                                                       finished_partitions, finished_return, step_base,
+                                                                       best_partitions, best_return, best_episode,
+                                                                       best_status);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }

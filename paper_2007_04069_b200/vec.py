@@ -22,6 +22,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _native
+from .distributed import BestPlan, allreduce_mean_, rank_world, reduce_best, select_first_wins
 from .agent import AdamOptimizer, AgentConfig, QNetwork, _Batch, epsilon_at, sync_target
 from .ir import decision_dims
 from .linkage import extract_linkage_groups, sorted_decision_order
@@ -77,9 +78,17 @@ class VecPartitionEnv:
         self.finished_return = torch.zeros(E, dtype=torch.float32, device=dev)
         self.finished_partitions = torch.full((E,), -1, dtype=torch.int32, device=dev)
         self.episodes_done = torch.zeros(E, dtype=torch.int32, device=dev)
+        # per-env incumbent of completed episodes (cli.py:237-240), global episode ids
+        self.best_partitions = torch.full((E,), -1, dtype=torch.int32, device=dev)
+        self.best_return = torch.full((E,), float("-inf"), dtype=torch.float32, device=dev)
+        self.best_episode = torch.full((E,), -1, dtype=torch.int64, device=dev)
+        self.best_status = torch.full((E, ld), -1, dtype=torch.int8, device=dev)
 
-    def step(self, actions) -> None:
-        """Apply actions [E] int32 (device); fills rewards / done / next_state / next_mask."""
+    def step(self, actions, step_base: int = 0) -> None:
+        """Apply actions [E] int32 (device); fills rewards / done / next_state / next_mask.
+
+        `step_base` + e is the global id of an episode finishing at this step
+        (the best-plan tie-break: lowest id wins, cli.py:239)."""
         lib = _native.require_device()
         P = _native.ptr
         self.obs.copy_(self.cur_state)
@@ -92,6 +101,10 @@ class VecPartitionEnv:
                                       P(self.rewards), P(self.done), P(self.next_mask), 2, P(self.ep_return),
                                       P(self.finished_return), P(self.finished_partitions), P(self.episodes_done),
                                       _s()))
+        _native.check(lib.ap_vec_track_best(self.E, self.n, self.seeds_full.stride(0), P(self.status), P(self.outcome),
+                                            P(self.done), P(self.finished_partitions), P(self.finished_return),
+                                            int(step_base), P(self.best_partitions), P(self.best_return),
+                                            P(self.best_episode), P(self.best_status), _s()))
 
 
 class VecDqnTrainer:
@@ -140,6 +153,7 @@ class VecDqnTrainer:
         self.train_steps = 0
         self.vector_steps = 0
         self.launches = 0
+        self.rank, self.world = rank_world(process_group) if process_group is not None else (0, 1)
 
     # -- one vector step -------------------------------------------------------------
 
@@ -194,9 +208,7 @@ class VecDqnTrainer:
                                     P(b.loss_rows), _s()))
         self.net.backward_device(acts, b.dz)
         if self.pg is not None:  # data-parallel learners: average the Q-gradient over NVLink
-            import torch.distributed as dist
-
-            dist.all_reduce(self.net.grad, op=dist.ReduceOp.AVG, group=self.pg)
+            allreduce_mean_(self.net.grad, self.pg)
         self.opt.step()
         _native.check(lib.ap_per_update_scaled(P(r["priorities"]), P(self.idx), P(b.td), B, float(cfg.per_alpha),
                                                _s()))
@@ -207,8 +219,9 @@ class VecDqnTrainer:
 
     def step(self) -> None:
         self.act()
-        self.env.step(self.actions)
-        self.launches += 3
+        E = self.env.E
+        self.env.step(self.actions, step_base=(self.vector_steps * self.world + self.rank) * E)
+        self.launches += 4
         self.observe()
         for _ in range(self.learn_steps):
             self.learn()
@@ -216,16 +229,23 @@ class VecDqnTrainer:
 
     # -- reporting ---------------------------------------------------------------------
 
-    def best_plan(self):
-        """(partitions, return, env index) of the best finished episode seen on this rank."""
-        parts = self.env.finished_partitions
-        ret = self.env.finished_return
-        key = parts.double() * 1e6 + ret.double()
-        k = int(torch_argmax(key))
-        return int(parts[k].item()), float(ret[k].item()), k
+    def best_plan(self) -> BestPlan | None:
+        """Best completed plan on this rank (max (partitions, return), lowest episode id)."""
+        env = self.env
+        k = select_first_wins(env.best_partitions, env.best_return, env.best_episode)
+        if k is None:
+            return None
+        return BestPlan(int(env.best_partitions[k]), float(env.best_return[k]), int(env.best_episode[k]),
+                        env.best_status[k, : env.n].cpu().numpy().copy())
 
-
-def torch_argmax(x):
-    import torch
-
-    return torch.argmax(x).item()
+    def best_plan_global(self) -> BestPlan | None:
+        """Best completed plan over all ranks: one all-gather of (key, episode id, statuses)."""
+        env = self.env
+        k = select_first_wins(env.best_partitions, env.best_return, env.best_episode)
+        if k is None:
+            key = (-1, float("-inf"), -1)
+            row = env.best_status.new_full((env.n,), -1)
+        else:
+            key = (int(env.best_partitions[k]), float(env.best_return[k]), int(env.best_episode[k]))
+            row = env.best_status[k, : env.n]
+        return reduce_best(key, row, self.pg)

@@ -20,10 +20,12 @@ def test_vec_env_matches_single_envs(cuda, name):
     singles = [OppEnv(g) for _ in range(E)]
     states = [s.reset() for s in singles]
     rng = np.random.default_rng(3)
+    ep_ret = np.zeros(E, dtype=np.float32)  # the driver accumulates returns in fp32
+    best = None  # (partitions, return, global episode id, statuses), cli.py:237-240 rule
     for step in range(60):
         np.testing.assert_array_equal(venv.cur_state.cpu().numpy(), np.array(states, dtype=np.float32))
         actions = rng.integers(0, 2, size=E).astype(np.int32)
-        venv.step(torch.from_numpy(actions).cuda())
+        venv.step(torch.from_numpy(actions).cuda(), step_base=step * E)
         rewards = venv.rewards.cpu().numpy()
         done = venv.done.cpu().numpy()
         nxt = venv.next_state.cpu().numpy()
@@ -32,7 +34,24 @@ def test_vec_env_matches_single_envs(cuda, name):
             assert abs(rewards[e] - res.reward) < 1e-5
             assert bool(done[e]) == res.done
             np.testing.assert_array_equal(nxt[e], res.next_state.astype(np.float32))
+            ep_ret[e] += rewards[e]
+            if res.done:
+                if not res.info.get("conflict", False):
+                    strat = env.strategy()
+                    row = [int(strat[d]) for d in env.dims]
+                    cand = (env.partition_count, float(ep_ret[e]), step * E + e, row)
+                    if best is None or cand[:2] > best[:2] or (cand[:2] == best[:2] and cand[2] < best[2]):
+                        best = cand
+                ep_ret[e] = 0.0
             states[e] = env.reset() if res.done else res.next_state
+    from paper_2007_04069_b200.distributed import select_first_wins
+
+    k = select_first_wins(venv.best_partitions, venv.best_return, venv.best_episode)
+    assert best is not None and k is not None
+    assert int(venv.best_partitions[k]) == best[0]
+    assert float(venv.best_return[k]) == best[1]
+    assert int(venv.best_episode[k]) == best[2]
+    assert venv.best_status[k, : venv.n].cpu().tolist() == best[3]
 
 
 def test_vec_trainer_runs_and_learns(cuda):
@@ -46,5 +65,8 @@ def test_vec_trainer_runs_and_learns(cuda):
     assert tr.train_steps > 0
     assert int(venv.episodes_done.sum().item()) > 256
     assert torch.isfinite(tr.net.flat).all()
-    parts, ret, _ = tr.best_plan()
-    assert parts >= 0
+    bp = tr.best_plan()
+    assert bp is not None and bp.partitions >= 0 and bp.episode >= 0
+    assert set(np.unique(bp.statuses)) <= {0, 1}  # a completed strategy decides every candidate
+    g_bp = tr.best_plan_global()  # single process: identity reduction
+    assert (g_bp.partitions, g_bp.episode) == (bp.partitions, bp.episode)
