@@ -51,6 +51,7 @@ def parse_args():
     p.add_argument("--dqn-envs", type=int, default=4096)
     p.add_argument("--dqn-learn-steps", type=int, default=4)
     p.add_argument("--dqn-steps", type=int, default=30)
+    p.add_argument("--dqn-eager", action="store_true", help="launch the vector step eagerly (no CUDA graph)")
     p.add_argument("--pp-envs", type=int, default=64)
     p.add_argument("--single-steps", type=int, default=300)
     return p.parse_args()
@@ -467,7 +468,8 @@ def bench_dqn_vec(args, g, world, rank):
     env = VecPartitionEnv(g, E)
     cfg = AgentConfig(lr=0.0005, epsilon_decay_iters=2000)
     pg = dist.group.WORLD if world > 1 else None
-    tr = VecDqnTrainer(env, cfg, capacity=max(4 * E, 4096), seed=rank, learn_steps=L, process_group=pg)
+    tr = VecDqnTrainer(env, cfg, capacity=max(4 * E, 4096), seed=rank, learn_steps=L, process_group=pg,
+                       use_graph=not args.dqn_eager)
     for _ in range(5):
         tr.step()
     torch.cuda.synchronize()
@@ -506,6 +508,9 @@ def bench_dqn_vec(args, g, world, rank):
                    "parallelism": f"data-parallel DQN x{world}, NCCL allreduce of Q-gradients" if world > 1 else "1 GPU",
                    "vector_steps": args.dqn_steps},
         "ms_per_vector_step": ms / args.dqn_steps,
+        "cuda_graph": tr.graph is not None,
+        "episodes_finished_rank0": int(env.episodes_done.sum().item()),
+        "envs_with_completed_episode_rank0": int((env.best_episode >= 0).sum().item()),
         "best_plan": None if best is None else {"partitions": best.partitions, "return": best.reward,
                                                 "global_episode": best.episode},
         "gpu_launches_per_vector_step": (tr.launches - launches0) / args.dqn_steps,

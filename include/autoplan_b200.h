@@ -291,8 +291,37 @@ int ap_vec_post(int32_t E, int32_t n, int64_t ld, int8_t* seeds, const int8_t* s
  * reference's first-wins by lowest episode id. */
 int ap_vec_track_best(int32_t E, int32_t n, int64_t ld, const int8_t* status, const uint8_t* outcome,
                       const uint8_t* done, const int32_t* finished_partitions, const float* finished_return,
-                      int64_t step_base, int32_t* best_partitions, float* best_return, int64_t* best_episode,
-                      int8_t* best_status, void* stream);
+                      int64_t step_base, const int64_t* ctl, int32_t world, int32_t rank, int32_t* best_partitions,
+                      float* best_return, int64_t* best_episode, int8_t* best_status, void* stream);
+
+/* ---- graph-capturable driver: device control block --------------------------------
+ * ctl = int64[4] in device memory: {vector_step, ring_slot, ring_size, train_steps}.
+ * The *_ctl entry points read their step counters from it instead of by-value
+ * arguments, so one captured CUDA graph of a whole vector step replays
+ * correctly (cli.py:193-248 loop body).  With ctl, ap_vec_track_best uses
+ * step_base = (ctl[0] * world + rank) * E. */
+
+/* epsilon-greedy act (agent.py:50-55,147-170) with epsilon from ctl[3] and the
+ * hash counter ctl[0] + 1 */
+int ap_dqn_act_ctl(const float* q, int64_t ldq, const uint8_t* mask, int64_t ldm, int32_t E, int32_t A,
+                   float epsilon_start, float epsilon_final, int64_t decay_iters, const int64_t* ctl, int32_t* actions,
+                   void* stream);
+/* Adam (agent.py:229-250) with bias corrections for t = ctl[3] + 1 */
+int ap_dqn_adam_ctl(float* params, const float* grads, float* m, float* v, int64_t n, float lr, float beta1,
+                    float beta2, float eps, const int64_t* ctl, void* stream);
+/* ap_per_push at ring slot ctl[1] */
+int ap_per_push_ctl(int32_t E, int32_t S, int32_t A, int64_t cap, const float* states, const float* next_states,
+                    int64_t lds, const int32_t* actions, const float* rewards, const uint8_t* done,
+                    const uint8_t* masks, float* r_states, float* r_next, int32_t* r_actions, float* r_rewards,
+                    uint8_t* r_done, uint8_t* r_masks, double* r_prio, const double* max_prio, const int64_t* ctl,
+                    void* stream);
+/* ap_per_sample_fast over the first ctl[2] ring entries, uniforms from a counter
+ * hash of (seed, ctl[3], row) (agent.py:207-223 semantics, throughput RNG) */
+int ap_per_sample_ctl(const double* priorities, double beta, int32_t B, uint64_t seed, double* cdf_scratch,
+                      int32_t* indices, float* weights, double* max_priority, const int64_t* ctl, void* stream);
+/* mode 0: ctl[3] += 1 (one learn step); mode 1: ctl[0] += 1, ctl[1] = (ctl[1] + E) % cap,
+ * ctl[2] = min(ctl[2] + E, cap) (one vector step) */
+int ap_vec_ctl_advance(int64_t* ctl, int32_t mode, int64_t E, int64_t cap, void* stream);
 
 /* E transitions into the device replay ring at slots (slot0 + e) % cap with
  * the running max priority (agent.py:197-205). */

@@ -92,6 +92,8 @@ _VP = ctypes.c_void_p
 _I64 = ctypes.c_int64
 _I32 = ctypes.c_int32
 _F64 = ctypes.c_double
+_F32 = ctypes.c_float
+_U64 = ctypes.c_uint64
 _TOPO = ctypes.POINTER(Topology)
 SIGNATURES: dict[str, tuple] = {
     "ap_graph_create": (ctypes.c_int, [ctypes.POINTER(GraphDesc), ctypes.POINTER(_VP)]),
@@ -127,7 +129,14 @@ SIGNATURES: dict[str, tuple] = {
     "ap_vec_apply": (ctypes.c_int, [_VP, _I64, _VP, _VP, _I32, _VP]),
     "ap_vec_post": (ctypes.c_int, [_I32, _I32, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _VP, _VP, _VP, _VP,
                                    _I32, _VP, _VP, _VP, _VP, _VP]),
-    "ap_vec_track_best": (ctypes.c_int, [_I32, _I32, _I64, _VP, _VP, _VP, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP]),
+    "ap_vec_track_best": (ctypes.c_int, [_I32, _I32, _I64, _VP, _VP, _VP, _VP, _VP, _I64, _VP, _I32, _I32, _VP, _VP,
+                                         _VP, _VP, _VP]),
+    "ap_dqn_act_ctl": (ctypes.c_int, [_VP, _I64, _VP, _I64, _I32, _I32, _F32, _F32, _I64, _VP, _VP, _VP]),
+    "ap_dqn_adam_ctl": (ctypes.c_int, [_VP, _VP, _VP, _VP, _I64, _F32, _F32, _F32, _F32, _VP, _VP]),
+    "ap_per_push_ctl": (ctypes.c_int, [_I32, _I32, _I32, _I64, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
+                                       _VP, _VP, _VP, _VP, _VP, _VP]),
+    "ap_per_sample_ctl": (ctypes.c_int, [_VP, _F64, _I32, _U64, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "ap_vec_ctl_advance": (ctypes.c_int, [_VP, _I32, _I64, _I64, _VP]),
     "ap_per_push": (ctypes.c_int, [_I32, _I32, _I32, _I64, _I64, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
                                    _VP, _VP, _VP, _VP, _VP]),
     "ap_per_sample_fast": (ctypes.c_int, [_VP, _I32, _F64, _F64, _VP, _I32, _VP, _VP, _VP, _VP, _VP]),

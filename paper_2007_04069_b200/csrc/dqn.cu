@@ -46,11 +46,24 @@ __device__ inline uint32_t hash32(uint64_t x) {
   return (uint32_t)x;
 }
 
+// Linear epsilon decay (agent.py:50-55) from the device train-step counter.
+__device__ inline float epsilon_dev(int64_t it, float e0, float e1, int64_t decay) {
+  if (decay <= 0) return e1;
+  const double frac = fmin(1.0, fmax(0.0, (double)it / (double)decay));
+  return (float)((double)e0 + ((double)e1 - (double)e0) * frac);
+}
+
+// ctl != nullptr (graph-capturable driver): epsilon from ctl[AP_CTL_TRAIN], hash
+// counter ctl[AP_CTL_STEP] + 1, instead of the by-value arguments
 __global__ void act_kernel(const float* q, int64_t ldq, const uint8_t* mask, int64_t ldm, int E, int A, float eps,
-                           uint64_t seed, int32_t* out) {
+                           uint64_t seed, int32_t* out, const int64_t* ctl, float eps0, float eps1, int64_t decay) {
   const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (e >= E) return;
+  if (ctl) {
+    eps = epsilon_dev(ctl[AP_CTL_TRAIN], eps0, eps1, decay);
+    seed = (uint64_t)ctl[AP_CTL_STEP] + 1;
+  }
   const uint8_t* m = mask + (int64_t)e * ldm;
   int count = 0;
   float best = -INFINITY;
@@ -166,8 +179,14 @@ __global__ void colsum_kernel(const float* x, int64_t ld, int rows, int cols, fl
   out[c] = s;
 }
 
+// ctl != nullptr: bias corrections from step t = ctl[AP_CTL_TRAIN] + 1
 __global__ void adam_kernel(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
-                            float eps, float c1, float c2) {
+                            float eps, float c1, float c2, const int64_t* ctl) {
+  if (ctl) {
+    const double t = (double)(ctl[AP_CTL_TRAIN] + 1);
+    c1 = (float)(1.0 - pow((double)b1, t));
+    c2 = (float)(1.0 - pow((double)b2, t));
+  }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const float gi = g[i];
     const float mi = b1 * m[i] + (1.0f - b1) * gi;
@@ -330,7 +349,22 @@ int ap_dqn_act(const float* q, int64_t ldq, const uint8_t* mask, int64_t ldm, in
     return AP_ERR_INVALID;
   }
   if (E == 0) return AP_OK;
-  act_kernel<<<(E + 7) / 8, 256, 0, (cudaStream_t)stream>>>(q, ldq, mask, ldm, E, A, epsilon, seed, actions);
+  act_kernel<<<(E + 7) / 8, 256, 0, (cudaStream_t)stream>>>(q, ldq, mask, ldm, E, A, epsilon, seed, actions, nullptr,
+                                                            0.f, 0.f, 0);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_dqn_act_ctl(const float* q, int64_t ldq, const uint8_t* mask, int64_t ldm, int32_t E, int32_t A,
+                   float epsilon_start, float epsilon_final, int64_t decay_iters, const int64_t* ctl, int32_t* actions,
+                   void* stream) {
+  if (!q || !mask || !actions || !ctl || E < 0 || A < 1) {
+    set_error("ap_dqn_act_ctl: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  if (E == 0) return AP_OK;
+  act_kernel<<<(E + 7) / 8, 256, 0, (cudaStream_t)stream>>>(q, ldq, mask, ldm, E, A, 0.f, 0, actions, ctl,
+                                                            epsilon_start, epsilon_final, decay_iters);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
@@ -369,7 +403,20 @@ int ap_dqn_adam(float* params, const float* grads, float* m, float* v, int64_t n
                 float eps, float correct1, float correct2, void* stream) {
   if (n <= 0) return AP_OK;
   adam_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(params, grads, m, v, n, lr, beta1, beta2, eps,
-                                                                     correct1, correct2);
+                                                                     correct1, correct2, nullptr);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_dqn_adam_ctl(float* params, const float* grads, float* m, float* v, int64_t n, float lr, float beta1,
+                    float beta2, float eps, const int64_t* ctl, void* stream) {
+  if (!ctl) {
+    set_error("ap_dqn_adam_ctl: null control block");
+    return AP_ERR_INVALID;
+  }
+  if (n <= 0) return AP_OK;
+  adam_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(params, grads, m, v, n, lr, beta1, beta2, eps,
+                                                                     1.f, 1.f, ctl);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }

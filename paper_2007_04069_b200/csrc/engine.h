@@ -9,6 +9,10 @@
 
 #include "../../include/autoplan_b200.h"
 
+// Control block of the graph-capturable vectorised driver: int64[AP_CTL_WORDS]
+// read by the *_ctl entry points instead of by-value step counters.
+enum { AP_CTL_STEP = 0, AP_CTL_SLOT = 1, AP_CTL_SIZE = 2, AP_CTL_TRAIN = 3, AP_CTL_WORDS = 4 };
+
 namespace apb {
 
 void set_error(const std::string& msg);

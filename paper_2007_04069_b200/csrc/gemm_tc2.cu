@@ -294,8 +294,17 @@ int launch_gemm_v2(const float* A, int64_t lda, int transA, const float* B, int6
   if (splits > 1) {
     const size_t need = (size_t)splits * M * N * sizeof(float);
     if (need > g_work_bytes) {
-      if (g_work) cudaFree(g_work);
-      AP_CUDA_CHECK(cudaMalloc(&g_work, need));
+      // A captured CUDA graph may hold the old workspace: never free it, and
+      // never allocate inside a capture (warm the shapes up eagerly first).
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      AP_CUDA_CHECK(cudaStreamIsCapturing(stream, &cs));
+      if (cs != cudaStreamCaptureStatusNone) {
+        set_error("gemm: split-K workspace must grow during graph capture; run the shapes once before capturing");
+        return AP_ERR_INVALID;
+      }
+      float* fresh = nullptr;
+      AP_CUDA_CHECK(cudaMalloc(&fresh, need));
+      g_work = fresh;  // the previous buffer is intentionally kept alive
       g_work_bytes = need;
     }
     g.work = g_work;

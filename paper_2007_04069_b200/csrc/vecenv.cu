@@ -19,6 +19,15 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+__device__ inline uint32_t mix64to32(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdULL;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ULL;
+  x ^= x >> 33;
+  return (uint32_t)x;
+}
+
 __global__ void vec_apply_kernel(int8_t* seeds, int64_t ld, const int32_t* position, const int32_t* actions, int E) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= E) return;
@@ -102,11 +111,13 @@ __global__ void vec_post_kernel(int E, int n, int64_t ld, int8_t* seeds, const i
 // One warp per env; the winning per-candidate status row is copied.
 __global__ void vec_track_best_kernel(int E, int n, int64_t ld, const int8_t* status, const uint8_t* outcome,
                                       const uint8_t* done, const int32_t* finished_partitions,
-                                      const float* finished_return, int64_t step_base, int32_t* best_partitions,
-                                      float* best_return, int64_t* best_episode, int8_t* best_status) {
+                                      const float* finished_return, int64_t step_base, const int64_t* ctl, int world,
+                                      int rank, int32_t* best_partitions, float* best_return, int64_t* best_episode,
+                                      int8_t* best_status) {
   const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (e >= E || !done[e] || outcome[e] == AP_OUTCOME_CONFLICT) return;
+  if (ctl) step_base = (ctl[AP_CTL_STEP] * world + rank) * (int64_t)E;
   const int32_t p = finished_partitions[e];
   const float r = finished_return[e];
   const int32_t bp = best_partitions[e];
@@ -125,8 +136,9 @@ __global__ void per_push_kernel(int E, int S, int A, int64_t slot0, int64_t cap,
                                 const float* next_states, int64_t lds, const int32_t* actions, const float* rewards,
                                 const uint8_t* done, const uint8_t* masks, float* r_states, float* r_next,
                                 int32_t* r_actions, float* r_rewards, uint8_t* r_done, uint8_t* r_masks,
-                                double* r_prio, const double* max_prio) {
+                                double* r_prio, const double* max_prio, const int64_t* ctl) {
   const int e = blockIdx.x;
+  if (ctl) slot0 = ctl[AP_CTL_SLOT];
   const int64_t slot = (slot0 + e) % cap;
   for (int j = threadIdx.x; j < S; j += blockDim.x) {
     r_states[slot * S + j] = states[(int64_t)e * lds + j];
@@ -143,11 +155,26 @@ __global__ void per_push_kernel(int E, int S, int A, int64_t slot0, int64_t cap,
 
 // throughput-mode PER sample: priorities**alpha, CTA-parallel scan, searchsorted,
 // IS weights; also refreshes the running max priority used by per_push
+// ctl != nullptr: n = ctl[AP_CTL_SIZE], uniforms from a counter hash of
+// (seed, ctl[AP_CTL_TRAIN], b) instead of the `uniforms` array
 __global__ void per_sample_fast_kernel(const double* prio, int n, double alpha, double beta, const float* uniforms,
-                                       int B, double* cdf, int32_t* idx_out, float* w_out, double* max_prio) {
+                                       int B, double* cdf, int32_t* idx_out, float* w_out, double* max_prio,
+                                       const int64_t* ctl, uint64_t seed) {
   __shared__ double part[1024];
   __shared__ double pmax[1024];
   const int t = threadIdx.x, T = blockDim.x;
+  uint64_t draw = 0;
+  if (ctl) {
+    n = (int)ctl[AP_CTL_SIZE];
+    draw = (seed * 0x9E3779B97F4A7C15ULL) ^ ((uint64_t)ctl[AP_CTL_TRAIN] << 20);
+    if (n < 1) {  // empty ring (caller bug): keep indices in bounds
+      for (int b = t; b < B; b += T) {
+        idx_out[b] = 0;
+        w_out[b] = 0.0f;
+      }
+      return;
+    }
+  }
   const int per = (n + T - 1) / T;
   const int lo = t * per, hi = min(n, lo + per);
   double acc = 0.0, mx = 0.0;
@@ -177,7 +204,8 @@ __global__ void per_sample_fast_kernel(const double* prio, int n, double alpha, 
   for (int i = lo; i < hi; ++i) cdf[i] += part[t];
   __syncthreads();
   for (int b = t; b < B; b += T) {
-    const double u = (double)uniforms[b] * total;
+    const float ub = ctl ? (float)(mix64to32(draw + (uint64_t)b) >> 8) * (1.0f / 16777216.0f) : uniforms[b];
+    const double u = (double)ub * total;
     int l = 0, h = n;
     while (l < h) {
       const int mid = (l + h) >> 1;
@@ -206,6 +234,18 @@ __global__ void per_sample_fast_kernel(const double* prio, int n, double alpha, 
   }
   __syncthreads();
   for (int b = t; b < B; b += T) w_out[b] /= s_w[0];
+}
+
+// mode 0: one learn step done (train counter); mode 1: one vector step done
+// (step counter, ring slot and size after pushing E transitions)
+__global__ void ctl_advance_kernel(int64_t* ctl, int mode, int64_t E, int64_t cap) {
+  if (mode == 0) {
+    ctl[AP_CTL_TRAIN] += 1;
+  } else {
+    ctl[AP_CTL_STEP] += 1;
+    ctl[AP_CTL_SLOT] = (ctl[AP_CTL_SLOT] + E) % cap;
+    ctl[AP_CTL_SIZE] = ctl[AP_CTL_SIZE] + E < cap ? ctl[AP_CTL_SIZE] + E : cap;
+  }
 }
 
 // scaled[idx] = (|td| + 1e-6)**alpha, last duplicate wins
@@ -246,13 +286,16 @@ int ap_vec_post(int32_t E, int32_t n, int64_t ld, int8_t* seeds, const int8_t* s
 
 int ap_vec_track_best(int32_t E, int32_t n, int64_t ld, const int8_t* status, const uint8_t* outcome,
                       const uint8_t* done, const int32_t* finished_partitions, const float* finished_return,
-                      int64_t step_base, int32_t* best_partitions, float* best_return, int64_t* best_episode,
-                      int8_t* best_status, void* stream) {
+                      int64_t step_base, const int64_t* ctl, int32_t world, int32_t rank, int32_t* best_partitions,
+                      float* best_return, int64_t* best_episode, int8_t* best_status, void* stream) {
   if (E <= 0) return AP_OK;
-  vec_track_best_kernel<<<(E + 7) / 8, 256, 0, (cudaStream_t)stream>>>(E, n, ld, status, outcome, done,
-                                                                       finished_partitions, finished_return, step_base,
-                                                                       best_partitions, best_return, best_episode,
-                                                                       best_status);
+  if (ctl && (world < 1 || rank < 0 || rank >= world)) {
+    set_error("ap_vec_track_best: bad world / rank");
+    return AP_ERR_INVALID;
+  }
+  vec_track_best_kernel<<<(E + 7) / 8, 256, 0, (cudaStream_t)stream>>>(
+      E, n, ld, status, outcome, done, finished_partitions, finished_return, step_base, ctl, world, rank,
+      best_partitions, best_return, best_episode, best_status);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
@@ -265,7 +308,24 @@ int ap_per_push(int32_t E, int32_t S, int32_t A, int64_t slot0, int64_t cap, con
   if (E <= 0) return AP_OK;
   per_push_kernel<<<E, 128, 0, (cudaStream_t)stream>>>(E, S, A, slot0, cap, states, next_states, lds, actions, rewards,
                                                        done, masks, r_states, r_next, r_actions, r_rewards, r_done,
-                                                       r_masks, r_prio, max_prio);
+                                                       r_masks, r_prio, max_prio, nullptr);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_per_push_ctl(int32_t E, int32_t S, int32_t A, int64_t cap, const float* states, const float* next_states,
+                    int64_t lds, const int32_t* actions, const float* rewards, const uint8_t* done,
+                    const uint8_t* masks, float* r_states, float* r_next, int32_t* r_actions, float* r_rewards,
+                    uint8_t* r_done, uint8_t* r_masks, double* r_prio, const double* max_prio, const int64_t* ctl,
+                    void* stream) {
+  if (!ctl || cap < 1) {
+    set_error("ap_per_push_ctl: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  if (E <= 0) return AP_OK;
+  per_push_kernel<<<E, 128, 0, (cudaStream_t)stream>>>(E, S, A, 0, cap, states, next_states, lds, actions, rewards,
+                                                       done, masks, r_states, r_next, r_actions, r_rewards, r_done,
+                                                       r_masks, r_prio, max_prio, ctl);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
@@ -277,7 +337,29 @@ int ap_per_sample_fast(const double* priorities, int32_t n, double alpha, double
     return AP_ERR_INVALID;
   }
   per_sample_fast_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(priorities, n, alpha, beta, uniforms, B, cdf_scratch,
-                                                               indices, weights, max_priority);
+                                                               indices, weights, max_priority, nullptr, 0);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_per_sample_ctl(const double* priorities, double beta, int32_t B, uint64_t seed, double* cdf_scratch,
+                      int32_t* indices, float* weights, double* max_priority, const int64_t* ctl, void* stream) {
+  if (!ctl || B < 1) {
+    set_error("ap_per_sample_ctl: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  per_sample_fast_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(priorities, 0, 0.0, beta, nullptr, B, cdf_scratch,
+                                                               indices, weights, max_priority, ctl, seed);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_vec_ctl_advance(int64_t* ctl, int32_t mode, int64_t E, int64_t cap, void* stream) {
+  if (!ctl || (mode != 0 && mode != 1) || cap < 1) {
+    set_error("ap_vec_ctl_advance: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  ctl_advance_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(ctl, mode, E, cap);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }

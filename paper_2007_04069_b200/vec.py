@@ -23,7 +23,7 @@ import numpy as np
 
 from . import _native
 from .distributed import BestPlan, allreduce_mean_, rank_world, reduce_best, select_first_wins
-from .agent import AdamOptimizer, AgentConfig, QNetwork, _Batch, epsilon_at, sync_target
+from .agent import AdamOptimizer, AgentConfig, QNetwork, _Batch, sync_target
 from .ir import decision_dims
 from .linkage import extract_linkage_groups, sorted_decision_order
 from .sharding import PropagationEngine, pad16
@@ -84,11 +84,12 @@ class VecPartitionEnv:
         self.best_episode = torch.full((E,), -1, dtype=torch.int64, device=dev)
         self.best_status = torch.full((E, ld), -1, dtype=torch.int8, device=dev)
 
-    def step(self, actions, step_base: int = 0) -> None:
+    def step(self, actions, step_base: int = 0, ctl=None, world: int = 1, rank: int = 0) -> None:
         """Apply actions [E] int32 (device); fills rewards / done / next_state / next_mask.
 
         `step_base` + e is the global id of an episode finishing at this step
-        (the best-plan tie-break: lowest id wins, cli.py:239)."""
+        (the best-plan tie-break: lowest id wins, cli.py:239).  With a device
+        control block `ctl` the base is (ctl[0]·world + rank)·E instead."""
         lib = _native.require_device()
         P = _native.ptr
         self.obs.copy_(self.cur_state)
@@ -103,15 +104,28 @@ class VecPartitionEnv:
                                       _s()))
         _native.check(lib.ap_vec_track_best(self.E, self.n, self.seeds_full.stride(0), P(self.status), P(self.outcome),
                                             P(self.done), P(self.finished_partitions), P(self.finished_return),
-                                            int(step_base), P(self.best_partitions), P(self.best_return),
+                                            int(step_base), P(ctl) if ctl is not None else None, int(world),
+                                            int(rank), P(self.best_partitions), P(self.best_return),
                                             P(self.best_episode), P(self.best_status), _s()))
 
 
 class VecDqnTrainer:
-    """Batched acting + device replay + (data-parallel) DQN learner over a VecPartitionEnv."""
+    """Batched acting + device replay + (data-parallel) DQN learner over a VecPartitionEnv.
+
+    Every step counter the kernels need (vector step, ring slot / size, train
+    steps) lives in a device control block `ctl` (`AP_CTL_*`), so one vector
+    step has no host-baked arguments.  With `use_graph=True` the whole step —
+    act, K1 propagation, post, best-plan tracking, replay push and the L learn
+    steps (including the NCCL gradient all-reduce) — is captured once into a
+    CUDA graph and replayed; the host keeps mirrors of the counters and does
+    the target sync (a device copy) between replays every `target_sync_every`
+    train steps.
+    """
+
+    CTL_STEP, CTL_SLOT, CTL_SIZE, CTL_TRAIN = 0, 1, 2, 3
 
     def __init__(self, env: VecPartitionEnv, config: AgentConfig, capacity: int, seed: int = 0,
-                 learn_steps: int = 1, process_group=None, precision: int = 1):
+                 learn_steps: int = 1, process_group=None, precision: int = 1, use_graph: bool = False):
         import torch
 
         self.env = env
@@ -119,6 +133,7 @@ class VecDqnTrainer:
         self.capacity = capacity
         self.learn_steps = learn_steps
         self.pg = process_group
+        self.seed = seed
         rng = np.random.default_rng(seed)
         self.net = QNetwork(env.state_dim, env.num_actions, config.hidden, rng)
         self.net.precision = precision  # TF32 tensor cores by default in throughput mode
@@ -141,58 +156,52 @@ class VecDqnTrainer:
             "cdf": torch.zeros(capacity, dtype=torch.float64, device=dev),
         }
         self.max_prio = torch.ones(1, dtype=torch.float64, device=dev)
-        self.size = 0
+        self.ctl = torch.zeros(4, dtype=torch.int64, device=dev)
+        self.size = 0  # host mirrors of ctl
         self.slot = 0
         self.actions = torch.empty(env.E, dtype=torch.int32, device=dev)
         self.batch = _Batch(config.batch_size, S, A)
         self.idx = torch.empty(config.batch_size, dtype=torch.int32, device=dev)
         self.weights = torch.empty(config.batch_size, dtype=torch.float32, device=dev)
-        self.uniforms = torch.empty(config.batch_size, dtype=torch.float32, device=dev)
-        self.gen = torch.Generator(device=dev)
-        self.gen.manual_seed(seed)
         self.train_steps = 0
         self.vector_steps = 0
         self.launches = 0
         self.rank, self.world = rank_world(process_group) if process_group is not None else (0, 1)
+        self.use_graph = use_graph
+        self.graph = None
+        self._graph_launches = 0
 
     # -- one vector step -------------------------------------------------------------
 
     def act(self) -> None:
         lib = _native.require_device()
-        env = self.env
+        env, cfg = self.env, self.config
         q = self.net.forward_device(env.cur_state)
-        eps = epsilon_at(self.train_steps, self.config)
-        _native.check(lib.ap_dqn_act(_native.ptr(q), q.stride(0), _native.ptr(env.mask), env.mask.stride(0), env.E,
-                                     env.num_actions, float(eps), self.vector_steps + 1, _native.ptr(self.actions),
-                                     _s()))
+        _native.check(lib.ap_dqn_act_ctl(_native.ptr(q), q.stride(0), _native.ptr(env.mask), env.mask.stride(0), env.E,
+                                         env.num_actions, float(cfg.epsilon_start), float(cfg.epsilon_final),
+                                         int(cfg.epsilon_decay_iters), _native.ptr(self.ctl),
+                                         _native.ptr(self.actions), _s()))
         self.launches += 4  # 3 GEMMs + act
 
     def observe(self) -> None:
         lib = _native.require_device()
         env, r = self.env, self.ring
         P = _native.ptr
-        _native.check(lib.ap_per_push(env.E, env.state_dim, env.num_actions, self.slot, self.capacity, P(env.obs),
-                                      P(env.next_state), env.obs.stride(0), P(self.actions), P(env.rewards),
-                                      P(env.done), P(env.next_mask), P(r["states"]), P(r["next_states"]),
-                                      P(r["actions"]), P(r["rewards"]), P(r["done"]), P(r["next_mask"]),
-                                      P(r["priorities"]), P(self.max_prio), _s()))
-        self.slot = (self.slot + env.E) % self.capacity
-        self.size = min(self.size + env.E, self.capacity)
+        _native.check(lib.ap_per_push_ctl(env.E, env.state_dim, env.num_actions, self.capacity, P(env.obs),
+                                          P(env.next_state), env.obs.stride(0), P(self.actions), P(env.rewards),
+                                          P(env.done), P(env.next_mask), P(r["states"]), P(r["next_states"]),
+                                          P(r["actions"]), P(r["rewards"]), P(r["done"]), P(r["next_mask"]),
+                                          P(r["priorities"]), P(self.max_prio), P(self.ctl), _s()))
         self.launches += 1
 
     def learn(self) -> None:
-        import torch
-
         cfg, r, b = self.config, self.ring, self.batch
         B = cfg.batch_size
-        if self.size < B:
-            return
         lib = _native.require_device()
         P = _native.ptr
-        torch.rand(B, generator=self.gen, device="cuda", out=self.uniforms)
-        _native.check(lib.ap_per_sample_fast(P(r["priorities"]), self.size, cfg.per_alpha, cfg.per_beta,
-                                             P(self.uniforms), B, P(r["cdf"]), P(self.idx), P(self.weights),
-                                             P(self.max_prio), _s()))
+        _native.check(lib.ap_per_sample_ctl(P(r["priorities"]), cfg.per_beta, B, self.seed * 1000003 + self.rank,
+                                            P(r["cdf"]), P(self.idx), P(self.weights), P(self.max_prio), P(self.ctl),
+                                            _s()))
         for src, dst in ((r["states"], b.states), (r["next_states"], b.next_states)):
             _native.check(lib.ap_gather_rows(P(src), src.stride(0), P(self.idx), B, src.shape[1], P(dst),
                                              dst.stride(0), _s()))
@@ -209,23 +218,71 @@ class VecDqnTrainer:
         self.net.backward_device(acts, b.dz)
         if self.pg is not None:  # data-parallel learners: average the Q-gradient over NVLink
             allreduce_mean_(self.net.grad, self.pg)
-        self.opt.step()
+        opt = self.opt
+        _native.check(lib.ap_dqn_adam_ctl(P(self.net.flat), P(self.net.grad), P(opt.m), P(opt.v), self.net.flat.numel(),
+                                          opt.lr, opt.beta1, opt.beta2, opt.eps, P(self.ctl), _s()))
+        self.net.refresh_transposed()
         _native.check(lib.ap_per_update_scaled(P(r["priorities"]), P(self.idx), P(b.td), B, float(cfg.per_alpha),
                                                _s()))
-        self.train_steps += 1
-        if self.train_steps % cfg.target_sync_every == 0:
-            sync_target(self.net, self.target)
-        self.launches += 2 + 2 + 9 + 1 + 9 + 1 + 1
+        _native.check(lib.ap_vec_ctl_advance(P(self.ctl), 0, self.env.E, self.capacity, _s()))
+        self.launches += 2 + 2 + 9 + 1 + 9 + 1 + 1 + 1
 
-    def step(self) -> None:
+    def _step_body(self, learn: bool) -> None:
         self.act()
         E = self.env.E
-        self.env.step(self.actions, step_base=(self.vector_steps * self.world + self.rank) * E)
+        self.env.step(self.actions, ctl=self.ctl, world=self.world, rank=self.rank)
         self.launches += 4
         self.observe()
-        for _ in range(self.learn_steps):
-            self.learn()
+        # step counter, ring slot and size advance right after the push: every
+        # reader of the step counter (act, track-best) has run, and the learner
+        # must sample over the ring including this step's transitions
+        lib = _native.require_device()
+        _native.check(lib.ap_vec_ctl_advance(_native.ptr(self.ctl), 1, E, self.capacity, _s()))
+        self.launches += 1
+        if learn:
+            for _ in range(self.learn_steps):
+                self.learn()
+
+    def _advance_host(self, learned: bool) -> None:
+        E = self.env.E
+        if learned:
+            for _ in range(self.learn_steps):
+                self.train_steps += 1
+                if self.train_steps % self.config.target_sync_every == 0:
+                    sync_target(self.net, self.target)
+        self.slot = (self.slot + E) % self.capacity
+        self.size = min(self.size + E, self.capacity)
         self.vector_steps += 1
+
+    def step(self) -> None:
+        import torch
+
+        # learn once the ring holds a batch after this step's push (agent.py:318-337)
+        learn = min(self.size + self.env.E, self.capacity) >= self.config.batch_size
+        if not (self.use_graph and learn):
+            self._step_body(learn)
+            self._advance_host(learn)
+            return
+        if self.graph is None:
+            # one eager step first: allocates every lazily-sized buffer (split-K
+            # workspace, torch temporaries) outside the capture
+            self._step_body(learn)
+            self._advance_host(learn)
+            launches0 = self.launches
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(self.graph, stream=s):
+                    self._step_body(learn)
+            torch.cuda.current_stream().wait_stream(s)
+            # capture records the work without running it: device state is unchanged
+            self._graph_launches = self.launches - launches0
+            self.launches = launches0
+            return  # this call's vector step was the eager warm-up
+        self.graph.replay()
+        self.launches += self._graph_launches
+        self._advance_host(learn)
 
     # -- reporting ---------------------------------------------------------------------
 

@@ -70,3 +70,32 @@ def test_vec_trainer_runs_and_learns(cuda):
     assert set(np.unique(bp.statuses)) <= {0, 1}  # a completed strategy decides every candidate
     g_bp = tr.best_plan_global()  # single process: identity reduction
     assert (g_bp.partitions, g_bp.episode) == (bp.partitions, bp.episode)
+
+
+def _train(use_graph, steps, E=64, learn_steps=2):
+    g = graphs.generate("bert_base")
+    venv = VecPartitionEnv(g, E)
+    cfg = AgentConfig(lr=0.0005, epsilon_decay_iters=50, target_sync_every=4)
+    tr = VecDqnTrainer(venv, cfg, capacity=512, seed=7, learn_steps=learn_steps, use_graph=use_graph)
+    for _ in range(steps):
+        tr.step()
+    torch.cuda.synchronize()
+    return tr
+
+
+def test_cuda_graph_step_matches_eager(cuda):
+    """One captured vector step replayed N times == N eager steps, bit for bit
+    (counters in the device control block, counter-hash RNG, deterministic kernels)."""
+    a = _train(False, 12)
+    b = _train(True, 12)
+    assert b.graph is not None
+    for name in ("flat", "grad"):
+        assert torch.equal(getattr(a.net, name), getattr(b.net, name)), name
+    assert torch.equal(a.target.flat, b.target.flat)
+    assert torch.equal(a.ctl, b.ctl)
+    assert a.ctl.tolist() == [12, (12 * 64) % 512, 512, 12 * 2]  # step, slot, size, train
+    for k in a.ring:
+        assert torch.equal(a.ring[k], b.ring[k]), k
+    for k in ("cur_state", "episodes_done", "ep_return", "best_partitions", "best_episode"):
+        assert torch.equal(getattr(a.env, k), getattr(b.env, k)), k
+    assert (a.train_steps, a.vector_steps, a.size, a.slot) == (b.train_steps, b.vector_steps, b.size, b.slot)
