@@ -251,6 +251,11 @@ int ap_dqn_td(const float* q, const float* online_next, const float* target_next
 int ap_dqn_relu_backward(float* dh, const float* h, int64_t n, void* stream);
 /* out[c] = sum_r x[r*ld + c] (bias gradients, agent.py:118,134). */
 int ap_dqn_colsum(const float* x, int64_t ld, int32_t rows, int32_t cols, float* out, void* stream);
+/* Gradient into the last hidden layer from the (1 + A)-wide head (agent.py:120-132):
+ * dh = relu'(h) * (dz @ wh^T), wh [H, A1] row-major; dh_t (nullable) gets dh^T [H, B]. */
+int ap_dqn_head_backward(const float* dz, int64_t ldz, const float* wh, int64_t ldw, const float* h, int64_t ldh,
+                         int32_t B, int32_t H, int32_t A1, float* dh, int64_t lddh, float* dh_t, int64_t ldt,
+                         void* stream);
 /* Adam over a flat parameter buffer (agent.py:240-250); correct1/2 = 1 - beta^t. */
 int ap_dqn_adam(float* params, const float* grads, float* m, float* v, int64_t n, float lr, float beta1, float beta2,
                 float eps, float correct1, float correct2, void* stream);
@@ -317,8 +322,9 @@ int ap_per_push_ctl(int32_t E, int32_t S, int32_t A, int64_t cap, const float* s
                     void* stream);
 /* ap_per_sample_fast over the first ctl[2] ring entries, uniforms from a counter
  * hash of (seed, ctl[3], row) (agent.py:207-223 semantics, throughput RNG) */
-int ap_per_sample_ctl(const double* priorities, double beta, int32_t B, uint64_t seed, double* cdf_scratch,
-                      int32_t* indices, float* weights, double* max_priority, const int64_t* ctl, void* stream);
+int ap_per_sample_ctl(const double* priorities, int64_t capacity, double beta, int32_t B, uint64_t seed,
+                      double* cdf_scratch, int32_t* indices, float* weights, double* max_priority, const int64_t* ctl,
+                      void* stream);
 /* mode 0: ctl[3] += 1 (one learn step); mode 1: ctl[0] += 1, ctl[1] = (ctl[1] + E) % cap,
  * ctl[2] = min(ctl[2] + E, cap) (one vector step) */
 int ap_vec_ctl_advance(int64_t* ctl, int32_t mode, int64_t E, int64_t cap, void* stream);

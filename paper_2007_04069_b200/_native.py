@@ -121,6 +121,8 @@ SIGNATURES: dict[str, tuple] = {
                                  ctypes.c_float, _VP, _I64, _VP, _VP, _VP]),
     "ap_dqn_relu_backward": (ctypes.c_int, [_VP, _VP, _I64, _VP]),
     "ap_dqn_colsum": (ctypes.c_int, [_VP, _I64, _I32, _I32, _VP, _VP]),
+    "ap_dqn_head_backward": (ctypes.c_int, [_VP, _I64, _VP, _I64, _VP, _I64, _I32, _I32, _I32, _VP, _I64, _VP, _I64,
+                                            _VP]),
     "ap_dqn_adam": (ctypes.c_int, [_VP, _VP, _VP, _VP, _I64, ctypes.c_float, ctypes.c_float, ctypes.c_float,
                                    ctypes.c_float, ctypes.c_float, ctypes.c_float, _VP]),
     "ap_per_sample": (ctypes.c_int, [_VP, _I32, _F64, _F64, _VP, _I32, _VP, _VP, _VP, _VP]),
@@ -135,7 +137,7 @@ SIGNATURES: dict[str, tuple] = {
     "ap_dqn_adam_ctl": (ctypes.c_int, [_VP, _VP, _VP, _VP, _I64, _F32, _F32, _F32, _F32, _VP, _VP]),
     "ap_per_push_ctl": (ctypes.c_int, [_I32, _I32, _I32, _I64, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
                                        _VP, _VP, _VP, _VP, _VP, _VP]),
-    "ap_per_sample_ctl": (ctypes.c_int, [_VP, _F64, _I32, _U64, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "ap_per_sample_ctl": (ctypes.c_int, [_VP, _I64, _F64, _I32, _U64, _VP, _VP, _VP, _VP, _VP, _VP]),
     "ap_vec_ctl_advance": (ctypes.c_int, [_VP, _I32, _I64, _I64, _VP]),
     "ap_per_push": (ctypes.c_int, [_I32, _I32, _I32, _I64, _I64, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
                                    _VP, _VP, _VP, _VP, _VP]),

@@ -201,11 +201,24 @@ class QNetwork:
         gemm(h.t().contiguous(), dz.t().contiguous(), trans_b=True, out=self.grads["wh"], precision=self.precision)
         _native.check(lib.ap_dqn_colsum(_native.ptr(dz), dz.stride(0), b, dz.shape[1], _native.ptr(self.grads["bh"]),
                                         _stream()))
-        dh = gemm(dz, self.views["wh"], trans_b=True, precision=self.precision)
+        # head -> last hidden layer: K = 1 + A is too narrow for the tensor cores;
+        # one kernel does dz @ wh^T, the ReLU mask and the transposed copy
+        import torch
+
+        wh = self.views["wh"]
+        H = wh.shape[0]
+        dh = torch.empty((b, H), dtype=torch.float32, device="cuda")
+        dh_t = torch.empty((H, b), dtype=torch.float32, device="cuda")
+        _native.check(lib.ap_dqn_head_backward(_native.ptr(dz), dz.stride(0), _native.ptr(wh), wh.stride(0),
+                                               _native.ptr(h), h.stride(0), b, H, dz.shape[1], _native.ptr(dh),
+                                               dh.stride(0), _native.ptr(dh_t), dh_t.stride(0), _stream()))
         for i in range(len(self.hidden) - 1, -1, -1):
-            _native.check(lib.ap_dqn_relu_backward(_native.ptr(dh), _native.ptr(acts[i + 1]), dh.numel(), _stream()))
-            gemm(acts[i].t().contiguous(), dh.t().contiguous(), trans_b=True, out=self.grads[f"w{i}"],
-                 precision=self.precision)
+            if dh_t is None:  # layers below the last: ReLU mask, then the K-major copy
+                _native.check(lib.ap_dqn_relu_backward(_native.ptr(dh), _native.ptr(acts[i + 1]), dh.numel(),
+                                                       _stream()))
+                dh_t = dh.t().contiguous()
+            gemm(acts[i].t().contiguous(), dh_t, trans_b=True, out=self.grads[f"w{i}"], precision=self.precision)
+            dh_t = None
             _native.check(lib.ap_dqn_colsum(_native.ptr(dh), dh.stride(0), b, dh.shape[1],
                                             _native.ptr(self.grads[f"b{i}"]), _stream()))
             if i > 0:

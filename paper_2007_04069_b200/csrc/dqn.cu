@@ -171,6 +171,23 @@ __global__ void relu_bwd_kernel(float* dh, const float* h, int64_t n) {
     if (!(h[i] > 0.0f)) dh[i] = 0.0f;
 }
 
+// Gradient into the last hidden layer from the (1 + A)-wide dueling head
+// (agent.py:120-129): dh = relu'(h) * (dz @ wh^T), a K = 1 + A contraction too
+// narrow for the tensor cores; optionally also dh^T (the next weight-gradient
+// GEMM's K-major operand).  One thread per (row, unit).
+__global__ void head_backward_kernel(const float* dz, int64_t ldz, const float* wh, int64_t ldw, const float* h,
+                                     int64_t ldh, int B, int H, int A1, float* dh, int64_t lddh, float* dh_t,
+                                     int64_t ldt) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)B * H) return;
+  const int b = (int)(i / H), j = (int)(i % H);
+  float acc = 0.0f;
+  for (int k = 0; k < A1; ++k) acc = fmaf(dz[(int64_t)b * ldz + k], wh[(int64_t)j * ldw + k], acc);
+  if (!(h[(int64_t)b * ldh + j] > 0.0f)) acc = 0.0f;
+  dh[(int64_t)b * lddh + j] = acc;
+  if (dh_t) dh_t[(int64_t)j * ldt + b] = acc;
+}
+
 __global__ void colsum_kernel(const float* x, int64_t ld, int rows, int cols, float* out) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= cols) return;
@@ -388,6 +405,21 @@ int ap_dqn_td(const float* q, const float* online_next, const float* target_next
 int ap_dqn_relu_backward(float* dh, const float* h, int64_t n, void* stream) {
   if (n <= 0) return AP_OK;
   relu_bwd_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(dh, h, n);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_dqn_head_backward(const float* dz, int64_t ldz, const float* wh, int64_t ldw, const float* h, int64_t ldh,
+                         int32_t B, int32_t H, int32_t A1, float* dh, int64_t lddh, float* dh_t, int64_t ldt,
+                         void* stream) {
+  if (!dz || !wh || !h || !dh || B < 0 || H < 1 || A1 < 1) {
+    set_error("ap_dqn_head_backward: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  const int64_t n = (int64_t)B * H;
+  if (n == 0) return AP_OK;
+  head_backward_kernel<<<(int)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(dz, ldz, wh, ldw, h, ldh, B, H, A1,
+                                                                                 dh, lddh, dh_t, ldt);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }

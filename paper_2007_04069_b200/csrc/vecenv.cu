@@ -10,6 +10,8 @@
 //   per_push    transitions into the device replay ring at max priority
 // plus a throughput-mode PER sampler (parallel CTA scan; the parity sampler
 // in dqn.cu keeps numpy's sequential order).
+#include <algorithm>
+#include <climits>
 #include <cmath>
 
 #include "engine.h"
@@ -153,87 +155,134 @@ __global__ void per_push_kernel(int E, int S, int A, int64_t slot0, int64_t cap,
   }
 }
 
-// throughput-mode PER sample: priorities**alpha, CTA-parallel scan, searchsorted,
-// IS weights; also refreshes the running max priority used by per_push
+// throughput-mode PER sample over priorities already raised to alpha (kept
+// scaled by ap_per_update_scaled): one 1024-thread CTA, warp-shuffle block
+// scan into a CDF held in shared memory when it fits (global scratch
+// otherwise), searchsorted(side='right'), IS weights normalised by the batch
+// max; also refreshes the running max priority used by per_push.
 // ctl != nullptr: n = ctl[AP_CTL_SIZE], uniforms from a counter hash of
-// (seed, ctl[AP_CTL_TRAIN], b) instead of the `uniforms` array
-__global__ void per_sample_fast_kernel(const double* prio, int n, double alpha, double beta, const float* uniforms,
-                                       int B, double* cdf, int32_t* idx_out, float* w_out, double* max_prio,
-                                       const int64_t* ctl, uint64_t seed) {
-  __shared__ double part[1024];
-  __shared__ double pmax[1024];
-  const int t = threadIdx.x, T = blockDim.x;
+// (seed, ctl[AP_CTL_TRAIN], b) instead of the `uniforms` array.
+constexpr int kSampleThreads = 1024;
+constexpr int kSampleSmemMax = 24576;  // doubles of CDF kept in shared memory (192 KB)
+
+__device__ inline double warp_incl_scan(double v, int lane) {
+  for (int o = 1; o < 32; o <<= 1) {
+    const double u = __shfl_up_sync(kFull, v, o);
+    if (lane >= o) v += u;
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(kSampleThreads) per_sample_fast_kernel(
+    const double* prio, int n, double alpha, double beta, const float* uniforms, int B, double* cdf,
+    int32_t* idx_out, float* w_out, double* max_prio, const int64_t* ctl, uint64_t seed, int smem_cap) {
+  extern __shared__ double s_cdf[];
+  __shared__ double w_tot[32], w_max[32];
+  __shared__ float s_w[32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  (void)alpha;
   uint64_t draw = 0;
   if (ctl) {
     n = (int)ctl[AP_CTL_SIZE];
     draw = (seed * 0x9E3779B97F4A7C15ULL) ^ ((uint64_t)ctl[AP_CTL_TRAIN] << 20);
     if (n < 1) {  // empty ring (caller bug): keep indices in bounds
-      for (int b = t; b < B; b += T) {
+      for (int b = t; b < B; b += kSampleThreads) {
         idx_out[b] = 0;
         w_out[b] = 0.0f;
       }
       return;
     }
   }
-  const int per = (n + T - 1) / T;
-  const int lo = t * per, hi = min(n, lo + per);
-  double acc = 0.0, mx = 0.0;
-  (void)alpha;  // `prio` already holds priority**alpha (kept scaled by ap_per_update_scaled)
-  for (int i = lo; i < hi; ++i) {
-    const double v = prio[i];
-    acc += v;
-    cdf[i] = acc;
+  double* c = n <= smem_cap ? s_cdf : cdf;
+  // each warp owns a contiguous chunk, 32 elements per iteration (coalesced)
+  const int chunk = ((n + 31) / 32 + 31) / 32 * 32;
+  const int lo = warp * chunk, hi = min(n, lo + chunk);
+  double tot = 0.0, mx = 0.0;
+  for (int base = lo; base < hi; base += 32) {
+    const int i = base + lane;
+    const double v = i < hi ? prio[i] : 0.0;
+    if (i < hi) c[i] = v;
+    tot += v;
     mx = fmax(mx, v);
   }
-  part[t] = acc;
-  pmax[t] = mx;
-  __syncthreads();
-  if (t == 0) {
-    double run = 0.0, m = 0.0;
-    for (int k = 0; k < T; ++k) {
-      const double v = part[k];
-      part[k] = run;
-      run += v;
-      m = fmax(m, pmax[k]);
-    }
-    pmax[0] = run;
-    *max_prio = m;
+  for (int o = 16; o; o >>= 1) {
+    tot += __shfl_xor_sync(kFull, tot, o);
+    mx = fmax(mx, __shfl_xor_sync(kFull, mx, o));
+  }
+  if (lane == 0) {
+    w_tot[warp] = tot;
+    w_max[warp] = mx;
   }
   __syncthreads();
-  const double total = pmax[0];
-  for (int i = lo; i < hi; ++i) cdf[i] += part[t];
+  if (warp == 0) {
+    const double v = w_tot[lane];
+    const double incl = warp_incl_scan(v, lane);
+    w_tot[lane] = incl - v;  // exclusive offsets
+    const double m = w_max[lane];
+    double mm = m;
+    for (int o = 16; o; o >>= 1) mm = fmax(mm, __shfl_xor_sync(kFull, mm, o));
+    if (lane == 31) {
+      w_max[0] = incl;  // grand total
+      *max_prio = mm;
+    }
+  }
   __syncthreads();
-  for (int b = t; b < B; b += T) {
+  const double total = w_max[0];
+  double carry = w_tot[warp];
+  for (int base = lo; base < hi; base += 32) {
+    const int i = base + lane;
+    const double v = i < hi ? c[i] : 0.0;
+    const double incl = warp_incl_scan(v, lane) + carry;
+    if (i < hi) c[i] = incl;
+    carry = __shfl_sync(kFull, incl, 31);
+  }
+  __syncthreads();
+  float wm = 0.0f;
+  for (int b = t; b < B; b += kSampleThreads) {
     const float ub = ctl ? (float)(mix64to32(draw + (uint64_t)b) >> 8) * (1.0f / 16777216.0f) : uniforms[b];
     const double u = (double)ub * total;
     int l = 0, h = n;
     while (l < h) {
       const int mid = (l + h) >> 1;
-      if (cdf[mid] <= u)
+      if (c[mid] <= u)
         l = mid + 1;
       else
         h = mid;
     }
     if (l >= n) l = n - 1;
     idx_out[b] = l;
-    const double p = (cdf[l] - (l ? cdf[l - 1] : 0.0)) / total;
-    w_out[b] = (float)pow((double)n * p, -beta);
+    const double pr = (c[l] - (l ? c[l - 1] : 0.0)) / total;
+    const float w = (float)pow((double)n * pr, -beta);
+    w_out[b] = w;
+    wm = fmaxf(wm, w);
   }
-  __syncthreads();
   // normalise by the batch maximum
-  float wm = 0.0f;
-  for (int b = t; b < B; b += T) wm = fmaxf(wm, w_out[b]);
   for (int o = 16; o; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(kFull, wm, o));
-  __shared__ float s_w[32];
-  if ((t & 31) == 0) s_w[t >> 5] = wm;
+  if (lane == 0) s_w[warp] = wm;
   __syncthreads();
-  if (t == 0) {
-    float m = 0.0f;
-    for (int k = 0; k < (T >> 5); ++k) m = fmaxf(m, s_w[k]);
-    s_w[0] = m;
+  if (warp == 0) {
+    float m = s_w[lane];
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
+    if (lane == 0) s_w[0] = m;
   }
   __syncthreads();
-  for (int b = t; b < B; b += T) w_out[b] /= s_w[0];
+  for (int b = t; b < B; b += kSampleThreads) w_out[b] /= s_w[0];
+}
+
+int launch_per_sample(const double* prio, int n_host_max, double beta, const float* uniforms, int B, double* cdf,
+                      int32_t* idx, float* w, double* max_prio, const int64_t* ctl, uint64_t seed, cudaStream_t s) {
+  // shared CDF sized for the largest ring this launch can see
+  const int64_t smem = n_host_max <= kSampleSmemMax ? (int64_t)n_host_max * 8 : 0;
+  static int64_t configured = -1;
+  if (smem > configured) {
+    AP_CUDA_CHECK(cudaFuncSetAttribute(per_sample_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)std::max<int64_t>(smem, 0)));
+    configured = smem;
+  }
+  per_sample_fast_kernel<<<1, kSampleThreads, (size_t)smem, s>>>(prio, n_host_max, 0.0, beta, uniforms, B, cdf, idx, w,
+                                                                 max_prio, ctl, seed, (int)(smem / 8));
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
 }
 
 // mode 0: one learn step done (train counter); mode 1: one vector step done
@@ -336,22 +385,20 @@ int ap_per_sample_fast(const double* priorities, int32_t n, double alpha, double
     set_error("ap_per_sample_fast: empty buffer or batch");
     return AP_ERR_INVALID;
   }
-  per_sample_fast_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(priorities, n, alpha, beta, uniforms, B, cdf_scratch,
-                                                               indices, weights, max_priority, nullptr, 0);
-  AP_CUDA_CHECK(cudaGetLastError());
-  return AP_OK;
+  (void)alpha;  // priorities are kept raised to alpha
+  return launch_per_sample(priorities, n, beta, uniforms, B, cdf_scratch, indices, weights, max_priority, nullptr, 0,
+                           (cudaStream_t)stream);
 }
 
-int ap_per_sample_ctl(const double* priorities, double beta, int32_t B, uint64_t seed, double* cdf_scratch,
-                      int32_t* indices, float* weights, double* max_priority, const int64_t* ctl, void* stream) {
-  if (!ctl || B < 1) {
+int ap_per_sample_ctl(const double* priorities, int64_t capacity, double beta, int32_t B, uint64_t seed,
+                      double* cdf_scratch, int32_t* indices, float* weights, double* max_priority, const int64_t* ctl,
+                      void* stream) {
+  if (!ctl || B < 1 || capacity < 1 || capacity > INT32_MAX) {
     set_error("ap_per_sample_ctl: bad arguments");
     return AP_ERR_INVALID;
   }
-  per_sample_fast_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(priorities, 0, 0.0, beta, nullptr, B, cdf_scratch,
-                                                               indices, weights, max_priority, ctl, seed);
-  AP_CUDA_CHECK(cudaGetLastError());
-  return AP_OK;
+  return launch_per_sample(priorities, (int)capacity, beta, nullptr, B, cdf_scratch, indices, weights, max_priority,
+                           ctl, seed, (cudaStream_t)stream);
 }
 
 int ap_vec_ctl_advance(int64_t* ctl, int32_t mode, int64_t E, int64_t cap, void* stream) {

@@ -199,7 +199,8 @@ class VecDqnTrainer:
         B = cfg.batch_size
         lib = _native.require_device()
         P = _native.ptr
-        _native.check(lib.ap_per_sample_ctl(P(r["priorities"]), cfg.per_beta, B, self.seed * 1000003 + self.rank,
+        _native.check(lib.ap_per_sample_ctl(P(r["priorities"]), self.capacity, cfg.per_beta, B,
+                                            self.seed * 1000003 + self.rank,
                                             P(r["cdf"]), P(self.idx), P(self.weights), P(self.max_prio), P(self.ctl),
                                             _s()))
         for src, dst in ((r["states"], b.states), (r["next_states"], b.next_states)):
