@@ -52,7 +52,7 @@ def parse_args():
     p.add_argument("--dqn-learn-steps", type=int, default=4)
     p.add_argument("--dqn-steps", type=int, default=30)
     p.add_argument("--dqn-eager", action="store_true", help="launch the vector step eagerly (no CUDA graph)")
-    p.add_argument("--pp-envs", type=int, default=64)
+    p.add_argument("--pp-envs", type=int, default=512, help="PP-train env states evaluated per launch")
     p.add_argument("--single-steps", type=int, default=300)
     return p.parse_args()
 
@@ -522,6 +522,35 @@ def bench_dqn_vec(args, g, world, rank):
     }
 
 
+_FP64_PEAK = None
+
+
+def measure_fp64_add_peak() -> float:
+    """FP64 adds/s of this GPU (MEASURED_PEAKS.json has no fp64 figure): best of 5 probe launches."""
+    global _FP64_PEAK
+    if _FP64_PEAK is not None:
+        return _FP64_PEAK
+    import torch
+
+    from paper_2007_04069_b200 import _native
+
+    lib = _native.require_device()
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    blocks, iters = sms * 8, 20000
+    scratch = torch.zeros(1, dtype=torch.float64, device="cuda")
+    best = 0.0
+    for rep in range(6):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        _native.check(lib.ap_probe_fp64_add(blocks, iters, _native.ptr(scratch), _native.stream_handle()))
+        e.record()
+        torch.cuda.synchronize()
+        if rep:
+            best = max(best, blocks * 256 * 8 * iters / (s.elapsed_time(e) / 1e3))
+    _FP64_PEAK = best
+    return best
+
+
 def bench_pp_train(args, world, want_cpu):
     """PP-train candidate plans/s: PipeTrainEnv._state over all allowed pivots of E random partial plans."""
     import ctypes
@@ -573,11 +602,18 @@ def bench_pp_train(args, world, want_cpu):
     torch.cuda.synchronize()
     ms = _max_over_ranks(s.elapsed_time(e), world)
     evaluated = int(mask.sum())
+    F = env._model.num_forward
+    peak = measure_fp64_add_peak()
+    adds_per_s = evaluated * F * iters / (ms / 1e3)  # per GPU
     out = {"value": world * evaluated * iters / (ms / 1e3), "unit": "candidate plans/s",
            "config": {"graph": args.workload, "topology": "2x4", "stages": K, "radius": 3, "candidates": C,
-                      "env_states_per_launch": E, "allowed_candidates_per_launch": evaluated},
+                      "env_states_per_launch": E, "allowed_candidates_per_launch": evaluated,
+                      "forward_instructions": F},
            "ms_per_launch": ms / iters,
-           "bound": "fp64 add latency (N_f sequential adds per candidate)"}
+           "roofline": {"bound": "fp64 add", "achieved": adds_per_s / 1e12, "peak": peak / 1e12, "unit": "Tadd/s",
+                        "frac": adds_per_s / peak,
+                        "algorithmic": "N_f sequential fp64 adds per candidate (SURVEY §8(d)), per GPU",
+                        "peak_source": "measured: ap_probe_fp64_add (8 independent add chains per thread)"}}
     if want_cpu:
         out["cpu_baseline"] = cpu_pp_train(g, topo, K, env, applied, mask)
     return out

@@ -251,6 +251,12 @@ int ap_dqn_td(const float* q, const float* online_next, const float* target_next
 int ap_dqn_relu_backward(float* dh, const float* h, int64_t n, void* stream);
 /* out[c] = sum_r x[r*ld + c] (bias gradients, agent.py:118,134). */
 int ap_dqn_colsum(const float* x, int64_t ld, int32_t rows, int32_t cols, float* out, void* stream);
+/* Roofline probe (no reference counterpart): `blocks` x 256 threads each run 8
+ * independent fp64 add chains of `iters` adds; time the launch to get the
+ * FP64 add throughput that bounds the PP-train cost kernels.  scratch_dev:
+ * one double, never written in practice. */
+int ap_probe_fp64_add(int32_t blocks, int64_t iters, double* scratch_dev, void* stream);
+
 /* Gradient into the last hidden layer from the (1 + A)-wide head (agent.py:120-132):
  * dh = relu'(h) * (dz @ wh^T), wh [H, A1] row-major; dh_t (nullable) gets dh^T [H, B]. */
 int ap_dqn_head_backward(const float* dz, int64_t ldz, const float* wh, int64_t ldw, const float* h, int64_t ldh,

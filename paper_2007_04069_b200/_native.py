@@ -121,6 +121,7 @@ SIGNATURES: dict[str, tuple] = {
                                  ctypes.c_float, _VP, _I64, _VP, _VP, _VP]),
     "ap_dqn_relu_backward": (ctypes.c_int, [_VP, _VP, _I64, _VP]),
     "ap_dqn_colsum": (ctypes.c_int, [_VP, _I64, _I32, _I32, _VP, _VP]),
+    "ap_probe_fp64_add": (ctypes.c_int, [_I32, _I64, _VP, _VP]),
     "ap_dqn_head_backward": (ctypes.c_int, [_VP, _I64, _VP, _I64, _VP, _I64, _I32, _I32, _I32, _VP, _I64, _VP, _I64,
                                             _VP]),
     "ap_dqn_adam": (ctypes.c_int, [_VP, _VP, _VP, _VP, _I64, ctypes.c_float, ctypes.c_float, ctypes.c_float,

@@ -16,6 +16,7 @@
 //  * expressions keep Python's left-to-right association, ties in max/min
 //    and in the largest-remainder sort resolve to the lowest index.
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <vector>
 
@@ -169,22 +170,10 @@ struct PipeDev {
   int32_t vtotal;
 };
 
-// stage_metrics for sorted cut positions cuts[0..P-1] (pipecost.py:72-141).
-// Costs are read through `cost` (shared or global memory).
-__device__ inline void stage_metrics_dev(const PipeDev& pd, const double* cost, const int* cuts, int P, double scale,
-                                         double* comp, double* act, double* param, int* nvars) {
-  int s = 0;
-  double acc = 0.0;
-  for (int i = 0; i < pd.F; ++i) {
-    if (s < P && i > cuts[s]) {
-      comp[s] = acc;
-      ++s;
-      acc = 0.0;
-    }
-    acc = acc + cost[i];
-  }
-  comp[s] = acc;
-  for (++s; s <= P; ++s) comp[s] = 0.0;
+// Everything in stage_metrics after the stage sums (pipecost.py:104-141):
+// scale, crossing activation bytes, parameter bytes and variable counts.
+__device__ inline void stage_tail(const PipeDev& pd, const int* cuts, int P, double scale, double* comp, double* act,
+                                  double* param, int* nvars) {
   int64_t wprev = 0;
   int32_t vprev = 0;
   for (int k = 0; k <= P; ++k) {
@@ -197,6 +186,33 @@ __device__ inline void stage_metrics_dev(const PipeDev& pd, const double* cost, 
     wprev = w;
     vprev = v;
   }
+}
+
+// stage_metrics for sorted cut positions cuts[0..P-1] (pipecost.py:72-141).
+// Costs are read through `cost` (shared or global memory).
+__device__ inline void stage_metrics_dev(const PipeDev& pd, const double* cost, const int* cuts, int P, double scale,
+                                         double* comp, double* act, double* param, int* nvars) {
+  // One pass over the instructions; a stage closes at the first i past its
+  // cut (at most one per i, as in the reference loop).  The next boundary is a
+  // register so the per-instruction path is compare + load + add; lanes of a
+  // warp (different candidates) stay in lockstep over i, reading the same
+  // cost[i] (a shared-memory broadcast).
+  int s = 0;
+  int nb = P > 0 ? cuts[0] : INT_MAX;
+  double acc = 0.0;
+#pragma unroll 4
+  for (int i = 0; i < pd.F; ++i) {
+    if (i > nb) {
+      comp[s] = acc;
+      ++s;
+      acc = 0.0;
+      nb = s < P ? cuts[s] : INT_MAX;
+    }
+    acc = acc + cost[i];
+  }
+  comp[s] = acc;
+  for (++s; s <= P; ++s) comp[s] = 0.0;
+  stage_tail(pd, cuts, P, scale, comp, act, param, nvars);
 }
 
 __global__ void metrics_kernel(PipeDev pd, const int32_t* pivots, int64_t batch, int P, double scale, double* comp,
@@ -265,52 +281,185 @@ __global__ void candidates_kernel(int F, const double* prefix, double total, con
   }
 }
 
-// PipeTrainEnv._state raw features: one thread per (env, candidate)
-__global__ void train_cand_kernel(PipeDev pd, Topo t, const int32_t* cand_pos, int C, const int32_t* applied, int A,
-                                  const uint8_t* mask, int64_t E, double scale, double* state) {
+// Raw PipeTrainEnv._state features of one candidate from its stage metrics
+// (envs.py:378-397): max allreduce, max transfer, min/max compute balance.
+__device__ inline void train_features(const Topo& t, int K, const double* c, const double* a, const double* w,
+                                      double* red_o, double* tra_o, double* bal_o) {
+  int counts[kMaxStages], start[kMaxStages], end[kMaxStages];
+  proportional_counts(c, K, t.d, counts);
+  groups_from_counts(counts, K, start, end);
+  double red = 0.0, tra = 0.0, top = c[0], bot = c[0];
+  for (int s = 0; s < K; ++s) {
+    const double r = allreduce(t, w[s], start[s], end[s]);
+    if (s == 0 || r > red) red = r;
+    if (c[s] > top) top = c[s];
+    if (c[s] < bot) bot = c[s];
+  }
+  for (int s = 0; s + 1 < K; ++s) {
+    const double x = transfer(t, a[s], end[s] - 1, start[s + 1]);
+    if (s == 0 || x > tra) tra = x;
+  }
+  *red_o = red;
+  *tra_o = tra;
+  *bal_o = top > 0.0 ? bot / top : 1.0;
+}
+
+// Per-env compaction of the action mask: list[e*C + k] = k-th allowed
+// candidate of env e (ascending), count[e] = #allowed; disallowed candidates
+// get their three raw features zeroed here (envs.py:386-392).  One CTA per env,
+// block scan by warp ballots.
+__global__ void __launch_bounds__(1024) train_compact_kernel(const uint8_t* mask, int C, int64_t E, int32_t* list,
+                                                             int32_t* count, double* state) {
+  __shared__ int s_warp[32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nwarps = blockDim.x >> 5;
+  for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+    double* st = state + e * 4 * (int64_t)C;
+    int base = 0;
+    for (int c0 = 0; c0 < C; c0 += blockDim.x) {
+      const int i = c0 + t;
+      const bool ok = i < C && mask[e * C + i] != 0;
+      if (i < C && !ok) {
+        st[i] = 0.0;
+        st[C + i] = 0.0;
+        st[2 * C + i] = 0.0;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, ok);
+      if (lane == 0) s_warp[warp] = __popc(bal);
+      __syncthreads();
+      int off = 0, tot = 0;
+      for (int w = 0; w < nwarps; ++w) {
+        const int v = s_warp[w];
+        off += w < warp ? v : 0;
+        tot += v;
+      }
+      if (ok) list[e * C + base + off + __popc(bal & ((1u << lane) - 1u))] = i;
+      base += tot;
+      __syncthreads();
+    }
+    if (t == 0) count[e] = base;
+  }
+}
+
+// PipeTrainEnv._state raw features.  Each thread evaluates kCandPerThread
+// candidates of one env (i = chunk*128 + lane + 32*j): their stage sums run
+// as interleaved add chains over one shared pass of the cost array (one
+// shared-memory load and one boundary test per instruction for all chains),
+// which hides the fp64 add latency and amortises the loop.  Every chain
+// keeps the reference's sequential summation order, so results are
+// bit-identical to the one-candidate loop.
+#ifndef AP_PP_CHAINS
+#define AP_PP_CHAINS 2
+#endif
+constexpr int kCandPerThread = AP_PP_CHAINS;
+constexpr int kCandPerWarp = 32 * kCandPerThread;
+
+__global__ void __launch_bounds__(128) train_cand_kernel(PipeDev pd, Topo t, const int32_t* cand_pos, int C,
+                                                         const int32_t* applied, int A, const int32_t* list,
+                                                         const int32_t* count, int64_t E, double scale,
+                                                         double* state) {
   extern __shared__ double s_cost[];
   for (int i = threadIdx.x; i < pd.F; i += blockDim.x) s_cost[i] = pd.cost[i];
   __syncthreads();
-  const int64_t total = E * (int64_t)C;
+  const int nchunk = (C + kCandPerWarp - 1) / kCandPerWarp;
+  const int64_t total = E * (int64_t)nchunk * 32;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = idx / C;
-    const int i = (int)(idx % C);
+    const int64_t e = idx / (32 * (int64_t)nchunk);
+    const int chunk = (int)((idx / 32) % nchunk), lane = (int)(idx % 32);
+    const int n_ok = count[e];
+    if (chunk * kCandPerWarp >= n_ok) continue;  // whole warp past this env's list
     double* st = state + e * 4 * (int64_t)C;
-    const bool allowed = mask[e * C + i] != 0;
-    if (!allowed) {
-      st[i] = 0.0;
-      st[C + i] = 0.0;
-      st[2 * C + i] = 0.0;
-      continue;
+    int cand[kCandPerThread];
+    bool ok[kCandPerThread];
+#pragma unroll
+    for (int j = 0; j < kCandPerThread; ++j) {
+      const int k = chunk * kCandPerWarp + lane + 32 * j;
+      ok[j] = k < n_ok;
+      cand[j] = ok[j] ? list[e * C + k] : 0;
     }
-    int cuts[kMaxStages];
-    int P = 0;
+    // shared applied cuts, then each chain's own candidate cut (the mask only
+    // allows candidates after the last applied one, so each list is sorted)
+    int acut[kMaxStages];
+    int P0 = 0;
     for (int k = 0; k < A; ++k) {
       const int a = applied[e * A + k];
-      if (a >= 0) cuts[P++] = cand_pos[a];
+      if (a >= 0) acut[P0++] = cand_pos[a];
     }
-    cuts[P++] = cand_pos[i];
-    const int K = P + 1;
-    double c[kMaxStages], a[kMaxStages], w[kMaxStages];
-    stage_metrics_dev(pd, s_cost, cuts, P, scale, c, a, w, nullptr);
-    int counts[kMaxStages], start[kMaxStages], end[kMaxStages];
-    proportional_counts(c, K, t.d, counts);
-    groups_from_counts(counts, K, start, end);
-    double red = 0.0, tra = 0.0, top = c[0], bot = c[0];
-    for (int s = 0; s < K; ++s) {
-      const double r = allreduce(t, w[s], start[s], end[s]);
-      if (s == 0 || r > red) red = r;
-      if (c[s] > top) top = c[s];
-      if (c[s] < bot) bot = c[s];
+    int cpos[kCandPerThread], s[kCandPerThread], nb[kCandPerThread];
+    double acc[kCandPerThread];
+    double comp[kCandPerThread][kMaxStages];
+#pragma unroll
+    for (int j = 0; j < kCandPerThread; ++j) {
+      cpos[j] = ok[j] ? cand_pos[cand[j]] : INT_MAX - 1;  // idle chain: never closes
+      s[j] = 0;
+      nb[j] = P0 > 0 ? acut[0] : cpos[j];
+      acc[j] = 0.0;
     }
-    for (int s = 0; s + 1 < K; ++s) {
-      const double x = transfer(t, a[s], end[s] - 1, start[s + 1]);
-      if (s == 0 || x > tra) tra = x;
+    int nbmin = nb[0];
+#pragma unroll
+    for (int j = 1; j < kCandPerThread; ++j) nbmin = min(nbmin, nb[j]);
+    const int P = P0 + 1;
+    // one instruction with boundary handling (some chain closes a stage at i)
+    auto step = [&](int i) {
+      if (i > nbmin) {
+#pragma unroll
+        for (int j = 0; j < kCandPerThread; ++j) {
+          if (i > nb[j]) {
+            comp[j][s[j]] = acc[j];
+            ++s[j];
+            acc[j] = 0.0;
+            nb[j] = s[j] < P0 ? acut[s[j]] : (s[j] == P0 ? cpos[j] : INT_MAX);
+          }
+        }
+        nbmin = nb[0];
+#pragma unroll
+        for (int j = 1; j < kCandPerThread; ++j) nbmin = min(nbmin, nb[j]);
+      }
+      const double c = s_cost[i];
+#pragma unroll
+      for (int j = 0; j < kCandPerThread; ++j) acc[j] = acc[j] + c;
+    };
+    // blocks of kBlk instructions: no boundary inside -> kBlk/2 16-byte
+    // shared loads from a hoisted base address and kBlk sequential adds per
+    // chain (the same order as one at a time)
+    constexpr int kBlk = 8;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_cost);
+    const int Fb = pd.F - pd.F % kBlk;
+    int i = 0;
+    for (; i < Fb; i += kBlk) {
+      if (i + kBlk - 1 > nbmin) {
+#pragma unroll
+        for (int u = 0; u < kBlk; ++u) step(i + u);
+      } else {
+        double c[kBlk];
+#pragma unroll
+        for (int u = 0; u < kBlk; u += 2)
+          asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(c[u]), "=d"(c[u + 1]) : "r"(sbase + 8u * (uint32_t)(i + u)));
+#pragma unroll
+        for (int u = 0; u < kBlk; ++u)
+#pragma unroll
+          for (int j = 0; j < kCandPerThread; ++j) acc[j] = acc[j] + c[u];
+      }
     }
-    st[i] = red;
-    st[C + i] = tra;
-    st[2 * C + i] = top > 0.0 ? bot / top : 1.0;
+    for (; i < pd.F; ++i) step(i);
+#pragma unroll
+    for (int j = 0; j < kCandPerThread; ++j) {
+      if (!ok[j]) continue;
+      double* cj = comp[j];
+      int sj = s[j];
+      cj[sj] = acc[j];
+      for (++sj; sj <= P; ++sj) cj[sj] = 0.0;
+      int cuts[kMaxStages];
+      for (int k = 0; k < P0; ++k) cuts[k] = acut[k];
+      cuts[P0] = cpos[j];
+      double a[kMaxStages], w[kMaxStages];
+      stage_tail(pd, cuts, P, scale, cj, a, w, nullptr);
+      double red, tra, bal;
+      train_features(t, P + 1, cj, a, w, &red, &tra, &bal);
+      st[cand[j]] = red;
+      st[C + cand[j]] = tra;
+      st[2 * C + cand[j]] = bal;
+    }
   }
 }
 
@@ -471,6 +620,24 @@ struct ap_pipe {
   DevBuf<int32_t> d_vprefix, d_cp_prefix;
   bool uploaded = false;
   int device = 0;
+  // PP-train compaction scratch (grow-only)
+  int32_t* d_list = nullptr;
+  int32_t* d_count = nullptr;
+  int64_t list_cap = 0, count_cap = 0;
+
+  int ensure_train_scratch(int64_t n_list, int64_t n_env) {
+    if (n_list > list_cap) {
+      if (d_list) cudaFree(d_list);
+      AP_CUDA_CHECK(cudaMalloc(&d_list, n_list * sizeof(int32_t)));
+      list_cap = n_list;
+    }
+    if (n_env > count_cap) {
+      if (d_count) cudaFree(d_count);
+      AP_CUDA_CHECK(cudaMalloc(&d_count, n_env * sizeof(int32_t)));
+      count_cap = n_env;
+    }
+    return AP_OK;
+  }
 
   int ensure() {
     int cur = 0;
@@ -497,6 +664,10 @@ struct ap_pipe {
     return PipeDev{F, d_cost.ptr, d_crossing.ptr, d_wprefix.ptr, d_vprefix.ptr, wtotal, vtotal};
   }
   void release() {
+    if (d_list) cudaFree(d_list);
+    if (d_count) cudaFree(d_count);
+    d_list = d_count = nullptr;
+    list_cap = count_cap = 0;
     d_cost.release();
     d_prefix.release();
     d_crossing.release();
@@ -649,9 +820,14 @@ int ap_pipe_train_state(ap_pipe_t p, const ap_topology* topo, const int32_t* can
   }
   AP_CUDA_CHECK(cudaFuncSetAttribute(train_cand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const Topo t = make_topo(topo);
-  train_cand_kernel<<<grid_for(E * (int64_t)C, 128), 128, smem, (cudaStream_t)stream>>>(p->dev(), t, cand_pos, C,
-                                                                                        applied, A, mask, E, 1.0 + bwm,
-                                                                                        state);
+  if ((rc = p->ensure_train_scratch(E * (int64_t)C, E)) != AP_OK) return rc;
+  train_compact_kernel<<<(int)std::min<int64_t>(E, 148 * 4), 1024, 0, (cudaStream_t)stream>>>(
+      mask, C, E, p->d_list, p->d_count, state);
+  AP_CUDA_CHECK(cudaGetLastError());
+  const int64_t threads = E * (int64_t)((C + kCandPerWarp - 1) / kCandPerWarp) * 32;
+  train_cand_kernel<<<grid_for(threads, 128), 128, smem, (cudaStream_t)stream>>>(p->dev(), t, cand_pos, C, applied, A,
+                                                                                 p->d_list, p->d_count, E, 1.0 + bwm,
+                                                                                 state);
   AP_CUDA_CHECK(cudaGetLastError());
   train_norm_kernel<<<(int)std::min<int64_t>(E, 148 * 8), 256, 0, (cudaStream_t)stream>>>(C, applied, A, E, state);
   AP_CUDA_CHECK(cudaGetLastError());
