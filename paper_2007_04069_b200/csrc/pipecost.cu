@@ -17,6 +17,7 @@
 //    and in the largest-remainder sort resolve to the lowest index.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -586,6 +587,162 @@ __global__ void infer_search_kernel(const double* arr, int G, Topo t, int K, int
   }
 }
 
+// Table-driven exhaustive search (K <= 8 stages, <= 63 devices), bit-identical
+// to infer_search_kernel.  Every division in infer_point has one operand fixed
+// by the boundary combo and the other drawn from a handful of values fixed by
+// the cut combo:
+//   times[s] = cq[s] / n            n = group size (<= D)
+//   red[s]   = (fac(n) * par[s]) / slow,  slow in {intra, inter}
+//   trans[s] = act[s] / bw,         bw in {intra, inter}
+// so each warp takes one boundary combo, tabulates those quotients in shared
+// memory (same operands, same operations as the reference), and its lanes
+// sweep the cut combos, each described by one packed word: per stage 8 bits =
+// n (6) | slow is inter (1) | transfer is inter (1).
+constexpr int kTabN = 64;  // table rows per stage (n = 0..63)
+constexpr int kTabWarps = 8;
+
+template <int K>
+__global__ void __launch_bounds__(32 * kTabWarps) infer_search_tab_kernel(const double* arr, int G, Topo t, int M,
+                                                                          const int32_t* band, const int32_t* band_off,
+                                                                          int64_t nprod, const uint64_t* cword,
+                                                                          int64_t nc, double* blk_len,
+                                                                          int64_t* blk_idx,
+                                                                          unsigned long long* n_valid) {
+  extern __shared__ double s_tab[];
+  constexpr int kPerWarp = K * kTabN * 3 + 2 * K;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* T = s_tab + warp * kPerWarp;  // [K][kTabN]
+  double* R = T + K * kTabN;            // [K][kTabN][2]
+  double* TR = R + K * kTabN * 2;       // [K][2]
+  const double* cc = arr;
+  const double* aa = arr + G;
+  const double* ww = arr + 2 * G;
+  const int nmax = t.d + 1 < kTabN ? t.d + 1 : kTabN;
+  double best = INFINITY;
+  int64_t best_i = INT64_MAX;
+  // Boundary tuples are enumerated over the product of the per-pick bands
+  // (mixed radix, last pick fastest = the host odometer's lexicographic
+  // order); non-increasing tuples are skipped.  The product index ib is
+  // monotone in that order, so first-wins on ib * nc + ic selects the same
+  // winner as ranking the valid combos.
+  for (int64_t ib = blockIdx.x * (int64_t)kTabWarps + warp; ib < nprod; ib += (int64_t)gridDim.x * kTabWarps) {
+    int bnd[K];
+    {
+      int64_t rest = ib;
+      bool inc = true;
+#pragma unroll
+      for (int s = K - 2; s >= 0; --s) {
+        const int len = band_off[s + 1] - band_off[s];
+        bnd[s] = band[band_off[s] + (int)(rest % len)];
+        rest /= len;
+      }
+#pragma unroll
+      for (int s = 1; s + 1 < K; ++s) inc &= bnd[s] > bnd[s - 1];
+      if (!inc) continue;  // warp-uniform
+      if (lane == 0) atomicAdd(n_valid, 1ull);
+    }
+    // boundary-combo metrics (infer_point's first loop)
+    double cq[K], par[K], act[K];
+    int lo = 0;
+#pragma unroll
+    for (int s = 0; s < K; ++s) {
+      const int hi = s + 1 < K ? bnd[s] : G;
+      const double c = cc[hi - 1] - (lo > 0 ? cc[lo - 1] : 0.0);
+      const double w = ww[hi - 1] - (lo > 0 ? ww[lo - 1] : 0.0);
+      cq[s] = (c * 1000.0) / 1000.0;  // comp[s] / 1000.0 as in pipeline_len
+      par[s] = w;
+      act[s] = hi < G ? aa[hi - 1] : 0.0;
+      lo = hi;
+    }
+    __syncwarp();
+    for (int e = lane; e < K * nmax; e += 32) {
+      const int s = e / nmax, n = e % nmax;
+      double q = 0.0, r0 = 0.0, r1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if (k == s) {
+          q = n >= 1 ? cq[k] / (double)n : 0.0;
+          if (!(n <= 1 || par[k] == 0.0)) {  // allreduce() (topology.py:131-148)
+            const double f = (2.0 * (double)(n - 1)) / (double)n;
+            r0 = f * par[k] / t.intra;
+            r1 = f * par[k] / t.inter;
+          }
+        }
+      T[s * kTabN + n] = q;
+      R[(s * kTabN + n) * 2 + 0] = r0;
+      R[(s * kTabN + n) * 2 + 1] = r1;
+    }
+    if (lane < 2 * K) {
+      const int s = lane >> 1;
+      double a = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if (k == s) a = act[k];
+      TR[lane] = a / ((lane & 1) ? t.inter : t.intra);  // transfer(): bytes / bw
+    }
+    __syncwarp();
+    for (int64_t ic = lane; ic < nc; ic += 32) {
+      const uint64_t w = cword[ic];
+      double times[K], tr[K];
+      double t_max = 0.0, red_max = 0.0;
+#pragma unroll
+      for (int s = 0; s < K; ++s) {
+        const uint32_t b = (uint32_t)(w >> (8 * s)) & 0xFFu;
+        const int n = (int)(b & 63u);
+        times[s] = T[s * kTabN + n];
+        if (s == 0 || times[s] > t_max) t_max = times[s];
+        const double r = R[(s * kTabN + n) * 2 + ((b >> 6) & 1u)];
+        if (s == 0 || r > red_max) red_max = r;
+        if (s + 1 < K) tr[s] = TR[2 * s + ((b >> 7) & 1u)];
+      }
+      double len = (double)(M - 1) * t_max;
+      len = len + naive_sum(times, K);
+      len = len + naive_sum(tr, K - 1);
+      len = len + red_max;
+      if (len < 1e-12) len = 1e-12;  // _MIN_LENGTH (envs.py:53, 584)
+      const int64_t idx = ib * nc + ic;
+      if (len < best || (len == best && idx < best_i)) {
+        best = len;
+        best_i = idx;
+      }
+    }
+    __syncwarp();
+  }
+  // block-level first-wins argmin
+  __shared__ double s_len[32 * kTabWarps];
+  __shared__ int64_t s_idx[32 * kTabWarps];
+  s_len[threadIdx.x] = best;
+  s_idx[threadIdx.x] = best_i;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      const double l2 = s_len[threadIdx.x + o];
+      const int64_t i2 = s_idx[threadIdx.x + o];
+      if (l2 < s_len[threadIdx.x] || (l2 == s_len[threadIdx.x] && i2 < s_idx[threadIdx.x])) {
+        s_len[threadIdx.x] = l2;
+        s_idx[threadIdx.x] = i2;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    blk_len[blockIdx.x] = s_len[0];
+    blk_idx[blockIdx.x] = s_idx[0];
+  }
+}
+
+template <int K>
+int launch_infer_tab(const double* arr, int G, const Topo& t, int M, const int32_t* d_band, const int32_t* d_off,
+                     int64_t nprod, const uint64_t* d_w, int64_t nc, double* d_len, int64_t* d_idx,
+                     unsigned long long* d_valid, int blocks, cudaStream_t s) {
+  const size_t smem = (size_t)kTabWarps * (K * kTabN * 3 + 2 * K) * sizeof(double);
+  auto k = infer_search_tab_kernel<K>;
+  AP_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<blocks, 32 * kTabWarps, smem, s>>>(arr, G, t, M, d_band, d_off, nprod, d_w, nc, d_len, d_idx, d_valid);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
 Topo make_topo(const ap_topology* t) { return Topo{t->gpus_per_server, t->num_servers * t->gpus_per_server, t->intra_bw, t->inter_bw}; }
 
 int check_topo(const ap_topology* t, int stages) {
@@ -887,36 +1044,108 @@ extern "C" int ap_infer_search(const double* arrays, int32_t G, const ap_topolog
   }
   const int picks = K - 1;
   std::vector<int32_t> bc, cc;
-  combos(band_b, band_b_off, picks, &bc);
   combos(band_c, band_c_off, picks, &cc);
-  const int64_t nb = (int64_t)bc.size() / picks, nc = (int64_t)cc.size() / picks;
-  if (evaluated) *evaluated = nb * nc;
-  if (nb == 0 || nc == 0) {
+  const int64_t nc = (int64_t)cc.size() / picks;
+  int64_t nprod = 1;  // boundary band product (the table kernel enumerates it on the device)
+  for (int st = 0; st < picks; ++st) nprod *= band_b_off[st + 1] - band_b_off[st];
+  cudaStream_t s = (cudaStream_t)stream;
+  const Topo t = make_topo(topo);
+  // packed per-cut-combo words for the table-driven kernel (see
+  // infer_search_tab_kernel); any combo it cannot encode selects the general one
+  std::vector<uint64_t> cw;
+  bool tab = K <= 8 && t.d < kTabN && std::getenv("AP_INFER_GENERAL") == nullptr;
+  if (tab) {
+    cw.resize((size_t)nc);
+    for (int64_t ic = 0; ic < nc && tab; ++ic) {
+      uint64_t w = 0;
+      int prev = 0;
+      for (int st = 0; st < K && tab; ++st) {
+        const int end = st + 1 < K ? cc[ic * picks + st] : t.d;
+        const int n = end - prev;
+        if (n < 1 || n >= kTabN) {
+          tab = false;
+          break;
+        }
+        double slow = INFINITY;  // allreduce()'s ring minimum
+        for (int i = 0; i < n; ++i) slow = std::min(slow, bw(t, prev + i, prev + (i + 1) % n));
+        uint64_t bits = (uint64_t)n | ((n > 1 && slow != t.intra) ? 64u : 0u);
+        if (st + 1 < K) {
+          const int src = end - 1, dst = end;  // transfer(end[s]-1, start[s+1])
+          if (src == dst) tab = false;
+          if (bw(t, src, dst) != t.intra) bits |= 128u;
+        }
+        w |= bits << (8 * st);
+        prev = end;
+      }
+      if (tab) cw[(size_t)ic] = w;
+    }
+  }
+  int64_t nb = 0;
+  if (!tab) {
+    combos(band_b, band_b_off, picks, &bc);
+    nb = (int64_t)bc.size() / picks;
+  }
+  if (nc == 0 || nprod == 0 || (!tab && nb == 0)) {
+    if (evaluated) *evaluated = 0;
     set_error("ap_infer_search: empty search space");
     return AP_ERR_INFEASIBLE;
   }
-  cudaStream_t s = (cudaStream_t)stream;
-  int32_t *d_b = nullptr, *d_c = nullptr;
+  int32_t *d_b = nullptr, *d_c = nullptr, *d_band = nullptr, *d_off = nullptr;
+  uint64_t* d_w = nullptr;
+  unsigned long long* d_valid = nullptr;
   double* d_len = nullptr;
   int64_t* d_idx = nullptr;
-  const int blocks = (int)std::min<int64_t>((nb * nc + 255) / 256, 148 * 8);
-  AP_CUDA_CHECK(cudaMalloc(&d_b, bc.size() * sizeof(int32_t)));
-  AP_CUDA_CHECK(cudaMalloc(&d_c, cc.size() * sizeof(int32_t)));
+  const int blocks = tab ? (int)std::min<int64_t>((nprod + kTabWarps - 1) / kTabWarps, 148 * 8)
+                         : (int)std::min<int64_t>((nb * nc + 255) / 256, 148 * 8);
   AP_CUDA_CHECK(cudaMalloc(&d_len, blocks * sizeof(double)));
   AP_CUDA_CHECK(cudaMalloc(&d_idx, blocks * sizeof(int64_t)));
-  AP_CUDA_CHECK(cudaMemcpyAsync(d_b, bc.data(), bc.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-  AP_CUDA_CHECK(cudaMemcpyAsync(d_c, cc.data(), cc.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-  infer_search_kernel<<<blocks, 256, 0, s>>>(arrays, G, make_topo(topo), K, M, d_b, nb, d_c, nc, d_len, d_idx);
-  AP_CUDA_CHECK(cudaGetLastError());
+  unsigned long long n_valid = 0;
+  if (tab) {
+    const int nband = band_b_off[picks];
+    AP_CUDA_CHECK(cudaMalloc(&d_band, std::max(nband, 1) * sizeof(int32_t)));
+    AP_CUDA_CHECK(cudaMalloc(&d_off, (picks + 1) * sizeof(int32_t)));
+    AP_CUDA_CHECK(cudaMalloc(&d_valid, sizeof(unsigned long long)));
+    AP_CUDA_CHECK(cudaMalloc(&d_w, cw.size() * sizeof(uint64_t)));
+    AP_CUDA_CHECK(cudaMemcpyAsync(d_band, band_b, nband * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    AP_CUDA_CHECK(cudaMemcpyAsync(d_off, band_b_off, (picks + 1) * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    AP_CUDA_CHECK(cudaMemsetAsync(d_valid, 0, sizeof(unsigned long long), s));
+    AP_CUDA_CHECK(cudaMemcpyAsync(d_w, cw.data(), cw.size() * sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+#define AP_TAB(KK) \
+  launch_infer_tab<KK>(arrays, G, t, M, d_band, d_off, nprod, d_w, nc, d_len, d_idx, d_valid, blocks, s)
+    switch (K) {
+      case 2: rc = AP_TAB(2); break;
+      case 3: rc = AP_TAB(3); break;
+      case 4: rc = AP_TAB(4); break;
+      case 5: rc = AP_TAB(5); break;
+      case 6: rc = AP_TAB(6); break;
+      case 7: rc = AP_TAB(7); break;
+      default: rc = AP_TAB(8); break;
+    }
+#undef AP_TAB
+    if (rc != AP_OK) return rc;
+    AP_CUDA_CHECK(cudaMemcpyAsync(&n_valid, d_valid, sizeof(n_valid), cudaMemcpyDeviceToHost, s));
+  } else {
+    AP_CUDA_CHECK(cudaMalloc(&d_b, bc.size() * sizeof(int32_t)));
+    AP_CUDA_CHECK(cudaMalloc(&d_c, cc.size() * sizeof(int32_t)));
+    AP_CUDA_CHECK(cudaMemcpyAsync(d_b, bc.data(), bc.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    AP_CUDA_CHECK(cudaMemcpyAsync(d_c, cc.data(), cc.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    infer_search_kernel<<<blocks, 256, 0, s>>>(arrays, G, t, K, M, d_b, nb, d_c, nc, d_len, d_idx);
+    AP_CUDA_CHECK(cudaGetLastError());
+  }
   std::vector<double> hl(blocks);
   std::vector<int64_t> hi(blocks);
   AP_CUDA_CHECK(cudaMemcpyAsync(hl.data(), d_len, blocks * sizeof(double), cudaMemcpyDeviceToHost, s));
   AP_CUDA_CHECK(cudaMemcpyAsync(hi.data(), d_idx, blocks * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   AP_CUDA_CHECK(cudaStreamSynchronize(s));
-  cudaFree(d_b);
-  cudaFree(d_c);
-  cudaFree(d_len);
-  cudaFree(d_idx);
+  for (void* ptr : {(void*)d_b, (void*)d_c, (void*)d_band, (void*)d_off, (void*)d_valid, (void*)d_w, (void*)d_len,
+                    (void*)d_idx})
+    cudaFree(ptr);
+  if (tab && n_valid == 0) {
+    if (evaluated) *evaluated = 0;
+    set_error("ap_infer_search: empty search space");
+    return AP_ERR_INFEASIBLE;
+  }
+  if (evaluated) *evaluated = (tab ? (int64_t)n_valid : nb) * nc;
   double bl = INFINITY;
   int64_t bi = INT64_MAX;
   for (int k = 0; k < blocks; ++k)
@@ -925,10 +1154,17 @@ extern "C" int ap_infer_search(const double* arrays, int32_t G, const ap_topolog
       bi = hi[k];
     }
   const int64_t ib = bi / nc, ic = bi % nc;
-  for (int s2 = 0; s2 < picks; ++s2) {
-    best_b[s2] = bc[ib * picks + s2];
-    best_c[s2] = cc[ic * picks + s2];
+  if (tab) {  // ib is a band product index: decode it (last pick fastest)
+    int64_t rest = ib;
+    for (int s2 = picks - 1; s2 >= 0; --s2) {
+      const int len = band_b_off[s2 + 1] - band_b_off[s2];
+      best_b[s2] = band_b[band_b_off[s2] + (int)(rest % len)];
+      rest /= len;
+    }
+  } else {
+    for (int s2 = 0; s2 < picks; ++s2) best_b[s2] = bc[ib * picks + s2];
   }
+  for (int s2 = 0; s2 < picks; ++s2) best_c[s2] = cc[ic * picks + s2];
   *best_len = bl;
   return AP_OK;
 }

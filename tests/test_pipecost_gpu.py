@@ -143,6 +143,32 @@ def test_bert48_profile_known_optimum(cuda):
     assert length == 0.8745000000000145
 
 
+@pytest.mark.parametrize("preset,K,seed", [("configa", 2, 1), ("configb", 3, 2), ("configc", 4, 3),
+                                           ("configc", 5, 4), ("configb", 4, 5)])
+def test_infer_table_search_matches_general(cuda, monkeypatch, preset, K, seed):
+    """The table-driven K3 search (per-boundary-combo quotient tables) returns the
+    same optimum, length bits and point count as the general per-point kernel,
+    over whole (banded and unbanded) search spaces."""
+    from paper_2007_04069_b200.dataproc import generate_environment
+    from paper_2007_04069_b200.topology import PRESETS
+
+    arrays = generate_environment("uniform" if seed % 2 else "normal", 1280, seed)
+    topo = PRESETS[preset]
+    for banded in (True, False):
+        kw = {}
+        if banded:
+            bb_, cc_ = infer_search_bands(arrays, topo, K, 3)
+            kw = {"allowed_boundaries": bb_, "allowed_cuts": cc_}
+        env = PipeInferEnv(arrays, topo, K, **kw)
+        if not banded and K > 3:
+            continue  # the unbanded K >= 4 space is ~1e9 points: covered by the bench
+        fast = brute_force_plan(env)
+        monkeypatch.setenv("AP_INFER_GENERAL", "1")
+        general = brute_force_plan(env)
+        monkeypatch.delenv("AP_INFER_GENERAL")
+        assert fast == general
+
+
 def test_scalar_api(cuda):
     d = load("pipe", "uniform_chain_configa")
     g = graph_from_dict(json.loads(bytes(d["graph_json"]).decode()))
