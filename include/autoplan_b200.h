@@ -246,6 +246,19 @@ int ap_dqn_td(const float* q, const float* online_next, const float* target_next
               const float* rewards, const uint8_t* done, const uint8_t* next_mask, int64_t ldm, const float* weights,
               int32_t B, int32_t A, float gamma, float huber_delta, float* dz, int64_t ldz, float* td,
               float* loss_rows, void* stream);
+/* ap_dqn_td reading actions / rewards / done / next masks straight from replay-ring
+ * rows indices[b] (the sample gather of agent.py:207-223 fused in); dz_t
+ * (nullable) also receives dz^T [1 + A, B]. */
+int ap_dqn_td_ring(const float* q, const float* online_next, const float* target_next, int64_t ldq,
+                   const int32_t* indices, const int32_t* ring_actions, const float* ring_rewards,
+                   const uint8_t* ring_done, const uint8_t* ring_next_mask, int64_t ldm, const float* weights,
+                   int32_t B, int32_t A, float gamma, float huber_delta, float* dz, int64_t ldz, float* dz_t,
+                   int64_t ldzt, float* td, float* loss_rows, void* stream);
+/* n <= 8 transposes in one launch: dst_i[c * ld_dst_i + r] = src_i[r * ld_src_i + c]
+ * for r < rows_i, c < cols_i (descriptor arrays are host memory). Refreshes the
+ * transposed weight copies the K-major tcgen05 GEMMs read. */
+int ap_transpose_batch(int32_t n, const float* const* src, const int64_t* ld_src, float* const* dst,
+                       const int64_t* ld_dst, const int32_t* rows, const int32_t* cols, void* stream);
 
 /* dh[i] = 0 where h[i] <= 0 (ReLU backward, agent.py:132). */
 int ap_dqn_relu_backward(float* dh, const float* h, int64_t n, void* stream);

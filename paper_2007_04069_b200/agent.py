@@ -161,8 +161,26 @@ class QNetwork:
         self.refresh_transposed()
 
     def refresh_transposed(self) -> None:
-        for name, t in self.wt.items():
-            t.copy_(self.views[name].t())
+        """All transposed weight copies in one launch (ap_transpose_batch)."""
+        import ctypes
+
+        if getattr(self, "_tdesc", None) is None:  # descriptors: the tensors never move
+            names = list(self.wt)
+            n = len(names)
+            src = [self.views[k] for k in names]
+            dst = [self.wt[k] for k in names]
+            self._tdesc = (
+                n,
+                (ctypes.c_void_p * n)(*[t.data_ptr() for t in src]),
+                (ctypes.c_int64 * n)(*[t.stride(0) for t in src]),
+                (ctypes.c_void_p * n)(*[t.data_ptr() for t in dst]),
+                (ctypes.c_int64 * n)(*[t.stride(0) for t in dst]),
+                (ctypes.c_int32 * n)(*[t.shape[0] for t in src]),
+                (ctypes.c_int32 * n)(*[t.shape[1] for t in src]),
+            )
+        n, src, lds, dst, ldd, rows, cols = self._tdesc
+        lib = _native.require_device()
+        _native.check(lib.ap_transpose_batch(n, src, lds, dst, ldd, rows, cols, _stream()))
 
     # -- compute ----------------------------------------------------------------------
 
@@ -191,14 +209,17 @@ class QNetwork:
             raise ValueError(f"expected state dim {self.state_dim}, got {x.shape[1]}")
         return self.forward_device(x).double().cpu().numpy()
 
-    def backward_device(self, acts, dz) -> None:
-        """Gradients into self.grad from dLoss/dz (z = [V, A] head outputs)."""
+    def backward_device(self, acts, dz, dz_t=None) -> None:
+        """Gradients into self.grad from dLoss/dz (z = [V, A] head outputs).
+
+        `dz_t` (optional) is dz^T already materialised (ap_dqn_td_ring writes it)."""
         lib = _native.require_device()
         h = acts[-1]
         b = dz.shape[0]
         # weight gradients as K-major GEMMs (contraction over the batch):
         # dW = h^T dz  ->  A = h^T [in, B], B-operand = dz^T [out, B]
-        gemm(h.t().contiguous(), dz.t().contiguous(), trans_b=True, out=self.grads["wh"], precision=self.precision)
+        gemm(h.t().contiguous(), dz_t if dz_t is not None else dz.t().contiguous(), trans_b=True,
+             out=self.grads["wh"], precision=self.precision)
         _native.check(lib.ap_dqn_colsum(_native.ptr(dz), dz.stride(0), b, dz.shape[1], _native.ptr(self.grads["bh"]),
                                         _stream()))
         # head -> last hidden layer: K = 1 + A is too narrow for the tensor cores;

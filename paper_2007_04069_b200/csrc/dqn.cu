@@ -13,6 +13,7 @@
 //        priority scatter                                        (agent.py:183-226)
 // PER arithmetic is fp64 and follows numpy's evaluation order so the sampled
 // indices match the reference for the same uniforms.
+#include <algorithm>
 #include <cmath>
 
 #include "engine.h"
@@ -113,14 +114,19 @@ __global__ void act_kernel(const float* q, int64_t ldq, const uint8_t* mask, int
 
 // Double-DQN TD error, Huber-weighted loss and the gradient w.r.t. the fused
 // head outputs z = [V, A_0..A_{n-1}] (agent.py:258-299, 114-118).
+// idx != nullptr: the transition fields are read from replay-ring rows idx[b]
+// (fused gather); dz_t != nullptr: also writes dz^T [1 + A, B] (the K-major
+// operand of the head weight-gradient GEMM)
 __global__ void td_kernel(const float* q, const float* online_next, const float* target_next, int64_t ldq,
                           const int32_t* actions, const float* rewards, const uint8_t* done, const uint8_t* next_mask,
                           int64_t ldm, const float* weights, int B, int A, float gamma, float delta, float* dz,
-                          int64_t ldz, float* td_out, float* loss_out) {
+                          int64_t ldz, float* td_out, float* loss_out, const int32_t* idx, float* dz_t,
+                          int64_t ldzt) {
   const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (b >= B) return;
-  const uint8_t* m = next_mask + (int64_t)b * ldm;
+  const int64_t row = idx ? (int64_t)idx[b] : (int64_t)b;
+  const uint8_t* m = next_mask + row * ldm;
   // best next action by the online net over the (safe) next mask
   bool any = false;
   float best = -INFINITY;
@@ -144,9 +150,9 @@ __global__ void td_kernel(const float* q, const float* online_next, const float*
   }
   any = __any_sync(kFull, any);
   const int a_next = any ? best_j : 0;  // empty mask: action 0 is "safe", bootstrap zeroed below
-  const float d = (done[b] || !any) ? 1.0f : 0.0f;
-  const float target = rewards[b] + gamma * (1.0f - d) * target_next[(int64_t)b * ldq + a_next];
-  const int a = actions[b];
+  const float d = (done[row] || !any) ? 1.0f : 0.0f;
+  const float target = rewards[row] + gamma * (1.0f - d) * target_next[(int64_t)b * ldq + a_next];
+  const int a = actions[row];
   const float td = q[(int64_t)b * ldq + a] - target;
   const float w = weights[b];
   const float ad = fabsf(td);
@@ -159,10 +165,40 @@ __global__ void td_kernel(const float* q, const float* online_next, const float*
     else
       v = ((j - 1) == a ? g : 0.0f) - g / (float)A;  // dA_j = dQ_j - sum(dQ)/A
     dz[(int64_t)b * ldz + j] = v;
+    if (dz_t) dz_t[(int64_t)j * ldzt + b] = v;
   }
   if (lane == 0) {
     td_out[b] = td;
     loss_out[b] = w * hub;  // loss = mean over rows, reduced deterministically by the caller
+  }
+}
+
+// Up to 8 matrix transposes in one launch (the transposed weight copies the
+// K-major GEMMs read, refreshed after every Adam step): blockIdx.z = segment,
+// 32x32 tiles staged through shared memory so both sides are coalesced.
+struct TransposeBatch {
+  const float* src[8];
+  float* dst[8];
+  int64_t lds[8], ldd[8];
+  int32_t rows[8], cols[8];
+};
+
+__global__ void transpose_batch_kernel(TransposeBatch tb) {
+  __shared__ float tile[32][33];
+  const int z = blockIdx.z;
+  const int rows = tb.rows[z], cols = tb.cols[z];
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  if (r0 >= rows || c0 >= cols) return;
+  const float* src = tb.src[z];
+  float* dst = tb.dst[z];
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int r = r0 + k, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[k][threadIdx.x] = src[(int64_t)r * tb.lds[z] + c];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int c = c0 + k, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) dst[(int64_t)c * tb.ldd[z] + r] = tile[threadIdx.x][k];
   }
 }
 
@@ -397,7 +433,50 @@ int ap_dqn_td(const float* q, const float* online_next, const float* target_next
   }
   td_kernel<<<(B + 7) / 8, 256, 0, (cudaStream_t)stream>>>(q, online_next, target_next, ldq, actions, rewards, done,
                                                            next_mask, ldm, weights, B, A, gamma, huber_delta, dz, ldz,
-                                                           td, loss);
+                                                           td, loss, nullptr, nullptr, 0);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_transpose_batch(int32_t n, const float* const* src, const int64_t* ld_src, float* const* dst,
+                       const int64_t* ld_dst, const int32_t* rows, const int32_t* cols, void* stream) {
+  if (n < 0 || n > 8 || (n > 0 && (!src || !ld_src || !dst || !ld_dst || !rows || !cols))) {
+    set_error("ap_transpose_batch: 0..8 segments with host descriptor arrays");
+    return AP_ERR_INVALID;
+  }
+  if (n == 0) return AP_OK;
+  TransposeBatch tb{};
+  int max_r = 0, max_c = 0;
+  for (int i = 0; i < n; ++i) {
+    tb.src[i] = src[i];
+    tb.dst[i] = dst[i];
+    tb.lds[i] = ld_src[i];
+    tb.ldd[i] = ld_dst[i];
+    tb.rows[i] = rows[i];
+    tb.cols[i] = cols[i];
+    max_r = std::max(max_r, (int)rows[i]);
+    max_c = std::max(max_c, (int)cols[i]);
+  }
+  const dim3 grid((max_c + 31) / 32, (max_r + 31) / 32, n);
+  transpose_batch_kernel<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(tb);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_dqn_td_ring(const float* q, const float* online_next, const float* target_next, int64_t ldq,
+                   const int32_t* indices, const int32_t* ring_actions, const float* ring_rewards,
+                   const uint8_t* ring_done, const uint8_t* ring_next_mask, int64_t ldm, const float* weights,
+                   int32_t B, int32_t A, float gamma, float huber_delta, float* dz, int64_t ldz, float* dz_t,
+                   int64_t ldzt, float* td, float* loss, void* stream) {
+  if (!q || !online_next || !target_next || !indices || !ring_actions || !ring_rewards || !ring_done ||
+      !ring_next_mask || !weights || !dz || !td || !loss || B < 1 || A < 1) {
+    set_error("ap_dqn_td_ring: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  td_kernel<<<(B + 7) / 8, 256, 0, (cudaStream_t)stream>>>(q, online_next, target_next, ldq, ring_actions,
+                                                           ring_rewards, ring_done, ring_next_mask, ldm, weights, B,
+                                                           A, gamma, huber_delta, dz, ldz, td, loss, indices, dz_t,
+                                                           ldzt);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }

@@ -161,6 +161,8 @@ class VecDqnTrainer:
         self.slot = 0
         self.actions = torch.empty(env.E, dtype=torch.int32, device=dev)
         self.batch = _Batch(config.batch_size, S, A)
+        self.sn = torch.empty((2 * config.batch_size, S), dtype=torch.float32, device=dev)
+        self.dz_t = torch.empty((1 + A, config.batch_size), dtype=torch.float32, device=dev)
         self.idx = torch.empty(config.batch_size, dtype=torch.int32, device=dev)
         self.weights = torch.empty(config.batch_size, dtype=torch.float32, device=dev)
         self.train_steps = 0
@@ -203,20 +205,22 @@ class VecDqnTrainer:
                                             self.seed * 1000003 + self.rank,
                                             P(r["cdf"]), P(self.idx), P(self.weights), P(self.max_prio), P(self.ctl),
                                             _s()))
-        for src, dst in ((r["states"], b.states), (r["next_states"], b.next_states)):
+        # states and next states gathered into one [2B, S] block: the online
+        # network runs once over both (M = 2B), the target net over the second half
+        sn = self.sn
+        for src, dst in ((r["states"], sn[:B]), (r["next_states"], sn[B:])):
             _native.check(lib.ap_gather_rows(P(src), src.stride(0), P(self.idx), B, src.shape[1], P(dst),
                                              dst.stride(0), _s()))
-        il = self.idx.long()
-        actions, rewards, done = r["actions"][il], r["rewards"][il], r["done"][il]
-        masks = r["next_mask"][il]
-        online_next = self.net.forward_device(b.next_states)
-        target_next = self.target.forward_device(b.next_states)
-        q_all, acts = self.net.forward_device(b.states, cache=True)
-        _native.check(lib.ap_dqn_td(P(q_all), P(online_next), P(target_next), q_all.stride(0), P(actions), P(rewards),
-                                    P(done), P(masks), masks.stride(0), P(self.weights), B, self.env.num_actions,
-                                    float(cfg.gamma), float(cfg.huber_delta), P(b.dz), b.dz.stride(0), P(b.td),
-                                    P(b.loss_rows), _s()))
-        self.net.backward_device(acts, b.dz)
+        q2, acts2 = self.net.forward_device(sn, cache=True)
+        target_next = self.target.forward_device(sn[B:])
+        q_all, online_next = q2[:B], q2[B:]
+        acts = [a[:B] for a in acts2]
+        _native.check(lib.ap_dqn_td_ring(P(q_all), P(online_next), P(target_next), q2.stride(0), P(self.idx),
+                                         P(r["actions"]), P(r["rewards"]), P(r["done"]), P(r["next_mask"]),
+                                         r["next_mask"].stride(0), P(self.weights), B, self.env.num_actions,
+                                         float(cfg.gamma), float(cfg.huber_delta), P(b.dz), b.dz.stride(0),
+                                         P(self.dz_t), self.dz_t.stride(0), P(b.td), P(b.loss_rows), _s()))
+        self.net.backward_device(acts, b.dz, self.dz_t)
         if self.pg is not None:  # data-parallel learners: average the Q-gradient over NVLink
             allreduce_mean_(self.net.grad, self.pg)
         opt = self.opt
@@ -226,7 +230,9 @@ class VecDqnTrainer:
         _native.check(lib.ap_per_update_scaled(P(r["priorities"]), P(self.idx), P(b.td), B, float(cfg.per_alpha),
                                                _s()))
         _native.check(lib.ap_vec_ctl_advance(P(self.ctl), 0, self.env.E, self.capacity, _s()))
-        self.launches += 2 + 2 + 9 + 1 + 9 + 1 + 1 + 1
+        # sample, 2 gathers, 2 forwards (4 GEMMs + 2 dueling), td, backward (4 GEMMs, 3 colsum,
+        # head, relu), adam, transpose, priority scatter, ctl (split-K reduces not counted)
+        self.launches += 1 + 2 + 6 + 1 + 9 + 1 + 1 + 1 + 1
 
     def _step_body(self, learn: bool) -> None:
         self.act()
