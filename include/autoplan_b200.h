@@ -260,6 +260,9 @@ int ap_dqn_td_ring(const float* q, const float* online_next, const float* target
 int ap_transpose_batch(int32_t n, const float* const* src, const int64_t* ld_src, float* const* dst,
                        const int64_t* ld_dst, const int32_t* rows, const int32_t* cols, void* stream);
 
+/* ReLU backward in place on dh [B, H] (agent.py:132) that also writes dh^T [H, B]. */
+int ap_dqn_relu_backward_t(float* dh, int64_t lddh, const float* h, int64_t ldh, int32_t B, int32_t H, float* dh_t,
+                           int64_t ldt, void* stream);
 /* dh[i] = 0 where h[i] <= 0 (ReLU backward, agent.py:132). */
 int ap_dqn_relu_backward(float* dh, const float* h, int64_t n, void* stream);
 /* out[c] = sum_r x[r*ld + c] (bias gradients, agent.py:118,134). */

@@ -212,38 +212,69 @@ class QNetwork:
     def backward_device(self, acts, dz, dz_t=None) -> None:
         """Gradients into self.grad from dLoss/dz (z = [V, A] head outputs).
 
-        `dz_t` (optional) is dz^T already materialised (ap_dqn_td_ring writes it)."""
-        lib = _native.require_device()
-        h = acts[-1]
-        b = dz.shape[0]
-        # weight gradients as K-major GEMMs (contraction over the batch):
-        # dW = h^T dz  ->  A = h^T [in, B], B-operand = dz^T [out, B]
-        gemm(h.t().contiguous(), dz_t if dz_t is not None else dz.t().contiguous(), trans_b=True,
-             out=self.grads["wh"], precision=self.precision)
-        _native.check(lib.ap_dqn_colsum(_native.ptr(dz), dz.stride(0), b, dz.shape[1], _native.ptr(self.grads["bh"]),
-                                        _stream()))
-        # head -> last hidden layer: K = 1 + A is too narrow for the tensor cores;
-        # one kernel does dz @ wh^T, the ReLU mask and the transposed copy
+        `dz_t` (optional) is dz^T already materialised (ap_dqn_td_ring writes it).
+
+        Weight gradients are K-major GEMMs contracting over the batch, dW = h^T dz
+        (A = h^T [in, B], B-operand = dz^T [out, B]).  Each layer's activations are
+        transposed into a ones-augmented [in + 1, B] buffer (all layers in one
+        launch), and since b_i follows w_i in the flat buffer the GEMM writes the
+        [in + 1, out] block [dW_i; db_i] at once: the bias gradient is the ones-row
+        product, the column sum of dh (agent.py:118, 134)."""
+        import ctypes
+
         import torch
 
+        lib = _native.require_device()
+        P = _native.ptr
+        L = len(self.hidden)
+        b = dz.shape[0]
+        aug = self._augmented(b)
+        n = L + 1
+        _native.check(lib.ap_transpose_batch(
+            n, (ctypes.c_void_p * n)(*[a.data_ptr() for a in acts]),
+            (ctypes.c_int64 * n)(*[a.stride(0) for a in acts]), (ctypes.c_void_p * n)(*[t.data_ptr() for t in aug]),
+            (ctypes.c_int64 * n)(*[t.stride(0) for t in aug]), (ctypes.c_int32 * n)(*[b] * n),
+            (ctypes.c_int32 * n)(*[a.shape[1] for a in acts]), _stream()))
+        gemm(aug[L], dz_t if dz_t is not None else dz.t().contiguous(), trans_b=True, out=self._grad_block("wh"),
+             precision=self.precision)
+        # head -> last hidden layer: K = 1 + A is too narrow for the tensor cores;
+        # one kernel does dz @ wh^T, the ReLU mask and the transposed copy
+        h = acts[-1]
         wh = self.views["wh"]
         H = wh.shape[0]
         dh = torch.empty((b, H), dtype=torch.float32, device="cuda")
         dh_t = torch.empty((H, b), dtype=torch.float32, device="cuda")
-        _native.check(lib.ap_dqn_head_backward(_native.ptr(dz), dz.stride(0), _native.ptr(wh), wh.stride(0),
-                                               _native.ptr(h), h.stride(0), b, H, dz.shape[1], _native.ptr(dh),
-                                               dh.stride(0), _native.ptr(dh_t), dh_t.stride(0), _stream()))
-        for i in range(len(self.hidden) - 1, -1, -1):
-            if dh_t is None:  # layers below the last: ReLU mask, then the K-major copy
-                _native.check(lib.ap_dqn_relu_backward(_native.ptr(dh), _native.ptr(acts[i + 1]), dh.numel(),
-                                                       _stream()))
-                dh_t = dh.t().contiguous()
-            gemm(acts[i].t().contiguous(), dh_t, trans_b=True, out=self.grads[f"w{i}"], precision=self.precision)
-            dh_t = None
-            _native.check(lib.ap_dqn_colsum(_native.ptr(dh), dh.stride(0), b, dh.shape[1],
-                                            _native.ptr(self.grads[f"b{i}"]), _stream()))
-            if i > 0:
+        _native.check(lib.ap_dqn_head_backward(P(dz), dz.stride(0), P(wh), wh.stride(0), P(h), h.stride(0), b, H,
+                                               dz.shape[1], P(dh), dh.stride(0), P(dh_t), dh_t.stride(0), _stream()))
+        for i in range(L - 1, -1, -1):
+            gemm(aug[i], dh_t, trans_b=True, out=self._grad_block(f"w{i}"), precision=self.precision)
+            if i > 0:  # gradient into layer i-1's output: dh @ W_i^T, ReLU mask, K-major copy
                 dh = gemm(dh, self.views[f"w{i}"], trans_b=True, precision=self.precision)
+                hin = acts[i]
+                dh_t = torch.empty((dh.shape[1], b), dtype=torch.float32, device="cuda")
+                _native.check(lib.ap_dqn_relu_backward_t(P(dh), dh.stride(0), P(hin), hin.stride(0), b, dh.shape[1],
+                                                         P(dh_t), dh_t.stride(0), _stream()))
+
+    def _augmented(self, b: int):
+        """Per-batch-size [in + 1, b] buffers (last row ones) for each layer's input."""
+        import torch
+
+        cache = self.__dict__.setdefault("_aug_cache", {})
+        if b not in cache:
+            ins = [self.state_dim, *self.hidden]
+            bufs = []
+            for w in ins:
+                t = torch.empty((w + 1, b), dtype=torch.float32, device="cuda")
+                t[w].fill_(1.0)
+                bufs.append(t)
+            cache[b] = bufs
+        return cache[b]
+
+    def _grad_block(self, wname: str):
+        """The contiguous [in + 1, out] gradient block of weight `wname` and its bias."""
+        g = self.grads[wname]
+        return self.grad[g.storage_offset() - self.grad.storage_offset():][: (g.shape[0] + 1) * g.shape[1]].view(
+            g.shape[0] + 1, g.shape[1])
 
     def forward_cached(self, states):
         import torch

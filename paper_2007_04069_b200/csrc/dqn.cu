@@ -202,6 +202,21 @@ __global__ void transpose_batch_kernel(TransposeBatch tb) {
   }
 }
 
+// ReLU backward in place on dh [B, H] plus the transposed copy dh_t [H, B]
+// (the K-major operand of the next weight-gradient GEMM)
+__global__ void relu_bwd_t_kernel(float* dh, int64_t lddh, const float* h, int64_t ldh, int B, int H, float* dh_t,
+                                  int64_t ldt) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)B * H) return;
+  const int b = (int)(i / H), j = (int)(i % H);
+  float v = dh[(int64_t)b * lddh + j];
+  if (!(h[(int64_t)b * ldh + j] > 0.0f)) {
+    v = 0.0f;
+    dh[(int64_t)b * lddh + j] = 0.0f;
+  }
+  dh_t[(int64_t)j * ldt + b] = v;
+}
+
 __global__ void relu_bwd_kernel(float* dh, const float* h, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     if (!(h[i] > 0.0f)) dh[i] = 0.0f;
@@ -434,6 +449,19 @@ int ap_dqn_td(const float* q, const float* online_next, const float* target_next
   td_kernel<<<(B + 7) / 8, 256, 0, (cudaStream_t)stream>>>(q, online_next, target_next, ldq, actions, rewards, done,
                                                            next_mask, ldm, weights, B, A, gamma, huber_delta, dz, ldz,
                                                            td, loss, nullptr, nullptr, 0);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_dqn_relu_backward_t(float* dh, int64_t lddh, const float* h, int64_t ldh, int32_t B, int32_t H, float* dh_t,
+                           int64_t ldt, void* stream) {
+  if (!dh || !h || !dh_t || B < 0 || H < 0) {
+    set_error("ap_dqn_relu_backward_t: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  const int64_t n = (int64_t)B * H;
+  if (n == 0) return AP_OK;
+  relu_bwd_t_kernel<<<(int)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(dh, lddh, h, ldh, B, H, dh_t, ldt);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
