@@ -132,6 +132,8 @@ int launch_propagate_fast(const GraphTables* g, const DecisionTables* d, const i
 
 int launch_gemm_v2(const float* A, int64_t lda, int transA, const float* B, int64_t ldb, int transB, float* C,
                    int64_t ldc, int M, int N, int K, const float* bias, int relu, int precision, cudaStream_t stream);
+int launch_gemm_v3(const float* A, int64_t lda, int transA, const float* B, int64_t ldb, int transB, float* C,
+                   int64_t ldc, int M, int N, int K, const float* bias, int relu, int precision, cudaStream_t stream);
 
 int launch_propagate(const GraphTables* g, const DecisionTables* d, const int8_t* seeds, int64_t batch,
                      int64_t seed_stride, int8_t* slots_out, int64_t slots_stride, int8_t* cand_out,

@@ -275,8 +275,12 @@ extern "C" int ap_gemm_tf32(const float* A, int64_t lda, int32_t transA, const f
   // AP_GEMM_V1=1 forces this file's kernel (parity tests run both)
   const char* v1 = std::getenv("AP_GEMM_V1");
   if (!(v1 && v1[0] == '1') && K > 0) {
-    const int rc = apb::launch_gemm_v2(A, lda, transA, B, ldb, transB, C, ldc, M, N, K, bias, relu, precision,
-                                       static_cast<cudaStream_t>(stream));
+    // TMA-fed warp-specialised kernel (gemm_tc3.cu) for TF32 K-major operands
+    int rc = apb::launch_gemm_v3(A, lda, transA, B, ldb, transB, C, ldc, M, N, K, bias, relu, precision,
+                                 static_cast<cudaStream_t>(stream));
+    if (rc != AP_ERR_UNSUPPORTED) return rc;
+    rc = apb::launch_gemm_v2(A, lda, transA, B, ldb, transB, C, ldc, M, N, K, bias, relu, precision,
+                             static_cast<cudaStream_t>(stream));
     if (rc != AP_ERR_UNSUPPORTED) return rc;
   }
   return apb::launch_gemm_tf32(A, lda, transA, B, ldb, transB, C, ldc, M, N, K, bias, relu, precision,

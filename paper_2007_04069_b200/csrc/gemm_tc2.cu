@@ -284,11 +284,15 @@ int launch_gemm_v2(const float* A, int64_t lda, int transA, const float* B, int6
   // stay on the thread-staged kernel until that layout is pinned down.
   if (transA || !transB) return AP_ERR_UNSUPPORTED;
   G2 g{A, lda, 0, B, ldb, 0, C, ldc, M, N, K, bias, relu, 0, nullptr};
-  const int bn = N <= 32 ? 32 : (N <= 64 ? 64 : 64);
+  // dev overrides for tile sweeps: AP_GEMM_BN (32 | 64), AP_GEMM_SPLITS
+  static const int env_bn = std::getenv("AP_GEMM_BN") ? std::atoi(std::getenv("AP_GEMM_BN")) : 0;
+  static const int env_splits = std::getenv("AP_GEMM_SPLITS") ? std::atoi(std::getenv("AP_GEMM_SPLITS")) : 0;
+  const int bn = env_bn == 32 || env_bn == 64 ? env_bn : (N <= 32 ? 32 : 64);
   const int mt = (M + BM - 1) / BM, nt = (N + bn - 1) / bn;
   const int nk = (K + BK - 1) / BK;
   int splits = 1;
   if (mt * nt < 120 && nk >= 4) splits = std::min(std::min(nk / 2, 16), std::max(1, 148 / (mt * nt)));
+  if (env_splits > 0) splits = std::min(env_splits, nk);
   g.kps = (nk + splits - 1) / splits;
   splits = (nk + g.kps - 1) / g.kps;
   if (splits > 1) {

@@ -1,0 +1,286 @@
+// tcgen05 GEMM v3: TMA-fed, warp-specialised, 128-byte swizzle (TF32, K-major).
+//
+// C[M, N] = A[M, K] * B[N, K]^T (+ bias[N]) (ReLU), fp32 in / fp32 out, TF32
+// tensor-core math (the throughput-mode Q-network GEMMs; 3xTF32 stays on v2).
+//   * operand tiles are moved by TMA (cp.async.bulk.tensor.2d) with
+//     CU_TENSOR_MAP_SWIZZLE_128B: box = 32 fp32 (one 128-byte row) x rows, which
+//     is exactly the canonical K-major SW128 UMMA atom (8 rows x 128 B, SBO 1024);
+//     out-of-bounds rows / k are zero-filled by the TMA unit;
+//   * a STAGES-deep ring with full (TMA complete_tx) and empty (tcgen05.commit)
+//     mbarriers: thread 0 of warp 0 produces, thread 0 of warp 1 issues the
+//     MMAs (4 x K=8 per 32-wide k slice, the descriptor start advanced by 32 B
+//     inside the swizzled row), accumulators in TMEM;
+//   * epilogue: all 4 warps tcgen05.ld their 32 TMEM lanes, add bias / ReLU and
+//     store; with split-K the partials go to a workspace and a fixed-order
+//     reduce kernel sums them (bit-reproducible).
+// Tensor maps are encoded per call with cuTensorMapEncodeTiled obtained through
+// cudaGetDriverEntryPoint (no libcuda link dependency).
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "engine.h"
+
+namespace apb {
+namespace {
+
+constexpr int BM3 = 128;
+constexpr int BK3 = 32;  // fp32 elements = 128 bytes = one swizzle row
+
+struct G3 {
+  float* C;
+  int64_t ldc;
+  int M, N, K;
+  const float* bias;
+  int relu;
+  int kps;      // k slices per split
+  float* work;  // [splits, M, N] partials when split-K
+};
+
+__device__ __forceinline__ uint32_t sa3(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+  // start >> 4 | LBO field 1 (unused for swizzled K-major) | SBO 1024 B >> 4 |
+  // version 1 (bit 46) | layout SWIZZLE_128B (2 at bits 61-63)
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n"
+      "W3_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+      "@!done bra W3_%=;\n\t}\n" ::"r"(mbar),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(mbar)
+      : "memory");
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(128) gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                      const __grid_constant__ CUtensorMap tmB, G3 g) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], done;
+  __shared__ uint32_t tmem_slot;
+  constexpr int A_BYTES = BM3 * BK3 * 4;
+  constexpr int B_BYTES = BN * BK3 * 4;
+  constexpr int STAGE = A_BYTES + B_BYTES;
+  constexpr int COLS = BN < 32 ? 32 : BN;
+  // 1024-byte aligned stage base (SWIZZLE_128B atoms)
+  const uint32_t base = (sa3(smem_raw) + 1023u) & ~1023u;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM3, n0 = blockIdx.y * BN;
+  const int nk_total = (g.K + BK3 - 1) / BK3;
+  const int kb = blockIdx.z * g.kps;
+  const int nk = max(0, min(g.kps, nk_total - kb));
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa3(&tmem_slot)),
+                 "r"(COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < STAGES; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa3(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa3(&empty[s])));
+    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa3(&done)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_slot;
+
+  if (threadIdx.x == 0) {
+    // TMA producer
+    for (int it = 0; it < nk; ++it) {
+      const int s = it % STAGES;
+      if (it >= STAGES) mbar_wait(sa3(&empty[s]), ((it / STAGES) - 1) & 1);
+      const uint32_t st = base + s * STAGE;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa3(&full[s])), "r"(STAGE)
+                   : "memory");
+      const int kc = (kb + it) * BK3;
+      tma_load_2d(st, &tmA, kc, m0, sa3(&full[s]));
+      tma_load_2d(st + A_BYTES, &tmB, kc, n0, sa3(&full[s]));
+    }
+  } else if (threadIdx.x == 32) {
+    // MMA issuer
+    const uint32_t idesc =
+        (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM3 >> 4) << 24);
+    for (int it = 0; it < nk; ++it) {
+      const int s = it % STAGES;
+      mbar_wait(sa3(&full[s]), (it / STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t a = base + s * STAGE, b = a + A_BYTES;
+#pragma unroll
+      for (int ks = 0; ks < BK3 / 8; ++ks) {
+        const uint64_t da = desc_sw128(a + ks * 32), db = desc_sw128(b + ks * 32);
+        const uint32_t acc = (it | ks) != 0;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+            "l"(da), "l"(db), "r"(idesc), "r"(acc));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       sa3(&empty[s]))
+                   : "memory");
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sa3(&done))
+                 : "memory");
+  }
+  __syncwarp();
+  if (nk > 0) mbar_wait(sa3(&done), 0);
+  asm volatile("tcgen05.fence::after_thread_sync;");
+
+  const int row = m0 + warp * 32 + lane;
+  float* out = g.work ? g.work + (int64_t)blockIdx.z * g.M * g.N : g.C;
+  const int64_t ld = g.work ? g.N : g.ldc;
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN; c0 += 16) {
+    uint32_t v[16];
+    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (row < g.M) {
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        const int col = n0 + c0 + t;
+        if (col < g.N) {
+          float x = nk > 0 ? __uint_as_float(v[t]) : 0.0f;
+          if (!g.work) {
+            if (g.bias) x += g.bias[col];
+            if (g.relu) x = fmaxf(x, 0.0f);
+          }
+          out[(int64_t)row * ld + col] = x;
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(COLS));
+}
+
+__global__ void splitk_reduce3_kernel(const float* work, int splits, int M, int N, float* C, int64_t ldc,
+                                      const float* bias, int relu) {
+  const int64_t total = (int64_t)M * N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    float acc = 0.0f;
+    for (int s = 0; s < splits; ++s) acc += work[(int64_t)s * total + i];  // fixed order: reproducible
+    const int r = (int)(i / N), c = (int)(i % N);
+    if (bias) acc += bias[c];
+    if (relu) acc = fmaxf(acc, 0.0f);
+    C[(int64_t)r * ldc + c] = acc;
+  }
+}
+
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encode_fn() {
+  static EncodeTiled fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiled>(p);
+  }
+  return fn;
+}
+
+// row-major [rows, K] fp32 (K contiguous, ld elements), box 32 x box_rows, SW128
+bool make_map(CUtensorMap* m, const float* ptr, int64_t rows, int64_t K, int64_t ld, int box_rows) {
+  EncodeTiled fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)BK3, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN, int STAGES>
+int run3(const CUtensorMap& ma, const CUtensorMap& mb, const G3& g, dim3 grid, cudaStream_t s) {
+  constexpr int SMEM = (BM3 + BN) * BK3 * 4 * STAGES + 1024;
+  auto k = gemm_v3_kernel<BN, STAGES>;
+  static bool configured = false;
+  if (!configured) {
+    AP_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    configured = true;
+  }
+  k<<<grid, 128, SMEM, s>>>(ma, mb, g);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+float* g_work3 = nullptr;
+size_t g_work3_bytes = 0;
+
+}  // namespace
+
+// TF32 only, both operands K-major (A [M, K], B [N, K]); AP_ERR_UNSUPPORTED otherwise.
+int launch_gemm_v3(const float* A, int64_t lda, int transA, const float* B, int64_t ldb, int transB, float* C,
+                   int64_t ldc, int M, int N, int K, const float* bias, int relu, int precision, cudaStream_t stream) {
+  if (precision != 1 || transA || !transB || std::getenv("AP_GEMM_NO_TMA")) return AP_ERR_UNSUPPORTED;
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (!al(A) || !al(B) || lda % 4 || ldb % 4 || M < 1 || N < 1 || K < 1) return AP_ERR_UNSUPPORTED;
+  const int bn = N <= 32 ? 32 : 64;
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, A, M, K, lda, BM3) || !make_map(&mb, B, N, K, ldb, bn)) return AP_ERR_UNSUPPORTED;
+  G3 g{C, ldc, M, N, K, bias, relu, 0, nullptr};
+  const int mt = (M + BM3 - 1) / BM3, nt = (N + bn - 1) / bn;
+  const int nk = (K + BK3 - 1) / BK3;
+  int splits = 1;
+  if (mt * nt < 120 && nk >= 4) splits = std::min(std::min(nk / 2, 16), std::max(1, 148 / (mt * nt)));
+  g.kps = (nk + splits - 1) / splits;
+  splits = (nk + g.kps - 1) / g.kps;
+  if (splits > 1) {
+    const size_t need = (size_t)splits * M * N * sizeof(float);
+    if (need > g_work3_bytes) {
+      // a captured graph may hold the old workspace: never free it, never grow mid-capture
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      AP_CUDA_CHECK(cudaStreamIsCapturing(stream, &cs));
+      if (cs != cudaStreamCaptureStatusNone) {
+        set_error("gemm: split-K workspace must grow during graph capture; run the shapes once before capturing");
+        return AP_ERR_INVALID;
+      }
+      float* fresh = nullptr;
+      AP_CUDA_CHECK(cudaMalloc(&fresh, need));
+      g_work3 = fresh;
+      g_work3_bytes = need;
+    }
+    g.work = g_work3;
+  }
+  const dim3 grid(mt, nt, splits);
+  const int rc = bn == 32 ? run3<32, 6>(ma, mb, g, grid, stream) : run3<64, 6>(ma, mb, g, grid, stream);
+  if (rc != AP_OK || splits == 1) return rc;
+  const int64_t total = (int64_t)M * N;
+  splitk_reduce3_kernel<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, stream>>>(
+      g_work3, splits, M, N, C, ldc, bias, relu);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+}  // namespace apb

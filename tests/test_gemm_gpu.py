@@ -62,6 +62,24 @@ def test_pipelined_kernel_matches_simple_kernel(cuda, m, n, k, ta, tb, monkeypat
         assert (slow.double() - r).abs().max().item() < tol
 
 
+@pytest.mark.parametrize("m,n,k", SHAPES + [(128, 256, 1060), (1061, 256, 64), (257, 3, 64), (5, 7, 9),
+                                            (4096, 3, 256)])
+def test_tma_kernel_matches_cp_async_kernel(cuda, m, n, k, monkeypatch):
+    """TMA-fed SW128 kernel (gemm_tc3.cu, TF32, K-major) vs the cp.async kernel and fp64."""
+    g = torch.Generator(device="cuda").manual_seed(3 * m + n + 7 * k)
+    a = torch.randn((m, k), device="cuda", generator=g)
+    b = torch.randn((n, k), device="cuda", generator=g)
+    bias = torch.randn(n, device="cuda", generator=g)
+    tma = gemm(a, b, trans_b=True, bias=bias, relu=True, precision=1)
+    monkeypatch.setenv("AP_GEMM_NO_TMA", "1")
+    cpa = gemm(a, b, trans_b=True, bias=bias, relu=True, precision=1)
+    monkeypatch.delenv("AP_GEMM_NO_TMA")
+    r = ref(a, b, False, True, bias, True)
+    scale = r.abs().max().item()
+    assert (tma.double() - r).abs().max().item() < 5e-3 * scale
+    assert (tma - cpa).abs().max().item() <= 1e-5 * scale
+
+
 @pytest.mark.parametrize("m,n,k", SHAPES[:4])
 def test_gemm_tf32_is_tf32_accurate(cuda, m, n, k):
     g = torch.Generator(device="cuda").manual_seed(1)
