@@ -484,13 +484,24 @@ def bench_dqn_vec(args, g, world, rank):
     torch.cuda.synchronize()
     ms = _max_over_ranks(s.elapsed_time(e), world)
     # tensor-pipe figure for the batched act forward (the dominant GEMMs)
+    # (10 forwards captured in a CUDA graph: the kernels, not the Python launch path)
     x = env.cur_state
     for _ in range(3):
         tr.net.forward_device(x)
+    torch.cuda.synchronize()
+    fwd_graph = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(fwd_graph, stream=side):
+            for _ in range(10):
+                tr.net.forward_device(x)
+    torch.cuda.current_stream().wait_stream(side)
+    fwd_graph.replay()
+    torch.cuda.synchronize()
     s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s2.record()
-    for _ in range(10):
-        tr.net.forward_device(x)
+    fwd_graph.replay()
     e2.record()
     torch.cuda.synchronize()
     fwd_s = s2.elapsed_time(e2) / 1e3 / 10
