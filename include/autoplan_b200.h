@@ -260,6 +260,11 @@ int ap_dqn_td_ring(const float* q, const float* online_next, const float* target
 int ap_transpose_batch(int32_t n, const float* const* src, const int64_t* ld_src, float* const* dst,
                        const int64_t* ld_dst, const int32_t* rows, const int32_t* cols, void* stream);
 
+/* Dueling head forward for 1 + A <= 8 outputs (agent.py:99-109): q = V + A - mean(A)
+ * with [V, A] = h @ wh + bh; wh_t is wh transposed ([1 + A, H], row stride ldw).
+ * AP_ERR_UNSUPPORTED for wider heads (GEMM + ap_dqn_dueling). */
+int ap_dqn_head_forward(const float* h, int64_t ldh, const float* wh_t, int64_t ldw, const float* bh, int32_t B,
+                        int32_t H, int32_t A1, float* q, int64_t ldq, void* stream);
 /* ReLU backward in place on dh [B, H] (agent.py:132) that also writes dh^T [H, B]. */
 int ap_dqn_relu_backward_t(float* dh, int64_t lddh, const float* h, int64_t ldh, int32_t B, int32_t H, float* dh_t,
                            int64_t ldt, void* stream);

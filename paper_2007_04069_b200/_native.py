@@ -121,6 +121,7 @@ SIGNATURES: dict[str, tuple] = {
                                  ctypes.c_float, _VP, _I64, _VP, _VP, _VP]),
     "ap_dqn_td_ring": (ctypes.c_int, [_VP, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _I64, _VP, _I32, _I32, _F32, _F32,
                                       _VP, _I64, _VP, _I64, _VP, _VP, _VP]),
+    "ap_dqn_head_forward": (ctypes.c_int, [_VP, _I64, _VP, _I64, _VP, _I32, _I32, _I32, _VP, _I64, _VP]),
     "ap_dqn_relu_backward_t": (ctypes.c_int, [_VP, _I64, _VP, _I64, _I32, _I32, _VP, _I64, _VP]),
     "ap_transpose_batch": (ctypes.c_int, [_I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "ap_dqn_relu_backward": (ctypes.c_int, [_VP, _VP, _I64, _VP]),

@@ -193,12 +193,18 @@ class QNetwork:
         for i in range(len(self.hidden)):
             h = gemm(h, self.wt[f"w{i}"], trans_b=True, bias=self.views[f"b{i}"], relu=True, precision=self.precision)
             acts.append(h)
-        z = gemm(h, self.wt["wh"], trans_b=True, bias=self.views["bh"], precision=self.precision)
         b = x.shape[0]
         q = torch.empty((b, self.num_actions), dtype=torch.float32, device="cuda")
         lib = _native.require_device()
-        _native.check(lib.ap_dqn_dueling(_native.ptr(z), z.stride(0), _native.ptr(q), q.stride(0), b,
-                                         self.num_actions, _stream()))
+        wt = self.wt["wh"]
+        if 1 + self.num_actions <= 8:  # narrow head: dot products + dueling in one warp-per-row kernel
+            _native.check(lib.ap_dqn_head_forward(_native.ptr(h), h.stride(0), _native.ptr(wt), wt.stride(0),
+                                                  _native.ptr(self.views["bh"]), b, h.shape[1],
+                                                  1 + self.num_actions, _native.ptr(q), q.stride(0), _stream()))
+        else:
+            z = gemm(h, wt, trans_b=True, bias=self.views["bh"], precision=self.precision)
+            _native.check(lib.ap_dqn_dueling(_native.ptr(z), z.stride(0), _native.ptr(q), q.stride(0), b,
+                                             self.num_actions, _stream()))
         return (q, acts) if cache else q
 
     def forward(self, states) -> np.ndarray:

@@ -173,6 +173,41 @@ __global__ void td_kernel(const float* q, const float* online_next, const float*
   }
 }
 
+// Dueling head forward for narrow heads (1 + A <= kHeadMax outputs): one warp
+// per row computes z = h @ wh + bh (wh given transposed, [1 + A, H]) with the
+// lanes splitting H, then Q = V + A - mean(A) (agent.py:99-109).
+constexpr int kHeadMax = 8;
+
+template <int A1>
+__global__ void head_forward_kernel(const float* h, int64_t ldh, const float* wht, int64_t ldw, const float* bh,
+                                    int B, int H, float* q, int64_t ldq) {
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= B) return;
+  float z[A1];
+#pragma unroll
+  for (int j = 0; j < A1; ++j) z[j] = 0.0f;
+  const float* hr = h + (int64_t)b * ldh;
+  for (int k = lane; k < H; k += 32) {
+    const float x = hr[k];
+#pragma unroll
+    for (int j = 0; j < A1; ++j) z[j] = fmaf(x, wht[(int64_t)j * ldw + k], z[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < A1; ++j)
+    for (int o = 16; o; o >>= 1) z[j] += __shfl_xor_sync(kFull, z[j], o);
+  if (lane == 0) {
+    float mean = 0.0f;
+#pragma unroll
+    for (int j = 0; j < A1; ++j) z[j] += bh[j];
+#pragma unroll
+    for (int j = 1; j < A1; ++j) mean += z[j];
+    mean /= (float)(A1 - 1);
+#pragma unroll
+    for (int j = 1; j < A1; ++j) q[(int64_t)b * ldq + (j - 1)] = z[0] + z[j] - mean;
+  }
+}
+
 // Up to 8 matrix transposes in one launch (the transposed weight copies the
 // K-major GEMMs read, refreshed after every Adam step): blockIdx.z = segment,
 // 32x32 tiles staged through shared memory so both sides are coalesced.
@@ -449,6 +484,32 @@ int ap_dqn_td(const float* q, const float* online_next, const float* target_next
   td_kernel<<<(B + 7) / 8, 256, 0, (cudaStream_t)stream>>>(q, online_next, target_next, ldq, actions, rewards, done,
                                                            next_mask, ldm, weights, B, A, gamma, huber_delta, dz, ldz,
                                                            td, loss, nullptr, nullptr, 0);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_dqn_head_forward(const float* h, int64_t ldh, const float* wh_t, int64_t ldw, const float* bh, int32_t B,
+                        int32_t H, int32_t A1, float* q, int64_t ldq, void* stream) {
+  if (!h || !wh_t || !bh || !q || B < 0 || H < 1 || A1 < 2) {
+    set_error("ap_dqn_head_forward: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  if (A1 > kHeadMax) {
+    set_error("ap_dqn_head_forward: head wider than 8 outputs (use the GEMM + ap_dqn_dueling path)");
+    return AP_ERR_UNSUPPORTED;
+  }
+  if (B == 0) return AP_OK;
+  const dim3 grid((B + 7) / 8), block(256);
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (A1) {
+    case 2: head_forward_kernel<2><<<grid, block, 0, s>>>(h, ldh, wh_t, ldw, bh, B, H, q, ldq); break;
+    case 3: head_forward_kernel<3><<<grid, block, 0, s>>>(h, ldh, wh_t, ldw, bh, B, H, q, ldq); break;
+    case 4: head_forward_kernel<4><<<grid, block, 0, s>>>(h, ldh, wh_t, ldw, bh, B, H, q, ldq); break;
+    case 5: head_forward_kernel<5><<<grid, block, 0, s>>>(h, ldh, wh_t, ldw, bh, B, H, q, ldq); break;
+    case 6: head_forward_kernel<6><<<grid, block, 0, s>>>(h, ldh, wh_t, ldw, bh, B, H, q, ldq); break;
+    case 7: head_forward_kernel<7><<<grid, block, 0, s>>>(h, ldh, wh_t, ldw, bh, B, H, q, ldq); break;
+    default: head_forward_kernel<8><<<grid, block, 0, s>>>(h, ldh, wh_t, ldw, bh, B, H, q, ldq); break;
+  }
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
