@@ -285,10 +285,16 @@ __global__ void colsum_kernel(const float* x, int64_t ld, int rows, int cols, fl
 // ctl != nullptr: bias corrections from step t = ctl[AP_CTL_TRAIN] + 1
 __global__ void adam_kernel(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
                             float eps, float c1, float c2, const int64_t* ctl) {
-  if (ctl) {
-    const double t = (double)(ctl[AP_CTL_TRAIN] + 1);
-    c1 = (float)(1.0 - pow((double)b1, t));
-    c2 = (float)(1.0 - pow((double)b2, t));
+  if (ctl) {  // bias corrections once per block, not per thread (two fp64 pow)
+    __shared__ float s_c[2];
+    if (threadIdx.x == 0) {
+      const double t = (double)(ctl[AP_CTL_TRAIN] + 1);
+      s_c[0] = (float)(1.0 - pow((double)b1, t));
+      s_c[1] = (float)(1.0 - pow((double)b2, t));
+    }
+    __syncthreads();
+    c1 = s_c[0];
+    c2 = s_c[1];
   }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const float gi = g[i];

@@ -35,7 +35,8 @@ struct G3 {
   const float* bias;
   int relu;
   int kps;      // k slices per split
-  float* work;  // [splits, M, N] partials when split-K
+  float* work;  // [splits, M, N] partials when split-K through global memory
+  int cluster;  // split-K CTAs of a tile form one cluster: reduce through DSMEM
 };
 
 __device__ __forceinline__ uint32_t sa3(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -144,6 +145,57 @@ __global__ void __launch_bounds__(128) gemm_v3_kernel(const __grid_constant__ CU
   if (nk > 0) mbar_wait(sa3(&done), 0);
   asm volatile("tcgen05.fence::after_thread_sync;");
 
+  if (g.cluster) {
+    // split-K through distributed shared memory: every CTA of the cluster (the
+    // splits of one output tile) parks its partial tile in its own shared
+    // memory (the drained stage ring, rows padded to BN + 1 floats), then CTA
+    // r sums row slice r over all splits in split order and stores C
+    constexpr int LDP = BN + 1;
+    float* part = reinterpret_cast<float*>(smem_raw + (base - sa3(smem_raw)));
+    const int lrow = warp * 32 + lane;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      uint32_t v[16];
+      const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int t = 0; t < 16; ++t) part[lrow * LDP + c0 + t] = nk > 0 ? __uint_as_float(v[t]) : 0.0f;
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    const int S = (int)gridDim.z, rank = (int)blockIdx.z;
+    const int rows_per = (BM3 + S - 1) / S;
+    const int r_lo = rank * rows_per, r_hi = min(BM3, r_lo + rows_per);
+    const uint32_t local = sa3(part);
+    for (int e = threadIdx.x; e < (r_hi - r_lo) * BN; e += blockDim.x) {
+      const int r = r_lo + e / BN, c = e % BN;
+      const int grow = m0 + r, gcol = n0 + c;
+      if (grow >= g.M || gcol >= g.N) continue;
+      const uint32_t off = local + (uint32_t)(r * LDP + c) * 4u;
+      float acc = 0.0f;
+      for (int s = 0; s < S; ++s) {
+        uint32_t ra;
+        float x;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(off), "r"(s));
+        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(x) : "r"(ra) : "memory");
+        acc += x;
+      }
+      if (g.bias) acc += g.bias[gcol];
+      if (g.relu) acc = fmaxf(acc, 0.0f);
+      g.C[(int64_t)grow * g.ldc + gcol] = acc;
+    }
+    // no CTA may leave while a peer still reads its shared memory
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(COLS));
+    return;
+  }
+
   const int row = m0 + warp * 32 + lane;
   float* out = g.work ? g.work + (int64_t)blockIdx.z * g.M * g.N : g.C;
   const int64_t ld = g.work ? g.N : g.ldc;
@@ -228,10 +280,28 @@ int run3(const CUtensorMap& ma, const CUtensorMap& mb, const G3& g, dim3 grid, c
   static bool configured = false;
   if (!configured) {
     AP_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+    // split-K clusters of up to 16 CTAs (beyond the portable 8)
+    AP_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     configured = true;
   }
-  k<<<grid, 128, SMEM, s>>>(ma, mb, g);
-  AP_CUDA_CHECK(cudaGetLastError());
+  if (!g.cluster) {
+    k<<<grid, 128, SMEM, s>>>(ma, mb, g);
+    AP_CUDA_CHECK(cudaGetLastError());
+    return AP_OK;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = grid.z;  // the split-K CTAs of one tile
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  AP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k, ma, mb, g));
   return AP_OK;
 }
 
@@ -249,14 +319,20 @@ int launch_gemm_v3(const float* A, int64_t lda, int transA, const float* B, int6
   const int bn = N <= 32 ? 32 : 64;
   CUtensorMap ma, mb;
   if (!make_map(&ma, A, M, K, lda, BM3) || !make_map(&mb, B, N, K, ldb, bn)) return AP_ERR_UNSUPPORTED;
-  G3 g{C, ldc, M, N, K, bias, relu, 0, nullptr};
+  G3 g{C, ldc, M, N, K, bias, relu, 0, nullptr, 0};
   const int mt = (M + BM3 - 1) / BM3, nt = (N + bn - 1) / bn;
   const int nk = (K + BK3 - 1) / BK3;
+  // split-K for grids that would leave SMs idle; the splits of a tile reduce
+  // inside one thread-block cluster (<= 16 CTAs, non-portable size) through
+  // DSMEM: no workspace, no extra launch (AP_GEMM_NO_CLUSTER=1: workspace path)
+  static const bool no_cluster = std::getenv("AP_GEMM_NO_CLUSTER") != nullptr;
+  static const int max_split = std::getenv("AP_GEMM_MAX_SPLIT") ? std::atoi(std::getenv("AP_GEMM_MAX_SPLIT")) : 16;
   int splits = 1;
-  if (mt * nt < 120 && nk >= 4) splits = std::min(std::min(nk / 2, 16), std::max(1, 148 / (mt * nt)));
+  if (mt * nt < 120 && nk >= 4) splits = std::min(std::min(nk / 2, max_split), std::max(1, 148 / (mt * nt)));
   g.kps = (nk + splits - 1) / splits;
   splits = (nk + g.kps - 1) / g.kps;
-  if (splits > 1) {
+  if (splits > 1 && !no_cluster) g.cluster = 1;
+  if (splits > 1 && !g.cluster) {
     const size_t need = (size_t)splits * M * N * sizeof(float);
     if (need > g_work3_bytes) {
       // a captured graph may hold the old workspace: never free it, never grow mid-capture
@@ -275,7 +351,7 @@ int launch_gemm_v3(const float* A, int64_t lda, int transA, const float* B, int6
   }
   const dim3 grid(mt, nt, splits);
   const int rc = bn == 32 ? run3<32, 6>(ma, mb, g, grid, stream) : run3<64, 6>(ma, mb, g, grid, stream);
-  if (rc != AP_OK || splits == 1) return rc;
+  if (rc != AP_OK || splits == 1 || g.cluster) return rc;
   const int64_t total = (int64_t)M * N;
   splitk_reduce3_kernel<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, stream>>>(
       g_work3, splits, M, N, C, ldc, bias, relu);
