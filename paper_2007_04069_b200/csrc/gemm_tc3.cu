@@ -325,8 +325,8 @@ int launch_gemm_v3(const float* A, int64_t lda, int transA, const float* B, int6
   // split-K for grids that would leave SMs idle; the splits of a tile reduce
   // inside one thread-block cluster (<= 16 CTAs, non-portable size) through
   // DSMEM: no workspace, no extra launch (AP_GEMM_NO_CLUSTER=1: workspace path)
-  static const bool no_cluster = std::getenv("AP_GEMM_NO_CLUSTER") != nullptr;
-  static const int max_split = std::getenv("AP_GEMM_MAX_SPLIT") ? std::atoi(std::getenv("AP_GEMM_MAX_SPLIT")) : 16;
+  const bool no_cluster = std::getenv("AP_GEMM_NO_CLUSTER") != nullptr;
+  const int max_split = std::getenv("AP_GEMM_MAX_SPLIT") ? std::atoi(std::getenv("AP_GEMM_MAX_SPLIT")) : 16;
   int splits = 1;
   if (mt * nt < 120 && nk >= 4) splits = std::min(std::min(nk / 2, max_split), std::max(1, 148 / (mt * nt)));
   g.kps = (nk + splits - 1) / splits;

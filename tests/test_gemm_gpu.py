@@ -80,6 +80,23 @@ def test_tma_kernel_matches_cp_async_kernel(cuda, m, n, k, monkeypatch):
     assert (tma - cpa).abs().max().item() <= 1e-5 * scale
 
 
+@pytest.mark.parametrize("m,n,k", [(64, 256, 1060), (128, 256, 1060), (64, 256, 256), (200, 40, 777)])
+def test_cluster_splitk_matches_workspace_splitk(cuda, m, n, k, monkeypatch):
+    """Split-K reduced through DSMEM inside a thread-block cluster == split-K through a
+    global workspace + reduce kernel (same splits, same fixed order: bit-identical)."""
+    g = torch.Generator(device="cuda").manual_seed(m * n + k)
+    a = torch.randn((m, k), device="cuda", generator=g)
+    b = torch.randn((n, k), device="cuda", generator=g)
+    bias = torch.randn(n, device="cuda", generator=g)
+    clu = gemm(a, b, trans_b=True, bias=bias, relu=True, precision=1)
+    monkeypatch.setenv("AP_GEMM_NO_CLUSTER", "1")
+    monkeypatch.setenv("AP_GEMM_MAX_SPLIT", "16")
+    ws = gemm(a, b, trans_b=True, bias=bias, relu=True, precision=1)
+    r = ref(a, b, False, True, bias, True)
+    assert (clu.double() - r).abs().max().item() < 5e-3 * r.abs().max().item()
+    assert torch.equal(clu, ws)
+
+
 @pytest.mark.parametrize("m,n,k", SHAPES[:4])
 def test_gemm_tf32_is_tf32_accurate(cuda, m, n, k):
     g = torch.Generator(device="cuda").manual_seed(1)
