@@ -181,6 +181,45 @@ def test_generic_kernel_matches_reference(cuda, name, monkeypatch):
     test_batch_kernel_matches_reference(cuda, name)
 
 
+def _wide_graph(blocks: int):
+    """`blocks` independent x_i @ w_i @ v_i chains with pairwise-distinct extents: 4 link
+    classes and 4 candidate dims per block, nothing links across blocks."""
+    from paper_2007_04069_b200.graphs import GraphWriter
+
+    w = GraphWriter()
+    for i in range(blocks):
+        a, b, c, d = 2 + 4 * i, 3 + 4 * i, 4 + 4 * i, 5 + 4 * i
+        x = w.param(f"x{i}", (a, b), trainable=False)
+        wi = w.param(f"w{i}", (b, c))
+        vi = w.param(f"v{i}", (c, d))
+        h = w.op(f"h{i}", "dot", (a, c), [x, wi])
+        w.op(f"y{i}", "dot", (a, d), [h, vi])
+    return w.graph()
+
+
+@pytest.mark.parametrize("blocks", [80, 1100])
+def test_beyond_fast_kernel_limits_matches_oracle(cuda, blocks):
+    """> 255 link classes (80 blocks: 320 classes) and > 4096 candidate dims (1100 blocks:
+    4400 dims): the engine takes the generic kernel and still matches the C oracle."""
+    g = _wide_graph(blocks)
+    dims = decision_dims(g, g.trainable_variables)
+    n = len(dims)
+    rng = np.random.default_rng(blocks)
+    seeds = np.concatenate([
+        random_prefix_seeds(rng, n, 48, rng.permutation(n)),
+        np.where(rng.random((16, n)) < 0.01, rng.integers(0, 3, size=(16, n)), -1).astype(np.int8),
+    ])
+    eng = PropagationEngine(g, dims)
+    out = eng.run_batch(torch.from_numpy(seeds), want_slots=True)
+    flat = g.flat()
+    cand_slots = np.array([flat.slot_offset[d.instruction_id] + d.dim for d in dims])
+    st, oc, _ = oracle.propagate_batch(flat, cand_slots, seeds, cand_slots)
+    np.testing.assert_array_equal(out["outcome"].cpu().numpy(), oc)
+    ok = oc != 2
+    np.testing.assert_array_equal(out["slots"].cpu().numpy()[ok], st[ok])
+    assert ok.sum() > 0
+
+
 def test_properties_at_scale(cuda):
     """Size-independent properties: idempotence, monotonicity, order independence."""
     g = graphs.bert48()
