@@ -22,7 +22,10 @@ int cuda_fail(cudaError_t err, const char* what) {
 
 static void release_graph(GraphTables* t) {
   t->d_slot_class.release();
-  t->d_class_forced.release();
+  t->d_forced_words.release();
+  if (t->d_scratch) cudaFree(t->d_scratch);
+  t->d_scratch = nullptr;
+  t->scratch_words = 0;
   t->d_imp_offset.release();
   t->d_imp_target.release();
   t->d_program.release();

@@ -59,7 +59,8 @@ struct GraphTables {
   std::vector<uint8_t> slot_forced;   // [S] directly forced replicated
   std::vector<uint8_t> class_forced;  // [C]
   std::vector<int32_t> imp_offset;    // [C+1]
-  std::vector<uint16_t> imp_target;   // [T]
+  std::vector<int32_t> imp_target;    // [T]
+  std::vector<uint32_t> forced_words; // [ceil(C/32)] forced-replicated class bitset (generic kernel)
   std::vector<int32_t> program;       // trace program (reference sweep order)
   std::vector<int32_t> forced_list;   // forced slots in reference order
 
@@ -77,10 +78,13 @@ struct GraphTables {
   DevBuf<uint8_t> d_slot_cls8;
   DevBuf<uint32_t> d_imp_bits;
   DevBuf<uint32_t> d_forced_bits;
-  DevBuf<uint16_t> d_slot_class;
-  DevBuf<uint8_t> d_class_forced;
+  DevBuf<int32_t> d_slot_class;
+  DevBuf<uint32_t> d_forced_words;
   DevBuf<int32_t> d_imp_offset;
-  DevBuf<uint16_t> d_imp_target;
+  DevBuf<int32_t> d_imp_target;
+  // generic kernel: global per-warp P/R bitset scratch when shared memory is too small (grow-only)
+  mutable uint32_t* d_scratch = nullptr;
+  mutable int64_t scratch_words = 0;
   DevBuf<int32_t> d_program;
   DevBuf<int32_t> d_forced_list;
   DevBuf<int64_t> d_slot_base;
@@ -92,7 +96,7 @@ struct GraphTables {
 struct DecisionTables {
   int32_t n = 0;
   std::vector<int64_t> slots;
-  std::vector<uint16_t> dec_class;
+  std::vector<int32_t> dec_class;
   std::vector<uint8_t> dec_flags;     // bit0 candidate, bit1 slot directly forced
   std::vector<int32_t> first_same;    // [n] first position on the same tensor (U-seed pin rule)
   // fast-kernel tables
@@ -106,7 +110,7 @@ struct DecisionTables {
   DevBuf<uint32_t> d_dec_masks;
   DevBuf<uint8_t> d_dec_cls8;
   DevBuf<uint16_t> d_class_ncand;
-  DevBuf<uint16_t> d_dec_class;
+  DevBuf<int32_t> d_dec_class;
   DevBuf<uint8_t> d_dec_flags;
   DevBuf<int32_t> d_first_same;
   DevBuf<int64_t> d_slots;

@@ -246,19 +246,17 @@ int build_graph(const ap_graph_desc* desc, GraphTables* g) {
     g->class_of_slot[s] = root_class[r];
   }
   g->num_classes = C;
-  if (C > 65535) {
-    set_error("ap_graph_create: more than 65535 link classes (uint16 class ids)");
-    return AP_ERR_UNSUPPORTED;
-  }
   auto cls = [&](int64_t s) { return g->class_of_slot[s]; };
 
   g->slot_forced.assign(S, 0);
   g->class_forced.assign(C, 0);
+  g->forced_words.assign((size_t)(C + 31) / 32, 0u);
   g->forced_list.clear();
   for (int64_t s : forced) {
     g->forced_list.push_back((int32_t)s);
     g->slot_forced[s] = 1;
     g->class_forced[cls(s)] = 1;
+    g->forced_words[(size_t)cls(s) >> 5] |= 1u << (cls(s) & 31);
   }
 
   // implication edges: P on class x forces R on class y
@@ -291,7 +289,7 @@ int build_graph(const ap_graph_desc* desc, GraphTables* g) {
     auto& v = imp[c];
     std::sort(v.begin(), v.end());
     v.erase(std::unique(v.begin(), v.end()), v.end());
-    for (int32_t t : v) g->imp_target.push_back((uint16_t)t);
+    for (int32_t t : v) g->imp_target.push_back(t);
     g->imp_offset[c + 1] = (int32_t)g->imp_target.size();
   }
   build_fast_graph(g);
@@ -311,10 +309,9 @@ int ensure_graph_on_device(GraphTables* g) {
     return AP_OK;
   }
   g->device = cur;
-  std::vector<uint16_t> slot_class16(g->class_of_slot.begin(), g->class_of_slot.end());
   int rc;
-  if ((rc = g->d_slot_class.upload(slot_class16)) != AP_OK) return rc;
-  if ((rc = g->d_class_forced.upload(g->class_forced)) != AP_OK) return rc;
+  if ((rc = g->d_slot_class.upload(g->class_of_slot)) != AP_OK) return rc;
+  if ((rc = g->d_forced_words.upload(g->forced_words)) != AP_OK) return rc;
   if ((rc = g->d_imp_offset.upload(g->imp_offset)) != AP_OK) return rc;
   if ((rc = g->d_imp_target.upload(g->imp_target)) != AP_OK) return rc;
   if ((rc = g->d_program.upload(g->program)) != AP_OK) return rc;
@@ -366,7 +363,7 @@ int build_decision(const GraphTables* g, const int64_t* slots, const uint8_t* is
       set_error("ap_decision_create: slots must be valid and strictly increasing");
       return AP_ERR_INVALID;
     }
-    d->dec_class[i] = (uint16_t)g->class_of_slot[s];
+    d->dec_class[i] = g->class_of_slot[s];
     d->dec_flags[i] = (uint8_t)((is_cand[i] ? 1 : 0) | (g->slot_forced[s] ? 2 : 0));
     const bool same = i > 0 && g->slot_owner[slots[i - 1]] == g->slot_owner[s];
     d->first_same[i] = same ? d->first_same[i - 1] : i;

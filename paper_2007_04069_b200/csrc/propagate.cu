@@ -14,8 +14,10 @@
 //                     reductions), optional per-position output;
 //   5. slots          16 slots per lane-iteration: two 16-byte class-id
 //                     loads, 16 table lookups, one 16-byte store.
-// Graph tables (slot->class, implication CSR, forced flags) are staged in
-// shared memory once per CTA when they fit, else read through L1/L2.
+// Graph tables (slot->class, implication CSR, forced bitset) are staged in
+// shared memory once per CTA when they fit, else read through L1/L2; the
+// per-plan class flags are P / R bitsets (shared memory, or global memory for
+// very wide graphs), so any class count is supported.
 #include <algorithm>
 
 #include "engine.h"
@@ -28,15 +30,15 @@ constexpr int kThreads = kWarps * 32;
 constexpr unsigned kFull = 0xffffffffu;
 
 struct PropParams {
-  const uint16_t* slot_class;
-  const uint8_t* class_forced;
+  const int32_t* slot_class;
+  const uint32_t* forced_words;  // [Cw] forced-replicated class bitset
   const int32_t* imp_offset;
-  const uint16_t* imp_target;
-  const uint16_t* dec_class;
+  const int32_t* imp_target;
+  const int32_t* dec_class;
   const uint8_t* dec_flags;
   const int32_t* first_same;
   int64_t S;
-  int32_t C, Cp, D, T, ncand;
+  int32_t C, Cw, D, T, ncand;  // Cw = bitset words per row (multiple of 4)
   const int8_t* seeds;
   int64_t seed_stride, batch;
   int8_t* slots_out;
@@ -45,7 +47,9 @@ struct PropParams {
   int64_t cand_stride;
   uint8_t* outcome;
   int32_t* counts;
-  int stage_tables;  // copy tables to shared memory
+  int stage_tables;        // copy tables to shared memory
+  uint32_t* gscratch;      // per-warp P/R bitsets in global memory (nullptr: shared)
+  int64_t warp_stride;     // bytes of shared scratch per warp
   // byte offsets of the staged tables inside dynamic shared memory
   int off_slot_class, off_dec_class, off_dec_flags, off_forced, off_imp_off, off_imp_tgt, off_first_same,
       off_scratch;
@@ -58,51 +62,59 @@ __device__ inline void copy_to_smem(uint8_t* dst, const void* src, int64_t bytes
   for (int64_t i = threadIdx.x; i < bytes; i += blockDim.x) dst[i] = s[i];
 }
 
-__device__ inline uint32_t pack4(const int8_t* table, uint32_t c01, uint32_t c23) {
-  const uint32_t s0 = (uint8_t)table[c01 & 0xffffu];
-  const uint32_t s1 = (uint8_t)table[c01 >> 16];
-  const uint32_t s2 = (uint8_t)table[c23 & 0xffffu];
-  const uint32_t s3 = (uint8_t)table[c23 >> 16];
-  return s0 | (s1 << 8) | (s2 << 16) | (s3 << 24);
+// status of class c from the plan's P / R bitsets and the forced bitset
+__device__ __forceinline__ int class_status(const uint32_t* P, const uint32_t* R, const uint32_t* F, int32_t c) {
+  const int w = c >> 5;
+  const uint32_t m = 1u << (c & 31);
+  return (P[w] & m) ? 1 : (((R[w] | F[w]) & m) ? 0 : -1);
 }
 
-template <bool kVecSlots>
+// Generic K1 for any graph: P / R class flags are per-warp bitsets (C/4 bytes
+// per plan) in shared memory, or in global memory when even that does not
+// fit; class ids are 32-bit.
+// kTable: also materialise a per-warp byte status table (C bytes) after the
+// class pass, so candidate / slot lookups are one byte load (graphs whose
+// per-warp scratch still fits in shared memory)
+template <bool kVecSlots, bool kTable>
 __global__ void __launch_bounds__(kThreads) propagate_kernel(PropParams p) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const uint16_t* slot_class = p.slot_class;
-  const uint16_t* dec_class = p.dec_class;
+  const int32_t* slot_class = p.slot_class;
+  const int32_t* dec_class = p.dec_class;
   const uint8_t* dec_flags = p.dec_flags;
-  const uint8_t* class_forced = p.class_forced;
+  const uint32_t* F = p.forced_words;
   const int32_t* imp_offset = p.imp_offset;
-  const uint16_t* imp_target = p.imp_target;
+  const int32_t* imp_target = p.imp_target;
   const int32_t* first_same = p.first_same;
   if (p.stage_tables) {
-    copy_to_smem(smem + p.off_slot_class, p.slot_class, p.S * 2);
-    copy_to_smem(smem + p.off_dec_class, p.dec_class, (int64_t)p.D * 2);
+    copy_to_smem(smem + p.off_slot_class, p.slot_class, p.S * 4);
+    copy_to_smem(smem + p.off_dec_class, p.dec_class, (int64_t)p.D * 4);
     copy_to_smem(smem + p.off_dec_flags, p.dec_flags, p.D);
-    copy_to_smem(smem + p.off_forced, p.class_forced, p.C);
+    copy_to_smem(smem + p.off_forced, p.forced_words, (int64_t)p.Cw * 4);
     copy_to_smem(smem + p.off_imp_off, p.imp_offset, (int64_t)(p.C + 1) * 4);
-    copy_to_smem(smem + p.off_imp_tgt, p.imp_target, (int64_t)p.T * 2);
+    copy_to_smem(smem + p.off_imp_tgt, p.imp_target, (int64_t)p.T * 4);
     copy_to_smem(smem + p.off_first_same, p.first_same, (int64_t)p.D * 4);
     __syncthreads();
-    slot_class = reinterpret_cast<const uint16_t*>(smem + p.off_slot_class);
-    dec_class = reinterpret_cast<const uint16_t*>(smem + p.off_dec_class);
+    slot_class = reinterpret_cast<const int32_t*>(smem + p.off_slot_class);
+    dec_class = reinterpret_cast<const int32_t*>(smem + p.off_dec_class);
     dec_flags = smem + p.off_dec_flags;
-    class_forced = smem + p.off_forced;
+    F = reinterpret_cast<const uint32_t*>(smem + p.off_forced);
     imp_offset = reinterpret_cast<const int32_t*>(smem + p.off_imp_off);
-    imp_target = reinterpret_cast<const uint16_t*>(smem + p.off_imp_tgt);
+    imp_target = reinterpret_cast<const int32_t*>(smem + p.off_imp_tgt);
     first_same = reinterpret_cast<const int32_t*>(smem + p.off_first_same);
   }
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  uint8_t* flagP = smem + p.off_scratch + (int64_t)warp * 3 * p.Cp;
-  uint8_t* flagR = flagP + p.Cp;
-  int8_t* table = reinterpret_cast<int8_t*>(flagR + p.Cp);
+  const int64_t gwarp = (int64_t)blockIdx.x * kWarps + warp;
+  uint32_t* P = p.gscratch ? p.gscratch + gwarp * 2 * p.Cw
+                           : reinterpret_cast<uint32_t*>(smem + p.off_scratch + (int64_t)warp * p.warp_stride);
+  uint32_t* R = P + p.Cw;
+  int8_t* table = reinterpret_cast<int8_t*>(R + p.Cw);  // kTable only: C bytes after the bitsets
+  auto status = [&](int32_t c) -> int { return kTable ? (int)table[c] : class_status(P, R, F, c); };
 
   const int64_t nwarps = (int64_t)gridDim.x * kWarps;
-  for (int64_t b = (int64_t)blockIdx.x * kWarps + warp; b < p.batch; b += nwarps) {
-    // 0. clear the flag rows (Cp is a multiple of 16)
-    for (int i = lane; i < (2 * p.Cp) / 16; i += 32) reinterpret_cast<uint4*>(flagP)[i] = make_uint4(0, 0, 0, 0);
+  for (int64_t b = gwarp; b < p.batch; b += nwarps) {
+    // 0. clear the bitsets (Cw is a multiple of 4)
+    for (int i = lane; i < (2 * p.Cw) / 4; i += 32) reinterpret_cast<uint4*>(P)[i] = make_uint4(0, 0, 0, 0);
     __syncwarp();
 
     // 1. seeds
@@ -110,10 +122,9 @@ __global__ void __launch_bounds__(kThreads) propagate_kernel(PropParams p) {
     bool conflict = false;
     for (int j = lane; j < p.D; j += 32) {
       const int v = srow[j];
-      if (v == 1) {
-        flagP[dec_class[j]] = 1;
-      } else if (v == 0) {
-        flagR[dec_class[j]] = 1;
+      if (v == 1 || v == 0) {
+        const int32_t c = dec_class[j];
+        atomicOr(v == 1 ? &P[c >> 5] : &R[c >> 5], 1u << (c & 31));
       } else if (v == 2) {
         // an UNDECIDED seed conflicts iff its slot is already decided when it
         // is applied: forced replicated, or pinned by an earlier P seed on the
@@ -125,30 +136,34 @@ __global__ void __launch_bounds__(kThreads) propagate_kernel(PropParams p) {
     }
     __syncwarp();
 
-    // 2. implications of partitioned classes
-    for (int c = lane; c < p.C; c += 32) {
-      if (flagP[c]) {
+    // 2. implications of partitioned classes (set bits of P)
+    for (int w = lane; w < p.Cw; w += 32) {
+      uint32_t bits = P[w];
+      while (bits) {
+        const int32_t c = 32 * w + __ffs(bits) - 1;
+        bits &= bits - 1;
         const int e = imp_offset[c + 1];
-        for (int k = imp_offset[c]; k < e; ++k) flagR[imp_target[k]] = 1;
+        for (int k = imp_offset[c]; k < e; ++k) {
+          const int32_t t = imp_target[k];
+          atomicOr(&R[t >> 5], 1u << (t & 31));
+        }
       }
     }
     __syncwarp();
 
-    // 3. class statuses
-    for (int c = lane; c < p.C; c += 32) {
-      const bool isP = flagP[c] != 0;
-      const bool isR = (flagR[c] | class_forced[c]) != 0;
-      conflict |= isP && isR;
-      table[c] = isP ? 1 : (isR ? 0 : -1);
-    }
+    // 3. conflict: a class both partitioned and replicated (or forced)
+    for (int w = lane; w < p.Cw; w += 32) conflict |= (P[w] & (R[w] | F[w])) != 0;
     conflict = __any_sync(kFull, conflict);
-    __syncwarp();
+    if (kTable) {
+      for (int c = lane; c < p.C; c += 32) table[c] = (int8_t)class_status(P, R, F, c);
+      __syncwarp();
+    }
 
     // 4. candidate positions
     int dP = 0, dR = 0, nP = 0, nR = 0;
     int8_t* crow = p.cand_out ? p.cand_out + b * p.cand_stride : nullptr;
     for (int j = lane; j < p.D; j += 32) {
-      const int s = table[dec_class[j]];
+      const int s = status(dec_class[j]);
       if (crow) crow[j] = (int8_t)s;
       if (dec_flags[j] & 1) {
         const bool seeded = srow[j] != -1;
@@ -163,24 +178,25 @@ __global__ void __launch_bounds__(kThreads) propagate_kernel(PropParams p) {
     nP = __reduce_add_sync(kFull, nP);
     nR = __reduce_add_sync(kFull, nR);
 
-    // 5. all slots
+    // 5. all slots (16 per lane-iteration on the vector path)
     if (p.slots_out) {
       int8_t* orow = p.slots_out + b * p.slots_stride;
       const int64_t full = p.S / 16;
       if (kVecSlots) {
         for (int64_t k = lane; k < full; k += 32) {
-          const uint4 ca = reinterpret_cast<const uint4*>(slot_class)[2 * k];
-          const uint4 cb = reinterpret_cast<const uint4*>(slot_class)[2 * k + 1];
-          uint4 o;
-          o.x = pack4(table, ca.x, ca.y);
-          o.y = pack4(table, ca.z, ca.w);
-          o.z = pack4(table, cb.x, cb.y);
-          o.w = pack4(table, cb.z, cb.w);
-          reinterpret_cast<uint4*>(orow)[k] = o;
+          const int4* cq = reinterpret_cast<const int4*>(slot_class) + 4 * k;
+          uint32_t ow[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int4 c = cq[q];
+            ow[q] = (uint32_t)(uint8_t)status(c.x) | ((uint32_t)(uint8_t)status(c.y) << 8) |
+                    ((uint32_t)(uint8_t)status(c.z) << 16) | ((uint32_t)(uint8_t)status(c.w) << 24);
+          }
+          reinterpret_cast<uint4*>(orow)[k] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
         }
-        for (int64_t s = full * 16 + lane; s < p.S; s += 32) orow[s] = table[slot_class[s]];
+        for (int64_t s = full * 16 + lane; s < p.S; s += 32) orow[s] = (int8_t)status(slot_class[s]);
       } else {
-        for (int64_t s = lane; s < p.S; s += 32) orow[s] = table[slot_class[s]];
+        for (int64_t s = lane; s < p.S; s += 32) orow[s] = (int8_t)status(slot_class[s]);
       }
     }
     if (lane == 0) {
@@ -339,7 +355,7 @@ int launch_propagate(const GraphTables* g, const DecisionTables* d, const int8_t
   if (batch == 0) return AP_OK;
   PropParams p{};
   p.slot_class = g->d_slot_class.ptr;
-  p.class_forced = g->d_class_forced.ptr;
+  p.forced_words = g->d_forced_words.ptr;
   p.imp_offset = g->d_imp_offset.ptr;
   p.imp_target = g->d_imp_target.ptr;
   p.dec_class = d->d_dec_class.ptr;
@@ -347,7 +363,7 @@ int launch_propagate(const GraphTables* g, const DecisionTables* d, const int8_t
   p.first_same = d->d_first_same.ptr;
   p.S = g->num_slots;
   p.C = g->num_classes;
-  p.Cp = (int32_t)align16(std::max(g->num_classes, 1));
+  p.Cw = (int32_t)(((std::max(g->num_classes, 1) + 31) / 32 + 3) & ~3);  // words, multiple of 4
   p.D = d->n;
   p.T = (int32_t)g->imp_target.size();
   int ncand = 0;
@@ -369,31 +385,34 @@ int launch_propagate(const GraphTables* g, const DecisionTables* d, const int8_t
     off += align16(bytes);
     return (int)o;
   };
-  p.off_slot_class = place(p.S * 2);
-  p.off_dec_class = place((int64_t)p.D * 2);
+  p.off_slot_class = place(p.S * 4);
+  p.off_dec_class = place((int64_t)p.D * 4);
   p.off_dec_flags = place(p.D);
-  p.off_forced = place(p.C);
+  p.off_forced = place((int64_t)p.Cw * 4);
   p.off_imp_off = place((int64_t)(p.C + 1) * 4);
-  p.off_imp_tgt = place((int64_t)p.T * 2);
+  p.off_imp_tgt = place((int64_t)p.T * 4);
   p.off_first_same = place((int64_t)p.D * 4);
   const int64_t tables_bytes = off;
-  const int64_t scratch_bytes = (int64_t)kWarps * 3 * p.Cp;
   const int64_t kSmemCap = 200 * 1024;
-  int64_t smem = tables_bytes + scratch_bytes;
-  p.stage_tables = 1;
-  if (smem > kSmemCap) {
-    p.stage_tables = 0;
-    smem = scratch_bytes;
-    p.off_scratch = 0;
-    if (smem > kSmemCap) {
-      set_error("ap_propagate_batch: too many link classes for the per-warp shared-memory scratch");
-      return AP_ERR_UNSUPPORTED;
-    }
-  } else {
-    p.off_scratch = (int)tables_bytes;
+  // per-warp scratch: P / R bitsets, plus a byte status table when it fits
+  const int64_t bits_bytes = (int64_t)kWarps * 2 * p.Cw * 4;
+  const int64_t table_bytes = (int64_t)kWarps * (2 * p.Cw * 4 + align16(p.C));
+  bool use_table = true, global_scratch = false;
+  int64_t smem;
+  if (tables_bytes + table_bytes <= kSmemCap) {
+    p.stage_tables = 1, p.off_scratch = (int)tables_bytes, smem = tables_bytes + table_bytes;
+  } else if (table_bytes <= kSmemCap) {
+    p.stage_tables = 0, p.off_scratch = 0, smem = table_bytes;
+  } else if (bits_bytes <= kSmemCap) {
+    p.stage_tables = 0, p.off_scratch = 0, smem = bits_bytes, use_table = false;
+  } else {  // very wide graphs: bitsets in global memory
+    p.stage_tables = 0, p.off_scratch = 0, smem = 0, use_table = false, global_scratch = true;
   }
+  // per-warp layout: [P: Cw words][R: Cw words][status table: align16(C) bytes if kTable]
+  p.warp_stride = (int64_t)2 * p.Cw * 4 + (use_table ? align16(p.C) : 0);
   const bool vec = slots_out && (slots_stride % 16 == 0) && ((reinterpret_cast<uintptr_t>(slots_out) & 15) == 0);
-  auto kern = vec ? propagate_kernel<true> : propagate_kernel<false>;
+  auto kern = vec ? (use_table ? propagate_kernel<true, true> : propagate_kernel<true, false>)
+                  : (use_table ? propagate_kernel<false, true> : propagate_kernel<false, false>);
   AP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (g_num_sms < 0) {
     int dev = 0;
@@ -403,8 +422,24 @@ int launch_propagate(const GraphTables* g, const DecisionTables* d, const int8_t
   int per_sm = 0;
   AP_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, (size_t)smem));
   per_sm = std::max(per_sm, 1);
+  if (global_scratch) per_sm = std::min(per_sm, 2);  // bounds the global scratch footprint
   const int64_t want = (batch + kWarps - 1) / kWarps;
   const int grid = (int)std::min<int64_t>(want, (int64_t)g_num_sms * per_sm);
+  if (global_scratch) {
+    const int64_t words = (int64_t)grid * kWarps * 2 * p.Cw;
+    if (words > g->scratch_words) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      AP_CUDA_CHECK(cudaStreamIsCapturing(stream, &cs));
+      if (cs != cudaStreamCaptureStatusNone) {
+        set_error("ap_propagate_batch: generic scratch must grow during graph capture; launch once before");
+        return AP_ERR_INVALID;
+      }
+      if (g->d_scratch) AP_CUDA_CHECK(cudaFree(g->d_scratch));
+      AP_CUDA_CHECK(cudaMalloc(&g->d_scratch, words * sizeof(uint32_t)));
+      g->scratch_words = words;
+    }
+    p.gscratch = g->d_scratch;
+  }
   kern<<<grid, kThreads, (size_t)smem, stream>>>(p);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;

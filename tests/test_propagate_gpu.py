@@ -197,17 +197,23 @@ def _wide_graph(blocks: int):
     return w.graph()
 
 
-@pytest.mark.parametrize("blocks", [80, 1100])
-def test_beyond_fast_kernel_limits_matches_oracle(cuda, blocks):
-    """> 255 link classes (80 blocks: 320 classes) and > 4096 candidate dims (1100 blocks:
-    4400 dims): the engine takes the generic kernel and still matches the C oracle."""
+@pytest.mark.parametrize("blocks,batch", [(80, 48), (1100, 48), (26000, 6)])
+def test_beyond_fast_kernel_limits_matches_oracle(cuda, blocks, batch):
+    """> 255 link classes (80 blocks: 320 classes), > 4096 candidate dims (1100 blocks:
+    4400 dims) and > 65535 classes with bitsets beyond shared memory (26000 blocks:
+    104000 classes, 130000 instructions): the generic kernel matches the C oracle."""
     g = _wide_graph(blocks)
     dims = decision_dims(g, g.trainable_variables)
     n = len(dims)
     rng = np.random.default_rng(blocks)
+    all_r = np.where(np.arange(n)[None, :] < rng.integers(1, n + 1, size=(2, 1)), 0, -1).astype(np.int8)
+    sparse_p = np.full((2, n), -1, np.int8)  # one P seed on every 4th candidate dim
+    sparse_p[0, ::4] = 1
+    sparse_p[1, 1::4] = 1
     seeds = np.concatenate([
-        random_prefix_seeds(rng, n, 48, rng.permutation(n)),
-        np.where(rng.random((16, n)) < 0.01, rng.integers(0, 3, size=(16, n)), -1).astype(np.int8),
+        random_prefix_seeds(rng, n, batch, rng.permutation(n)),
+        np.where(rng.random((batch // 3, n)) < 0.01, rng.integers(0, 3, size=(batch // 3, n)), -1).astype(np.int8),
+        all_r, sparse_p,
     ])
     eng = PropagationEngine(g, dims)
     out = eng.run_batch(torch.from_numpy(seeds), want_slots=True)
