@@ -19,6 +19,7 @@
 // per-plan class flags are P / R bitsets (shared memory, or global memory for
 // very wide graphs), so any class count is supported.
 #include <algorithm>
+#include <cstdlib>
 
 #include "engine.h"
 
@@ -211,6 +212,121 @@ __global__ void __launch_bounds__(kThreads) propagate_kernel(PropParams p) {
   }
 }
 
+// Generic K1 for very wide graphs (per-warp scratch does not fit): the whole
+// CTA works on one plan at a time, so the per-plan work (tens of thousands of
+// slots, tables read through L2) is spread over 8 warps and several plans are
+// in flight per SM.  Same phases as propagate_kernel with CTA barriers; P / R
+// bitsets plus (kTable) a byte status table per CTA in shared memory.
+template <bool kVecSlots, bool kTable>
+__global__ void __launch_bounds__(kThreads) propagate_cta_kernel(PropParams p) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  __shared__ int s_red[kWarps][4];
+  const int32_t* slot_class = p.slot_class;
+  const int32_t* dec_class = p.dec_class;
+  const uint8_t* dec_flags = p.dec_flags;
+  const uint32_t* F = p.forced_words;
+  const int32_t* imp_offset = p.imp_offset;
+  const int32_t* imp_target = p.imp_target;
+  const int32_t* first_same = p.first_same;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint32_t* P = reinterpret_cast<uint32_t*>(smem);
+  uint32_t* R = P + p.Cw;
+  int8_t* table = reinterpret_cast<int8_t*>(R + p.Cw);
+  auto status = [&](int32_t c) -> int { return kTable ? (int)table[c] : class_status(P, R, F, c); };
+
+  for (int64_t b = blockIdx.x; b < p.batch; b += gridDim.x) {
+    for (int i = tid; i < (2 * p.Cw) / 4; i += kThreads) reinterpret_cast<uint4*>(P)[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    const int8_t* srow = p.seeds + b * p.seed_stride;
+    int conflict = 0;
+    for (int j = tid; j < p.D; j += kThreads) {
+      const int v = srow[j];
+      if (v == 1 || v == 0) {
+        const int32_t c = dec_class[j];
+        atomicOr(v == 1 ? &P[c >> 5] : &R[c >> 5], 1u << (c & 31));
+      } else if (v == 2) {  // sharding.py:116-118, 219-229
+        if (dec_flags[j] & 2) conflict = 1;
+        for (int k = first_same[j]; k < j; ++k)
+          if (srow[k] == 1) conflict = 1;
+      }
+    }
+    __syncthreads();
+    for (int w = tid; w < p.Cw; w += kThreads) {
+      uint32_t bits = P[w];
+      while (bits) {
+        const int32_t c = 32 * w + __ffs(bits) - 1;
+        bits &= bits - 1;
+        const int e = imp_offset[c + 1];
+        for (int k = imp_offset[c]; k < e; ++k) {
+          const int32_t t = imp_target[k];
+          atomicOr(&R[t >> 5], 1u << (t & 31));
+        }
+      }
+    }
+    __syncthreads();
+    for (int w = tid; w < p.Cw; w += kThreads) conflict |= (P[w] & (R[w] | F[w])) != 0;
+    conflict = __syncthreads_or(conflict);
+    if (kTable) {
+      for (int c = tid; c < p.C; c += kThreads) table[c] = (int8_t)class_status(P, R, F, c);
+      __syncthreads();
+    }
+    int dP = 0, dR = 0, nP = 0, nR = 0;
+    int8_t* crow = p.cand_out ? p.cand_out + b * p.cand_stride : nullptr;
+    for (int j = tid; j < p.D; j += kThreads) {
+      const int s = status(dec_class[j]);
+      if (crow) crow[j] = (int8_t)s;
+      if (dec_flags[j] & 1) {
+        const bool seeded = srow[j] != -1;
+        dP += (s == 1);
+        dR += (s == 0);
+        nP += (s == 1) && !seeded;
+        nR += (s == 0) && !seeded;
+      }
+    }
+    if (p.slots_out) {
+      int8_t* orow = p.slots_out + b * p.slots_stride;
+      const int64_t full = p.S / 16;
+      if (kVecSlots) {
+        for (int64_t k = tid; k < full; k += kThreads) {
+          const int4* cq = reinterpret_cast<const int4*>(slot_class) + 4 * k;
+          uint32_t ow[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int4 c = cq[q];
+            ow[q] = (uint32_t)(uint8_t)status(c.x) | ((uint32_t)(uint8_t)status(c.y) << 8) |
+                    ((uint32_t)(uint8_t)status(c.z) << 16) | ((uint32_t)(uint8_t)status(c.w) << 24);
+          }
+          reinterpret_cast<uint4*>(orow)[k] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+        }
+        for (int64_t s = full * 16 + tid; s < p.S; s += kThreads) orow[s] = (int8_t)status(slot_class[s]);
+      } else {
+        for (int64_t s = tid; s < p.S; s += kThreads) orow[s] = (int8_t)status(slot_class[s]);
+      }
+    }
+    dP = __reduce_add_sync(kFull, dP);
+    dR = __reduce_add_sync(kFull, dR);
+    nP = __reduce_add_sync(kFull, nP);
+    nR = __reduce_add_sync(kFull, nR);
+    if (lane == 0) {
+      s_red[warp][0] = dP;
+      s_red[warp][1] = dR;
+      s_red[warp][2] = nP;
+      s_red[warp][3] = nR;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int t[4] = {0, 0, 0, 0};
+      for (int w = 0; w < kWarps; ++w)
+        for (int q = 0; q < 4; ++q) t[q] += s_red[w][q];
+      p.outcome[b] = conflict ? AP_OUTCOME_CONFLICT
+                              : ((t[0] + t[1] == p.ncand) ? AP_OUTCOME_COMPLETE : AP_OUTCOME_INCOMPLETE);
+      if (p.counts)
+        reinterpret_cast<int4*>(p.counts)[b] = conflict ? make_int4(0, 0, 0, 0) : make_int4(t[0], t[1], t[2], t[3]);
+    }
+    __syncthreads();
+  }
+}
+
 // ---- exact-order replay (one thread) --------------------------------------
 
 struct TraceState {
@@ -395,17 +511,42 @@ int launch_propagate(const GraphTables* g, const DecisionTables* d, const int8_t
   const int64_t tables_bytes = off;
   const int64_t kSmemCap = 200 * 1024;
   // per-warp scratch: P / R bitsets, plus a byte status table when it fits
-  const int64_t bits_bytes = (int64_t)kWarps * 2 * p.Cw * 4;
   const int64_t table_bytes = (int64_t)kWarps * (2 * p.Cw * 4 + align16(p.C));
   bool use_table = true, global_scratch = false;
   int64_t smem;
-  if (tables_bytes + table_bytes <= kSmemCap) {
+  // one plan per CTA when a plan is large (measured on B200: 4.4k classes / 11k
+  // slots 11 -> 24 M plans/s; 320 classes / 800 slots is 3x faster per warp);
+  // AP_PROPAGATE_CTA=1 forces it (tests)
+  const bool force_cta = std::getenv("AP_PROPAGATE_CTA") != nullptr || p.S + p.D >= 6144;
+  if (!force_cta && tables_bytes + table_bytes <= kSmemCap) {
     p.stage_tables = 1, p.off_scratch = (int)tables_bytes, smem = tables_bytes + table_bytes;
-  } else if (table_bytes <= kSmemCap) {
+  } else if (!force_cta && table_bytes <= kSmemCap) {
     p.stage_tables = 0, p.off_scratch = 0, smem = table_bytes;
-  } else if (bits_bytes <= kSmemCap) {
-    p.stage_tables = 0, p.off_scratch = 0, smem = bits_bytes, use_table = false;
-  } else {  // very wide graphs: bitsets in global memory
+  } else {
+    // very wide graphs: one plan per CTA (propagate_cta_kernel) with the
+    // bitsets (+ status table when it fits) shared by the whole CTA
+    const bool vec = slots_out && (slots_stride % 16 == 0) && ((reinterpret_cast<uintptr_t>(slots_out) & 15) == 0);
+    const int64_t cta_bits = (int64_t)2 * p.Cw * 4, cta_table = cta_bits + align16(p.C);
+    if (cta_bits <= kSmemCap && std::getenv("AP_PROPAGATE_NO_CTA") == nullptr) {
+      const bool tbl = cta_table <= kSmemCap;
+      const int64_t csmem = tbl ? cta_table : cta_bits;
+      auto ck = vec ? (tbl ? propagate_cta_kernel<true, true> : propagate_cta_kernel<true, false>)
+                    : (tbl ? propagate_cta_kernel<false, true> : propagate_cta_kernel<false, false>);
+      AP_CUDA_CHECK(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+      if (g_num_sms < 0) {
+        int dev = 0;
+        AP_CUDA_CHECK(cudaGetDevice(&dev));
+        AP_CUDA_CHECK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+      }
+      int cper = 0;
+      AP_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cper, ck, kThreads, (size_t)csmem));
+      const int cgrid = (int)std::min<int64_t>(batch, (int64_t)g_num_sms * std::max(cper, 1));
+      p.stage_tables = 0;
+      ck<<<cgrid, kThreads, (size_t)csmem, stream>>>(p);
+      AP_CUDA_CHECK(cudaGetLastError());
+      return AP_OK;
+    }
+    // beyond even per-CTA bitsets in shared memory: per-warp bitsets in global memory
     p.stage_tables = 0, p.off_scratch = 0, smem = 0, use_table = false, global_scratch = true;
   }
   // per-warp layout: [P: Cw words][R: Cw words][status table: align16(C) bytes if kTable]

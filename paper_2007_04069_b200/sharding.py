@@ -323,9 +323,13 @@ class PropagationEngine:
         """Device graph + decision set for the candidate list (identity column order required)."""
         if self.candidates is None:
             raise ValueError("batched propagation needs an explicit candidate list")
+        cached = self.__dict__.get("_prepared")
+        if cached is not None and cached[0] is self.candidates:  # validated once per candidate list
+            return cached[1], cached[2]
         dev, dec, pos, cand_slots = self._decision_for(self.candidates)
         if any(pos[s] != k for k, s in enumerate(cand_slots)):
             raise ValueError("launch() needs candidates in ascending (instruction id, dim) order")
+        self.__dict__["_prepared"] = (self.candidates, dev, dec)
         return dev, dec
 
     @property
