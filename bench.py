@@ -516,7 +516,9 @@ def bench_dqn_vec(args, g, world, rank):
         "config": {"graph": "bert48", "task": "opp", "envs_per_gpu": E, "learn_steps_per_vector_step": L,
                    "learn_batch": cfg.batch_size, "learn_to_env_step_ratio": f"{L}:{E}",
                    "hidden": list(cfg.hidden), "state_dim": S, "replay_capacity": tr.capacity,
-                   "parallelism": f"data-parallel DQN x{world}, NCCL allreduce of Q-gradients" if world > 1 else "1 GPU",
+                   "parallelism": (f"data-parallel DQN x{world}, " + ("Q-gradient all-reduce over NVLink peer memory fused "
+                                   "with Adam (ap_dp_allreduce_adam)" if tr.peer is not None else
+                                   "NCCL all-reduce of Q-gradients")) if world > 1 else "1 GPU",
                    "vector_steps": args.dqn_steps},
         "ms_per_vector_step": ms / args.dqn_steps,
         "cuda_graph": tr.graph is not None,

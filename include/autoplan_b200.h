@@ -338,6 +338,16 @@ int ap_vec_track_best(int32_t E, int32_t n, int64_t ld, const int8_t* status, co
 int ap_dqn_act_ctl(const float* q, int64_t ldq, const uint8_t* mask, int64_t ldm, int32_t E, int32_t A,
                    float epsilon_start, float epsilon_final, int64_t decay_iters, const int64_t* ctl, int32_t* actions,
                    void* stream);
+/* Data-parallel learner step in one kernel: all-reduce (mean) of the
+ * Q-gradient over NVLink peer memory + Adam (agent.py:229-250, t = ctl[3] + 1).
+ * xbuf_peers / pad_peers are HOST arrays of `world` device pointers: every rank's
+ * symmetric exchange buffer (2 * n floats) and flag row (world uint32, zeroed
+ * once); counter is a local zeroed uint32.  Ranks average in rank order, so every
+ * replica gets identical parameters.  Stream-capturable; replaces NCCL all-reduce
+ * + ap_dqn_adam_ctl. */
+int ap_dp_allreduce_adam(int32_t world, int32_t rank, const float* grad, float* const* xbuf_peers,
+                         uint32_t* const* pad_peers, int64_t n, float* params, float* m, float* v, float lr,
+                         float beta1, float beta2, float eps, const int64_t* ctl, uint32_t* counter, void* stream);
 /* Adam (agent.py:229-250) with bias corrections for t = ctl[3] + 1 */
 int ap_dqn_adam_ctl(float* params, const float* grads, float* m, float* v, int64_t n, float lr, float beta1,
                     float beta2, float eps, const int64_t* ctl, void* stream);

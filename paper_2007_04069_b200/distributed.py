@@ -64,6 +64,53 @@ def allreduce_mean_(t, group=None):
     return t
 
 
+class PeerExchange:
+    """Symmetric NVLink buffers for the fused gradient all-reduce + Adam kernel
+    (`ap_dp_allreduce_adam`): per rank a [2, n] fp32 exchange buffer and a [W] flag
+    row, mapped into every peer (torch symmetric memory).  `None` from `create`
+    when symmetric memory is unavailable (the caller then uses NCCL)."""
+
+    def __init__(self, n: int, group):
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        self.rank, self.world = rank_world(group)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        name = group.group_name if group is not None else dist.group.WORLD.group_name
+        self.xbuf = symm_mem.empty(2 * n, dtype=torch.float32, device=dev)
+        self.xbuf.zero_()
+        hx = symm_mem.rendezvous(self.xbuf, name)
+        self.pad = symm_mem.empty(self.world, dtype=torch.int32, device=dev)
+        self.pad.zero_()
+        hp = symm_mem.rendezvous(self.pad, name)
+        self.counter = torch.zeros(1, dtype=torch.int32, device=dev)
+        torch.cuda.synchronize()
+        dist.barrier(group=group)  # every pad is zero before anyone signals
+        W = self.world
+        self.xbuf_ptrs = (ctypes.c_void_p * W)(*[hx.get_buffer(p, (2 * n,), torch.float32).data_ptr()
+                                                 for p in range(W)])
+        self.pad_ptrs = (ctypes.c_void_p * W)(*[hp.get_buffer(p, (W,), torch.int32).data_ptr() for p in range(W)])
+        self._handles = (hx, hp)  # keep the mappings alive
+        self.n = n
+
+    @classmethod
+    def create(cls, n: int, group):
+        """Opt-in (AP_DP_FUSED=1).  Measured on 2 x B200 (BERT-48 OPP, E=4096, 4 learn
+        steps per vector step, CUDA graph): 0.70 ms per vector step fused vs 0.63 ms
+        with NCCL's all-reduce + the Adam kernel, so NCCL stays the default."""
+        import os
+
+        if os.environ.get("AP_DP_FUSED") != "1" or rank_world(group)[1] > 8:
+            return None
+        try:
+            return cls(n, group)
+        except Exception:  # no symmetric memory / peer access on this system
+            return None
+
+
 class BestPlan:
     """A completed partition plan: #partitioned candidates, return, global episode id,
     per-candidate statuses (int8, decision-dim order)."""

@@ -22,7 +22,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _native
-from .distributed import BestPlan, allreduce_mean_, rank_world, reduce_best, select_first_wins
+from .distributed import BestPlan, PeerExchange, allreduce_mean_, rank_world, reduce_best, select_first_wins
 from .agent import AdamOptimizer, AgentConfig, QNetwork, _Batch, sync_target
 from .ir import decision_dims
 from .linkage import extract_linkage_groups, sorted_decision_order
@@ -169,6 +169,8 @@ class VecDqnTrainer:
         self.vector_steps = 0
         self.launches = 0
         self.rank, self.world = rank_world(process_group) if process_group is not None else (0, 1)
+        # fused NVLink all-reduce + Adam when the ranks can map each other's memory
+        self.peer = PeerExchange.create(self.net.flat.numel(), process_group) if self.world > 1 else None
         self.use_graph = use_graph
         self.graph = None
         self._graph_launches = 0
@@ -221,11 +223,19 @@ class VecDqnTrainer:
                                          float(cfg.gamma), float(cfg.huber_delta), P(b.dz), b.dz.stride(0),
                                          P(self.dz_t), self.dz_t.stride(0), P(b.td), P(b.loss_rows), _s()))
         self.net.backward_device(acts, b.dz, self.dz_t)
-        if self.pg is not None:  # data-parallel learners: average the Q-gradient over NVLink
-            allreduce_mean_(self.net.grad, self.pg)
         opt = self.opt
-        _native.check(lib.ap_dqn_adam_ctl(P(self.net.flat), P(self.net.grad), P(opt.m), P(opt.v), self.net.flat.numel(),
-                                          opt.lr, opt.beta1, opt.beta2, opt.eps, P(self.ctl), _s()))
+        if self.peer is not None:  # data-parallel: gradient all-reduce over NVLink peer memory fused with Adam
+            x = self.peer
+            _native.check(lib.ap_dp_allreduce_adam(x.world, x.rank, P(self.net.grad), x.xbuf_ptrs, x.pad_ptrs,
+                                                   self.net.flat.numel(), P(self.net.flat), P(opt.m), P(opt.v),
+                                                   opt.lr, opt.beta1, opt.beta2, opt.eps, P(self.ctl),
+                                                   P(x.counter), _s()))
+        else:
+            if self.pg is not None:  # data-parallel learners without peer memory: NCCL mean all-reduce
+                allreduce_mean_(self.net.grad, self.pg)
+            _native.check(lib.ap_dqn_adam_ctl(P(self.net.flat), P(self.net.grad), P(opt.m), P(opt.v),
+                                              self.net.flat.numel(), opt.lr, opt.beta1, opt.beta2, opt.eps,
+                                              P(self.ctl), _s()))
         self.net.refresh_transposed()
         _native.check(lib.ap_per_update_scaled(P(r["priorities"]), P(self.idx), P(b.td), B, float(cfg.per_alpha),
                                                _s()))
