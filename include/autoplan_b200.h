@@ -362,6 +362,23 @@ int ap_per_push_ctl(int32_t E, int32_t S, int32_t A, int64_t cap, const float* s
 int ap_per_sample_ctl(const double* priorities, int64_t capacity, double beta, int32_t B, uint64_t seed,
                       double* cdf_scratch, int32_t* indices, float* weights, double* max_priority, const int64_t* ctl,
                       void* stream);
+/* Vectorised PipeTrainEnv (envs.py:276-404), E envs on the device.  picks / positions
+ * [E, P] (P = K - 1 candidate indices / their forward positions), n_applied [E].
+ * ap_vec_pipe_apply appends actions[e] and flags the envs whose last pick it was. */
+int ap_vec_pipe_apply(int32_t E, int32_t P, const int32_t* actions, const int32_t* cand_pos, int32_t* picks,
+                      int32_t* positions, int32_t* n_applied, uint8_t* done, void* stream);
+/* After ap_pipe_metrics + ap_pipe_length over every env's positions: terminal
+ * rewards (reward_shape 0: 1/L, 1: 1/sqrt L; -1/sqrt L if infeasible; L >= 1e-12),
+ * per-env incumbents (min L over feasible episodes, strict <, cli.py:315; global
+ * episode id (ctl[0] * world + rank) * E + e), auto-reset (positions back to
+ * dummy_pos [P]), and the next state inputs: applied_state [E, a_max] and the
+ * action mask [E, C] (envs.py:284-293); next_mask = 0 for finished envs. */
+int ap_vec_pipe_post(int32_t E, int32_t C, int32_t P, int32_t a_max, const double* length, const uint8_t* feasible,
+                     const uint8_t* done, int32_t reward_shape, const int32_t* dummy_pos, float* rewards,
+                     int32_t* picks, int32_t* positions, int32_t* n_applied, int32_t* applied_state, uint8_t* mask,
+                     uint8_t* next_mask, double* best_len, int32_t* best_picks, int64_t* best_episode,
+                     float* ep_return, float* finished_return, int32_t* episodes_done, const int64_t* ctl,
+                     int32_t world, int32_t rank, void* stream);
 /* mode 0: ctl[3] += 1 (one learn step); mode 1: ctl[0] += 1, ctl[1] = (ctl[1] + E) % cap,
  * ctl[2] = min(ctl[2] + E, cap) (one vector step) */
 int ap_vec_ctl_advance(int64_t* ctl, int32_t mode, int64_t E, int64_t cap, void* stream);

@@ -146,6 +146,9 @@ SIGNATURES: dict[str, tuple] = {
     "ap_per_push_ctl": (ctypes.c_int, [_I32, _I32, _I32, _I64, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
                                        _VP, _VP, _VP, _VP, _VP, _VP]),
     "ap_per_sample_ctl": (ctypes.c_int, [_VP, _I64, _F64, _I32, _U64, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "ap_vec_pipe_apply": (ctypes.c_int, [_I32, _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "ap_vec_pipe_post": (ctypes.c_int, [_I32, _I32, _I32, _I32, _VP, _VP, _VP, _I32, _VP, _VP, _VP, _VP, _VP, _VP,
+                                        _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I32, _I32, _VP]),
     "ap_vec_ctl_advance": (ctypes.c_int, [_VP, _I32, _I64, _I64, _VP]),
     "ap_per_push": (ctypes.c_int, [_I32, _I32, _I32, _I64, _I64, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
                                    _VP, _VP, _VP, _VP, _VP]),

@@ -285,6 +285,74 @@ int launch_per_sample(const double* prio, int n_host_max, double beta, const flo
   return AP_OK;
 }
 
+// ---- vectorised PipeTrainEnv (envs.py:276-404) --------------------------------
+// picks [E, P] (P = K - 1 candidate indices), positions [E, P] (their forward
+// positions, pre-filled with valid dummies so every row is a legal pivot tuple
+// for the batched metrics kernel), n_applied [E].
+__global__ void vec_pipe_apply_kernel(int E, int P, const int32_t* actions, const int32_t* cand_pos, int32_t* picks,
+                                      int32_t* positions, int32_t* n_applied, uint8_t* done) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const int k = n_applied[e];
+  const int a = actions[e];
+  picks[(int64_t)e * P + k] = a;
+  positions[(int64_t)e * P + k] = cand_pos[a];
+  n_applied[e] = k + 1;
+  done[e] = (k + 1 == P) ? 1 : 0;
+}
+
+// Terminal rewards (1 / L, 1 / sqrt L, -1 / sqrt L when infeasible), per-env
+// incumbents (min L over feasible episodes, strict <: cli.py:315), reset of
+// finished envs, then the state inputs of every env: the applied picks (first
+// a_max) and the action mask (envs.py:284-293); next_mask = 0 for finished envs.
+__global__ void vec_pipe_post_kernel(int E, int C, int P, int a_max, const double* length, const uint8_t* feasible,
+                                     const uint8_t* done, int reward_shape, const int32_t* dummy_pos, float* rewards,
+                                     int32_t* picks, int32_t* positions, int32_t* n_applied, int32_t* applied_state,
+                                     uint8_t* mask, uint8_t* next_mask, double* best_len, int32_t* best_picks,
+                                     int64_t* best_episode, float* ep_return, float* finished_return,
+                                     int32_t* episodes_done, const int64_t* ctl, int world, int rank) {
+  const int e = blockIdx.x;
+  const bool fin = done[e] != 0;
+  const int64_t step_base = (ctl[AP_CTL_STEP] * world + rank) * (int64_t)E;
+  __shared__ int s_k, s_last;
+  if (threadIdx.x == 0) {
+    float r = 0.0f;
+    if (fin) {
+      const double L = fmax(length[e], 1e-12);  // _MIN_LENGTH
+      const bool feas = feasible[e] != 0;
+      r = !feas ? (float)(-1.0 / sqrt(L)) : (reward_shape == 0 ? (float)(1.0 / L) : (float)(1.0 / sqrt(L)));
+      if (feas && L < best_len[e]) {
+        best_len[e] = L;
+        for (int k = 0; k < P; ++k) best_picks[(int64_t)e * P + k] = picks[(int64_t)e * P + k];
+        best_episode[e] = step_base + e;
+      }
+      finished_return[e] = ep_return[e] + r;
+      ep_return[e] = 0.0f;
+      episodes_done[e] += 1;
+      n_applied[e] = 0;  // auto-reset (envs.py:275-278)
+      for (int k = 0; k < P; ++k) {
+        picks[(int64_t)e * P + k] = -1;
+        positions[(int64_t)e * P + k] = dummy_pos[k];
+      }
+    } else {
+      ep_return[e] += r;
+    }
+    rewards[e] = r;
+    const int k = n_applied[e];
+    s_k = k;
+    s_last = k > 0 ? picks[(int64_t)e * P + k - 1] : -1;
+    for (int j = 0; j < a_max; ++j) applied_state[(int64_t)e * a_max + j] = j < k ? picks[(int64_t)e * P + j] : -1;
+  }
+  __syncthreads();
+  const int remaining = P - s_k;
+  const int hi = C - remaining;  // keep room for the picks still owed
+  for (int i = threadIdx.x; i < C; i += blockDim.x) {
+    const uint8_t m = (i > s_last && i <= hi) ? 1 : 0;
+    mask[(int64_t)e * C + i] = m;
+    next_mask[(int64_t)e * C + i] = fin ? 0 : m;
+  }
+}
+
 // mode 0: one learn step done (train counter); mode 1: one vector step done
 // (step counter, ring slot and size after pushing E transitions)
 __global__ void ctl_advance_kernel(int64_t* ctl, int mode, int64_t E, int64_t cap) {
@@ -399,6 +467,40 @@ int ap_per_sample_ctl(const double* priorities, int64_t capacity, double beta, i
   }
   return launch_per_sample(priorities, (int)capacity, beta, nullptr, B, cdf_scratch, indices, weights, max_priority,
                            ctl, seed, (cudaStream_t)stream);
+}
+
+int ap_vec_pipe_apply(int32_t E, int32_t P, const int32_t* actions, const int32_t* cand_pos, int32_t* picks,
+                      int32_t* positions, int32_t* n_applied, uint8_t* done, void* stream) {
+  if (E < 0 || P < 1 || (E > 0 && (!actions || !cand_pos || !picks || !positions || !n_applied || !done))) {
+    set_error("ap_vec_pipe_apply: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  if (E == 0) return AP_OK;
+  vec_pipe_apply_kernel<<<(E + 255) / 256, 256, 0, (cudaStream_t)stream>>>(E, P, actions, cand_pos, picks, positions,
+                                                                           n_applied, done);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_vec_pipe_post(int32_t E, int32_t C, int32_t P, int32_t a_max, const double* length, const uint8_t* feasible,
+                     const uint8_t* done, int32_t reward_shape, const int32_t* dummy_pos, float* rewards,
+                     int32_t* picks, int32_t* positions, int32_t* n_applied, int32_t* applied_state, uint8_t* mask,
+                     uint8_t* next_mask, double* best_len, int32_t* best_picks, int64_t* best_episode,
+                     float* ep_return, float* finished_return, int32_t* episodes_done, const int64_t* ctl,
+                     int32_t world, int32_t rank, void* stream) {
+  if (E < 0 || C < 1 || P < 1 || a_max < 1 || (reward_shape != 0 && reward_shape != 1) || !ctl || world < 1 ||
+      rank < 0 || rank >= world) {
+    set_error("ap_vec_pipe_post: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  if (E == 0) return AP_OK;
+  // one CTA per env; episodes finishing at this step get global ids (step * world + rank) * E + e
+  vec_pipe_post_kernel<<<E, 128, 0, (cudaStream_t)stream>>>(
+      E, C, P, a_max, length, feasible, done, reward_shape, dummy_pos, rewards, picks, positions, n_applied,
+      applied_state, mask, next_mask, best_len, best_picks, best_episode, ep_return, finished_return, episodes_done,
+      ctl, world, rank);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
 }
 
 int ap_vec_ctl_advance(int64_t* ctl, int32_t mode, int64_t E, int64_t cap, void* stream) {

@@ -109,6 +109,129 @@ class VecPartitionEnv:
                                             P(self.best_episode), P(self.best_status), _s()))
 
 
+class VecPipeTrainEnv:
+    """E PipeTrainEnv episodes (envs.py:276-404) stepping in lockstep on the device.
+
+    Each vector step appends one pivot per env (ap_vec_pipe_apply), evaluates the
+    finished tuples (ap_pipe_metrics + ap_pipe_length over every env), pays the
+    terminal rewards, records per-env incumbents and resets finished envs
+    (ap_vec_pipe_post), then evaluates the next state of every env with K2
+    (ap_pipe_train_state: all allowed candidates' features, [E, 4C]).  Finished
+    transitions carry done = 1 and an empty next mask, so their next state (the
+    reset state) never bootstraps.  Same device interface as VecPartitionEnv, so
+    VecDqnTrainer drives it (and captures it in a CUDA graph) unchanged.
+    """
+
+    def __init__(self, graph, topo, num_stages: int, E: int, radius: int = 3, micro_batches: int = 4,
+                 mem_per_device: float | None = None, reward_shape: str = "inv", backward_multiplier: float = 2.0):
+        import torch
+
+        from .envs import PipeTrainEnv
+
+        host = PipeTrainEnv(graph, topo, num_stages, radius, micro_batches, mem_per_device=mem_per_device,
+                            reward_shape=reward_shape, backward_multiplier=backward_multiplier)
+        self.host = host
+        self.E = E
+        self.K = num_stages
+        self.P = P = num_stages - 1
+        self.C = C = host.num_actions
+        self.a_max = max(1, num_stages - 2)
+        self.num_actions = C
+        self.state_dim = 4 * C
+        self.topo_c = _native.Topology.of(topo)
+        self.micro_batches = micro_batches
+        self.mem = -1.0 if mem_per_device is None else float(mem_per_device)
+        self.reward_shape = 0 if reward_shape == "inv" else 1
+        self.bwm = float(backward_multiplier)
+        dev = "cuda"
+        i32, u8, f64, f32 = torch.int32, torch.uint8, torch.float64, torch.float32
+        self.cand_pos = torch.from_numpy(host._cand_pos).to(dev)
+        self.dummy_pos = self.cand_pos[C - P:].clone()  # a legal increasing pivot tuple
+        self.picks = torch.full((E, P), -1, dtype=i32, device=dev)
+        self.positions = self.dummy_pos.repeat(E, 1).contiguous()
+        self.n_applied = torch.zeros(E, dtype=i32, device=dev)
+        self.done = torch.zeros(E, dtype=u8, device=dev)
+        self.applied_state = torch.full((E, self.a_max), -1, dtype=i32, device=dev)
+        self.mask = torch.zeros((E, C), dtype=u8, device=dev)
+        self.next_mask = torch.zeros((E, C), dtype=u8, device=dev)
+        self.state64 = torch.zeros((E, 4 * C), dtype=f64, device=dev)
+        self.cur_state = torch.zeros((E, 4 * C), dtype=f32, device=dev)
+        self.obs = torch.empty_like(self.cur_state)
+        self.next_state = torch.empty_like(self.cur_state)
+        self.rewards = torch.zeros(E, dtype=f32, device=dev)
+        K = num_stages
+        self.comp = torch.empty((E, K), dtype=f64, device=dev)
+        self.act = torch.empty((E, K), dtype=f64, device=dev)
+        self.param = torch.empty((E, K), dtype=f64, device=dev)
+        self.nvars = torch.empty((E, K), dtype=i32, device=dev)
+        self.cuts = torch.empty((E, K - 1), dtype=i32, device=dev)
+        self.length = torch.zeros(E, dtype=f64, device=dev)
+        self.feasible = torch.zeros(E, dtype=u8, device=dev)
+        self.best_len = torch.full((E,), float("inf"), dtype=f64, device=dev)
+        self.best_picks = torch.full((E, P), -1, dtype=i32, device=dev)
+        self.best_episode = torch.full((E,), -1, dtype=torch.int64, device=dev)
+        self.ep_return = torch.zeros(E, dtype=f32, device=dev)
+        self.finished_return = torch.zeros(E, dtype=f32, device=dev)
+        self.episodes_done = torch.zeros(E, dtype=i32, device=dev)
+        self._ctl0 = torch.zeros(4, dtype=torch.int64, device=dev)
+        self._post(self._ctl0, 1, 0)  # initial masks / applied rows (nothing is done yet)
+        self._state_eval()
+
+    def _post(self, ctl, world, rank) -> None:
+        lib = _native.require_device()
+        P_ = _native.ptr
+        _native.check(lib.ap_vec_pipe_post(self.E, self.C, self.P, self.a_max, P_(self.length), P_(self.feasible),
+                                           P_(self.done), self.reward_shape, P_(self.dummy_pos), P_(self.rewards),
+                                           P_(self.picks), P_(self.positions), P_(self.n_applied),
+                                           P_(self.applied_state), P_(self.mask), P_(self.next_mask),
+                                           P_(self.best_len), P_(self.best_picks), P_(self.best_episode),
+                                           P_(self.ep_return), P_(self.finished_return), P_(self.episodes_done),
+                                           P_(ctl), int(world), int(rank), _s()))
+
+    def _state_eval(self) -> None:
+        import ctypes
+
+        lib = _native.require_device()
+        P_ = _native.ptr
+        _native.check(lib.ap_pipe_train_state(self.host._model.handle, ctypes.byref(self.topo_c), P_(self.cand_pos),
+                                              self.C, P_(self.applied_state), self.a_max, P_(self.mask), self.E,
+                                              self.bwm, P_(self.state64), _s()))
+        self.cur_state.copy_(self.state64)
+
+    def step(self, actions, step_base: int = 0, ctl=None, world: int = 1, rank: int = 0) -> None:
+        """Apply one pick per env (actions [E] int32, device); fills rewards / done /
+        next_state / next_mask and the post-reset cur_state / mask."""
+        import ctypes
+
+        lib = _native.require_device()
+        P_ = _native.ptr
+        self.obs.copy_(self.cur_state)
+        _native.check(lib.ap_vec_pipe_apply(self.E, self.P, P_(actions), P_(self.cand_pos), P_(self.picks),
+                                            P_(self.positions), P_(self.n_applied), P_(self.done), _s()))
+        _native.check(lib.ap_pipe_metrics(self.host._model.handle, P_(self.positions), self.E, self.P, self.bwm,
+                                          P_(self.comp), P_(self.act), P_(self.param), P_(self.nvars), _s()))
+        _native.check(lib.ap_pipe_length(ctypes.byref(self.topo_c), self.K, self.micro_batches, self.E, P_(self.comp),
+                                         P_(self.act), P_(self.param), P_(self.cuts), 0, self.mem, 4.0, 1,
+                                         P_(self.length), P_(self.feasible), _s()))
+        self._post(ctl if ctl is not None else self._ctl0, world, rank)
+        self._state_eval()
+        self.next_state.copy_(self.cur_state)
+
+    def best_plan(self):
+        """(pipeline length, pivot names, global episode id) of the best feasible finished
+        episode on this rank (min length, lowest episode id among ties), or None."""
+        import torch
+
+        valid = self.best_episode >= 0
+        if not bool(valid.any()):
+            return None
+        L = torch.where(valid, self.best_len, torch.full_like(self.best_len, float("inf")))
+        cand = valid & (L == L.min())
+        k = int(torch.argmin(torch.where(cand, self.best_episode, torch.full_like(self.best_episode, 1 << 62))))
+        picks = self.best_picks[k].tolist()
+        return float(self.best_len[k]), tuple(self.host.candidates[i] for i in picks), int(self.best_episode[k])
+
+
 class VecDqnTrainer:
     """Batched acting + device replay + (data-parallel) DQN learner over a VecPartitionEnv.
 
@@ -304,8 +427,11 @@ class VecDqnTrainer:
     # -- reporting ---------------------------------------------------------------------
 
     def best_plan(self) -> BestPlan | None:
-        """Best completed plan on this rank (max (partitions, return), lowest episode id)."""
+        """Best completed plan on this rank (max (partitions, return), lowest episode id);
+        for a VecPipeTrainEnv the env's own (length, pivots, episode) incumbent."""
         env = self.env
+        if isinstance(env, VecPipeTrainEnv):
+            return env.best_plan()
         k = select_first_wins(env.best_partitions, env.best_return, env.best_episode)
         if k is None:
             return None
@@ -313,8 +439,17 @@ class VecDqnTrainer:
                         env.best_status[k, : env.n].cpu().numpy().copy())
 
     def best_plan_global(self) -> BestPlan | None:
-        """Best completed plan over all ranks: one all-gather of (key, episode id, statuses)."""
+        """Best completed plan over all ranks: one all-gather of (key, episode id, statuses).
+        PP-train: key (0, -length) so the shortest pipeline wins; the row holds the picks."""
         env = self.env
+        if isinstance(env, VecPipeTrainEnv):
+            best = env.best_plan()
+            if best is None:
+                key, row = (-1, float("-inf"), -1), env.best_picks.new_full((env.P,), -1)
+            else:
+                k = int(torch_argmax_episode(env, best[2]))
+                key, row = (0, -best[0], best[2]), env.best_picks[k]
+            return reduce_best(key, row, self.pg)
         k = select_first_wins(env.best_partitions, env.best_return, env.best_episode)
         if k is None:
             key = (-1, float("-inf"), -1)
@@ -323,3 +458,10 @@ class VecDqnTrainer:
             key = (int(env.best_partitions[k]), float(env.best_return[k]), int(env.best_episode[k]))
             row = env.best_status[k, : env.n]
         return reduce_best(key, row, self.pg)
+
+
+def torch_argmax_episode(env, episode: int) -> int:
+    """Env index holding the incumbent with global episode id `episode`."""
+    import torch
+
+    return int(torch.nonzero(env.best_episode == episode)[0, 0])

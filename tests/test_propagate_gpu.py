@@ -197,11 +197,14 @@ def _wide_graph(blocks: int):
     return w.graph()
 
 
-@pytest.mark.parametrize("blocks,batch", [(80, 48), (1100, 48), (26000, 6)])
-def test_beyond_fast_kernel_limits_matches_oracle(cuda, blocks, batch):
+@pytest.mark.parametrize("blocks,batch,no_cta", [(80, 48, 0), (1100, 48, 0), (26000, 6, 0), (26000, 6, 1)])
+def test_beyond_fast_kernel_limits_matches_oracle(cuda, blocks, batch, no_cta, monkeypatch):
     """> 255 link classes (80 blocks: 320 classes), > 4096 candidate dims (1100 blocks:
     4400 dims) and > 65535 classes with bitsets beyond shared memory (26000 blocks:
-    104000 classes, 130000 instructions): the generic kernel matches the C oracle."""
+    104000 classes, 130000 instructions: one plan per CTA, or with no_cta the per-warp
+    bitsets in global memory): the generic kernels match the C oracle."""
+    if no_cta:
+        monkeypatch.setenv("AP_PROPAGATE_NO_CTA", "1")
     g = _wide_graph(blocks)
     dims = decision_dims(g, g.trainable_variables)
     n = len(dims)

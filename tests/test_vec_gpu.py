@@ -99,3 +99,66 @@ def test_cuda_graph_step_matches_eager(cuda):
     for k in ("cur_state", "episodes_done", "ep_return", "best_partitions", "best_episode"):
         assert torch.equal(getattr(a.env, k), getattr(b.env, k)), k
     assert (a.train_steps, a.vector_steps, a.size, a.slot) == (b.train_steps, b.vector_steps, b.size, b.slot)
+
+
+@pytest.mark.parametrize("K", [2, 3, 4])
+def test_vec_pipe_env_matches_single_envs(cuda, K):
+    """VecPipeTrainEnv (E envs on the device) vs E reference-exact PipeTrainEnv instances:
+    states (fp32 of the fp64 state), masks, rewards, done flags and the incumbent."""
+    from paper_2007_04069_b200.envs import PipeTrainEnv
+    from paper_2007_04069_b200.topology import DeviceTopology
+    from paper_2007_04069_b200.vec import VecPipeTrainEnv
+
+    g = graphs.generate("bert_base")
+    topo = DeviceTopology(2, 4)
+    E = 16
+    venv = VecPipeTrainEnv(g, topo, K, E)
+    singles = [PipeTrainEnv(g, topo, K) for _ in range(E)]
+    states = [s.reset() for s in singles]
+    rng = np.random.default_rng(K)
+    best = {}
+    for step in range(3 * K):
+        np.testing.assert_array_equal(venv.cur_state.cpu().numpy(), np.array(states, dtype=np.float32))
+        masks = [s.action_mask() for s in singles]
+        np.testing.assert_array_equal(venv.mask.cpu().numpy().astype(bool), np.array(masks))
+        actions = np.array([rng.choice(np.flatnonzero(m)) for m in masks], dtype=np.int32)
+        venv.step(torch.from_numpy(actions).cuda())
+        rewards, done = venv.rewards.cpu().numpy(), venv.done.cpu().numpy()
+        for e, env in enumerate(singles):
+            res = env.step(int(actions[e]))
+            assert bool(done[e]) == res.done
+            assert rewards[e] == np.float32(res.reward)
+            if res.done:
+                L = res.info["pipeline_length"]
+                if e not in best or L < best[e][0]:
+                    best[e] = (L, tuple(res.info["plan"].pivot_ids))
+                states[e] = env.reset()
+            else:
+                np.testing.assert_array_equal(venv.next_state[e].cpu().numpy(), res.next_state.astype(np.float32))
+                states[e] = res.next_state
+    got = venv.best_plan()
+    want = min(best.values(), key=lambda t: t[0])
+    assert got[0] == want[0]
+    assert got[1] in {v[1] for v in best.values() if v[0] == want[0]}
+
+
+def test_vec_pipe_trainer_graph_matches_eager(cuda):
+    """The PP-train driver inside the CUDA-graph DQN trainer: replay == eager, bit for bit."""
+    from paper_2007_04069_b200.topology import DeviceTopology
+    from paper_2007_04069_b200.vec import VecPipeTrainEnv
+
+    def run(use_graph):
+        env = VecPipeTrainEnv(graphs.generate("bert_base"), DeviceTopology(2, 4), 3, 32)
+        cfg = AgentConfig(lr=0.0005, epsilon_decay_iters=50, target_sync_every=4)
+        tr = VecDqnTrainer(env, cfg, capacity=256, seed=3, learn_steps=2, use_graph=use_graph)
+        for _ in range(8):
+            tr.step()
+        torch.cuda.synchronize()
+        return tr
+
+    a, b = run(False), run(True)
+    assert b.graph is not None
+    assert torch.equal(a.net.flat, b.net.flat)
+    assert torch.equal(a.env.cur_state, b.env.cur_state)
+    assert torch.equal(a.env.best_len, b.env.best_len)
+    assert int(a.env.episodes_done.sum()) > 0
