@@ -53,6 +53,7 @@ def parse_args():
     p.add_argument("--dqn-steps", type=int, default=30)
     p.add_argument("--dqn-eager", action="store_true", help="launch the vector step eagerly (no CUDA graph)")
     p.add_argument("--pp-envs", type=int, default=512, help="PP-train env states evaluated per launch")
+    p.add_argument("--pp-dqn-envs", type=int, default=1024, help="vectorised PP-train DQN envs per GPU")
     p.add_argument("--single-steps", type=int, default=300)
     return p.parse_args()
 
@@ -386,6 +387,7 @@ def run_ours(args):
     if not args.no_secondary:
         want_cpu = rank == 0 and world == 1 and not args.no_cpu_baseline
         secondary["dqn_env_steps_per_s"] = bench_dqn_vec(args, g, world, rank)
+        secondary["dqn_env_steps_per_s_pp_train"] = bench_dqn_pipe(args, g, world, rank)
         secondary["pp_train_candidates_per_s"] = bench_pp_train(args, world, want_cpu)
         secondary["pp_infer_points_per_s"] = bench_pp_infer(args, world, want_cpu)
         if rank == 0 and world == 1:
@@ -454,6 +456,50 @@ def _max_over_ranks(x: float, world: int) -> float:
     from paper_2007_04069_b200.distributed import max_over_ranks
 
     return max_over_ranks(x) if world > 1 else float(x)
+
+
+def bench_dqn_pipe(args, g, world, rank):
+    """Throughput-mode DQN on PP-train (BERT-48, 2x4, K=4): E VecPipeTrainEnv episodes per GPU, each vector
+    step = act (state 4C wide) + pick + terminal metrics / length + K2 next states + L learn steps."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2007_04069_b200.agent import AgentConfig
+    from paper_2007_04069_b200.topology import DeviceTopology
+    from paper_2007_04069_b200.vec import VecDqnTrainer, VecPipeTrainEnv
+
+    E, L = args.pp_dqn_envs, args.dqn_learn_steps
+    env = VecPipeTrainEnv(g, DeviceTopology(2, 4), 4, E)
+    cfg = AgentConfig(lr=0.0005, epsilon_decay_iters=2000)
+    pg = dist.group.WORLD if world > 1 else None
+    tr = VecDqnTrainer(env, cfg, capacity=4 * E, seed=rank, learn_steps=L, process_group=pg, use_graph=True)
+    for _ in range(5):
+        tr.step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(args.dqn_steps):
+        tr.step()
+    e.record()
+    torch.cuda.synchronize()
+    ms = _max_over_ranks(s.elapsed_time(e), world)
+    best = tr.best_plan_global()
+    return {
+        "value": world * E * args.dqn_steps / (ms / 1e3),
+        "unit": "env-steps/s",
+        "config": {"graph": "bert48", "task": "pp-train", "topology": "2x4", "stages": 4, "radius": 3,
+                   "candidates": env.C, "state_dim": env.state_dim, "envs_per_gpu": E,
+                   "learn_steps_per_vector_step": L, "learn_batch": cfg.batch_size,
+                   "learn_to_env_step_ratio": f"{L}:{E}", "hidden": list(cfg.hidden), "replay_capacity": tr.capacity,
+                   "vector_steps": args.dqn_steps, "cuda_graph": tr.graph is not None},
+        "ms_per_vector_step": ms / args.dqn_steps,
+        "episodes_finished_rank0": int(env.episodes_done.sum().item()),
+        "best_plan": None if best is None else {"pipeline_length": -best.reward, "global_episode": best.episode},
+        "reference_note": "reference PipeTrainEnv._state takes seconds per state on the host (pp_train_candidates_per_s "
+                          "cpu_baseline), i.e. < 1 env-step/s",
+    }
 
 
 def bench_dqn_vec(args, g, world, rank):
