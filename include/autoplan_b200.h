@@ -379,6 +379,21 @@ int ap_vec_pipe_post(int32_t E, int32_t C, int32_t P, int32_t a_max, const doubl
                      uint8_t* next_mask, double* best_len, int32_t* best_picks, int64_t* best_episode,
                      float* ep_return, float* finished_return, int32_t* episodes_done, const int64_t* ctl,
                      int32_t world, int32_t rank, void* stream);
+/* Vectorised PipeInferEnv (envs.py:407-626): bnd / cut [E, P] picks (boundaries in
+ * 1..G-1, device cuts in 1..D-1), nb / nc [E]; ap_vec_infer_apply routes action a
+ * (a < G-1: boundary a+1, else cut a-(G-1)+1) and flags finished envs.
+ * ap_vec_infer_post (after ap_infer_length over every row): terminal rewards
+ * 1 / max(L, 1e-12), incumbents (min L, strict <), reset to the dummy tails, the
+ * phased action mask [E, (G-1)+(D-1)] within the per-pick bands band_b [P, G] /
+ * band_c [P, D] (1 = allowed), and the 2P pick slots at the end of each fp32 state row. */
+int ap_vec_infer_apply(int32_t E, int32_t P, int32_t G, const int32_t* actions, int32_t* bnd, int32_t* cut,
+                       int32_t* nb, int32_t* nc, uint8_t* done, void* stream);
+int ap_vec_infer_post(int32_t E, int32_t P, int32_t G, int32_t D, int32_t S, const double* length,
+                      const uint8_t* done, const int32_t* dummy_b, const int32_t* dummy_c, const uint8_t* band_b,
+                      const uint8_t* band_c, float* rewards, int32_t* bnd, int32_t* cut, int32_t* nb, int32_t* nc,
+                      uint8_t* mask, uint8_t* next_mask, float* state, double* best_len, int32_t* best_b,
+                      int32_t* best_c, int64_t* best_episode, float* ep_return, float* finished_return,
+                      int32_t* episodes_done, const int64_t* ctl, int32_t world, int32_t rank, void* stream);
 /* mode 0: ctl[3] += 1 (one learn step); mode 1: ctl[0] += 1, ctl[1] = (ctl[1] + E) % cap,
  * ctl[2] = min(ctl[2] + E, cap) (one vector step) */
 int ap_vec_ctl_advance(int64_t* ctl, int32_t mode, int64_t E, int64_t cap, void* stream);

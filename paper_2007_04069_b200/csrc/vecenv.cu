@@ -353,6 +353,91 @@ __global__ void vec_pipe_post_kernel(int E, int C, int P, int a_max, const doubl
   }
 }
 
+// ---- vectorised PipeInferEnv (envs.py:407-626) --------------------------------
+// bnd / cut [E, P] boundaries in 1..G-1 and device cuts in 1..D-1 (dummy tails keep
+// every row a legal point for the batched length kernel), nb / nc [E] counts.
+__global__ void vec_infer_apply_kernel(int E, int P, int G, const int32_t* actions, int32_t* bnd, int32_t* cut,
+                                       int32_t* nb, int32_t* nc, uint8_t* done) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const int a = actions[e];
+  if (a < G - 1) {
+    bnd[(int64_t)e * P + nb[e]] = a + 1;
+    nb[e] += 1;
+  } else {
+    cut[(int64_t)e * P + nc[e]] = a - (G - 1) + 1;
+    nc[e] += 1;
+  }
+  done[e] = nc[e] == P ? 1 : 0;
+}
+
+// Terminal rewards 1 / max(L, 1e-12), incumbents (min L, strict <), reset,
+// the phased action mask (boundaries, then cuts, each increasing and leaving
+// room for the picks still owed, within the per-pick bands: envs.py:447-469)
+// and the pick slots of the state (b / G, c / D after the static part).
+__global__ void vec_infer_post_kernel(int E, int P, int G, int D, int S, const double* length, const uint8_t* done,
+                                      const int32_t* dummy_b, const int32_t* dummy_c, const uint8_t* band_b,
+                                      const uint8_t* band_c, float* rewards, int32_t* bnd, int32_t* cut,
+                                      int32_t* nb, int32_t* nc, uint8_t* mask, uint8_t* next_mask, float* state,
+                                      double* best_len, int32_t* best_b, int32_t* best_c, int64_t* best_episode,
+                                      float* ep_return, float* finished_return, int32_t* episodes_done,
+                                      const int64_t* ctl, int world, int rank) {
+  const int e = blockIdx.x;
+  const bool fin = done[e] != 0;
+  __shared__ int s_nb, s_nc, s_lb, s_lc;
+  if (threadIdx.x == 0) {
+    float r = 0.0f;
+    if (fin) {
+      const double L = fmax(length[e], 1e-12);
+      r = (float)(1.0 / L);
+      if (L < best_len[e]) {
+        best_len[e] = L;
+        for (int k = 0; k < P; ++k) {
+          best_b[(int64_t)e * P + k] = bnd[(int64_t)e * P + k];
+          best_c[(int64_t)e * P + k] = cut[(int64_t)e * P + k];
+        }
+        best_episode[e] = (ctl[AP_CTL_STEP] * world + rank) * (int64_t)E + e;
+      }
+      finished_return[e] = ep_return[e] + r;
+      ep_return[e] = 0.0f;
+      episodes_done[e] += 1;
+      nb[e] = 0;
+      nc[e] = 0;
+      for (int k = 0; k < P; ++k) {
+        bnd[(int64_t)e * P + k] = dummy_b[k];
+        cut[(int64_t)e * P + k] = dummy_c[k];
+      }
+    } else {
+      ep_return[e] += r;
+    }
+    rewards[e] = r;
+    s_nb = nb[e];
+    s_nc = nc[e];
+    s_lb = s_nb > 0 ? bnd[(int64_t)e * P + s_nb - 1] : 0;
+    s_lc = s_nc > 0 ? cut[(int64_t)e * P + s_nc - 1] : 0;
+    float* slots = state + (int64_t)e * S + (S - 2 * P);
+    for (int k = 0; k < P; ++k) {
+      slots[k] = k < s_nb ? (float)((double)bnd[(int64_t)e * P + k] / (double)G) : 0.0f;
+      slots[P + k] = k < s_nc ? (float)((double)cut[(int64_t)e * P + k] / (double)D) : 0.0f;
+    }
+  }
+  __syncthreads();
+  const int A = (G - 1) + (D - 1);
+  const bool bphase = s_nb < P;
+  for (int j = threadIdx.x; j < A; j += blockDim.x) {
+    uint8_t m = 0;
+    if (bphase && j < G - 1) {
+      const int b = j + 1;
+      m = b > s_lb && b <= G - (P - s_nb) && band_b[(int64_t)s_nb * G + b];
+    } else if (!bphase && j >= G - 1) {
+      const int c = j - (G - 1) + 1;
+      m = c > s_lc && c <= D - (P - s_nc) && band_c[(int64_t)s_nc * D + c];
+    }
+    mask[(int64_t)e * A + j] = m;
+    next_mask[(int64_t)e * A + j] = fin ? 0 : m;
+  }
+}
+
 // mode 0: one learn step done (train counter); mode 1: one vector step done
 // (step counter, ring slot and size after pushing E transitions)
 __global__ void ctl_advance_kernel(int64_t* ctl, int mode, int64_t E, int64_t cap) {
@@ -499,6 +584,36 @@ int ap_vec_pipe_post(int32_t E, int32_t C, int32_t P, int32_t a_max, const doubl
       E, C, P, a_max, length, feasible, done, reward_shape, dummy_pos, rewards, picks, positions, n_applied,
       applied_state, mask, next_mask, best_len, best_picks, best_episode, ep_return, finished_return, episodes_done,
       ctl, world, rank);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_vec_infer_apply(int32_t E, int32_t P, int32_t G, const int32_t* actions, int32_t* bnd, int32_t* cut,
+                       int32_t* nb, int32_t* nc, uint8_t* done, void* stream) {
+  if (E < 0 || P < 1 || G < 2 || (E > 0 && (!actions || !bnd || !cut || !nb || !nc || !done))) {
+    set_error("ap_vec_infer_apply: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  if (E == 0) return AP_OK;
+  vec_infer_apply_kernel<<<(E + 255) / 256, 256, 0, (cudaStream_t)stream>>>(E, P, G, actions, bnd, cut, nb, nc, done);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_vec_infer_post(int32_t E, int32_t P, int32_t G, int32_t D, int32_t S, const double* length,
+                      const uint8_t* done, const int32_t* dummy_b, const int32_t* dummy_c, const uint8_t* band_b,
+                      const uint8_t* band_c, float* rewards, int32_t* bnd, int32_t* cut, int32_t* nb, int32_t* nc,
+                      uint8_t* mask, uint8_t* next_mask, float* state, double* best_len, int32_t* best_b,
+                      int32_t* best_c, int64_t* best_episode, float* ep_return, float* finished_return,
+                      int32_t* episodes_done, const int64_t* ctl, int32_t world, int32_t rank, void* stream) {
+  if (E < 0 || P < 1 || G < 2 || D < 2 || S < 2 * P || !ctl || world < 1 || rank < 0 || rank >= world) {
+    set_error("ap_vec_infer_post: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  if (E == 0) return AP_OK;
+  vec_infer_post_kernel<<<E, 128, 0, (cudaStream_t)stream>>>(
+      E, P, G, D, S, length, done, dummy_b, dummy_c, band_b, band_c, rewards, bnd, cut, nb, nc, mask, next_mask, state,
+      best_len, best_b, best_c, best_episode, ep_return, finished_return, episodes_done, ctl, world, rank);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }

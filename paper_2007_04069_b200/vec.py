@@ -232,6 +232,115 @@ class VecPipeTrainEnv:
         return float(self.best_len[k]), tuple(self.host.candidates[i] for i in picks), int(self.best_episode[k])
 
 
+class VecPipeInferEnv:
+    """E PipeInferEnv episodes (envs.py:407-626) stepping in lockstep on the device.
+
+    Boundaries first, then device cuts (ap_vec_infer_apply); every row's point is
+    evaluated by the batched PP-infer length kernel (ap_infer_length, dummy tails
+    keep unfinished rows legal); ap_vec_infer_post pays 1 / L on the last cut,
+    keeps per-env incumbents, resets, and rebuilds the phased masks and the pick
+    slots of the fp32 state (static part: C*, A*, W*, normalised bandwidths).
+    """
+
+    def __init__(self, arrays, topo, num_stages: int, E: int, micro_batches: int = 1,
+                 allowed_boundaries=None, allowed_cuts=None):
+        import ctypes  # noqa: F401
+
+        import torch
+
+        from .envs import GRANULARITY, PipeInferEnv
+
+        host = PipeInferEnv(arrays, topo, num_stages, micro_batches=micro_batches,
+                            allowed_boundaries=allowed_boundaries, allowed_cuts=allowed_cuts)
+        self.host = host
+        self.E, self.K, self.P = E, num_stages, num_stages - 1
+        self.G, self.D = GRANULARITY, topo.num_devices
+        self.num_actions = host.num_actions
+        self.state_dim = S = host.state_dim
+        self.micro_batches = micro_batches
+        self.topo_c = _native.Topology.of(host.topo_norm)
+        dev = "cuda"
+        i32, u8, f64, f32 = torch.int32, torch.uint8, torch.float64, torch.float32
+        P, G, D = self.P, self.G, self.D
+        self.arrays_dev = host._arrays_dev()
+        self.dummy_b = torch.arange(G - P, G, dtype=i32, device=dev)
+        self.dummy_c = torch.arange(D - P, D, dtype=i32, device=dev)
+        band_b = np.ones((P, G), np.uint8)
+        band_c = np.ones((P, D), np.uint8)
+        for k in range(P):
+            if allowed_boundaries is not None:
+                band_b[k] = 0
+                band_b[k, sorted(allowed_boundaries[k])] = 1
+            if allowed_cuts is not None:
+                band_c[k] = 0
+                band_c[k, sorted(allowed_cuts[k])] = 1
+        self.band_b = torch.from_numpy(band_b).to(dev)
+        self.band_c = torch.from_numpy(band_c).to(dev)
+        self.bnd = self.dummy_b.repeat(E, 1).contiguous()
+        self.cut = self.dummy_c.repeat(E, 1).contiguous()
+        self.nb = torch.zeros(E, dtype=i32, device=dev)
+        self.nc = torch.zeros(E, dtype=i32, device=dev)
+        self.done = torch.zeros(E, dtype=u8, device=dev)
+        A = self.num_actions
+        self.mask = torch.zeros((E, A), dtype=u8, device=dev)
+        self.next_mask = torch.zeros((E, A), dtype=u8, device=dev)
+        static = torch.from_numpy(host._static.astype(np.float32)).to(dev)
+        self.cur_state = torch.zeros((E, S), dtype=f32, device=dev)
+        self.cur_state[:, : S - 2 * P] = static
+        self.obs = torch.empty_like(self.cur_state)
+        self.next_state = torch.empty_like(self.cur_state)
+        self.rewards = torch.zeros(E, dtype=f32, device=dev)
+        self.length = torch.zeros(E, dtype=f64, device=dev)
+        self.best_len = torch.full((E,), float("inf"), dtype=f64, device=dev)
+        self.best_b = torch.full((E, P), -1, dtype=i32, device=dev)
+        self.best_c = torch.full((E, P), -1, dtype=i32, device=dev)
+        self.best_episode = torch.full((E,), -1, dtype=torch.int64, device=dev)
+        self.ep_return = torch.zeros(E, dtype=f32, device=dev)
+        self.finished_return = torch.zeros(E, dtype=f32, device=dev)
+        self.episodes_done = torch.zeros(E, dtype=i32, device=dev)
+        self._ctl0 = torch.zeros(4, dtype=torch.int64, device=dev)
+        self._post(self._ctl0, 1, 0)
+
+    def _post(self, ctl, world, rank) -> None:
+        lib = _native.require_device()
+        P_ = _native.ptr
+        _native.check(lib.ap_vec_infer_post(self.E, self.P, self.G, self.D, self.state_dim, P_(self.length),
+                                            P_(self.done), P_(self.dummy_b), P_(self.dummy_c), P_(self.band_b),
+                                            P_(self.band_c), P_(self.rewards), P_(self.bnd), P_(self.cut),
+                                            P_(self.nb), P_(self.nc), P_(self.mask), P_(self.next_mask),
+                                            P_(self.cur_state), P_(self.best_len), P_(self.best_b), P_(self.best_c),
+                                            P_(self.best_episode), P_(self.ep_return), P_(self.finished_return),
+                                            P_(self.episodes_done), P_(ctl), int(world), int(rank), _s()))
+
+    def step(self, actions, step_base: int = 0, ctl=None, world: int = 1, rank: int = 0) -> None:
+        import ctypes
+
+        lib = _native.require_device()
+        P_ = _native.ptr
+        self.obs.copy_(self.cur_state)
+        _native.check(lib.ap_vec_infer_apply(self.E, self.P, self.G, P_(actions), P_(self.bnd), P_(self.cut),
+                                             P_(self.nb), P_(self.nc), P_(self.done), _s()))
+        _native.check(lib.ap_infer_length(P_(self.arrays_dev), self.G, ctypes.byref(self.topo_c), self.K,
+                                          self.micro_batches, P_(self.bnd), P_(self.cut), self.E, P_(self.length),
+                                          _s()))
+        self._post(ctl if ctl is not None else self._ctl0, world, rank)
+        self.next_state.copy_(self.cur_state)
+
+    def best_plan(self):
+        """(pipeline length, boundaries, device cuts, global episode id) of the best finished
+        episode on this rank (min length, lowest episode id among ties), or None."""
+        import torch
+
+        valid = self.best_episode >= 0
+        if not bool(valid.any()):
+            return None
+        L = torch.where(valid, self.best_len, torch.full_like(self.best_len, float("inf")))
+        cand = valid & (L == L.min())
+        k = int(torch.argmin(torch.where(cand, self.best_episode, torch.full_like(self.best_episode, 1 << 62))))
+        return (float(self.best_len[k]), tuple(self.best_b[k].tolist()), tuple(self.best_c[k].tolist()),
+                int(self.best_episode[k]))
+
+
 class VecDqnTrainer:
     """Batched acting + device replay + (data-parallel) DQN learner over a VecPartitionEnv.
 
@@ -428,9 +537,9 @@ class VecDqnTrainer:
 
     def best_plan(self) -> BestPlan | None:
         """Best completed plan on this rank (max (partitions, return), lowest episode id);
-        for a VecPipeTrainEnv the env's own (length, pivots, episode) incumbent."""
+        for the PP envs the env's own (length, picks..., episode) incumbent."""
         env = self.env
-        if isinstance(env, VecPipeTrainEnv):
+        if isinstance(env, (VecPipeTrainEnv, VecPipeInferEnv)):
             return env.best_plan()
         k = select_first_wins(env.best_partitions, env.best_return, env.best_episode)
         if k is None:
@@ -440,15 +549,19 @@ class VecDqnTrainer:
 
     def best_plan_global(self) -> BestPlan | None:
         """Best completed plan over all ranks: one all-gather of (key, episode id, statuses).
-        PP-train: key (0, -length) so the shortest pipeline wins; the row holds the picks."""
+        PP envs: key (0, -length) so the shortest pipeline wins; the row holds the picks
+        (PP-train pivots, or PP-infer boundaries followed by cuts)."""
         env = self.env
-        if isinstance(env, VecPipeTrainEnv):
+        if isinstance(env, (VecPipeTrainEnv, VecPipeInferEnv)):
+            import torch
+
             best = env.best_plan()
+            picks = env.best_picks if isinstance(env, VecPipeTrainEnv) else torch.cat([env.best_b, env.best_c], 1)
             if best is None:
-                key, row = (-1, float("-inf"), -1), env.best_picks.new_full((env.P,), -1)
+                key, row = (-1, float("-inf"), -1), picks.new_full((picks.shape[1],), -1)
             else:
-                k = int(torch_argmax_episode(env, best[2]))
-                key, row = (0, -best[0], best[2]), env.best_picks[k]
+                k = int(torch_argmax_episode(env, best[-1]))
+                key, row = (0, -best[0], best[-1]), picks[k]
             return reduce_best(key, row, self.pg)
         k = select_first_wins(env.best_partitions, env.best_return, env.best_episode)
         if k is None:

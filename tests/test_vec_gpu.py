@@ -162,3 +162,46 @@ def test_vec_pipe_trainer_graph_matches_eager(cuda):
     assert torch.equal(a.env.cur_state, b.env.cur_state)
     assert torch.equal(a.env.best_len, b.env.best_len)
     assert int(a.env.episodes_done.sum()) > 0
+
+
+@pytest.mark.parametrize("K,banded", [(2, False), (4, True), (4, False)])
+def test_vec_infer_env_matches_single_envs(cuda, K, banded):
+    """VecPipeInferEnv vs E reference-exact PipeInferEnv instances: states, phased masks,
+    rewards, done flags and the incumbent."""
+    from paper_2007_04069_b200.dataproc import generate_environment
+    from paper_2007_04069_b200.envs import PipeInferEnv, infer_search_bands
+    from paper_2007_04069_b200.topology import PRESETS
+    from paper_2007_04069_b200.vec import VecPipeInferEnv
+
+    arrays = generate_environment("uniform", 1280, K)
+    topo = PRESETS["configc"]
+    kw = {}
+    if banded:
+        bb, cc = infer_search_bands(arrays, topo, K, 3)
+        kw = {"allowed_boundaries": bb, "allowed_cuts": cc}
+    E = 12
+    venv = VecPipeInferEnv(arrays, topo, K, E, **kw)
+    singles = [PipeInferEnv(arrays, topo, K, **kw) for _ in range(E)]
+    states = [s.reset() for s in singles]
+    rng = np.random.default_rng(K + banded)
+    best = []
+    for step in range(5 * (K - 1)):
+        np.testing.assert_array_equal(venv.cur_state.cpu().numpy(), np.array(states, dtype=np.float32))
+        masks = [s.action_mask() for s in singles]
+        np.testing.assert_array_equal(venv.mask.cpu().numpy().astype(bool), np.array(masks))
+        actions = np.array([rng.choice(np.flatnonzero(m)) for m in masks], dtype=np.int32)
+        venv.step(torch.from_numpy(actions).cuda())
+        rewards, done = venv.rewards.cpu().numpy(), venv.done.cpu().numpy()
+        for e, env in enumerate(singles):
+            res = env.step(int(actions[e]))
+            assert bool(done[e]) == res.done
+            assert rewards[e] == np.float32(res.reward)
+            if res.done:
+                best.append((res.info["pipeline_length"], env.boundaries, env.device_cuts))
+                states[e] = env.reset()
+            else:
+                states[e] = res.next_state
+    got = venv.best_plan()
+    want = min(b[0] for b in best)
+    assert got[0] == want
+    assert (got[1], got[2]) in {(b[1], b[2]) for b in best if b[0] == want}
