@@ -388,6 +388,7 @@ def run_ours(args):
         want_cpu = rank == 0 and world == 1 and not args.no_cpu_baseline
         secondary["dqn_env_steps_per_s"] = bench_dqn_vec(args, g, world, rank)
         secondary["dqn_env_steps_per_s_pp_train"] = bench_dqn_pipe(args, g, world, rank)
+        secondary["dqn_env_steps_per_s_pp_infer"] = bench_dqn_infer(args, world, rank)
         secondary["pp_train_candidates_per_s"] = bench_pp_train(args, world, want_cpu)
         secondary["pp_infer_points_per_s"] = bench_pp_infer(args, world, want_cpu)
         if rank == 0 and world == 1:
@@ -499,6 +500,54 @@ def bench_dqn_pipe(args, g, world, rank):
         "best_plan": None if best is None else {"pipeline_length": -best.reward, "global_episode": best.episode},
         "reference_note": "reference PipeTrainEnv._state takes seconds per state on the host (pp_train_candidates_per_s "
                           "cpu_baseline), i.e. < 1 env-step/s",
+    }
+
+
+def bench_dqn_infer(args, world, rank):
+    """Throughput-mode DQN on PP-infer (configC, K=4, banded as in the paper's search): E VecPipeInferEnv
+    episodes per GPU, each vector step = act + pick + batched terminal lengths + L learn steps."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2007_04069_b200.agent import AgentConfig
+    from paper_2007_04069_b200.dataproc import generate_environment
+    from paper_2007_04069_b200.envs import infer_search_bands
+    from paper_2007_04069_b200.topology import PRESETS
+    from paper_2007_04069_b200.vec import VecDqnTrainer, VecPipeInferEnv
+
+    E, L = args.dqn_envs, args.dqn_learn_steps
+    arrays = generate_environment("uniform", 1280, 0)
+    topo = PRESETS["configc"]
+    bb, cc = infer_search_bands(arrays, topo, 4, 3)
+    env = VecPipeInferEnv(arrays, topo, 4, E, allowed_boundaries=bb, allowed_cuts=cc)
+    cfg = AgentConfig(lr=0.0005, epsilon_decay_iters=2000)
+    pg = dist.group.WORLD if world > 1 else None
+    tr = VecDqnTrainer(env, cfg, capacity=max(4 * E, 4096), seed=rank, learn_steps=L, process_group=pg,
+                       use_graph=True)
+    for _ in range(5):
+        tr.step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(args.dqn_steps):
+        tr.step()
+    e.record()
+    torch.cuda.synchronize()
+    ms = _max_over_ranks(s.elapsed_time(e), world)
+    best = tr.best_plan_global()
+    return {
+        "value": world * E * args.dqn_steps / (ms / 1e3),
+        "unit": "env-steps/s",
+        "config": {"profile": "generate_environment(uniform, 1280, 0)", "topology": "configc", "stages": 4,
+                   "bands": "infer_search_bands(radius 3)", "state_dim": env.state_dim, "actions": env.num_actions,
+                   "envs_per_gpu": E, "learn_steps_per_vector_step": L, "learn_batch": cfg.batch_size,
+                   "learn_to_env_step_ratio": f"{L}:{E}", "hidden": list(cfg.hidden), "vector_steps": args.dqn_steps,
+                   "cuda_graph": tr.graph is not None},
+        "ms_per_vector_step": ms / args.dqn_steps,
+        "episodes_finished_rank0": int(env.episodes_done.sum().item()),
+        "best_plan": None if best is None else {"pipeline_length": -best.reward, "global_episode": best.episode},
     }
 
 
