@@ -385,10 +385,11 @@ int ap_vec_pipe_post(int32_t E, int32_t C, int32_t P, int32_t a_max, const doubl
  * ap_vec_infer_post (after ap_infer_length over every row): terminal rewards
  * 1 / max(L, 1e-12), incumbents (min L, strict <), reset to the dummy tails, the
  * phased action mask [E, (G-1)+(D-1)] within the per-pick bands band_b [P, G] /
- * band_c [P, D] (1 = allowed), and the 2P pick slots at the end of each fp32 state row. */
+ * band_c [P, D] (1 = allowed), and the 2P pick slots at the end of each fp32 state row
+ * (S wide, row stride ld_state). */
 int ap_vec_infer_apply(int32_t E, int32_t P, int32_t G, const int32_t* actions, int32_t* bnd, int32_t* cut,
                        int32_t* nb, int32_t* nc, uint8_t* done, void* stream);
-int ap_vec_infer_post(int32_t E, int32_t P, int32_t G, int32_t D, int32_t S, const double* length,
+int ap_vec_infer_post(int32_t E, int32_t P, int32_t G, int32_t D, int32_t S, int64_t ld_state, const double* length,
                       const uint8_t* done, const int32_t* dummy_b, const int32_t* dummy_c, const uint8_t* band_b,
                       const uint8_t* band_c, float* rewards, int32_t* bnd, int32_t* cut, int32_t* nb, int32_t* nc,
                       uint8_t* mask, uint8_t* next_mask, float* state, double* best_len, int32_t* best_b,

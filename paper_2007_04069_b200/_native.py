@@ -150,7 +150,7 @@ SIGNATURES: dict[str, tuple] = {
     "ap_vec_pipe_post": (ctypes.c_int, [_I32, _I32, _I32, _I32, _VP, _VP, _VP, _I32, _VP, _VP, _VP, _VP, _VP, _VP,
                                         _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I32, _I32, _VP]),
     "ap_vec_infer_apply": (ctypes.c_int, [_I32, _I32, _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
-    "ap_vec_infer_post": (ctypes.c_int, [_I32, _I32, _I32, _I32, _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
+    "ap_vec_infer_post": (ctypes.c_int, [_I32, _I32, _I32, _I32, _I32, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
                                          _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I32, _I32,
                                          _VP]),
     "ap_vec_ctl_advance": (ctypes.c_int, [_VP, _I32, _I64, _I64, _VP]),

@@ -111,7 +111,8 @@ class QNetwork:
         # [out, in] copies of every weight: the forward GEMMs then read both
         # operands K-major (the pipelined tcgen05 kernel); refreshed whenever
         # the parameters change
-        self.wt = {name: torch.empty((s[1], s[0]), dtype=torch.float32, device="cuda")
+        # (rows padded to a 16-byte stride: the TMA-fed GEMM needs it for any fan-in)
+        self.wt = {name: torch.empty((s[1], (s[0] + 3) // 4 * 4), dtype=torch.float32, device="cuda")[:, : s[0]]
                    for name, s in shapes if len(s) == 2}
         if _init:
             rng = rng or np.random.default_rng(0)

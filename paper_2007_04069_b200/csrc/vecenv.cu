@@ -375,7 +375,8 @@ __global__ void vec_infer_apply_kernel(int E, int P, int G, const int32_t* actio
 // the phased action mask (boundaries, then cuts, each increasing and leaving
 // room for the picks still owed, within the per-pick bands: envs.py:447-469)
 // and the pick slots of the state (b / G, c / D after the static part).
-__global__ void vec_infer_post_kernel(int E, int P, int G, int D, int S, const double* length, const uint8_t* done,
+__global__ void vec_infer_post_kernel(int E, int P, int G, int D, int S, int64_t lds, const double* length,
+                                      const uint8_t* done,
                                       const int32_t* dummy_b, const int32_t* dummy_c, const uint8_t* band_b,
                                       const uint8_t* band_c, float* rewards, int32_t* bnd, int32_t* cut,
                                       int32_t* nb, int32_t* nc, uint8_t* mask, uint8_t* next_mask, float* state,
@@ -415,7 +416,7 @@ __global__ void vec_infer_post_kernel(int E, int P, int G, int D, int S, const d
     s_nc = nc[e];
     s_lb = s_nb > 0 ? bnd[(int64_t)e * P + s_nb - 1] : 0;
     s_lc = s_nc > 0 ? cut[(int64_t)e * P + s_nc - 1] : 0;
-    float* slots = state + (int64_t)e * S + (S - 2 * P);
+    float* slots = state + (int64_t)e * lds + (S - 2 * P);
     for (int k = 0; k < P; ++k) {
       slots[k] = k < s_nb ? (float)((double)bnd[(int64_t)e * P + k] / (double)G) : 0.0f;
       slots[P + k] = k < s_nc ? (float)((double)cut[(int64_t)e * P + k] / (double)D) : 0.0f;
@@ -600,19 +601,21 @@ int ap_vec_infer_apply(int32_t E, int32_t P, int32_t G, const int32_t* actions, 
   return AP_OK;
 }
 
-int ap_vec_infer_post(int32_t E, int32_t P, int32_t G, int32_t D, int32_t S, const double* length,
+int ap_vec_infer_post(int32_t E, int32_t P, int32_t G, int32_t D, int32_t S, int64_t ld_state, const double* length,
                       const uint8_t* done, const int32_t* dummy_b, const int32_t* dummy_c, const uint8_t* band_b,
                       const uint8_t* band_c, float* rewards, int32_t* bnd, int32_t* cut, int32_t* nb, int32_t* nc,
                       uint8_t* mask, uint8_t* next_mask, float* state, double* best_len, int32_t* best_b,
                       int32_t* best_c, int64_t* best_episode, float* ep_return, float* finished_return,
                       int32_t* episodes_done, const int64_t* ctl, int32_t world, int32_t rank, void* stream) {
-  if (E < 0 || P < 1 || G < 2 || D < 2 || S < 2 * P || !ctl || world < 1 || rank < 0 || rank >= world) {
+  if (E < 0 || P < 1 || G < 2 || D < 2 || S < 2 * P || ld_state < S || !ctl || world < 1 || rank < 0 ||
+      rank >= world) {
     set_error("ap_vec_infer_post: bad arguments");
     return AP_ERR_INVALID;
   }
   if (E == 0) return AP_OK;
   vec_infer_post_kernel<<<E, 128, 0, (cudaStream_t)stream>>>(
-      E, P, G, D, S, length, done, dummy_b, dummy_c, band_b, band_c, rewards, bnd, cut, nb, nc, mask, next_mask, state,
+      E, P, G, D, S, ld_state, length, done, dummy_b, dummy_c, band_b, band_c, rewards, bnd, cut, nb, nc, mask,
+      next_mask, state,
       best_len, best_b, best_c, best_episode, ep_return, finished_return, episodes_done, ctl, world, rank);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;

@@ -285,10 +285,12 @@ class VecPipeInferEnv:
         self.mask = torch.zeros((E, A), dtype=u8, device=dev)
         self.next_mask = torch.zeros((E, A), dtype=u8, device=dev)
         static = torch.from_numpy(host._static.astype(np.float32)).to(dev)
-        self.cur_state = torch.zeros((E, S), dtype=f32, device=dev)
+        # state rows padded to a 16-byte stride (TMA-fed GEMMs need it), width S
+        ld = (S + 3) // 4 * 4
+        self.cur_state = torch.zeros((E, ld), dtype=f32, device=dev)[:, :S]
         self.cur_state[:, : S - 2 * P] = static
-        self.obs = torch.empty_like(self.cur_state)
-        self.next_state = torch.empty_like(self.cur_state)
+        self.obs = torch.zeros((E, ld), dtype=f32, device=dev)[:, :S]
+        self.next_state = torch.zeros((E, ld), dtype=f32, device=dev)[:, :S]
         self.rewards = torch.zeros(E, dtype=f32, device=dev)
         self.length = torch.zeros(E, dtype=f64, device=dev)
         self.best_len = torch.full((E,), float("inf"), dtype=f64, device=dev)
@@ -304,7 +306,8 @@ class VecPipeInferEnv:
     def _post(self, ctl, world, rank) -> None:
         lib = _native.require_device()
         P_ = _native.ptr
-        _native.check(lib.ap_vec_infer_post(self.E, self.P, self.G, self.D, self.state_dim, P_(self.length),
+        _native.check(lib.ap_vec_infer_post(self.E, self.P, self.G, self.D, self.state_dim,
+                                            self.cur_state.stride(0), P_(self.length),
                                             P_(self.done), P_(self.dummy_b), P_(self.dummy_c), P_(self.band_b),
                                             P_(self.band_c), P_(self.rewards), P_(self.bnd), P_(self.cut),
                                             P_(self.nb), P_(self.nc), P_(self.mask), P_(self.next_mask),
@@ -393,7 +396,8 @@ class VecDqnTrainer:
         self.slot = 0
         self.actions = torch.empty(env.E, dtype=torch.int32, device=dev)
         self.batch = _Batch(config.batch_size, S, A)
-        self.sn = torch.empty((2 * config.batch_size, S), dtype=torch.float32, device=dev)
+        # [2B, S] with rows padded to a 16-byte stride (TMA operand rule)
+        self.sn = torch.empty((2 * config.batch_size, (S + 3) // 4 * 4), dtype=torch.float32, device=dev)[:, :S]
         self.dz_t = torch.empty((1 + A, config.batch_size), dtype=torch.float32, device=dev)
         self.idx = torch.empty(config.batch_size, dtype=torch.int32, device=dev)
         self.weights = torch.empty(config.batch_size, dtype=torch.float32, device=dev)
