@@ -423,7 +423,10 @@ __global__ void __launch_bounds__(128) train_cand_kernel(PipeDev pd, Topo t, con
     // blocks of kBlk instructions: no boundary inside -> kBlk/2 16-byte
     // shared loads from a hoisted base address and kBlk sequential adds per
     // chain (the same order as one at a time)
-    constexpr int kBlk = 8;
+#ifndef AP_PP_BLOCK
+#define AP_PP_BLOCK 16  // measured on B200: 16 > 8 (+4%) > 4
+#endif
+    constexpr int kBlk = AP_PP_BLOCK;
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_cost);
     const int Fb = pd.F - pd.F % kBlk;
     int i = 0;
