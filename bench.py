@@ -767,6 +767,18 @@ def bench_pp_infer(args, world, want_cpu):
            "config": {"profile": "generate_environment(uniform, 1280, 0)", "topology": "configc", "stages": 4,
                       "points_per_search": points, "best": {"boundaries": bb, "cuts": cc, "length": length}},
            "seconds_per_search": dt}
+    # compute-only search (64 KB of DRAM traffic per 1.5 G points): bounded by instruction issue.  Per-point
+    # instruction count from the committed ncu capture; peak = 4 schedulers x 32 lanes x SMs x max SM clock.
+    ncu = json.loads((ROOT / "profiles" / "ncu_summary.json").read_text()).get("kernels", {}).get("pp_infer_search")
+    if ncu:
+        props = torch.cuda.get_device_properties(0)
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+        issue_peak = 4 * 32 * props.multi_processor_count * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+        achieved = points / dt * ncu["thread_instructions_per_point"]  # per GPU
+        out["roofline"] = {"bound": "issue", "achieved": achieved / 1e12, "peak": issue_peak / 1e12,
+                           "unit": "T thread-instr/s", "frac": achieved / issue_peak,
+                           "note": "API call time (host combo words + launch + sync) over the ncu per-point "
+                                   "instruction count of infer_search_tab_kernel"}
     if want_cpu:
         try:
             _ref_import()
