@@ -329,6 +329,9 @@ int launch_gemm_v3(const float* A, int64_t lda, int transA, const float* B, int6
   const int max_split = std::getenv("AP_GEMM_MAX_SPLIT") ? std::atoi(std::getenv("AP_GEMM_MAX_SPLIT")) : 16;
   int splits = 1;
   if (mt * nt < 120 && nk >= 4) splits = std::min(std::min(nk / 2, max_split), std::max(1, 148 / (mt * nt)));
+  // dev knobs for sweeps: AP_GEMM_V3_SPLITS (forced split count), AP_GEMM_V3_STAGES (4 | 6)
+  if (const char* e = std::getenv("AP_GEMM_V3_SPLITS")) splits = std::max(1, std::min(std::atoi(e), nk));
+  const bool four_stages = std::getenv("AP_GEMM_V3_STAGES") && std::atoi(std::getenv("AP_GEMM_V3_STAGES")) == 4;
   g.kps = (nk + splits - 1) / splits;
   splits = (nk + g.kps - 1) / g.kps;
   if (splits > 1 && !no_cluster) g.cluster = 1;
@@ -350,7 +353,8 @@ int launch_gemm_v3(const float* A, int64_t lda, int transA, const float* B, int6
     g.work = g_work3;
   }
   const dim3 grid(mt, nt, splits);
-  const int rc = bn == 32 ? run3<32, 6>(ma, mb, g, grid, stream) : run3<64, 6>(ma, mb, g, grid, stream);
+  const int rc = four_stages ? (bn == 32 ? run3<32, 4>(ma, mb, g, grid, stream) : run3<64, 4>(ma, mb, g, grid, stream))
+                             : (bn == 32 ? run3<32, 6>(ma, mb, g, grid, stream) : run3<64, 6>(ma, mb, g, grid, stream));
   if (rc != AP_OK || splits == 1 || g.cluster) return rc;
   const int64_t total = (int64_t)M * N;
   splitk_reduce3_kernel<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, stream>>>(
