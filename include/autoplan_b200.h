@@ -348,6 +348,16 @@ int ap_dqn_act_ctl(const float* q, int64_t ldq, const uint8_t* mask, int64_t ldm
 int ap_dp_allreduce_adam(int32_t world, int32_t rank, const float* grad, float* const* xbuf_peers,
                          uint32_t* const* pad_peers, int64_t n, float* params, float* m, float* v, float lr,
                          float beta1, float beta2, float eps, const int64_t* ctl, uint32_t* counter, void* stream);
+/* ap_dqn_adam_ctl that also writes the transposed weight copies: element i of
+ * segment s (flat offset seg_off[s], [rows, cols] row-major) goes to
+ * seg_dst[s][c * seg_ldd[s] + r] too (host descriptor arrays, <= 8 segments). */
+int ap_dqn_adam_ctl_t(float* params, const float* grads, float* m, float* v, int64_t n, float lr, float beta1,
+                      float beta2, float eps, const int64_t* ctl, int32_t nseg, const int64_t* seg_off,
+                      const int32_t* seg_rows, const int32_t* seg_cols, float* const* seg_dst, const int64_t* seg_ldd,
+                      void* stream);
+/* ap_per_update_scaled that also counts the learn step: ctl[3] += 1. */
+int ap_per_update_scaled_ctl(double* scaled, const int32_t* indices, const float* td, int32_t B, double alpha,
+                             int64_t* ctl, void* stream);
 /* Adam (agent.py:229-250) with bias corrections for t = ctl[3] + 1 */
 int ap_dqn_adam_ctl(float* params, const float* grads, float* m, float* v, int64_t n, float lr, float beta1,
                     float beta2, float eps, const int64_t* ctl, void* stream);

@@ -142,6 +142,9 @@ SIGNATURES: dict[str, tuple] = {
     "ap_dqn_act_ctl": (ctypes.c_int, [_VP, _I64, _VP, _I64, _I32, _I32, _F32, _F32, _I64, _VP, _VP, _VP]),
     "ap_dp_allreduce_adam": (ctypes.c_int, [_I32, _I32, _VP, _VP, _VP, _I64, _VP, _VP, _VP, _F32, _F32, _F32, _F32,
                                             _VP, _VP, _VP]),
+    "ap_dqn_adam_ctl_t": (ctypes.c_int, [_VP, _VP, _VP, _VP, _I64, _F32, _F32, _F32, _F32, _VP, _I32, _VP, _VP, _VP,
+                                         _VP, _VP, _VP]),
+    "ap_per_update_scaled_ctl": (ctypes.c_int, [_VP, _VP, _VP, _I32, _F64, _VP, _VP]),
     "ap_dqn_adam_ctl": (ctypes.c_int, [_VP, _VP, _VP, _VP, _I64, _F32, _F32, _F32, _F32, _VP, _VP]),
     "ap_per_push_ctl": (ctypes.c_int, [_I32, _I32, _I32, _I64, _VP, _VP, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
                                        _VP, _VP, _VP, _VP, _VP, _VP]),

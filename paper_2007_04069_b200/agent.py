@@ -161,6 +161,27 @@ class QNetwork:
         self.views["bh"].copy_(torch.from_numpy(bh))
         self.refresh_transposed()
 
+    def adam_segments(self):
+        """Host descriptors for ap_dqn_adam_ctl_t: (n, flat offsets, rows, cols, transposed
+        destinations, their row strides) of every weight matrix (cached; tensors never move)."""
+        import ctypes
+
+        if getattr(self, "_aseg", None) is None:
+            names = list(self.wt)
+            n = len(names)
+            base = self.flat.storage_offset()
+            src = [self.views[k] for k in names]
+            dst = [self.wt[k] for k in names]
+            self._aseg = (
+                n,
+                (ctypes.c_int64 * n)(*[t.storage_offset() - base for t in src]),
+                (ctypes.c_int32 * n)(*[t.shape[0] for t in src]),
+                (ctypes.c_int32 * n)(*[t.shape[1] for t in src]),
+                (ctypes.c_void_p * n)(*[t.data_ptr() for t in dst]),
+                (ctypes.c_int64 * n)(*[t.stride(0) for t in dst]),
+            )
+        return self._aseg
+
     def refresh_transposed(self) -> None:
         """All transposed weight copies in one launch (ap_transpose_batch)."""
         import ctypes

@@ -306,6 +306,47 @@ __global__ void adam_kernel(float* p, const float* g, float* m, float* v, int64_
   }
 }
 
+// Adam (control-block step count) that also refreshes the transposed weight
+// copies the K-major GEMMs read: element i of segment s (flat offset off[s],
+// [rows, cols] row-major) is written to dst[s][c * ldd[s] + r] as well, so no
+// separate transpose launch follows the update.
+struct AdamSegments {
+  int64_t off[8];
+  int32_t rows[8], cols[8];
+  float* dst[8];
+  int64_t ldd[8];
+  int n;
+};
+
+__global__ void adam_t_kernel(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
+                              float eps, const int64_t* ctl, AdamSegments segs) {
+  __shared__ float s_c[2];
+  if (threadIdx.x == 0) {
+    const double t = (double)(ctl[AP_CTL_TRAIN] + 1);
+    s_c[0] = (float)(1.0 - pow((double)b1, t));
+    s_c[1] = (float)(1.0 - pow((double)b2, t));
+  }
+  __syncthreads();
+  const float c1 = s_c[0], c2 = s_c[1];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    const float mi = b1 * m[i] + (1.0f - b1) * gi;
+    const float vi = b2 * v[i] + (1.0f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    const float pi = p[i] - lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+    p[i] = pi;
+    for (int s = 0; s < segs.n; ++s) {
+      const int64_t rel = i - segs.off[s];
+      if (rel >= 0 && rel < (int64_t)segs.rows[s] * segs.cols[s]) {
+        const int64_t r = rel / segs.cols[s], c = rel % segs.cols[s];
+        segs.dst[s][c * segs.ldd[s] + r] = pi;
+        break;
+      }
+    }
+  }
+}
+
 // numpy pairwise summation of a block of <= 128 doubles
 // (numpy/_core/src/umath/loops_utils.h.src, PW_BLOCKSIZE = 128)
 __device__ double pairwise_leaf(const double* x, int64_t m) {
@@ -610,6 +651,30 @@ int ap_dqn_adam(float* params, const float* grads, float* m, float* v, int64_t n
   if (n <= 0) return AP_OK;
   adam_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(params, grads, m, v, n, lr, beta1, beta2, eps,
                                                                      correct1, correct2, nullptr);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_dqn_adam_ctl_t(float* params, const float* grads, float* m, float* v, int64_t n, float lr, float beta1,
+                      float beta2, float eps, const int64_t* ctl, int32_t nseg, const int64_t* seg_off,
+                      const int32_t* seg_rows, const int32_t* seg_cols, float* const* seg_dst, const int64_t* seg_ldd,
+                      void* stream) {
+  if (!ctl || nseg < 0 || nseg > 8 || (nseg > 0 && (!seg_off || !seg_rows || !seg_cols || !seg_dst || !seg_ldd))) {
+    set_error("ap_dqn_adam_ctl_t: bad arguments (0..8 segments, host descriptor arrays)");
+    return AP_ERR_INVALID;
+  }
+  if (n <= 0) return AP_OK;
+  AdamSegments segs{};
+  segs.n = nseg;
+  for (int s = 0; s < nseg; ++s) {
+    segs.off[s] = seg_off[s];
+    segs.rows[s] = seg_rows[s];
+    segs.cols[s] = seg_cols[s];
+    segs.dst[s] = seg_dst[s];
+    segs.ldd[s] = seg_ldd[s];
+  }
+  adam_t_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(params, grads, m, v, n, lr, beta1, beta2, eps,
+                                                                       ctl, segs);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }

@@ -452,8 +452,11 @@ __global__ void ctl_advance_kernel(int64_t* ctl, int mode, int64_t E, int64_t ca
 }
 
 // scaled[idx] = (|td| + 1e-6)**alpha, last duplicate wins
-__global__ void per_update_scaled_kernel(double* scaled, const int32_t* idx, const float* td, int B, double alpha) {
+// ctl != nullptr: also counts the finished learn step (ctl[AP_CTL_TRAIN] += 1)
+__global__ void per_update_scaled_kernel(double* scaled, const int32_t* idx, const float* td, int B, double alpha,
+                                         int64_t* ctl) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ctl && b == 0) ctl[AP_CTL_TRAIN] += 1;
   if (b >= B) return;
   for (int k = b + 1; k < B; ++k)
     if (idx[k] == idx[b]) return;
@@ -634,7 +637,19 @@ int ap_vec_ctl_advance(int64_t* ctl, int32_t mode, int64_t E, int64_t cap, void*
 int ap_per_update_scaled(double* scaled, const int32_t* indices, const float* td, int32_t B, double alpha,
                          void* stream) {
   if (B <= 0) return AP_OK;
-  per_update_scaled_kernel<<<(B + 127) / 128, 128, 0, (cudaStream_t)stream>>>(scaled, indices, td, B, alpha);
+  per_update_scaled_kernel<<<(B + 127) / 128, 128, 0, (cudaStream_t)stream>>>(scaled, indices, td, B, alpha,
+                                                                             nullptr);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_per_update_scaled_ctl(double* scaled, const int32_t* indices, const float* td, int32_t B, double alpha,
+                             int64_t* ctl, void* stream) {
+  if (!ctl || B < 1) {
+    set_error("ap_per_update_scaled_ctl: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  per_update_scaled_kernel<<<(B + 127) / 128, 128, 0, (cudaStream_t)stream>>>(scaled, indices, td, B, alpha, ctl);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }

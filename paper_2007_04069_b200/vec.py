@@ -469,16 +469,19 @@ class VecDqnTrainer:
         else:
             if self.pg is not None:  # data-parallel learners without peer memory: NCCL mean all-reduce
                 allreduce_mean_(self.net.grad, self.pg)
-            _native.check(lib.ap_dqn_adam_ctl(P(self.net.flat), P(self.net.grad), P(opt.m), P(opt.v),
-                                              self.net.flat.numel(), opt.lr, opt.beta1, opt.beta2, opt.eps,
-                                              P(self.ctl), _s()))
-        self.net.refresh_transposed()
-        _native.check(lib.ap_per_update_scaled(P(r["priorities"]), P(self.idx), P(b.td), B, float(cfg.per_alpha),
-                                               _s()))
-        _native.check(lib.ap_vec_ctl_advance(P(self.ctl), 0, self.env.E, self.capacity, _s()))
-        # sample, 2 gathers, 2 forwards (4 GEMMs + 2 dueling), td, backward (4 GEMMs, 3 colsum,
-        # head, relu), adam, transpose, priority scatter, ctl (split-K reduces not counted)
-        self.launches += 1 + 2 + 6 + 1 + 9 + 1 + 1 + 1 + 1
+            # Adam also rewrites the transposed weight copies (no separate transpose launch)
+            sg = self.net.adam_segments()
+            _native.check(lib.ap_dqn_adam_ctl_t(P(self.net.flat), P(self.net.grad), P(opt.m), P(opt.v),
+                                                self.net.flat.numel(), opt.lr, opt.beta1, opt.beta2, opt.eps,
+                                                P(self.ctl), *sg, _s()))
+        if self.peer is not None:
+            self.net.refresh_transposed()
+        # the priority scatter also counts the learn step (ctl[AP_CTL_TRAIN] += 1)
+        _native.check(lib.ap_per_update_scaled_ctl(P(r["priorities"]), P(self.idx), P(b.td), B,
+                                                   float(cfg.per_alpha), P(self.ctl), _s()))
+        # sample, 2 gathers, 2 forwards (4 GEMMs + 2 heads), td, backward (1 transpose, 4 GEMMs,
+        # head, relu), adam (+ transposed copies), priority scatter (+ counter)
+        self.launches += 1 + 2 + 6 + 1 + 7 + 1 + 1
 
     def _step_body(self, learn: bool) -> None:
         self.act()
