@@ -208,6 +208,79 @@ __global__ void head_forward_kernel(const float* h, int64_t ldh, const float* wh
   }
 }
 
+// td_kernel for wide action spaces (PP): one CTA per row, the masked argmax
+// over the next-state Q and the dz row writes spread over the CTA's threads.
+// Same arithmetic and tie rules as td_kernel.
+__global__ void td_wide_kernel(const float* q, const float* online_next, const float* target_next, int64_t ldq,
+                               const int32_t* actions, const float* rewards, const uint8_t* done,
+                               const uint8_t* next_mask, int64_t ldm, const float* weights, int B, int A, float gamma,
+                               float delta, float* dz, int64_t ldz, float* td_out, float* loss_out, const int32_t* idx,
+                               float* dz_t, int64_t ldzt) {
+  __shared__ float s_best[32];
+  __shared__ int s_bj[32], s_any[32];
+  __shared__ float s_g;
+  __shared__ int s_a;
+  const int b = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int64_t row = idx ? (int64_t)idx[b] : (int64_t)b;
+  const uint8_t* m = next_mask + row * ldm;
+  float best = -INFINITY;
+  int best_j = 0x7fffffff, any = 0;
+  for (int j = threadIdx.x; j < A; j += blockDim.x) {
+    if (!m[j]) continue;
+    any = 1;
+    const float v = online_next[(int64_t)b * ldq + j];
+    if (v > best || (v == best && j < best_j)) {
+      best = v;
+      best_j = j;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    const float ov = __shfl_xor_sync(kFull, best, o);
+    const int oj = __shfl_xor_sync(kFull, best_j, o);
+    if (ov > best || (ov == best && oj < best_j)) {
+      best = ov;
+      best_j = oj;
+    }
+    any |= __shfl_xor_sync(kFull, any, o);
+  }
+  if (lane == 0) {
+    s_best[warp] = best;
+    s_bj[warp] = best_j;
+    s_any[warp] = any;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < nw; ++w) {
+      if (s_best[w] > best || (s_best[w] == best && s_bj[w] < best_j)) {
+        best = s_best[w];
+        best_j = s_bj[w];
+      }
+      any |= s_any[w];
+    }
+    const int a_next = any ? best_j : 0;  // empty mask: action 0 is "safe", bootstrap zeroed below
+    const float d = (done[row] || !any) ? 1.0f : 0.0f;
+    const float target = rewards[row] + gamma * (1.0f - d) * target_next[(int64_t)b * ldq + a_next];
+    const int a = actions[row];
+    const float td = q[(int64_t)b * ldq + a] - target;
+    const float w = weights[b];
+    const float ad = fabsf(td);
+    const float hub = ad <= delta ? 0.5f * td * td : delta * (ad - 0.5f * delta);
+    s_g = w * fminf(fmaxf(td, -delta), delta) / (float)B;
+    s_a = a;
+    td_out[b] = td;
+    loss_out[b] = w * hub;
+  }
+  __syncthreads();
+  const float g = s_g;
+  const int a = s_a;
+  for (int j = threadIdx.x; j <= A; j += blockDim.x) {
+    const float v = j == 0 ? g : (((j - 1) == a ? g : 0.0f) - g / (float)A);
+    dz[(int64_t)b * ldz + j] = v;
+    if (dz_t) dz_t[(int64_t)j * ldzt + b] = v;
+  }
+}
+
 // Up to 8 matrix transposes in one launch (the transposed weight copies the
 // K-major GEMMs read, refreshed after every Adam step): blockIdx.z = segment,
 // 32x32 tiles staged through shared memory so both sides are coalesced.
@@ -272,6 +345,28 @@ __global__ void head_backward_kernel(const float* dz, int64_t ldz, const float* 
   if (!(h[(int64_t)b * ldh + j] > 0.0f)) acc = 0.0f;
   dh[(int64_t)b * lddh + j] = acc;
   if (dh_t) dh_t[(int64_t)j * ldt + b] = acc;
+}
+
+// Wide-head variant: a warp per (row, unit) with the lanes striding the 1 + A
+// head outputs (coalesced reads of the dz row and of the unit's wh row), then a
+// shuffle reduction.
+__global__ void head_backward_wide_kernel(const float* dz, int64_t ldz, const float* wh, int64_t ldw, const float* h,
+                                          int64_t ldh, int B, int H, int A1, float* dh, int64_t lddh, float* dh_t,
+                                          int64_t ldt) {
+  const int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w >= (int64_t)B * H) return;
+  const int b = (int)(w / H), j = (int)(w % H);
+  const float* zr = dz + (int64_t)b * ldz;
+  const float* wr = wh + (int64_t)j * ldw;
+  float acc = 0.0f;
+  for (int k = lane; k < A1; k += 32) acc = fmaf(zr[k], wr[k], acc);
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+  if (lane == 0) {
+    if (!(h[(int64_t)b * ldh + j] > 0.0f)) acc = 0.0f;
+    dh[(int64_t)b * lddh + j] = acc;
+    if (dh_t) dh_t[(int64_t)j * ldt + b] = acc;
+  }
 }
 
 __global__ void colsum_kernel(const float* x, int64_t ld, int rows, int cols, float* out) {
@@ -609,10 +704,15 @@ int ap_dqn_td_ring(const float* q, const float* online_next, const float* target
     set_error("ap_dqn_td_ring: bad arguments");
     return AP_ERR_INVALID;
   }
-  td_kernel<<<(B + 7) / 8, 256, 0, (cudaStream_t)stream>>>(q, online_next, target_next, ldq, ring_actions,
-                                                           ring_rewards, ring_done, ring_next_mask, ldm, weights, B,
-                                                           A, gamma, huber_delta, dz, ldz, td, loss, indices, dz_t,
-                                                           ldzt);
+  if (A > 64)  // wide action spaces: a CTA per row
+    td_wide_kernel<<<B, 256, 0, (cudaStream_t)stream>>>(q, online_next, target_next, ldq, ring_actions, ring_rewards,
+                                                        ring_done, ring_next_mask, ldm, weights, B, A, gamma,
+                                                        huber_delta, dz, ldz, td, loss, indices, dz_t, ldzt);
+  else
+    td_kernel<<<(B + 7) / 8, 256, 0, (cudaStream_t)stream>>>(q, online_next, target_next, ldq, ring_actions,
+                                                             ring_rewards, ring_done, ring_next_mask, ldm, weights, B,
+                                                             A, gamma, huber_delta, dz, ldz, td, loss, indices, dz_t,
+                                                             ldzt);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
@@ -633,6 +733,12 @@ int ap_dqn_head_backward(const float* dz, int64_t ldz, const float* wh, int64_t 
   }
   const int64_t n = (int64_t)B * H;
   if (n == 0) return AP_OK;
+  if (A1 > 32) {  // wide heads (PP actions): one warp per (row, unit), lanes over the head outputs
+    head_backward_wide_kernel<<<(int)((n + 7) / 8), 256, 0, (cudaStream_t)stream>>>(dz, ldz, wh, ldw, h, ldh, B, H,
+                                                                                  A1, dh, lddh, dh_t, ldt);
+    AP_CUDA_CHECK(cudaGetLastError());
+    return AP_OK;
+  }
   head_backward_kernel<<<(int)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(dz, ldz, wh, ldw, h, ldh, B, H, A1,
                                                                                  dh, lddh, dh_t, ldt);
   AP_CUDA_CHECK(cudaGetLastError());

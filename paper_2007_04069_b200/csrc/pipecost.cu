@@ -216,14 +216,23 @@ __device__ inline void stage_metrics_dev(const PipeDev& pd, const double* cost, 
   stage_tail(pd, cuts, P, scale, comp, act, param, nvars);
 }
 
+// One thread per pivot tuple; the cost array is staged in shared memory when it
+// fits (stage_smem), so the per-tuple sequential sums read it with broadcast loads.
 __global__ void metrics_kernel(PipeDev pd, const int32_t* pivots, int64_t batch, int P, double scale, double* comp,
-                               double* act, double* param, int32_t* nvars) {
+                               double* act, double* param, int32_t* nvars, int stage_smem) {
+  extern __shared__ double s_mcost[];
+  const double* cost = pd.cost;
+  if (stage_smem) {
+    for (int i = threadIdx.x; i < pd.F; i += blockDim.x) s_mcost[i] = pd.cost[i];
+    __syncthreads();
+    cost = s_mcost;
+  }
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < batch; b += (int64_t)gridDim.x * blockDim.x) {
     int cuts[kMaxStages];
     for (int k = 0; k < P; ++k) cuts[k] = pivots[b * P + k];
     double c[kMaxStages], a[kMaxStages], w[kMaxStages];
     int v[kMaxStages];
-    stage_metrics_dev(pd, pd.cost, cuts, P, scale, c, a, w, v);
+    stage_metrics_dev(pd, cost, cuts, P, scale, c, a, w, v);
     for (int k = 0; k <= P; ++k) {
       comp[b * (P + 1) + k] = c[k];
       act[b * (P + 1) + k] = a[k];
@@ -938,8 +947,13 @@ int ap_pipe_metrics(ap_pipe_t p, const int32_t* pivots, int64_t batch, int32_t P
   int rc = p->ensure();
   if (rc != AP_OK) return rc;
   if (batch == 0) return AP_OK;
-  metrics_kernel<<<grid_for(batch, 128), 128, 0, (cudaStream_t)stream>>>(p->dev(), pivots, batch, P, 1.0 + bwm, comp,
-                                                                         act, param, nvars);
+  // small CTAs spread the (sequential-per-tuple) work over more SMs; costs in shared memory when they fit
+  const size_t msmem = (size_t)p->F * sizeof(double);
+  const int stage = msmem <= 200 * 1024 ? 1 : 0;
+  if (stage) AP_CUDA_CHECK(cudaFuncSetAttribute(metrics_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem));
+  metrics_kernel<<<grid_for(batch, 32), 32, stage ? msmem : 0, (cudaStream_t)stream>>>(p->dev(), pivots, batch, P,
+                                                                                       1.0 + bwm, comp, act, param,
+                                                                                       nvars, stage);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }

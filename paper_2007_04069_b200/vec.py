@@ -469,7 +469,8 @@ class VecDqnTrainer:
         else:
             if self.pg is not None:  # data-parallel learners without peer memory: NCCL mean all-reduce
                 allreduce_mean_(self.net.grad, self.pg)
-            # Adam also rewrites the transposed weight copies (no separate transpose launch)
+            # Adam also rewrites the transposed weight copies (no separate transpose launch;
+            # measured faster than Adam + a tiled transpose even for the 4 M-parameter PP-train net)
             sg = self.net.adam_segments()
             _native.check(lib.ap_dqn_adam_ctl_t(P(self.net.flat), P(self.net.grad), P(opt.m), P(opt.v),
                                                 self.net.flat.numel(), opt.lr, opt.beta1, opt.beta2, opt.eps,
