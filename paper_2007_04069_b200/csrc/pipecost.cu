@@ -476,6 +476,148 @@ __global__ void __launch_bounds__(128) train_cand_kernel(PipeDev pd, Topo t, con
   }
 }
 
+// ---- K2 with per-env reuse -------------------------------------------------
+// Every allowed candidate of an env cuts after the env's last applied cut
+// c_last, so its stages are: the env's fixed stages (identical for all its
+// candidates), [c_last+1 .. pos] and the tail [pos+1 .. F-1].  The middle
+// stage's naive sequential sum is the running sum R[pos] of one pass from
+// c_last+1 (the same additions in the same order), so per candidate only the
+// tail is summed.  train_prefix_kernel: one CTA per env writes fixed[e][k] and
+// R[e][i]; train_tail_kernel: the candidates' tail chains + features.
+__global__ void train_prefix_kernel(PipeDev pd, const int32_t* cand_pos, const int32_t* applied, int A, int64_t E,
+                                    double* fixed, double* R) {
+  extern __shared__ double s_pc[];
+  for (int i = threadIdx.x; i < pd.F; i += blockDim.x) s_pc[i] = pd.cost[i];
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+    int acut[kMaxStages];
+    int P0 = 0;
+    for (int k = 0; k < A; ++k) {
+      const int a = applied[e * A + k];
+      if (a >= 0) acut[P0++] = cand_pos[a];
+    }
+    int i = 0;
+    for (int k = 0; k < P0; ++k) {  // fixed stages [prev+1 .. acut[k]]
+      double acc = 0.0;
+      for (; i <= acut[k]; ++i) acc = acc + s_pc[i];
+      fixed[e * kMaxStages + k] = acc;
+    }
+    double* __restrict__ r = R + e * (int64_t)pd.F;
+    const double* __restrict__ c = s_pc;
+    double acc = 0.0;  // running sum of the stage that starts at c_last + 1
+    // the additions stay sequential; loads and stores are batched 8 at a time
+    for (; i + 8 <= pd.F; i += 8) {
+      double x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = c[i + u];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        acc = acc + x[u];
+        r[i + u] = acc;
+      }
+    }
+    for (; i < pd.F; ++i) {
+      acc = acc + c[i];
+      r[i] = acc;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128) train_tail_kernel(PipeDev pd, Topo t, const int32_t* cand_pos, int C,
+                                                         const int32_t* applied, int A, const int32_t* list,
+                                                         const int32_t* count, int64_t E, double scale,
+                                                         const double* fixed, const double* R, double* state) {
+  extern __shared__ double s_cost[];
+  for (int i = threadIdx.x; i < pd.F; i += blockDim.x) s_cost[i] = pd.cost[i];
+  __syncthreads();
+  const int nchunk = (C + kCandPerWarp - 1) / kCandPerWarp;
+  const int64_t total = E * (int64_t)nchunk * 32;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(s_cost);
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = idx / (32 * (int64_t)nchunk);
+    const int chunk = (int)((idx / 32) % nchunk), lane = (int)(idx % 32);
+    const int n_ok = count[e];
+    if (chunk * kCandPerWarp >= n_ok) continue;  // whole warp past this env's list
+    double* st = state + e * 4 * (int64_t)C;
+    int cand[kCandPerThread], pos[kCandPerThread];
+    bool ok[kCandPerThread];
+    int lo = pd.F, hi = -1;
+#pragma unroll
+    for (int j = 0; j < kCandPerThread; ++j) {
+      const int k = chunk * kCandPerWarp + lane + 32 * j;
+      ok[j] = k < n_ok;
+      cand[j] = ok[j] ? list[e * C + k] : 0;
+      pos[j] = ok[j] ? cand_pos[cand[j]] : pd.F;  // idle chain: empty tail
+      lo = min(lo, pos[j] + 1);
+      hi = max(hi, ok[j] ? pos[j] : -1);
+    }
+    // tails [pos+1 .. F-1]: sequential per chain.  The warp walks one uniform
+    // i (broadcast shared loads, no divergence) from its lowest start, aligned
+    // down to the block; below a chain's start it adds +0.0, which leaves the
+    // sum bit-identical (acc starts at +0.0 and so is never -0.0).  Blocks past
+    // every start in the warp take the unconditional path.
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    double acc[kCandPerThread];
+#pragma unroll
+    for (int j = 0; j < kCandPerThread; ++j) acc[j] = 0.0;
+    constexpr int kBlk = AP_PP_BLOCK;
+    int i = lo - lo % kBlk;
+    for (; i + kBlk <= pd.F && i <= hi; i += kBlk) {
+      double c[kBlk];
+#pragma unroll
+      for (int u = 0; u < kBlk; u += 2)
+        asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(c[u]), "=d"(c[u + 1]) : "r"(sbase + 8u * (uint32_t)(i + u)));
+#pragma unroll
+      for (int u = 0; u < kBlk; ++u)
+#pragma unroll
+        for (int j = 0; j < kCandPerThread; ++j) acc[j] = acc[j] + (i + u > pos[j] ? c[u] : 0.0);
+    }
+    for (; i + kBlk <= pd.F; i += kBlk) {
+      double c[kBlk];
+#pragma unroll
+      for (int u = 0; u < kBlk; u += 2)
+        asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(c[u]), "=d"(c[u + 1]) : "r"(sbase + 8u * (uint32_t)(i + u)));
+#pragma unroll
+      for (int u = 0; u < kBlk; ++u)
+#pragma unroll
+        for (int j = 0; j < kCandPerThread; ++j) acc[j] = acc[j] + c[u];
+    }
+    for (; i < pd.F; ++i) {
+      const double c = s_cost[i];
+#pragma unroll
+      for (int j = 0; j < kCandPerThread; ++j) acc[j] = acc[j] + (i > pos[j] ? c : 0.0);
+    }
+    int acut[kMaxStages];
+    int P0 = 0;
+    for (int k = 0; k < A; ++k) {
+      const int a = applied[e * A + k];
+      if (a >= 0) acut[P0++] = cand_pos[a];
+    }
+    const int P = P0 + 1;
+#pragma unroll
+    for (int j = 0; j < kCandPerThread; ++j) {
+      if (!ok[j]) continue;
+      double cj[kMaxStages];
+      for (int k = 0; k < P0; ++k) cj[k] = fixed[e * kMaxStages + k];
+      cj[P0] = R[e * (int64_t)pd.F + pos[j]];
+      cj[P0 + 1] = acc[j];
+      int cuts[kMaxStages];
+      for (int k = 0; k < P0; ++k) cuts[k] = acut[k];
+      cuts[P0] = pos[j];
+      double a[kMaxStages], w[kMaxStages];
+      stage_tail(pd, cuts, P, scale, cj, a, w, nullptr);
+      double red, tra, bal;
+      train_features(t, P + 1, cj, a, w, &red, &tra, &bal);
+      st[cand[j]] = red;
+      st[C + cand[j]] = tra;
+      st[2 * C + cand[j]] = bal;
+    }
+  }
+}
+
 // block normalisation and one-hot (envs.py:398-404): one CTA per env
 __global__ void train_norm_kernel(int C, const int32_t* applied, int A, int64_t E, double* state) {
   __shared__ double s_max[2][32];
@@ -794,6 +936,22 @@ struct ap_pipe {
   int32_t* d_count = nullptr;
   int64_t list_cap = 0, count_cap = 0;
 
+  // per-env reuse scratch: fixed stage sums [E, kMaxStages] and running sums [E, F] (grow-only)
+  double* d_fixed = nullptr;
+  double* d_R = nullptr;
+  int64_t prefix_cap = 0;
+
+  int ensure_prefix_scratch(int64_t n_env) {
+    if (n_env > prefix_cap) {
+      if (d_fixed) cudaFree(d_fixed);
+      if (d_R) cudaFree(d_R);
+      AP_CUDA_CHECK(cudaMalloc(&d_fixed, n_env * kMaxStages * sizeof(double)));
+      AP_CUDA_CHECK(cudaMalloc(&d_R, n_env * (int64_t)std::max(F, 1) * sizeof(double)));
+      prefix_cap = n_env;
+    }
+    return AP_OK;
+  }
+
   int ensure_train_scratch(int64_t n_list, int64_t n_env) {
     if (n_list > list_cap) {
       if (d_list) cudaFree(d_list);
@@ -833,6 +991,10 @@ struct ap_pipe {
     return PipeDev{F, d_cost.ptr, d_crossing.ptr, d_wprefix.ptr, d_vprefix.ptr, wtotal, vtotal};
   }
   void release() {
+    if (d_fixed) cudaFree(d_fixed);
+    if (d_R) cudaFree(d_R);
+    d_fixed = d_R = nullptr;
+    prefix_cap = 0;
     if (d_list) cudaFree(d_list);
     if (d_count) cudaFree(d_count);
     d_list = d_count = nullptr;
@@ -999,9 +1161,20 @@ int ap_pipe_train_state(ap_pipe_t p, const ap_topology* topo, const int32_t* can
       mask, C, E, p->d_list, p->d_count, state);
   AP_CUDA_CHECK(cudaGetLastError());
   const int64_t threads = E * (int64_t)((C + kCandPerWarp - 1) / kCandPerWarp) * 32;
-  train_cand_kernel<<<grid_for(threads, 128), 128, smem, (cudaStream_t)stream>>>(p->dev(), t, cand_pos, C, applied, A,
-                                                                                 p->d_list, p->d_count, E, 1.0 + bwm,
-                                                                                 state);
+  if (std::getenv("AP_PP_FULL") == nullptr) {
+    // per-env reuse: fixed stages + running sums once per env, tails per candidate
+    if ((rc = p->ensure_prefix_scratch(E)) != AP_OK) return rc;
+    AP_CUDA_CHECK(cudaFuncSetAttribute(train_prefix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    AP_CUDA_CHECK(cudaFuncSetAttribute(train_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    train_prefix_kernel<<<(int)std::min<int64_t>(E, 148 * 8), 32, smem, (cudaStream_t)stream>>>(
+        p->dev(), cand_pos, applied, A, E, p->d_fixed, p->d_R);
+    AP_CUDA_CHECK(cudaGetLastError());
+    train_tail_kernel<<<grid_for(threads, 128), 128, smem, (cudaStream_t)stream>>>(
+        p->dev(), t, cand_pos, C, applied, A, p->d_list, p->d_count, E, 1.0 + bwm, p->d_fixed, p->d_R, state);
+  } else {  // one full sweep of the cost array per candidate (AP_PP_FULL=1)
+    train_cand_kernel<<<grid_for(threads, 128), 128, smem, (cudaStream_t)stream>>>(
+        p->dev(), t, cand_pos, C, applied, A, p->d_list, p->d_count, E, 1.0 + bwm, state);
+  }
   AP_CUDA_CHECK(cudaGetLastError());
   train_norm_kernel<<<(int)std::min<int64_t>(E, 148 * 8), 256, 0, (cudaStream_t)stream>>>(C, applied, A, E, state);
   AP_CUDA_CHECK(cudaGetLastError());

@@ -184,3 +184,47 @@ def test_scalar_api(cuda):
     assert pc.proportional_device_counts([1.0, 1.0, 2.0], 8) == [2, 2, 4]
     with pytest.raises(pc.InfeasiblePlanError):
         pc.stage_metrics(g, [order[5], order[3]])
+
+
+@pytest.mark.parametrize("K", [2, 3, 4, 6])
+def test_train_state_reuse_matches_full_sweep(cuda, monkeypatch, K):
+    """K2 with per-env reuse (fixed stages + running sums once per env, per-candidate tails)
+    is bit-identical to one full sequential sweep per candidate (AP_PP_FULL=1)."""
+    import ctypes
+
+    import torch
+
+    from paper_2007_04069_b200 import _native, graphs
+    from paper_2007_04069_b200.topology import DeviceTopology
+
+    g = graphs.generate("bert48")
+    topo = DeviceTopology(2, 4)
+    env = PipeTrainEnv(g, topo, K, radius=3)
+    C = env.num_actions
+    E = 48
+    A = max(1, K - 2)
+    rng = np.random.default_rng(K)
+    applied = np.full((E, A), -1, dtype=np.int32)
+    mask = np.zeros((E, C), dtype=np.uint8)
+    for e in range(E):
+        k = int(rng.integers(0, K - 1))
+        picks = np.sort(rng.choice(C - (K - 1), size=k, replace=False)) if k else np.zeros(0, int)
+        applied[e, :k] = picks
+        last = picks[-1] if k else -1
+        mask[e, last + 1: C - ((K - 1) - k) + 1] = 1
+    d_cand = torch.from_numpy(env._cand_pos).cuda()
+    d_app, d_mask = torch.from_numpy(applied).cuda(), torch.from_numpy(mask).cuda()
+    lib = _native.require_device()
+    topo_c = _native.Topology.of(topo)
+
+    def run():
+        st = torch.full((E, 4 * C), float("nan"), dtype=torch.float64, device="cuda")
+        _native.check(lib.ap_pipe_train_state(env._model.handle, ctypes.byref(topo_c), _native.ptr(d_cand), C,
+                                              _native.ptr(d_app), A, _native.ptr(d_mask), E, 2.0, _native.ptr(st),
+                                              _native.stream_handle()))
+        return st
+
+    reuse = run()
+    monkeypatch.setenv("AP_PP_FULL", "1")
+    full = run()
+    assert torch.equal(reuse, full)
