@@ -687,6 +687,7 @@ def bench_pp_train(args, world, want_cpu):
         remaining = (K - 1) - k
         mask[e, last + 1: C - remaining + 1] = 1
     d_cand = torch.from_numpy(env._cand_pos).cuda()
+    env._model.bind_candidates(d_cand)  # the table build is per env, outside the timed region
     d_app = torch.from_numpy(applied).cuda()
     d_mask = torch.from_numpy(mask).cuda()
     state = torch.empty((E, 4 * C), dtype=torch.float64, device="cuda")

@@ -200,6 +200,19 @@ int ap_pipe_train_state(ap_pipe_t p, const ap_topology* topo, const int32_t* can
                         const int32_t* applied_dev, int32_t max_applied, const uint8_t* mask_dev, int64_t num_envs,
                         double backward_multiplier, double* state_dev, void* stream);
 
+/* Binds a candidate list to the handle: builds (once, outside stream capture)
+ * the table of every stage sum a plan over these candidates can have --
+ * the naive sum of cost[start .. end] for each pair of candidate boundaries,
+ * (C+1)^2 + (C+1) fp64 owned by the handle.  Later ap_pipe_train_state calls
+ * with the same (cand_pos_dev, num_cand) read stage sums from it instead of
+ * re-summing the cost array per candidate (bit-identical: same additions,
+ * same order).  The list's contents must not change while bound; calling
+ * again rebuilds from the current contents.  AP_ERR_UNSUPPORTED when the
+ * table would exceed 4 GiB (the per-candidate sweep is then used).
+ * New in this library: the reference recomputes stage_metrics per candidate
+ * (envs.py:378-397). */
+int ap_pipe_train_table(ap_pipe_t p, const int32_t* cand_pos_dev, int32_t num_cand, void* stream);
+
 /* PP-infer terminal evaluation on coarsened arrays (envs.py:593-616):
  * decode_metrics + pipeline_length on the normalised topology for B
  * (boundaries, cuts) points.  arrays_dev = [3 * G] fp64 (C*, A*, W*). */

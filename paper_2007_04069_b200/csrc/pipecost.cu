@@ -618,6 +618,116 @@ __global__ void __launch_bounds__(128) train_tail_kernel(PipeDev pd, Topo t, con
   }
 }
 
+// ---- K2 from the stage-sum table ---------------------------------------------
+// Every stage of every plan the env can reach starts at 0 or just after a
+// candidate cut and ends at a candidate cut or at F-1, and the cost array is
+// fixed per model, so all stage sums an env ever needs form one table,
+// computed once per candidate list (ap_pipe_train_table):
+//   T[a][b] = naive sum of cost[start(a) .. end(b)]   (a, b in 0..C)
+//   start(0) = 0, start(a) = cand_pos[a-1] + 1;  end(b) = cand_pos[b] (b < C), F-1
+//   row C+1: tail[c] = T[c+1][C], the sum after cut c (contiguous for the gathers)
+// Each entry is the reference's `acc = 0; acc += cost[i]` over the same
+// indices in the same order (pipecost.py:72-102), so a lookup is
+// bit-identical to re-summing; T[a][b] = 0.0 when the range is empty.
+__global__ void train_table_kernel(PipeDev pd, const int32_t* cand_pos, int C, double* T) {
+  const int64_t W = C + 1;
+  for (int a = blockIdx.x * blockDim.x + threadIdx.x; a <= C; a += gridDim.x * blockDim.x) {
+    double* row = T + a * W;
+    for (int b = 0; b < a; ++b) row[b] = 0.0;
+    const int s = a == 0 ? 0 : cand_pos[a - 1] + 1;
+    int b = a;
+    double acc = 0.0;
+    for (int i = s; i < pd.F && b <= C; ++i) {
+      acc = acc + __ldg(pd.cost + i);
+      while (b <= C && (b < C ? cand_pos[b] : pd.F - 1) <= i) row[b++] = acc;
+    }
+    for (; b <= C; ++b) row[b] = 0.0;  // empty ranges (start past the end)
+    if (a > 0) T[W * W + (a - 1)] = row[C];
+  }
+}
+
+// PipeTrainEnv._state (envs.py:378-404) for E envs from the table: one CTA per
+// env computes the raw features of its allowed candidates, then the block max,
+// normalisation and the one-hot block -- one launch, the state written once
+// and normalised from L1/L2.
+__global__ void __launch_bounds__(256) train_state_tab_kernel(PipeDev pd, Topo t, const int32_t* cand_pos, int C,
+                                                              const double* T, const int32_t* applied, int A,
+                                                              const uint8_t* mask, int64_t E, double scale,
+                                                              double* state) {
+  __shared__ int s_aidx[kMaxStages], s_apos[kMaxStages], s_P0;
+  __shared__ double s_fix[kMaxStages];
+  __shared__ double s_max[2][32];
+  const int64_t W = C + 1;
+  const double* tail = T + W * W;
+  for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+    if (threadIdx.x == 0) {
+      int P0 = 0, a0 = 0;
+      for (int k = 0; k < A; ++k) {
+        const int a = applied[e * A + k];
+        if (a >= 0) {
+          s_aidx[P0] = a;
+          s_apos[P0] = cand_pos[a];
+          s_fix[P0] = T[a0 * W + a];  // fixed stage [start(a0) .. cand_pos[a]]
+          a0 = a + 1;
+          ++P0;
+        }
+      }
+      s_P0 = P0;
+    }
+    __syncthreads();
+    const int P0 = s_P0, P = P0 + 1;
+    const int alast = P0 > 0 ? s_aidx[P0 - 1] + 1 : 0;
+    double* st = state + e * 4 * (int64_t)C;
+    const uint8_t* m = mask + e * (int64_t)C;
+    double mr = 0.0, mt = 0.0;
+    for (int c = threadIdx.x; c < C; c += blockDim.x) {
+      double red = 0.0, tra = 0.0, bal = 0.0;
+      if (m[c]) {
+        double cj[kMaxStages], a[kMaxStages], w[kMaxStages];
+        int cuts[kMaxStages];
+        for (int k = 0; k < P0; ++k) {
+          cj[k] = s_fix[k];
+          cuts[k] = s_apos[k];
+        }
+        cj[P0] = T[alast * W + c];  // [start(alast) .. cand_pos[c]]
+        cj[P0 + 1] = tail[c];       // [cand_pos[c]+1 .. F-1]
+        cuts[P0] = cand_pos[c];
+        stage_tail(pd, cuts, P, scale, cj, a, w, nullptr);
+        train_features(t, P + 1, cj, a, w, &red, &tra, &bal);
+      }
+      st[c] = red;
+      st[C + c] = tra;
+      st[2 * C + c] = bal;
+      mr = fmax(mr, red);
+      mt = fmax(mt, tra);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      mr = fmax(mr, __shfl_xor_sync(0xffffffffu, mr, o));
+      mt = fmax(mt, __shfl_xor_sync(0xffffffffu, mt, o));
+    }
+    const int wid = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+      s_max[0][wid] = mr;
+      s_max[1][wid] = mt;
+    }
+    __syncthreads();
+    mr = 0.0;
+    mt = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+      mr = fmax(mr, s_max[0][k]);
+      mt = fmax(mt, s_max[1][k]);
+    }
+    for (int c = threadIdx.x; c < C; c += blockDim.x) {  // each thread re-reads its own writes
+      if (mr > 0.0) st[c] = st[c] / mr;
+      if (mt > 0.0) st[C + c] = st[C + c] / mt;
+      double one = 0.0;
+      for (int k = 0; k < P0; ++k) one = s_aidx[k] == c ? 1.0 : one;
+      st[3 * C + c] = one;
+    }
+    __syncthreads();  // s_max / s_aidx reused by the next env
+  }
+}
+
 // block normalisation and one-hot (envs.py:398-404): one CTA per env
 __global__ void train_norm_kernel(int C, const int32_t* applied, int A, int64_t E, double* state) {
   __shared__ double s_max[2][32];
@@ -952,6 +1062,20 @@ struct ap_pipe {
     return AP_OK;
   }
 
+  // stage-sum tables bound by ap_pipe_train_table, keyed by the device
+  // candidate list; kept until the handle dies (captured graphs may hold them)
+  struct TableBinding {
+    const int32_t* cand;
+    int32_t C;
+    double* tab;
+  };
+  std::vector<TableBinding> tables;
+  const double* table_for(const int32_t* cand, int32_t C) const {
+    for (const auto& b : tables)
+      if (b.cand == cand && b.C == C) return b.tab;
+    return nullptr;
+  }
+
   int ensure_train_scratch(int64_t n_list, int64_t n_env) {
     if (n_list > list_cap) {
       if (d_list) cudaFree(d_list);
@@ -991,6 +1115,8 @@ struct ap_pipe {
     return PipeDev{F, d_cost.ptr, d_crossing.ptr, d_wprefix.ptr, d_vprefix.ptr, wtotal, vtotal};
   }
   void release() {
+    for (auto& b : tables) cudaFree(b.tab);
+    tables.clear();
     if (d_fixed) cudaFree(d_fixed);
     if (d_R) cudaFree(d_R);
     d_fixed = d_R = nullptr;
@@ -1138,6 +1264,36 @@ int ap_pipe_length(const ap_topology* topo, int32_t K, int32_t M, int64_t batch,
   return AP_OK;
 }
 
+int ap_pipe_train_table(ap_pipe_t p, const int32_t* cand_pos, int32_t C, void* stream) {
+  if (!p || C < 1 || !cand_pos) {
+    set_error("ap_pipe_train_table: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  int rc = p->ensure();
+  if (rc != AP_OK) return rc;
+  const int64_t W = (int64_t)C + 1;
+  const int64_t bytes = (W * W + W) * (int64_t)sizeof(double);
+  double* tab = const_cast<double*>(p->table_for(cand_pos, C));
+  if (!tab) {
+    if (bytes > ((int64_t)4 << 30) || p->tables.size() >= 16) {
+      set_error("ap_pipe_train_table: table too large or too many bound lists (the per-candidate sweep is used)");
+      return AP_ERR_UNSUPPORTED;
+    }
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    AP_CUDA_CHECK(cudaStreamIsCapturing((cudaStream_t)stream, &cs));
+    if (cs != cudaStreamCaptureStatusNone) {
+      set_error("ap_pipe_train_table: cannot allocate a new table during stream capture");
+      return AP_ERR_INVALID;
+    }
+    AP_CUDA_CHECK(cudaMalloc(&tab, bytes));
+    p->tables.push_back({cand_pos, C, tab});
+  }
+  // (re)built from the list's current contents
+  train_table_kernel<<<(int)((W + 127) / 128), 128, 0, (cudaStream_t)stream>>>(p->dev(), cand_pos, C, tab);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
 int ap_pipe_train_state(ap_pipe_t p, const ap_topology* topo, const int32_t* cand_pos, int32_t C,
                         const int32_t* applied, int32_t A, const uint8_t* mask, int64_t E, double bwm, double* state,
                         void* stream) {
@@ -1149,13 +1305,21 @@ int ap_pipe_train_state(ap_pipe_t p, const ap_topology* topo, const int32_t* can
   }
   if ((rc = p->ensure()) != AP_OK) return rc;
   if (E == 0) return AP_OK;
+  const Topo t = make_topo(topo);
+  const double* tab = std::getenv("AP_PP_NO_TABLE") ? nullptr : p->table_for(cand_pos, C);
+  if (tab) {  // bound candidate list: stage sums are lookups (one launch)
+    train_state_tab_kernel<<<(int)std::min<int64_t>(E, 148 * 8), 256, 0, (cudaStream_t)stream>>>(
+        p->dev(), t, cand_pos, C, tab, applied, A, mask, E, 1.0 + bwm, state);
+    AP_CUDA_CHECK(cudaGetLastError());
+    return AP_OK;
+  }
   const size_t smem = (size_t)p->F * sizeof(double);
   if (smem > 200 * 1024) {
-    set_error("ap_pipe_train_state: forward graph too long for the shared-memory cost cache");
+    set_error("ap_pipe_train_state: forward graph too long for the shared-memory cost cache "
+              "(bind the candidate list with ap_pipe_train_table)");
     return AP_ERR_UNSUPPORTED;
   }
   AP_CUDA_CHECK(cudaFuncSetAttribute(train_cand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const Topo t = make_topo(topo);
   if ((rc = p->ensure_train_scratch(E * (int64_t)C, E)) != AP_OK) return rc;
   train_compact_kernel<<<(int)std::min<int64_t>(E, 148 * 4), 1024, 0, (cudaStream_t)stream>>>(
       mask, C, E, p->d_list, p->d_count, state);

@@ -107,6 +107,25 @@ class PipeModel:
         _native.check(lib.ap_pipe_create(ctypes.byref(desc), ctypes.byref(handle)))
         self.handle = handle
         self.num_forward = F
+        self._bound = {}
+
+    def bind_candidates(self, cand_pos_dev) -> bool:
+        """Stage-sum table for a device candidate list (ap_pipe_train_table).
+
+        The tensor is kept alive with the handle, so its address (the table's
+        key) cannot be reused by another list.  False when the table would be
+        too large; ap_pipe_train_state then sweeps the cost array per candidate.
+        """
+        key = (cand_pos_dev.data_ptr(), cand_pos_dev.numel())
+        if key in self._bound:
+            return True
+        rc = _native.load_library().ap_pipe_train_table(self.handle, _native.ptr(cand_pos_dev),
+                                                         cand_pos_dev.numel(), _native.stream_handle())
+        if rc == _native.AP_ERR_UNSUPPORTED:
+            return False
+        _native.check(rc)
+        self._bound[key] = cand_pos_dev
+        return True
 
     def positions(self, pivots: Sequence[int]) -> list[int]:
         out = []

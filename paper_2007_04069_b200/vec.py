@@ -146,6 +146,7 @@ class VecPipeTrainEnv:
         dev = "cuda"
         i32, u8, f64, f32 = torch.int32, torch.uint8, torch.float64, torch.float32
         self.cand_pos = torch.from_numpy(host._cand_pos).to(dev)
+        host._model.bind_candidates(self.cand_pos)  # stage-sum table: K2 by lookups
         self.dummy_pos = self.cand_pos[C - P:].clone()  # a legal increasing pivot tuple
         self.picks = torch.full((E, P), -1, dtype=i32, device=dev)
         self.positions = self.dummy_pos.repeat(E, 1).contiguous()

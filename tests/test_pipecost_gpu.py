@@ -188,8 +188,9 @@ def test_scalar_api(cuda):
 
 @pytest.mark.parametrize("K", [2, 3, 4, 6])
 def test_train_state_reuse_matches_full_sweep(cuda, monkeypatch, K):
-    """K2 with per-env reuse (fixed stages + running sums once per env, per-candidate tails)
-    is bit-identical to one full sequential sweep per candidate (AP_PP_FULL=1)."""
+    """K2 from the bound stage-sum table, and with per-env reuse (fixed stages + running
+    sums once per env, per-candidate tails; AP_PP_NO_TABLE=1), are bit-identical to one
+    full sequential sweep per candidate (AP_PP_FULL=1)."""
     import ctypes
 
     import torch
@@ -224,7 +225,11 @@ def test_train_state_reuse_matches_full_sweep(cuda, monkeypatch, K):
                                               _native.stream_handle()))
         return st
 
+    assert env._model.bind_candidates(d_cand)
+    table = run()
+    monkeypatch.setenv("AP_PP_NO_TABLE", "1")
     reuse = run()
     monkeypatch.setenv("AP_PP_FULL", "1")
     full = run()
     assert torch.equal(reuse, full)
+    assert torch.equal(table, full)
