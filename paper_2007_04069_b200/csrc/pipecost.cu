@@ -96,11 +96,15 @@ __host__ __device__ inline void proportional_counts(const double* comp, int k, i
 __host__ __device__ inline double allreduce(const Topo& t, double bytes, int start, int end) {
   const int n = end - start;
   if (n <= 1 || bytes == 0.0) return 0.0;
+  // the slowest link of the ring start -> .. -> end-1 -> start, in closed form
+  // (the reference walks the n links): one server -> all intra; otherwise the
+  // wrap link is inter-server, the n-1 consecutive links cross `hops` server
+  // boundaries, and the rest are intra.  min() over the same link set.
+  const int s0 = start / t.g, s1 = (end - 1) / t.g;
+  const bool has_inter = s0 != s1, has_intra = s0 == s1 || n - 1 > s1 - s0;
   double slow = INFINITY;
-  for (int i = 0; i < n; ++i) {
-    const double b = bw(t, start + i, start + (i + 1) % n);
-    if (b < slow) slow = b;
-  }
+  if (has_inter && t.inter < slow) slow = t.inter;
+  if (has_intra && t.intra < slow) slow = t.intra;
   return ((2.0 * (double)(n - 1)) / (double)n) * bytes / slow;
 }
 
@@ -646,60 +650,109 @@ __global__ void train_table_kernel(PipeDev pd, const int32_t* cand_pos, int C, d
   }
 }
 
+// Per-env constants of the fixed stages (stage_tail's terms for cuts that are
+// the same for every candidate of the env).
+struct FixedStages {
+  int P0;
+  int aidx[kMaxStages];
+  double comp[kMaxStages], act[kMaxStages], param[kMaxStages];
+  int64_t wlast;  // wprefix at the last applied cut (0 when none)
+};
+
+// One candidate's raw features for a plan of KC stages (KC = P0 + 2 cuts + 1;
+// KC == 0: the stage count Kr is a runtime value).  With KC fixed every loop
+// in stage_tail / proportional_counts / train_features unrolls and the stage
+// arrays live in registers.  Same operations, same order as stage_tail +
+// train_features over the full cut list.
+template <int KC>
+__device__ __forceinline__ void cand_features(const PipeDev& pd, const Topo& t, int Kr, const FixedStages& fs,
+                                              double comp_mid, double comp_tail, int pos, double scale, double* red,
+                                              double* tra, double* bal) {
+  constexpr int KM = KC ? KC : kMaxStages;
+  const int K = KC ? KC : Kr;
+  const int P0 = K - 2;
+  double c[KM], a[KM], w[KM];
+#pragma unroll
+  for (int k = 0; k < KM; ++k)
+    if (k < P0) {
+      c[k] = fs.comp[k];
+      a[k] = fs.act[k];
+      w[k] = fs.param[k];
+    }
+  const int64_t wp = pd.wprefix[pos];
+  c[P0] = comp_mid * scale;
+  a[P0] = (double)pd.crossing[pos];
+  w[P0] = (double)(wp - fs.wlast);
+  c[P0 + 1] = comp_tail * scale;
+  a[P0 + 1] = 0.0;
+  w[P0 + 1] = (double)(pd.wtotal - wp);
+  train_features(t, K, c, a, w, red, tra, bal);
+}
+
 // PipeTrainEnv._state (envs.py:378-404) for E envs from the table: one CTA per
 // env computes the raw features of its allowed candidates, then the block max,
 // normalisation and the one-hot block -- one launch, the state written once
 // and normalised from L1/L2.
+template <int KC>
+__device__ __forceinline__ void tab_candidates(const PipeDev& pd, const Topo& t, const int32_t* cand_pos, int C,
+                                               const double* Trow, const double* tail, const uint8_t* m,
+                                               const FixedStages& fs, double scale, double* st, double& mr,
+                                               double& mt) {
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    double red = 0.0, tra = 0.0, bal = 0.0;
+    if (m[c])  // stages: fixed..., [start(alast) .. cand_pos[c]], [cand_pos[c]+1 .. F-1]
+      cand_features<KC>(pd, t, fs.P0 + 2, fs, Trow[c], tail[c], cand_pos[c], scale, &red, &tra, &bal);
+    st[c] = red;
+    st[C + c] = tra;
+    st[2 * C + c] = bal;
+    mr = fmax(mr, red);
+    mt = fmax(mt, tra);
+  }
+}
+
 __global__ void __launch_bounds__(256) train_state_tab_kernel(PipeDev pd, Topo t, const int32_t* cand_pos, int C,
                                                               const double* T, const int32_t* applied, int A,
                                                               const uint8_t* mask, int64_t E, double scale,
                                                               double* state) {
-  __shared__ int s_aidx[kMaxStages], s_apos[kMaxStages], s_P0;
-  __shared__ double s_fix[kMaxStages];
+  __shared__ FixedStages fs;
   __shared__ double s_max[2][32];
   const int64_t W = C + 1;
   const double* tail = T + W * W;
   for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
     if (threadIdx.x == 0) {
       int P0 = 0, a0 = 0;
+      int64_t wprev = 0;
       for (int k = 0; k < A; ++k) {
         const int a = applied[e * A + k];
         if (a >= 0) {
-          s_aidx[P0] = a;
-          s_apos[P0] = cand_pos[a];
-          s_fix[P0] = T[a0 * W + a];  // fixed stage [start(a0) .. cand_pos[a]]
+          const int pos = cand_pos[a];
+          const int64_t wk = pd.wprefix[pos];
+          fs.aidx[P0] = a;
+          fs.comp[P0] = T[a0 * W + a] * scale;  // fixed stage [start(a0) .. pos]
+          fs.act[P0] = (double)pd.crossing[pos];
+          fs.param[P0] = (double)(wk - wprev);
+          wprev = wk;
           a0 = a + 1;
           ++P0;
         }
       }
-      s_P0 = P0;
+      fs.P0 = P0;
+      fs.wlast = wprev;
     }
     __syncthreads();
-    const int P0 = s_P0, P = P0 + 1;
-    const int alast = P0 > 0 ? s_aidx[P0 - 1] + 1 : 0;
+    const int P0 = fs.P0;
+    const double* Trow = T + (P0 > 0 ? fs.aidx[P0 - 1] + 1 : 0) * W;
     double* st = state + e * 4 * (int64_t)C;
     const uint8_t* m = mask + e * (int64_t)C;
     double mr = 0.0, mt = 0.0;
-    for (int c = threadIdx.x; c < C; c += blockDim.x) {
-      double red = 0.0, tra = 0.0, bal = 0.0;
-      if (m[c]) {
-        double cj[kMaxStages], a[kMaxStages], w[kMaxStages];
-        int cuts[kMaxStages];
-        for (int k = 0; k < P0; ++k) {
-          cj[k] = s_fix[k];
-          cuts[k] = s_apos[k];
-        }
-        cj[P0] = T[alast * W + c];  // [start(alast) .. cand_pos[c]]
-        cj[P0 + 1] = tail[c];       // [cand_pos[c]+1 .. F-1]
-        cuts[P0] = cand_pos[c];
-        stage_tail(pd, cuts, P, scale, cj, a, w, nullptr);
-        train_features(t, P + 1, cj, a, w, &red, &tra, &bal);
-      }
-      st[c] = red;
-      st[C + c] = tra;
-      st[2 * C + c] = bal;
-      mr = fmax(mr, red);
-      mt = fmax(mt, tra);
+    switch (P0 + 2) {  // CTA-uniform
+      case 2: tab_candidates<2>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt); break;
+      case 3: tab_candidates<3>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt); break;
+      case 4: tab_candidates<4>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt); break;
+      case 5: tab_candidates<5>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt); break;
+      case 6: tab_candidates<6>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt); break;
+      case 8: tab_candidates<8>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt); break;
+      default: tab_candidates<0>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt); break;
     }
     for (int o = 16; o > 0; o >>= 1) {
       mr = fmax(mr, __shfl_xor_sync(0xffffffffu, mr, o));
@@ -721,10 +774,10 @@ __global__ void __launch_bounds__(256) train_state_tab_kernel(PipeDev pd, Topo t
       if (mr > 0.0) st[c] = st[c] / mr;
       if (mt > 0.0) st[C + c] = st[C + c] / mt;
       double one = 0.0;
-      for (int k = 0; k < P0; ++k) one = s_aidx[k] == c ? 1.0 : one;
+      for (int k = 0; k < P0; ++k) one = fs.aidx[k] == c ? 1.0 : one;
       st[3 * C + c] = one;
     }
-    __syncthreads();  // s_max / s_aidx reused by the next env
+    __syncthreads();  // s_max / fs reused by the next env
   }
 }
 
