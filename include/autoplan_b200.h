@@ -175,6 +175,14 @@ int ap_pipe_metrics(ap_pipe_t p, const int32_t* pivots_dev, int64_t batch, int32
                     double backward_multiplier, double* compute_dev, double* act_dev, double* param_dev,
                     int32_t* nvars_dev, void* stream);
 
+/* ap_pipe_metrics for tuples of candidate positions of a list bound with
+ * ap_pipe_train_table: stage sums are read from the bound table (tuples with
+ * any other pivot fall back to the sweep; an unbound list is plain
+ * ap_pipe_metrics).  Same outputs, bit for bit. */
+int ap_pipe_metrics_bound(ap_pipe_t p, const int32_t* cand_pos_dev, int32_t num_cand, const int32_t* pivots_dev,
+                          int64_t batch, int32_t num_pivots, double backward_multiplier, double* compute_dev,
+                          double* act_dev, double* param_dev, int32_t* nvars_dev, void* stream);
+
 /* Batched proportional_device_cuts + pipeline_length + memory_feasible
  * (pipecost.py:144-252) from per-stage metrics [B, K].  cuts_dev [B, K-1]:
  * if `given_cuts` is non-zero they are inputs, else they are written with

@@ -108,6 +108,7 @@ SIGNATURES: dict[str, tuple] = {
     "ap_pipe_destroy": (ctypes.c_int, [_VP]),
     "ap_pipe_candidates": (ctypes.c_int, [_VP, _TOPO, _I32, _I32, _VP, _VP]),
     "ap_pipe_metrics": (ctypes.c_int, [_VP, _VP, _I64, _I32, _F64, _VP, _VP, _VP, _VP, _VP]),
+    "ap_pipe_metrics_bound": (ctypes.c_int, [_VP, _VP, _I32, _VP, _I64, _I32, _F64, _VP, _VP, _VP, _VP, _VP]),
     "ap_pipe_length": (ctypes.c_int, [_TOPO, _I32, _I32, _I64, _VP, _VP, _VP, _VP, _I32, _F64, _F64, _I32, _VP, _VP,
                                       _VP]),
     "ap_pipe_train_state": (ctypes.c_int, [_VP, _TOPO, _VP, _I32, _VP, _I32, _VP, _I64, _F64, _VP, _VP]),

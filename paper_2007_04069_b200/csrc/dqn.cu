@@ -23,17 +23,30 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
-__global__ void dueling_kernel(const float* z, int64_t ldz, float* q, int64_t ldq, int B, int A) {
+// Q = V + A - mean(A), one warp per row.  Loads are issued 4 deep ahead of the
+// adds (each lane's add order is unchanged); z and q never alias.
+__global__ void dueling_kernel(const float* __restrict__ z, int64_t ldz, float* __restrict__ q, int64_t ldq, int B,
+                               int A) {
   const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (b >= B) return;
-  const float* row = z + (int64_t)b * ldz;
+  const float* __restrict__ row = z + (int64_t)b * ldz + 1;
+  float* __restrict__ out = q + (int64_t)b * ldq;
   float s = 0.0f;
-  for (int j = lane; j < A; j += 32) s += row[1 + j];
+  int j = lane;
+  for (; j + 96 < A; j += 128) {
+    const float x0 = row[j], x1 = row[j + 32], x2 = row[j + 64], x3 = row[j + 96];
+    s += x0;
+    s += x1;
+    s += x2;
+    s += x3;
+  }
+  for (; j < A; j += 32) s += row[j];
   for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
   const float mean = s / (float)A;
-  const float v = row[0];
-  for (int j = lane; j < A; j += 32) q[(int64_t)b * ldq + j] = v + row[1 + j] - mean;
+  const float v = z[(int64_t)b * ldz];
+#pragma unroll 4
+  for (int k = lane; k < A; k += 32) out[k] = v + row[k] - mean;
 }
 
 // masked argmax (ties -> lowest index); eps-greedy with a counter-based hash
@@ -65,19 +78,32 @@ __global__ void act_kernel(const float* q, int64_t ldq, const uint8_t* mask, int
     eps = epsilon_dev(ctl[AP_CTL_TRAIN], eps0, eps1, decay);
     seed = (uint64_t)ctl[AP_CTL_STEP] + 1;
   }
-  const uint8_t* m = mask + (int64_t)e * ldm;
+  const uint8_t* __restrict__ m = mask + (int64_t)e * ldm;
+  const float* __restrict__ qr = q + (int64_t)e * ldq;
   int count = 0;
   float best = -INFINITY;
   int best_j = 0x7fffffff;
-  for (int j = lane; j < A; j += 32) {
-    if (!m[j]) continue;
+  auto visit = [&](int j, uint8_t ok, float v) {
+    if (!ok) return;
     ++count;
-    const float v = q[(int64_t)e * ldq + j];
     if (v > best || (v == best && j < best_j)) {
       best = v;
       best_j = j;
     }
+  };
+  int j = lane;
+  for (; j + 96 < A; j += 128) {  // 4 rows of loads in flight, visited in ascending j
+    uint8_t ok[4];
+    float v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      ok[u] = m[j + 32 * u];
+      v[u] = qr[j + 32 * u];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) visit(j + 32 * u, ok[u], v[u]);
   }
+  for (; j < A; j += 32) visit(j, m[j], qr[j]);
   for (int o = 16; o; o >>= 1) {
     const float ov = __shfl_xor_sync(kFull, best, o);
     const int oj = __shfl_xor_sync(kFull, best_j, o);

@@ -689,6 +689,48 @@ __device__ __forceinline__ void cand_features(const PipeDev& pd, const Topo& t, 
   train_features(t, K, c, a, w, red, tra, bal);
 }
 
+__global__ void index_positions_kernel(const int32_t* cand_pos, int C, int F, int32_t* idx_of_pos) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < C && cand_pos[c] >= 0 && cand_pos[c] < F) idx_of_pos[cand_pos[c]] = c;
+}
+
+// Batched stage_metrics from the table: a tuple whose pivots are all bound
+// candidates, strictly increasing, reads its stage sums (stage k =
+// T[after previous pivot][pivot k], the last T[..][C]); any other tuple takes
+// the sequential sweep.  Outputs are those of metrics_kernel.
+__global__ void metrics_tab_kernel(PipeDev pd, const int32_t* idx_of_pos, int C, const double* T,
+                                   const int32_t* pivots, int64_t batch, int P, double scale, double* comp,
+                                   double* act, double* param, int32_t* nvars) {
+  const int64_t W = C + 1;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < batch; b += (int64_t)gridDim.x * blockDim.x) {
+    int cuts[kMaxStages];
+    double c[kMaxStages], a[kMaxStages], w[kMaxStages];
+    int v[kMaxStages];
+    bool ok = true;
+    int prev = -1;
+    for (int k = 0; k < P; ++k) {
+      const int pos = pivots[b * P + k];
+      cuts[k] = pos;
+      const int idx = (pos >= 0 && pos < pd.F) ? idx_of_pos[pos] : -1;
+      ok = ok && idx > prev;
+      if (ok) c[k] = T[(prev + 1) * W + idx];
+      prev = idx;
+    }
+    if (ok) {
+      c[P] = T[(prev + 1) * W + C];
+      stage_tail(pd, cuts, P, scale, c, a, w, v);
+    } else {
+      stage_metrics_dev(pd, pd.cost, cuts, P, scale, c, a, w, v);
+    }
+    for (int k = 0; k <= P; ++k) {
+      comp[b * (P + 1) + k] = c[k];
+      act[b * (P + 1) + k] = a[k];
+      param[b * (P + 1) + k] = w[k];
+      if (nvars) nvars[b * (P + 1) + k] = v[k];
+    }
+  }
+}
+
 // PipeTrainEnv._state (envs.py:378-404) for E envs from the table: one CTA per
 // env computes the raw features of its allowed candidates, then the block max,
 // normalisation and the one-hot block -- one launch, the state written once
@@ -710,7 +752,10 @@ __device__ __forceinline__ void tab_candidates(const PipeDev& pd, const Topo& t,
   }
 }
 
-__global__ void __launch_bounds__(256) train_state_tab_kernel(PipeDev pd, Topo t, const int32_t* cand_pos, int C,
+#ifndef AP_PP_TAB_MINB
+#define AP_PP_TAB_MINB 4  // measured on B200: 4 (64 regs) > 3 > 2 (124 regs, 25% occupancy)
+#endif
+__global__ void __launch_bounds__(256, AP_PP_TAB_MINB) train_state_tab_kernel(PipeDev pd, Topo t, const int32_t* cand_pos, int C,
                                                               const double* T, const int32_t* applied, int A,
                                                               const uint8_t* mask, int64_t E, double scale,
                                                               double* state) {
@@ -1121,12 +1166,17 @@ struct ap_pipe {
     const int32_t* cand;
     int32_t C;
     double* tab;
+    int32_t* idx_of_pos;  // [F]: candidate index at a forward position, -1 elsewhere
   };
   std::vector<TableBinding> tables;
-  const double* table_for(const int32_t* cand, int32_t C) const {
+  const TableBinding* binding(const int32_t* cand, int32_t C) const {
     for (const auto& b : tables)
-      if (b.cand == cand && b.C == C) return b.tab;
+      if (b.cand == cand && b.C == C) return &b;
     return nullptr;
+  }
+  const double* table_for(const int32_t* cand, int32_t C) const {
+    const TableBinding* b = binding(cand, C);
+    return b ? b->tab : nullptr;
   }
 
   int ensure_train_scratch(int64_t n_list, int64_t n_env) {
@@ -1168,7 +1218,10 @@ struct ap_pipe {
     return PipeDev{F, d_cost.ptr, d_crossing.ptr, d_wprefix.ptr, d_vprefix.ptr, wtotal, vtotal};
   }
   void release() {
-    for (auto& b : tables) cudaFree(b.tab);
+    for (auto& b : tables) {
+      cudaFree(b.tab);
+      cudaFree(b.idx_of_pos);
+    }
     tables.clear();
     if (d_fixed) cudaFree(d_fixed);
     if (d_R) cudaFree(d_R);
@@ -1299,6 +1352,25 @@ int ap_pipe_metrics(ap_pipe_t p, const int32_t* pivots, int64_t batch, int32_t P
   return AP_OK;
 }
 
+int ap_pipe_metrics_bound(ap_pipe_t p, const int32_t* cand_pos, int32_t C, const int32_t* pivots, int64_t batch,
+                          int32_t P, double bwm, double* comp, double* act, double* param, int32_t* nvars,
+                          void* stream) {
+  const auto* bnd = p ? p->binding(cand_pos, C) : nullptr;
+  if (!bnd || std::getenv("AP_PP_NO_TABLE")) return ap_pipe_metrics(p, pivots, batch, P, bwm, comp, act, param, nvars,
+                                                                     stream);
+  if (batch < 0 || P < 0 || P + 1 > kMaxStages || (batch && (!comp || !act || !param || (P && !pivots)))) {
+    set_error("ap_pipe_metrics_bound: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  int rc = p->ensure();
+  if (rc != AP_OK) return rc;
+  if (batch == 0) return AP_OK;
+  metrics_tab_kernel<<<grid_for(batch, 128), 128, 0, (cudaStream_t)stream>>>(
+      p->dev(), bnd->idx_of_pos, C, bnd->tab, pivots, batch, P, 1.0 + bwm, comp, act, param, nvars);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
 int ap_pipe_length(const ap_topology* topo, int32_t K, int32_t M, int64_t batch, const double* comp,
                    const double* act, const double* param, int32_t* cuts, int32_t given, double mem, double opt,
                    int32_t python_floats, double* len, uint8_t* feas, void* stream) {
@@ -1338,11 +1410,17 @@ int ap_pipe_train_table(ap_pipe_t p, const int32_t* cand_pos, int32_t C, void* s
       set_error("ap_pipe_train_table: cannot allocate a new table during stream capture");
       return AP_ERR_INVALID;
     }
+    int32_t* iop = nullptr;
     AP_CUDA_CHECK(cudaMalloc(&tab, bytes));
-    p->tables.push_back({cand_pos, C, tab});
+    AP_CUDA_CHECK(cudaMalloc(&iop, (size_t)p->F * sizeof(int32_t)));
+    p->tables.push_back({cand_pos, C, tab, iop});
   }
   // (re)built from the list's current contents
+  const auto* bnd = p->binding(cand_pos, C);
   train_table_kernel<<<(int)((W + 127) / 128), 128, 0, (cudaStream_t)stream>>>(p->dev(), cand_pos, C, tab);
+  AP_CUDA_CHECK(cudaGetLastError());
+  AP_CUDA_CHECK(cudaMemsetAsync(bnd->idx_of_pos, 0xff, (size_t)p->F * sizeof(int32_t), (cudaStream_t)stream));
+  index_positions_kernel<<<(C + 255) / 256, 256, 0, (cudaStream_t)stream>>>(cand_pos, C, p->F, bnd->idx_of_pos);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }

@@ -142,9 +142,34 @@ __global__ void per_push_kernel(int E, int S, int A, int64_t slot0, int64_t cap,
   const int e = blockIdx.x;
   if (ctl) slot0 = ctl[AP_CTL_SLOT];
   const int64_t slot = (slot0 + e) % cap;
-  for (int j = threadIdx.x; j < S; j += blockDim.x) {
-    r_states[slot * S + j] = states[(int64_t)e * lds + j];
-    r_next[slot * S + j] = next_states[(int64_t)e * lds + j];
+  // the replay ring never aliases the env's state rows: loads are batched
+  // ahead of the stores (16-byte vectors when rows and bases allow)
+  const float* __restrict__ s_in = states + (int64_t)e * lds;
+  const float* __restrict__ n_in = next_states + (int64_t)e * lds;
+  float* __restrict__ s_out = r_states + slot * S;
+  float* __restrict__ n_out = r_next + slot * S;
+  const bool vec = (S % 4 == 0) && (lds % 4 == 0) &&
+                   ((reinterpret_cast<uintptr_t>(states) | reinterpret_cast<uintptr_t>(next_states) |
+                     reinterpret_cast<uintptr_t>(r_states) | reinterpret_cast<uintptr_t>(r_next)) % 16 == 0);
+  if (vec) {
+    const int S4 = S / 4;
+    const float4* __restrict__ a = reinterpret_cast<const float4*>(s_in);
+    const float4* __restrict__ b = reinterpret_cast<const float4*>(n_in);
+    float4* __restrict__ ao = reinterpret_cast<float4*>(s_out);
+    float4* __restrict__ bo = reinterpret_cast<float4*>(n_out);
+#pragma unroll 4
+    for (int j = threadIdx.x; j < S4; j += blockDim.x) {
+      const float4 x = a[j], y = b[j];
+      ao[j] = x;
+      bo[j] = y;
+    }
+  } else {
+#pragma unroll 4
+    for (int j = threadIdx.x; j < S; j += blockDim.x) {
+      const float x = s_in[j], y = n_in[j];
+      s_out[j] = x;
+      n_out[j] = y;
+    }
   }
   for (int j = threadIdx.x; j < A; j += blockDim.x) r_masks[slot * A + j] = masks[(int64_t)e * A + j];
   if (threadIdx.x == 0) {

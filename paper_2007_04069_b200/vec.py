@@ -209,8 +209,9 @@ class VecPipeTrainEnv:
         self.obs.copy_(self.cur_state)
         _native.check(lib.ap_vec_pipe_apply(self.E, self.P, P_(actions), P_(self.cand_pos), P_(self.picks),
                                             P_(self.positions), P_(self.n_applied), P_(self.done), _s()))
-        _native.check(lib.ap_pipe_metrics(self.host._model.handle, P_(self.positions), self.E, self.P, self.bwm,
-                                          P_(self.comp), P_(self.act), P_(self.param), P_(self.nvars), _s()))
+        _native.check(lib.ap_pipe_metrics_bound(self.host._model.handle, P_(self.cand_pos), self.C, P_(self.positions),
+                                                self.E, self.P, self.bwm, P_(self.comp), P_(self.act), P_(self.param),
+                                                P_(self.nvars), _s()))
         _native.check(lib.ap_pipe_length(ctypes.byref(self.topo_c), self.K, self.micro_batches, self.E, P_(self.comp),
                                          P_(self.act), P_(self.param), P_(self.cuts), 0, self.mem, 4.0, 1,
                                          P_(self.length), P_(self.feasible), _s()))

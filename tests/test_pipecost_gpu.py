@@ -233,3 +233,38 @@ def test_train_state_reuse_matches_full_sweep(cuda, monkeypatch, K):
     full = run()
     assert torch.equal(reuse, full)
     assert torch.equal(table, full)
+
+
+@pytest.mark.parametrize("K", [2, 4, 6])
+def test_metrics_bound_matches_sweep(cuda, K):
+    """ap_pipe_metrics_bound (stage sums from the bound table) equals ap_pipe_metrics bit for bit,
+    including tuples with non-candidate pivots (the per-tuple sweep fallback)."""
+    from paper_2007_04069_b200 import _native, graphs
+
+    g = graphs.generate("bert48")
+    env = PipeTrainEnv(g, DeviceTopology(2, 4), K, radius=3)
+    C, P = env.num_actions, K - 1
+    F = env._model.num_forward
+    rng = np.random.default_rng(K)
+    rows = [np.sort(rng.choice(C, size=P, replace=False)) for _ in range(300)]
+    piv = np.stack([env._cand_pos[r] for r in rows]).astype(np.int32)
+    for b in range(0, 300, 7):  # some tuples with an arbitrary forward position
+        piv[b] = np.sort(rng.choice(F - 1, size=P, replace=False))
+    piv[1, -1] = env._cand_pos[-1]  # last candidate as the final pivot
+    d_cand = torch.from_numpy(env._cand_pos).cuda()
+    assert env._model.bind_candidates(d_cand)
+    d_piv = torch.from_numpy(piv).cuda()
+    lib = _native.require_device()
+    P_ = _native.ptr
+
+    def out():
+        return [torch.full((300, K), float("nan"), dtype=torch.float64, device="cuda") for _ in range(3)] + [
+            torch.full((300, K), -7, dtype=torch.int32, device="cuda")]
+
+    a, b = out(), out()
+    _native.check(lib.ap_pipe_metrics(env._model.handle, P_(d_piv), 300, P, 2.0, *[P_(x) for x in a],
+                                      _native.stream_handle()))
+    _native.check(lib.ap_pipe_metrics_bound(env._model.handle, P_(d_cand), C, P_(d_piv), 300, P, 2.0,
+                                            *[P_(x) for x in b], _native.stream_handle()))
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
