@@ -439,6 +439,76 @@ struct AdamSegments {
   int n;
 };
 
+// one Adam element update (shared by the flat and tiled kernels: same code, same rounding)
+__device__ __forceinline__ float adam_elem(float* p, const float* g, float* m, float* v, int64_t i, float lr, float b1,
+                                           float b2, float eps, float c1, float c2) {
+  const float gi = g[i];
+  const float mi = b1 * m[i] + (1.0f - b1) * gi;
+  const float vi = b2 * v[i] + (1.0f - b2) * gi * gi;
+  m[i] = mi;
+  v[i] = vi;
+  const float pi = p[i] - lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+  p[i] = pi;
+  return pi;
+}
+
+// Tiled adam_t: one 256-thread block per 32x32 tile of a weight segment
+// (coalesced reads / writes of p, g, m, v; the transposed copy goes out
+// through a shared-memory tile, coalesced as well), then flat blocks over the
+// elements outside every segment (biases).  tile_base / gap ranges are built
+// on the host; segments are disjoint.
+struct AdamTiles {
+  AdamSegments segs;
+  int64_t tile_base[9];
+  int32_t tcols[8];
+  int64_t gap_lo[9], gap_base[10];
+  int ngap;
+};
+
+__global__ void __launch_bounds__(256) adam_tile_kernel(float* p, const float* g, float* m, float* v, float lr,
+                                                        float b1, float b2, float eps, const int64_t* ctl,
+                                                        AdamTiles at) {
+  __shared__ float s_c[2];
+  __shared__ float tile[32][33];
+  if (threadIdx.x == 0) {
+    const double t = (double)(ctl[AP_CTL_TRAIN] + 1);
+    s_c[0] = (float)(1.0 - pow((double)b1, t));
+    s_c[1] = (float)(1.0 - pow((double)b2, t));
+  }
+  __syncthreads();
+  const float c1 = s_c[0], c2 = s_c[1];
+  const int64_t ntiles = at.tile_base[at.segs.n];
+  const int64_t blk = blockIdx.x;
+  if (blk < ntiles) {
+    int s = 0;
+    while (blk >= at.tile_base[s + 1]) ++s;
+    const int64_t t = blk - at.tile_base[s];
+    const int tr = (int)(t / at.tcols[s]), tc = (int)(t % at.tcols[s]);
+    const int rows = at.segs.rows[s], cols = at.segs.cols[s];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int64_t off = at.segs.off[s];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int r = tr * 32 + ty + 8 * k, c = tc * 32 + tx;
+      if (r < rows && c < cols) tile[ty + 8 * k][tx] = adam_elem(p, g, m, v, off + (int64_t)r * cols + c, lr, b1, b2, eps, c1, c2);
+    }
+    __syncthreads();
+    float* dst = at.segs.dst[s];
+    const int64_t ldd = at.segs.ldd[s];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int c = tc * 32 + ty + 8 * k, r = tr * 32 + tx;  // dst[c][r] = w[r][c]
+      if (r < rows && c < cols) dst[(int64_t)c * ldd + r] = tile[tx][ty + 8 * k];
+    }
+    return;
+  }
+  const int64_t idx = (blk - ntiles) * blockDim.x + threadIdx.x;
+  if (idx >= at.gap_base[at.ngap]) return;
+  int q = 0;
+  while (idx >= at.gap_base[q + 1]) ++q;
+  adam_elem(p, g, m, v, at.gap_lo[q] + (idx - at.gap_base[q]), lr, b1, b2, eps, c1, c2);
+}
+
 __global__ void adam_t_kernel(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
                               float eps, const int64_t* ctl, AdamSegments segs) {
   __shared__ float s_c[2];
@@ -450,13 +520,7 @@ __global__ void adam_t_kernel(float* p, const float* g, float* m, float* v, int6
   __syncthreads();
   const float c1 = s_c[0], c2 = s_c[1];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const float gi = g[i];
-    const float mi = b1 * m[i] + (1.0f - b1) * gi;
-    const float vi = b2 * v[i] + (1.0f - b2) * gi * gi;
-    m[i] = mi;
-    v[i] = vi;
-    const float pi = p[i] - lr * (mi / c1) / (sqrtf(vi / c2) + eps);
-    p[i] = pi;
+    const float pi = adam_elem(p, g, m, v, i, lr, b1, b2, eps, c1, c2);
     for (int s = 0; s < segs.n; ++s) {
       const int64_t rel = i - segs.off[s];
       if (rel >= 0 && rel < (int64_t)segs.rows[s] * segs.cols[s]) {
@@ -805,8 +869,45 @@ int ap_dqn_adam_ctl_t(float* params, const float* grads, float* m, float* v, int
     segs.dst[s] = seg_dst[s];
     segs.ldd[s] = seg_ldd[s];
   }
-  adam_t_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(params, grads, m, v, n, lr, beta1, beta2, eps,
-                                                                       ctl, segs);
+  // tiled path when the segments are disjoint and inside [0, n)
+  int order[8];
+  for (int s = 0; s < nseg; ++s) order[s] = s;
+  std::sort(order, order + nseg, [&](int a, int b) { return segs.off[a] < segs.off[b]; });
+  bool tiled = std::getenv("AP_ADAM_FLAT") == nullptr;
+  int64_t end = 0;
+  for (int k = 0; k < nseg && tiled; ++k) {
+    const int s = order[k];
+    tiled = segs.off[s] >= end && segs.rows[s] > 0 && segs.cols[s] > 0;
+    end = segs.off[s] + (int64_t)segs.rows[s] * segs.cols[s];
+  }
+  tiled = tiled && end <= n;
+  if (tiled) {
+    AdamTiles at{};
+    at.segs = segs;
+    at.tile_base[0] = 0;
+    for (int s = 0; s < nseg; ++s) {
+      at.tcols[s] = (segs.cols[s] + 31) / 32;
+      at.tile_base[s + 1] = at.tile_base[s] + (int64_t)((segs.rows[s] + 31) / 32) * at.tcols[s];
+    }
+    int64_t lo = 0;
+    at.ngap = 0;
+    at.gap_base[0] = 0;
+    for (int k = 0; k <= nseg; ++k) {
+      const int64_t hi = k < nseg ? segs.off[order[k]] : n;
+      if (hi > lo) {
+        at.gap_lo[at.ngap] = lo;
+        at.gap_base[at.ngap + 1] = at.gap_base[at.ngap] + (hi - lo);
+        ++at.ngap;
+      }
+      if (k < nseg) lo = segs.off[order[k]] + (int64_t)segs.rows[order[k]] * segs.cols[order[k]];
+    }
+    const int64_t blocks = at.tile_base[nseg] + (at.gap_base[at.ngap] + 255) / 256;
+    adam_tile_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(params, grads, m, v, lr, beta1, beta2, eps,
+                                                                         ctl, at);
+  } else {
+    adam_t_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(params, grads, m, v, n, lr, beta1, beta2, eps,
+                                                                         ctl, segs);
+  }
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }

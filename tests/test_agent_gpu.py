@@ -144,3 +144,33 @@ def test_pp_infer_trace_replay(cuda):
     env = PipeInferEnv(Arrays, topo, rec["stages"], micro_batches=rec["micro_batches"], allowed_boundaries=bb,
                        allowed_cuts=cc)
     assert replay(env, rec["trace"]) == trace_of(rec["trace"])
+
+
+@pytest.mark.parametrize("shape", [(37, 5, (45, 33)), (1414, 9, (256, 256))])
+def test_adam_tiled_transposed_matches_flat(cuda, monkeypatch, shape):
+    """ap_dqn_adam_ctl_t: the tiled kernel (32x32 tiles, transposed copies through shared memory,
+    flat blocks for the biases) equals the flat per-element kernel bit for bit."""
+    from paper_2007_04069_b200 import _native
+
+    s, a, hidden = shape
+    lib = _native.require_device()
+    P = _native.ptr
+
+    def run():
+        net = QNetwork(s, a, hidden, np.random.default_rng(3))
+        gen = torch.Generator(device="cuda").manual_seed(5)
+        net.grad.copy_(torch.randn(net.grad.shape, generator=gen, device="cuda"))
+        m = torch.randn(net.flat.shape, generator=gen, device="cuda") * 0.1
+        v = torch.rand(net.flat.shape, generator=gen, device="cuda") * 0.1
+        ctl = torch.tensor([0, 0, 0, 7], dtype=torch.int64, device="cuda")
+        for t in net.wt.values():
+            t.fill_(float("nan"))
+        _native.check(lib.ap_dqn_adam_ctl_t(P(net.flat), P(net.grad), P(m), P(v), net.flat.numel(), 1e-3, 0.9, 0.999,
+                                            1e-8, P(ctl), *net.adam_segments(), _native.stream_handle()))
+        return [net.flat.clone(), m, v] + [t.clone() for t in net.wt.values()]
+
+    tiled = run()
+    monkeypatch.setenv("AP_ADAM_FLAT", "1")
+    flat = run()
+    for x, y in zip(tiled, flat):
+        assert torch.equal(x.nan_to_num(7.0), y.nan_to_num(7.0))
