@@ -32,6 +32,32 @@ from . import _native
 from .tc import gemm
 
 
+def fork_to(side) -> None:
+    """`side` waits for all work issued so far on the current stream (a graph fork under capture)."""
+    import torch
+
+    ev = torch.cuda.Event()
+    ev.record(torch.cuda.current_stream())
+    side.wait_event(ev)
+
+
+def join_from(side) -> None:
+    """The current stream waits for `side` (a graph join under capture)."""
+    import torch
+
+    ev = torch.cuda.Event()
+    ev.record(side)
+    torch.cuda.current_stream().wait_event(ev)
+
+
+def stream_or_current(side):
+    import contextlib
+
+    import torch
+
+    return torch.cuda.stream(side) if side is not None else contextlib.nullcontext()
+
+
 class CheckpointError(Exception):
     """A checkpoint file does not match the expected layout."""
 
@@ -237,7 +263,7 @@ class QNetwork:
             raise ValueError(f"expected state dim {self.state_dim}, got {x.shape[1]}")
         return self.forward_device(x).double().cpu().numpy()
 
-    def backward_device(self, acts, dz, dz_t=None) -> None:
+    def backward_device(self, acts, dz, dz_t=None, side=None) -> None:
         """Gradients into self.grad from dLoss/dz (z = [V, A] head outputs).
 
         `dz_t` (optional) is dz^T already materialised (ap_dqn_td_ring writes it).
@@ -247,7 +273,12 @@ class QNetwork:
         transposed into a ones-augmented [in + 1, B] buffer (all layers in one
         launch), and since b_i follows w_i in the flat buffer the GEMM writes the
         [in + 1, out] block [dW_i; db_i] at once: the bias gradient is the ones-row
-        product, the column sum of dh (agent.py:118, 134)."""
+        product, the column sum of dh (agent.py:118, 134).
+
+        `side` (a CUDA stream): the weight-gradient GEMMs run there, a parallel
+        branch beside the data-gradient chain (one graph branch under capture);
+        joined back before returning.  Tensors read across streams stay
+        referenced until the join, so the caching allocator cannot recycle them."""
         import ctypes
 
         import torch
@@ -263,8 +294,13 @@ class QNetwork:
             (ctypes.c_int64 * n)(*[a.stride(0) for a in acts]), (ctypes.c_void_p * n)(*[t.data_ptr() for t in aug]),
             (ctypes.c_int64 * n)(*[t.stride(0) for t in aug]), (ctypes.c_int32 * n)(*[b] * n),
             (ctypes.c_int32 * n)(*[a.shape[1] for a in acts]), _stream()))
-        gemm(aug[L], dz_t if dz_t is not None else dz.t().contiguous(), trans_b=True, out=self._grad_block("wh"),
-             precision=self.precision)
+        keep = []
+        if dz_t is None:
+            dz_t = dz.t().contiguous()
+        if side is not None:
+            fork_to(side)
+        with stream_or_current(side):
+            gemm(aug[L], dz_t, trans_b=True, out=self._grad_block("wh"), precision=self.precision)
         # head -> last hidden layer: K = 1 + A is too narrow for the tensor cores;
         # one kernel does dz @ wh^T, the ReLU mask and the transposed copy
         h = acts[-1]
@@ -275,13 +311,20 @@ class QNetwork:
         _native.check(lib.ap_dqn_head_backward(P(dz), dz.stride(0), P(wh), wh.stride(0), P(h), h.stride(0), b, H,
                                                dz.shape[1], P(dh), dh.stride(0), P(dh_t), dh_t.stride(0), _stream()))
         for i in range(L - 1, -1, -1):
-            gemm(aug[i], dh_t, trans_b=True, out=self._grad_block(f"w{i}"), precision=self.precision)
+            if side is not None:
+                fork_to(side)  # the branch waits for this layer's dh_t
+                keep.append(dh_t)
+            with stream_or_current(side):
+                gemm(aug[i], dh_t, trans_b=True, out=self._grad_block(f"w{i}"), precision=self.precision)
             if i > 0:  # gradient into layer i-1's output: dh @ W_i^T, ReLU mask, K-major copy
                 dh = gemm(dh, self.views[f"w{i}"], trans_b=True, precision=self.precision)
                 hin = acts[i]
                 dh_t = torch.empty((dh.shape[1], b), dtype=torch.float32, device="cuda")
                 _native.check(lib.ap_dqn_relu_backward_t(P(dh), dh.stride(0), P(hin), hin.stride(0), b, dh.shape[1],
                                                          P(dh_t), dh_t.stride(0), _stream()))
+        if side is not None:
+            join_from(side)
+        del keep
 
     def _augmented(self, b: int):
         """Per-batch-size [in + 1, b] buffers (last row ones) for each layer's input."""

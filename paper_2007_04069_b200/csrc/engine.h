@@ -136,6 +136,12 @@ int launch_propagate_fast(const GraphTables* g, const DecisionTables* d, const i
 
 int launch_gemm_v2(const float* A, int64_t lda, int transA, const float* B, int64_t ldb, int transB, float* C,
                    int64_t ldc, int M, int N, int K, const float* bias, int relu, int precision, cudaStream_t stream);
+// Split-K partials workspace of at least `bytes`, one per stream (concurrent
+// GEMMs on parallel graph branches never share it).  Grow-only: a captured
+// graph may hold an older buffer, so none is freed, and none grows inside a
+// capture (AP_ERR_INVALID then; warm the shapes up eagerly first).
+int splitk_workspace(cudaStream_t stream, size_t bytes, float** out);
+
 int launch_gemm_v3(const float* A, int64_t lda, int transA, const float* B, int64_t ldb, int transB, float* C,
                    int64_t ldc, int M, int N, int K, const float* bias, int relu, int precision, cudaStream_t stream);
 

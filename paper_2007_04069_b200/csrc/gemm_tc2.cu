@@ -20,6 +20,9 @@
 //   MN-major: (r/4)*512  + (k/8)*128 + (k%8)*16 + (r%4)*4   LBO 128, SBO 512
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
+#include <unordered_map>
+#include <utility>
 
 #include "engine.h"
 
@@ -269,8 +272,6 @@ int run(const G2& g, dim3 grid, cudaStream_t stream) {
   return AP_OK;
 }
 
-float* g_work = nullptr;
-size_t g_work_bytes = 0;
 
 }  // namespace
 
@@ -296,22 +297,8 @@ int launch_gemm_v2(const float* A, int64_t lda, int transA, const float* B, int6
   g.kps = (nk + splits - 1) / splits;
   splits = (nk + g.kps - 1) / g.kps;
   if (splits > 1) {
-    const size_t need = (size_t)splits * M * N * sizeof(float);
-    if (need > g_work_bytes) {
-      // A captured CUDA graph may hold the old workspace: never free it, and
-      // never allocate inside a capture (warm the shapes up eagerly first).
-      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-      AP_CUDA_CHECK(cudaStreamIsCapturing(stream, &cs));
-      if (cs != cudaStreamCaptureStatusNone) {
-        set_error("gemm: split-K workspace must grow during graph capture; run the shapes once before capturing");
-        return AP_ERR_INVALID;
-      }
-      float* fresh = nullptr;
-      AP_CUDA_CHECK(cudaMalloc(&fresh, need));
-      g_work = fresh;  // the previous buffer is intentionally kept alive
-      g_work_bytes = need;
-    }
-    g.work = g_work;
+    const int wrc = splitk_workspace(stream, (size_t)splits * M * N * sizeof(float), &g.work);
+    if (wrc != AP_OK) return wrc;
   }
   dim3 grid(mt, nt, splits);
   int rc;
@@ -323,9 +310,32 @@ int launch_gemm_v2(const float* A, int64_t lda, int transA, const float* B, int6
   if (rc != AP_OK || splits == 1) return rc;
   const int64_t total = (int64_t)M * N;
   splitk_reduce_kernel<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, stream>>>(
-      g_work, splits, M, N, C, ldc, bias, relu);
+      g.work, splits, M, N, C, ldc, bias, relu);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
 
 }  // namespace apb
+
+namespace apb {
+int splitk_workspace(cudaStream_t stream, size_t bytes, float** out) {
+  static std::mutex mu;
+  static std::unordered_map<cudaStream_t, std::pair<float*, size_t>> ws;
+  std::lock_guard<std::mutex> lock(mu);
+  auto& w = ws[stream];
+  if (bytes > w.second) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    AP_CUDA_CHECK(cudaStreamIsCapturing(stream, &cs));
+    if (cs != cudaStreamCaptureStatusNone) {
+      set_error("gemm: split-K workspace must grow during graph capture; run the shapes once before capturing");
+      return AP_ERR_INVALID;
+    }
+    float* fresh = nullptr;
+    AP_CUDA_CHECK(cudaMalloc(&fresh, bytes));
+    w = {fresh, bytes};  // the previous buffer is intentionally kept alive
+  }
+  *out = w.first;
+  return AP_OK;
+}
+}  // namespace apb
+

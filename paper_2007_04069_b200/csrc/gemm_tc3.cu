@@ -305,8 +305,6 @@ int run3(const CUtensorMap& ma, const CUtensorMap& mb, const G3& g, dim3 grid, c
   return AP_OK;
 }
 
-float* g_work3 = nullptr;
-size_t g_work3_bytes = 0;
 
 }  // namespace
 
@@ -336,21 +334,8 @@ int launch_gemm_v3(const float* A, int64_t lda, int transA, const float* B, int6
   splits = (nk + g.kps - 1) / g.kps;
   if (splits > 1 && !no_cluster) g.cluster = 1;
   if (splits > 1 && !g.cluster) {
-    const size_t need = (size_t)splits * M * N * sizeof(float);
-    if (need > g_work3_bytes) {
-      // a captured graph may hold the old workspace: never free it, never grow mid-capture
-      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-      AP_CUDA_CHECK(cudaStreamIsCapturing(stream, &cs));
-      if (cs != cudaStreamCaptureStatusNone) {
-        set_error("gemm: split-K workspace must grow during graph capture; run the shapes once before capturing");
-        return AP_ERR_INVALID;
-      }
-      float* fresh = nullptr;
-      AP_CUDA_CHECK(cudaMalloc(&fresh, need));
-      g_work3 = fresh;
-      g_work3_bytes = need;
-    }
-    g.work = g_work3;
+    const int wrc = splitk_workspace(stream, (size_t)splits * M * N * sizeof(float), &g.work);
+    if (wrc != AP_OK) return wrc;
   }
   const dim3 grid(mt, nt, splits);
   const int rc = four_stages ? (bn == 32 ? run3<32, 4>(ma, mb, g, grid, stream) : run3<64, 4>(ma, mb, g, grid, stream))
@@ -358,7 +343,7 @@ int launch_gemm_v3(const float* A, int64_t lda, int transA, const float* B, int6
   if (rc != AP_OK || splits == 1 || g.cluster) return rc;
   const int64_t total = (int64_t)M * N;
   splitk_reduce3_kernel<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, stream>>>(
-      g_work3, splits, M, N, C, ldc, bias, relu);
+      g.work, splits, M, N, C, ldc, bias, relu);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }

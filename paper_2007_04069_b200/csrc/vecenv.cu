@@ -223,7 +223,19 @@ __global__ void __launch_bounds__(kSampleThreads) per_sample_fast_kernel(
   const int chunk = ((n + 31) / 32 + 31) / 32 * 32;
   const int lo = warp * chunk, hi = min(n, lo + chunk);
   double tot = 0.0, mx = 0.0;
-  for (int base = lo; base < hi; base += 32) {
+  int base = lo;
+  for (; base + 128 <= hi; base += 128) {  // 4 loads in flight; the same per-lane accumulation order
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldg(prio + base + 32 * u + lane);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      c[base + 32 * u + lane] = v[u];
+      tot += v[u];
+      mx = fmax(mx, v[u]);
+    }
+  }
+  for (; base < hi; base += 32) {
     const int i = base + lane;
     const double v = i < hi ? prio[i] : 0.0;
     if (i < hi) c[i] = v;
@@ -480,12 +492,20 @@ __global__ void ctl_advance_kernel(int64_t* ctl, int mode, int64_t E, int64_t ca
 // ctl != nullptr: also counts the finished learn step (ctl[AP_CTL_TRAIN] += 1)
 __global__ void per_update_scaled_kernel(double* scaled, const int32_t* idx, const float* td, int B, double alpha,
                                          int64_t* ctl) {
+  __shared__ int32_t s_idx[1024];  // the batch's indices for the duplicate scan (B <= 1024)
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (ctl && b == 0) ctl[AP_CTL_TRAIN] += 1;
+  const bool staged = B <= 1024;
+  if (staged) {
+    for (int k = threadIdx.x; k < B; k += blockDim.x) s_idx[k] = idx[k];
+    __syncthreads();
+  }
   if (b >= B) return;
-  for (int k = b + 1; k < B; ++k)
-    if (idx[k] == idx[b]) return;
-  scaled[idx[b]] = pow(fabs((double)td[b]) + 1e-6, alpha);
+  const int32_t* ix = staged ? s_idx : idx;
+  const int32_t mine = ix[b];
+  for (int k = b + 1; k < B; ++k)  // last write wins (agent.py:224-226)
+    if (ix[k] == mine) return;
+  scaled[mine] = pow(fabs((double)td[b]) + 1e-6, alpha);
 }
 
 }  // namespace

@@ -19,11 +19,13 @@ is for throughput.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from . import _native
 from .distributed import BestPlan, PeerExchange, allreduce_mean_, rank_world, reduce_best, select_first_wins
-from .agent import AdamOptimizer, AgentConfig, QNetwork, _Batch, sync_target
+from .agent import AdamOptimizer, AgentConfig, QNetwork, _Batch, fork_to, join_from, stream_or_current, sync_target
 from .ir import decision_dims
 from .linkage import extract_linkage_groups, sorted_decision_order
 from .sharding import PropagationEngine, pad16
@@ -412,6 +414,9 @@ class VecDqnTrainer:
         self.use_graph = use_graph
         self.graph = None
         self._graph_launches = 0
+        # side stream for the learner's parallel branches (target forward, weight gradients);
+        # AP_DQN_NO_FORK=1 keeps one serial chain
+        self.side = None if os.environ.get("AP_DQN_NO_FORK") else torch.cuda.Stream()
 
     # -- one vector step -------------------------------------------------------------
 
@@ -451,8 +456,14 @@ class VecDqnTrainer:
         for src, dst in ((r["states"], sn[:B]), (r["next_states"], sn[B:])):
             _native.check(lib.ap_gather_rows(P(src), src.stride(0), P(self.idx), B, src.shape[1], P(dst),
                                              dst.stride(0), _s()))
+        side = self.side
+        if side is not None:  # the target forward is a parallel branch beside the online forward
+            fork_to(side)
+        with stream_or_current(side):
+            target_next = self.target.forward_device(sn[B:])
         q2, acts2 = self.net.forward_device(sn, cache=True)
-        target_next = self.target.forward_device(sn[B:])
+        if side is not None:
+            join_from(side)
         q_all, online_next = q2[:B], q2[B:]
         acts = [a[:B] for a in acts2]
         _native.check(lib.ap_dqn_td_ring(P(q_all), P(online_next), P(target_next), q2.stride(0), P(self.idx),
@@ -460,7 +471,7 @@ class VecDqnTrainer:
                                          r["next_mask"].stride(0), P(self.weights), B, self.env.num_actions,
                                          float(cfg.gamma), float(cfg.huber_delta), P(b.dz), b.dz.stride(0),
                                          P(self.dz_t), self.dz_t.stride(0), P(b.td), P(b.loss_rows), _s()))
-        self.net.backward_device(acts, b.dz, self.dz_t)
+        self.net.backward_device(acts, b.dz, self.dz_t, side=side)
         opt = self.opt
         if self.peer is not None:  # data-parallel: gradient all-reduce over NVLink peer memory fused with Adam
             x = self.peer
