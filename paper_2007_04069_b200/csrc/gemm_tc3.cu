@@ -66,6 +66,18 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
+#ifdef AP_GEMM_TRACE  // dev-only: SM-clock stamps of CTA (0,0,0) (scratch/gemm_trace)
+__device__ long long g_trace[8];
+#define GTRACE(k)                                                                   \
+  do {                                                                              \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) g_trace[k] = clock64(); \
+  } while (0)
+#else
+#define GTRACE(k) \
+  do {            \
+  } while (0)
+#endif
+
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(128) gemm_v3_kernel(const __grid_constant__ CUtensorMap tmA,
                                                       const __grid_constant__ CUtensorMap tmB, G3 g) {
@@ -84,6 +96,7 @@ __global__ void __launch_bounds__(128) gemm_v3_kernel(const __grid_constant__ CU
   const int kb = blockIdx.z * g.kps;
   const int nk = max(0, min(g.kps, nk_total - kb));
 
+  if (threadIdx.x == 0) GTRACE(0);
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa3(&tmem_slot)),
                  "r"(COLS));
@@ -103,6 +116,7 @@ __global__ void __launch_bounds__(128) gemm_v3_kernel(const __grid_constant__ CU
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_slot;
+  if (threadIdx.x == 0) GTRACE(1);
 
   if (threadIdx.x == 0) {
     // TMA producer
@@ -123,6 +137,7 @@ __global__ void __launch_bounds__(128) gemm_v3_kernel(const __grid_constant__ CU
     for (int it = 0; it < nk; ++it) {
       const int s = it % STAGES;
       mbar_wait(sa3(&full[s]), (it / STAGES) & 1);
+      if (it == 0) GTRACE(2);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t a = base + s * STAGE, b = a + A_BYTES;
 #pragma unroll
@@ -143,6 +158,7 @@ __global__ void __launch_bounds__(128) gemm_v3_kernel(const __grid_constant__ CU
   }
   __syncwarp();
   if (nk > 0) mbar_wait(sa3(&done), 0);
+  if (threadIdx.x == 0) GTRACE(3);
   asm volatile("tcgen05.fence::after_thread_sync;");
 
   if (g.cluster) {
@@ -171,34 +187,51 @@ __global__ void __launch_bounds__(128) gemm_v3_kernel(const __grid_constant__ CU
     const int rows_per = (BM3 + S - 1) / S;
     const int r_lo = rank * rows_per, r_hi = min(BM3, r_lo + rows_per);
     const uint32_t local = sa3(part);
+    const int cc = threadIdx.x % BN;  // BN | 128: one column per thread, bias loaded once
+    const float bcc = (g.bias && n0 + cc < g.N) ? g.bias[n0 + cc] : 0.0f;
     for (int e = threadIdx.x; e < (r_hi - r_lo) * BN; e += blockDim.x) {
-      const int r = r_lo + e / BN, c = e % BN;
+      const int r = r_lo + e / BN, c = cc;
       const int grow = m0 + r, gcol = n0 + c;
       if (grow >= g.M || gcol >= g.N) continue;
       const uint32_t off = local + (uint32_t)(r * LDP + c) * 4u;
-      float acc = 0.0f;
-      for (int s = 0; s < S; ++s) {
-        uint32_t ra;
-        float x;
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(off), "r"(s));
-        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(x) : "r"(ra) : "memory");
-        acc += x;
+      // all splits' loads in flight first, then the sum in split order
+      float x[16];
+#pragma unroll
+      for (int s = 0; s < 16; ++s) {
+        x[s] = 0.0f;
+        if (s < S) {
+          uint32_t ra;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(off), "r"(s));
+          asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(x[s]) : "r"(ra));
+        }
       }
-      if (g.bias) acc += g.bias[gcol];
+      float acc = 0.0f;
+#pragma unroll
+      for (int s = 0; s < 16; ++s)
+        if (s < S) acc += x[s];
+      if (g.bias) acc += bcc;
       if (g.relu) acc = fmaxf(acc, 0.0f);
       g.C[(int64_t)grow * g.ldc + gcol] = acc;
     }
+    if (threadIdx.x == 0) GTRACE(4);
     // no CTA may leave while a peer still reads its shared memory
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(COLS));
+    if (threadIdx.x == 0) GTRACE(5);
     return;
   }
 
-  const int row = m0 + warp * 32 + lane;
+  // Epilogue through shared memory: TMEM rows (one per lane) go into the
+  // drained stage ring ([BM][BN+1], conflict-free), then consecutive threads
+  // store consecutive columns of a row -- one transaction per warp store
+  // instead of 32 (a lane-per-row store was ~4 us of a small GEMM).
   float* out = g.work ? g.work + (int64_t)blockIdx.z * g.M * g.N : g.C;
   const int64_t ld = g.work ? g.N : g.ldc;
+  constexpr int LDT = BN + 1;
+  float* tile = reinterpret_cast<float*>(smem_raw + (base - sa3(smem_raw)));
+  const int lrow = warp * 32 + lane;
 #pragma unroll 1
   for (int c0 = 0; c0 < BN; c0 += 16) {
     uint32_t v[16];
@@ -209,24 +242,33 @@ __global__ void __launch_bounds__(128) gemm_v3_kernel(const __grid_constant__ CU
           "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    if (row < g.M) {
 #pragma unroll
-      for (int t = 0; t < 16; ++t) {
-        const int col = n0 + c0 + t;
-        if (col < g.N) {
-          float x = nk > 0 ? __uint_as_float(v[t]) : 0.0f;
-          if (!g.work) {
-            if (g.bias) x += g.bias[col];
-            if (g.relu) x = fmaxf(x, 0.0f);
-          }
-          out[(int64_t)row * ld + col] = x;
-        }
-      }
+    for (int t = 0; t < 16; ++t) tile[lrow * LDT + c0 + t] = nk > 0 ? __uint_as_float(v[t]) : 0.0f;
+  }
+  __syncthreads();
+  // 128 threads, BN | 128: each thread owns one column (bias loaded once) and
+  // walks rows; nothing in the loop waits on a global load
+  const int rows = min(BM3, g.M - m0), cols = min(BN, g.N - n0);
+  const int c = threadIdx.x % BN;
+  if (c < cols) {
+    const bool epi = !g.work;
+    const bool has_bias = epi && g.bias;
+    const float bc = has_bias ? g.bias[n0 + c] : 0.0f;
+    const bool relu = epi && g.relu;
+    float* __restrict__ o = out + (int64_t)m0 * ld + n0 + c;
+#pragma unroll 4
+    for (int r = threadIdx.x / BN; r < rows; r += 128 / BN) {
+      float x = tile[r * LDT + c];
+      if (has_bias) x += bc;
+      if (relu) x = fmaxf(x, 0.0f);
+      o[(int64_t)r * ld] = x;
     }
   }
+  if (threadIdx.x == 0) GTRACE(4);
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(COLS));
+  if (threadIdx.x == 0) GTRACE(5);
 }
 
 __global__ void splitk_reduce3_kernel(const float* work, int splits, int M, int N, float* C, int64_t ldc,
@@ -326,13 +368,15 @@ int launch_gemm_v3(const float* A, int64_t lda, int transA, const float* B, int6
   const bool no_cluster = std::getenv("AP_GEMM_NO_CLUSTER") != nullptr;
   const int max_split = std::getenv("AP_GEMM_MAX_SPLIT") ? std::atoi(std::getenv("AP_GEMM_MAX_SPLIT")) : 16;
   int splits = 1;
-  if (mt * nt < 120 && nk >= 4) splits = std::min(std::min(nk / 2, max_split), std::max(1, 148 / (mt * nt)));
+  // (measured on B200 with the staged epilogue: a split costs a cluster barrier pair and a DSMEM
+  // reduce, ~2-3 us, which only pays once each split saves several k slices -- K >= 512)
+  if (mt * nt < 120 && nk >= 16) splits = std::min(std::min(nk / 2, max_split), std::max(1, 148 / (mt * nt)));
   // dev knobs for sweeps: AP_GEMM_V3_SPLITS (forced split count), AP_GEMM_V3_STAGES (4 | 6)
   if (const char* e = std::getenv("AP_GEMM_V3_SPLITS")) splits = std::max(1, std::min(std::atoi(e), nk));
   const bool four_stages = std::getenv("AP_GEMM_V3_STAGES") && std::atoi(std::getenv("AP_GEMM_V3_STAGES")) == 4;
   g.kps = (nk + splits - 1) / splits;
   splits = (nk + g.kps - 1) / g.kps;
-  if (splits > 1 && !no_cluster) g.cluster = 1;
+  if (splits > 1 && splits <= 16 && !no_cluster) g.cluster = 1;
   if (splits > 1 && !g.cluster) {
     const int wrc = splitk_workspace(stream, (size_t)splits * M * N * sizeof(float), &g.work);
     if (wrc != AP_OK) return wrc;
@@ -349,3 +393,9 @@ int launch_gemm_v3(const float* A, int64_t lda, int transA, const float* B, int6
 }
 
 }  // namespace apb
+
+#ifdef AP_GEMM_TRACE
+extern "C" int ap_gemm_trace_read(long long* out) {
+  return cudaMemcpyFromSymbol(out, apb::g_trace, sizeof(long long) * 8) == cudaSuccess ? 0 : -1;
+}
+#endif
