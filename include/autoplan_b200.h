@@ -330,9 +330,13 @@ int ap_vec_apply(int8_t* seeds, int64_t ld, const int32_t* position, const int32
 /* After ap_propagate_batch over the E seed rows: rewards (0.4 newP + 0.1 newR
  * or -1 on conflict), done flags, next decision positions (first undecided dim
  * in `order`), next states [E, n+1], next masks, episode bookkeeping and
- * auto-reset of finished envs (envs.py:103-177, 207-221). */
+ * auto-reset of finished envs (envs.py:103-177, 207-221).  order_index [n]
+ * (nullable) is the inverse of `order`: the search for the first undecided
+ * dim starts at the current position's rank (decided dims stay decided within
+ * an episode, so nothing before it can be undecided). */
 int ap_vec_post(int32_t E, int32_t n, int64_t ld, int8_t* seeds, const int8_t* status, const uint8_t* outcome,
-                const int32_t* counts, int32_t* prev_counts, int32_t* position, const int32_t* order, float* cur_state,
+                const int32_t* counts, int32_t* prev_counts, int32_t* position, const int32_t* order,
+                const int32_t* order_index, float* cur_state,
                 int64_t lds, float* next_state, float* rewards, uint8_t* done, uint8_t* next_mask, int32_t A,
                 float* ep_return, float* finished_return, int32_t* finished_partitions, int32_t* episodes_done,
                 void* stream);

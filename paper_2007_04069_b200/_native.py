@@ -137,7 +137,7 @@ SIGNATURES: dict[str, tuple] = {
     "ap_per_update": (ctypes.c_int, [_VP, _VP, _VP, _I32, _VP]),
     "ap_gather_rows": (ctypes.c_int, [_VP, _I64, _VP, _I32, _I32, _VP, _I64, _VP]),
     "ap_vec_apply": (ctypes.c_int, [_VP, _I64, _VP, _VP, _I32, _VP]),
-    "ap_vec_post": (ctypes.c_int, [_I32, _I32, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _VP, _VP, _VP, _VP,
+    "ap_vec_post": (ctypes.c_int, [_I32, _I32, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _VP, _VP, _VP, _VP,
                                    _I32, _VP, _VP, _VP, _VP, _VP]),
     "ap_vec_track_best": (ctypes.c_int, [_I32, _I32, _I64, _VP, _VP, _VP, _VP, _VP, _I64, _VP, _I32, _I32, _VP, _VP,
                                          _VP, _VP, _VP]),

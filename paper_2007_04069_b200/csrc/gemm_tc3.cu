@@ -184,8 +184,9 @@ __global__ void __launch_bounds__(128) gemm_v3_kernel(const __grid_constant__ CU
     }
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     const int S = (int)gridDim.z, rank = (int)blockIdx.z;
-    const int rows_per = (BM3 + S - 1) / S;
-    const int r_lo = rank * rows_per, r_hi = min(BM3, r_lo + rows_per);
+    const int vrows = min(BM3, g.M - m0);  // only the tile's valid rows are reduced
+    const int rows_per = (vrows + S - 1) / S;
+    const int r_lo = rank * rows_per, r_hi = min(vrows, r_lo + rows_per);
     const uint32_t local = sa3(part);
     const int cc = threadIdx.x % BN;  // BN | 128: one column per thread, bias loaded once
     const float bcc = (g.bias && n0 + cc < g.N) ? g.bias[n0 + cc] : 0.0f;

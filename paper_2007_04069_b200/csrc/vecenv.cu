@@ -39,7 +39,8 @@ __global__ void vec_apply_kernel(int8_t* seeds, int64_t ld, const int32_t* posit
 // one warp per env
 __global__ void vec_post_kernel(int E, int n, int64_t ld, int8_t* seeds, const int8_t* status,
                                 const uint8_t* outcome, const int32_t* counts, int32_t* prev_counts, int32_t* position,
-                                const int32_t* order, float* cur_state, int64_t lds, float* next_state,
+                                const int32_t* order, const int32_t* order_index, float* cur_state, int64_t lds,
+                                float* next_state,
                                 float* rewards, uint8_t* done, uint8_t* next_mask, int A, float* ep_return,
                                 float* finished_return, int32_t* finished_partitions, int32_t* episodes_done) {
   const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -61,7 +62,8 @@ __global__ void vec_post_kernel(int E, int n, int64_t ld, int8_t* seeds, const i
     fin = oc == AP_OUTCOME_COMPLETE;
     // next position: first undecided dim in linkage order (envs.py:207-211)
     int pos = -1;
-    for (int base = 0; base < n && pos < 0; base += 32) {
+    const int from = order_index ? order_index[position[e]] : 0;  // decided prefix of the order
+    for (int base = from & ~31; base < n && pos < 0; base += 32) {
       const int j = base + lane;
       const bool und = j < n && st[order[j]] == -1;
       const unsigned bal = __ballot_sync(kFull, und);
@@ -523,13 +525,15 @@ int ap_vec_apply(int8_t* seeds, int64_t ld, const int32_t* position, const int32
 }
 
 int ap_vec_post(int32_t E, int32_t n, int64_t ld, int8_t* seeds, const int8_t* status, const uint8_t* outcome,
-                const int32_t* counts, int32_t* prev_counts, int32_t* position, const int32_t* order, float* cur_state,
+                const int32_t* counts, int32_t* prev_counts, int32_t* position, const int32_t* order,
+                const int32_t* order_index, float* cur_state,
                 int64_t lds, float* next_state, float* rewards, uint8_t* done, uint8_t* next_mask, int32_t A,
                 float* ep_return, float* finished_return, int32_t* finished_partitions, int32_t* episodes_done,
                 void* stream) {
   if (E <= 0) return AP_OK;
   vec_post_kernel<<<(E + 7) / 8, 256, 0, (cudaStream_t)stream>>>(
-      E, n, ld, seeds, status, outcome, counts, prev_counts, position, order, cur_state, lds, next_state, rewards, done,
+      E, n, ld, seeds, status, outcome, counts, prev_counts, position, order, order_index, cur_state, lds, next_state,
+      rewards, done,
       next_mask, A, ep_return, finished_return, finished_partitions, episodes_done);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;

@@ -58,6 +58,8 @@ class VecPartitionEnv:
         self.engine.prepare()
         idx = {d: k for k, d in enumerate(dims)}
         self.order = torch.tensor([idx[d] for d in order], dtype=torch.int32, device="cuda")
+        self.order_index = torch.empty_like(self.order)  # inverse permutation: dim -> rank in the order
+        self.order_index[self.order.long()] = torch.arange(len(order), dtype=torch.int32, device="cuda")
         ld = pad16(n)
         dev = "cuda"
         self.seeds_full = torch.full((E, ld), -1, dtype=torch.int8, device=dev)
@@ -100,7 +102,8 @@ class VecPartitionEnv:
         self.engine.launch(self.seeds, self.outcome, self.counts, None, self.status)
         _native.check(lib.ap_vec_post(self.E, self.n, self.seeds_full.stride(0), P(self.seeds_full), P(self.status),
                                       P(self.outcome), P(self.counts), P(self.prev_counts), P(self.position),
-                                      P(self.order), P(self.cur_state), self.cur_state.stride(0), P(self.next_state),
+                                      P(self.order), P(self.order_index), P(self.cur_state), self.cur_state.stride(0),
+                                      P(self.next_state),
                                       P(self.rewards), P(self.done), P(self.next_mask), 2, P(self.ep_return),
                                       P(self.finished_return), P(self.finished_partitions), P(self.episodes_done),
                                       _s()))
