@@ -49,6 +49,36 @@ __global__ void dueling_kernel(const float* __restrict__ z, int64_t ldz, float* 
   for (int k = lane; k < A; k += 32) out[k] = v + row[k] - mean;
 }
 
+// Wide action spaces (A > 256): one 256-thread CTA per row (a warp per row
+// leaves too few loads in flight when A is in the thousands and B is small).
+__global__ void __launch_bounds__(256) dueling_wide_kernel(const float* __restrict__ z, int64_t ldz,
+                                                           float* __restrict__ q, int64_t ldq, int B, int A) {
+  __shared__ float s_part[8];
+  const int b = blockIdx.x;
+  const float* __restrict__ row = z + (int64_t)b * ldz + 1;
+  float* __restrict__ out = q + (int64_t)b * ldq;
+  float s = 0.0f;
+  int j = threadIdx.x;
+  for (; j + 768 < A; j += 1024) {
+    const float x0 = row[j], x1 = row[j + 256], x2 = row[j + 512], x3 = row[j + 768];
+    s += x0;
+    s += x1;
+    s += x2;
+    s += x3;
+  }
+  for (; j < A; j += 256) s += row[j];
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = s;
+  __syncthreads();
+  float tot = 0.0f;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) tot += s_part[w];
+  const float mean = tot / (float)A;
+  const float v = z[(int64_t)b * ldz];
+#pragma unroll 4
+  for (int k = threadIdx.x; k < A; k += 256) out[k] = v + row[k] - mean;
+}
+
 // masked argmax (ties -> lowest index); eps-greedy with a counter-based hash
 // when eps > 0 (throughput mode; parity mode draws on the host)
 __device__ inline uint32_t hash32(uint64_t x) {
@@ -249,18 +279,32 @@ __global__ void td_wide_kernel(const float* q, const float* online_next, const f
   const int b = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int64_t row = idx ? (int64_t)idx[b] : (int64_t)b;
-  const uint8_t* m = next_mask + row * ldm;
+  const uint8_t* __restrict__ m = next_mask + row * ldm;
+  const float* __restrict__ on = online_next + (int64_t)b * ldq;
   float best = -INFINITY;
   int best_j = 0x7fffffff, any = 0;
-  for (int j = threadIdx.x; j < A; j += blockDim.x) {
-    if (!m[j]) continue;
+  auto visit = [&](int j, uint8_t ok, float v) {
+    if (!ok) return;
     any = 1;
-    const float v = online_next[(int64_t)b * ldq + j];
     if (v > best || (v == best && j < best_j)) {
       best = v;
       best_j = j;
     }
+  };
+  const int st = blockDim.x;
+  int j = threadIdx.x;
+  for (; j + 3 * st < A; j += 4 * st) {  // 4 loads in flight per thread
+    uint8_t ok[4];
+    float v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      ok[u] = m[j + u * st];
+      v[u] = on[j + u * st];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) visit(j + u * st, ok[u], v[u]);
   }
+  for (; j < A; j += st) visit(j, m[j], on[j]);
   for (int o = 16; o; o >>= 1) {
     const float ov = __shfl_xor_sync(kFull, best, o);
     const int oj = __shfl_xor_sync(kFull, best_j, o);
@@ -440,14 +484,26 @@ struct AdamSegments {
 };
 
 // one Adam element update (shared by the flat and tiled kernels: same code, same rounding)
+// Throughput-mode Adam element (the graph-captured learner; the parity agent's
+// ap_dqn_adam keeps the reference expression).  Explicitly rounded operations
+// (never contracted, so every kernel computes the same bits), reciprocal bias
+// corrections ic1 = 1/c1, ic2 = 1/c2, one fast divide: the IEEE divide / sqrt
+// subroutines made the update instruction-bound (28.7 M instructions for 4.1 M
+// parameters, 2.8 TB/s).
+__device__ __forceinline__ void adam_math(float gi, float& mi, float& vi, float& pi, float lr, float b1, float b2,
+                                          float eps, float ic1, float ic2) {
+  mi = __fadd_rn(__fmul_rn(b1, mi), __fmul_rn(1.0f - b1, gi));
+  vi = __fadd_rn(__fmul_rn(b2, vi), __fmul_rn(__fmul_rn(1.0f - b2, gi), gi));
+  const float den = __fadd_rn(__fsqrt_rn(__fmul_rn(vi, ic2)), eps);
+  pi = __fsub_rn(pi, __fdividef(__fmul_rn(lr, __fmul_rn(mi, ic1)), den));
+}
+
 __device__ __forceinline__ float adam_elem(float* p, const float* g, float* m, float* v, int64_t i, float lr, float b1,
                                            float b2, float eps, float c1, float c2) {
-  const float gi = g[i];
-  const float mi = b1 * m[i] + (1.0f - b1) * gi;
-  const float vi = b2 * v[i] + (1.0f - b2) * gi * gi;
+  float mi = m[i], vi = v[i], pi = p[i];
+  adam_math(g[i], mi, vi, pi, lr, b1, b2, eps, c1, c2);
   m[i] = mi;
   v[i] = vi;
-  const float pi = p[i] - lr * (mi / c1) / (sqrtf(vi / c2) + eps);
   p[i] = pi;
   return pi;
 }
@@ -470,13 +526,13 @@ __global__ void __launch_bounds__(256) adam_tile_kernel(float* p, const float* g
                                                         AdamTiles at) {
   __shared__ float s_c[2];
   __shared__ float tile[32][33];
-  if (threadIdx.x == 0) {
-    const double t = (double)(ctl[AP_CTL_TRAIN] + 1);
-    s_c[0] = (float)(1.0 - pow((double)b1, t));
-    s_c[1] = (float)(1.0 - pow((double)b2, t));
-  }
-  __syncthreads();
-  const float c1 = s_c[0], c2 = s_c[1];
+  auto corrections = [&]() {  // bias corrections (thread 0), published by the caller's barrier
+    if (threadIdx.x == 0) {
+      const double t = (double)(ctl[AP_CTL_TRAIN] + 1);
+      s_c[0] = (float)(1.0 / (1.0 - pow((double)b1, t)));
+      s_c[1] = (float)(1.0 / (1.0 - pow((double)b2, t)));
+    }
+  };
   const int64_t ntiles = at.tile_base[at.segs.n];
   const int64_t blk = blockIdx.x;
   if (blk < ntiles) {
@@ -487,10 +543,34 @@ __global__ void __launch_bounds__(256) adam_tile_kernel(float* p, const float* g
     const int rows = at.segs.rows[s], cols = at.segs.cols[s];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int64_t off = at.segs.off[s];
+    // the tile's loads go out before the (pow-latency) bias corrections are awaited
+    float gv[4], mv[4], vv[4], pv[4];
+    int64_t ix[4];
+    bool ok[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int r = tr * 32 + ty + 8 * k, c = tc * 32 + tx;
-      if (r < rows && c < cols) tile[ty + 8 * k][tx] = adam_elem(p, g, m, v, off + (int64_t)r * cols + c, lr, b1, b2, eps, c1, c2);
+      ok[k] = r < rows && c < cols;
+      ix[k] = off + (int64_t)r * cols + c;
+      if (ok[k]) {
+        gv[k] = g[ix[k]];
+        mv[k] = m[ix[k]];
+        vv[k] = v[ix[k]];
+        pv[k] = p[ix[k]];
+      }
+    }
+    corrections();
+    __syncthreads();
+    const float c1 = s_c[0], c2 = s_c[1];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (ok[k]) {
+        adam_math(gv[k], mv[k], vv[k], pv[k], lr, b1, b2, eps, c1, c2);
+        m[ix[k]] = mv[k];
+        v[ix[k]] = vv[k];
+        p[ix[k]] = pv[k];
+        tile[ty + 8 * k][tx] = pv[k];
+      }
     }
     __syncthreads();
     float* dst = at.segs.dst[s];
@@ -502,6 +582,9 @@ __global__ void __launch_bounds__(256) adam_tile_kernel(float* p, const float* g
     }
     return;
   }
+  corrections();
+  __syncthreads();
+  const float c1 = s_c[0], c2 = s_c[1];
   const int64_t idx = (blk - ntiles) * blockDim.x + threadIdx.x;
   if (idx >= at.gap_base[at.ngap]) return;
   int q = 0;
@@ -514,8 +597,8 @@ __global__ void adam_t_kernel(float* p, const float* g, float* m, float* v, int6
   __shared__ float s_c[2];
   if (threadIdx.x == 0) {
     const double t = (double)(ctl[AP_CTL_TRAIN] + 1);
-    s_c[0] = (float)(1.0 - pow((double)b1, t));
-    s_c[1] = (float)(1.0 - pow((double)b2, t));
+    s_c[0] = (float)(1.0 / (1.0 - pow((double)b1, t)));  // reciprocals (adam_math)
+    s_c[1] = (float)(1.0 / (1.0 - pow((double)b2, t)));
   }
   __syncthreads();
   const float c1 = s_c[0], c2 = s_c[1];
@@ -672,7 +755,10 @@ int ap_dqn_dueling(const float* z, int64_t ldz, float* q, int64_t ldq, int32_t B
     return AP_ERR_INVALID;
   }
   if (B == 0) return AP_OK;
-  dueling_kernel<<<(B + 7) / 8, 256, 0, (cudaStream_t)stream>>>(z, ldz, q, ldq, B, A);
+  if (A > 256)
+    dueling_wide_kernel<<<B, 256, 0, (cudaStream_t)stream>>>(z, ldz, q, ldq, B, A);
+  else
+    dueling_kernel<<<(B + 7) / 8, 256, 0, (cudaStream_t)stream>>>(z, ldz, q, ldq, B, A);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
