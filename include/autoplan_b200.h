@@ -304,6 +304,14 @@ int ap_probe_fp64_add(int32_t blocks, int64_t iters, double* scratch_dev, void* 
 int ap_dqn_head_backward(const float* dz, int64_t ldz, const float* wh, int64_t ldw, const float* h, int64_t ldh,
                          int32_t B, int32_t H, int32_t A1, float* dh, int64_t lddh, float* dh_t, int64_t ldt,
                          void* stream);
+/* ap_dqn_head_backward for the dueling TD gradient the TD kernels write (dz[b] =
+ * g_b (e_0 + e_{1+a_b}) - (g_b/A)[0, 1, .., 1]): dh[b, j] = relu'(h) (g_b wh[j,0] +
+ * g_b wh[j,1+a_b] - (g_b/A) sum_k wh[j,1+k]) in O(B H) after one row-sum pass over
+ * wh (rowsum_scratch [H]) instead of the O(B H A) product.  Same value up to fp32
+ * rounding; the throughput learner uses it for wide heads. */
+int ap_dqn_head_backward_dueling(const float* dz, int64_t ldz, const float* wh, int64_t ldw, const float* h,
+                                 int64_t ldh, int32_t B, int32_t H, int32_t A1, float* rowsum_scratch, float* dh,
+                                 int64_t lddh, float* dh_t, int64_t ldt, void* stream);
 /* Adam over a flat parameter buffer (agent.py:240-250); correct1/2 = 1 - beta^t. */
 int ap_dqn_adam(float* params, const float* grads, float* m, float* v, int64_t n, float lr, float beta1, float beta2,
                 float eps, float correct1, float correct2, void* stream);

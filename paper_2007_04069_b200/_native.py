@@ -129,6 +129,8 @@ SIGNATURES: dict[str, tuple] = {
     "ap_dqn_relu_backward": (ctypes.c_int, [_VP, _VP, _I64, _VP]),
     "ap_dqn_colsum": (ctypes.c_int, [_VP, _I64, _I32, _I32, _VP, _VP]),
     "ap_probe_fp64_add": (ctypes.c_int, [_I32, _I64, _VP, _VP]),
+    "ap_dqn_head_backward_dueling": (ctypes.c_int, [_VP, _I64, _VP, _I64, _VP, _I64, _I32, _I32, _I32, _VP, _VP, _I64, _VP,
+                                                     _I64, _VP]),
     "ap_dqn_head_backward": (ctypes.c_int, [_VP, _I64, _VP, _I64, _VP, _I64, _I32, _I32, _I32, _VP, _I64, _VP, _I64,
                                             _VP]),
     "ap_dqn_adam": (ctypes.c_int, [_VP, _VP, _VP, _VP, _I64, ctypes.c_float, ctypes.c_float, ctypes.c_float,

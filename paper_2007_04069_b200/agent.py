@@ -263,7 +263,7 @@ class QNetwork:
             raise ValueError(f"expected state dim {self.state_dim}, got {x.shape[1]}")
         return self.forward_device(x).double().cpu().numpy()
 
-    def backward_device(self, acts, dz, dz_t=None, side=None) -> None:
+    def backward_device(self, acts, dz, dz_t=None, side=None, dueling_td: bool = False) -> None:
         """Gradients into self.grad from dLoss/dz (z = [V, A] head outputs).
 
         `dz_t` (optional) is dz^T already materialised (ap_dqn_td_ring writes it).
@@ -274,6 +274,10 @@ class QNetwork:
         launch), and since b_i follows w_i in the flat buffer the GEMM writes the
         [in + 1, out] block [dW_i; db_i] at once: the bias gradient is the ones-row
         product, the column sum of dh (agent.py:118, 134).
+
+        `dueling_td`: dz is the TD kernels' dueling gradient (one advantage entry
+        differs from -g/A per row), so a wide head back-propagates in closed form
+        (ap_dqn_head_backward_dueling).
 
         `side` (a CUDA stream): the weight-gradient GEMMs run there, a parallel
         branch beside the data-gradient chain (one graph branch under capture);
@@ -308,8 +312,17 @@ class QNetwork:
         H = wh.shape[0]
         dh = torch.empty((b, H), dtype=torch.float32, device="cuda")
         dh_t = torch.empty((H, b), dtype=torch.float32, device="cuda")
-        _native.check(lib.ap_dqn_head_backward(P(dz), dz.stride(0), P(wh), wh.stride(0), P(h), h.stride(0), b, H,
-                                               dz.shape[1], P(dh), dh.stride(0), P(dh_t), dh_t.stride(0), _stream()))
+        if dueling_td and dz.shape[1] > 32:
+            rs = self.__dict__.get("_rowsum")
+            if rs is None or rs.numel() < H:
+                rs = self._rowsum = torch.empty(H, dtype=torch.float32, device="cuda")
+            _native.check(lib.ap_dqn_head_backward_dueling(P(dz), dz.stride(0), P(wh), wh.stride(0), P(h), h.stride(0),
+                                                           b, H, dz.shape[1], P(rs), P(dh), dh.stride(0), P(dh_t),
+                                                           dh_t.stride(0), _stream()))
+        else:
+            _native.check(lib.ap_dqn_head_backward(P(dz), dz.stride(0), P(wh), wh.stride(0), P(h), h.stride(0), b, H,
+                                                   dz.shape[1], P(dh), dh.stride(0), P(dh_t), dh_t.stride(0),
+                                                   _stream()))
         for i in range(L - 1, -1, -1):
             if side is not None:
                 fork_to(side)  # the branch waits for this layer's dh_t

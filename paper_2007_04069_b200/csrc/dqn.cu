@@ -420,6 +420,74 @@ __global__ void head_backward_kernel(const float* dz, int64_t ldz, const float* 
 // Wide-head variant: a warp per (row, unit) with the lanes striding the 1 + A
 // head outputs (coalesced reads of the dz row and of the unit's wh row), then a
 // shuffle reduction.
+// Dueling-structured head backward (throughput learner): the TD kernels write
+// dz[b] = g_b * (e_0 + e_{1+a_b}) - (g_b / A) * [0, 1, .., 1], so
+//   dh[b, j] = g_b * wh[j, 0] + g_b * wh[j, 1 + a_b] - (g_b / A) * rowsum_j,
+// rowsum_j = sum_k wh[j, 1 + k] (head_rowsum_kernel, once per backward).
+// a_b is the one advantage entry that differs from 0 - g_b/A (the TD kernels'
+// own expression, so the comparison is exact); g_b == 0 gives dh = 0.
+__global__ void __launch_bounds__(256) head_rowsum_kernel(const float* __restrict__ wh, int64_t ldw, int A1,
+                                                          float* __restrict__ rowsum) {
+  __shared__ float s_part[8];
+  const float* __restrict__ w = wh + (int64_t)blockIdx.x * ldw;
+  float s = 0.0f;
+  for (int k = 1 + threadIdx.x; k < A1; k += 256) s += w[k];
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.0f;
+    for (int k = 0; k < 8; ++k) t += s_part[k];
+    rowsum[blockIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(256) head_backward_dueling_kernel(const float* __restrict__ dz, int64_t ldz,
+                                                                    const float* __restrict__ wh, int64_t ldw,
+                                                                    const float* __restrict__ h, int64_t ldh,
+                                                                    const float* __restrict__ rowsum, int H, int A1,
+                                                                    float* __restrict__ dh, int64_t lddh,
+                                                                    float* __restrict__ dh_t, int64_t ldt) {
+  __shared__ int s_a, s_cnt, s_nz;
+  const int b = blockIdx.x;
+  const int A = A1 - 1;
+  const float* __restrict__ z = dz + (int64_t)b * ldz;
+  const float g = z[0];
+  const float other = 0.0f - g / (float)A;
+  if (threadIdx.x == 0) {
+    s_a = 0;
+    s_cnt = 0;
+    s_nz = 0;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < A; k += blockDim.x) {
+    const float x = z[1 + k];
+    if (x != other) {
+      s_a = k;
+      atomicAdd(&s_cnt, 1);
+    }
+    if (x != 0.0f) s_nz = 1;
+  }
+  __syncthreads();
+  const int a = s_a;
+  // rows not of the TD shape (never produced by the TD kernels) take the full product
+  const bool closed = g != 0.0f ? s_cnt == 1 : s_nz == 0;
+  const float ga = g / (float)A;
+  for (int j = threadIdx.x; j < H; j += blockDim.x) {
+    const float* __restrict__ w = wh + (int64_t)j * ldw;
+    float acc;
+    if (closed) {
+      acc = g == 0.0f ? 0.0f : g * w[0] + g * w[1 + a] - ga * rowsum[j];
+    } else {
+      acc = 0.0f;
+      for (int k = 0; k < A1; ++k) acc = fmaf(z[k], w[k], acc);
+    }
+    if (!(h[(int64_t)b * ldh + j] > 0.0f)) acc = 0.0f;
+    dh[(int64_t)b * lddh + j] = acc;
+    if (dh_t) dh_t[(int64_t)j * ldt + b] = acc;
+  }
+}
+
 __global__ void head_backward_wide_kernel(const float* dz, int64_t ldz, const float* wh, int64_t ldw, const float* h,
                                           int64_t ldh, int B, int H, int A1, float* dh, int64_t lddh, float* dh_t,
                                           int64_t ldt) {
@@ -896,6 +964,22 @@ int ap_dqn_td_ring(const float* q, const float* online_next, const float* target
 int ap_dqn_relu_backward(float* dh, const float* h, int64_t n, void* stream) {
   if (n <= 0) return AP_OK;
   relu_bwd_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(dh, h, n);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_dqn_head_backward_dueling(const float* dz, int64_t ldz, const float* wh, int64_t ldw, const float* h,
+                                 int64_t ldh, int32_t B, int32_t H, int32_t A1, float* rowsum_scratch, float* dh,
+                                 int64_t lddh, float* dh_t, int64_t ldt, void* stream) {
+  if (!dz || !wh || !h || !dh || !rowsum_scratch || B < 0 || H < 1 || A1 < 2) {
+    set_error("ap_dqn_head_backward_dueling: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  if (B == 0) return AP_OK;
+  head_rowsum_kernel<<<H, 256, 0, (cudaStream_t)stream>>>(wh, ldw, A1, rowsum_scratch);
+  AP_CUDA_CHECK(cudaGetLastError());
+  head_backward_dueling_kernel<<<B, 256, 0, (cudaStream_t)stream>>>(dz, ldz, wh, ldw, h, ldh, rowsum_scratch, H, A1,
+                                                                    dh, lddh, dh_t, ldt);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }

@@ -474,7 +474,7 @@ class VecDqnTrainer:
                                          r["next_mask"].stride(0), P(self.weights), B, self.env.num_actions,
                                          float(cfg.gamma), float(cfg.huber_delta), P(b.dz), b.dz.stride(0),
                                          P(self.dz_t), self.dz_t.stride(0), P(b.td), P(b.loss_rows), _s()))
-        self.net.backward_device(acts, b.dz, self.dz_t, side=side)
+        self.net.backward_device(acts, b.dz, self.dz_t, side=side, dueling_td=True)
         opt = self.opt
         if self.peer is not None:  # data-parallel: gradient all-reduce over NVLink peer memory fused with Adam
             x = self.peer

@@ -174,3 +174,43 @@ def test_adam_tiled_transposed_matches_flat(cuda, monkeypatch, shape):
     flat = run()
     for x, y in zip(tiled, flat):
         assert torch.equal(x.nan_to_num(7.0), y.nan_to_num(7.0))
+
+
+@pytest.mark.parametrize("A", [158, 3170])
+def test_head_backward_dueling_closed_form(cuda, A):
+    """ap_dqn_head_backward_dueling (O(B H) closed form for the TD kernels' dueling gradient)
+    matches the O(B H A) product of ap_dqn_head_backward within fp32 rounding (1e-5 of max |dh|)."""
+    from paper_2007_04069_b200 import _native
+
+    B, H, A1 = 64, 256, A + 1
+    gen = torch.Generator(device="cuda").manual_seed(A)
+    g = torch.randn(B, generator=gen, device="cuda")
+    g[::9] = 0.0
+    a = torch.randint(0, A, (B,), generator=gen, device="cuda")
+    q = g / torch.full_like(g, float(A))  # elementwise IEEE quotient, as the TD kernels compute it
+    dz = torch.empty(B, A1, device="cuda")
+    dz[:, 0] = g
+    dz[:, 1:] = (0.0 - q)[:, None]
+    dz[torch.arange(B), 1 + a] = g - q
+    dz[5, 7] += 1.0  # one row not of the TD shape: the full-product fallback
+    wh = torch.randn(H, A1, generator=gen, device="cuda")
+    h = torch.randn(B, H, generator=gen, device="cuda")
+    lib, P = _native.require_device(), _native.ptr
+    outs = []
+    for closed in (False, True):
+        dh = torch.full((B, H), float("nan"), device="cuda")
+        dh_t = torch.full((H, B), float("nan"), device="cuda")
+        if closed:
+            rs = torch.empty(H, device="cuda")
+            _native.check(lib.ap_dqn_head_backward_dueling(P(dz), A1, P(wh), A1, P(h), H, B, H, A1, P(rs), P(dh), H,
+                                                           P(dh_t), B, _native.stream_handle()))
+        else:
+            _native.check(lib.ap_dqn_head_backward(P(dz), A1, P(wh), A1, P(h), H, B, H, A1, P(dh), H, P(dh_t), B,
+                                                   _native.stream_handle()))
+        assert torch.equal(dh.t(), dh_t)
+        outs.append(dh)
+    ref = (dz.double() @ wh.double().t()) * (h > 0)
+    scale = ref.abs().max().item()
+    for o in outs:
+        assert (o.double() - ref).abs().max().item() <= 1e-5 * scale
+    assert torch.all(outs[1][::9] == 0)
