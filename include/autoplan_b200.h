@@ -208,6 +208,15 @@ int ap_pipe_train_state(ap_pipe_t p, const ap_topology* topo, const int32_t* can
                         const int32_t* applied_dev, int32_t max_applied, const uint8_t* mask_dev, int64_t num_envs,
                         double backward_multiplier, double* state_dev, void* stream);
 
+/* ap_pipe_train_state that also writes the state as fp32 rows (the learner's
+ * input) into state_f32 [E, >= 4C] (row stride ld_f32) and, when non-null, a
+ * second copy state_f32_b: from the fused table kernel directly when the list
+ * is bound, else by one conversion pass.  state_dev (fp64) is written as well. */
+int ap_pipe_train_state_ex(ap_pipe_t p, const ap_topology* topo, const int32_t* cand_pos_dev, int32_t num_cand,
+                           const int32_t* applied_dev, int32_t max_applied, const uint8_t* mask_dev, int64_t num_envs,
+                           double backward_multiplier, double* state_dev, float* state_f32, int64_t ld_f32,
+                           float* state_f32_b, int64_t ld_f32_b, void* stream);
+
 /* Binds a candidate list to the handle: builds (once, outside stream capture)
  * the table of every stage sum a plan over these candidates can have --
  * the naive sum of cost[start .. end] for each pair of candidate boundaries,

@@ -758,7 +758,8 @@ __device__ __forceinline__ void tab_candidates(const PipeDev& pd, const Topo& t,
 __global__ void __launch_bounds__(256, AP_PP_TAB_MINB) train_state_tab_kernel(PipeDev pd, Topo t, const int32_t* cand_pos, int C,
                                                               const double* T, const int32_t* applied, int A,
                                                               const uint8_t* mask, int64_t E, double scale,
-                                                              double* state) {
+                                                              double* state, float* f32a, int64_t lda32,
+                                                              float* f32b, int64_t ldb32) {
   __shared__ FixedStages fs;
   __shared__ double s_max[2][32];
   const int64_t W = C + 1;
@@ -821,6 +822,21 @@ __global__ void __launch_bounds__(256, AP_PP_TAB_MINB) train_state_tab_kernel(Pi
       double one = 0.0;
       for (int k = 0; k < P0; ++k) one = fs.aidx[k] == c ? 1.0 : one;
       st[3 * C + c] = one;
+      if (f32a) {  // the learner's fp32 rows (cur / next state) straight from the same values
+        const float x0 = (float)st[c], x1 = (float)st[C + c], x2 = (float)st[2 * C + c], x3 = (float)one;
+        float* ra = f32a + e * lda32;
+        ra[c] = x0;
+        ra[C + c] = x1;
+        ra[2 * C + c] = x2;
+        ra[3 * C + c] = x3;
+        if (f32b) {
+          float* rb = f32b + e * ldb32;
+          rb[c] = x0;
+          rb[C + c] = x1;
+          rb[2 * C + c] = x2;
+          rb[3 * C + c] = x3;
+        }
+      }
     }
     __syncthreads();  // s_max / fs reused by the next env
   }
@@ -1425,9 +1441,46 @@ int ap_pipe_train_table(ap_pipe_t p, const int32_t* cand_pos, int32_t C, void* s
   return AP_OK;
 }
 
+namespace apb {
+__global__ void state_to_f32_kernel(const double* state, int64_t E, int W, float* f32a, int64_t lda32, float* f32b,
+                                    int64_t ldb32) {
+  const int64_t total = E * (int64_t)W;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = i / W;
+    const int c = (int)(i % W);
+    const float x = (float)state[i];
+    f32a[e * lda32 + c] = x;
+    if (f32b) f32b[e * ldb32 + c] = x;
+  }
+}
+
+int train_state_impl(ap_pipe_t p, const ap_topology* topo, const int32_t* cand_pos, int32_t C, const int32_t* applied,
+                     int32_t A, const uint8_t* mask, int64_t E, double bwm, double* state, float* f32a, int64_t lda32,
+                     float* f32b, int64_t ldb32, void* stream);
+}  // namespace apb
+
 int ap_pipe_train_state(ap_pipe_t p, const ap_topology* topo, const int32_t* cand_pos, int32_t C,
                         const int32_t* applied, int32_t A, const uint8_t* mask, int64_t E, double bwm, double* state,
                         void* stream) {
+  return apb::train_state_impl(p, topo, cand_pos, C, applied, A, mask, E, bwm, state, nullptr, 0, nullptr, 0, stream);
+}
+
+int ap_pipe_train_state_ex(ap_pipe_t p, const ap_topology* topo, const int32_t* cand_pos, int32_t C,
+                           const int32_t* applied, int32_t A, const uint8_t* mask, int64_t E, double bwm,
+                           double* state, float* state_f32, int64_t ld_f32, float* state_f32_b, int64_t ld_f32_b,
+                           void* stream) {
+  if (!state_f32 || ld_f32 < 4 * (int64_t)C || (state_f32_b && ld_f32_b < 4 * (int64_t)C)) {
+    set_error("ap_pipe_train_state_ex: bad fp32 outputs");
+    return AP_ERR_INVALID;
+  }
+  return apb::train_state_impl(p, topo, cand_pos, C, applied, A, mask, E, bwm, state, state_f32, ld_f32, state_f32_b,
+                          ld_f32_b, stream);
+}
+
+namespace apb {
+int train_state_impl(ap_pipe_t p, const ap_topology* topo, const int32_t* cand_pos, int32_t C, const int32_t* applied,
+                     int32_t A, const uint8_t* mask, int64_t E, double bwm, double* state, float* f32a, int64_t lda32,
+                     float* f32b, int64_t ldb32, void* stream) {
   int rc = check_topo(topo, A + 2);
   if (rc != AP_OK) return rc;
   if (!p || C < 1 || A < 0 || E < 0 || (E && (!cand_pos || !mask || !state || (A && !applied)))) {
@@ -1440,7 +1493,7 @@ int ap_pipe_train_state(ap_pipe_t p, const ap_topology* topo, const int32_t* can
   const double* tab = std::getenv("AP_PP_NO_TABLE") ? nullptr : p->table_for(cand_pos, C);
   if (tab) {  // bound candidate list: stage sums are lookups (one launch)
     train_state_tab_kernel<<<(int)std::min<int64_t>(E, 148 * 8), 256, 0, (cudaStream_t)stream>>>(
-        p->dev(), t, cand_pos, C, tab, applied, A, mask, E, 1.0 + bwm, state);
+        p->dev(), t, cand_pos, C, tab, applied, A, mask, E, 1.0 + bwm, state, f32a, lda32, f32b, ldb32);
     AP_CUDA_CHECK(cudaGetLastError());
     return AP_OK;
   }
@@ -1473,8 +1526,14 @@ int ap_pipe_train_state(ap_pipe_t p, const ap_topology* topo, const int32_t* can
   AP_CUDA_CHECK(cudaGetLastError());
   train_norm_kernel<<<(int)std::min<int64_t>(E, 148 * 8), 256, 0, (cudaStream_t)stream>>>(C, applied, A, E, state);
   AP_CUDA_CHECK(cudaGetLastError());
+  if (f32a) {
+    state_to_f32_kernel<<<grid_for(E * 4 * (int64_t)C, 256), 256, 0, (cudaStream_t)stream>>>(state, E, 4 * C, f32a,
+                                                                                          lda32, f32b, ldb32);
+    AP_CUDA_CHECK(cudaGetLastError());
+  }
   return AP_OK;
 }
+}  // namespace apb
 
 int ap_infer_length(const double* arrays, int32_t G, const ap_topology* topo, int32_t K, int32_t M,
                     const int32_t* bnd, const int32_t* cut, int64_t batch, double* len, void* stream) {

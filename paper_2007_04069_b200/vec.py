@@ -194,15 +194,18 @@ class VecPipeTrainEnv:
                                            P_(self.ep_return), P_(self.finished_return), P_(self.episodes_done),
                                            P_(ctl), int(world), int(rank), _s()))
 
-    def _state_eval(self) -> None:
+    def _state_eval(self, next_too: bool = False) -> None:
+        """K2 into state64 and the fp32 cur_state (and next_state) rows in one call."""
         import ctypes
 
         lib = _native.require_device()
         P_ = _native.ptr
-        _native.check(lib.ap_pipe_train_state(self.host._model.handle, ctypes.byref(self.topo_c), P_(self.cand_pos),
-                                              self.C, P_(self.applied_state), self.a_max, P_(self.mask), self.E,
-                                              self.bwm, P_(self.state64), _s()))
-        self.cur_state.copy_(self.state64)
+        nxt = self.next_state if next_too else None
+        _native.check(lib.ap_pipe_train_state_ex(self.host._model.handle, ctypes.byref(self.topo_c), P_(self.cand_pos),
+                                                 self.C, P_(self.applied_state), self.a_max, P_(self.mask), self.E,
+                                                 self.bwm, P_(self.state64), P_(self.cur_state),
+                                                 self.cur_state.stride(0), P_(nxt) if nxt is not None else None,
+                                                 nxt.stride(0) if nxt is not None else 0, _s()))
 
     def step(self, actions, step_base: int = 0, ctl=None, world: int = 1, rank: int = 0) -> None:
         """Apply one pick per env (actions [E] int32, device); fills rewards / done /
@@ -221,8 +224,7 @@ class VecPipeTrainEnv:
                                          P_(self.act), P_(self.param), P_(self.cuts), 0, self.mem, 4.0, 1,
                                          P_(self.length), P_(self.feasible), _s()))
         self._post(ctl if ctl is not None else self._ctl0, world, rank)
-        self._state_eval()
-        self.next_state.copy_(self.cur_state)
+        self._state_eval(next_too=True)  # cur_state and next_state written by the K2 kernel
 
     def best_plan(self):
         """(pipeline length, pivot names, global episode id) of the best feasible finished

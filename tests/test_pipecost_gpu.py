@@ -268,3 +268,42 @@ def test_metrics_bound_matches_sweep(cuda, K):
                                             *[P_(x) for x in b], _native.stream_handle()))
     for x, y in zip(a, b):
         assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("table", [True, False])
+def test_train_state_ex_fp32_rows(cuda, monkeypatch, table):
+    """ap_pipe_train_state_ex writes the fp64 state and two fp32 copies (strided rows) equal to its cast."""
+    import ctypes
+
+    from paper_2007_04069_b200 import _native, graphs
+
+    g = graphs.generate("bert48")
+    topo = DeviceTopology(2, 4)
+    K = 4
+    env = PipeTrainEnv(g, topo, K, radius=3)
+    C, E, A = env.num_actions, 40, K - 2
+    rng = np.random.default_rng(11)
+    applied = np.full((E, A), -1, dtype=np.int32)
+    mask = np.zeros((E, C), dtype=np.uint8)
+    for e in range(E):
+        k = int(rng.integers(0, K - 1))
+        picks = np.sort(rng.choice(C - (K - 1), size=k, replace=False)) if k else np.zeros(0, int)
+        applied[e, :k] = picks
+        mask[e, (picks[-1] if k else -1) + 1: C - ((K - 1) - k) + 1] = 1
+    d_cand = torch.from_numpy(env._cand_pos).cuda()
+    if table:
+        assert env._model.bind_candidates(d_cand)
+    else:
+        monkeypatch.setenv("AP_PP_NO_TABLE", "1")
+    d_app, d_mask = torch.from_numpy(applied).cuda(), torch.from_numpy(mask).cuda()
+    st = torch.empty((E, 4 * C), dtype=torch.float64, device="cuda")
+    fa = torch.full((E, 4 * C + 12), float("nan"), device="cuda")
+    fb = torch.full((E, 4 * C + 4), float("nan"), device="cuda")
+    lib = _native.require_device()
+    _native.check(lib.ap_pipe_train_state_ex(env._model.handle, ctypes.byref(_native.Topology.of(topo)),
+                                             _native.ptr(d_cand), C, _native.ptr(d_app), A, _native.ptr(d_mask), E, 2.0,
+                                             _native.ptr(st), _native.ptr(fa), fa.stride(0), _native.ptr(fb),
+                                             fb.stride(0), _native.stream_handle()))
+    assert torch.equal(fa[:, : 4 * C], st.float())
+    assert torch.equal(fb[:, : 4 * C], st.float())
+    assert torch.isnan(fa[:, 4 * C:]).all()
