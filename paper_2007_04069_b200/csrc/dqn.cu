@@ -799,12 +799,22 @@ __global__ void per_update_kernel(double* prio, const int32_t* idx, const float*
   prio[idx[b]] = fabs((double)td[b]) + 1e-6;
 }
 
-__global__ void gather_rows_kernel(const float* src, int64_t lds, const int32_t* idx, int B, int cols, float* dst,
-                                   int64_t ldd) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)B * cols;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int b = (int)(i / cols), c = (int)(i % cols);
-    dst[(int64_t)b * ldd + c] = src[(int64_t)idx[b] * lds + c];
+// dst[b, :cols] = src[idx[b], :cols]: blockIdx.y = b, 16-byte vectors when the
+// rows and bases allow (no per-element index arithmetic)
+__global__ void gather_rows_kernel(const float* __restrict__ src, int64_t lds, const int32_t* __restrict__ idx, int B,
+                                   int cols, float* __restrict__ dst, int64_t ldd, int vec) {
+  const int b = blockIdx.y;
+  const float* __restrict__ s = src + (int64_t)idx[b] * lds;
+  float* __restrict__ d = dst + (int64_t)b * ldd;
+  const int step = gridDim.x * blockDim.x;
+  if (vec) {
+    const float4* __restrict__ s4 = reinterpret_cast<const float4*>(s);
+    float4* __restrict__ d4 = reinterpret_cast<float4*>(d);
+#pragma unroll 4
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cols / 4; c += step) d4[c] = s4[c];
+  } else {
+#pragma unroll 4
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += step) d[c] = s[c];
   }
 }
 
@@ -1118,8 +1128,15 @@ int ap_per_update(double* priorities, const int32_t* indices, const float* td, i
 int ap_gather_rows(const float* src, int64_t lds, const int32_t* idx, int32_t B, int32_t cols, float* dst,
                    int64_t ldd, void* stream) {
   if (B <= 0 || cols <= 0) return AP_OK;
-  gather_rows_kernel<<<blocks_for((int64_t)B * cols, 256), 256, 0, (cudaStream_t)stream>>>(src, lds, idx, B, cols, dst,
-                                                                                         ldd);
+  if (B > 65535) {
+    set_error("ap_gather_rows: at most 65535 rows per call");
+    return AP_ERR_INVALID;
+  }
+  const int vec = cols % 4 == 0 && lds % 4 == 0 && ldd % 4 == 0 &&
+                  ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+  const int per_row = vec ? cols / 4 : cols;
+  const dim3 grid((unsigned)std::max(1, std::min((per_row + 255) / 256, 16)), (unsigned)B);
+  gather_rows_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(src, lds, idx, B, cols, dst, ldd, vec);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
