@@ -357,7 +357,17 @@ int launch_gemm_v3(const float* A, int64_t lda, int transA, const float* B, int6
   if (precision != 1 || transA || !transB || std::getenv("AP_GEMM_NO_TMA")) return AP_ERR_UNSUPPORTED;
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (!al(A) || !al(B) || lda % 4 || ldb % 4 || M < 1 || N < 1 || K < 1) return AP_ERR_UNSUPPORTED;
-  const int bn = N <= 32 ? 32 : 64;
+  // BN: 32 for narrow N; 128 when the BN=64 grid (one CTA per SM) needs more waves over the 148 SMs
+  // than the BN=128 grid (measured: 12681x64x256 12.5 -> 9.4 us, 1024x256x3171 16.7 -> 12.4 us,
+  // 257x64x3171 7.2 -> 5.3 us; grids that fit one wave either way stay at 64).  AP_GEMM_V3_BN=64|128 forces.
+  const int env_bn = std::getenv("AP_GEMM_V3_BN") ? std::atoi(std::getenv("AP_GEMM_V3_BN")) : 0;
+  int bn = N <= 32 ? 32 : 64;
+  if (bn == 64 && N > 64) {
+    const int64_t mt0 = (M + BM3 - 1) / BM3;
+    const int64_t w64 = (mt0 * ((N + 63) / 64) + 147) / 148, w128 = (mt0 * ((N + 127) / 128) + 147) / 148;
+    const bool unsplit = mt0 * ((N + 63) / 64) >= 120;
+    if (env_bn == 128 || (env_bn == 0 && unsplit && w128 < w64)) bn = 128;
+  }
   CUtensorMap ma, mb;
   if (!make_map(&ma, A, M, K, lda, BM3) || !make_map(&mb, B, N, K, ldb, bn)) return AP_ERR_UNSUPPORTED;
   G3 g{C, ldc, M, N, K, bias, relu, 0, nullptr, 0};
@@ -383,8 +393,9 @@ int launch_gemm_v3(const float* A, int64_t lda, int transA, const float* B, int6
     if (wrc != AP_OK) return wrc;
   }
   const dim3 grid(mt, nt, splits);
-  const int rc = four_stages ? (bn == 32 ? run3<32, 4>(ma, mb, g, grid, stream) : run3<64, 4>(ma, mb, g, grid, stream))
-                             : (bn == 32 ? run3<32, 6>(ma, mb, g, grid, stream) : run3<64, 6>(ma, mb, g, grid, stream));
+  const int rc = bn == 128     ? run3<128, 6>(ma, mb, g, grid, stream)
+                 : four_stages ? (bn == 32 ? run3<32, 4>(ma, mb, g, grid, stream) : run3<64, 4>(ma, mb, g, grid, stream))
+                               : (bn == 32 ? run3<32, 6>(ma, mb, g, grid, stream) : run3<64, 6>(ma, mb, g, grid, stream));
   if (rc != AP_OK || splits == 1 || g.cluster) return rc;
   const int64_t total = (int64_t)M * N;
   splitk_reduce3_kernel<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, stream>>>(

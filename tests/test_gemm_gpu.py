@@ -109,3 +109,21 @@ def test_gemm_tf32_is_tf32_accurate(cuda, m, n, k):
     out3 = gemm(a, b, precision=3)
     rel3 = ((out3.double() - r).abs().max() / r.abs().max()).item()
     assert rel3 < 1e-5 and rel3 < rel
+
+
+@pytest.mark.parametrize("m,n,k", [(12681, 256, 64), (1024, 3171, 256), (257, 3171, 64), (300, 130, 1060),
+                                   (64, 256, 1060)])
+def test_bn128_tiles_match_bn64(cuda, m, n, k, monkeypatch):
+    """BN = 128 tiles (picked automatically when they need fewer waves) vs BN = 64 tiles and fp64:
+    the same k order per output element, so bit-identical without split-K."""
+    g = torch.Generator(device="cuda").manual_seed(m + 3 * n + k)
+    a = torch.randn((m, k), device="cuda", generator=g)
+    b = torch.randn((n, k), device="cuda", generator=g)
+    bias = torch.randn(n, device="cuda", generator=g)
+    outs = []
+    for bn in ("64", "128"):
+        monkeypatch.setenv("AP_GEMM_V3_BN", bn)
+        outs.append(gemm(a, b, trans_b=True, bias=bias, relu=True, precision=1))
+    r = ref(a, b, False, True, bias, True)
+    assert (outs[1].double() - r).abs().max().item() < 5e-3 * r.abs().max().item()
+    assert (outs[1] - outs[0]).abs().max().item() <= 1e-5 * r.abs().max().item()
