@@ -254,3 +254,32 @@ def test_properties_at_scale(cuda):
     assert empty["outcome"].numel() == 0
     one = eng.run_batch(torch.full((1, n), -1, dtype=torch.int8))
     assert int(one["outcome"][0]) in (0, 1)
+
+
+@pytest.mark.parametrize("layers", [400, 1000])
+def test_real_hlo_scale_matches_oracle(cuda, layers):
+    """BERT stacks at real-HLO scale (> 50k instructions): 400 layers = 26k
+    instructions / 1.2k link classes, 1000 layers = 66k instructions / 117k slots / 3k classes
+    (the CTA-per-plan kernel).  Outcomes and every slot of the non-conflicting plans match the
+    C oracle; short linkage-order prefixes and all-R rows keep conflict-free plans in the batch."""
+    g = graphs.bert(layers, 1024, 4096)
+    dims = decision_dims(g, g.trainable_variables)
+    n = len(dims)
+    order = np.asarray([d.flat_index for d in sorted_decision_order(extract_linkage_groups(g, dims))])
+    pos = {d.flat_index: i for i, d in enumerate(dims)}
+    order = np.asarray([pos[f] for f in order])
+    rng = np.random.default_rng(layers)
+    short = np.full((96, n), -1, np.int8)
+    for b in range(96):
+        k = int(rng.integers(1, 12))
+        short[b, order[:k]] = rng.integers(0, 2, size=k)
+    all_r = np.where(np.arange(n)[None, :] < rng.integers(1, n + 1, size=(16, 1)), 0, -1).astype(np.int8)
+    seeds = np.concatenate([random_prefix_seeds(rng, n, 64, order), short, all_r])
+    out = PropagationEngine(g, dims).run_batch(torch.from_numpy(seeds), want_slots=True)
+    flat = g.flat()
+    cand_slots = np.array([flat.slot_offset[d.instruction_id] + d.dim for d in dims])
+    st, oc, _ = oracle.propagate_batch(flat, cand_slots, seeds, cand_slots)
+    np.testing.assert_array_equal(out["outcome"].cpu().numpy(), oc)
+    ok = oc != 2
+    assert ok.sum() >= 16
+    np.testing.assert_array_equal(out["slots"].cpu().numpy()[ok][:, : flat.num_slots], st[ok])
