@@ -239,8 +239,7 @@ __global__ void __launch_bounds__(kThreads) propagate_cta_kernel(PropParams p) {
     __syncthreads();
     const int8_t* srow = p.seeds + b * p.seed_stride;
     int conflict = 0;
-    for (int j = tid; j < p.D; j += kThreads) {
-      const int v = srow[j];
+    auto seed_one = [&](int j, int v) {
       if (v == 1 || v == 0) {
         const int32_t c = dec_class[j];
         atomicOr(v == 1 ? &P[c >> 5] : &R[c >> 5], 1u << (c & 31));
@@ -249,13 +248,26 @@ __global__ void __launch_bounds__(kThreads) propagate_cta_kernel(PropParams p) {
         for (int k = first_same[j]; k < j; ++k)
           if (srow[k] == 1) conflict = 1;
       }
+    };
+    // 16 seeds per load (rows are 16-byte aligned); all-unseeded chunks cost one load
+    const int dfull = kVecSlots ? p.D / 16 : 0;
+    for (int q = tid; q < dfull; q += kThreads) {
+      const uint4 w = reinterpret_cast<const uint4*>(srow)[q];
+      if ((w.x & w.y & w.z & w.w) == 0xffffffffu) continue;
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int v = (int8_t)(ws[u >> 2] >> (8 * (u & 3)));
+        if (v != -1) seed_one(16 * q + u, v);
+      }
     }
+    for (int j = 16 * dfull + tid; j < p.D; j += kThreads) seed_one(j, srow[j]);
     __syncthreads();
-    for (int w = tid; w < p.Cw; w += kThreads) {
-      uint32_t bits = P[w];
-      while (bits) {
-        const int32_t c = 32 * w + __ffs(bits) - 1;
-        bits &= bits - 1;
+    // implications of every P class: a warp per bitset word, a lane per bit
+    // (P is read-only here and R only gains bits, so the order is irrelevant)
+    for (int w = warp; w < p.Cw; w += kWarps) {
+      if (P[w] & (1u << lane)) {
+        const int32_t c = 32 * w + lane;
         const int e = imp_offset[c + 1];
         for (int k = imp_offset[c]; k < e; ++k) {
           const int32_t t = imp_target[k];
@@ -272,16 +284,41 @@ __global__ void __launch_bounds__(kThreads) propagate_cta_kernel(PropParams p) {
     }
     int dP = 0, dR = 0, nP = 0, nR = 0;
     int8_t* crow = p.cand_out ? p.cand_out + b * p.cand_stride : nullptr;
-    for (int j = tid; j < p.D; j += kThreads) {
-      const int s = status(dec_class[j]);
-      if (crow) crow[j] = (int8_t)s;
-      if (dec_flags[j] & 1) {
-        const bool seeded = srow[j] != -1;
+    auto tally = [&](int s, int flags, int seedv) {
+      if (flags & 1) {
+        const bool seeded = seedv != -1;
         dP += (s == 1);
         dR += (s == 0);
         nP += (s == 1) && !seeded;
         nR += (s == 0) && !seeded;
       }
+    };
+    // 16 candidates per step: class ids (4 x int4), flags and seeds (one uint4
+    // each) in flight together, statuses stored as one uint4
+    const bool cvec =
+        kVecSlots && (!crow || (p.cand_stride % 16 == 0 && (reinterpret_cast<uintptr_t>(p.cand_out) & 15) == 0));
+    const int cfull = cvec ? p.D / 16 : 0;
+    for (int q = tid; q < cfull; q += kThreads) {
+      const int4* cq = reinterpret_cast<const int4*>(dec_class) + 4 * q;
+      const int4 c0 = cq[0], c1 = cq[1], c2 = cq[2], c3 = cq[3];
+      const uint4 fl = reinterpret_cast<const uint4*>(dec_flags)[q];
+      const uint4 sd = reinterpret_cast<const uint4*>(srow)[q];
+      const int cls[16] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w,
+                           c2.x, c2.y, c2.z, c2.w, c3.x, c3.y, c3.z, c3.w};
+      const uint32_t fw[4] = {fl.x, fl.y, fl.z, fl.w}, sw[4] = {sd.x, sd.y, sd.z, sd.w};
+      uint32_t ow[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int st = status(cls[u]);
+        ow[u >> 2] |= (uint32_t)(uint8_t)st << (8 * (u & 3));
+        tally(st, (int)((fw[u >> 2] >> (8 * (u & 3))) & 0xffu), (int)(int8_t)(sw[u >> 2] >> (8 * (u & 3))));
+      }
+      if (crow) reinterpret_cast<uint4*>(crow)[q] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+    }
+    for (int j = 16 * cfull + tid; j < p.D; j += kThreads) {
+      const int s = status(dec_class[j]);
+      if (crow) crow[j] = (int8_t)s;
+      tally(s, dec_flags[j], srow[j]);
     }
     if (p.slots_out) {
       int8_t* orow = p.slots_out + b * p.slots_stride;
@@ -525,7 +562,9 @@ int launch_propagate(const GraphTables* g, const DecisionTables* d, const int8_t
   } else {
     // very wide graphs: one plan per CTA (propagate_cta_kernel) with the
     // bitsets (+ status table when it fits) shared by the whole CTA
-    const bool vec = slots_out && (slots_stride % 16 == 0) && ((reinterpret_cast<uintptr_t>(slots_out) & 15) == 0);
+    // 16-byte rows: slot rows (when written) and seed rows; candidate rows are checked in the kernel
+    const bool vec = (!slots_out || ((slots_stride % 16 == 0) && ((reinterpret_cast<uintptr_t>(slots_out) & 15) == 0))) &&
+                     (seed_stride % 16 == 0) && ((reinterpret_cast<uintptr_t>(seeds) & 15) == 0);
     const int64_t cta_bits = (int64_t)2 * p.Cw * 4, cta_table = cta_bits + align16(p.C);
     if (cta_bits <= kSmemCap && std::getenv("AP_PROPAGATE_NO_CTA") == nullptr) {
       const bool tbl = cta_table <= kSmemCap;
