@@ -15,10 +15,14 @@
 // indices match the reference for the same uniforms.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "engine.h"
 
 namespace apb {
+
+bool pdl_enabled() { return std::getenv("AP_NO_PDL") == nullptr; }
+
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -27,6 +31,7 @@ constexpr unsigned kFull = 0xffffffffu;
 // adds (each lane's add order is unchanged); z and q never alias.
 __global__ void dueling_kernel(const float* __restrict__ z, int64_t ldz, float* __restrict__ q, int64_t ldq, int B,
                                int A) {
+  pdl_entry();
   const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (b >= B) return;
@@ -53,6 +58,7 @@ __global__ void dueling_kernel(const float* __restrict__ z, int64_t ldz, float* 
 // leaves too few loads in flight when A is in the thousands and B is small).
 __global__ void __launch_bounds__(256) dueling_wide_kernel(const float* __restrict__ z, int64_t ldz,
                                                            float* __restrict__ q, int64_t ldq, int B, int A) {
+  pdl_entry();
   __shared__ float s_part[8];
   const int b = blockIdx.x;
   const float* __restrict__ row = z + (int64_t)b * ldz + 1;
@@ -101,6 +107,7 @@ __device__ inline float epsilon_dev(int64_t it, float e0, float e1, int64_t deca
 // counter ctl[AP_CTL_STEP] + 1, instead of the by-value arguments
 __global__ void act_kernel(const float* q, int64_t ldq, const uint8_t* mask, int64_t ldm, int E, int A, float eps,
                            uint64_t seed, int32_t* out, const int64_t* ctl, float eps0, float eps1, int64_t decay) {
+  pdl_entry();
   const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (e >= E) return;
@@ -178,6 +185,7 @@ __global__ void td_kernel(const float* q, const float* online_next, const float*
                           int64_t ldm, const float* weights, int B, int A, float gamma, float delta, float* dz,
                           int64_t ldz, float* td_out, float* loss_out, const int32_t* idx, float* dz_t,
                           int64_t ldzt) {
+  pdl_entry();
   const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (b >= B) return;
@@ -237,6 +245,7 @@ constexpr int kHeadMax = 8;
 template <int A1>
 __global__ void head_forward_kernel(const float* h, int64_t ldh, const float* wht, int64_t ldw, const float* bh,
                                     int B, int H, float* q, int64_t ldq) {
+  pdl_entry();
   const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (b >= B) return;
@@ -272,6 +281,7 @@ __global__ void td_wide_kernel(const float* q, const float* online_next, const f
                                const uint8_t* next_mask, int64_t ldm, const float* weights, int B, int A, float gamma,
                                float delta, float* dz, int64_t ldz, float* td_out, float* loss_out, const int32_t* idx,
                                float* dz_t, int64_t ldzt) {
+  pdl_entry();
   __shared__ float s_best[32];
   __shared__ int s_bj[32], s_any[32];
   __shared__ float s_g;
@@ -362,6 +372,7 @@ struct TransposeBatch {
 };
 
 __global__ void transpose_batch_kernel(TransposeBatch tb) {
+  pdl_entry();
   __shared__ float tile[32][33];
   const int z = blockIdx.z;
   const int rows = tb.rows[z], cols = tb.cols[z];
@@ -384,6 +395,7 @@ __global__ void transpose_batch_kernel(TransposeBatch tb) {
 // (the K-major operand of the next weight-gradient GEMM)
 __global__ void relu_bwd_t_kernel(float* dh, int64_t lddh, const float* h, int64_t ldh, int B, int H, float* dh_t,
                                   int64_t ldt) {
+  pdl_entry();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)B * H) return;
   const int b = (int)(i / H), j = (int)(i % H);
@@ -396,6 +408,7 @@ __global__ void relu_bwd_t_kernel(float* dh, int64_t lddh, const float* h, int64
 }
 
 __global__ void relu_bwd_kernel(float* dh, const float* h, int64_t n) {
+  pdl_entry();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     if (!(h[i] > 0.0f)) dh[i] = 0.0f;
 }
@@ -407,6 +420,7 @@ __global__ void relu_bwd_kernel(float* dh, const float* h, int64_t n) {
 __global__ void head_backward_kernel(const float* dz, int64_t ldz, const float* wh, int64_t ldw, const float* h,
                                      int64_t ldh, int B, int H, int A1, float* dh, int64_t lddh, float* dh_t,
                                      int64_t ldt) {
+  pdl_entry();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)B * H) return;
   const int b = (int)(i / H), j = (int)(i % H);
@@ -428,6 +442,7 @@ __global__ void head_backward_kernel(const float* dz, int64_t ldz, const float* 
 // own expression, so the comparison is exact); g_b == 0 gives dh = 0.
 __global__ void __launch_bounds__(256) head_rowsum_kernel(const float* __restrict__ wh, int64_t ldw, int A1,
                                                           float* __restrict__ rowsum) {
+  pdl_entry();
   __shared__ float s_part[8];
   const float* __restrict__ w = wh + (int64_t)blockIdx.x * ldw;
   float s = 0.0f;
@@ -448,6 +463,7 @@ __global__ void __launch_bounds__(256) head_backward_dueling_kernel(const float*
                                                                     const float* __restrict__ rowsum, int H, int A1,
                                                                     float* __restrict__ dh, int64_t lddh,
                                                                     float* __restrict__ dh_t, int64_t ldt) {
+  pdl_entry();
   __shared__ int s_a, s_cnt, s_nz;
   const int b = blockIdx.x;
   const int A = A1 - 1;
@@ -491,6 +507,7 @@ __global__ void __launch_bounds__(256) head_backward_dueling_kernel(const float*
 __global__ void head_backward_wide_kernel(const float* dz, int64_t ldz, const float* wh, int64_t ldw, const float* h,
                                           int64_t ldh, int B, int H, int A1, float* dh, int64_t lddh, float* dh_t,
                                           int64_t ldt) {
+  pdl_entry();
   const int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (w >= (int64_t)B * H) return;
@@ -508,6 +525,7 @@ __global__ void head_backward_wide_kernel(const float* dz, int64_t ldz, const fl
 }
 
 __global__ void colsum_kernel(const float* x, int64_t ld, int rows, int cols, float* out) {
+  pdl_entry();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= cols) return;
   float s = 0.0f;
@@ -518,6 +536,7 @@ __global__ void colsum_kernel(const float* x, int64_t ld, int rows, int cols, fl
 // ctl != nullptr: bias corrections from step t = ctl[AP_CTL_TRAIN] + 1
 __global__ void adam_kernel(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
                             float eps, float c1, float c2, const int64_t* ctl) {
+  pdl_entry();
   if (ctl) {  // bias corrections once per block, not per thread (two fp64 pow)
     __shared__ float s_c[2];
     if (threadIdx.x == 0) {
@@ -592,6 +611,7 @@ struct AdamTiles {
 __global__ void __launch_bounds__(256) adam_tile_kernel(float* p, const float* g, float* m, float* v, float lr,
                                                         float b1, float b2, float eps, const int64_t* ctl,
                                                         AdamTiles at) {
+  pdl_entry();
   __shared__ float s_c[2];
   __shared__ float tile[32][33];
   auto corrections = [&]() {  // bias corrections (thread 0), published by the caller's barrier
@@ -662,6 +682,7 @@ __global__ void __launch_bounds__(256) adam_tile_kernel(float* p, const float* g
 
 __global__ void adam_t_kernel(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
                               float eps, const int64_t* ctl, AdamSegments segs) {
+  pdl_entry();
   __shared__ float s_c[2];
   if (threadIdx.x == 0) {
     const double t = (double)(ctl[AP_CTL_TRAIN] + 1);
@@ -742,6 +763,7 @@ __device__ double pairwise_sum(const double* a, int64_t n) {
 // one CTA: PER sample (agent.py:207-223) for B uniforms drawn by the caller
 __global__ void per_sample_kernel(const double* prio, int n, double alpha, double beta, const double* uniforms, int B,
                                   double* scaled, double* cdf, int32_t* idx_out, float* w_out) {
+  pdl_entry();
   __shared__ double s_total, s_last, s_wmax;
   for (int i = threadIdx.x; i < n; i += blockDim.x) scaled[i] = pow(prio[i], alpha);
   __syncthreads();
@@ -792,6 +814,7 @@ __global__ void per_sample_kernel(const double* prio, int n, double alpha, doubl
 
 // priorities[idx] = |td| + 1e-6, duplicates: the last occurrence wins (agent.py:226)
 __global__ void per_update_kernel(double* prio, const int32_t* idx, const float* td, int B) {
+  pdl_entry();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   for (int k = b + 1; k < B; ++k)
@@ -803,6 +826,7 @@ __global__ void per_update_kernel(double* prio, const int32_t* idx, const float*
 // rows and bases allow (no per-element index arithmetic)
 __global__ void gather_rows_kernel(const float* __restrict__ src, int64_t lds, const int32_t* __restrict__ idx, int B,
                                    int cols, float* __restrict__ dst, int64_t ldd, int vec) {
+  pdl_entry();
   const int b = blockIdx.y;
   const float* __restrict__ s = src + (int64_t)idx[b] * lds;
   float* __restrict__ d = dst + (int64_t)b * ldd;
@@ -834,9 +858,9 @@ int ap_dqn_dueling(const float* z, int64_t ldz, float* q, int64_t ldq, int32_t B
   }
   if (B == 0) return AP_OK;
   if (A > 256)
-    dueling_wide_kernel<<<B, 256, 0, (cudaStream_t)stream>>>(z, ldz, q, ldq, B, A);
+    launch_pdl(dueling_wide_kernel, dim3(B), dim3(256), 0, (cudaStream_t)stream, z, ldz, q, ldq, B, A);
   else
-    dueling_kernel<<<(B + 7) / 8, 256, 0, (cudaStream_t)stream>>>(z, ldz, q, ldq, B, A);
+    launch_pdl(dueling_kernel, dim3((B + 7) / 8), dim3(256), 0, (cudaStream_t)stream, z, ldz, q, ldq, B, A);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
@@ -848,7 +872,7 @@ int ap_dqn_act(const float* q, int64_t ldq, const uint8_t* mask, int64_t ldm, in
     return AP_ERR_INVALID;
   }
   if (E == 0) return AP_OK;
-  act_kernel<<<(E + 7) / 8, 256, 0, (cudaStream_t)stream>>>(q, ldq, mask, ldm, E, A, epsilon, seed, actions, nullptr,
+  launch_pdl(act_kernel, dim3((E + 7) / 8), dim3(256), 0, (cudaStream_t)stream, q, ldq, mask, ldm, E, A, epsilon, seed, actions, nullptr,
                                                             0.f, 0.f, 0);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
@@ -862,7 +886,7 @@ int ap_dqn_act_ctl(const float* q, int64_t ldq, const uint8_t* mask, int64_t ldm
     return AP_ERR_INVALID;
   }
   if (E == 0) return AP_OK;
-  act_kernel<<<(E + 7) / 8, 256, 0, (cudaStream_t)stream>>>(q, ldq, mask, ldm, E, A, 0.f, 0, actions, ctl,
+  launch_pdl(act_kernel, dim3((E + 7) / 8), dim3(256), 0, (cudaStream_t)stream, q, ldq, mask, ldm, E, A, 0.f, 0, actions, ctl,
                                                             epsilon_start, epsilon_final, decay_iters);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
@@ -877,7 +901,7 @@ int ap_dqn_td(const float* q, const float* online_next, const float* target_next
     set_error("ap_dqn_td: bad arguments");
     return AP_ERR_INVALID;
   }
-  td_kernel<<<(B + 7) / 8, 256, 0, (cudaStream_t)stream>>>(q, online_next, target_next, ldq, actions, rewards, done,
+  launch_pdl(td_kernel, dim3((B + 7) / 8), dim3(256), 0, (cudaStream_t)stream, q, online_next, target_next, ldq, actions, rewards, done,
                                                            next_mask, ldm, weights, B, A, gamma, huber_delta, dz, ldz,
                                                            td, loss, nullptr, nullptr, 0);
   AP_CUDA_CHECK(cudaGetLastError());
@@ -898,13 +922,13 @@ int ap_dqn_head_forward(const float* h, int64_t ldh, const float* wh_t, int64_t 
   const dim3 grid((B + 7) / 8), block(256);
   cudaStream_t s = (cudaStream_t)stream;
   switch (A1) {
-    case 2: head_forward_kernel<2><<<grid, block, 0, s>>>(h, ldh, wh_t, ldw, bh, B, H, q, ldq); break;
-    case 3: head_forward_kernel<3><<<grid, block, 0, s>>>(h, ldh, wh_t, ldw, bh, B, H, q, ldq); break;
-    case 4: head_forward_kernel<4><<<grid, block, 0, s>>>(h, ldh, wh_t, ldw, bh, B, H, q, ldq); break;
-    case 5: head_forward_kernel<5><<<grid, block, 0, s>>>(h, ldh, wh_t, ldw, bh, B, H, q, ldq); break;
-    case 6: head_forward_kernel<6><<<grid, block, 0, s>>>(h, ldh, wh_t, ldw, bh, B, H, q, ldq); break;
-    case 7: head_forward_kernel<7><<<grid, block, 0, s>>>(h, ldh, wh_t, ldw, bh, B, H, q, ldq); break;
-    default: head_forward_kernel<8><<<grid, block, 0, s>>>(h, ldh, wh_t, ldw, bh, B, H, q, ldq); break;
+    case 2: launch_pdl(head_forward_kernel<2>, dim3(grid), dim3(block), 0, s, h, ldh, wh_t, ldw, bh, B, H, q, ldq); break;
+    case 3: launch_pdl(head_forward_kernel<3>, dim3(grid), dim3(block), 0, s, h, ldh, wh_t, ldw, bh, B, H, q, ldq); break;
+    case 4: launch_pdl(head_forward_kernel<4>, dim3(grid), dim3(block), 0, s, h, ldh, wh_t, ldw, bh, B, H, q, ldq); break;
+    case 5: launch_pdl(head_forward_kernel<5>, dim3(grid), dim3(block), 0, s, h, ldh, wh_t, ldw, bh, B, H, q, ldq); break;
+    case 6: launch_pdl(head_forward_kernel<6>, dim3(grid), dim3(block), 0, s, h, ldh, wh_t, ldw, bh, B, H, q, ldq); break;
+    case 7: launch_pdl(head_forward_kernel<7>, dim3(grid), dim3(block), 0, s, h, ldh, wh_t, ldw, bh, B, H, q, ldq); break;
+    default: launch_pdl(head_forward_kernel<8>, dim3(grid), dim3(block), 0, s, h, ldh, wh_t, ldw, bh, B, H, q, ldq); break;
   }
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
@@ -918,7 +942,7 @@ int ap_dqn_relu_backward_t(float* dh, int64_t lddh, const float* h, int64_t ldh,
   }
   const int64_t n = (int64_t)B * H;
   if (n == 0) return AP_OK;
-  relu_bwd_t_kernel<<<(int)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(dh, lddh, h, ldh, B, H, dh_t, ldt);
+  launch_pdl(relu_bwd_t_kernel, dim3((int)((n + 255) / 256)), dim3(256), 0, (cudaStream_t)stream, dh, lddh, h, ldh, B, H, dh_t, ldt);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
@@ -943,7 +967,7 @@ int ap_transpose_batch(int32_t n, const float* const* src, const int64_t* ld_src
     max_c = std::max(max_c, (int)cols[i]);
   }
   const dim3 grid((max_c + 31) / 32, (max_r + 31) / 32, n);
-  transpose_batch_kernel<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(tb);
+  launch_pdl(transpose_batch_kernel, dim3(grid), dim3(dim3(32, 8)), 0, (cudaStream_t)stream, tb);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
@@ -959,11 +983,11 @@ int ap_dqn_td_ring(const float* q, const float* online_next, const float* target
     return AP_ERR_INVALID;
   }
   if (A > 64)  // wide action spaces: a CTA per row
-    td_wide_kernel<<<B, 256, 0, (cudaStream_t)stream>>>(q, online_next, target_next, ldq, ring_actions, ring_rewards,
+    launch_pdl(td_wide_kernel, dim3(B), dim3(256), 0, (cudaStream_t)stream, q, online_next, target_next, ldq, ring_actions, ring_rewards,
                                                         ring_done, ring_next_mask, ldm, weights, B, A, gamma,
                                                         huber_delta, dz, ldz, td, loss, indices, dz_t, ldzt);
   else
-    td_kernel<<<(B + 7) / 8, 256, 0, (cudaStream_t)stream>>>(q, online_next, target_next, ldq, ring_actions,
+    launch_pdl(td_kernel, dim3((B + 7) / 8), dim3(256), 0, (cudaStream_t)stream, q, online_next, target_next, ldq, ring_actions,
                                                              ring_rewards, ring_done, ring_next_mask, ldm, weights, B,
                                                              A, gamma, huber_delta, dz, ldz, td, loss, indices, dz_t,
                                                              ldzt);
@@ -973,7 +997,7 @@ int ap_dqn_td_ring(const float* q, const float* online_next, const float* target
 
 int ap_dqn_relu_backward(float* dh, const float* h, int64_t n, void* stream) {
   if (n <= 0) return AP_OK;
-  relu_bwd_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(dh, h, n);
+  launch_pdl(relu_bwd_kernel, dim3(blocks_for(n, 256)), dim3(256), 0, (cudaStream_t)stream, dh, h, n);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
@@ -986,9 +1010,9 @@ int ap_dqn_head_backward_dueling(const float* dz, int64_t ldz, const float* wh, 
     return AP_ERR_INVALID;
   }
   if (B == 0) return AP_OK;
-  head_rowsum_kernel<<<H, 256, 0, (cudaStream_t)stream>>>(wh, ldw, A1, rowsum_scratch);
+  launch_pdl(head_rowsum_kernel, dim3(H), dim3(256), 0, (cudaStream_t)stream, wh, ldw, A1, rowsum_scratch);
   AP_CUDA_CHECK(cudaGetLastError());
-  head_backward_dueling_kernel<<<B, 256, 0, (cudaStream_t)stream>>>(dz, ldz, wh, ldw, h, ldh, rowsum_scratch, H, A1,
+  launch_pdl(head_backward_dueling_kernel, dim3(B), dim3(256), 0, (cudaStream_t)stream, dz, ldz, wh, ldw, h, ldh, rowsum_scratch, H, A1,
                                                                     dh, lddh, dh_t, ldt);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
@@ -1004,12 +1028,12 @@ int ap_dqn_head_backward(const float* dz, int64_t ldz, const float* wh, int64_t 
   const int64_t n = (int64_t)B * H;
   if (n == 0) return AP_OK;
   if (A1 > 32) {  // wide heads (PP actions): one warp per (row, unit), lanes over the head outputs
-    head_backward_wide_kernel<<<(int)((n + 7) / 8), 256, 0, (cudaStream_t)stream>>>(dz, ldz, wh, ldw, h, ldh, B, H,
+    launch_pdl(head_backward_wide_kernel, dim3((int)((n + 7) / 8)), dim3(256), 0, (cudaStream_t)stream, dz, ldz, wh, ldw, h, ldh, B, H,
                                                                                   A1, dh, lddh, dh_t, ldt);
     AP_CUDA_CHECK(cudaGetLastError());
     return AP_OK;
   }
-  head_backward_kernel<<<(int)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(dz, ldz, wh, ldw, h, ldh, B, H, A1,
+  launch_pdl(head_backward_kernel, dim3((int)((n + 255) / 256)), dim3(256), 0, (cudaStream_t)stream, dz, ldz, wh, ldw, h, ldh, B, H, A1,
                                                                                  dh, lddh, dh_t, ldt);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
@@ -1017,7 +1041,7 @@ int ap_dqn_head_backward(const float* dz, int64_t ldz, const float* wh, int64_t 
 
 int ap_dqn_colsum(const float* x, int64_t ld, int32_t rows, int32_t cols, float* out, void* stream) {
   if (cols <= 0) return AP_OK;
-  colsum_kernel<<<(cols + 127) / 128, 128, 0, (cudaStream_t)stream>>>(x, ld, rows, cols, out);
+  launch_pdl(colsum_kernel, dim3((cols + 127) / 128), dim3(128), 0, (cudaStream_t)stream, x, ld, rows, cols, out);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
@@ -1025,7 +1049,7 @@ int ap_dqn_colsum(const float* x, int64_t ld, int32_t rows, int32_t cols, float*
 int ap_dqn_adam(float* params, const float* grads, float* m, float* v, int64_t n, float lr, float beta1, float beta2,
                 float eps, float correct1, float correct2, void* stream) {
   if (n <= 0) return AP_OK;
-  adam_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(params, grads, m, v, n, lr, beta1, beta2, eps,
+  launch_pdl(adam_kernel, dim3(blocks_for(n, 256)), dim3(256), 0, (cudaStream_t)stream, params, grads, m, v, n, lr, beta1, beta2, eps,
                                                                      correct1, correct2, nullptr);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
@@ -1082,10 +1106,10 @@ int ap_dqn_adam_ctl_t(float* params, const float* grads, float* m, float* v, int
       if (k < nseg) lo = segs.off[order[k]] + (int64_t)segs.rows[order[k]] * segs.cols[order[k]];
     }
     const int64_t blocks = at.tile_base[nseg] + (at.gap_base[at.ngap] + 255) / 256;
-    adam_tile_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(params, grads, m, v, lr, beta1, beta2, eps,
+    launch_pdl(adam_tile_kernel, dim3((unsigned)blocks), dim3(256), 0, (cudaStream_t)stream, params, grads, m, v, lr, beta1, beta2, eps,
                                                                          ctl, at);
   } else {
-    adam_t_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(params, grads, m, v, n, lr, beta1, beta2, eps,
+    launch_pdl(adam_t_kernel, dim3(blocks_for(n, 256)), dim3(256), 0, (cudaStream_t)stream, params, grads, m, v, n, lr, beta1, beta2, eps,
                                                                          ctl, segs);
   }
   AP_CUDA_CHECK(cudaGetLastError());
@@ -1099,7 +1123,7 @@ int ap_dqn_adam_ctl(float* params, const float* grads, float* m, float* v, int64
     return AP_ERR_INVALID;
   }
   if (n <= 0) return AP_OK;
-  adam_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(params, grads, m, v, n, lr, beta1, beta2, eps,
+  launch_pdl(adam_kernel, dim3(blocks_for(n, 256)), dim3(256), 0, (cudaStream_t)stream, params, grads, m, v, n, lr, beta1, beta2, eps,
                                                                      1.f, 1.f, ctl);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
@@ -1112,7 +1136,7 @@ int ap_per_sample(const double* priorities, int32_t n, double alpha, double beta
     return AP_ERR_INVALID;
   }
   // scratch: [n] scaled + [n + B] cdf / weights
-  per_sample_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(priorities, n, alpha, beta, uniforms, B, scratch,
+  launch_pdl(per_sample_kernel, dim3(1), dim3(256), 0, (cudaStream_t)stream, priorities, n, alpha, beta, uniforms, B, scratch,
                                                          scratch + n, indices, weights);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
@@ -1120,7 +1144,7 @@ int ap_per_sample(const double* priorities, int32_t n, double alpha, double beta
 
 int ap_per_update(double* priorities, const int32_t* indices, const float* td, int32_t B, void* stream) {
   if (B <= 0) return AP_OK;
-  per_update_kernel<<<(B + 127) / 128, 128, 0, (cudaStream_t)stream>>>(priorities, indices, td, B);
+  launch_pdl(per_update_kernel, dim3((B + 127) / 128), dim3(128), 0, (cudaStream_t)stream, priorities, indices, td, B);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
@@ -1136,7 +1160,7 @@ int ap_gather_rows(const float* src, int64_t lds, const int32_t* idx, int32_t B,
                   ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
   const int per_row = vec ? cols / 4 : cols;
   const dim3 grid((unsigned)std::max(1, std::min((per_row + 255) / 256, 16)), (unsigned)B);
-  gather_rows_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(src, lds, idx, B, cols, dst, ldd, vec);
+  launch_pdl(gather_rows_kernel, dim3(grid), dim3(256), 0, (cudaStream_t)stream, src, lds, idx, B, cols, dst, ldd, vec);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }

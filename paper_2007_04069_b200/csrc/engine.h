@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/autoplan_b200.h"
@@ -23,6 +24,40 @@ int cuda_fail(cudaError_t err, const char* what);
     cudaError_t _e = (expr);                                  \
     if (_e != cudaSuccess) return ::apb::cuda_fail(_e, #expr); \
   } while (0)
+
+// Programmatic dependent launch (PDL) for the chains of small dependent
+// kernels (the DQN vector step): a kernel launched through launch_pdl may be
+// scheduled while its predecessor in the stream is still finishing; every
+// such kernel starts with pdl_entry(), which releases its own dependents and
+// then waits until the predecessor has completed and its writes are visible
+// (griddepcontrol is a no-op for a normally launched kernel).  AP_NO_PDL=1
+// launches normally.
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_entry() {
+  pdl_trigger();
+  pdl_wait();
+}
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+#endif
 
 // Device buffer owned by a handle.
 template <typename T>

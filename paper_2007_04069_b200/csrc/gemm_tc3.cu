@@ -117,6 +117,10 @@ __global__ void __launch_bounds__(128) gemm_v3_kernel(const __grid_constant__ CU
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_slot;
   if (threadIdx.x == 0) GTRACE(1);
+  // PDL: the TMEM / barrier / tensor-map prologue above overlapped the previous
+  // kernel; no global memory is touched before its writes are visible
+  pdl_trigger();
+  pdl_wait();
 
   if (threadIdx.x == 0) {
     // TMA producer
@@ -328,7 +332,7 @@ int run3(const CUtensorMap& ma, const CUtensorMap& mb, const G3& g, dim3 grid, c
     configured = true;
   }
   if (!g.cluster) {
-    k<<<grid, 128, SMEM, s>>>(ma, mb, g);
+    launch_pdl(k, grid, dim3(128), SMEM, s, ma, mb, g);
     AP_CUDA_CHECK(cudaGetLastError());
     return AP_OK;
   }
@@ -337,13 +341,15 @@ int run3(const CUtensorMap& ma, const CUtensorMap& mb, const G3& g, dim3 grid, c
   cfg.blockDim = dim3(128);
   cfg.dynamicSmemBytes = SMEM;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 1;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = grid.z;  // the split-K CTAs of one tile
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   AP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k, ma, mb, g));
   return AP_OK;
 }

@@ -31,6 +31,7 @@ __device__ inline uint32_t mix64to32(uint64_t x) {
 }
 
 __global__ void vec_apply_kernel(int8_t* seeds, int64_t ld, const int32_t* position, const int32_t* actions, int E) {
+  pdl_entry();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= E) return;
   seeds[(int64_t)e * ld + position[e]] = actions[e] == 0 ? 1 : 0;  // ACTION_PARTITION -> P (envs.py:45-48,137-142)
@@ -43,6 +44,7 @@ __global__ void vec_post_kernel(int E, int n, int64_t ld, int8_t* seeds, const i
                                 float* next_state,
                                 float* rewards, uint8_t* done, uint8_t* next_mask, int A, float* ep_return,
                                 float* finished_return, int32_t* finished_partitions, int32_t* episodes_done) {
+  pdl_entry();
   const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (e >= E) return;
@@ -118,6 +120,7 @@ __global__ void vec_track_best_kernel(int E, int n, int64_t ld, const int8_t* st
                                       const float* finished_return, int64_t step_base, const int64_t* ctl, int world,
                                       int rank, int32_t* best_partitions, float* best_return, int64_t* best_episode,
                                       int8_t* best_status) {
+  pdl_entry();
   const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (e >= E || !done[e] || outcome[e] == AP_OUTCOME_CONFLICT) return;
@@ -141,6 +144,7 @@ __global__ void per_push_kernel(int E, int S, int A, int64_t slot0, int64_t cap,
                                 const uint8_t* done, const uint8_t* masks, float* r_states, float* r_next,
                                 int32_t* r_actions, float* r_rewards, uint8_t* r_done, uint8_t* r_masks,
                                 double* r_prio, const double* max_prio, const int64_t* ctl) {
+  pdl_entry();
   const int e = blockIdx.x;
   if (ctl) slot0 = ctl[AP_CTL_SLOT];
   const int64_t slot = (slot0 + e) % cap;
@@ -203,6 +207,7 @@ __device__ inline double warp_incl_scan(double v, int lane) {
 __global__ void __launch_bounds__(kSampleThreads) per_sample_fast_kernel(
     const double* prio, int n, double alpha, double beta, const float* uniforms, int B, double* cdf,
     int32_t* idx_out, float* w_out, double* max_prio, const int64_t* ctl, uint64_t seed, int smem_cap) {
+  pdl_entry();
   extern __shared__ double s_cdf[];
   __shared__ double w_tot[32], w_max[32];
   __shared__ float s_w[32];
@@ -318,7 +323,7 @@ int launch_per_sample(const double* prio, int n_host_max, double beta, const flo
                                        (int)std::max<int64_t>(smem, 0)));
     configured = smem;
   }
-  per_sample_fast_kernel<<<1, kSampleThreads, (size_t)smem, s>>>(prio, n_host_max, 0.0, beta, uniforms, B, cdf, idx, w,
+  launch_pdl(per_sample_fast_kernel, dim3(1), dim3(kSampleThreads), (size_t)smem, s, prio, n_host_max, 0.0, beta, uniforms, B, cdf, idx, w,
                                                                  max_prio, ctl, seed, (int)(smem / 8));
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
@@ -330,6 +335,7 @@ int launch_per_sample(const double* prio, int n_host_max, double beta, const flo
 // for the batched metrics kernel), n_applied [E].
 __global__ void vec_pipe_apply_kernel(int E, int P, const int32_t* actions, const int32_t* cand_pos, int32_t* picks,
                                       int32_t* positions, int32_t* n_applied, uint8_t* done) {
+  pdl_entry();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= E) return;
   const int k = n_applied[e];
@@ -350,6 +356,7 @@ __global__ void vec_pipe_post_kernel(int E, int C, int P, int a_max, const doubl
                                      uint8_t* mask, uint8_t* next_mask, double* best_len, int32_t* best_picks,
                                      int64_t* best_episode, float* ep_return, float* finished_return,
                                      int32_t* episodes_done, const int64_t* ctl, int world, int rank) {
+  pdl_entry();
   const int e = blockIdx.x;
   const bool fin = done[e] != 0;
   const int64_t step_base = (ctl[AP_CTL_STEP] * world + rank) * (int64_t)E;
@@ -397,6 +404,7 @@ __global__ void vec_pipe_post_kernel(int E, int C, int P, int a_max, const doubl
 // every row a legal point for the batched length kernel), nb / nc [E] counts.
 __global__ void vec_infer_apply_kernel(int E, int P, int G, const int32_t* actions, int32_t* bnd, int32_t* cut,
                                        int32_t* nb, int32_t* nc, uint8_t* done) {
+  pdl_entry();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= E) return;
   const int a = actions[e];
@@ -422,6 +430,7 @@ __global__ void vec_infer_post_kernel(int E, int P, int G, int D, int S, int64_t
                                       double* best_len, int32_t* best_b, int32_t* best_c, int64_t* best_episode,
                                       float* ep_return, float* finished_return, int32_t* episodes_done,
                                       const int64_t* ctl, int world, int rank) {
+  pdl_entry();
   const int e = blockIdx.x;
   const bool fin = done[e] != 0;
   __shared__ int s_nb, s_nc, s_lb, s_lc;
@@ -481,6 +490,7 @@ __global__ void vec_infer_post_kernel(int E, int P, int G, int D, int S, int64_t
 // mode 0: one learn step done (train counter); mode 1: one vector step done
 // (step counter, ring slot and size after pushing E transitions)
 __global__ void ctl_advance_kernel(int64_t* ctl, int mode, int64_t E, int64_t cap) {
+  pdl_entry();
   if (mode == 0) {
     ctl[AP_CTL_TRAIN] += 1;
   } else {
@@ -494,6 +504,7 @@ __global__ void ctl_advance_kernel(int64_t* ctl, int mode, int64_t E, int64_t ca
 // ctl != nullptr: also counts the finished learn step (ctl[AP_CTL_TRAIN] += 1)
 __global__ void per_update_scaled_kernel(double* scaled, const int32_t* idx, const float* td, int B, double alpha,
                                          int64_t* ctl) {
+  pdl_entry();
   __shared__ int32_t s_idx[1024];  // the batch's indices for the duplicate scan (B <= 1024)
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (ctl && b == 0) ctl[AP_CTL_TRAIN] += 1;
@@ -519,7 +530,7 @@ extern "C" {
 
 int ap_vec_apply(int8_t* seeds, int64_t ld, const int32_t* position, const int32_t* actions, int32_t E, void* stream) {
   if (E <= 0) return AP_OK;
-  vec_apply_kernel<<<(E + 255) / 256, 256, 0, (cudaStream_t)stream>>>(seeds, ld, position, actions, E);
+  launch_pdl(vec_apply_kernel, dim3((E + 255) / 256), dim3(256), 0, (cudaStream_t)stream, seeds, ld, position, actions, E);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
@@ -531,7 +542,7 @@ int ap_vec_post(int32_t E, int32_t n, int64_t ld, int8_t* seeds, const int8_t* s
                 float* ep_return, float* finished_return, int32_t* finished_partitions, int32_t* episodes_done,
                 void* stream) {
   if (E <= 0) return AP_OK;
-  vec_post_kernel<<<(E + 7) / 8, 256, 0, (cudaStream_t)stream>>>(
+  launch_pdl(vec_post_kernel, dim3((E + 7) / 8), dim3(256), 0, (cudaStream_t)stream, 
       E, n, ld, seeds, status, outcome, counts, prev_counts, position, order, order_index, cur_state, lds, next_state,
       rewards, done,
       next_mask, A, ep_return, finished_return, finished_partitions, episodes_done);
@@ -548,7 +559,7 @@ int ap_vec_track_best(int32_t E, int32_t n, int64_t ld, const int8_t* status, co
     set_error("ap_vec_track_best: bad world / rank");
     return AP_ERR_INVALID;
   }
-  vec_track_best_kernel<<<(E + 7) / 8, 256, 0, (cudaStream_t)stream>>>(
+  launch_pdl(vec_track_best_kernel, dim3((E + 7) / 8), dim3(256), 0, (cudaStream_t)stream, 
       E, n, ld, status, outcome, done, finished_partitions, finished_return, step_base, ctl, world, rank,
       best_partitions, best_return, best_episode, best_status);
   AP_CUDA_CHECK(cudaGetLastError());
@@ -561,7 +572,7 @@ int ap_per_push(int32_t E, int32_t S, int32_t A, int64_t slot0, int64_t cap, con
                 float* r_rewards, uint8_t* r_done, uint8_t* r_masks, double* r_prio, const double* max_prio,
                 void* stream) {
   if (E <= 0) return AP_OK;
-  per_push_kernel<<<E, 128, 0, (cudaStream_t)stream>>>(E, S, A, slot0, cap, states, next_states, lds, actions, rewards,
+  launch_pdl(per_push_kernel, dim3(E), dim3(128), 0, (cudaStream_t)stream, E, S, A, slot0, cap, states, next_states, lds, actions, rewards,
                                                        done, masks, r_states, r_next, r_actions, r_rewards, r_done,
                                                        r_masks, r_prio, max_prio, nullptr);
   AP_CUDA_CHECK(cudaGetLastError());
@@ -578,7 +589,7 @@ int ap_per_push_ctl(int32_t E, int32_t S, int32_t A, int64_t cap, const float* s
     return AP_ERR_INVALID;
   }
   if (E <= 0) return AP_OK;
-  per_push_kernel<<<E, 128, 0, (cudaStream_t)stream>>>(E, S, A, 0, cap, states, next_states, lds, actions, rewards,
+  launch_pdl(per_push_kernel, dim3(E), dim3(128), 0, (cudaStream_t)stream, E, S, A, 0, cap, states, next_states, lds, actions, rewards,
                                                        done, masks, r_states, r_next, r_actions, r_rewards, r_done,
                                                        r_masks, r_prio, max_prio, ctl);
   AP_CUDA_CHECK(cudaGetLastError());
@@ -614,7 +625,7 @@ int ap_vec_pipe_apply(int32_t E, int32_t P, const int32_t* actions, const int32_
     return AP_ERR_INVALID;
   }
   if (E == 0) return AP_OK;
-  vec_pipe_apply_kernel<<<(E + 255) / 256, 256, 0, (cudaStream_t)stream>>>(E, P, actions, cand_pos, picks, positions,
+  launch_pdl(vec_pipe_apply_kernel, dim3((E + 255) / 256), dim3(256), 0, (cudaStream_t)stream, E, P, actions, cand_pos, picks, positions,
                                                                            n_applied, done);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
@@ -633,7 +644,7 @@ int ap_vec_pipe_post(int32_t E, int32_t C, int32_t P, int32_t a_max, const doubl
   }
   if (E == 0) return AP_OK;
   // one CTA per env; episodes finishing at this step get global ids (step * world + rank) * E + e
-  vec_pipe_post_kernel<<<E, 128, 0, (cudaStream_t)stream>>>(
+  launch_pdl(vec_pipe_post_kernel, dim3(E), dim3(128), 0, (cudaStream_t)stream, 
       E, C, P, a_max, length, feasible, done, reward_shape, dummy_pos, rewards, picks, positions, n_applied,
       applied_state, mask, next_mask, best_len, best_picks, best_episode, ep_return, finished_return, episodes_done,
       ctl, world, rank);
@@ -648,7 +659,7 @@ int ap_vec_infer_apply(int32_t E, int32_t P, int32_t G, const int32_t* actions, 
     return AP_ERR_INVALID;
   }
   if (E == 0) return AP_OK;
-  vec_infer_apply_kernel<<<(E + 255) / 256, 256, 0, (cudaStream_t)stream>>>(E, P, G, actions, bnd, cut, nb, nc, done);
+  launch_pdl(vec_infer_apply_kernel, dim3((E + 255) / 256), dim3(256), 0, (cudaStream_t)stream, E, P, G, actions, bnd, cut, nb, nc, done);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
@@ -665,7 +676,7 @@ int ap_vec_infer_post(int32_t E, int32_t P, int32_t G, int32_t D, int32_t S, int
     return AP_ERR_INVALID;
   }
   if (E == 0) return AP_OK;
-  vec_infer_post_kernel<<<E, 128, 0, (cudaStream_t)stream>>>(
+  launch_pdl(vec_infer_post_kernel, dim3(E), dim3(128), 0, (cudaStream_t)stream, 
       E, P, G, D, S, ld_state, length, done, dummy_b, dummy_c, band_b, band_c, rewards, bnd, cut, nb, nc, mask,
       next_mask, state,
       best_len, best_b, best_c, best_episode, ep_return, finished_return, episodes_done, ctl, world, rank);
@@ -678,7 +689,7 @@ int ap_vec_ctl_advance(int64_t* ctl, int32_t mode, int64_t E, int64_t cap, void*
     set_error("ap_vec_ctl_advance: bad arguments");
     return AP_ERR_INVALID;
   }
-  ctl_advance_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(ctl, mode, E, cap);
+  launch_pdl(ctl_advance_kernel, dim3(1), dim3(1), 0, (cudaStream_t)stream, ctl, mode, E, cap);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
@@ -686,7 +697,7 @@ int ap_vec_ctl_advance(int64_t* ctl, int32_t mode, int64_t E, int64_t cap, void*
 int ap_per_update_scaled(double* scaled, const int32_t* indices, const float* td, int32_t B, double alpha,
                          void* stream) {
   if (B <= 0) return AP_OK;
-  per_update_scaled_kernel<<<(B + 127) / 128, 128, 0, (cudaStream_t)stream>>>(scaled, indices, td, B, alpha,
+  launch_pdl(per_update_scaled_kernel, dim3((B + 127) / 128), dim3(128), 0, (cudaStream_t)stream, scaled, indices, td, B, alpha,
                                                                              nullptr);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
@@ -698,7 +709,7 @@ int ap_per_update_scaled_ctl(double* scaled, const int32_t* indices, const float
     set_error("ap_per_update_scaled_ctl: bad arguments");
     return AP_ERR_INVALID;
   }
-  per_update_scaled_kernel<<<(B + 127) / 128, 128, 0, (cudaStream_t)stream>>>(scaled, indices, td, B, alpha, ctl);
+  launch_pdl(per_update_scaled_kernel, dim3((B + 127) / 128), dim3(128), 0, (cudaStream_t)stream, scaled, indices, td, B, alpha, ctl);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
