@@ -224,6 +224,7 @@ __device__ inline void stage_metrics_dev(const PipeDev& pd, const double* cost, 
 // fits (stage_smem), so the per-tuple sequential sums read it with broadcast loads.
 __global__ void metrics_kernel(PipeDev pd, const int32_t* pivots, int64_t batch, int P, double scale, double* comp,
                                double* act, double* param, int32_t* nvars, int stage_smem) {
+  pdl_entry();
   extern __shared__ double s_mcost[];
   const double* cost = pd.cost;
   if (stage_smem) {
@@ -249,6 +250,7 @@ __global__ void metrics_kernel(PipeDev pd, const int32_t* pivots, int64_t batch,
 __global__ void length_kernel(Topo t, int K, int M, int64_t batch, const double* comp, const double* act,
                               const double* param, int32_t* cuts, int given, double mem, double opt, int exact,
                               double* len, uint8_t* feas) {
+  pdl_entry();
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < batch; b += (int64_t)gridDim.x * blockDim.x) {
     const double* c = comp + b * K;
     const double* a = act + b * K;
@@ -276,6 +278,7 @@ __global__ void length_kernel(Topo t, int K, int M, int64_t batch, const double*
 // proportional device cut lies in the allowed set and trainables sit on both sides
 __global__ void candidates_kernel(int F, const double* prefix, double total, const int32_t* cp_prefix, int32_t cp_total,
                                   Topo t, int radius, uint8_t* allowed) {
+  pdl_entry();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < F - 1; i += gridDim.x * blockDim.x) {
     double two[2] = {prefix[i], total - prefix[i]};
     int counts[2];
@@ -324,6 +327,7 @@ __device__ inline void train_features(const Topo& t, int K, const double* c, con
 // block scan by warp ballots.
 __global__ void __launch_bounds__(1024) train_compact_kernel(const uint8_t* mask, int C, int64_t E, int32_t* list,
                                                              int32_t* count, double* state) {
+  pdl_entry();
   __shared__ int s_warp[32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nwarps = blockDim.x >> 5;
   for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
@@ -371,6 +375,7 @@ __global__ void __launch_bounds__(128) train_cand_kernel(PipeDev pd, Topo t, con
                                                          const int32_t* applied, int A, const int32_t* list,
                                                          const int32_t* count, int64_t E, double scale,
                                                          double* state) {
+  pdl_entry();
   extern __shared__ double s_cost[];
   for (int i = threadIdx.x; i < pd.F; i += blockDim.x) s_cost[i] = pd.cost[i];
   __syncthreads();
@@ -490,6 +495,7 @@ __global__ void __launch_bounds__(128) train_cand_kernel(PipeDev pd, Topo t, con
 // R[e][i]; train_tail_kernel: the candidates' tail chains + features.
 __global__ void train_prefix_kernel(PipeDev pd, const int32_t* cand_pos, const int32_t* applied, int A, int64_t E,
                                     double* fixed, double* R) {
+  pdl_entry();
   extern __shared__ double s_pc[];
   for (int i = threadIdx.x; i < pd.F; i += blockDim.x) s_pc[i] = pd.cost[i];
   __syncthreads();
@@ -532,6 +538,7 @@ __global__ void __launch_bounds__(128) train_tail_kernel(PipeDev pd, Topo t, con
                                                          const int32_t* applied, int A, const int32_t* list,
                                                          const int32_t* count, int64_t E, double scale,
                                                          const double* fixed, const double* R, double* state) {
+  pdl_entry();
   extern __shared__ double s_cost[];
   for (int i = threadIdx.x; i < pd.F; i += blockDim.x) s_cost[i] = pd.cost[i];
   __syncthreads();
@@ -634,6 +641,7 @@ __global__ void __launch_bounds__(128) train_tail_kernel(PipeDev pd, Topo t, con
 // indices in the same order (pipecost.py:72-102), so a lookup is
 // bit-identical to re-summing; T[a][b] = 0.0 when the range is empty.
 __global__ void train_table_kernel(PipeDev pd, const int32_t* cand_pos, int C, double* T) {
+  pdl_entry();
   const int64_t W = C + 1;
   for (int a = blockIdx.x * blockDim.x + threadIdx.x; a <= C; a += gridDim.x * blockDim.x) {
     double* row = T + a * W;
@@ -690,6 +698,7 @@ __device__ __forceinline__ void cand_features(const PipeDev& pd, const Topo& t, 
 }
 
 __global__ void index_positions_kernel(const int32_t* cand_pos, int C, int F, int32_t* idx_of_pos) {
+  pdl_entry();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c < C && cand_pos[c] >= 0 && cand_pos[c] < F) idx_of_pos[cand_pos[c]] = c;
 }
@@ -701,6 +710,7 @@ __global__ void index_positions_kernel(const int32_t* cand_pos, int C, int F, in
 __global__ void metrics_tab_kernel(PipeDev pd, const int32_t* idx_of_pos, int C, const double* T,
                                    const int32_t* pivots, int64_t batch, int P, double scale, double* comp,
                                    double* act, double* param, int32_t* nvars) {
+  pdl_entry();
   const int64_t W = C + 1;
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < batch; b += (int64_t)gridDim.x * blockDim.x) {
     int cuts[kMaxStages];
@@ -760,6 +770,7 @@ __global__ void __launch_bounds__(256, AP_PP_TAB_MINB) train_state_tab_kernel(Pi
                                                               const uint8_t* mask, int64_t E, double scale,
                                                               double* state, float* f32a, int64_t lda32,
                                                               float* f32b, int64_t ldb32) {
+  pdl_entry();
   __shared__ FixedStages fs;
   __shared__ double s_max[2][32];
   const int64_t W = C + 1;
@@ -844,6 +855,7 @@ __global__ void __launch_bounds__(256, AP_PP_TAB_MINB) train_state_tab_kernel(Pi
 
 // block normalisation and one-hot (envs.py:398-404): one CTA per env
 __global__ void train_norm_kernel(int C, const int32_t* applied, int A, int64_t E, double* state) {
+  pdl_entry();
   __shared__ double s_max[2][32];
   for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
     double* st = state + e * 4 * (int64_t)C;
@@ -912,6 +924,7 @@ __device__ inline double infer_point(const double* arr, int G, const Topo& t, in
 
 __global__ void infer_kernel(const double* arr, int G, Topo t, int K, int M, const int32_t* bnd, const int32_t* cut,
                              int64_t batch, double* len) {
+  pdl_entry();
   for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < batch; b += (int64_t)gridDim.x * blockDim.x) {
     int bb[kMaxStages], cc[kMaxStages];
     for (int s = 0; s + 1 < K; ++s) {
@@ -925,6 +938,7 @@ __global__ void infer_kernel(const double* arr, int G, Topo t, int K, int M, con
 // exhaustive search: every (b-combo, c-combo), first-wins argmin per block
 __global__ void infer_search_kernel(const double* arr, int G, Topo t, int K, int M, const int32_t* bcomb, int64_t nb,
                                     const int32_t* ccomb, int64_t nc, double* blk_len, int64_t* blk_idx) {
+  pdl_entry();
   __shared__ double s_len[256];
   __shared__ int64_t s_idx[256];
   double best = INFINITY;
@@ -986,6 +1000,7 @@ __global__ void __launch_bounds__(32 * kTabWarps) infer_search_tab_kernel(const 
                                                                           int64_t nc, double* blk_len,
                                                                           int64_t* blk_idx,
                                                                           unsigned long long* n_valid) {
+  pdl_entry();
   extern __shared__ double s_tab[];
   constexpr int kPerWarp = K * kTabN * 3 + 2 * K;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1116,7 +1131,7 @@ int launch_infer_tab(const double* arr, int G, const Topo& t, int M, const int32
   const size_t smem = (size_t)kTabWarps * (K * kTabN * 3 + 2 * K) * sizeof(double);
   auto k = infer_search_tab_kernel<K>;
   AP_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k<<<blocks, 32 * kTabWarps, smem, s>>>(arr, G, t, M, d_band, d_off, nprod, d_w, nc, d_len, d_idx, d_valid);
+  launch_pdl(k, dim3(blocks), dim3(32 * kTabWarps), smem, s, arr, G, t, M, d_band, d_off, nprod, d_w, nc, d_len, d_idx, d_valid);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
@@ -1341,7 +1356,7 @@ int ap_pipe_candidates(ap_pipe_t p, const ap_topology* topo, int32_t num_stages,
   if ((rc = p->ensure()) != AP_OK) return rc;
   (void)num_stages;
   const Topo t = make_topo(topo);
-  candidates_kernel<<<grid_for(p->F, 256), 256, 0, (cudaStream_t)stream>>>(p->F, p->d_prefix.ptr, p->total,
+  launch_pdl(candidates_kernel, dim3(grid_for(p->F, 256)), dim3(256), 0, (cudaStream_t)stream, p->F, p->d_prefix.ptr, p->total,
                                                                           p->d_cp_prefix.ptr, p->cp_total, t, radius,
                                                                           allowed);
   AP_CUDA_CHECK(cudaGetLastError());
@@ -1361,7 +1376,7 @@ int ap_pipe_metrics(ap_pipe_t p, const int32_t* pivots, int64_t batch, int32_t P
   const size_t msmem = (size_t)p->F * sizeof(double);
   const int stage = msmem <= 200 * 1024 ? 1 : 0;
   if (stage) AP_CUDA_CHECK(cudaFuncSetAttribute(metrics_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem));
-  metrics_kernel<<<grid_for(batch, 32), 32, stage ? msmem : 0, (cudaStream_t)stream>>>(p->dev(), pivots, batch, P,
+  launch_pdl(metrics_kernel, dim3(grid_for(batch, 32)), dim3(32), stage ? msmem : 0, (cudaStream_t)stream, p->dev(), pivots, batch, P,
                                                                                        1.0 + bwm, comp, act, param,
                                                                                        nvars, stage);
   AP_CUDA_CHECK(cudaGetLastError());
@@ -1381,7 +1396,7 @@ int ap_pipe_metrics_bound(ap_pipe_t p, const int32_t* cand_pos, int32_t C, const
   int rc = p->ensure();
   if (rc != AP_OK) return rc;
   if (batch == 0) return AP_OK;
-  metrics_tab_kernel<<<grid_for(batch, 128), 128, 0, (cudaStream_t)stream>>>(
+  launch_pdl(metrics_tab_kernel, dim3(grid_for(batch, 128)), dim3(128), 0, (cudaStream_t)stream, 
       p->dev(), bnd->idx_of_pos, C, bnd->tab, pivots, batch, P, 1.0 + bwm, comp, act, param, nvars);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
@@ -1398,7 +1413,7 @@ int ap_pipe_length(const ap_topology* topo, int32_t K, int32_t M, int64_t batch,
     return AP_ERR_INVALID;
   }
   if (batch == 0) return AP_OK;
-  length_kernel<<<grid_for(batch, 128), 128, 0, (cudaStream_t)stream>>>(make_topo(topo), K, M, batch, comp, act, param,
+  launch_pdl(length_kernel, dim3(grid_for(batch, 128)), dim3(128), 0, (cudaStream_t)stream, make_topo(topo), K, M, batch, comp, act, param,
                                                                          cuts, given, mem, opt, python_floats, len,
                                                                          feas);
   AP_CUDA_CHECK(cudaGetLastError());
@@ -1433,10 +1448,10 @@ int ap_pipe_train_table(ap_pipe_t p, const int32_t* cand_pos, int32_t C, void* s
   }
   // (re)built from the list's current contents
   const auto* bnd = p->binding(cand_pos, C);
-  train_table_kernel<<<(int)((W + 127) / 128), 128, 0, (cudaStream_t)stream>>>(p->dev(), cand_pos, C, tab);
+  launch_pdl(train_table_kernel, dim3((int)((W + 127) / 128)), dim3(128), 0, (cudaStream_t)stream, p->dev(), cand_pos, C, tab);
   AP_CUDA_CHECK(cudaGetLastError());
   AP_CUDA_CHECK(cudaMemsetAsync(bnd->idx_of_pos, 0xff, (size_t)p->F * sizeof(int32_t), (cudaStream_t)stream));
-  index_positions_kernel<<<(C + 255) / 256, 256, 0, (cudaStream_t)stream>>>(cand_pos, C, p->F, bnd->idx_of_pos);
+  launch_pdl(index_positions_kernel, dim3((C + 255) / 256), dim3(256), 0, (cudaStream_t)stream, cand_pos, C, p->F, bnd->idx_of_pos);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
@@ -1444,6 +1459,7 @@ int ap_pipe_train_table(ap_pipe_t p, const int32_t* cand_pos, int32_t C, void* s
 namespace apb {
 __global__ void state_to_f32_kernel(const double* state, int64_t E, int W, float* f32a, int64_t lda32, float* f32b,
                                     int64_t ldb32) {
+  pdl_entry();
   const int64_t total = E * (int64_t)W;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = i / W;
@@ -1492,7 +1508,7 @@ int train_state_impl(ap_pipe_t p, const ap_topology* topo, const int32_t* cand_p
   const Topo t = make_topo(topo);
   const double* tab = std::getenv("AP_PP_NO_TABLE") ? nullptr : p->table_for(cand_pos, C);
   if (tab) {  // bound candidate list: stage sums are lookups (one launch)
-    train_state_tab_kernel<<<(int)std::min<int64_t>(E, 148 * 8), 256, 0, (cudaStream_t)stream>>>(
+    launch_pdl(train_state_tab_kernel, dim3((int)std::min<int64_t>(E, 148 * 8)), dim3(256), 0, (cudaStream_t)stream, 
         p->dev(), t, cand_pos, C, tab, applied, A, mask, E, 1.0 + bwm, state, f32a, lda32, f32b, ldb32);
     AP_CUDA_CHECK(cudaGetLastError());
     return AP_OK;
@@ -1505,7 +1521,7 @@ int train_state_impl(ap_pipe_t p, const ap_topology* topo, const int32_t* cand_p
   }
   AP_CUDA_CHECK(cudaFuncSetAttribute(train_cand_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if ((rc = p->ensure_train_scratch(E * (int64_t)C, E)) != AP_OK) return rc;
-  train_compact_kernel<<<(int)std::min<int64_t>(E, 148 * 4), 1024, 0, (cudaStream_t)stream>>>(
+  launch_pdl(train_compact_kernel, dim3((int)std::min<int64_t>(E, 148 * 4)), dim3(1024), 0, (cudaStream_t)stream, 
       mask, C, E, p->d_list, p->d_count, state);
   AP_CUDA_CHECK(cudaGetLastError());
   const int64_t threads = E * (int64_t)((C + kCandPerWarp - 1) / kCandPerWarp) * 32;
@@ -1514,20 +1530,20 @@ int train_state_impl(ap_pipe_t p, const ap_topology* topo, const int32_t* cand_p
     if ((rc = p->ensure_prefix_scratch(E)) != AP_OK) return rc;
     AP_CUDA_CHECK(cudaFuncSetAttribute(train_prefix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     AP_CUDA_CHECK(cudaFuncSetAttribute(train_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    train_prefix_kernel<<<(int)std::min<int64_t>(E, 148 * 8), 32, smem, (cudaStream_t)stream>>>(
+    launch_pdl(train_prefix_kernel, dim3((int)std::min<int64_t>(E, 148 * 8)), dim3(32), smem, (cudaStream_t)stream, 
         p->dev(), cand_pos, applied, A, E, p->d_fixed, p->d_R);
     AP_CUDA_CHECK(cudaGetLastError());
-    train_tail_kernel<<<grid_for(threads, 128), 128, smem, (cudaStream_t)stream>>>(
+    launch_pdl(train_tail_kernel, dim3(grid_for(threads, 128)), dim3(128), smem, (cudaStream_t)stream, 
         p->dev(), t, cand_pos, C, applied, A, p->d_list, p->d_count, E, 1.0 + bwm, p->d_fixed, p->d_R, state);
   } else {  // one full sweep of the cost array per candidate (AP_PP_FULL=1)
-    train_cand_kernel<<<grid_for(threads, 128), 128, smem, (cudaStream_t)stream>>>(
+    launch_pdl(train_cand_kernel, dim3(grid_for(threads, 128)), dim3(128), smem, (cudaStream_t)stream, 
         p->dev(), t, cand_pos, C, applied, A, p->d_list, p->d_count, E, 1.0 + bwm, state);
   }
   AP_CUDA_CHECK(cudaGetLastError());
-  train_norm_kernel<<<(int)std::min<int64_t>(E, 148 * 8), 256, 0, (cudaStream_t)stream>>>(C, applied, A, E, state);
+  launch_pdl(train_norm_kernel, dim3((int)std::min<int64_t>(E, 148 * 8)), dim3(256), 0, (cudaStream_t)stream, C, applied, A, E, state);
   AP_CUDA_CHECK(cudaGetLastError());
   if (f32a) {
-    state_to_f32_kernel<<<grid_for(E * 4 * (int64_t)C, 256), 256, 0, (cudaStream_t)stream>>>(state, E, 4 * C, f32a,
+    launch_pdl(state_to_f32_kernel, dim3(grid_for(E * 4 * (int64_t)C, 256)), dim3(256), 0, (cudaStream_t)stream, state, E, 4 * C, f32a,
                                                                                           lda32, f32b, ldb32);
     AP_CUDA_CHECK(cudaGetLastError());
   }
@@ -1544,7 +1560,7 @@ int ap_infer_length(const double* arrays, int32_t G, const ap_topology* topo, in
     return AP_ERR_INVALID;
   }
   if (batch == 0) return AP_OK;
-  infer_kernel<<<grid_for(batch, 128), 128, 0, (cudaStream_t)stream>>>(arrays, G, make_topo(topo), K, M, bnd, cut,
+  launch_pdl(infer_kernel, dim3(grid_for(batch, 128)), dim3(128), 0, (cudaStream_t)stream, arrays, G, make_topo(topo), K, M, bnd, cut,
                                                                         batch, len);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
@@ -1673,7 +1689,7 @@ extern "C" int ap_infer_search(const double* arrays, int32_t G, const ap_topolog
     AP_CUDA_CHECK(cudaMalloc(&d_c, cc.size() * sizeof(int32_t)));
     AP_CUDA_CHECK(cudaMemcpyAsync(d_b, bc.data(), bc.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
     AP_CUDA_CHECK(cudaMemcpyAsync(d_c, cc.data(), cc.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-    infer_search_kernel<<<blocks, 256, 0, s>>>(arrays, G, t, K, M, d_b, nb, d_c, nc, d_len, d_idx);
+    launch_pdl(infer_search_kernel, dim3(blocks), dim3(256), 0, s, arrays, G, t, K, M, d_b, nb, d_c, nc, d_len, d_idx);
     AP_CUDA_CHECK(cudaGetLastError());
   }
   std::vector<double> hl(blocks);

@@ -78,6 +78,7 @@ __device__ __forceinline__ int class_status(const uint32_t* P, const uint32_t* R
 // per-warp scratch still fits in shared memory)
 template <bool kVecSlots, bool kTable>
 __global__ void __launch_bounds__(kThreads) propagate_kernel(PropParams p) {
+  pdl_entry();
   extern __shared__ __align__(16) uint8_t smem[];
   const int32_t* slot_class = p.slot_class;
   const int32_t* dec_class = p.dec_class;
@@ -219,6 +220,7 @@ __global__ void __launch_bounds__(kThreads) propagate_kernel(PropParams p) {
 // bitsets plus (kTable) a byte status table per CTA in shared memory.
 template <bool kVecSlots, bool kTable>
 __global__ void __launch_bounds__(kThreads) propagate_cta_kernel(PropParams p) {
+  pdl_entry();
   extern __shared__ __align__(16) uint8_t smem[];
   __shared__ int s_red[kWarps][4];
   const int32_t* slot_class = p.slot_class;
@@ -417,6 +419,7 @@ __global__ void trace_kernel(const int32_t* prog, int64_t prog_len, const int32_
                              const int64_t* dec_slots, const int8_t* seeds, int32_t D, int8_t* st,
                              const int64_t* base, const int32_t* owner, int64_t S, int64_t cap, bool has_init,
                              int32_t* result) {
+  pdl_entry();
   TraceState t{st, base, owner, -1};
   if (!has_init)
     for (int64_t s = 0; s < S; ++s) st[s] = -1;
@@ -581,7 +584,7 @@ int launch_propagate(const GraphTables* g, const DecisionTables* d, const int8_t
       AP_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cper, ck, kThreads, (size_t)csmem));
       const int cgrid = (int)std::min<int64_t>(batch, (int64_t)g_num_sms * std::max(cper, 1));
       p.stage_tables = 0;
-      ck<<<cgrid, kThreads, (size_t)csmem, stream>>>(p);
+      launch_pdl(ck, dim3(cgrid), dim3(kThreads), (size_t)csmem, stream, p);
       AP_CUDA_CHECK(cudaGetLastError());
       return AP_OK;
     }
@@ -620,7 +623,7 @@ int launch_propagate(const GraphTables* g, const DecisionTables* d, const int8_t
     }
     p.gscratch = g->d_scratch;
   }
-  kern<<<grid, kThreads, (size_t)smem, stream>>>(p);
+  launch_pdl(kern, dim3(grid), dim3(kThreads), (size_t)smem, stream, p);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
@@ -640,7 +643,7 @@ int run_trace(const GraphTables* g, const DecisionTables* d, const int8_t* seeds
   for (int32_t q = 0; q < g->num_instr; ++q)
     max_rank = std::max<int>(max_rank, (int)(g->slot_base[q + 1] - g->slot_base[q]));
   const int64_t cap = std::max<int64_t>(2, (int64_t)g->num_instr * max_rank + 2);  // sharding.py:251-252
-  trace_kernel<<<1, 1, 0, stream>>>(g->d_program.ptr, (int64_t)g->program.size(), g->d_forced_list.ptr,
+  launch_pdl(trace_kernel, dim3(1), dim3(1), 0, stream, g->d_program.ptr, (int64_t)g->program.size(), g->d_forced_list.ptr,
                                     (int64_t)g->forced_list.size(), d->d_slots.ptr, d_seeds, d->n, d_state,
                                     g->d_slot_base.ptr, g->d_slot_owner.ptr, S, cap, init_host != nullptr, d_res);
   AP_CUDA_CHECK(cudaGetLastError());

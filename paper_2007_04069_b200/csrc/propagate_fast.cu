@@ -302,6 +302,7 @@ __device__ __forceinline__ void seed_masks(uint4 s, uint32_t* xp, uint32_t* xr, 
 // MAXCH: 16-byte seed chunks per lane; NW: 32-bit class words (classes <= 32*NW)
 template <int MAXCH, int NW>
 __global__ void __launch_bounds__(kThreadsF, AP_K1_MIN_BLOCKS) propagate_fast_kernel(FastParams p) {
+  pdl_entry();
   extern __shared__ __align__(16) uint8_t smem[];
   // stage the static tables
   auto stage = [&](int off, const void* src, int64_t bytes) {
@@ -579,7 +580,7 @@ int launch_fast_t(const FastParams& p, int64_t smem, cudaStream_t stream) {
   per_sm = std::max(per_sm, 1);
   const int64_t want = (p.batch + kWarpsF - 1) / kWarpsF;
   const int grid = (int)std::min<int64_t>(want, (int64_t)num_sms * per_sm);
-  kern<<<grid, kThreadsF, (size_t)smem, stream>>>(p);
+  launch_pdl(kern, dim3(grid), dim3(kThreadsF), (size_t)smem, stream, p);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
