@@ -217,6 +217,15 @@ int ap_pipe_train_state_ex(ap_pipe_t p, const ap_topology* topo, const int32_t* 
                            double backward_multiplier, double* state_dev, float* state_f32, int64_t ld_f32,
                            float* state_f32_b, int64_t ld_f32_b, void* stream);
 
+/* PP-infer data plane: num_envs synthetic uniform
+ * profiles at once, bit-identical to generate_environment("uniform", n, seed)
+ * (dataproc.py:123-145 -> build_environment_arrays :99-120 -> coarsen :79-96).
+ * pcg_states [E, 4] uint64 = each seed's PCG64 (state hi, state lo, inc hi,
+ * inc lo) as numpy's default_rng(seed) initialises it; arrays_out [E, 3, G]
+ * fp64 = the coarsened, jointly scaled C, A, W arrays.  n <= 8533. */
+int ap_generate_uniform_envs(const uint64_t* pcg_states, int64_t num_envs, int32_t n, int32_t granularity,
+                             double* arrays_out, void* stream);
+
 /* Binds a candidate list to the handle: builds (once, outside stream capture)
  * the table of every stage sum a plan over these candidates can have --
  * the naive sum of cost[start .. end] for each pair of candidate boundaries,

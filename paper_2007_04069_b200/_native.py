@@ -113,6 +113,7 @@ SIGNATURES: dict[str, tuple] = {
                                       _VP]),
     "ap_pipe_train_state": (ctypes.c_int, [_VP, _TOPO, _VP, _I32, _VP, _I32, _VP, _I64, _F64, _VP, _VP]),
     "ap_pipe_train_table": (ctypes.c_int, [_VP, _VP, _I32, _VP]),
+    "ap_generate_uniform_envs": (ctypes.c_int, [_VP, _I64, _I32, _I32, _VP, _VP]),
     "ap_pipe_train_state_ex": (ctypes.c_int, [_VP, _TOPO, _VP, _I32, _VP, _I32, _VP, _I64, _F64, _VP, _VP, _I64, _VP, _I64,
                                               _VP]),
     "ap_infer_length": (ctypes.c_int, [_VP, _I32, _TOPO, _I32, _I32, _VP, _VP, _I64, _VP, _VP]),

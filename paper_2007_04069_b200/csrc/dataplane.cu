@@ -1,0 +1,136 @@
+// PP-infer data plane on the device: batched synthetic
+// profiles, bit-identical to the reference's generate_environment for the
+// uniform distribution (reference dataproc.py:123-145, build_environment_arrays
+// dataproc.py:99-120, coarsen dataproc.py:79-96).
+//
+// numpy's default_rng(seed) is PCG64 (XSL-RR 128/64): each draw advances the
+// 128-bit LCG state = state * M + inc and outputs rotr64(hi ^ lo, state >> 122)
+// of the new state; Generator.uniform(0, 1) is (x >> 11) * 2^-53.  The host
+// passes each environment's initial (state, inc) as numpy computes them from
+// the seed (SeedSequence); the device reproduces the stream.  The three draws
+// c, a, w are stream positions [0, n), [n, 2n), [2n, 3n): every thread jumps
+// ahead (PCG's O(log k) advance) to its slice and steps sequentially.
+// Then, as the reference: naive sequential cumsum of c and w, right-endpoint
+// coarsening to G points, joint scaling by max(cs, as, ws, 0).
+//
+// normal / binomial profiles use numpy's ziggurat / BTPE rejection samplers,
+// which consume a data-dependent number of draws; they stay on the host.
+#include <algorithm>
+#include <cstdint>
+
+#include "engine.h"
+
+namespace apb {
+namespace {
+
+using u128 = unsigned __int128;
+
+__device__ __forceinline__ u128 pcg_mult() {
+  return ((u128)0x2360ED051FC65DA4ULL << 64) | (u128)0x4385DF649FCCF645ULL;
+}
+
+// state after `delta` steps (PCG advance: repeated squaring of the affine map)
+__device__ u128 pcg_advance(u128 state, u128 inc, uint64_t delta) {
+  u128 cur_mult = pcg_mult(), cur_plus = inc, acc_mult = 1, acc_plus = 0;
+  while (delta > 0) {
+    if (delta & 1) {
+      acc_mult *= cur_mult;
+      acc_plus = acc_plus * cur_mult + cur_plus;
+    }
+    cur_plus = (cur_mult + 1) * cur_plus;
+    cur_mult *= cur_mult;
+    delta >>= 1;
+  }
+  return acc_mult * state + acc_plus;
+}
+
+__device__ __forceinline__ double pcg_next_double(u128& state, u128 inc) {
+  state = state * pcg_mult() + inc;
+  const uint64_t hi = (uint64_t)(state >> 64), lo = (uint64_t)state;
+  const unsigned rot = (unsigned)(state >> 122);
+  const uint64_t x = hi ^ lo;
+  const uint64_t r = (x >> rot) | (x << ((64u - rot) & 63u));
+  return (double)(r >> 11) * (1.0 / 9007199254740992.0);
+}
+
+constexpr int kGenThreads = 256;
+
+__global__ void __launch_bounds__(kGenThreads) uniform_env_kernel(const uint64_t* seeds4, int64_t E, int n, int G,
+                                                                 double* out) {
+  extern __shared__ double s_draw[];  // [3n]: c, a, w
+  __shared__ double s_max[kGenThreads / 32];
+  for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
+    const uint64_t* q = seeds4 + 4 * e;
+    const u128 state0 = ((u128)q[0] << 64) | (u128)q[1];
+    const u128 inc = ((u128)q[2] << 64) | (u128)q[3];
+    const int total = 3 * n;
+    const int chunk = (total + kGenThreads - 1) / kGenThreads;
+    const int lo = threadIdx.x * chunk, hi = min(total, lo + chunk);
+    if (lo < hi) {
+      u128 st = pcg_advance(state0, inc, (uint64_t)lo);
+      for (int k = lo; k < hi; ++k) s_draw[k] = pcg_next_double(st, inc);
+    }
+    __syncthreads();
+    // np.cumsum (sequential) of c and w, one thread each
+    if (threadIdx.x < 2) {
+      double* x = s_draw + (threadIdx.x == 0 ? 0 : 2 * n);
+      double acc = x[0];
+      for (int i = 1; i < n; ++i) {
+        acc = acc + x[i];
+        x[i] = acc;
+      }
+    }
+    __syncthreads();
+    // coarsen (right endpoints; arrays shorter than G are padded with their last value)
+    double m = 0.0;
+    double* o = out + e * 3 * (int64_t)G;
+    for (int i = threadIdx.x; i < G; i += kGenThreads) {
+      const int src = n >= G ? (int)(((int64_t)(i + 1) * n) / G - 1) : min(i, n - 1);
+      const double c = s_draw[src], a = s_draw[n + src], w = s_draw[2 * n + src];
+      o[i] = c;
+      o[G + i] = a;
+      o[2 * G + i] = w;
+      m = fmax(m, fmax(c, fmax(a, w)));
+    }
+    for (int off = 16; off; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = m;
+    __syncthreads();
+    double peak = 0.0;
+    for (int k = 0; k < kGenThreads / 32; ++k) peak = fmax(peak, s_max[k]);
+    if (peak > 0.0)
+      for (int i = threadIdx.x; i < 3 * G; i += kGenThreads) o[i] = o[i] / peak;
+    __syncthreads();  // s_draw / s_max reused by the next environment
+  }
+}
+
+}  // namespace
+}  // namespace apb
+
+using namespace apb;
+
+extern "C" {
+
+int ap_generate_uniform_envs(const uint64_t* pcg_states, int64_t num_envs, int32_t n, int32_t granularity,
+                             double* arrays_out, void* stream) {
+  if (num_envs < 0 || n < 1 || granularity < 1 || (num_envs > 0 && (!pcg_states || !arrays_out))) {
+    set_error("ap_generate_uniform_envs: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  const size_t smem = (size_t)3 * n * sizeof(double);
+  if (smem > 200 * 1024) {
+    set_error("ap_generate_uniform_envs: n > 8533 does not fit the shared-memory draw buffer");
+    return AP_ERR_UNSUPPORTED;
+  }
+  if (num_envs == 0) return AP_OK;
+  AP_CUDA_CHECK(cudaFuncSetAttribute(uniform_env_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev = 0, sms = 148;
+  AP_CUDA_CHECK(cudaGetDevice(&dev));
+  AP_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t grid = std::min<int64_t>(num_envs, (int64_t)sms * 8);
+  uniform_env_kernel<<<(unsigned)grid, kGenThreads, smem, (cudaStream_t)stream>>>(pcg_states, num_envs, n, granularity,
+                                                                                  arrays_out);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+}  // extern "C"

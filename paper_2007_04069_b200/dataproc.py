@@ -69,3 +69,37 @@ def generate_environment(distribution: str, n: int, seed: int, granularity: int 
 
     c, a, w = draw(), draw(), draw()
     return build_environment_arrays(c, a, w, granularity)
+
+
+def pcg64_states(seeds) -> np.ndarray:
+    """[E, 4] uint64: numpy default_rng(seed)'s PCG64 (state hi, state lo, inc hi, inc lo) per seed."""
+    seeds = list(seeds)
+    out = np.empty((len(seeds), 4), dtype=np.uint64)
+    mask = (1 << 64) - 1
+    for i, s in enumerate(seeds):
+        st = np.random.PCG64(s).state["state"]
+        out[i] = (st["state"] >> 64, st["state"] & mask, st["inc"] >> 64, st["inc"] & mask)
+    return out
+
+
+def generate_environments_device(distribution: str, n: int, seeds, granularity: int = GRANULARITY, states=None):
+    """generate_environment(distribution, n, s) for every seed s at once on the GPU
+    (ap_generate_uniform_envs): a CUDA fp64 tensor [E, 3, G] of the scaled C, A, W arrays,
+    bit-identical to the host path.  Only the uniform profile: numpy's normal / binomial
+    samplers consume a data-dependent number of draws (ziggurat / BTPE) and stay on the host.
+    `states` may pass precomputed pcg64_states(seeds)."""
+    import torch
+
+    from . import _native
+
+    if distribution != "uniform":
+        raise ProfileError("the device generator covers the uniform profile (normal / binomial: generate_environment)")
+    if n < 1:
+        raise ProfileError("environment length must be >= 1")
+    st = pcg64_states(seeds) if states is None else np.asarray(states, dtype=np.uint64)
+    lib = _native.require_device()
+    d_st = torch.from_numpy(st.view(np.int64)).cuda()
+    out = torch.empty((st.shape[0], 3, granularity), dtype=torch.float64, device="cuda")
+    _native.check(lib.ap_generate_uniform_envs(_native.ptr(d_st), st.shape[0], n, granularity, _native.ptr(out),
+                                               _native.stream_handle()))
+    return out

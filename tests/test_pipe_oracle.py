@@ -68,3 +68,42 @@ def test_oracle_infer_lengths(name):
         assert po.decode_length(c, a, w, list(b), list(cu), M, topo_n) == ln
     best = max(po.decode_length(c, a, w, list(d["best_b"]), list(d["best_c"]), M, topo_n), 1e-12)
     assert best == d["best_len"][0]
+
+
+def test_pcg64_state_words_restate_numpy_stream():
+    """dataproc.pcg64_states packs default_rng(seed)'s PCG64 state; stepping it with the XSL-RR
+    output (the device generator's algorithm, csrc/dataplane.cu) reproduces numpy's uniform draws,
+    also after a jump-ahead (PCG advance)."""
+    import numpy as np
+
+    from paper_2007_04069_b200.dataproc import pcg64_states
+
+    M = 0x2360ED051FC65DA44385DF649FCCF645
+    mask = (1 << 128) - 1
+
+    def advance(state, inc, delta):
+        cm, cp, am, ap = M, inc, 1, 0
+        while delta:
+            if delta & 1:
+                am, ap = (am * cm) & mask, (ap * cm + cp) & mask
+            cp, cm = ((cm + 1) * cp) & mask, (cm * cm) & mask
+            delta >>= 1
+        return (am * state + ap) & mask
+
+    def draw(state, inc):
+        state = (state * M + inc) & mask
+        x = ((state >> 64) ^ state) & ((1 << 64) - 1)
+        rot = state >> 122
+        r = ((x >> rot) | (x << ((64 - rot) % 64))) & ((1 << 64) - 1)
+        return state, (r >> 11) * (1.0 / 9007199254740992.0)
+
+    for seed in (0, 7, 20201007):
+        w = [int(v) for v in pcg64_states([seed])[0]]
+        state, inc = (w[0] << 64) | w[1], (w[2] << 64) | w[3]
+        ref = np.random.default_rng(seed).uniform(0.0, 1.0, 40)
+        s = state
+        for k in range(40):
+            s, x = draw(s, inc)
+            assert x == ref[k]
+        s = advance(state, inc, 33)
+        assert draw(s, inc)[1] == ref[33]

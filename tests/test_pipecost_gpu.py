@@ -307,3 +307,18 @@ def test_train_state_ex_fp32_rows(cuda, monkeypatch, table):
     assert torch.equal(fa[:, : 4 * C], st.float())
     assert torch.equal(fb[:, : 4 * C], st.float())
     assert torch.isnan(fa[:, 4 * C:]).all()
+
+
+@pytest.mark.parametrize("n", [1280, 129, 128, 100, 1])
+def test_device_uniform_envs_match_generate_environment(cuda, n):
+    """ap_generate_uniform_envs (PCG64 stream on the device, cumsum, coarsen, joint scaling) is
+    bit-identical to the reference-semantics generate_environment('uniform', n, seed)."""
+    from paper_2007_04069_b200.dataproc import generate_environment, generate_environments_device
+
+    seeds = [0, 1, 7, 20201007, 2**40 + 3] + list(range(100, 120))
+    dev = generate_environments_device("uniform", n, seeds).cpu().numpy()
+    for i, s in enumerate(seeds):
+        host = generate_environment("uniform", n, s)
+        np.testing.assert_array_equal(dev[i, 0], host.c)
+        np.testing.assert_array_equal(dev[i, 1], host.a)
+        np.testing.assert_array_equal(dev[i, 2], host.w)
