@@ -345,6 +345,10 @@ int ap_per_update(double* priorities, const int32_t* indices, const float* td, i
 /* dst[b, :] = src[idx[b], :] (replay minibatch gather). */
 int ap_gather_rows(const float* src, int64_t lds, const int32_t* idx, int32_t B, int32_t cols, float* dst,
                    int64_t ldd, void* stream);
+/* Two row gathers with the same indices in one launch: dst0[b] = src0[idx[b]],
+ * dst1[b] = src1[idx[b]] (src1 nullable: a single gather). */
+int ap_gather_rows_pair(const float* src0, int64_t lds0, float* dst0, int64_t ldd0, const float* src1, int64_t lds1,
+                        float* dst1, int64_t ldd1, const int32_t* idx, int32_t B, int32_t cols, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Vectorised episode driver (device-resident train_partition, cli.py:193-248)

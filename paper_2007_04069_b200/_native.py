@@ -140,6 +140,7 @@ SIGNATURES: dict[str, tuple] = {
                                    ctypes.c_float, ctypes.c_float, ctypes.c_float, _VP]),
     "ap_per_sample": (ctypes.c_int, [_VP, _I32, _F64, _F64, _VP, _I32, _VP, _VP, _VP, _VP]),
     "ap_per_update": (ctypes.c_int, [_VP, _VP, _VP, _I32, _VP]),
+    "ap_gather_rows_pair": (ctypes.c_int, [_VP, _I64, _VP, _I64, _VP, _I64, _VP, _I64, _VP, _I32, _I32, _VP]),
     "ap_gather_rows": (ctypes.c_int, [_VP, _I64, _VP, _I32, _I32, _VP, _I64, _VP]),
     "ap_vec_apply": (ctypes.c_int, [_VP, _I64, _VP, _VP, _I32, _VP]),
     "ap_vec_post": (ctypes.c_int, [_I32, _I32, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _VP, _VP, _VP, _VP,

@@ -293,17 +293,19 @@ class QNetwork:
         b = dz.shape[0]
         aug = self._augmented(b)
         n = L + 1
-        _native.check(lib.ap_transpose_batch(
-            n, (ctypes.c_void_p * n)(*[a.data_ptr() for a in acts]),
-            (ctypes.c_int64 * n)(*[a.stride(0) for a in acts]), (ctypes.c_void_p * n)(*[t.data_ptr() for t in aug]),
-            (ctypes.c_int64 * n)(*[t.stride(0) for t in aug]), (ctypes.c_int32 * n)(*[b] * n),
-            (ctypes.c_int32 * n)(*[a.shape[1] for a in acts]), _stream()))
         keep = []
         if dz_t is None:
             dz_t = dz.t().contiguous()
         if side is not None:
             fork_to(side)
         with stream_or_current(side):
+            # the ones-augmented activation transposes only feed the weight-gradient
+            # GEMMs, so with a side stream they leave the data-gradient chain entirely
+            _native.check(lib.ap_transpose_batch(
+                n, (ctypes.c_void_p * n)(*[a.data_ptr() for a in acts]),
+                (ctypes.c_int64 * n)(*[a.stride(0) for a in acts]), (ctypes.c_void_p * n)(*[t.data_ptr() for t in aug]),
+                (ctypes.c_int64 * n)(*[t.stride(0) for t in aug]), (ctypes.c_int32 * n)(*[b] * n),
+                (ctypes.c_int32 * n)(*[a.shape[1] for a in acts]), _stream()))
             gemm(aug[L], dz_t, trans_b=True, out=self._grad_block("wh"), precision=self.precision)
         # head -> last hidden layer: K = 1 + A is too narrow for the tensor cores;
         # one kernel does dz @ wh^T, the ReLU mask and the transposed copy

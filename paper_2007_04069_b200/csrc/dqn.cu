@@ -824,12 +824,19 @@ __global__ void per_update_kernel(double* prio, const int32_t* idx, const float*
 
 // dst[b, :cols] = src[idx[b], :cols]: blockIdx.y = b, 16-byte vectors when the
 // rows and bases allow (no per-element index arithmetic)
-__global__ void gather_rows_kernel(const float* __restrict__ src, int64_t lds, const int32_t* __restrict__ idx, int B,
-                                   int cols, float* __restrict__ dst, int64_t ldd, int vec) {
+// blockIdx.z selects one of up to two (src, dst) pairs gathered with the same indices
+struct GatherPair {
+  const float* src[2];
+  int64_t lds[2];
+  float* dst[2];
+  int64_t ldd[2];
+};
+
+__global__ void gather_rows_kernel(GatherPair gp, const int32_t* __restrict__ idx, int B, int cols, int vec) {
   pdl_entry();
-  const int b = blockIdx.y;
-  const float* __restrict__ s = src + (int64_t)idx[b] * lds;
-  float* __restrict__ d = dst + (int64_t)b * ldd;
+  const int b = blockIdx.y, z = blockIdx.z;
+  const float* __restrict__ s = gp.src[z] + (int64_t)idx[b] * gp.lds[z];
+  float* __restrict__ d = gp.dst[z] + (int64_t)b * gp.ldd[z];
   const int step = gridDim.x * blockDim.x;
   if (vec) {
     const float4* __restrict__ s4 = reinterpret_cast<const float4*>(s);
@@ -1149,20 +1156,32 @@ int ap_per_update(double* priorities, const int32_t* indices, const float* td, i
   return AP_OK;
 }
 
-int ap_gather_rows(const float* src, int64_t lds, const int32_t* idx, int32_t B, int32_t cols, float* dst,
-                   int64_t ldd, void* stream) {
+int ap_gather_rows_pair(const float* src0, int64_t lds0, float* dst0, int64_t ldd0, const float* src1, int64_t lds1,
+                        float* dst1, int64_t ldd1, const int32_t* idx, int32_t B, int32_t cols, void* stream) {
   if (B <= 0 || cols <= 0) return AP_OK;
-  if (B > 65535) {
-    set_error("ap_gather_rows: at most 65535 rows per call");
+  if (B > 65535 || !src0 || !dst0 || !idx) {
+    set_error("ap_gather_rows: bad arguments (at most 65535 rows per call)");
     return AP_ERR_INVALID;
   }
-  const int vec = cols % 4 == 0 && lds % 4 == 0 && ldd % 4 == 0 &&
-                  ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+  const int pairs = src1 ? 2 : 1;
+  GatherPair gp{{src0, src1}, {lds0, lds1}, {dst0, dst1}, {ldd0, ldd1}};
+  uintptr_t bases = reinterpret_cast<uintptr_t>(src0) | reinterpret_cast<uintptr_t>(dst0);
+  int64_t strides = lds0 | ldd0;
+  if (src1) {
+    bases |= reinterpret_cast<uintptr_t>(src1) | reinterpret_cast<uintptr_t>(dst1);
+    strides |= lds1 | ldd1;
+  }
+  const int vec = cols % 4 == 0 && strides % 4 == 0 && (bases & 15) == 0;
   const int per_row = vec ? cols / 4 : cols;
-  const dim3 grid((unsigned)std::max(1, std::min((per_row + 255) / 256, 16)), (unsigned)B);
-  launch_pdl(gather_rows_kernel, dim3(grid), dim3(256), 0, (cudaStream_t)stream, src, lds, idx, B, cols, dst, ldd, vec);
+  const dim3 grid((unsigned)std::max(1, std::min((per_row + 255) / 256, 16)), (unsigned)B, (unsigned)pairs);
+  launch_pdl(gather_rows_kernel, grid, dim3(256), 0, (cudaStream_t)stream, gp, idx, B, cols, vec);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
+}
+
+int ap_gather_rows(const float* src, int64_t lds, const int32_t* idx, int32_t B, int32_t cols, float* dst,
+                   int64_t ldd, void* stream) {
+  return ap_gather_rows_pair(src, lds, dst, ldd, nullptr, 0, nullptr, 0, idx, B, cols, stream);
 }
 
 }  // extern "C"

@@ -458,9 +458,9 @@ class VecDqnTrainer:
         # states and next states gathered into one [2B, S] block: the online
         # network runs once over both (M = 2B), the target net over the second half
         sn = self.sn
-        for src, dst in ((r["states"], sn[:B]), (r["next_states"], sn[B:])):
-            _native.check(lib.ap_gather_rows(P(src), src.stride(0), P(self.idx), B, src.shape[1], P(dst),
-                                             dst.stride(0), _s()))
+        s0, s1 = r["states"], r["next_states"]
+        _native.check(lib.ap_gather_rows_pair(P(s0), s0.stride(0), P(sn[:B]), sn.stride(0), P(s1), s1.stride(0),
+                                              P(sn[B:]), sn.stride(0), P(self.idx), B, s0.shape[1], _s()))
         side = self.side
         if side is not None:  # the target forward is a parallel branch beside the online forward
             fork_to(side)
@@ -498,9 +498,11 @@ class VecDqnTrainer:
         # the priority scatter also counts the learn step (ctl[AP_CTL_TRAIN] += 1)
         _native.check(lib.ap_per_update_scaled_ctl(P(r["priorities"]), P(self.idx), P(b.td), B,
                                                    float(cfg.per_alpha), P(self.ctl), _s()))
-        # sample, 2 gathers, 2 forwards (4 GEMMs + 2 heads), td, backward (1 transpose, 4 GEMMs,
-        # head, relu), adam (+ transposed copies), priority scatter (+ counter)
-        self.launches += 1 + 2 + 6 + 1 + 7 + 1 + 1
+        Lh = len(self.net.hidden)
+        head = 1 if 1 + self.env.num_actions <= 8 else 2  # narrow fused head | GEMM + dueling (row-sum + closed form)
+        fwd = 2 * (Lh + head)  # online and target forwards
+        bwd = 1 + 1 + head + Lh + 2 * (Lh - 1)  # transpose, head wgrad, head dgrad, wgrads, dgrad + ReLU per layer
+        self.launches += 1 + 1 + fwd + 1 + bwd + 1 + 1  # sample, pair gather, .., td, .., adam, priority scatter
 
     def _step_body(self, learn: bool) -> None:
         self.act()
