@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 
 #include "engine.h"
 
@@ -313,8 +314,128 @@ __global__ void __launch_bounds__(kSampleThreads) per_sample_fast_kernel(
   for (int b = t; b < B; b += kSampleThreads) w_out[b] /= s_w[0];
 }
 
+// Same sampler for rings whose CDF fits shared memory, with a cheaper scan:
+// the CDF lives at padded index i + i/16 (conflict-free for both the coalesced
+// fill and the per-thread walks); thread t sums its k = ceil(n/1024)
+// contiguous priorities serially, one block scan of the thread totals gives
+// the offsets, and a second serial walk writes the prefix.  (The warp-row
+// kernel above runs 32 dependent warp scans per 1024 priorities.)
+__device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
+
+__global__ void __launch_bounds__(kSampleThreads) per_sample_pad_kernel(const double* prio, int n, double beta,
+                                                                        const float* uniforms, int B,
+                                                                        int32_t* idx_out, float* w_out,
+                                                                        double* max_prio, const int64_t* ctl,
+                                                                        uint64_t seed) {
+  pdl_entry();
+  extern __shared__ double s_c[];
+  __shared__ double w_tot[32], w_max[32];
+  __shared__ float s_w[32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  uint64_t draw = 0;
+  if (ctl) {
+    n = (int)ctl[AP_CTL_SIZE];
+    draw = (seed * 0x9E3779B97F4A7C15ULL) ^ ((uint64_t)ctl[AP_CTL_TRAIN] << 20);
+    if (n < 1) {  // empty ring (caller bug): keep indices in bounds
+      for (int b = t; b < B; b += kSampleThreads) {
+        idx_out[b] = 0;
+        w_out[b] = 0.0f;
+      }
+      return;
+    }
+  }
+  double mx = 0.0;
+  int i = t;
+  for (; i + 3 * kSampleThreads < n; i += 4 * kSampleThreads) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = __ldg(prio + i + u * kSampleThreads);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      s_c[pad16(i + u * kSampleThreads)] = v[u];
+      mx = fmax(mx, v[u]);
+    }
+  }
+  for (; i < n; i += kSampleThreads) {
+    const double v = __ldg(prio + i);
+    s_c[pad16(i)] = v;
+    mx = fmax(mx, v);
+  }
+  __syncthreads();
+  const int k = (n + kSampleThreads - 1) / kSampleThreads;
+  const int lo = min(n, t * k), hi = min(n, lo + k);
+  double tot = 0.0;
+  for (int j = lo; j < hi; ++j) tot += s_c[pad16(j)];
+  const double incl = warp_incl_scan(tot, lane);
+  for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(kFull, mx, o));
+  if (lane == 31) w_tot[warp] = incl;
+  if (lane == 0) w_max[warp] = mx;
+  __syncthreads();
+  if (warp == 0) {
+    const double v = w_tot[lane];
+    const double wi = warp_incl_scan(v, lane);
+    w_tot[lane] = wi - v;  // exclusive warp offsets
+    double mm = w_max[lane];
+    for (int o = 16; o; o >>= 1) mm = fmax(mm, __shfl_xor_sync(kFull, mm, o));
+    if (lane == 31) {
+      w_max[0] = wi;  // grand total
+      *max_prio = mm;
+    }
+  }
+  __syncthreads();
+  double run = (incl - tot) + w_tot[warp];
+  for (int j = lo; j < hi; ++j) {
+    run += s_c[pad16(j)];
+    s_c[pad16(j)] = run;
+  }
+  __syncthreads();
+  const double total = w_max[0];
+  float wm = 0.0f;
+  for (int b = t; b < B; b += kSampleThreads) {
+    const float ub = ctl ? (float)(mix64to32(draw + (uint64_t)b) >> 8) * (1.0f / 16777216.0f) : uniforms[b];
+    const double u = (double)ub * total;
+    int l = 0, h = n;
+    while (l < h) {
+      const int mid = (l + h) >> 1;
+      if (s_c[pad16(mid)] <= u)
+        l = mid + 1;
+      else
+        h = mid;
+    }
+    if (l >= n) l = n - 1;
+    idx_out[b] = l;
+    const double pr = (s_c[pad16(l)] - (l ? s_c[pad16(l - 1)] : 0.0)) / total;
+    const float w = (float)pow((double)n * pr, -beta);
+    w_out[b] = w;
+    wm = fmaxf(wm, w);
+  }
+  for (int o = 16; o; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(kFull, wm, o));
+  if (lane == 0) s_w[warp] = wm;
+  __syncthreads();
+  if (warp == 0) {
+    float m = s_w[lane];
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
+    if (lane == 0) s_w[0] = m;
+  }
+  __syncthreads();
+  for (int b = t; b < B; b += kSampleThreads) w_out[b] /= s_w[0];
+}
+
 int launch_per_sample(const double* prio, int n_host_max, double beta, const float* uniforms, int B, double* cdf,
                       int32_t* idx, float* w, double* max_prio, const int64_t* ctl, uint64_t seed, cudaStream_t s) {
+  if (n_host_max <= kSampleSmemMax && std::getenv("AP_PER_ROWSCAN") == nullptr) {  // padded CDF in shared memory
+    const int64_t psmem = (int64_t)(n_host_max + n_host_max / 16 + 1) * 8;
+    static int64_t pconfigured = -1;
+    if (psmem > pconfigured) {
+      AP_CUDA_CHECK(cudaFuncSetAttribute(per_sample_pad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)psmem));
+      pconfigured = psmem;
+    }
+    launch_pdl(per_sample_pad_kernel, dim3(1), dim3(kSampleThreads), (size_t)psmem, s, prio, n_host_max, beta,
+               uniforms, B, idx, w, max_prio, ctl, seed);
+    AP_CUDA_CHECK(cudaGetLastError());
+    return AP_OK;
+  }
   // shared CDF sized for the largest ring this launch can see
   const int64_t smem = n_host_max <= kSampleSmemMax ? (int64_t)n_host_max * 8 : 0;
   static int64_t configured = -1;
