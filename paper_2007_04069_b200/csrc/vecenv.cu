@@ -50,14 +50,15 @@ __global__ void vec_post_kernel(int E, int n, int64_t ld, int8_t* seeds, const i
   const int lane = threadIdx.x & 31;
   if (e >= E) return;
   const int8_t* st = status + (int64_t)e * ld;
-  float* cs = cur_state + (int64_t)e * lds;
-  float* ns = next_state + (int64_t)e * lds;
+  float* __restrict__ cs = cur_state + (int64_t)e * lds;
+  float* __restrict__ ns = next_state + (int64_t)e * lds;
   const int oc = outcome[e];
   float reward;
   bool fin;
   if (oc == AP_OUTCOME_CONFLICT) {
     reward = -1.0f;
     fin = true;
+#pragma unroll 4
     for (int j = lane; j <= n; j += 32) ns[j] = cs[j];  // state unchanged (envs.py:147-149)
   } else {
     const int dP = counts[(int64_t)e * 4 + 0], dR = counts[(int64_t)e * 4 + 1];
@@ -72,15 +73,22 @@ __global__ void vec_post_kernel(int E, int n, int64_t ld, int8_t* seeds, const i
       const unsigned bal = __ballot_sync(kFull, und);
       if (bal) pos = order[base + __ffs(bal) - 1];
     }
-    for (int j = lane; j < n; j += 32) ns[j] = (float)st[j];
+    // the decided statuses are the next state and the env's new current state:
+    // both rows written from the same registers (no read-back of ns)
+#pragma unroll 4
+    for (int j = lane; j < n; j += 32) {
+      const float v = (float)st[j];
+      ns[j] = v;
+      cs[j] = v;
+    }
     if (lane == 0) {
-      ns[n] = pos < 0 ? 1.0f : (float)pos / (float)n;
+      const float last = pos < 0 ? 1.0f : (float)pos / (float)n;
+      ns[n] = last;
+      cs[n] = last;
       prev_counts[2 * e] = dP;
       prev_counts[2 * e + 1] = dR;
       position[e] = pos < 0 ? 0 : pos;
     }
-    // keep the decided statuses as the env's new state
-    for (int j = lane; j <= n; j += 32) cs[j] = ns[j];
     if (fin && lane == 0) finished_partitions[e] = dP;
   }
   if (lane == 0) {
