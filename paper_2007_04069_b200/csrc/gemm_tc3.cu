@@ -10,9 +10,16 @@
 //     mbarriers: thread 0 of warp 0 produces, thread 0 of warp 1 issues the
 //     MMAs (4 x K=8 per 32-wide k slice, the descriptor start advanced by 32 B
 //     inside the swizzled row), accumulators in TMEM;
-//   * epilogue: all 4 warps tcgen05.ld their 32 TMEM lanes, add bias / ReLU and
-//     store; with split-K the partials go to a workspace and a fixed-order
-//     reduce kernel sums them (bit-reproducible).
+//   * epilogue: all 4 warps tcgen05.ld their 32 TMEM lanes into a [128][BN+1]
+//     shared tile (the drained stage ring), then each thread owns one column
+//     (bias loaded once) and consecutive threads store consecutive columns;
+//   * split-K (only when K >= 512 and the tile grid leaves SMs idle): the splits
+//     of a tile form one thread-block cluster (<= 16 CTAs) and reduce through
+//     DSMEM in split order (bit-reproducible); AP_GEMM_NO_CLUSTER=1 uses a
+//     per-stream global workspace + a fixed-order reduce kernel instead;
+//   * BN = 32 | 64 | 128 (128 when it needs fewer waves than 64);
+//   * programmatic dependent launch: the TMEM / barrier / tensor-map prologue
+//     overlaps the previous kernel (griddepcontrol.wait before any global access).
 // Tensor maps are encoded per call with cuTensorMapEncodeTiled obtained through
 // cudaGetDriverEntryPoint (no libcuda link dependency).
 #include <cuda.h>

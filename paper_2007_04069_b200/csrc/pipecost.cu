@@ -15,6 +15,14 @@
 //  * byte counts are integers (exact in int64, converted once);
 //  * expressions keep Python's left-to-right association, ties in max/min
 //    and in the largest-remainder sort resolve to the lowest index.
+//
+// K2 layout: a candidate list bound with ap_pipe_train_table gets a table of
+// every stage sum its plans can have (each entry summed in the reference's
+// order), so ap_pipe_train_state / ap_pipe_metrics_bound read stage sums
+// instead of re-summing the cost array (train_state_tab_kernel, one CTA per
+// env, features + block normalisation + one-hot fused).  Unbound lists take
+// the per-env-reuse sweep (train_prefix_kernel + train_tail_kernel) or, with
+// AP_PP_FULL=1, one sequential sweep per candidate (train_cand_kernel).
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
