@@ -410,6 +410,14 @@ int ap_dqn_adam_ctl_t(float* params, const float* grads, float* m, float* v, int
                       float beta2, float eps, const int64_t* ctl, int32_t nseg, const int64_t* seg_off,
                       const int32_t* seg_rows, const int32_t* seg_cols, float* const* seg_dst, const int64_t* seg_ldd,
                       void* stream);
+/* ap_dqn_adam_ctl_t when the learn-step counter ctl[AP_CTL_TRAIN] has already
+ * been advanced for this step (counter_advanced = 1: t = ctl[TRAIN]; 0: t =
+ * ctl[TRAIN] + 1) -- the pipelined learner runs the priority scatter, which
+ * advances it, on a parallel branch that joins before Adam. */
+int ap_dqn_adam_ctl_t_adv(float* params, const float* grads, float* m, float* v, int64_t n, float lr, float beta1,
+                          float beta2, float eps, const int64_t* ctl, int32_t nseg, const int64_t* seg_off,
+                          const int32_t* seg_rows, const int32_t* seg_cols, float* const* seg_dst,
+                          const int64_t* seg_ldd, int32_t counter_advanced, void* stream);
 /* ap_per_update_scaled that also counts the learn step: ctl[3] += 1. */
 int ap_per_update_scaled_ctl(double* scaled, const int32_t* indices, const float* td, int32_t B, double alpha,
                              int64_t* ctl, void* stream);

@@ -568,6 +568,7 @@ struct AdamSegments {
   float* dst[8];
   int64_t ldd[8];
   int n;
+  int t_add;  // Adam step t = ctl[AP_CTL_TRAIN] + t_add (0 when the counter was already advanced)
 };
 
 // one Adam element update (shared by the flat and tiled kernels: same code, same rounding)
@@ -616,7 +617,7 @@ __global__ void __launch_bounds__(256) adam_tile_kernel(float* p, const float* g
   __shared__ float tile[32][33];
   auto corrections = [&]() {  // bias corrections (thread 0), published by the caller's barrier
     if (threadIdx.x == 0) {
-      const double t = (double)(ctl[AP_CTL_TRAIN] + 1);
+      const double t = (double)(ctl[AP_CTL_TRAIN] + at.segs.t_add);
       s_c[0] = (float)(1.0 / (1.0 - pow((double)b1, t)));
       s_c[1] = (float)(1.0 / (1.0 - pow((double)b2, t)));
     }
@@ -685,7 +686,7 @@ __global__ void adam_t_kernel(float* p, const float* g, float* m, float* v, int6
   pdl_entry();
   __shared__ float s_c[2];
   if (threadIdx.x == 0) {
-    const double t = (double)(ctl[AP_CTL_TRAIN] + 1);
+    const double t = (double)(ctl[AP_CTL_TRAIN] + segs.t_add);
     s_c[0] = (float)(1.0 / (1.0 - pow((double)b1, t)));  // reciprocals (adam_math)
     s_c[1] = (float)(1.0 / (1.0 - pow((double)b2, t)));
   }
@@ -1062,10 +1063,23 @@ int ap_dqn_adam(float* params, const float* grads, float* m, float* v, int64_t n
   return AP_OK;
 }
 
+int ap_dqn_adam_ctl_t_adv(float* params, const float* grads, float* m, float* v, int64_t n, float lr, float beta1,
+                          float beta2, float eps, const int64_t* ctl, int32_t nseg, const int64_t* seg_off,
+                          const int32_t* seg_rows, const int32_t* seg_cols, float* const* seg_dst,
+                          const int64_t* seg_ldd, int32_t counter_advanced, void* stream);
+
 int ap_dqn_adam_ctl_t(float* params, const float* grads, float* m, float* v, int64_t n, float lr, float beta1,
                       float beta2, float eps, const int64_t* ctl, int32_t nseg, const int64_t* seg_off,
                       const int32_t* seg_rows, const int32_t* seg_cols, float* const* seg_dst, const int64_t* seg_ldd,
                       void* stream) {
+  return ap_dqn_adam_ctl_t_adv(params, grads, m, v, n, lr, beta1, beta2, eps, ctl, nseg, seg_off, seg_rows, seg_cols,
+                               seg_dst, seg_ldd, 0, stream);
+}
+
+int ap_dqn_adam_ctl_t_adv(float* params, const float* grads, float* m, float* v, int64_t n, float lr, float beta1,
+                          float beta2, float eps, const int64_t* ctl, int32_t nseg, const int64_t* seg_off,
+                          const int32_t* seg_rows, const int32_t* seg_cols, float* const* seg_dst,
+                          const int64_t* seg_ldd, int32_t counter_advanced, void* stream) {
   if (!ctl || nseg < 0 || nseg > 8 || (nseg > 0 && (!seg_off || !seg_rows || !seg_cols || !seg_dst || !seg_ldd))) {
     set_error("ap_dqn_adam_ctl_t: bad arguments (0..8 segments, host descriptor arrays)");
     return AP_ERR_INVALID;
@@ -1073,6 +1087,7 @@ int ap_dqn_adam_ctl_t(float* params, const float* grads, float* m, float* v, int
   if (n <= 0) return AP_OK;
   AdamSegments segs{};
   segs.n = nseg;
+  segs.t_add = counter_advanced ? 0 : 1;
   for (int s = 0; s < nseg; ++s) {
     segs.off[s] = seg_off[s];
     segs.rows[s] = seg_rows[s];

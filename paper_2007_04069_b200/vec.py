@@ -406,7 +406,9 @@ class VecDqnTrainer:
         self.actions = torch.empty(env.E, dtype=torch.int32, device=dev)
         self.batch = _Batch(config.batch_size, S, A)
         # [2B, S] with rows padded to a 16-byte stride (TMA operand rule)
-        self.sn = torch.empty((2 * config.batch_size, (S + 3) // 4 * 4), dtype=torch.float32, device=dev)[:, :S]
+        # double-buffered: the pipelined learner gathers step k + 1's batch while step k's backward reads its own
+        self.sn_bufs = [torch.empty((2 * config.batch_size, (S + 3) // 4 * 4), dtype=torch.float32, device=dev)[:, :S]
+                        for _ in range(2)]
         self.dz_t = torch.empty((1 + A, config.batch_size), dtype=torch.float32, device=dev)
         self.idx = torch.empty(config.batch_size, dtype=torch.int32, device=dev)
         self.weights = torch.empty(config.batch_size, dtype=torch.float32, device=dev)
@@ -422,6 +424,9 @@ class VecDqnTrainer:
         # side stream for the learner's parallel branches (target forward, weight gradients);
         # AP_DQN_NO_FORK=1 keeps one serial chain
         self.side = None if os.environ.get("AP_DQN_NO_FORK") else torch.cuda.Stream()
+        # second branch: priority scatter + next sample / gather beside the backward (AP_DQN_NO_PIPELINE=1: serial)
+        self.side2 = None if (os.environ.get("AP_DQN_NO_FORK") or os.environ.get("AP_DQN_NO_PIPELINE")) \
+            else torch.cuda.Stream()
 
     # -- one vector step -------------------------------------------------------------
 
@@ -446,8 +451,9 @@ class VecDqnTrainer:
                                           P(r["priorities"]), P(self.max_prio), P(self.ctl), _s()))
         self.launches += 1
 
-    def learn(self) -> None:
-        cfg, r, b = self.config, self.ring, self.batch
+    def _sample_gather(self, k: int) -> None:
+        """PER sample of learn step k and its [2B, S] state / next-state block (buffer k % 2)."""
+        cfg, r = self.config, self.ring
         B = cfg.batch_size
         lib = _native.require_device()
         P = _native.ptr
@@ -457,10 +463,24 @@ class VecDqnTrainer:
                                             _s()))
         # states and next states gathered into one [2B, S] block: the online
         # network runs once over both (M = 2B), the target net over the second half
-        sn = self.sn
+        sn = self.sn_bufs[k % 2]
         s0, s1 = r["states"], r["next_states"]
         _native.check(lib.ap_gather_rows_pair(P(s0), s0.stride(0), P(sn[:B]), sn.stride(0), P(s1), s1.stride(0),
                                               P(sn[B:]), sn.stride(0), P(self.idx), B, s0.shape[1], _s()))
+
+    def learn(self, k: int = 0, prefetched: bool = False, prefetch_next: bool = False) -> None:
+        """One learner update.  Pipelined (self.side2): the priority scatter of this
+        step, then the sample + gather of step k + 1, run on a parallel branch beside
+        the backward pass; the branch joins before Adam, which then reads the already
+        advanced step counter.  Every value equals the serial order's."""
+        cfg, r, b = self.config, self.ring, self.batch
+        B = cfg.batch_size
+        lib = _native.require_device()
+        P = _native.ptr
+        pipe = self.side2 is not None and self.peer is None
+        if not prefetched:
+            self._sample_gather(k)
+        sn = self.sn_bufs[k % 2]
         side = self.side
         if side is not None:  # the target forward is a parallel branch beside the online forward
             fork_to(side)
@@ -476,7 +496,16 @@ class VecDqnTrainer:
                                          r["next_mask"].stride(0), P(self.weights), B, self.env.num_actions,
                                          float(cfg.gamma), float(cfg.huber_delta), P(b.dz), b.dz.stride(0),
                                          P(self.dz_t), self.dz_t.stride(0), P(b.td), P(b.loss_rows), _s()))
+        if pipe:  # priority scatter (+ step counter) and the next step's sample / gather, beside the backward
+            fork_to(self.side2)
+            with stream_or_current(self.side2):
+                _native.check(lib.ap_per_update_scaled_ctl(P(r["priorities"]), P(self.idx), P(b.td), B,
+                                                           float(cfg.per_alpha), P(self.ctl), _s()))
+                if prefetch_next:
+                    self._sample_gather(k + 1)
         self.net.backward_device(acts, b.dz, self.dz_t, side=side, dueling_td=True)
+        if pipe:
+            join_from(self.side2)
         opt = self.opt
         if self.peer is not None:  # data-parallel: gradient all-reduce over NVLink peer memory fused with Adam
             x = self.peer
@@ -490,14 +519,14 @@ class VecDqnTrainer:
             # Adam also rewrites the transposed weight copies (no separate transpose launch;
             # measured faster than Adam + a tiled transpose even for the 4 M-parameter PP-train net)
             sg = self.net.adam_segments()
-            _native.check(lib.ap_dqn_adam_ctl_t(P(self.net.flat), P(self.net.grad), P(opt.m), P(opt.v),
-                                                self.net.flat.numel(), opt.lr, opt.beta1, opt.beta2, opt.eps,
-                                                P(self.ctl), *sg, _s()))
+            _native.check(lib.ap_dqn_adam_ctl_t_adv(P(self.net.flat), P(self.net.grad), P(opt.m), P(opt.v),
+                                                    self.net.flat.numel(), opt.lr, opt.beta1, opt.beta2, opt.eps,
+                                                    P(self.ctl), *sg, 1 if pipe else 0, _s()))
         if self.peer is not None:
             self.net.refresh_transposed()
-        # the priority scatter also counts the learn step (ctl[AP_CTL_TRAIN] += 1)
-        _native.check(lib.ap_per_update_scaled_ctl(P(r["priorities"]), P(self.idx), P(b.td), B,
-                                                   float(cfg.per_alpha), P(self.ctl), _s()))
+        if not pipe:  # the priority scatter also counts the learn step (ctl[AP_CTL_TRAIN] += 1)
+            _native.check(lib.ap_per_update_scaled_ctl(P(r["priorities"]), P(self.idx), P(b.td), B,
+                                                       float(cfg.per_alpha), P(self.ctl), _s()))
         Lh = len(self.net.hidden)
         head = 1 if 1 + self.env.num_actions <= 8 else 2  # narrow fused head | GEMM + dueling (row-sum + closed form)
         fwd = 2 * (Lh + head)  # online and target forwards
@@ -517,8 +546,10 @@ class VecDqnTrainer:
         _native.check(lib.ap_vec_ctl_advance(_native.ptr(self.ctl), 1, E, self.capacity, _s()))
         self.launches += 1
         if learn:
-            for _ in range(self.learn_steps):
-                self.learn()
+            pipe = self.side2 is not None and self.peer is None
+            L = self.learn_steps
+            for k in range(L):
+                self.learn(k, prefetched=pipe and k > 0, prefetch_next=pipe and k + 1 < L)
 
     def _advance_host(self, learned: bool) -> None:
         E = self.env.E

@@ -244,3 +244,21 @@ def test_throughput_per_sampler(cuda, monkeypatch, n):
         ref = (n * p) ** -0.4
         np.testing.assert_allclose(w, ref / ref.max(), rtol=2e-6)
     np.testing.assert_array_equal(res[0][0], res[1][0])
+
+
+@pytest.mark.parametrize("use_graph", [False, True])
+def test_pipelined_learner_matches_serial(cuda, monkeypatch, use_graph):
+    """Learner pipelining (priority scatter + next PER sample / gather on a branch beside the
+    backward, Adam reading the advanced step counter) == the serial learn order, bit for bit."""
+    monkeypatch.setenv("AP_DQN_NO_PIPELINE", "1")
+    a = _train(use_graph, 10, learn_steps=3)
+    monkeypatch.delenv("AP_DQN_NO_PIPELINE")
+    b = _train(use_graph, 10, learn_steps=3)
+    assert a.side2 is None and b.side2 is not None
+    for name in ("flat", "grad"):
+        assert torch.equal(getattr(a.net, name), getattr(b.net, name)), name
+    assert torch.equal(a.opt.m, b.opt.m) and torch.equal(a.opt.v, b.opt.v)
+    assert torch.equal(a.ctl, b.ctl)
+    for k in a.ring:
+        assert torch.equal(a.ring[k], b.ring[k]), k
+    assert torch.equal(a.idx, b.idx) and torch.equal(a.weights, b.weights)
