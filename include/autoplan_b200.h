@@ -410,6 +410,17 @@ int ap_dqn_adam_ctl_t(float* params, const float* grads, float* m, float* v, int
                       float beta2, float eps, const int64_t* ctl, int32_t nseg, const int64_t* seg_off,
                       const int32_t* seg_rows, const int32_t* seg_cols, float* const* seg_dst, const int64_t* seg_ldd,
                       void* stream);
+/* Weight-gradient GEMM with Adam fused into its epilogue (throughput learner, first
+ * layer): C[M, N] = A[M, K] B[N, K]^T is stored as the gradient and Adam updates
+ * m, v and params (each at C's offset, row stride ldc) in place, t = ctl[TRAIN] +
+ * (counter_advanced ? 0 : 1), same arithmetic as ap_dqn_adam_ctl_t; the updated
+ * rows r < t_rows are also written transposed to t_dst[c * t_ld + r].
+ * AP_ERR_UNSUPPORTED for shapes that need split-K (the caller runs the plain GEMM). */
+int ap_gemm_tf32_adam(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int32_t M,
+                      int32_t N, int32_t K, float* m, float* v, float* params, const int64_t* ctl,
+                      int32_t counter_advanced, float lr, float beta1, float beta2, float eps, float* t_dst,
+                      int64_t t_ld, int32_t t_rows, void* stream);
+
 /* ap_dqn_adam_ctl_t when the learn-step counter ctl[AP_CTL_TRAIN] has already
  * been advanced for this step (counter_advanced = 1: t = ctl[TRAIN]; 0: t =
  * ctl[TRAIN] + 1) -- the pipelined learner runs the priority scatter, which

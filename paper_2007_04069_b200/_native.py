@@ -152,6 +152,8 @@ SIGNATURES: dict[str, tuple] = {
                                             _VP, _VP, _VP]),
     "ap_dqn_adam_ctl_t": (ctypes.c_int, [_VP, _VP, _VP, _VP, _I64, _F32, _F32, _F32, _F32, _VP, _I32, _VP, _VP, _VP,
                                          _VP, _VP, _VP]),
+    "ap_gemm_tf32_adam": (ctypes.c_int, [_VP, _I64, _VP, _I64, _VP, _I64, _I32, _I32, _I32, _VP, _VP, _VP, _VP, _I32,
+                                         _F32, _F32, _F32, _F32, _VP, _I64, _I32, _VP]),
     "ap_dqn_adam_ctl_t_adv": (ctypes.c_int, [_VP, _VP, _VP, _VP, _I64, _F32, _F32, _F32, _F32, _VP, _I32, _VP, _VP,
                                              _VP, _VP, _VP, _I32, _VP]),
     "ap_per_update_scaled_ctl": (ctypes.c_int, [_VP, _VP, _VP, _I32, _F64, _VP, _VP]),

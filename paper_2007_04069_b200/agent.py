@@ -187,26 +187,38 @@ class QNetwork:
         self.views["bh"].copy_(torch.from_numpy(bh))
         self.refresh_transposed()
 
-    def adam_segments(self):
+    def adam_segments(self, skip_w0: bool = False):
         """Host descriptors for ap_dqn_adam_ctl_t: (n, flat offsets, rows, cols, transposed
-        destinations, their row strides) of every weight matrix (cached; tensors never move)."""
+        destinations, their row strides) of every weight matrix (cached; tensors never move).
+        skip_w0: the layers after the first [in + 1, out] block (w0 and b0), offsets relative
+        to that block's end -- the first layer's update is fused into its gradient GEMM."""
         import ctypes
 
-        if getattr(self, "_aseg", None) is None:
+        key = "_aseg_skip" if skip_w0 else "_aseg"
+        if getattr(self, key, None) is None:
             names = list(self.wt)
+            start = self.w0_block() if skip_w0 else 0
+            if skip_w0:
+                names = names[1:]
             n = len(names)
-            base = self.flat.storage_offset()
+            base = self.flat.storage_offset() + start
             src = [self.views[k] for k in names]
             dst = [self.wt[k] for k in names]
-            self._aseg = (
+            setattr(self, key, (
                 n,
                 (ctypes.c_int64 * n)(*[t.storage_offset() - base for t in src]),
                 (ctypes.c_int32 * n)(*[t.shape[0] for t in src]),
                 (ctypes.c_int32 * n)(*[t.shape[1] for t in src]),
                 (ctypes.c_void_p * n)(*[t.data_ptr() for t in dst]),
                 (ctypes.c_int64 * n)(*[t.stride(0) for t in dst]),
-            )
-        return self._aseg
+            ))
+        return getattr(self, key)
+
+    def w0_block(self) -> int:
+        """Length of the leading [in + 1, out] block of the flat buffers (w0 then b0)."""
+        w0 = self.views["w0"]
+        assert w0.storage_offset() == self.flat.storage_offset(), "w0 leads the flat parameter buffer"
+        return (w0.shape[0] + 1) * w0.shape[1]
 
     def refresh_transposed(self) -> None:
         """All transposed weight copies in one launch (ap_transpose_batch)."""
@@ -263,7 +275,7 @@ class QNetwork:
             raise ValueError(f"expected state dim {self.state_dim}, got {x.shape[1]}")
         return self.forward_device(x).double().cpu().numpy()
 
-    def backward_device(self, acts, dz, dz_t=None, side=None, dueling_td: bool = False) -> None:
+    def backward_device(self, acts, dz, dz_t=None, side=None, dueling_td: bool = False, fused_w0_adam=None) -> bool:
         """Gradients into self.grad from dLoss/dz (z = [V, A] head outputs).
 
         `dz_t` (optional) is dz^T already materialised (ap_dqn_td_ring writes it).
@@ -278,6 +290,11 @@ class QNetwork:
         `dueling_td`: dz is the TD kernels' dueling gradient (one advantage entry
         differs from -g/A per row), so a wide head back-propagates in closed form
         (ap_dqn_head_backward_dueling).
+
+        `fused_w0_adam` (dict: m, v, ctl, counter_advanced, lr, beta1, beta2, eps and an
+        optional `wait` event): the first layer's weight-gradient GEMM also applies Adam to
+        w0 / b0 and writes w0's transposed copy (ap_gemm_tf32_adam).  Returns True when it
+        did; the caller's Adam then skips that block (adam_segments(skip_w0=True)).
 
         `side` (a CUDA stream): the weight-gradient GEMMs run there, a parallel
         branch beside the data-gradient chain (one graph branch under capture);
@@ -294,6 +311,7 @@ class QNetwork:
         aug = self._augmented(b)
         n = L + 1
         keep = []
+        fused = False
         if dz_t is None:
             dz_t = dz.t().contiguous()
         if side is not None:
@@ -330,7 +348,25 @@ class QNetwork:
                 fork_to(side)  # the branch waits for this layer's dh_t
                 keep.append(dh_t)
             with stream_or_current(side):
-                gemm(aug[i], dh_t, trans_b=True, out=self._grad_block(f"w{i}"), precision=self.precision)
+                done = False
+                if i == 0 and fused_w0_adam is not None:
+                    fa = fused_w0_adam
+                    if fa.get("wait") is not None:
+                        torch.cuda.current_stream().wait_event(fa["wait"])
+                    n0 = self.w0_block()
+                    out = self._grad_block("w0")
+                    wt0 = self.wt["w0"]
+                    rc = lib.ap_gemm_tf32_adam(P(aug[0]), aug[0].stride(0), P(dh_t), dh_t.stride(0), P(out),
+                                               out.stride(0), out.shape[0], out.shape[1], b, P(fa["m"]), P(fa["v"]),
+                                               P(self.flat), P(fa["ctl"]), int(fa["counter_advanced"]),
+                                               float(fa["lr"]), float(fa["beta1"]), float(fa["beta2"]),
+                                               float(fa["eps"]), P(wt0), wt0.stride(0), out.shape[0] - 1, _stream())
+                    if rc != _native.AP_ERR_UNSUPPORTED:
+                        _native.check(rc)
+                        done = fused = True
+                    assert n0 == out.numel()
+                if not done:
+                    gemm(aug[i], dh_t, trans_b=True, out=self._grad_block(f"w{i}"), precision=self.precision)
             if i > 0:  # gradient into layer i-1's output: dh @ W_i^T, ReLU mask, K-major copy
                 dh = gemm(dh, self.views[f"w{i}"], trans_b=True, precision=self.precision)
                 hin = acts[i]
@@ -340,6 +376,7 @@ class QNetwork:
         if side is not None:
             join_from(side)
         del keep
+        return fused
 
     def _augmented(self, b: int):
         """Per-batch-size [in + 1, b] buffers (last row ones) for each layer's input."""

@@ -572,20 +572,6 @@ struct AdamSegments {
 };
 
 // one Adam element update (shared by the flat and tiled kernels: same code, same rounding)
-// Throughput-mode Adam element (the graph-captured learner; the parity agent's
-// ap_dqn_adam keeps the reference expression).  Explicitly rounded operations
-// (never contracted, so every kernel computes the same bits), reciprocal bias
-// corrections ic1 = 1/c1, ic2 = 1/c2, one fast divide: the IEEE divide / sqrt
-// subroutines made the update instruction-bound (28.7 M instructions for 4.1 M
-// parameters, 2.8 TB/s).
-__device__ __forceinline__ void adam_math(float gi, float& mi, float& vi, float& pi, float lr, float b1, float b2,
-                                          float eps, float ic1, float ic2) {
-  mi = __fadd_rn(__fmul_rn(b1, mi), __fmul_rn(1.0f - b1, gi));
-  vi = __fadd_rn(__fmul_rn(b2, vi), __fmul_rn(__fmul_rn(1.0f - b2, gi), gi));
-  const float den = __fadd_rn(__fsqrt_rn(__fmul_rn(vi, ic2)), eps);
-  pi = __fsub_rn(pi, __fdividef(__fmul_rn(lr, __fmul_rn(mi, ic1)), den));
-}
-
 __device__ __forceinline__ float adam_elem(float* p, const float* g, float* m, float* v, int64_t i, float lr, float b1,
                                            float b2, float eps, float c1, float c2) {
   float mi = m[i], vi = v[i], pi = p[i];

@@ -42,6 +42,19 @@ __device__ __forceinline__ void pdl_entry() {
 
 bool pdl_enabled();
 
+// Throughput-mode Adam element (the graph-captured learner; the parity agent's
+// ap_dqn_adam keeps the reference expression), shared by the Adam kernels and
+// the GEMM epilogue that fuses the first layer's update: explicitly rounded
+// operations (never contracted, so every kernel computes the same bits),
+// reciprocal bias corrections ic1 = 1/(1 - b1^t), ic2 = 1/(1 - b2^t), one fast divide.
+__device__ __forceinline__ void adam_math(float gi, float& mi, float& vi, float& pi, float lr, float b1, float b2,
+                                          float eps, float ic1, float ic2) {
+  mi = __fadd_rn(__fmul_rn(b1, mi), __fmul_rn(1.0f - b1, gi));
+  vi = __fadd_rn(__fmul_rn(b2, vi), __fmul_rn(__fmul_rn(1.0f - b2, gi), gi));
+  const float den = __fadd_rn(__fsqrt_rn(__fmul_rn(vi, ic2)), eps);
+  pi = __fsub_rn(pi, __fdividef(__fmul_rn(lr, __fmul_rn(mi, ic1)), den));
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
                               Args&&... args) {

@@ -44,6 +44,15 @@ struct G3 {
   int kps;      // k slices per split
   float* work;  // [splits, M, N] partials when split-K through global memory
   int cluster;  // split-K CTAs of a tile form one cluster: reduce through DSMEM
+  // fused Adam epilogue (am != nullptr; unsplit GEMMs only): C is a weight gradient,
+  // am / av / ap the Adam moments and parameters at C's offset (same layout, ld = ldc)
+  float *am, *av, *ap;
+  const int64_t* actl;
+  float lr, b1, b2, eps;
+  int t_add;       // Adam step t = ctl[AP_CTL_TRAIN] + t_add
+  float* tdst;     // transposed parameter copy tdst[c][r] for rows r < trows
+  int64_t tld;
+  int trows;
 };
 
 __device__ __forceinline__ uint32_t sa3(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -262,7 +271,58 @@ __global__ void __launch_bounds__(128) gemm_v3_kernel(const __grid_constant__ CU
   // walks rows; nothing in the loop waits on a global load
   const int rows = min(BM3, g.M - m0), cols = min(BN, g.N - n0);
   const int c = threadIdx.x % BN;
-  if (c < cols) {
+  if (g.am) {
+    // fused Adam: store the gradient, update moments and parameters in place,
+    // then write the transposed parameter copy from the tile (coalesced rows)
+    __shared__ float s_ic[2];
+    if (threadIdx.x == 0) {
+      const double t = (double)(g.actl[AP_CTL_TRAIN] + g.t_add);
+      s_ic[0] = (float)(1.0 / (1.0 - pow((double)g.b1, t)));
+      s_ic[1] = (float)(1.0 / (1.0 - pow((double)g.b2, t)));
+    }
+    __syncthreads();
+    const float ic1 = s_ic[0], ic2 = s_ic[1];
+    if (c < cols) {
+      constexpr int RS = 128 / BN, D = 8;  // row stride per thread; 8 rows' loads in flight
+      float* __restrict__ am = g.am;
+      float* __restrict__ av = g.av;
+      float* __restrict__ ap = g.ap;
+      for (int r0 = threadIdx.x / BN; r0 < rows; r0 += D * RS) {
+        float mi[D], vi[D], pi[D];
+#pragma unroll
+        for (int u = 0; u < D; ++u) {
+          const int r = r0 + u * RS;
+          if (r < rows) {
+            const int64_t i = (int64_t)(m0 + r) * ld + n0 + c;
+            mi[u] = am[i];
+            vi[u] = av[i];
+            pi[u] = ap[i];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < D; ++u) {
+          const int r = r0 + u * RS;
+          if (r < rows) {
+            const int64_t i = (int64_t)(m0 + r) * ld + n0 + c;
+            const float gr = tile[r * LDT + c];
+            out[i] = gr;
+            adam_math(gr, mi[u], vi[u], pi[u], g.lr, g.b1, g.b2, g.eps, ic1, ic2);
+            am[i] = mi[u];
+            av[i] = vi[u];
+            ap[i] = pi[u];
+            tile[r * LDT + c] = pi[u];
+          }
+        }
+      }
+    }
+    __syncthreads();
+    const int trr = min(rows, g.trows - m0);
+    if (g.tdst && trr > 0)
+      for (int e = threadIdx.x; e < cols * trr; e += blockDim.x) {
+        const int cc = e / trr, rr = e % trr;
+        g.tdst[(int64_t)(n0 + cc) * g.tld + m0 + rr] = tile[rr * LDT + cc];
+      }
+  } else if (c < cols) {
     const bool epi = !g.work;
     const bool has_bias = epi && g.bias;
     const float bc = has_bias ? g.bias[n0 + c] : 0.0f;
@@ -365,8 +425,18 @@ int run3(const CUtensorMap& ma, const CUtensorMap& mb, const G3& g, dim3 grid, c
 }  // namespace
 
 // TF32 only, both operands K-major (A [M, K], B [N, K]); AP_ERR_UNSUPPORTED otherwise.
+static int launch_v3_impl(const float* A, int64_t lda, int transA, const float* B, int64_t ldb, int transB, float* C,
+                          int64_t ldc, int M, int N, int K, const float* bias, int relu, int precision,
+                          cudaStream_t stream, const G3* adam);
+
 int launch_gemm_v3(const float* A, int64_t lda, int transA, const float* B, int64_t ldb, int transB, float* C,
                    int64_t ldc, int M, int N, int K, const float* bias, int relu, int precision, cudaStream_t stream) {
+  return launch_v3_impl(A, lda, transA, B, ldb, transB, C, ldc, M, N, K, bias, relu, precision, stream, nullptr);
+}
+
+static int launch_v3_impl(const float* A, int64_t lda, int transA, const float* B, int64_t ldb, int transB, float* C,
+                          int64_t ldc, int M, int N, int K, const float* bias, int relu, int precision,
+                          cudaStream_t stream, const G3* adam) {
   if (precision != 1 || transA || !transB || std::getenv("AP_GEMM_NO_TMA")) return AP_ERR_UNSUPPORTED;
   auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (!al(A) || !al(B) || lda % 4 || ldb % 4 || M < 1 || N < 1 || K < 1) return AP_ERR_UNSUPPORTED;
@@ -384,6 +454,11 @@ int launch_gemm_v3(const float* A, int64_t lda, int transA, const float* B, int6
   CUtensorMap ma, mb;
   if (!make_map(&ma, A, M, K, lda, BM3) || !make_map(&mb, B, N, K, ldb, bn)) return AP_ERR_UNSUPPORTED;
   G3 g{C, ldc, M, N, K, bias, relu, 0, nullptr, 0};
+  if (adam) {  // the Adam fields; bias / ReLU do not apply to a gradient
+    g = *adam;
+    g.C = C, g.ldc = ldc, g.M = M, g.N = N, g.K = K, g.bias = nullptr, g.relu = 0, g.kps = 0, g.work = nullptr;
+    g.cluster = 0;
+  }
   const int mt = (M + BM3 - 1) / BM3, nt = (N + bn - 1) / bn;
   const int nk = (K + BK3 - 1) / BK3;
   // split-K for grids that would leave SMs idle; the splits of a tile reduce
@@ -400,6 +475,7 @@ int launch_gemm_v3(const float* A, int64_t lda, int transA, const float* B, int6
   const bool four_stages = std::getenv("AP_GEMM_V3_STAGES") && std::atoi(std::getenv("AP_GEMM_V3_STAGES")) == 4;
   g.kps = (nk + splits - 1) / splits;
   splits = (nk + g.kps - 1) / g.kps;
+  if (adam && splits > 1) return AP_ERR_UNSUPPORTED;  // the fused epilogue needs the whole gradient tile
   if (splits > 1 && splits <= 16 && !no_cluster) g.cluster = 1;
   if (splits > 1 && !g.cluster) {
     const int wrc = splitk_workspace(stream, (size_t)splits * M * N * sizeof(float), &g.work);
@@ -424,3 +500,18 @@ extern "C" int ap_gemm_trace_read(long long* out) {
   return cudaMemcpyFromSymbol(out, apb::g_trace, sizeof(long long) * 8) == cudaSuccess ? 0 : -1;
 }
 #endif
+
+extern "C" int ap_gemm_tf32_adam(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
+                                 int32_t M, int32_t N, int32_t K, float* m, float* v, float* params,
+                                 const int64_t* ctl, int32_t counter_advanced, float lr, float beta1, float beta2,
+                                 float eps, float* t_dst, int64_t t_ld, int32_t t_rows, void* stream) {
+  if (!A || !B || !C || !m || !v || !params || !ctl || M < 1 || N < 1 || K < 1 || (t_dst && t_ld < t_rows)) {
+    apb::set_error("ap_gemm_tf32_adam: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  apb::G3 a{};
+  a.am = m, a.av = v, a.ap = params, a.actl = ctl;
+  a.lr = lr, a.b1 = beta1, a.b2 = beta2, a.eps = eps, a.t_add = counter_advanced ? 0 : 1;
+  a.tdst = t_dst, a.tld = t_ld, a.trows = t_dst ? t_rows : 0;
+  return apb::launch_v3_impl(A, lda, 0, B, ldb, 1, C, ldc, M, N, K, nullptr, 0, 1, (cudaStream_t)stream, &a);
+}

@@ -473,6 +473,8 @@ class VecDqnTrainer:
         step, then the sample + gather of step k + 1, run on a parallel branch beside
         the backward pass; the branch joins before Adam, which then reads the already
         advanced step counter.  Every value equals the serial order's."""
+        import torch
+
         cfg, r, b = self.config, self.ring, self.batch
         B = cfg.batch_size
         lib = _native.require_device()
@@ -496,17 +498,27 @@ class VecDqnTrainer:
                                          r["next_mask"].stride(0), P(self.weights), B, self.env.num_actions,
                                          float(cfg.gamma), float(cfg.huber_delta), P(b.dz), b.dz.stride(0),
                                          P(self.dz_t), self.dz_t.stride(0), P(b.td), P(b.loss_rows), _s()))
+        opt = self.opt
+        fused_adam = None
         if pipe:  # priority scatter (+ step counter) and the next step's sample / gather, beside the backward
             fork_to(self.side2)
             with stream_or_current(self.side2):
                 _native.check(lib.ap_per_update_scaled_ctl(P(r["priorities"]), P(self.idx), P(b.td), B,
                                                            float(cfg.per_alpha), P(self.ctl), _s()))
+                if self.pg is None and side is not None and os.environ.get("AP_FUSED_ADAM"):
+                    # opt-in (measured slower on B200: the gradient GEMM has too few CTAs to carry the
+                    # Adam traffic): the first layer's Adam in its weight-gradient GEMM epilogue, after
+                    # the step counter has advanced (the event), like the Adam below
+                    counted = torch.cuda.Event()
+                    counted.record(torch.cuda.current_stream())
+                    fused_adam = dict(m=opt.m, v=opt.v, ctl=self.ctl, counter_advanced=1, lr=opt.lr,
+                                      beta1=opt.beta1, beta2=opt.beta2, eps=opt.eps, wait=counted)
                 if prefetch_next:
                     self._sample_gather(k + 1)
-        self.net.backward_device(acts, b.dz, self.dz_t, side=side, dueling_td=True)
+        fused = self.net.backward_device(acts, b.dz, self.dz_t, side=side, dueling_td=True,
+                                         fused_w0_adam=fused_adam)
         if pipe:
             join_from(self.side2)
-        opt = self.opt
         if self.peer is not None:  # data-parallel: gradient all-reduce over NVLink peer memory fused with Adam
             x = self.peer
             _native.check(lib.ap_dp_allreduce_adam(x.world, x.rank, P(self.net.grad), x.xbuf_ptrs, x.pad_ptrs,
@@ -518,10 +530,11 @@ class VecDqnTrainer:
                 allreduce_mean_(self.net.grad, self.pg)
             # Adam also rewrites the transposed weight copies (no separate transpose launch;
             # measured faster than Adam + a tiled transpose even for the 4 M-parameter PP-train net)
-            sg = self.net.adam_segments()
-            _native.check(lib.ap_dqn_adam_ctl_t_adv(P(self.net.flat), P(self.net.grad), P(opt.m), P(opt.v),
-                                                    self.net.flat.numel(), opt.lr, opt.beta1, opt.beta2, opt.eps,
-                                                    P(self.ctl), *sg, 1 if pipe else 0, _s()))
+            o = self.net.w0_block() if fused else 0  # fused: w0 / b0 were updated by their gradient GEMM
+            sg = self.net.adam_segments(skip_w0=fused)
+            _native.check(lib.ap_dqn_adam_ctl_t_adv(P(self.net.flat[o:]), P(self.net.grad[o:]), P(opt.m[o:]),
+                                                    P(opt.v[o:]), self.net.flat.numel() - o, opt.lr, opt.beta1,
+                                                    opt.beta2, opt.eps, P(self.ctl), *sg, 1 if pipe else 0, _s()))
         if self.peer is not None:
             self.net.refresh_transposed()
         if not pipe:  # the priority scatter also counts the learn step (ctl[AP_CTL_TRAIN] += 1)

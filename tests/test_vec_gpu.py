@@ -262,3 +262,18 @@ def test_pipelined_learner_matches_serial(cuda, monkeypatch, use_graph):
     for k in a.ring:
         assert torch.equal(a.ring[k], b.ring[k]), k
     assert torch.equal(a.idx, b.idx) and torch.equal(a.weights, b.weights)
+
+
+@pytest.mark.parametrize("use_graph", [False, True])
+def test_fused_first_layer_adam_matches_unfused(cuda, monkeypatch, use_graph):
+    """Adam for w0 / b0 fused into their weight-gradient GEMM epilogue (+ the transposed w0
+    copy; opt-in AP_FUSED_ADAM=1) == the separate Adam kernel, bit for bit."""
+    a = _train(use_graph, 8, learn_steps=3)
+    monkeypatch.setenv("AP_FUSED_ADAM", "1")
+    b = _train(use_graph, 8, learn_steps=3)
+    for name in ("flat", "grad"):
+        assert torch.equal(getattr(a.net, name), getattr(b.net, name)), name
+    assert torch.equal(a.opt.m, b.opt.m) and torch.equal(a.opt.v, b.opt.v)
+    for k in a.net.wt:
+        assert torch.equal(a.net.wt[k], b.net.wt[k]), k
+    assert torch.equal(a.ctl, b.ctl)
