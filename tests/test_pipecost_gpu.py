@@ -316,7 +316,9 @@ def test_device_uniform_envs_match_generate_environment(cuda, n):
     from paper_2007_04069_b200.dataproc import generate_environment, generate_environments_device
 
     seeds = [0, 1, 7, 20201007, 2**40 + 3] + list(range(100, 120))
-    dev = generate_environments_device("uniform", n, seeds).cpu().numpy()
+    out = generate_environments_device("uniform", n, seeds)
+    assert out.shape == (len(seeds), 3, 128) and torch.isfinite(out).all()
+    dev = out.cpu().numpy()
     for i, s in enumerate(seeds):
         host = generate_environment("uniform", n, s)
         np.testing.assert_array_equal(dev[i, 0], host.c)

@@ -277,3 +277,25 @@ def test_fused_first_layer_adam_matches_unfused(cuda, monkeypatch, use_graph):
     for k in a.net.wt:
         assert torch.equal(a.net.wt[k], b.net.wt[k]), k
     assert torch.equal(a.ctl, b.ctl)
+
+
+@pytest.mark.parametrize("cols,pad", [(1060, 12), (1414, 2), (37, 3)])
+def test_gather_rows_pair_exact_and_in_bounds(cuda, cols, pad):
+    """ap_gather_rows_pair: both destinations get exactly src[idx[b], :cols] (16-byte vector path when
+    aligned, scalar otherwise); padding columns and rows past B keep their sentinel."""
+    from paper_2007_04069_b200 import _native
+
+    gen = torch.Generator(device="cuda").manual_seed(cols)
+    R, B = 300, 64
+    s0 = torch.randn(R, cols + pad, generator=gen, device="cuda")
+    s1 = torch.randn(R, cols + pad, generator=gen, device="cuda")
+    idx = torch.randint(0, R, (B,), generator=gen, device="cuda", dtype=torch.int32)
+    d = torch.full((2 * B + 3, cols + pad), float("nan"), device="cuda")
+    P = _native.ptr
+    _native.check(_native.require_device().ap_gather_rows_pair(
+        P(s0), s0.stride(0), P(d), d.stride(0), P(s1), s1.stride(0), P(d[B:]), d.stride(0), P(idx), B, cols,
+        _native.stream_handle()))
+    il = idx.long()
+    assert torch.equal(d[:B, :cols], s0[il, :cols])
+    assert torch.equal(d[B:2 * B, :cols], s1[il, :cols])
+    assert torch.isnan(d[:, cols:]).all() and torch.isnan(d[2 * B:]).all()
