@@ -444,7 +444,7 @@ static int launch_v3_impl(const float* A, int64_t lda, int transA, const float* 
   // than the BN=128 grid (measured: 12681x64x256 12.5 -> 9.4 us, 1024x256x3171 16.7 -> 12.4 us,
   // 257x64x3171 7.2 -> 5.3 us; grids that fit one wave either way stay at 64).  AP_GEMM_V3_BN=64|128 forces.
   const int env_bn = std::getenv("AP_GEMM_V3_BN") ? std::atoi(std::getenv("AP_GEMM_V3_BN")) : 0;
-  int bn = N <= 32 ? 32 : 64;
+  int bn = (N <= 32 || env_bn == 32) ? 32 : 64;
   if (bn == 64 && N > 64) {
     const int64_t mt0 = (M + BM3 - 1) / BM3;
     const int64_t w64 = (mt0 * ((N + 63) / 64) + 147) / 148, w128 = (mt0 * ((N + 127) / 128) + 147) / 148;
