@@ -101,7 +101,8 @@ __host__ __device__ inline void proportional_counts(const double* comp, int k, i
 }
 
 // ring allreduce over devices [start, end) (topology.py:131-148)
-__host__ __device__ inline double allreduce(const Topo& t, double bytes, int start, int end) {
+__host__ __device__ inline double allreduce(const Topo& t, double bytes, int start, int end,
+                                            const double* fac = nullptr) {
   const int n = end - start;
   if (n <= 1 || bytes == 0.0) return 0.0;
   // the slowest link of the ring start -> .. -> end-1 -> start, in closed form
@@ -113,7 +114,8 @@ __host__ __device__ inline double allreduce(const Topo& t, double bytes, int sta
   double slow = INFINITY;
   if (has_inter && t.inter < slow) slow = t.inter;
   if (has_intra && t.intra < slow) slow = t.intra;
-  return ((2.0 * (double)(n - 1)) / (double)n) * bytes / slow;
+  // fac (optional): fac[n] = (2.0 * (n - 1)) / n precomputed with the same operations
+  return (fac ? fac[n] : (2.0 * (double)(n - 1)) / (double)n) * bytes / slow;
 }
 
 // transfer between consecutive groups (topology.py:121-128)
@@ -309,13 +311,13 @@ __global__ void candidates_kernel(int F, const double* prefix, double total, con
 // Raw PipeTrainEnv._state features of one candidate from its stage metrics
 // (envs.py:378-397): max allreduce, max transfer, min/max compute balance.
 __device__ inline void train_features(const Topo& t, int K, const double* c, const double* a, const double* w,
-                                      double* red_o, double* tra_o, double* bal_o) {
+                                      double* red_o, double* tra_o, double* bal_o, const double* fac = nullptr) {
   int counts[kMaxStages], start[kMaxStages], end[kMaxStages];
   proportional_counts(c, K, t.d, counts);
   groups_from_counts(counts, K, start, end);
   double red = 0.0, tra = 0.0, top = c[0], bot = c[0];
   for (int s = 0; s < K; ++s) {
-    const double r = allreduce(t, w[s], start[s], end[s]);
+    const double r = allreduce(t, w[s], start[s], end[s], fac);
     if (s == 0 || r > red) red = r;
     if (c[s] > top) top = c[s];
     if (c[s] < bot) bot = c[s];
@@ -666,6 +668,8 @@ __global__ void train_table_kernel(PipeDev pd, const int32_t* cand_pos, int C, d
   }
 }
 
+constexpr int kFacMax = 512;  // devices covered by the table kernel's allreduce-factor table
+
 // Per-env constants of the fixed stages (stage_tail's terms for cuts that are
 // the same for every candidate of the env).
 struct FixedStages {
@@ -683,7 +687,7 @@ struct FixedStages {
 template <int KC>
 __device__ __forceinline__ void cand_features(const PipeDev& pd, const Topo& t, int Kr, const FixedStages& fs,
                                               double comp_mid, double comp_tail, int pos, double scale, double* red,
-                                              double* tra, double* bal) {
+                                              double* tra, double* bal, const double* fac) {
   constexpr int KM = KC ? KC : kMaxStages;
   const int K = KC ? KC : Kr;
   const int P0 = K - 2;
@@ -702,7 +706,7 @@ __device__ __forceinline__ void cand_features(const PipeDev& pd, const Topo& t, 
   c[P0 + 1] = comp_tail * scale;
   a[P0 + 1] = 0.0;
   w[P0 + 1] = (double)(pd.wtotal - wp);
-  train_features(t, K, c, a, w, red, tra, bal);
+  train_features(t, K, c, a, w, red, tra, bal, fac);
 }
 
 __global__ void index_positions_kernel(const int32_t* cand_pos, int C, int F, int32_t* idx_of_pos) {
@@ -757,11 +761,11 @@ template <int KC>
 __device__ __forceinline__ void tab_candidates(const PipeDev& pd, const Topo& t, const int32_t* cand_pos, int C,
                                                const double* Trow, const double* tail, const uint8_t* m,
                                                const FixedStages& fs, double scale, double* st, double& mr,
-                                               double& mt) {
+                                               double& mt, const double* fac) {
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
     double red = 0.0, tra = 0.0, bal = 0.0;
     if (m[c])  // stages: fixed..., [start(alast) .. cand_pos[c]], [cand_pos[c]+1 .. F-1]
-      cand_features<KC>(pd, t, fs.P0 + 2, fs, Trow[c], tail[c], cand_pos[c], scale, &red, &tra, &bal);
+      cand_features<KC>(pd, t, fs.P0 + 2, fs, Trow[c], tail[c], cand_pos[c], scale, &red, &tra, &bal, fac);
     st[c] = red;
     st[C + c] = tra;
     st[2 * C + c] = bal;
@@ -781,8 +785,14 @@ __global__ void __launch_bounds__(256, AP_PP_TAB_MINB) train_state_tab_kernel(Pi
   pdl_entry();
   __shared__ FixedStages fs;
   __shared__ double s_max[2][32];
+  __shared__ double s_fac[kFacMax + 1];  // ring allreduce factors (2(n-1))/n, n <= devices
   const int64_t W = C + 1;
   const double* tail = T + W * W;
+  const double* fac = nullptr;
+  if (t.d <= kFacMax) {
+    for (int n = threadIdx.x; n <= t.d; n += blockDim.x) s_fac[n] = n >= 1 ? (2.0 * (double)(n - 1)) / (double)n : 0.0;
+    fac = s_fac;  // published by the first barrier of the env loop
+  }
   for (int64_t e = blockIdx.x; e < E; e += gridDim.x) {
     if (threadIdx.x == 0) {
       int P0 = 0, a0 = 0;
@@ -811,13 +821,13 @@ __global__ void __launch_bounds__(256, AP_PP_TAB_MINB) train_state_tab_kernel(Pi
     const uint8_t* m = mask + e * (int64_t)C;
     double mr = 0.0, mt = 0.0;
     switch (P0 + 2) {  // CTA-uniform
-      case 2: tab_candidates<2>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt); break;
-      case 3: tab_candidates<3>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt); break;
-      case 4: tab_candidates<4>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt); break;
-      case 5: tab_candidates<5>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt); break;
-      case 6: tab_candidates<6>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt); break;
-      case 8: tab_candidates<8>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt); break;
-      default: tab_candidates<0>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt); break;
+      case 2: tab_candidates<2>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt, fac); break;
+      case 3: tab_candidates<3>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt, fac); break;
+      case 4: tab_candidates<4>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt, fac); break;
+      case 5: tab_candidates<5>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt, fac); break;
+      case 6: tab_candidates<6>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt, fac); break;
+      case 8: tab_candidates<8>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt, fac); break;
+      default: tab_candidates<0>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt, fac); break;
     }
     for (int o = 16; o > 0; o >>= 1) {
       mr = fmax(mr, __shfl_xor_sync(0xffffffffu, mr, o));
