@@ -686,8 +686,9 @@ struct FixedStages {
 // train_features over the full cut list.
 template <int KC>
 __device__ __forceinline__ void cand_features(const PipeDev& pd, const Topo& t, int Kr, const FixedStages& fs,
-                                              double comp_mid, double comp_tail, int pos, double scale, double* red,
-                                              double* tra, double* bal, const double* fac) {
+                                              double comp_mid, double comp_tail, int64_t wp, int64_t cross,
+                                              double scale, double* red, double* tra, double* bal,
+                                              const double* fac) {
   constexpr int KM = KC ? KC : kMaxStages;
   const int K = KC ? KC : Kr;
   const int P0 = K - 2;
@@ -699,9 +700,8 @@ __device__ __forceinline__ void cand_features(const PipeDev& pd, const Topo& t, 
       a[k] = fs.act[k];
       w[k] = fs.param[k];
     }
-  const int64_t wp = pd.wprefix[pos];
   c[P0] = comp_mid * scale;
-  a[P0] = (double)pd.crossing[pos];
+  a[P0] = (double)cross;
   w[P0] = (double)(wp - fs.wlast);
   c[P0 + 1] = comp_tail * scale;
   a[P0 + 1] = 0.0;
@@ -709,10 +709,16 @@ __device__ __forceinline__ void cand_features(const PipeDev& pd, const Topo& t, 
   train_features(t, K, c, a, w, red, tra, bal, fac);
 }
 
-__global__ void index_positions_kernel(const int32_t* cand_pos, int C, int F, int32_t* idx_of_pos) {
+__global__ void index_positions_kernel(const int32_t* cand_pos, int C, int F, int32_t* idx_of_pos, PipeDev pd,
+                                       int64_t* cand_wpre, int64_t* cand_cross) {
   pdl_entry();
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < C && cand_pos[c] >= 0 && cand_pos[c] < F) idx_of_pos[cand_pos[c]] = c;
+  if (c >= C) return;
+  const int pos = cand_pos[c];
+  const bool ok = pos >= 0 && pos < F;
+  if (ok) idx_of_pos[pos] = c;
+  cand_wpre[c] = ok ? pd.wprefix[pos] : 0;
+  cand_cross[c] = ok ? pd.crossing[pos] : 0;
 }
 
 // Batched stage_metrics from the table: a tuple whose pivots are all bound
@@ -758,14 +764,16 @@ __global__ void metrics_tab_kernel(PipeDev pd, const int32_t* idx_of_pos, int C,
 // normalisation and the one-hot block -- one launch, the state written once
 // and normalised from L1/L2.
 template <int KC>
-__device__ __forceinline__ void tab_candidates(const PipeDev& pd, const Topo& t, const int32_t* cand_pos, int C,
+__device__ __forceinline__ void tab_candidates(const PipeDev& pd, const Topo& t, const int64_t* cand_wpre,
+                                               const int64_t* cand_cross, int C,
                                                const double* Trow, const double* tail, const uint8_t* m,
                                                const FixedStages& fs, double scale, double* st, double& mr,
                                                double& mt, const double* fac) {
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
     double red = 0.0, tra = 0.0, bal = 0.0;
     if (m[c])  // stages: fixed..., [start(alast) .. cand_pos[c]], [cand_pos[c]+1 .. F-1]
-      cand_features<KC>(pd, t, fs.P0 + 2, fs, Trow[c], tail[c], cand_pos[c], scale, &red, &tra, &bal, fac);
+      cand_features<KC>(pd, t, fs.P0 + 2, fs, Trow[c], tail[c], cand_wpre[c], cand_cross[c], scale, &red, &tra,
+                        &bal, fac);
     st[c] = red;
     st[C + c] = tra;
     st[2 * C + c] = bal;
@@ -777,8 +785,9 @@ __device__ __forceinline__ void tab_candidates(const PipeDev& pd, const Topo& t,
 #ifndef AP_PP_TAB_MINB
 #define AP_PP_TAB_MINB 4  // measured on B200: 4 (64 regs) > 3 > 2 (124 regs, 25% occupancy)
 #endif
-__global__ void __launch_bounds__(256, AP_PP_TAB_MINB) train_state_tab_kernel(PipeDev pd, Topo t, const int32_t* cand_pos, int C,
-                                                              const double* T, const int32_t* applied, int A,
+__global__ void __launch_bounds__(256, AP_PP_TAB_MINB) train_state_tab_kernel(PipeDev pd, Topo t, const int32_t* cand_pos,
+                                                              const int64_t* cand_wpre, const int64_t* cand_cross,
+                                                              int C, const double* T, const int32_t* applied, int A,
                                                               const uint8_t* mask, int64_t E, double scale,
                                                               double* state, float* f32a, int64_t lda32,
                                                               float* f32b, int64_t ldb32) {
@@ -821,13 +830,13 @@ __global__ void __launch_bounds__(256, AP_PP_TAB_MINB) train_state_tab_kernel(Pi
     const uint8_t* m = mask + e * (int64_t)C;
     double mr = 0.0, mt = 0.0;
     switch (P0 + 2) {  // CTA-uniform
-      case 2: tab_candidates<2>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt, fac); break;
-      case 3: tab_candidates<3>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt, fac); break;
-      case 4: tab_candidates<4>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt, fac); break;
-      case 5: tab_candidates<5>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt, fac); break;
-      case 6: tab_candidates<6>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt, fac); break;
-      case 8: tab_candidates<8>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt, fac); break;
-      default: tab_candidates<0>(pd, t, cand_pos, C, Trow, tail, m, fs, scale, st, mr, mt, fac); break;
+      case 2: tab_candidates<2>(pd, t, cand_wpre, cand_cross, C, Trow, tail, m, fs, scale, st, mr, mt, fac); break;
+      case 3: tab_candidates<3>(pd, t, cand_wpre, cand_cross, C, Trow, tail, m, fs, scale, st, mr, mt, fac); break;
+      case 4: tab_candidates<4>(pd, t, cand_wpre, cand_cross, C, Trow, tail, m, fs, scale, st, mr, mt, fac); break;
+      case 5: tab_candidates<5>(pd, t, cand_wpre, cand_cross, C, Trow, tail, m, fs, scale, st, mr, mt, fac); break;
+      case 6: tab_candidates<6>(pd, t, cand_wpre, cand_cross, C, Trow, tail, m, fs, scale, st, mr, mt, fac); break;
+      case 8: tab_candidates<8>(pd, t, cand_wpre, cand_cross, C, Trow, tail, m, fs, scale, st, mr, mt, fac); break;
+      default: tab_candidates<0>(pd, t, cand_wpre, cand_cross, C, Trow, tail, m, fs, scale, st, mr, mt, fac); break;
     }
     for (int o = 16; o > 0; o >>= 1) {
       mr = fmax(mr, __shfl_xor_sync(0xffffffffu, mr, o));
@@ -1216,6 +1225,8 @@ struct ap_pipe {
     int32_t C;
     double* tab;
     int32_t* idx_of_pos;  // [F]: candidate index at a forward position, -1 elsewhere
+    int64_t* cand_wpre;   // [C]: wprefix at each candidate's position (no dependent gather per candidate)
+    int64_t* cand_cross;  // [C]: crossing bytes at each candidate's position
   };
   std::vector<TableBinding> tables;
   const TableBinding* binding(const int32_t* cand, int32_t C) const {
@@ -1270,6 +1281,8 @@ struct ap_pipe {
     for (auto& b : tables) {
       cudaFree(b.tab);
       cudaFree(b.idx_of_pos);
+      cudaFree(b.cand_wpre);
+      cudaFree(b.cand_cross);
     }
     tables.clear();
     if (d_fixed) cudaFree(d_fixed);
@@ -1460,16 +1473,20 @@ int ap_pipe_train_table(ap_pipe_t p, const int32_t* cand_pos, int32_t C, void* s
       return AP_ERR_INVALID;
     }
     int32_t* iop = nullptr;
+    int64_t *cw = nullptr, *cx = nullptr;
     AP_CUDA_CHECK(cudaMalloc(&tab, bytes));
     AP_CUDA_CHECK(cudaMalloc(&iop, (size_t)p->F * sizeof(int32_t)));
-    p->tables.push_back({cand_pos, C, tab, iop});
+    AP_CUDA_CHECK(cudaMalloc(&cw, (size_t)C * sizeof(int64_t)));
+    AP_CUDA_CHECK(cudaMalloc(&cx, (size_t)C * sizeof(int64_t)));
+    p->tables.push_back({cand_pos, C, tab, iop, cw, cx});
   }
   // (re)built from the list's current contents
   const auto* bnd = p->binding(cand_pos, C);
   launch_pdl(train_table_kernel, dim3((int)((W + 127) / 128)), dim3(128), 0, (cudaStream_t)stream, p->dev(), cand_pos, C, tab);
   AP_CUDA_CHECK(cudaGetLastError());
   AP_CUDA_CHECK(cudaMemsetAsync(bnd->idx_of_pos, 0xff, (size_t)p->F * sizeof(int32_t), (cudaStream_t)stream));
-  launch_pdl(index_positions_kernel, dim3((C + 255) / 256), dim3(256), 0, (cudaStream_t)stream, cand_pos, C, p->F, bnd->idx_of_pos);
+  launch_pdl(index_positions_kernel, dim3((C + 255) / 256), dim3(256), 0, (cudaStream_t)stream, cand_pos, C, p->F,
+             bnd->idx_of_pos, p->dev(), bnd->cand_wpre, bnd->cand_cross);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
@@ -1524,10 +1541,11 @@ int train_state_impl(ap_pipe_t p, const ap_topology* topo, const int32_t* cand_p
   if ((rc = p->ensure()) != AP_OK) return rc;
   if (E == 0) return AP_OK;
   const Topo t = make_topo(topo);
-  const double* tab = std::getenv("AP_PP_NO_TABLE") ? nullptr : p->table_for(cand_pos, C);
-  if (tab) {  // bound candidate list: stage sums are lookups (one launch)
-    launch_pdl(train_state_tab_kernel, dim3((int)std::min<int64_t>(E, 148 * 8)), dim3(256), 0, (cudaStream_t)stream, 
-        p->dev(), t, cand_pos, C, tab, applied, A, mask, E, 1.0 + bwm, state, f32a, lda32, f32b, ldb32);
+  const auto* bnd = std::getenv("AP_PP_NO_TABLE") ? nullptr : p->binding(cand_pos, C);
+  if (bnd) {  // bound candidate list: stage sums are lookups (one launch)
+    launch_pdl(train_state_tab_kernel, dim3((int)std::min<int64_t>(E, 148 * 8)), dim3(256), 0, (cudaStream_t)stream,
+               p->dev(), t, cand_pos, (const int64_t*)bnd->cand_wpre, (const int64_t*)bnd->cand_cross, C,
+               (const double*)bnd->tab, applied, A, mask, E, 1.0 + bwm, state, f32a, lda32, f32b, ldb32);
     AP_CUDA_CHECK(cudaGetLastError());
     return AP_OK;
   }
