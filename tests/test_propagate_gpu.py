@@ -283,3 +283,44 @@ def test_real_hlo_scale_matches_oracle(cuda, layers):
     ok = oc != 2
     assert ok.sum() >= 16
     np.testing.assert_array_equal(out["slots"].cpu().numpy()[ok][:, : flat.num_slots], st[ok])
+
+
+def test_full_size_batch_properties(cuda):
+    """BERT-48 at the bench's batch size (2^20 plans of the workload generator): outcomes and counts
+    are consistent (conflict -> zero counts; complete <=> every candidate decided), results are
+    deterministic and independent of how the batch is chunked, and sampled rows from across the whole
+    batch (first, middle, last) match the C oracle slot for slot."""
+    from paper_2007_04069_b200.workloads import prefix_seed_batch
+
+    g = graphs.generate("bert48")
+    dims = decision_dims(g, g.trainable_variables)
+    n = len(dims)
+    order = np.asarray([d.flat_index for d in sorted_decision_order(extract_linkage_groups(g, dims))])
+    B = 1 << 20
+    seeds = prefix_seed_batch(order, 0, B, device="cuda")
+    eng = PropagationEngine(g, dims)
+    a = eng.run_batch(seeds, want_slots=True)
+    oc, cnt = a["outcome"].long(), a["counts"]
+    assert bool(((oc >= 0) & (oc <= 2)).all())
+    conf = oc == 2
+    assert bool((cnt[conf] == 0).all())
+    decided = cnt[:, 0] + cnt[:, 1]
+    assert bool(((decided == n) == (oc == 0))[~conf].all())
+    assert bool((cnt[:, 2] <= cnt[:, 0]).all()) and bool((cnt[:, 3] <= cnt[:, 1]).all())
+    # deterministic, and chunking does not change any row
+    b = eng.run_batch(seeds, want_slots=True)
+    assert torch.equal(a["outcome"], b["outcome"]) and torch.equal(a["slots"], b["slots"])
+    cuts = [0, 333_333, 777_777, B]
+    for lo, hi in zip(cuts, cuts[1:]):
+        c = eng.run_batch(seeds[lo:hi], want_slots=True)
+        assert torch.equal(c["outcome"], a["outcome"][lo:hi]) and torch.equal(c["slots"], a["slots"][lo:hi])
+        assert torch.equal(c["counts"], a["counts"][lo:hi])
+    rows = np.concatenate([np.arange(64), np.arange(B // 2, B // 2 + 64), np.arange(B - 64, B)])
+    flat = g.flat()
+    cand_slots = np.array([flat.slot_offset[d.instruction_id] + d.dim for d in dims])
+    sub = seeds[torch.from_numpy(rows).cuda()].cpu().numpy()
+    st, ocr, _ = oracle.propagate_batch(flat, cand_slots, sub, cand_slots)
+    np.testing.assert_array_equal(a["outcome"][torch.from_numpy(rows).cuda()].cpu().numpy(), ocr)
+    ok = ocr != 2
+    np.testing.assert_array_equal(a["slots"][torch.from_numpy(rows).cuda()].cpu().numpy()[ok][:, : flat.num_slots],
+                                  st[ok])
