@@ -186,8 +186,8 @@ def test_scalar_api(cuda):
         pc.stage_metrics(g, [order[5], order[3]])
 
 
-@pytest.mark.parametrize("K", [2, 3, 4, 6])
-def test_train_state_reuse_matches_full_sweep(cuda, monkeypatch, K):
+@pytest.mark.parametrize("K,E", [(2, 48), (3, 48), (4, 48), (6, 48), (4, 512)])
+def test_train_state_reuse_matches_full_sweep(cuda, monkeypatch, K, E):
     """K2 from the bound stage-sum table, and with per-env reuse (fixed stages + running
     sums once per env, per-candidate tails; AP_PP_NO_TABLE=1), are bit-identical to one
     full sequential sweep per candidate (AP_PP_FULL=1)."""
@@ -202,7 +202,6 @@ def test_train_state_reuse_matches_full_sweep(cuda, monkeypatch, K):
     topo = DeviceTopology(2, 4)
     env = PipeTrainEnv(g, topo, K, radius=3)
     C = env.num_actions
-    E = 48
     A = max(1, K - 2)
     rng = np.random.default_rng(K)
     applied = np.full((E, A), -1, dtype=np.int32)
