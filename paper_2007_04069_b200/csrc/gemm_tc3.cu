@@ -472,7 +472,8 @@ static int launch_v3_impl(const float* A, int64_t lda, int transA, const float* 
   if (mt * nt < 120 && nk >= 16) splits = std::min(std::min(nk / 2, max_split), std::max(1, 148 / (mt * nt)));
   // dev knobs for sweeps: AP_GEMM_V3_SPLITS (forced split count), AP_GEMM_V3_STAGES (4 | 6)
   if (const char* e = std::getenv("AP_GEMM_V3_SPLITS")) splits = std::max(1, std::min(std::atoi(e), nk));
-  const bool four_stages = std::getenv("AP_GEMM_V3_STAGES") && std::atoi(std::getenv("AP_GEMM_V3_STAGES")) == 4;
+  const int env_stages = std::getenv("AP_GEMM_V3_STAGES") ? std::atoi(std::getenv("AP_GEMM_V3_STAGES")) : 0;
+  const bool four_stages = env_stages == 4, eight_stages = env_stages == 8 && bn == 64;
   g.kps = (nk + splits - 1) / splits;
   splits = (nk + g.kps - 1) / g.kps;
   if (adam && splits > 1) return AP_ERR_UNSUPPORTED;  // the fused epilogue needs the whole gradient tile
@@ -483,6 +484,7 @@ static int launch_v3_impl(const float* A, int64_t lda, int transA, const float* 
   }
   const dim3 grid(mt, nt, splits);
   const int rc = bn == 128     ? run3<128, 6>(ma, mb, g, grid, stream)
+                 : eight_stages ? run3<64, 8>(ma, mb, g, grid, stream)
                  : four_stages ? (bn == 32 ? run3<32, 4>(ma, mb, g, grid, stream) : run3<64, 4>(ma, mb, g, grid, stream))
                                : (bn == 32 ? run3<32, 6>(ma, mb, g, grid, stream) : run3<64, 6>(ma, mb, g, grid, stream));
   if (rc != AP_OK || splits == 1 || g.cluster) return rc;
