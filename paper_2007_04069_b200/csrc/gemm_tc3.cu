@@ -343,6 +343,134 @@ __global__ void __launch_bounds__(128) gemm_v3_kernel(const __grid_constant__ CU
   if (threadIdx.x == 0) GTRACE(5);
 }
 
+// A-tile multicast variant (unsplit grids, plain bias / ReLU epilogue): the MC
+// CTAs of a cluster share an M tile and take consecutive N tiles; each loads a
+// 1/MC slice of the A tile and multicasts it to every CTA of the cluster, so
+// A is read once per cluster instead of once per CTA.  A stage is released
+// when all MC consumers have committed (empty barriers count MC, every MMA
+// commit arrives on the whole cluster).
+template <int BN, int STAGES, int MC>
+__global__ void __launch_bounds__(128) gemm_v3_mc_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                         const __grid_constant__ CUtensorMap tmB, G3 g) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], done;
+  __shared__ uint32_t tmem_slot;
+  constexpr int A_BYTES = BM3 * BK3 * 4;
+  constexpr int B_BYTES = BN * BK3 * 4;
+  constexpr int STAGE = A_BYTES + B_BYTES;
+  constexpr int AQ = A_BYTES / MC;  // one CTA's slice of the A tile (BM3 / MC rows)
+  constexpr uint16_t kMask = (uint16_t)((1u << MC) - 1u);
+  const uint32_t base = (sa3(smem_raw) + 1023u) & ~1023u;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM3, n0 = blockIdx.y * BN;
+  const int nk = (g.K + BK3 - 1) / BK3;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(sa3(&tmem_slot)), "r"(BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < STAGES; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa3(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa3(&empty[s])), "r"(MC));
+    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa3(&done)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  // every barrier of the cluster is initialised before any multicast can reach it
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  const uint32_t tmem = tmem_slot;
+  pdl_trigger();
+  pdl_wait();
+
+  if (threadIdx.x == 0) {
+    for (int it = 0; it < nk; ++it) {
+      const int s = it % STAGES;
+      if (it >= STAGES) mbar_wait(sa3(&empty[s]), ((it / STAGES) - 1) & 1);
+      const uint32_t st = base + s * STAGE;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa3(&full[s])), "r"(STAGE)
+                   : "memory");
+      const int kc = it * BK3;
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+          " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(st + rank * AQ),
+          "l"(&tmA), "r"(kc), "r"(m0 + (int)rank * (BM3 / MC)), "r"(sa3(&full[s])), "h"(kMask)
+          : "memory");
+      tma_load_2d(st + A_BYTES, &tmB, kc, n0, sa3(&full[s]));
+    }
+  } else if (threadIdx.x == 32) {
+    const uint32_t idesc =
+        (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM3 >> 4) << 24);
+    for (int it = 0; it < nk; ++it) {
+      const int s = it % STAGES;
+      mbar_wait(sa3(&full[s]), (it / STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t a = base + s * STAGE, b = a + A_BYTES;
+#pragma unroll
+      for (int ks = 0; ks < BK3 / 8; ++ks) {
+        const uint64_t da = desc_sw128(a + ks * 32), db = desc_sw128(b + ks * 32);
+        const uint32_t acc = (it | ks) != 0;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+            "l"(da), "l"(db), "r"(idesc), "r"(acc));
+      }
+      asm volatile(
+          "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+              sa3(&empty[s])),
+          "h"(kMask)
+          : "memory");
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sa3(&done))
+                 : "memory");
+  }
+  __syncwarp();
+  if (nk > 0) mbar_wait(sa3(&done), 0);
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  // epilogue: as gemm_v3_kernel (staged tile, one column per thread)
+  constexpr int LDT = BN + 1;
+  float* tile = reinterpret_cast<float*>(smem_raw + (base - sa3(smem_raw)));
+  const int lrow = warp * 32 + lane;
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN; c0 += 16) {
+    uint32_t v[16];
+    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int t = 0; t < 16; ++t) tile[lrow * LDT + c0 + t] = nk > 0 ? __uint_as_float(v[t]) : 0.0f;
+  }
+  __syncthreads();
+  const int rows = min(BM3, g.M - m0), cols = min(BN, g.N - n0);
+  const int c = threadIdx.x % BN;
+  if (c < cols) {
+    const float bc = g.bias ? g.bias[n0 + c] : 0.0f;
+    float* __restrict__ o = g.C + (int64_t)m0 * g.ldc + n0 + c;
+#pragma unroll 4
+    for (int r = threadIdx.x / BN; r < rows; r += 128 / BN) {
+      float x = tile[r * LDT + c];
+      if (g.bias) x += bc;
+      if (g.relu) x = fmaxf(x, 0.0f);
+      o[(int64_t)r * g.ldc] = x;
+    }
+  }
+  // no CTA may exit while a peer's multicast commit can still arrive on its barriers
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+}
+
 __global__ void splitk_reduce3_kernel(const float* work, int splits, int M, int N, float* C, int64_t ldc,
                                       const float* bias, int relu) {
   const int64_t total = (int64_t)M * N;
@@ -483,6 +611,37 @@ static int launch_v3_impl(const float* A, int64_t lda, int transA, const float* 
     if (wrc != AP_OK) return wrc;
   }
   const dim3 grid(mt, nt, splits);
+  // A-tile multicast across 4 N tiles of a cluster for unsplit grids with K >= 512 (measured on B200:
+  // 4096x1060x256 14.3 -> 12.7 us; at K = 256 the cluster syncs cost more than the saved A reads, 5.6 -> 6.3 us).
+  // AP_GEMM_NO_MC=1 disables it, AP_GEMM_MC=1 forces it for any eligible shape.
+  const bool use_mc = !std::getenv("AP_GEMM_NO_MC") && (std::getenv("AP_GEMM_MC") || nk >= 16);
+  if (!adam && splits == 1 && bn == 64 && nt % 4 == 0 && use_mc) {
+    CUtensorMap maq;
+    if (!make_map(&maq, A, M, K, lda, BM3 / 4)) return AP_ERR_UNSUPPORTED;
+    constexpr int SMEM = (BM3 + 64) * BK3 * 4 * 6 + 1024;
+    auto k = gemm_v3_mc_kernel<64, 6, 4>;
+    static bool mc_configured = false;
+    if (!mc_configured) {
+      AP_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
+      mc_configured = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = SMEM;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 4;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    AP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k, maq, mb, g));
+    return AP_OK;
+  }
   const int rc = bn == 128     ? run3<128, 6>(ma, mb, g, grid, stream)
                  : eight_stages ? run3<64, 8>(ma, mb, g, grid, stream)
                  : four_stages ? (bn == 32 ? run3<32, 4>(ma, mb, g, grid, stream) : run3<64, 4>(ma, mb, g, grid, stream))

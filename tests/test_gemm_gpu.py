@@ -127,3 +127,22 @@ def test_bn128_tiles_match_bn64(cuda, m, n, k, monkeypatch):
     r = ref(a, b, False, True, bias, True)
     assert (outs[1].double() - r).abs().max().item() < 5e-3 * r.abs().max().item()
     assert (outs[1] - outs[0]).abs().max().item() <= 1e-5 * r.abs().max().item()
+
+
+@pytest.mark.parametrize("m,n,k", [(4096, 256, 1060), (4096, 256, 256), (257, 256, 64), (1000, 512, 96),
+                                   (300, 256, 1060)])
+def test_a_multicast_matches_plain(cuda, m, n, k, monkeypatch):
+    """A-tile multicast across a 4-CTA cluster (each CTA loads a quarter of the A tile for all four)
+    == the one-CTA kernel, bit for bit (same MMAs in the same k order)."""
+    g = torch.Generator(device="cuda").manual_seed(m + n + k)
+    a = torch.randn((m, k), device="cuda", generator=g)
+    b = torch.randn((n, k), device="cuda", generator=g)
+    bias = torch.randn(n, device="cuda", generator=g)
+    monkeypatch.setenv("AP_GEMM_MC", "1")
+    mc = gemm(a, b, trans_b=True, bias=bias, relu=True, precision=1)
+    monkeypatch.delenv("AP_GEMM_MC")
+    monkeypatch.setenv("AP_GEMM_NO_MC", "1")
+    plain = gemm(a, b, trans_b=True, bias=bias, relu=True, precision=1)
+    assert torch.equal(mc, plain)
+    r = ref(a, b, False, True, bias, True)
+    assert (mc.double() - r).abs().max().item() < 5e-3 * r.abs().max().item()
