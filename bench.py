@@ -224,8 +224,10 @@ def cpu_baseline_single(g, dims, order, seconds: float):
         "unit": UNIT,
         "cores": 1,
         "kind": kind,
-        "sample": f"first {done} plans of the same batch, PropagationEngine(graph, dims).run per plan, engine reused, "
-                  f"{dt:.1f} s on 1 host core",
+        "sample": f"first {done} plans of the same batch, "
+                  + ("PropagationEngine(graph, dims).run per plan, engine reused, " if kind == "reference"
+                     else "C oracle port (baseline/_ref not installed), 64-plan batches, ")
+                  + f"{dt:.2f} s on 1 host core",
     }
 
 
