@@ -380,12 +380,31 @@ def run_ours(args):
         out_host = eng.run_batch_host(seeds_host, out=out_host)
     e2e_s = time.perf_counter() - t0
     e2e_s = _max_over_ranks(e2e_s, world)
+    # the same host API with 2-bit packed slot rows (ap_pack_slots2): a quarter of the slot D2H
+    out_pk = None
+    for _ in range(2):
+        out_pk = eng.run_batch_host(seeds_host, want_slots="packed", out=out_pk)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        out_pk = eng.run_batch_host(seeds_host, want_slots="packed", out=out_pk)
+    e2e_pk_s = _max_over_ranks(time.perf_counter() - t0, world)
+    e2e_packed = {
+        "value": world * Be * args.e2e_steps / e2e_pk_s,
+        "unit": UNIT,
+        "h2d_bytes_per_step": Be * n,
+        "d2h_bytes_per_step": Be * (eng.packed_slots_stride + 1 + 16),
+        "api": 'PropagationEngine.run_batch_host(want_slots="packed") (K1 + ap_pack_slots2, 2-bit slot rows to host)',
+    }
+    del out_pk
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_single(g, dims, order, args.cpu_seconds)
 
-    secondary = {}
+    secondary = {"e2e_packed_slots": e2e_packed}
     if not args.no_secondary:
         want_cpu = rank == 0 and world == 1 and not args.no_cpu_baseline
         secondary["dqn_env_steps_per_s"] = bench_dqn_vec(args, g, world, rank)

@@ -217,6 +217,14 @@ int ap_pipe_train_state_ex(ap_pipe_t p, const ap_topology* topo, const int32_t* 
                            double backward_multiplier, double* state_dev, float* state_f32, int64_t ld_f32,
                            float* state_f32_b, int64_t ld_f32_b, void* stream);
 
+/* Host-consumer slot format (run_batch_host(want_slots="packed")): K1's int8
+ * slot rows [batch, slots_stride] (-1 / 0 / 1, sharding.py:36-48) packed to
+ * 2 bits per slot, code = status + 1, slot j in bits 2*(j%4) of byte j/4 of
+ * its row; packed rows are packed_stride >= 4*ceil(num_slots/16) bytes and
+ * codes past num_slots are 0.  Cuts the D2H of a full-contract plan 4x. */
+int ap_pack_slots2(const int8_t* slots_dev, int64_t batch, int64_t slots_stride, int64_t num_slots, uint8_t* packed_dev,
+                   int64_t packed_stride, void* stream);
+
 /* PP-infer data plane: num_envs synthetic uniform
  * profiles at once, bit-identical to generate_environment("uniform", n, seed)
  * (dataproc.py:123-145 -> build_environment_arrays :99-120 -> coarsen :79-96).

@@ -143,6 +143,7 @@ SIGNATURES: dict[str, tuple] = {
     "ap_gather_rows_pair": (ctypes.c_int, [_VP, _I64, _VP, _I64, _VP, _I64, _VP, _I64, _VP, _I32, _I32, _VP]),
     "ap_gather_rows": (ctypes.c_int, [_VP, _I64, _VP, _I32, _I32, _VP, _I64, _VP]),
     "ap_vec_apply": (ctypes.c_int, [_VP, _I64, _VP, _VP, _I32, _VP]),
+    "ap_pack_slots2": (ctypes.c_int, [_VP, _I64, _I64, _I64, _VP, _I64, _VP]),
     "ap_vec_post": (ctypes.c_int, [_I32, _I32, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _I64, _VP, _VP, _VP, _VP,
                                    _I32, _VP, _VP, _VP, _VP, _VP]),
     "ap_vec_track_best": (ctypes.c_int, [_I32, _I32, _I64, _VP, _VP, _VP, _VP, _VP, _I64, _VP, _I32, _I32, _VP, _VP,

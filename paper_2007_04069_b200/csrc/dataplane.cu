@@ -103,6 +103,29 @@ __global__ void __launch_bounds__(kGenThreads) uniform_env_kernel(const uint64_t
   }
 }
 
+// Slot statuses for host consumers: K1's int8 slot rows (-1 undecided, 0 R,
+// 1 P; sharding.py:36-48 DimStatus) packed 2 bits per slot, code = status + 1,
+// slot j of a row in bits 2*(j%4) of byte j/4.  One thread packs one 16-byte
+// chunk (16 slots) into one 32-bit word: 16-byte loads and 4-byte stores, both
+// coalesced along the row; codes past n are 0, so padding never leaks.
+__global__ void __launch_bounds__(256) pack_slots2_kernel(const int8_t* __restrict__ slots, int64_t batch,
+                                                          int64_t ld, int64_t n, uint8_t* __restrict__ out,
+                                                          int64_t out_ld) {
+  const int64_t chunks = (n + 15) / 16, total = batch * chunks;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / chunks, c = t - r * chunks, j0 = c * 16;
+    const int4 v = __ldcs(reinterpret_cast<const int4*>(slots + r * ld + j0));
+    const uint32_t w[4] = {(uint32_t)v.x, (uint32_t)v.y, (uint32_t)v.z, (uint32_t)v.w};
+    uint32_t packed = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const uint32_t code = ((w[k >> 2] >> (8 * (k & 3))) + 1u) & 3u;  // -1 -> 0, 0 -> 1, 1 -> 2
+      packed |= (j0 + k < n ? code : 0u) << (2 * k);
+    }
+    *reinterpret_cast<uint32_t*>(out + r * out_ld + c * 4) = packed;
+  }
+}
+
 }  // namespace
 }  // namespace apb
 
@@ -129,6 +152,27 @@ int ap_generate_uniform_envs(const uint64_t* pcg_states, int64_t num_envs, int32
   const int64_t grid = std::min<int64_t>(num_envs, (int64_t)sms * 8);
   uniform_env_kernel<<<(unsigned)grid, kGenThreads, smem, (cudaStream_t)stream>>>(pcg_states, num_envs, n, granularity,
                                                                                   arrays_out);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_pack_slots2(const int8_t* slots_dev, int64_t batch, int64_t slots_stride, int64_t num_slots, uint8_t* packed_dev,
+                   int64_t packed_stride, void* stream) {
+  const int64_t need = ((num_slots + 15) / 16) * 4;
+  if (batch < 0 || num_slots < 0 || slots_stride < ((num_slots + 15) / 16) * 16 || slots_stride % 16 ||
+      packed_stride < need || packed_stride % 4 || (batch > 0 && (!slots_dev || !packed_dev)) ||
+      ((uintptr_t)slots_dev % 16) || ((uintptr_t)packed_dev % 4)) {
+    set_error("ap_pack_slots2: bad arguments (slot rows 16-byte aligned and padded, packed rows >= 4*ceil(n/16) bytes)");
+    return AP_ERR_INVALID;
+  }
+  if (batch == 0 || num_slots == 0) return AP_OK;
+  int dev = 0, sms = 148;
+  AP_CUDA_CHECK(cudaGetDevice(&dev));
+  AP_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t total = batch * ((num_slots + 15) / 16);
+  const int64_t grid = std::min<int64_t>((total + 255) / 256, (int64_t)sms * 8);
+  pack_slots2_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(slots_dev, batch, slots_stride, num_slots,
+                                                                       packed_dev, packed_stride);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }

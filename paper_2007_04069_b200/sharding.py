@@ -65,6 +65,13 @@ SEED_NONE = -1
 SEED_UNDECIDED = 2
 
 
+def unpack_slots2(packed, num_slots: int) -> np.ndarray:
+    """Decode ap_pack_slots2 rows ([B, >= ceil(n/4)] uint8) to int8 statuses [B, n] (-1 / 0 / 1)."""
+    p = np.asarray(packed, dtype=np.uint8)
+    codes = (p[:, :, None] >> np.array([0, 2, 4, 6], dtype=np.uint8)) & 3
+    return codes.reshape(p.shape[0], -1)[:, :num_slots].astype(np.int8) - 1
+
+
 def pad16(n: int) -> int:
     """Row stride (bytes) of seed / status rows: 16-byte multiple for vector loads and stores."""
     return max(16, (n + 15) // 16 * 16)
@@ -337,6 +344,11 @@ class PropagationEngine:
         """Row stride of slot outputs: |S| rounded up to 16 bytes (vectorised stores)."""
         return max(16, (self._eng.num_slots + 15) // 16 * 16)
 
+    @property
+    def packed_slots_stride(self) -> int:
+        """Row stride of 2-bit packed slot outputs: 4 bytes per 16 slots (ap_pack_slots2)."""
+        return max(4, (self._eng.num_slots + 15) // 16 * 4)
+
     def launch(self, seeds, outcome, counts=None, slots=None, statuses=None, stream=None) -> None:
         """Raw stream-ordered launch on preallocated device tensors (no allocation, no sync).
 
@@ -361,20 +373,29 @@ class PropagationEngine:
 
         `seeds_host` is a (preferably pinned) CPU int8 tensor [B, |D|].
         Returns pinned CPU tensors `outcome`, `counts` and optionally
-        `slots` [B, slots_stride] after synchronising.
+        `slots` [B, slots_stride] after synchronising.  want_slots="packed"
+        returns `slots_packed` [B, packed_slots_stride] uint8 instead: the same
+        statuses at 2 bits per slot (ap_pack_slots2 on the device, decoded by
+        `unpack_slots2`), a quarter of the D2H bytes.
         """
         import torch
 
         self.prepare()
+        packed = want_slots == "packed"
+        if not (packed or isinstance(want_slots, bool)):
+            raise ValueError("want_slots must be True, False or 'packed'")
+        want_slots = bool(want_slots)
         b, n = seeds_host.shape
         if out is None:
             out = {
                 "outcome": torch.empty(b, dtype=torch.uint8, pin_memory=True),
                 "counts": torch.empty((b, 4), dtype=torch.int32, pin_memory=True),
             }
-            if want_slots:
+            if packed:
+                out["slots_packed"] = torch.empty((b, self.packed_slots_stride), dtype=torch.uint8, pin_memory=True)
+            elif want_slots:
                 out["slots"] = torch.empty((b, self.slots_stride), dtype=torch.int8, pin_memory=True)
-        key = (chunk, n, want_slots)
+        key = (chunk, n, want_slots, packed)
         bufs = getattr(self, "_host_bufs", None)
         if bufs is None or bufs[0] != key:
             streams = [torch.cuda.Stream(), torch.cuda.Stream()]
@@ -387,6 +408,8 @@ class PropagationEngine:
                 }
                 if want_slots:
                     d["slots"] = torch.empty((chunk, self.slots_stride), dtype=torch.int8, device="cuda")
+                if packed:
+                    d["packed"] = torch.empty((chunk, self.packed_slots_stride), dtype=torch.uint8, device="cuda")
                 dev_bufs.append(d)
             self._host_bufs = bufs = (key, streams, dev_bufs)
         _, streams, dev_bufs = bufs
@@ -402,7 +425,12 @@ class PropagationEngine:
                             stream=s)
                 out["outcome"][lo:hi].copy_(d["outcome"][: hi - lo], non_blocking=True)
                 out["counts"][lo:hi].copy_(d["counts"][: hi - lo], non_blocking=True)
-                if want_slots:
+                if packed:
+                    _native.check(_native.require_device().ap_pack_slots2(
+                        _native.ptr(d["slots"]), hi - lo, d["slots"].stride(0), self._eng.num_slots,
+                        _native.ptr(d["packed"]), d["packed"].stride(0), _native.stream_handle(s)))
+                    out["slots_packed"][lo:hi].copy_(d["packed"][: hi - lo], non_blocking=True)
+                elif want_slots:
                     out["slots"][lo:hi].copy_(d["slots"][: hi - lo], non_blocking=True)
         for s in streams:
             s.synchronize()

@@ -96,3 +96,21 @@ def test_class_counts_bert48():
     dev = _native.DeviceGraph(f.flat)
     assert dev.num_slots == 5633
     assert 0 < dev.num_classes < 1024
+
+
+def test_unpack_slots2_inverts_the_documented_packing():
+    """unpack_slots2 decodes the ap_pack_slots2 layout (code = status + 1, slot j in bits 2*(j%4) of
+    byte j/4), restated here with numpy, for ragged |S| and padded packed rows."""
+    import numpy as np
+
+    from paper_2007_04069_b200.sharding import unpack_slots2
+
+    rng = np.random.default_rng(3)
+    for n in (1, 4, 15, 16, 17, 5633):
+        st = rng.integers(-1, 2, size=(9, n)).astype(np.int8)
+        stride = max(4, (n + 15) // 16 * 4)
+        codes = np.zeros((9, stride * 4), dtype=np.uint8)
+        codes[:, :n] = (st + 1).astype(np.uint8)
+        c = codes.reshape(9, stride, 4)
+        packed = c[..., 0] | (c[..., 1] << 2) | (c[..., 2] << 4) | (c[..., 3] << 6)
+        assert np.array_equal(unpack_slots2(packed, n), st)

@@ -324,3 +324,32 @@ def test_full_size_batch_properties(cuda):
     ok = ocr != 2
     np.testing.assert_array_equal(a["slots"][torch.from_numpy(rows).cuda()].cpu().numpy()[ok][:, : flat.num_slots],
                                   st[ok])
+
+
+@pytest.mark.parametrize("name", ["bert48", "vgg19"])
+def test_run_batch_host_packed_slots_match_int8(cuda, name):
+    """run_batch_host(want_slots="packed") (K1 + ap_pack_slots2, 2 bits per slot) decodes to exactly the
+    int8 slot rows of the unpacked host path, with ragged chunking (batch not a multiple of the chunk)
+    and zero codes past |S|; outcome and counts are unchanged."""
+    from paper_2007_04069_b200.sharding import unpack_slots2
+    from paper_2007_04069_b200.workloads import prefix_seed_batch
+
+    g = graphs.generate(name)
+    dims = decision_dims(g, g.trainable_variables)
+    order = np.asarray([d.flat_index for d in sorted_decision_order(extract_linkage_groups(g, dims))])
+    B = 5000
+    seeds = prefix_seed_batch(order, 7, B).contiguous().pin_memory()
+    eng = PropagationEngine(g, dims)
+    full = eng.run_batch_host(seeds, want_slots=True, chunk=1536)
+    pk = eng.run_batch_host(seeds, want_slots="packed", chunk=1536)
+    n = eng._eng.num_slots
+    assert "slots" not in pk and pk["slots_packed"].shape == (B, eng.packed_slots_stride)
+    assert torch.equal(full["outcome"], pk["outcome"]) and torch.equal(full["counts"], pk["counts"])
+    dec = unpack_slots2(pk["slots_packed"].numpy(), n)
+    assert np.array_equal(dec, full["slots"][:, :n].numpy())
+    tail = pk["slots_packed"].numpy()
+    if n % 4:
+        assert not (tail[:, n // 4] >> (2 * (n % 4))).any()
+    assert not tail[:, (n + 3) // 4:].any()
+    with pytest.raises(ValueError):
+        eng.run_batch_host(seeds[:4], want_slots="bits")
