@@ -117,6 +117,20 @@ int ap_propagate_batch(ap_graph_t g, ap_decision_t d, const int8_t* seeds_dev, i
                        int8_t* cand_dev, int64_t cand_stride, uint8_t* outcome_dev,
                        int32_t* counts_dev, void* stream);
 
+/* ap_propagate_batch with the slot statuses emitted as 2-bit codes by K1
+ * itself (code = status + 1; slot j in bits 2*(j%16) of little-endian 32-bit
+ * word j/16 of its row, i.e. bits 2*(j%4) of byte j/4, codes past num_slots
+ * 0) — the ap_pack_slots2 layout without the int8 round trip through HBM.
+ *   packed_dev   [batch, packed_stride] uint8, packed_stride a multiple of 4
+ *                and >= 4*ceil(num_slots/16)
+ * Other arguments as ap_propagate_batch (same reference interface,
+ * sharding.py:210-248).  Graphs outside the fast kernel's limits run the
+ * generic kernel into a stream-ordered scratch and pack it. */
+int ap_propagate_batch_packed(ap_graph_t g, ap_decision_t d, const int8_t* seeds_dev, int64_t batch,
+                              int64_t seed_stride, uint8_t* packed_dev, int64_t packed_stride,
+                              int8_t* cand_dev, int64_t cand_stride, uint8_t* outcome_dev,
+                              int32_t* counts_dev, void* stream);
+
 /* Exact replay of the reference sweep order for one seed row (one device
  * thread): the CONFLICT snapshot of `assignments` and `conflict_site`
  * (sharding.py:219-239, 250-265).  conflict_site_out gets the *position*

@@ -103,6 +103,7 @@ SIGNATURES: dict[str, tuple] = {
     "ap_decision_create": (ctypes.c_int, [_VP, _VP, _VP, _I32, ctypes.POINTER(_VP)]),
     "ap_decision_destroy": (ctypes.c_int, [_VP]),
     "ap_propagate_batch": (ctypes.c_int, [_VP, _VP, _VP, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _VP, _VP]),
+    "ap_propagate_batch_packed": (ctypes.c_int, [_VP, _VP, _VP, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _VP, _VP]),
     "ap_propagate_trace": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "ap_pipe_create": (ctypes.c_int, [ctypes.POINTER(PipeDesc), ctypes.POINTER(_VP)]),
     "ap_pipe_destroy": (ctypes.c_int, [_VP]),

@@ -1,5 +1,7 @@
 // C-ABI entry points (include/autoplan_b200.h): argument checks, handle
 // lifetime and the thread-local error string.
+#include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <new>
@@ -12,6 +14,20 @@ namespace apb {
 static thread_local std::string g_last_error;
 
 void set_error(const std::string& msg) { g_last_error = msg; }
+
+int current_sm_count(int* sms) {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  AP_CUDA_CHECK(cudaGetDevice(&dev));
+  const bool cached = dev >= 0 && dev < 64;
+  int v = cached ? cache[dev].load(std::memory_order_relaxed) : 0;
+  if (v <= 0) {
+    AP_CUDA_CHECK(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+    if (cached) cache[dev].store(v, std::memory_order_relaxed);
+  }
+  *sms = v;
+  return AP_OK;
+}
 
 int cuda_fail(cudaError_t err, const char* what) {
   char buf[512];
@@ -33,6 +49,7 @@ static void release_graph(GraphTables* t) {
   t->d_slot_base.release();
   t->d_slot_owner.release();
   t->d_slot_desc.release();
+  t->d_slot_desc_t.release();
   t->d_slot_cls8.release();
   t->d_imp_bits.release();
   t->d_forced_bits.release();
@@ -167,6 +184,45 @@ int ap_propagate_batch(ap_graph_t g, ap_decision_t d, const int8_t* seeds_dev, i
   }
   return apb::launch_propagate(&g->t, &d->t, seeds_dev, batch, seed_stride, slots_dev, slots_stride, cand_dev,
                                cand_stride, outcome_dev, counts_dev, static_cast<cudaStream_t>(stream));
+}
+
+int ap_propagate_batch_packed(ap_graph_t g, ap_decision_t d, const int8_t* seeds_dev, int64_t batch,
+                              int64_t seed_stride, uint8_t* packed_dev, int64_t packed_stride, int8_t* cand_dev,
+                              int64_t cand_stride, uint8_t* outcome_dev, int32_t* counts_dev, void* stream) {
+  if (!g || !d) {
+    apb::set_error("ap_propagate_batch_packed: null handle");
+    return AP_ERR_INVALID;
+  }
+  const int64_t S = g->t.num_slots, need = 4 * ((S + 15) / 16);
+  if (batch < 0 || packed_stride < need || packed_stride % 4 || (batch > 0 && (!packed_dev || !seeds_dev)) ||
+      (reinterpret_cast<uintptr_t>(packed_dev) & 3)) {
+    apb::set_error("ap_propagate_batch_packed: bad arguments (packed rows 4-byte aligned, stride >= 4*ceil(S/16))");
+    return AP_ERR_INVALID;
+  }
+  int rc = apb::ensure_graph_on_device(&g->t);
+  if (rc == AP_OK) rc = apb::ensure_decision_on_device(&d->t);
+  if (rc != AP_OK || batch == 0) return rc;
+  auto st = static_cast<cudaStream_t>(stream);
+  const char* force = std::getenv("AP_PROPAGATE_GENERIC");
+  if (!(force && force[0] == '1')) {
+    rc = apb::launch_propagate_fast(&g->t, &d->t, seeds_dev, batch, seed_stride, nullptr, 0, cand_dev, cand_stride,
+                                    outcome_dev, counts_dev, st, packed_dev, packed_stride);
+    if (rc != AP_ERR_UNSUPPORTED) return rc;
+  }
+  // generic kernel into int8 rows (stream-ordered scratch, chunks of <= 64 Mi bytes), then pack
+  const int64_t stride = std::max<int64_t>(16, (S + 15) / 16 * 16);
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(batch, (64ll << 20) / stride));
+  int8_t* scratch = nullptr;
+  AP_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&scratch), chunk * stride, st));
+  for (int64_t lo = 0; lo < batch && rc == AP_OK; lo += chunk) {
+    const int64_t n = std::min(chunk, batch - lo);
+    rc = apb::launch_propagate(&g->t, &d->t, seeds_dev + lo * seed_stride, n, seed_stride, scratch, stride,
+                               cand_dev ? cand_dev + lo * cand_stride : nullptr, cand_stride, outcome_dev + lo,
+                               counts_dev ? counts_dev + 4 * lo : nullptr, st);
+    if (rc == AP_OK) rc = ap_pack_slots2(scratch, n, stride, S, packed_dev + lo * packed_stride, packed_stride, stream);
+  }
+  cudaFreeAsync(scratch, st);
+  return rc;
 }
 
 int ap_propagate_trace(ap_graph_t g, ap_decision_t d, const int8_t* seeds_host, const int8_t* init_state_host,

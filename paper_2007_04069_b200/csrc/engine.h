@@ -41,6 +41,13 @@ __device__ __forceinline__ void pdl_entry() {
 }
 
 bool pdl_enabled();
+#endif
+
+// SM count of the current device, cached per device ordinal (thread-safe: a
+// racing first call stores the same value).
+int current_sm_count(int* sms);
+
+#ifdef __CUDACC__
 
 // Throughput-mode Adam element (the graph-captured learner; the parity agent's
 // ap_dqn_adam keeps the reference expression), shared by the Adam kernels and
@@ -115,6 +122,7 @@ struct GraphTables {
   // fast-kernel tables (only when num_classes <= kMaxFastClasses)
   bool fast = false;
   std::vector<uint32_t> slot_desc;    // [nq_s * 4] chunk descriptors (see propagate_fast.cu)
+  std::vector<uint32_t> slot_desc_t;  // [nq_s * 4] same classes, transposed selectors (packed 2-bit output)
   std::vector<uint8_t> slot_cls8;     // [nq_s * 16] class id per slot, 0xFF padding
   std::vector<uint32_t> imp_bits;     // [C * 8] 256-bit implication row per class
   std::vector<uint32_t> forced_bits;  // [8] forced-replicated classes
@@ -123,6 +131,7 @@ struct GraphTables {
 
   // device copies
   DevBuf<uint32_t> d_slot_desc;
+  DevBuf<uint32_t> d_slot_desc_t;
   DevBuf<uint8_t> d_slot_cls8;
   DevBuf<uint32_t> d_imp_bits;
   DevBuf<uint32_t> d_forced_bits;
@@ -178,9 +187,12 @@ constexpr int kFastMaxChunks = 8;     // decision positions <= 32 lanes * 8 chun
 void build_fast_graph(GraphTables* g);
 void build_fast_decision(const GraphTables* g, DecisionTables* d);
 // Returns AP_ERR_UNSUPPORTED (without setting an error) when the fast path does not apply.
+// `packed_out` (nullable, [batch, packed_stride] bytes): slot statuses at 2 bits per slot
+// (code = status + 1, slot j in bits 2*(j%16) of 32-bit word j/16), exclusive with slots_out.
 int launch_propagate_fast(const GraphTables* g, const DecisionTables* d, const int8_t* seeds, int64_t batch,
                           int64_t seed_stride, int8_t* slots_out, int64_t slots_stride, int8_t* cand_out,
-                          int64_t cand_stride, uint8_t* outcome, int32_t* counts, cudaStream_t stream);
+                          int64_t cand_stride, uint8_t* outcome, int32_t* counts, cudaStream_t stream,
+                          uint8_t* packed_out = nullptr, int64_t packed_stride = 0);
 
 int launch_gemm_v2(const float* A, int64_t lda, int transA, const float* B, int64_t ldb, int transB, float* C,
                    int64_t ldc, int M, int N, int K, const float* bias, int relu, int precision, cudaStream_t stream);

@@ -320,6 +320,7 @@ int ensure_graph_on_device(GraphTables* g) {
   if ((rc = g->d_slot_owner.upload(g->slot_owner)) != AP_OK) return rc;
   if (g->fast) {
     if ((rc = g->d_slot_desc.upload(g->slot_desc)) != AP_OK) return rc;
+    if ((rc = g->d_slot_desc_t.upload(g->slot_desc_t)) != AP_OK) return rc;
     if ((rc = g->d_slot_cls8.upload(g->slot_cls8)) != AP_OK) return rc;
     if ((rc = g->d_imp_bits.upload(g->imp_bits)) != AP_OK) return rc;
     if ((rc = g->d_forced_bits.upload(g->forced_bits)) != AP_OK) return rc;

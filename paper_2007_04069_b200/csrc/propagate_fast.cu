@@ -24,6 +24,7 @@
 // is bit 4*b + i: OR-ing (word_i & 0x01010101) << i puts it at 8*b + i, and
 // `squeeze` packs those nibbles into 16 bits.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <set>
 
@@ -45,7 +46,7 @@ constexpr int kWarpsF = AP_K1_WARPS;
 constexpr int kThreadsF = kWarpsF * 32;
 constexpr unsigned kFullMask = 0xffffffffu;
 constexpr uint32_t kOnes = 0x01010101u;
-constexpr int kScratchPerWarp = 768;  // flagP[256] flagR[256] table[256]
+constexpr int kScratchPerWarp = 1024;  // flagP[256] flagR[256] table[256] codes[256]
 
 // 16-bit position mask bit of chunk position t = 4*i + b (word i, byte b)
 inline int perm_bit(int t) { return 4 * (t & 3) + (t >> 2); }
@@ -86,6 +87,19 @@ void pack_selectors(const int local[16], uint32_t* z, uint32_t* w) {
   *w = sel[2] | (sel[3] << 16);
 }
 
+// Transposed selectors for the packed 2-bit output: word j, byte b selects slot
+// 4*b + j, so OR-ing word j shifted left by 2*j puts slot t's code at bits 2*t.
+// Slots past the row end select byte 4 (a zero operand): codes 0 in the padding.
+void pack_selectors_t(const int local[16], int count, uint32_t* z, uint32_t* w) {
+  uint32_t sel[4];
+  for (int j = 0; j < 4; ++j) {
+    sel[j] = 0;
+    for (int b = 0; b < 4; ++b) sel[j] |= (uint32_t)(4 * b + j < count ? local[4 * b + j] : 4) << (4 * b);
+  }
+  *z = sel[0] | (sel[1] << 16);
+  *w = sel[2] | (sel[3] << 16);
+}
+
 }  // namespace
 
 void build_fast_graph(GraphTables* g) {
@@ -94,6 +108,7 @@ void build_fast_graph(GraphTables* g) {
   const int64_t S = g->num_slots;
   const int64_t nq = (S + 15) / 16;
   g->slot_desc.assign(nq * 4, 0);
+  g->slot_desc_t.assign(nq * 4, 0);
   g->slot_cls8.assign(nq * 16, 0xFF);
   std::vector<int> uniq;
   int local[16];
@@ -101,12 +116,17 @@ void build_fast_graph(GraphTables* g) {
     const int count = (int)std::min<int64_t>(16, S - 16 * q);
     for (int t = 0; t < count; ++t) g->slot_cls8[16 * q + t] = (uint8_t)g->class_of_slot[16 * q + t];
     uint32_t* d = &g->slot_desc[4 * q];
+    uint32_t* dt = &g->slot_desc_t[4 * q];
     if (!local_classes(&g->class_of_slot[16 * q], count, &uniq, local)) {
       d[0] = 0xFFFFFFFFu;  // fallback: per-slot lookups through slot_cls8
+      dt[0] = 0xFFFFFFFFu;
       continue;
     }
     pack_classes(uniq, &d[0], &d[1]);
     pack_selectors(local, &d[2], &d[3]);
+    dt[0] = d[0];
+    dt[1] = d[1];
+    pack_selectors_t(local, count, &dt[2], &dt[3]);
   }
   g->slot_fallback_chunks = 0;
   g->slot_all_k4 = true;
@@ -199,7 +219,13 @@ struct FastParams {
   int cand_vec;
   uint8_t* outcome;
   int32_t* counts;
+  uint32_t* packed_out;     // 2-bit slot codes, [batch, packed_stride] 32-bit words, or null
+  int64_t packed_stride;    // in 32-bit words
+  const uint4* slot_desc_t; // transposed-selector descriptors (packed output)
+  int bulk;                 // int8 slot rows staged in shared memory, stored by TMA bulk copies
+  int64_t stage_bytes;      // per-warp staging row (16 * nq_s)
   int off_slot_desc, off_slot_cls8, off_dec_desc, off_dec_masks, off_dec_cls8, off_ncand, off_imp_bits, off_scratch;
+  int off_stage;
 };
 
 __device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
@@ -313,7 +339,11 @@ __global__ void __launch_bounds__(kThreadsF, AP_K1_MIN_BLOCKS) propagate_fast_ke
     const uint8_t* sb = reinterpret_cast<const uint8_t*>(src);
     for (int64_t i = n16 * 16 + threadIdx.x; i < bytes; i += blockDim.x) smem[off + i] = sb[i];
   };
-  stage(p.off_slot_desc, p.slot_desc, (int64_t)p.nq_s * 16);
+  if (p.packed_out) {
+    stage(p.off_slot_desc, p.slot_desc_t, (int64_t)p.nq_s * 16);  // packed rows only use the transposed set
+  } else {
+    stage(p.off_slot_desc, p.slot_desc, (int64_t)p.nq_s * 16);
+  }
   if (p.any_slot_fallback) stage(p.off_slot_cls8, p.slot_cls8, (int64_t)p.nq_s * 16);
   stage(p.off_dec_desc, p.dec_desc, (int64_t)p.nq_d * 32);
   stage(p.off_dec_masks, p.dec_masks, (int64_t)p.nq_d * 4);
@@ -343,8 +373,13 @@ __global__ void __launch_bounds__(kThreadsF, AP_K1_MIN_BLOCKS) propagate_fast_ke
   uint8_t* flagP = scratch;
   uint8_t* flagR = scratch + 256;
   int8_t* table = reinterpret_cast<int8_t*>(scratch + 512);
+  uint8_t* codes = scratch + 768;  // status + 1 per class (packed output)
   const uint32_t fb = (uint32_t)__cvta_generic_to_shared(flagP);  // flagR = fb + 256
   const uint32_t tb = fb + 512;
+  const uint32_t cb = fb + 768;
+  const uint32_t stage_sa = smem_sa + (uint32_t)p.off_stage + (uint32_t)(warp * p.stage_bytes);
+  uint64_t evict_first = 0;
+  if (p.bulk) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(evict_first));
 
   const int64_t nwarps = (int64_t)gridDim.x * kWarpsF;
   int64_t b = (int64_t)blockIdx.x * kWarpsF + warp;
@@ -467,6 +502,7 @@ __global__ void __launch_bounds__(kThreadsF, AP_K1_MIN_BLOCKS) propagate_fast_ke
       const bool isP = (Pw[k] >> lane) & 1u;
       const bool isR = (Rw[k] >> lane) & 1u;
       table[c] = isP ? 1 : (isR ? 0 : -1);
+      if (p.packed_out) codes[c] = isP ? 2 : (isR ? 1 : 0);
       const uint32_t nc = ncand[c];
       dPR += isP ? nc : (isR ? (nc << 16) : 0u);
     }
@@ -512,8 +548,10 @@ __global__ void __launch_bounds__(kThreadsF, AP_K1_MIN_BLOCKS) propagate_fast_ke
           if (16 * q + 16 <= p.D) {
             reinterpret_cast<uint4*>(crow)[q] = o;
           } else {
-            const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
-            for (int t = 0; 16 * q + t < p.D; ++t) crow[16 * q + t] = (int8_t)(ow[t >> 2] >> (8 * (t & 3)));
+            for (int t = 0; 16 * q + t < p.D; ++t) {
+              const uint32_t wv = (t >> 2) == 0 ? o.x : ((t >> 2) == 1 ? o.y : ((t >> 2) == 2 ? o.z : o.w));
+              crow[16 * q + t] = (int8_t)(wv >> (8 * (t & 3)));
+            }
           }
         } else {
           for (int t = 0; t < 16 && 16 * q + t < p.D; ++t) crow[16 * q + t] = table[dec_cls8[16 * q + t]];
@@ -522,7 +560,67 @@ __global__ void __launch_bounds__(kThreadsF, AP_K1_MIN_BLOCKS) propagate_fast_ke
     }
 
     // 5. all slot statuses
-    if (p.slots_out && p.slot_all_k4) {
+    if (p.packed_out) {
+      // 2-bit codes, 16 slots per 32-bit word, one coalesced 4-byte store per lane
+      uint32_t* prow = p.packed_out + b * p.packed_stride;
+      if (p.slot_all_k4) {
+        const int rounds = (p.nq_s + 31) >> 5;
+        const int last = p.nq_s - 1;
+#pragma unroll 4
+        for (int it = 0; it < rounds; ++it) {
+          const int q = lane + 32 * it;
+          const uint4 d = slot_desc[min(q, last)];
+          const uint32_t lo = local_table4(d.x, cb);
+          const uint32_t w0 = prmt(lo, 0u, d.z), w1 = prmt(lo, 0u, d.z >> 16);
+          const uint32_t w2 = prmt(lo, 0u, d.w), w3 = prmt(lo, 0u, d.w >> 16);
+          const uint32_t word = w0 | (w1 << 2) | (w2 << 4) | (w3 << 6);
+          if (q <= last) __stcs(prow + q, word);
+        }
+      } else {
+        for (int q = lane; q < p.nq_s; q += 32) {
+          const uint4 d = slot_desc[q];
+          uint32_t word = 0;
+          if ((d.x & 0xFF) != 0xFF) {  // <= 8 local classes: the same selection on code bytes
+            uint32_t lo, hi;
+            local_table(d.x, d.y, cb, &lo, &hi);
+            word = prmt(lo, hi, d.z) | (prmt(lo, hi, d.z >> 16) << 2) | (prmt(lo, hi, d.w) << 4) |
+                   (prmt(lo, hi, d.w >> 16) << 6);
+            const int64_t rem = p.S - 16 * (int64_t)q;  // padding codes are 0
+            if (rem < 16) word &= (1u << (2 * rem)) - 1u;
+          } else {
+            for (int t = 0; t < 16 && 16 * q + t < p.S; ++t) word |= (uint32_t)codes[slot_cls8[16 * q + t]] << (2 * t);
+          }
+          __stcs(prow + q, word);
+        }
+      }
+    } else if (p.slots_out && p.slot_all_k4 && p.bulk) {
+      // stage the row in shared memory, one TMA bulk store per plan (issued by lane 0)
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      __syncwarp();
+      const int rounds = (p.nq_s + 31) >> 5;
+      const int last = p.nq_s - 1;
+#pragma unroll 4
+      for (int it = 0; it < rounds; ++it) {
+        const int q = lane + 32 * it;
+        const uint4 d = slot_desc[min(q, last)];
+        const uint32_t lo = local_table4(d.x, tb);
+        const uint4 o = select16(lo, lo, d.z, d.w);
+        if (q <= last)
+          asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(stage_sa + 16 * q), "r"(o.x), "r"(o.y),
+                       "r"(o.z), "r"(o.w)
+                       : "memory");
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile(
+            "cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
+                p.slots_out + b * p.slots_stride),
+            "r"(stage_sa), "r"((uint32_t)p.stage_bytes), "l"(evict_first)
+            : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    } else if (p.slots_out && p.slot_all_k4) {
       // common case (BERT-48): branch-free, four lookups per 16 slots
       // warp-uniform trip count: a per-lane `q < nq_s` bound diverges in the
       // last round and runs the unrolled body's remainder paths back to back
@@ -562,18 +660,15 @@ __global__ void __launch_bounds__(kThreadsF, AP_K1_MIN_BLOCKS) propagate_fast_ke
     }
     __syncwarp();
   }
+  if (p.bulk && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 template <int MAXCH, int NW>
 int launch_fast_t(const FastParams& p, int64_t smem, cudaStream_t stream) {
-  static int num_sms = -1;
+  int num_sms = 0;
+  if (int rc = current_sm_count(&num_sms)) return rc;
   auto kern = propagate_fast_kernel<MAXCH, NW>;
   AP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  if (num_sms < 0) {
-    int dev = 0;
-    AP_CUDA_CHECK(cudaGetDevice(&dev));
-    AP_CUDA_CHECK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
-  }
   int per_sm = 0;
   AP_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreadsF, (size_t)smem));
   if (AP_K1_MAX_CTAS_PER_SM > 0) per_sm = std::min(per_sm, AP_K1_MAX_CTAS_PER_SM);
@@ -605,8 +700,12 @@ int dispatch_nw(int nw, const FastParams& p, int64_t smem, cudaStream_t stream) 
 
 int launch_propagate_fast(const GraphTables* g, const DecisionTables* d, const int8_t* seeds, int64_t batch,
                           int64_t seed_stride, int8_t* slots_out, int64_t slots_stride, int8_t* cand_out,
-                          int64_t cand_stride, uint8_t* outcome, int32_t* counts, cudaStream_t stream) {
+                          int64_t cand_stride, uint8_t* outcome, int32_t* counts, cudaStream_t stream,
+                          uint8_t* packed_out, int64_t packed_stride) {
   if (!g->fast || !d->fast || d->n == 0) return AP_ERR_UNSUPPORTED;
+  if (packed_out && (slots_out || packed_stride % 4 || (reinterpret_cast<uintptr_t>(packed_out) & 3) ||
+                     packed_stride < 4 * ((g->num_slots + 15) / 16)))
+    return AP_ERR_UNSUPPORTED;
   const int nq_d = (d->n + 15) / 16;
   const int64_t nq_s = (g->num_slots + 15) / 16;
   auto aligned = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
@@ -641,6 +740,13 @@ int launch_propagate_fast(const GraphTables* g, const DecisionTables* d, const i
   p.cand_vec = cand_out && cand_stride % 16 == 0 && aligned(cand_out);
   p.outcome = outcome;
   p.counts = counts;
+  p.packed_out = reinterpret_cast<uint32_t*>(packed_out);
+  p.packed_stride = packed_stride / 4;
+  p.slot_desc_t = reinterpret_cast<const uint4*>(g->d_slot_desc_t.ptr);
+  // TMA bulk row stores (AP_K1_BULK=1): int8 rows of k<=4 graphs, staged per warp in shared memory
+  const char* bulk_env = std::getenv("AP_K1_BULK");
+  p.bulk = slots_out && g->slot_all_k4 && bulk_env && bulk_env[0] == '1';
+  p.stage_bytes = 16 * nq_s;
   int64_t off = 0;
   auto place = [&](int64_t bytes) {
     const int64_t o = off;
@@ -655,7 +761,13 @@ int launch_propagate_fast(const GraphTables* g, const DecisionTables* d, const i
   p.off_ncand = place(512);
   p.off_imp_bits = place((int64_t)std::max(p.C, 1) * 32);
   p.off_scratch = (int)off;
-  const int64_t smem = off + 256 + (int64_t)kWarpsF * kScratchPerWarp;
+  off += 256 + (int64_t)kWarpsF * kScratchPerWarp;
+  p.off_stage = (int)a16(off);
+  if (p.bulk) {
+    off = p.off_stage + (int64_t)kWarpsF * p.stage_bytes;
+    if (off > 110 * 1024) p.bulk = 0, off = p.off_stage;  // keep 2 CTAs per SM
+  }
+  const int64_t smem = off;
   if (smem > 200 * 1024) return AP_ERR_UNSUPPORTED;
   const int chunks = (nq_d + 31) / 32;
   const int nw = (p.C + 31) / 32;

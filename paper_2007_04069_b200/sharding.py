@@ -349,16 +349,32 @@ class PropagationEngine:
         """Row stride of 2-bit packed slot outputs: 4 bytes per 16 slots (ap_pack_slots2)."""
         return max(4, (self._eng.num_slots + 15) // 16 * 4)
 
-    def launch(self, seeds, outcome, counts=None, slots=None, statuses=None, stream=None) -> None:
+    def launch(self, seeds, outcome, counts=None, slots=None, statuses=None, stream=None, packed=None) -> None:
         """Raw stream-ordered launch on preallocated device tensors (no allocation, no sync).
 
         seeds int8 [B, |D|] (candidate order, which must be ascending), outcome
         uint8 [B], counts int32 [B, 4] | None, slots int8 [B, >=|S|] | None,
-        statuses int8 [B, >=|D|] | None.
+        statuses int8 [B, >=|D|] | None, packed uint8 [B, >=packed_slots_stride]
+        | None: the slot statuses as 2-bit codes written by K1 itself
+        (exclusive with `slots`; decode with `unpack_slots2`).
         """
         dev, dec = self.prepare()
         lib = _native.require_device()
         b = seeds.shape[0]
+        if seeds.dim() != 2 or seeds.shape[1] != dec.n:
+            raise ValueError(f"seeds must be [B, {dec.n}] over the candidate list, got {tuple(seeds.shape)}")
+        if packed is not None:
+            if slots is not None:
+                raise ValueError("launch: `slots` and `packed` are exclusive")
+            _native.check(
+                lib.ap_propagate_batch_packed(
+                    dev.handle, dec.handle, _native.ptr(seeds), b, seeds.stride(0) if b else pad16(dec.n),
+                    _native.ptr(packed), packed.stride(0),
+                    _native.ptr(statuses), 0 if statuses is None else statuses.stride(0),
+                    _native.ptr(outcome), _native.ptr(counts), _native.stream_handle(stream),
+                )
+            )
+            return
         _native.check(
             lib.ap_propagate_batch(
                 dev.handle, dec.handle, _native.ptr(seeds), b, seeds.stride(0) if b else pad16(dec.n),
@@ -375,8 +391,9 @@ class PropagationEngine:
         Returns pinned CPU tensors `outcome`, `counts` and optionally
         `slots` [B, slots_stride] after synchronising.  want_slots="packed"
         returns `slots_packed` [B, packed_slots_stride] uint8 instead: the same
-        statuses at 2 bits per slot (ap_pack_slots2 on the device, decoded by
-        `unpack_slots2`), a quarter of the D2H bytes.
+        statuses at 2 bits per slot, emitted by K1 itself
+        (ap_propagate_batch_packed, decoded by `unpack_slots2`), a quarter of
+        the D2H bytes.
         """
         import torch
 
@@ -386,6 +403,8 @@ class PropagationEngine:
             raise ValueError("want_slots must be True, False or 'packed'")
         want_slots = bool(want_slots)
         b, n = seeds_host.shape
+        if n != len(self.candidates):
+            raise ValueError(f"seeds must be [B, {len(self.candidates)}] over the candidate list, got {tuple(seeds_host.shape)}")
         if out is None:
             out = {
                 "outcome": torch.empty(b, dtype=torch.uint8, pin_memory=True),
@@ -406,7 +425,7 @@ class PropagationEngine:
                     "outcome": torch.empty(chunk, dtype=torch.uint8, device="cuda"),
                     "counts": torch.empty((chunk, 4), dtype=torch.int32, device="cuda"),
                 }
-                if want_slots:
+                if want_slots and not packed:
                     d["slots"] = torch.empty((chunk, self.slots_stride), dtype=torch.int8, device="cuda")
                 if packed:
                     d["packed"] = torch.empty((chunk, self.packed_slots_stride), dtype=torch.uint8, device="cuda")
@@ -421,14 +440,11 @@ class PropagationEngine:
             s, d = streams[i % 2], dev_bufs[i % 2]
             with torch.cuda.stream(s):
                 d["seeds"][: hi - lo].copy_(seeds_host[lo:hi], non_blocking=True)
-                self.launch(d["seeds"][: hi - lo], d["outcome"], d["counts"], d.get("slots") if want_slots else None,
-                            stream=s)
+                self.launch(d["seeds"][: hi - lo], d["outcome"], d["counts"], d.get("slots"), stream=s,
+                            packed=d["packed"][: hi - lo] if packed else None)
                 out["outcome"][lo:hi].copy_(d["outcome"][: hi - lo], non_blocking=True)
                 out["counts"][lo:hi].copy_(d["counts"][: hi - lo], non_blocking=True)
                 if packed:
-                    _native.check(_native.require_device().ap_pack_slots2(
-                        _native.ptr(d["slots"]), hi - lo, d["slots"].stride(0), self._eng.num_slots,
-                        _native.ptr(d["packed"]), d["packed"].stride(0), _native.stream_handle(s)))
                     out["slots_packed"][lo:hi].copy_(d["packed"][: hi - lo], non_blocking=True)
                 elif want_slots:
                     out["slots"][lo:hi].copy_(d["slots"][: hi - lo], non_blocking=True)

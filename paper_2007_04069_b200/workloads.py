@@ -33,11 +33,13 @@ def mix32(x):
     return x ^ (x >> 16)
 
 
-def prefix_seed_batch(order, start: int, count: int, seed: int = BATCH_SEED, device="cpu", chunk: int = 1 << 16):
+def prefix_seed_batch(order, start: int, count: int, seed: int = BATCH_SEED, device="cpu", chunk: int = 1 << 16,
+                      kmax: int | None = None):
     """Rows [start, start+count) of the synthetic prefix batch as int8 [count, |D|].
 
     `order` is the decision order as flat candidate indices (e.g.
     `sorted_decision_order`); column `order[j]` belongs to prefix position j.
+    Prefix lengths are k ~ U[1, min(|D|, kmax)] (kmax=None: the whole order).
     """
     import torch
 
@@ -51,11 +53,24 @@ def prefix_seed_batch(order, start: int, count: int, seed: int = BATCH_SEED, dev
     for lo in range(0, count, chunk):
         hi = min(count, lo + chunk)
         rows = torch.arange(start + lo, start + hi, dtype=torch.int64, device=device)
-        k = 1 + mix32(mix32((rows & _M32) ^ s0.to(device)) ^ (rows >> 32)) % n
+        k = 1 + mix32(mix32((rows & _M32) ^ s0.to(device)) ^ (rows >> 32)) % min(n, kmax or n)
         e = rows[:, None] * n + pos[None, :]
         bits = mix32(mix32((e & _M32) ^ s1.to(device)) ^ (e >> 32)) & 1
         ordered = torch.where(pos[None, :] < k[:, None], bits, torch.full_like(bits, -1)).to(torch.int8)
         out[lo:hi, order_t] = ordered
+    return out
+
+
+def trigger_seed_batch(num_dims: int, start: int, count: int, device="cpu"):
+    """Rows [start, start+count) of the 2*|D| linkage triggers tiled over the batch (row r is
+    trigger r mod 2|D|: dim (r mod 2|D|) // 2 seeded P for even, R for odd), int8 [count, |D|]."""
+    import torch
+
+    n = num_dims
+    out = torch.full((count, max(16, (n + 15) // 16 * 16)), -1, dtype=torch.int8, device=device)[:, :n]
+    t = torch.arange(start, start + count, dtype=torch.int64, device=device) % (2 * n)
+    rows = torch.arange(count, dtype=torch.int64, device=device)
+    out[rows, t // 2] = (1 - (t % 2)).to(torch.int8)
     return out
 
 
