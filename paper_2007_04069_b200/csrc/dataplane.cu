@@ -170,7 +170,8 @@ int ap_pack_slots2(const int8_t* slots_dev, int64_t batch, int64_t slots_stride,
   AP_CUDA_CHECK(cudaGetDevice(&dev));
   AP_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int64_t total = batch * ((num_slots + 15) / 16);
-  const int64_t grid = std::min<int64_t>((total + 255) / 256, (int64_t)sms * 64);  // many 16-B loads in flight
+  // oversubscribed grid (8 resident 256-thread CTAs per SM, 64 waves' worth): fewer grid-stride trips
+  const int64_t grid = std::min<int64_t>((total + 255) / 256, (int64_t)sms * 64);
   pack_slots2_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(slots_dev, batch, slots_stride, num_slots,
                                                                        packed_dev, packed_stride);
   AP_CUDA_CHECK(cudaGetLastError());

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 #include <utility>
 #include <vector>
@@ -46,6 +47,25 @@ bool pdl_enabled();
 // SM count of the current device, cached per device ordinal (thread-safe: a
 // racing first call stores the same value).
 int current_sm_count(int* sms);
+
+// Per-device grow-only configuration value (kernel attributes such as the
+// dynamic shared-memory limit are per device context): `need(dev, v)` is true
+// when v exceeds what was configured on `dev`, and records v.
+struct PerDeviceMax {
+  std::atomic<int64_t> v[64];
+  bool need(int dev, int64_t want) {
+    std::atomic<int64_t>& slot = v[dev & 63];
+    int64_t cur = slot.load(std::memory_order_relaxed);
+    while (want > cur)
+      if (slot.compare_exchange_weak(cur, want)) return true;
+    return false;
+  }
+};
+inline int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
 
 #ifdef __CUDACC__
 

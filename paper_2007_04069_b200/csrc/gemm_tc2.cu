@@ -20,6 +20,7 @@
 //   MN-major: (r/4)*512  + (k/8)*128 + (k%8)*16 + (r%4)*4   LBO 128, SBO 512
 #include <algorithm>
 #include <cstdlib>
+#include <map>
 #include <mutex>
 #include <unordered_map>
 #include <utility>
@@ -319,20 +320,23 @@ int launch_gemm_v2(const float* A, int64_t lda, int transA, const float* B, int6
 
 namespace apb {
 int splitk_workspace(cudaStream_t stream, size_t bytes, float** out) {
+  // one grow-only buffer per (device, stream): GEMMs on one stream are ordered, so they can share it
   static std::mutex mu;
-  static std::unordered_map<cudaStream_t, std::pair<float*, size_t>> ws;
+  static std::map<std::pair<int, cudaStream_t>, std::pair<float*, size_t>> ws;
+  int dev = 0;
+  AP_CUDA_CHECK(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(mu);
-  auto& w = ws[stream];
+  auto& w = ws[{dev, stream}];
   if (bytes > w.second) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    AP_CUDA_CHECK(cudaStreamIsCapturing(stream, &cs));
-    if (cs != cudaStreamCaptureStatusNone) {
-      set_error("gemm: split-K workspace must grow during graph capture; run the shapes once before capturing");
-      return AP_ERR_INVALID;
-    }
+    // a capture in global mode forbids cudaMalloc on this thread; the buffer is an ordinary
+    // persistent allocation (not a graph node), so allocate it in relaxed mode
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    AP_CUDA_CHECK(cudaThreadExchangeStreamCaptureMode(&mode));
     float* fresh = nullptr;
-    AP_CUDA_CHECK(cudaMalloc(&fresh, bytes));
-    w = {fresh, bytes};  // the previous buffer is intentionally kept alive
+    const cudaError_t e = cudaMalloc(&fresh, bytes);
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    AP_CUDA_CHECK(e);
+    w = {fresh, bytes};  // the previous buffer is intentionally kept alive (captured graphs may use it)
   }
   *out = w.first;
   return AP_OK;

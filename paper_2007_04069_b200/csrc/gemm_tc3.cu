@@ -489,16 +489,15 @@ using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, 
                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 EncodeTiled encode_fn() {
-  static EncodeTiled fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  // driver entry points are process-wide; a function-local static initialises once, thread-safely
+  static const EncodeTiled fn = []() -> EncodeTiled {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiled>(p);
-  }
+      return reinterpret_cast<EncodeTiled>(p);
+    return nullptr;
+  }();
   return fn;
 }
 
@@ -519,12 +518,11 @@ template <int BN, int STAGES>
 int run3(const CUtensorMap& ma, const CUtensorMap& mb, const G3& g, dim3 grid, cudaStream_t s) {
   constexpr int SMEM = (BM3 + BN) * BK3 * 4 * STAGES + 1024;
   auto k = gemm_v3_kernel<BN, STAGES>;
-  static bool configured = false;
-  if (!configured) {
+  static PerDeviceMax configured;
+  if (configured.need(current_device(), 1)) {
     AP_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
     // split-K clusters of up to 16 CTAs (beyond the portable 8)
     AP_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    configured = true;
   }
   if (!g.cluster) {
     launch_pdl(k, grid, dim3(128), SMEM, s, ma, mb, g);
@@ -620,11 +618,9 @@ static int launch_v3_impl(const float* A, int64_t lda, int transA, const float* 
     if (!make_map(&maq, A, M, K, lda, BM3 / 4)) return AP_ERR_UNSUPPORTED;
     constexpr int SMEM = (BM3 + 64) * BK3 * 4 * 6 + 1024;
     auto k = gemm_v3_mc_kernel<64, 6, 4>;
-    static bool mc_configured = false;
-    if (!mc_configured) {
+    static PerDeviceMax mc_configured;
+    if (mc_configured.need(current_device(), 1))
       AP_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
-      mc_configured = true;
-    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(128);

@@ -492,7 +492,6 @@ __global__ void trace_kernel(const int32_t* prog, int64_t prog_len, const int32_
   result[1] = t.conflict_site;
 }
 
-int g_num_sms = -1;
 
 }  // namespace
 
@@ -575,11 +574,8 @@ int launch_propagate(const GraphTables* g, const DecisionTables* d, const int8_t
       auto ck = vec ? (tbl ? propagate_cta_kernel<true, true> : propagate_cta_kernel<true, false>)
                     : (tbl ? propagate_cta_kernel<false, true> : propagate_cta_kernel<false, false>);
       AP_CUDA_CHECK(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
-      if (g_num_sms < 0) {
-        int dev = 0;
-        AP_CUDA_CHECK(cudaGetDevice(&dev));
-        AP_CUDA_CHECK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-      }
+      int g_num_sms = 0;
+      if (int rc = current_sm_count(&g_num_sms)) return rc;
       int cper = 0;
       AP_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cper, ck, kThreads, (size_t)csmem));
       const int cgrid = (int)std::min<int64_t>(batch, (int64_t)g_num_sms * std::max(cper, 1));
@@ -597,11 +593,8 @@ int launch_propagate(const GraphTables* g, const DecisionTables* d, const int8_t
   auto kern = vec ? (use_table ? propagate_kernel<true, true> : propagate_kernel<true, false>)
                   : (use_table ? propagate_kernel<false, true> : propagate_kernel<false, false>);
   AP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  if (g_num_sms < 0) {
-    int dev = 0;
-    AP_CUDA_CHECK(cudaGetDevice(&dev));
-    AP_CUDA_CHECK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-  }
+  int g_num_sms = 0;
+  if (int rc = current_sm_count(&g_num_sms)) return rc;
   int per_sm = 0;
   AP_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, (size_t)smem));
   per_sm = std::max(per_sm, 1);

@@ -433,12 +433,10 @@ int launch_per_sample(const double* prio, int n_host_max, double beta, const flo
                       int32_t* idx, float* w, double* max_prio, const int64_t* ctl, uint64_t seed, cudaStream_t s) {
   if (n_host_max <= kSampleSmemMax && std::getenv("AP_PER_ROWSCAN") == nullptr) {  // padded CDF in shared memory
     const int64_t psmem = (int64_t)(n_host_max + n_host_max / 16 + 1) * 8;
-    static int64_t pconfigured = -1;
-    if (psmem > pconfigured) {
+    static PerDeviceMax pconfigured;
+    if (pconfigured.need(current_device(), psmem + 1))
       AP_CUDA_CHECK(cudaFuncSetAttribute(per_sample_pad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)psmem));
-      pconfigured = psmem;
-    }
     launch_pdl(per_sample_pad_kernel, dim3(1), dim3(kSampleThreads), (size_t)psmem, s, prio, n_host_max, beta,
                uniforms, B, idx, w, max_prio, ctl, seed);
     AP_CUDA_CHECK(cudaGetLastError());
@@ -446,12 +444,10 @@ int launch_per_sample(const double* prio, int n_host_max, double beta, const flo
   }
   // shared CDF sized for the largest ring this launch can see
   const int64_t smem = n_host_max <= kSampleSmemMax ? (int64_t)n_host_max * 8 : 0;
-  static int64_t configured = -1;
-  if (smem > configured) {
+  static PerDeviceMax configured;
+  if (configured.need(current_device(), smem + 1))
     AP_CUDA_CHECK(cudaFuncSetAttribute(per_sample_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)std::max<int64_t>(smem, 0)));
-    configured = smem;
-  }
   launch_pdl(per_sample_fast_kernel, dim3(1), dim3(kSampleThreads), (size_t)smem, s, prio, n_host_max, 0.0, beta, uniforms, B, cdf, idx, w,
                                                                  max_prio, ctl, seed, (int)(smem / 8));
   AP_CUDA_CHECK(cudaGetLastError());

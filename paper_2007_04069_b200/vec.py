@@ -585,12 +585,16 @@ class VecDqnTrainer:
             self._advance_host(learn)
             return
         if self.graph is None:
-            # one eager step first: allocates every lazily-sized buffer (split-K
-            # workspace, torch temporaries) outside the capture
-            self._step_body(learn)
+            # one eager step first, on the stream the capture will use: allocates every
+            # lazily-sized buffer (split-K workspaces are per (device, stream), torch
+            # temporaries) outside the capture
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                self._step_body(learn)
+            torch.cuda.current_stream().wait_stream(s)
             self._advance_host(learn)
             launches0 = self.launches
-            s = torch.cuda.Stream()
             s.wait_stream(torch.cuda.current_stream())
             self.graph = torch.cuda.CUDAGraph()
             with torch.cuda.stream(s):
