@@ -68,6 +68,7 @@ def parse_args():
     p.add_argument("--pp-envs", type=int, default=512, help="PP-train env states evaluated per launch")
     p.add_argument("--pp-dqn-envs", type=int, default=1024, help="vectorised PP-train DQN envs per GPU")
     p.add_argument("--single-steps", type=int, default=300)
+    p.add_argument("--single-episodes", type=int, default=30, help="episodes of the device-resident single-env loop")
     return p.parse_args()
 
 
@@ -1130,7 +1131,24 @@ def bench_dqn_single(args, g, dims, groups, want_cpu):
     out = {"value": args.single_steps / dt, "unit": "env-steps/s",
            "config": {"graph": args.workload, "task": "opp", "envs": 1, "learn_batch": 64,
                       "learn_to_env_step_ratio": "1:1", "semantics": "reference train_partition loop",
+                      "driver": "host loop (search.train_partition): Python per step, kernels per call",
                       "precision": agent.net.precision}}
+    # the same loop entirely on the device (devloop.train_partition_device): numpy's PCG64 stream on the
+    # GPU, one CUDA graph with WHILE / IF nodes over whole episodes; bit-identical to the host loop
+    from paper_2007_04069_b200 import devloop
+
+    env_d = OppEnv(g, groups=groups)
+    agent_d = DqnAgent(cfg, env_d.state_dim, env_d.num_actions, 0)
+    devloop.train_partition_device(env_d, agent_d, 2)  # fills the ring past the first batch
+    t0 = time.perf_counter()
+    devloop.train_partition_device(env_d, agent_d, args.single_episodes)
+    wall = time.perf_counter() - t0
+    st = dict(devloop.last_stats)
+    out["device_loop"] = {"value": st["steps"] / (st["device_ms"] / 1e3), "unit": "env-steps/s",
+                          "steps": st["steps"], "episodes": args.single_episodes, "train_steps": st["train_steps"],
+                          "graph_launches": st["launches"], "device_ms": st["device_ms"],
+                          "wall_incl_capture_and_log_readback": st["steps"] / wall,
+                          "driver": "devloop.train_partition_device (CUDA graph, conditional nodes)"}
     if want_cpu:
         out["cpu_baseline"] = cpu_dqn_single(g, args.workload, "opp", args.cpu_seconds)
     return out

@@ -523,6 +523,106 @@ int ap_per_sample_fast(const double* scaled_priorities, int32_t n, double alpha,
 int ap_per_update_scaled(double* scaled, const int32_t* indices, const float* td, int32_t B, double alpha,
                          void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Reference-semantics search loop on the device (parity mode, one env):
+ * train_partition (cli.py:193-248) with agent.act / env.step / observe /
+ * learn (agent.py:155-337, envs.py:103-175) as kernels, numpy's PCG64 stream
+ * reproduced on the device, and a CUDA graph with WHILE / IF conditional nodes
+ * looping over episodes without returning to the host.
+ * ctl words 0..3 are the AP_CTL_* words of the vector driver.
+ * ------------------------------------------------------------------------- */
+enum {
+  AP_PL_STEP = 0,       /* env steps of this launch (log index) */
+  AP_PL_EPISODES = 4,   /* episodes finished in this launch */
+  AP_PL_BUDGET = 5,     /* episodes to run in this launch */
+  AP_PL_MAX_STEPS = 6,  /* log capacity (steps) */
+  AP_PL_POS = 7,        /* candidate index up for decision (-1 none) */
+  AP_PL_EP_STEPS = 8,   /* steps of the running episode */
+  AP_PL_BEST_PART = 9,  /* incumbent partitions (-1 none) */
+  AP_PL_BEST_EP = 10,   /* incumbent episode (run-relative) */
+  AP_PL_SYNC = 11,      /* target sync due after this learn step */
+  AP_PL_T_POS = 12,     /* decision position of the reset template */
+  AP_PL_EP_BASE = 13,   /* run-relative index of this launch's first episode */
+  AP_PL_TRAIN0 = 14,    /* train steps before the run (loss log base) */
+  AP_PL_LOSS_BAD = 15,  /* first run-relative train step with a non-finite loss, or -1 */
+  AP_PL_TAB_BASE = 16,  /* Adam step t of bias-correction table entry 0, minus 1 */
+  AP_PL_WORDS = 32
+};
+enum { AP_PLD_TOTAL = 0, AP_PLD_BEST_REWARD = 1, AP_PLD_WORDS = 2 };
+
+typedef struct ap_parity_loop {
+  int64_t* ctl;             /* [AP_PL_WORDS] */
+  double* dctl;             /* [AP_PLD_WORDS]: episode return so far, incumbent return */
+  uint64_t* rng;            /* numpy PCG64: state hi, lo, inc hi, lo, has_uint32, uinteger */
+  int32_t n, ld;            /* candidate dims, seed / status row stride */
+  int32_t num_actions;
+  int8_t* seeds;            /* [ld] committed seeds of the episode */
+  int8_t* seeds_try;        /* [ld] seeds + this step's decision (K1 input row) */
+  int8_t* decided;          /* [ld] decided candidate statuses */
+  const int8_t* status;     /* [ld] K1 candidate statuses of seeds_try */
+  const uint8_t* outcome;   /* [1] K1 outcome */
+  const int32_t* order;     /* [n] decision order (candidate indices) */
+  const int8_t* t_seeds;    /* reset template (reset or finetune_reset) */
+  const int8_t* t_decided;
+  float* state;             /* [n + 1] current state row (the Q-network input) */
+  float* r_states;          /* replay ring [cap, r_ld] */
+  float* r_next;
+  int64_t r_ld, cap;
+  int32_t* r_actions;
+  float* r_rewards;
+  uint8_t* r_done;
+  uint8_t* r_mask;          /* [cap, num_actions] */
+  double* r_prio;
+  double eps_start, eps_final;
+  int64_t eps_decay;
+  int8_t* best_row;         /* [ld] incumbent strategy */
+  int32_t* log_action;      /* [max_steps] */
+  double* log_reward;
+  int32_t* log_pos;
+  int8_t* log_decided;      /* [max_steps, ld] state rows before each step, or NULL */
+  uint8_t* ep_conflict;     /* [budget] */
+  int32_t* ep_len;
+  double* ep_return;
+  float* loss_log;          /* [loss_cap] summed batch loss per train step */
+  int64_t loss_cap;
+} ap_parity_loop;
+
+/* agent.act: eps-greedy with numpy's draws (random(), integers(A)) over Q of the
+ * current state; writes the K1 input row seeds_try. */
+int ap_parity_act(const ap_parity_loop* L, const float* q_dev, int32_t* action_dev, void* stream);
+/* env.step after K1 + episode bookkeeping + agent.observe (ring push at the
+ * current max priority) + reset to the template after a finished episode. */
+int ap_parity_post(const ap_parity_loop* L, const int32_t* action_dev, void* stream);
+/* B random() draws (the uniforms of rng.choice in PER sampling). */
+int ap_parity_uniforms(const ap_parity_loop* L, int32_t B, double* out_dev, void* stream);
+/* loss log, train-step counter, target-sync flag. */
+int ap_parity_learn_tail(const ap_parity_loop* L, const float* loss_dev, int32_t sync_every, void* stream);
+/* dst[k][:count[k]] = src[k][...] when ctl[AP_PL_SYNC] (n <= 8 segments). */
+int ap_parity_target_sync(const int64_t* ctl, int32_t n, const float* const* src, float* const* dst,
+                          const int64_t* count, void* stream);
+/* ap_per_sample over the first ctl[AP_CTL_SIZE] priorities (device-held ring
+ * size); scratch holds 2 * capacity + B doubles. */
+int ap_per_sample_n_ctl(const double* priorities, const int64_t* ctl, int64_t capacity, double alpha, double beta,
+                        const double* uniforms, int32_t B, double* scratch, int32_t* indices, float* weights,
+                        void* stream);
+/* ap_dqn_adam with the bias corrections of step t = ctl[AP_CTL_TRAIN] + t_offset + 1
+ * read from a host-computed table: ctab[2 * k + {0, 1}] = fp32(1 - beta{1,2}^t)
+ * for k = t - 1 - ctl[AP_PL_TAB_BASE] (the host's `1.0 - beta ** t`, agent.py:241-242). */
+int ap_dqn_adam_tab(float* params, const float* grads, float* m, float* v, int64_t n, float lr, float beta1,
+                    float beta2, float eps, const float* ctab, const int64_t* ctl, int64_t t_offset, void* stream);
+
+/* Host-side run of the device's numpy PCG64 emulation (pcg64.cuh), for tests:
+ * ops[i] = 0 draws random(), ops[i] = k >= 1 draws integers(k); state6 advances. */
+int ap_pcg64_host_draws(uint64_t* state6, const int64_t* ops, int32_t n, double* out);
+
+typedef struct ap_loop* ap_loop_t;
+/* Outer graph: WHILE(episodes < budget && steps < max_steps) { step_graph;
+ * IF(ring size >= batch) { learn_graph } }.  The graphs (cudaGraph_t) are
+ * cloned as child graphs. */
+int ap_loop_graph_create(void* step_graph, void* learn_graph, const int64_t* ctl, int64_t batch, ap_loop_t* out);
+int ap_loop_graph_launch(ap_loop_t loop, void* stream);
+int ap_loop_graph_destroy(ap_loop_t loop);
+
 const char* ap_last_error(void);
 const char* ap_version(void);
 

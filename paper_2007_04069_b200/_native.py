@@ -95,6 +95,32 @@ _F64 = ctypes.c_double
 _F32 = ctypes.c_float
 _U64 = ctypes.c_uint64
 _TOPO = ctypes.POINTER(Topology)
+
+
+class ParityLoopDesc(ctypes.Structure):
+    """ap_parity_loop (include/autoplan_b200.h): the device search loop's buffers."""
+
+    _fields_ = [
+        ("ctl", ctypes.c_void_p), ("dctl", ctypes.c_void_p), ("rng", ctypes.c_void_p),
+        ("n", ctypes.c_int32), ("ld", ctypes.c_int32), ("num_actions", ctypes.c_int32),
+        ("seeds", ctypes.c_void_p), ("seeds_try", ctypes.c_void_p), ("decided", ctypes.c_void_p),
+        ("status", ctypes.c_void_p), ("outcome", ctypes.c_void_p), ("order", ctypes.c_void_p),
+        ("t_seeds", ctypes.c_void_p), ("t_decided", ctypes.c_void_p), ("state", ctypes.c_void_p),
+        ("r_states", ctypes.c_void_p), ("r_next", ctypes.c_void_p), ("r_ld", ctypes.c_int64), ("cap", ctypes.c_int64),
+        ("r_actions", ctypes.c_void_p), ("r_rewards", ctypes.c_void_p), ("r_done", ctypes.c_void_p),
+        ("r_mask", ctypes.c_void_p), ("r_prio", ctypes.c_void_p),
+        ("eps_start", ctypes.c_double), ("eps_final", ctypes.c_double), ("eps_decay", ctypes.c_int64),
+        ("best_row", ctypes.c_void_p), ("log_action", ctypes.c_void_p), ("log_reward", ctypes.c_void_p),
+        ("log_pos", ctypes.c_void_p), ("log_decided", ctypes.c_void_p), ("ep_conflict", ctypes.c_void_p),
+        ("ep_len", ctypes.c_void_p), ("ep_return", ctypes.c_void_p), ("loss_log", ctypes.c_void_p),
+        ("loss_cap", ctypes.c_int64),
+    ]
+
+
+_PL = ctypes.POINTER(ParityLoopDesc)
+PL = {"STEP": 0, "SLOT": 1, "SIZE": 2, "TRAIN": 3, "EPISODES": 4, "BUDGET": 5, "MAX_STEPS": 6, "POS": 7,
+      "EP_STEPS": 8, "BEST_PART": 9, "BEST_EP": 10, "SYNC": 11, "T_POS": 12, "EP_BASE": 13, "TRAIN0": 14,
+      "LOSS_BAD": 15, "TAB_BASE": 16, "WORDS": 32}
 SIGNATURES: dict[str, tuple] = {
     "ap_graph_create": (ctypes.c_int, [ctypes.POINTER(GraphDesc), ctypes.POINTER(_VP)]),
     "ap_graph_destroy": (ctypes.c_int, [_VP]),
@@ -104,6 +130,17 @@ SIGNATURES: dict[str, tuple] = {
     "ap_decision_destroy": (ctypes.c_int, [_VP]),
     "ap_propagate_batch": (ctypes.c_int, [_VP, _VP, _VP, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _VP, _VP]),
     "ap_propagate_batch_packed": (ctypes.c_int, [_VP, _VP, _VP, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _VP, _VP]),
+    "ap_parity_act": (ctypes.c_int, [_PL, _VP, _VP, _VP]),
+    "ap_parity_post": (ctypes.c_int, [_PL, _VP, _VP]),
+    "ap_parity_uniforms": (ctypes.c_int, [_PL, _I32, _VP, _VP]),
+    "ap_parity_learn_tail": (ctypes.c_int, [_PL, _VP, _I32, _VP]),
+    "ap_parity_target_sync": (ctypes.c_int, [_VP, _I32, _VP, _VP, _VP, _VP]),
+    "ap_per_sample_n_ctl": (ctypes.c_int, [_VP, _VP, _I64, _F64, _F64, _VP, _I32, _VP, _VP, _VP, _VP]),
+    "ap_dqn_adam_tab": (ctypes.c_int, [_VP, _VP, _VP, _VP, _I64, _F32, _F32, _F32, _F32, _VP, _VP, _I64, _VP]),
+    "ap_loop_graph_create": (ctypes.c_int, [_VP, _VP, _VP, _I64, ctypes.POINTER(_VP)]),
+    "ap_loop_graph_launch": (ctypes.c_int, [_VP, _VP]),
+    "ap_loop_graph_destroy": (ctypes.c_int, [_VP]),
+    "ap_pcg64_host_draws": (ctypes.c_int, [_VP, _VP, _I32, _VP]),
     "ap_propagate_trace": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "ap_pipe_create": (ctypes.c_int, [ctypes.POINTER(PipeDesc), ctypes.POINTER(_VP)]),
     "ap_pipe_destroy": (ctypes.c_int, [_VP]),

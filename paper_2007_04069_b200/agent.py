@@ -621,11 +621,20 @@ class _Batch:
 def train_step_device(net: QNetwork, target_net: QNetwork, buffer: PrioritizedReplayBuffer, config: AgentConfig,
                       optimizer: AdamOptimizer, uniforms, batch: _Batch | None = None):
     """One double-DQN update, all on the device; returns the loss as a device scalar (agent.py:258-299)."""
+    b = config.batch_size
+    batch = batch or _Batch(b, net.state_dim, net.num_actions)
+    idx, weights = buffer.sample_device(b, config.per_alpha, config.per_beta, uniforms)
+    return update_on_indices(net, target_net, buffer, config, idx, weights, batch, optimizer.step)
+
+
+def update_on_indices(net: QNetwork, target_net: QNetwork, buffer: PrioritizedReplayBuffer, config: AgentConfig,
+                      idx, weights, batch: _Batch, adam_step) -> "torch.Tensor":
+    """The update of train_step (agent.py:277-299) for sampled ring indices / IS weights on the
+    device: gathers, double-DQN targets, Huber TD, backward, `adam_step()`, priorities, loss.
+    Shared by the host-driven agent and the device search loop (devloop.py), which captures it."""
     lib = _native.require_device()
     b = config.batch_size
     s = buffer.store
-    batch = batch or _Batch(b, net.state_dim, net.num_actions)
-    idx, weights = buffer.sample_device(b, config.per_alpha, config.per_beta, uniforms)
     for src, dst in ((s["states"], batch.states), (s["next_states"], batch.next_states)):
         _native.check(lib.ap_gather_rows(_native.ptr(src), src.stride(0), _native.ptr(idx), b, src.shape[1],
                                          _native.ptr(dst), dst.stride(0), _stream()))
@@ -643,7 +652,7 @@ def train_step_device(net: QNetwork, target_net: QNetwork, buffer: PrioritizedRe
                                 float(config.gamma), float(config.huber_delta), _native.ptr(batch.dz),
                                 batch.dz.stride(0), _native.ptr(batch.td), _native.ptr(batch.loss_rows), _stream()))
     net.backward_device(acts, batch.dz)
-    optimizer.step()
+    adam_step()
     buffer.update_priorities_device(idx, batch.td)
     _native.check(lib.ap_dqn_colsum(_native.ptr(batch.loss_rows), 1, b, 1, _native.ptr(batch.loss), _stream()))
     return batch.loss

@@ -19,39 +19,10 @@
 #include <cstdint>
 
 #include "engine.h"
+#include "pcg64.cuh"
 
 namespace apb {
 namespace {
-
-using u128 = unsigned __int128;
-
-__device__ __forceinline__ u128 pcg_mult() {
-  return ((u128)0x2360ED051FC65DA4ULL << 64) | (u128)0x4385DF649FCCF645ULL;
-}
-
-// state after `delta` steps (PCG advance: repeated squaring of the affine map)
-__device__ u128 pcg_advance(u128 state, u128 inc, uint64_t delta) {
-  u128 cur_mult = pcg_mult(), cur_plus = inc, acc_mult = 1, acc_plus = 0;
-  while (delta > 0) {
-    if (delta & 1) {
-      acc_mult *= cur_mult;
-      acc_plus = acc_plus * cur_mult + cur_plus;
-    }
-    cur_plus = (cur_mult + 1) * cur_plus;
-    cur_mult *= cur_mult;
-    delta >>= 1;
-  }
-  return acc_mult * state + acc_plus;
-}
-
-__device__ __forceinline__ double pcg_next_double(u128& state, u128 inc) {
-  state = state * pcg_mult() + inc;
-  const uint64_t hi = (uint64_t)(state >> 64), lo = (uint64_t)state;
-  const unsigned rot = (unsigned)(state >> 122);
-  const uint64_t x = hi ^ lo;
-  const uint64_t r = (x >> rot) | (x << ((64u - rot) & 63u));
-  return (double)(r >> 11) * (1.0 / 9007199254740992.0);
-}
 
 constexpr int kGenThreads = 256;
 

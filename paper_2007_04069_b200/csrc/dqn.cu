@@ -535,9 +535,14 @@ __global__ void colsum_kernel(const float* x, int64_t ld, int rows, int cols, fl
 
 // ctl != nullptr: bias corrections from step t = ctl[AP_CTL_TRAIN] + 1
 __global__ void adam_kernel(float* p, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2,
-                            float eps, float c1, float c2, const int64_t* ctl) {
+                            float eps, float c1, float c2, const int64_t* ctl, const float* ctab,
+                            int64_t t_offset) {
   pdl_entry();
-  if (ctl) {  // bias corrections once per block, not per thread (two fp64 pow)
+  if (ctab) {  // parity loop: the host's fp32(1 - beta**t), t = ctl[AP_CTL_TRAIN] + t_offset + 1
+    const int64_t k = ctl[AP_CTL_TRAIN] + t_offset - ctl[AP_PL_TAB_BASE];
+    c1 = ctab[2 * k];
+    c2 = ctab[2 * k + 1];
+  } else if (ctl) {  // bias corrections once per block, not per thread (two fp64 pow)
     __shared__ float s_c[2];
     if (threadIdx.x == 0) {
       const double t = (double)(ctl[AP_CTL_TRAIN] + 1);
@@ -749,8 +754,10 @@ __device__ double pairwise_sum(const double* a, int64_t n) {
 
 // one CTA: PER sample (agent.py:207-223) for B uniforms drawn by the caller
 __global__ void per_sample_kernel(const double* prio, int n, double alpha, double beta, const double* uniforms, int B,
-                                  double* scaled, double* cdf, int32_t* idx_out, float* w_out) {
+                                  double* scaled, double* cdf, int32_t* idx_out, float* w_out,
+                                  const int64_t* ctl) {
   pdl_entry();
+  if (ctl) n = (int)ctl[AP_CTL_SIZE];  // device-held ring size (parity loop)
   __shared__ double s_total, s_last, s_wmax;
   for (int i = threadIdx.x; i < n; i += blockDim.x) scaled[i] = pow(prio[i], alpha);
   __syncthreads();
@@ -1044,7 +1051,8 @@ int ap_dqn_adam(float* params, const float* grads, float* m, float* v, int64_t n
                 float eps, float correct1, float correct2, void* stream) {
   if (n <= 0) return AP_OK;
   launch_pdl(adam_kernel, dim3(blocks_for(n, 256)), dim3(256), 0, (cudaStream_t)stream, params, grads, m, v, n, lr, beta1, beta2, eps,
-                                                                     correct1, correct2, nullptr);
+                                                                     correct1, correct2, nullptr,
+             (const float*)nullptr, (int64_t)0);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
@@ -1132,7 +1140,8 @@ int ap_dqn_adam_ctl(float* params, const float* grads, float* m, float* v, int64
   }
   if (n <= 0) return AP_OK;
   launch_pdl(adam_kernel, dim3(blocks_for(n, 256)), dim3(256), 0, (cudaStream_t)stream, params, grads, m, v, n, lr, beta1, beta2, eps,
-                                                                     1.f, 1.f, ctl);
+                                                                     1.f, 1.f, ctl, (const float*)nullptr,
+             (int64_t)0);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
@@ -1145,7 +1154,34 @@ int ap_per_sample(const double* priorities, int32_t n, double alpha, double beta
   }
   // scratch: [n] scaled + [n + B] cdf / weights
   launch_pdl(per_sample_kernel, dim3(1), dim3(256), 0, (cudaStream_t)stream, priorities, n, alpha, beta, uniforms, B, scratch,
-                                                         scratch + n, indices, weights);
+                                                         scratch + n, indices, weights, (const int64_t*)nullptr);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_per_sample_n_ctl(const double* priorities, const int64_t* ctl, int64_t capacity, double alpha, double beta,
+                        const double* uniforms, int32_t B, double* scratch, int32_t* indices, float* weights,
+                        void* stream) {
+  if (!priorities || !ctl || !uniforms || !scratch || !indices || !weights || B < 1 || capacity < 1) {
+    set_error("ap_per_sample_n_ctl: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  // scratch: [capacity] scaled priorities, then [capacity + B] cdf / weights
+  launch_pdl(per_sample_kernel, dim3(1), dim3(256), 0, (cudaStream_t)stream, priorities, 0, alpha, beta, uniforms, B,
+             scratch, scratch + capacity, indices, weights, (const int64_t*)ctl);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_dqn_adam_tab(float* params, const float* grads, float* m, float* v, int64_t n, float lr, float beta1,
+                    float beta2, float eps, const float* ctab, const int64_t* ctl, int64_t t_offset, void* stream) {
+  if (!ctab || !ctl) {
+    set_error("ap_dqn_adam_tab: null table or control block");
+    return AP_ERR_INVALID;
+  }
+  if (n <= 0) return AP_OK;
+  launch_pdl(adam_kernel, dim3(blocks_for(n, 256)), dim3(256), 0, (cudaStream_t)stream, params, grads, m, v, n, lr,
+             beta1, beta2, eps, 1.f, 1.f, (const int64_t*)ctl, ctab, t_offset);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }
