@@ -995,54 +995,63 @@ def cpu_pp_train(g, topo, K, applied):
 
 
 def bench_env_gen(args, world, rank, want_cpu):
-    """PP-infer data plane: synthetic uniform profiles (generate_environment('uniform', 1280, seed) ->
-    3 x 128 scaled arrays) generated per second on the device, bit-identical to the host path.
-    Each rank generates its own contiguous seed range (weak scaling, no collective)."""
+    """PP-infer data plane: synthetic profiles (generate_environment(dist, 1280, seed) -> 3 x 128 scaled
+    arrays) generated per second on the device, bit-identical to the host path, for the reference's three
+    distributions.  Each rank generates its own contiguous seed range (weak scaling, no collective)."""
     import torch
 
     from paper_2007_04069_b200 import _native
     from paper_2007_04069_b200.dataproc import pcg64_states
 
-    E, n, G = 65536, 1280, 128
-    st = pcg64_states(range(rank * E, (rank + 1) * E))  # PCG64 seeding stays numpy's (host, untimed)
-    d_st = torch.from_numpy(st.view("int64")).cuda()
-    out = torch.empty((E, 3, G), dtype=torch.float64, device="cuda")
-    lib = _native.require_device()
+    n, G = 1280, 128
+    out_all = {}
+    for kind, dist, E in ((0, "uniform", 65536), (1, "normal", 65536), (2, "binomial", 16384)):
+        st = pcg64_states(range(rank * E, (rank + 1) * E))  # PCG64 seeding stays numpy's (host, untimed)
+        d_st = torch.from_numpy(st.view("int64")).cuda()
+        out = torch.empty((E, 3, G), dtype=torch.float64, device="cuda")
+        lib = _native.require_device()
 
-    def run():
-        _native.check(lib.ap_generate_uniform_envs(_native.ptr(d_st), E, n, G, _native.ptr(out),
-                                                   _native.stream_handle()))
+        def run():
+            _native.check(lib.ap_generate_envs(kind, _native.ptr(d_st), E, n, G, _native.ptr(out),
+                                               _native.stream_handle()))
 
-    for _ in range(3):
-        run()
-    torch.cuda.synchronize()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    iters = 10
-    s.record()
-    for _ in range(iters):
-        run()
-    e.record()
-    torch.cuda.synchronize()
-    ms = _max_over_ranks(s.elapsed_time(e), world) / iters
-    draws_per_s = E * 3 * n / (ms / 1e3)
-    res = {"value": world * E / (ms / 1e3), "unit": "environments/s",
-           "config": {"distribution": "uniform", "source_length": n, "granularity": G, "envs_per_launch": E,
-                      "seeds": "rank * 65536 + [0, 65536)"},
-           "ms_per_launch": ms, "pcg64_draws_per_s": draws_per_s}
-    if want_cpu:
-        try:
-            _ref_import()
-            from autoplan.dataproc import generate_environment as ref_gen
+        for _ in range(2):
+            run()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        iters = 5
+        s.record()
+        for _ in range(iters):
+            run()
+        e.record()
+        torch.cuda.synchronize()
+        ms = _max_over_ranks(s.elapsed_time(e), world) / iters
+        res = {"value": world * E / (ms / 1e3), "unit": "environments/s",
+               "config": {"distribution": dist, "source_length": n, "granularity": G, "envs_per_launch": E,
+                          "seeds": f"rank * {E} + [0, {E})",
+                          "sampler": {"uniform": "PCG64 jump-ahead, one CTA per env",
+                                      "normal": "numpy ziggurat, one thread per env",
+                                      "binomial": "numpy BTPE, one thread per env"}[dist]},
+               "ms_per_launch": ms}
+        if want_cpu:
+            try:
+                _ref_import()
+                from autoplan.dataproc import generate_environment as ref_gen
 
-            k, t0 = 0, time.perf_counter()
-            while time.perf_counter() - t0 < 2.0:
-                ref_gen("uniform", n, k)
-                k += 1
-            res["cpu_baseline"] = {"value": k / (time.perf_counter() - t0), "unit": "environments/s", "cores": 1,
-                                   "kind": "reference", "sample": f"{k} reference generate_environment calls (2 s)"}
-        except ImportError as exc:
-            res["cpu_baseline"] = {"unavailable": f"baseline/_ref not importable: {exc}"}
-    return res
+                k, t0 = 0, time.perf_counter()
+                while time.perf_counter() - t0 < 1.5:
+                    ref_gen(dist, n, k)
+                    k += 1
+                res["cpu_baseline"] = {"value": k / (time.perf_counter() - t0), "unit": "environments/s",
+                                       "cores": 1, "kind": "reference",
+                                       "sample": f"{k} reference generate_environment({dist!r}) calls (1.5 s)"}
+            except ImportError as exc:
+                res["cpu_baseline"] = {"unavailable": f"baseline/_ref not importable: {exc}"}
+        out_all[dist] = res
+        del out, d_st
+    head = dict(out_all["uniform"])
+    head["by_distribution"] = out_all
+    return head
 
 
 def bench_pp_infer(args, world, want_cpu):

@@ -231,6 +231,17 @@ int ap_pipe_train_state_ex(ap_pipe_t p, const ap_topology* topo, const int32_t* 
                            double backward_multiplier, double* state_dev, float* state_f32, int64_t ld_f32,
                            float* state_f32_b, int64_t ld_f32_b, void* stream);
 
+/* generate_environment(distribution, n, seed) (dataproc.py:123-145) for many
+ * seeds: kind 0 uniform (= ap_generate_uniform_envs), 1 normal (numpy's
+ * ziggurat, N(0.5, 0.15) clipped to [0, 1]), 2 binomial (numpy's BTPE,
+ * B(100, 0.5) / 100).  pcg_states as ap_generate_uniform_envs; arrays_out
+ * [num_envs, 3, granularity] fp64, bit-identical to the host. */
+int ap_generate_envs(int32_t kind, const uint64_t* pcg_states, int64_t num_envs, int32_t n, int32_t granularity,
+                     double* arrays_out, void* stream);
+/* Host run of the device samplers (tests): kind 0 Generator.standard_normal(),
+ * kind 1 Generator.binomial(bin_n, bin_p); state6 as ap_pcg64_host_draws. */
+int ap_np_samples_host(uint64_t* state6, int32_t kind, int64_t count, int64_t bin_n, double bin_p, double* out);
+
 /* Host-consumer slot format (run_batch_host(want_slots="packed")): K1's int8
  * slot rows [batch, slots_stride] (-1 / 0 / 1, sharding.py:36-48) packed to
  * 2 bits per slot, code = status + 1, slot j in bits 2*(j%4) of byte j/4 of

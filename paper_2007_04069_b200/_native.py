@@ -141,6 +141,8 @@ SIGNATURES: dict[str, tuple] = {
     "ap_loop_graph_launch": (ctypes.c_int, [_VP, _VP]),
     "ap_loop_graph_destroy": (ctypes.c_int, [_VP]),
     "ap_pcg64_host_draws": (ctypes.c_int, [_VP, _VP, _I32, _VP]),
+    "ap_generate_envs": (ctypes.c_int, [_I32, _VP, _I64, _I32, _I32, _VP, _VP]),
+    "ap_np_samples_host": (ctypes.c_int, [_VP, _I32, _I64, _I64, _F64, _VP]),
     "ap_propagate_trace": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "ap_pipe_create": (ctypes.c_int, [ctypes.POINTER(PipeDesc), ctypes.POINTER(_VP)]),
     "ap_pipe_destroy": (ctypes.c_int, [_VP]),

@@ -24,7 +24,9 @@ INCLUDE_DIR = PKG_DIR.parent / "include"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", f"-I{INCLUDE_DIR}"]
 # fp64 cost kernels must round every add / mul separately (bit parity with CPython)
-PER_FILE = {"pipecost.cu": ["-fmad=false"], "dqn.cu": ["--expt-relaxed-constexpr"]}
+PER_FILE = {"pipecost.cu": ["-fmad=false"], "dqn.cu": ["--expt-relaxed-constexpr"],
+            # numpy's samplers round every product / sum separately (no FMA in its baseline build)
+            "dataplane.cu": ["-fmad=false"], "parity.cu": ["-fmad=false"]}
 
 
 def _nvcc() -> str:

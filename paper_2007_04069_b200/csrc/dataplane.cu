@@ -13,13 +13,16 @@
 // Then, as the reference: naive sequential cumsum of c and w, right-endpoint
 // coarsening to G points, joint scaling by max(cs, as, ws, 0).
 //
-// normal / binomial profiles use numpy's ziggurat / BTPE rejection samplers,
-// which consume a data-dependent number of draws; they stay on the host.
+// normal / binomial profiles use numpy's ziggurat / BTPE rejection samplers
+// (np_samplers.cuh), which consume a data-dependent number of draws: one thread
+// walks one environment's stream sequentially, keeping the running cumsums and
+// capturing the coarse points as their source index passes.
 #include <algorithm>
 #include <cstdint>
 
 #include "engine.h"
 #include "pcg64.cuh"
+#include "np_samplers.cuh"
 
 namespace apb {
 namespace {
@@ -74,6 +77,57 @@ __global__ void __launch_bounds__(kGenThreads) uniform_env_kernel(const uint64_t
   }
 }
 
+// generate_environment(normal | binomial, n, seed) (dataproc.py:123-145), one thread
+// per environment: c, a, w drawn in the reference's order (n each), c and w as the
+// naive cumsum, right-endpoint coarsening to G points, joint scaling by the maximum.
+// kind 1: clip(0.5 + 0.15 * z, 0, 1); kind 2: binomial(100, 0.5) / 100.
+__global__ void __launch_bounds__(128) sampled_env_kernel(const uint64_t* __restrict__ seeds4, int64_t E, int n, int G,
+                                                         int kind, double* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const uint64_t* q = seeds4 + 4 * e;
+  NpPcg64 g;
+  g.state = ((u128)q[0] << 64) | (u128)q[1];
+  g.inc = ((u128)q[2] << 64) | (u128)q[3];
+  g.has_uint32 = 0;
+  g.uinteger = 0;
+  double* o = out + e * 3 * (int64_t)G;
+  double peak = 0.0;
+  for (int arr = 0; arr < 3; ++arr) {
+    const bool prefix = arr != 1;  // C and W are prefix sums, A stays pointwise
+    double acc = 0.0, last = 0.0;
+    int j = 0;  // next coarse point
+    for (int i = 0; i < n; ++i) {
+      double x;
+      if (kind == 1) {
+        x = __dadd_rn(0.5, __dmul_rn(0.15, np_standard_normal(g)));
+        x = fmin(fmax(x, 0.0), 1.0);  // np.clip(.., 0.0, 1.0)
+      } else {
+        x = __ddiv_rn((double)np_binomial(g, 100, 0.5), 100.0);
+      }
+      acc = prefix ? (i == 0 ? x : __dadd_rn(acc, x)) : x;
+      last = acc;
+      // right endpoint of coarse point j: floor((j + 1) * n / G) - 1 (n >= G)
+      while (j < G && n >= G && ((int64_t)(j + 1) * n) / G - 1 == i) {
+        o[arr * G + j] = acc;
+        peak = fmax(peak, acc);
+        ++j;
+      }
+      if (n < G && j < G && i == j) {  // shorter inputs: point j takes source j, padded with the last value
+        o[arr * G + j] = acc;
+        peak = fmax(peak, acc);
+        ++j;
+      }
+    }
+    for (; j < G; ++j) {  // n < G: right padding with the last value
+      o[arr * G + j] = last;
+      peak = fmax(peak, last);
+    }
+  }
+  if (peak > 0.0)
+    for (int i = 0; i < 3 * G; ++i) o[i] = __ddiv_rn(o[i], peak);
+}
+
 // Slot statuses for host consumers: K1's int8 slot rows (-1 undecided, 0 R,
 // 1 P; sharding.py:36-48 DimStatus) packed 2 bits per slot, code = status + 1,
 // slot j of a row in bits 2*(j%4) of byte j/4.  One thread packs one 16-byte
@@ -124,6 +178,33 @@ int ap_generate_uniform_envs(const uint64_t* pcg_states, int64_t num_envs, int32
   uniform_env_kernel<<<(unsigned)grid, kGenThreads, smem, (cudaStream_t)stream>>>(pcg_states, num_envs, n, granularity,
                                                                                   arrays_out);
   AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_generate_envs(int32_t kind, const uint64_t* pcg_states, int64_t num_envs, int32_t n, int32_t granularity,
+                     double* arrays_out, void* stream) {
+  if (kind == 0) return ap_generate_uniform_envs(pcg_states, num_envs, n, granularity, arrays_out, stream);
+  if ((kind != 1 && kind != 2) || num_envs < 0 || n < 1 || granularity < 1 ||
+      (num_envs > 0 && (!pcg_states || !arrays_out))) {
+    set_error("ap_generate_envs: bad arguments (kind 0 uniform, 1 normal, 2 binomial)");
+    return AP_ERR_INVALID;
+  }
+  if (num_envs == 0) return AP_OK;
+  const int64_t grid = (num_envs + 127) / 128;
+  sampled_env_kernel<<<(unsigned)grid, 128, 0, (cudaStream_t)stream>>>(pcg_states, num_envs, n, granularity, kind,
+                                                                        arrays_out);
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_np_samples_host(uint64_t* state6, int32_t kind, int64_t count, int64_t bin_n, double bin_p, double* out) {
+  if (!state6 || count < 0 || (count > 0 && !out) || (kind != 0 && kind != 1)) {
+    set_error("ap_np_samples_host: bad arguments (kind 0 standard_normal, 1 binomial)");
+    return AP_ERR_INVALID;
+  }
+  NpPcg64 g = NpPcg64::load(state6);
+  for (int64_t i = 0; i < count; ++i) out[i] = kind == 0 ? np_standard_normal(g) : (double)np_binomial(g, bin_n, bin_p);
+  g.store(state6);
   return AP_OK;
 }
 

@@ -84,22 +84,24 @@ def pcg64_states(seeds) -> np.ndarray:
 
 def generate_environments_device(distribution: str, n: int, seeds, granularity: int = GRANULARITY, states=None):
     """generate_environment(distribution, n, s) for every seed s at once on the GPU
-    (ap_generate_uniform_envs): a CUDA fp64 tensor [E, 3, G] of the scaled C, A, W arrays,
-    bit-identical to the host path.  Only the uniform profile: numpy's normal / binomial
-    samplers consume a data-dependent number of draws (ziggurat / BTPE) and stay on the host.
+    (ap_generate_envs): a CUDA fp64 tensor [E, 3, G] of the scaled C, A, W arrays,
+    bit-identical to the host path for all three distributions.  Uniform: one CTA per
+    environment, PCG64 jump-ahead per thread; normal / binomial: numpy's ziggurat / BTPE
+    samplers (data-dependent draw counts), one thread walking each environment's stream.
     `states` may pass precomputed pcg64_states(seeds)."""
     import torch
 
     from . import _native
 
-    if distribution != "uniform":
-        raise ProfileError("the device generator covers the uniform profile (normal / binomial: generate_environment)")
+    kinds = {"uniform": 0, "normal": 1, "binomial": 2}
+    if distribution not in kinds:
+        raise ProfileError(f"unknown distribution {distribution!r}")
     if n < 1:
         raise ProfileError("environment length must be >= 1")
     st = pcg64_states(seeds) if states is None else np.asarray(states, dtype=np.uint64)
     lib = _native.require_device()
     d_st = torch.from_numpy(st.view(np.int64)).cuda()
     out = torch.empty((st.shape[0], 3, granularity), dtype=torch.float64, device="cuda")
-    _native.check(lib.ap_generate_uniform_envs(_native.ptr(d_st), st.shape[0], n, granularity, _native.ptr(out),
-                                               _native.stream_handle()))
+    _native.check(lib.ap_generate_envs(kinds[distribution], _native.ptr(d_st), st.shape[0], n, granularity,
+                                       _native.ptr(out), _native.stream_handle()))
     return out
