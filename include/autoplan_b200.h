@@ -626,6 +626,58 @@ int ap_dqn_adam_tab(float* params, const float* grads, float* m, float* v, int64
  * ops[i] = 0 draws random(), ops[i] = k >= 1 draws integers(k); state6 advances. */
 int ap_pcg64_host_draws(uint64_t* state6, const int64_t* ops, int32_t n, double* out);
 
+/* ---------------------------------------------------------------------------
+ * Fused small-batch learner (csrc/fused_mlp.cu): one persistent cooperative
+ * kernel per DQN learn step -- forwards of the online and target networks,
+ * double-DQN TD + Huber (agent.py:258-299), the dueling-MLP backward
+ * (agent.py:111-136), priorities (agent.py:226) and Adam (agent.py:229-250),
+ * with grid barriers between dependent phases.  Network layout: the flat
+ * parameter buffer of QNetwork (w_i [dims[i], dims[i+1]] and b_i at w_off[i] /
+ * b_off[i], i <= L, the head at index L, dims[L+1] = 1 + A).
+ * ------------------------------------------------------------------------- */
+typedef struct ap_fused_learn {
+  int32_t L;                /* hidden layers, 1..4 */
+  int32_t dims[6];
+  int64_t w_off[5], b_off[5];
+  int32_t batch;            /* 1..256 */
+  float* params;            /* online flat parameters (updated in place) */
+  const float* target;      /* target flat parameters */
+  const float* r_states;    /* replay ring [cap, r_ld] */
+  const float* r_next;
+  int64_t r_ld;
+  const int32_t* r_actions;
+  const float* r_rewards;
+  const uint8_t* r_done;
+  const uint8_t* r_mask;    /* [cap, A] */
+  double* r_prio;           /* priorities[idx[b]] = |td| + 1e-6, the last duplicate wins */
+  const int32_t* idx;       /* [batch] sampled ring rows */
+  const float* weights;     /* [batch] importance weights */
+  float gamma, huber_delta;
+  float* grad;              /* [nparams] scratch gradient */
+  float* m;
+  float* v;
+  int64_t nparams;
+  float lr, beta1, beta2, eps;
+  float correct1, correct2; /* bias corrections, unless ctab (ap_dqn_adam_tab semantics) */
+  const float* ctab;
+  const int64_t* ctl;
+  int64_t t_offset;
+  float* wt[5];             /* transposed weight copies to refresh, or NULL */
+  int64_t wt_ld[5];
+  float* td;                /* [batch] */
+  float* loss;              /* [1] sum_b w_b huber(td_b) */
+  float* workspace;         /* ap_mlp_fused_workspace(L, dims, batch, 0) floats */
+  uint32_t* barrier;        /* [2] zero-initialised, private to the caller's stream */
+} ap_fused_learn;
+
+int64_t ap_mlp_fused_workspace(int32_t L, const int32_t* dims, int32_t rows, int32_t forward_only);
+int ap_dqn_learn_fused(const ap_fused_learn* args, void* stream);
+/* Q [rows, A] of the online network for rows x [rows, ldx] (rows <= 256), same kernel
+ * in forward mode: the act of the search loop. */
+int ap_mlp_forward_fused(int32_t L, const int32_t* dims, const int64_t* w_off, const int64_t* b_off,
+                         const float* params, const float* x, int64_t ldx, int32_t rows, float* q,
+                         float* workspace, uint32_t* barrier, void* stream);
+
 typedef struct ap_loop* ap_loop_t;
 /* Outer graph: WHILE(episodes < budget && steps < max_steps) { step_graph;
  * IF(ring size >= batch) { learn_graph } }.  The graphs (cudaGraph_t) are

@@ -118,6 +118,25 @@ class ParityLoopDesc(ctypes.Structure):
 
 
 _PL = ctypes.POINTER(ParityLoopDesc)
+
+
+class FusedLearnDesc(ctypes.Structure):
+    """ap_fused_learn (include/autoplan_b200.h): one fused DQN learn step."""
+
+    _fields_ = [
+        ("L", ctypes.c_int32), ("dims", ctypes.c_int32 * 6), ("w_off", ctypes.c_int64 * 5),
+        ("b_off", ctypes.c_int64 * 5), ("batch", ctypes.c_int32), ("params", ctypes.c_void_p),
+        ("target", ctypes.c_void_p), ("r_states", ctypes.c_void_p), ("r_next", ctypes.c_void_p),
+        ("r_ld", ctypes.c_int64), ("r_actions", ctypes.c_void_p), ("r_rewards", ctypes.c_void_p),
+        ("r_done", ctypes.c_void_p), ("r_mask", ctypes.c_void_p), ("r_prio", ctypes.c_void_p),
+        ("idx", ctypes.c_void_p), ("weights", ctypes.c_void_p), ("gamma", ctypes.c_float),
+        ("huber_delta", ctypes.c_float), ("grad", ctypes.c_void_p), ("m", ctypes.c_void_p), ("v", ctypes.c_void_p),
+        ("nparams", ctypes.c_int64), ("lr", ctypes.c_float), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float),
+        ("eps", ctypes.c_float), ("correct1", ctypes.c_float), ("correct2", ctypes.c_float),
+        ("ctab", ctypes.c_void_p), ("ctl", ctypes.c_void_p), ("t_offset", ctypes.c_int64),
+        ("wt", ctypes.c_void_p * 5), ("wt_ld", ctypes.c_int64 * 5), ("td", ctypes.c_void_p),
+        ("loss", ctypes.c_void_p), ("workspace", ctypes.c_void_p), ("barrier", ctypes.c_void_p),
+    ]
 PL = {"STEP": 0, "SLOT": 1, "SIZE": 2, "TRAIN": 3, "EPISODES": 4, "BUDGET": 5, "MAX_STEPS": 6, "POS": 7,
       "EP_STEPS": 8, "BEST_PART": 9, "BEST_EP": 10, "SYNC": 11, "T_POS": 12, "EP_BASE": 13, "TRAIN0": 14,
       "LOSS_BAD": 15, "TAB_BASE": 16, "WORDS": 32}
@@ -141,6 +160,9 @@ SIGNATURES: dict[str, tuple] = {
     "ap_loop_graph_launch": (ctypes.c_int, [_VP, _VP]),
     "ap_loop_graph_destroy": (ctypes.c_int, [_VP]),
     "ap_pcg64_host_draws": (ctypes.c_int, [_VP, _VP, _I32, _VP]),
+    "ap_mlp_fused_workspace": (ctypes.c_int64, [_I32, _VP, _I32, _I32]),
+    "ap_dqn_learn_fused": (ctypes.c_int, [ctypes.POINTER(FusedLearnDesc), _VP]),
+    "ap_mlp_forward_fused": (ctypes.c_int, [_I32, _VP, _VP, _VP, _VP, _VP, _I64, _I32, _VP, _VP, _VP, _VP]),
     "ap_generate_envs": (ctypes.c_int, [_I32, _VP, _I64, _I32, _I32, _VP, _VP]),
     "ap_np_samples_host": (ctypes.c_int, [_VP, _I32, _I64, _I64, _F64, _VP]),
     "ap_propagate_trace": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),

@@ -267,6 +267,53 @@ class QNetwork:
                                              self.num_actions, _stream()))
         return (q, acts) if cache else q
 
+    # -- fused small-batch path (csrc/fused_mlp.cu) -----------------------------------
+
+    def fused_layout(self):
+        """ctypes descriptors of the flat layout for the fused kernels (cached: tensors never move)."""
+        import ctypes
+
+        if getattr(self, "_flay", None) is None:
+            L = len(self.hidden)
+            names_w = [f"w{i}" for i in range(L)] + ["wh"]
+            names_b = [f"b{i}" for i in range(L)] + ["bh"]
+            base = self.flat.storage_offset()
+            pad = [0] * (5 - (L + 1))
+            dims = (ctypes.c_int32 * 6)(*([self.state_dim, *self.hidden, 1 + self.num_actions] + [0] * (4 - L)))
+            w_off = (ctypes.c_int64 * 5)(*([self.views[k].storage_offset() - base for k in names_w] + pad))
+            b_off = (ctypes.c_int64 * 5)(*([self.views[k].storage_offset() - base for k in names_b] + pad))
+            wt = (ctypes.c_void_p * 5)(*([self.wt[k].data_ptr() for k in names_w] + [None] * len(pad)))
+            wt_ld = (ctypes.c_int64 * 5)(*([self.wt[k].stride(0) for k in names_w] + pad))
+            self._flay = (L, dims, w_off, b_off, wt, wt_ld)
+        return self._flay
+
+    def _fused_scratch(self, rows: int, forward_only: bool):
+        """Per-network workspace + grid barrier of the fused kernels (grow-only; one stream at a time)."""
+        import torch
+
+        L, dims = self.fused_layout()[:2]
+        need = int(_native.require_device().ap_mlp_fused_workspace(L, dims, rows, int(forward_only)))
+        key = "_fws_f" if forward_only else "_fws_l"
+        ws = self.__dict__.get(key)
+        if ws is None or ws[0].numel() < need:
+            ws = (torch.empty(need, dtype=torch.float32, device="cuda"), torch.zeros(2, dtype=torch.int32, device="cuda"))
+            self.__dict__[key] = ws
+        return ws
+
+    def forward_fused(self, x, out=None):
+        """Q [rows, A] for device states x [rows, state_dim] (rows <= 256): one persistent
+        kernel (ap_mlp_forward_fused), fp32 CUDA-core tiles, grid barriers between layers."""
+        import torch
+
+        L, dims, w_off, b_off = self.fused_layout()[:4]
+        rows = x.shape[0]
+        q = out if out is not None else torch.empty((rows, self.num_actions), dtype=torch.float32, device="cuda")
+        ws, bar = self._fused_scratch(256, True)
+        _native.check(_native.require_device().ap_mlp_forward_fused(
+            L, dims, w_off, b_off, _native.ptr(self.flat), _native.ptr(x), x.stride(0), rows, _native.ptr(q),
+            _native.ptr(ws), _native.ptr(bar), _stream()))
+        return q
+
     def forward(self, states) -> np.ndarray:
         import torch
 
@@ -457,7 +504,7 @@ def act(net: QNetwork, state: np.ndarray, mask: np.ndarray, epsilon: float, rng:
         allowed = np.flatnonzero(mask)
         return int(allowed[rng.integers(len(allowed))])
     x = torch.as_tensor(np.asarray(state, dtype=np.float64), dtype=torch.float32).cuda().view(1, -1)
-    q = net.forward_device(x)
+    q = net.forward_fused(x) if getattr(net, "fused_act", False) else net.forward_device(x)
     m = torch.from_numpy(mask.astype(np.uint8)).cuda().view(1, -1)
     out = torch.empty(1, dtype=torch.int32, device="cuda")
     lib = _native.require_device()
@@ -658,6 +705,42 @@ def update_on_indices(net: QNetwork, target_net: QNetwork, buffer: PrioritizedRe
     return batch.loss
 
 
+class FusedLearnState:
+    """Device buffers of the fused learn step (td, loss, workspace, barrier) and its ctypes descriptor."""
+
+    def __init__(self, net: "QNetwork", target: "QNetwork", buffer: "PrioritizedReplayBuffer", config: AgentConfig,
+                 optimizer: "AdamOptimizer"):
+        import torch
+
+        B = config.batch_size
+        self.td = torch.zeros(B, dtype=torch.float32, device="cuda")
+        self.loss = torch.zeros(1, dtype=torch.float32, device="cuda")
+        self.ws, self.bar = net._fused_scratch(B, False)
+        L, dims, w_off, b_off, wt, wt_ld = net.fused_layout()
+        s = buffer.store
+        P = _native.ptr
+        self.desc = _native.FusedLearnDesc(
+            L=L, dims=dims, w_off=w_off, b_off=b_off, batch=B, params=P(net.flat), target=P(target.flat),
+            r_states=P(s["states"]), r_next=P(s["next_states"]), r_ld=s["states"].stride(0),
+            r_actions=P(s["actions"]), r_rewards=P(s["rewards"]), r_done=P(s["done"]), r_mask=P(s["next_mask"]),
+            r_prio=P(s["priorities"]), gamma=float(config.gamma), huber_delta=float(config.huber_delta),
+            grad=P(net.grad), m=P(optimizer.m), v=P(optimizer.v), nparams=net.flat.numel(), lr=optimizer.lr,
+            beta1=optimizer.beta1, beta2=optimizer.beta2, eps=optimizer.eps, wt=wt, wt_ld=wt_ld, td=P(self.td),
+            loss=P(self.loss), workspace=P(self.ws), barrier=P(self.bar))
+
+    def run(self, idx, weights, correct1=1.0, correct2=1.0, ctab=None, ctl=None, t_offset=0):
+        import ctypes
+
+        d = self.desc
+        d.idx, d.weights = idx.data_ptr(), weights.data_ptr()
+        d.correct1, d.correct2 = correct1, correct2
+        d.ctab = None if ctab is None else ctab.data_ptr()
+        d.ctl = None if ctl is None else ctl.data_ptr()
+        d.t_offset = int(t_offset)
+        _native.check(_native.require_device().ap_dqn_learn_fused(ctypes.byref(d), _stream()))
+        return self.loss
+
+
 def train_step(net, target_net, buffer, config, optimizer, rng) -> float:
     """Reference signature: draws the sampling uniforms from `rng`, returns the loss."""
     loss = train_step_device(net, target_net, buffer, config, optimizer, rng.random(config.batch_size))
@@ -676,6 +759,11 @@ class DqnAgent:
         self.optimizer = AdamOptimizer(self.net, config)
         self.train_steps = 0
         self._batch = None
+        # "fused": one persistent fp32 kernel per learn step and act forward (csrc/fused_mlp.cu),
+        # "gemm": the tcgen05 3xTF32 GEMM sequence (the throughput trainer's kernels)
+        self.learner = "fused"
+        self.net.fused_act = True
+        self._fused = None
 
     @property
     def epsilon(self) -> float:
@@ -690,10 +778,20 @@ class DqnAgent:
     def learn(self) -> float | None:
         if len(self.buffer) < self.config.batch_size:
             return None
-        if self._batch is None:
-            self._batch = _Batch(self.config.batch_size, self.net.state_dim, self.net.num_actions)
-        loss_t = train_step_device(self.net, self.target, self.buffer, self.config, self.optimizer,
-                                   self.rng.random(self.config.batch_size), self._batch)
+        if self.learner == "fused":
+            cfg = self.config
+            if self._fused is None:
+                self._fused = FusedLearnState(self.net, self.target, self.buffer, cfg, self.optimizer)
+            idx, w = self.buffer.sample_device(cfg.batch_size, cfg.per_alpha, cfg.per_beta,
+                                               self.rng.random(cfg.batch_size))
+            opt = self.optimizer
+            opt.t += 1
+            loss_t = self._fused.run(idx, w, 1.0 - opt.beta1 ** opt.t, 1.0 - opt.beta2 ** opt.t)
+        else:
+            if self._batch is None:
+                self._batch = _Batch(self.config.batch_size, self.net.state_dim, self.net.num_actions)
+            loss_t = train_step_device(self.net, self.target, self.buffer, self.config, self.optimizer,
+                                       self.rng.random(self.config.batch_size), self._batch)
         loss = float(loss_t.item()) / self.config.batch_size
         if not np.isfinite(loss):
             raise DivergenceError(f"training loss diverged to {loss}")

@@ -121,7 +121,8 @@ class DeviceSearch:
     def _step_body(self):
         lib = _native.require_device()
         t, L = self.t, ctypes.byref(self.desc)
-        q = self.agent.net.forward_device(t["state"])
+        net = self.agent.net
+        q = net.forward_fused(t["state"]) if getattr(net, "fused_act", False) else net.forward_device(t["state"])
         _native.check(lib.ap_parity_act(L, _native.ptr(q), _native.ptr(t["action"]), _stream()))
         self.env._engine.launch(t["seeds_try"][:, : self.n], t["outcome"], None, None, t["status"])
         _native.check(lib.ap_parity_post(L, _native.ptr(t["action"]), _stream()))
@@ -139,6 +140,11 @@ class DeviceSearch:
                                               _native.ptr(t["uniforms"]), B, _native.ptr(st["scratch"]),
                                               _native.ptr(t["idx"]), _native.ptr(t["weights"]), _stream()))
         opt, net = agent.optimizer, agent.net
+        if agent.learner == "fused":
+            loss = agent._fused.run(t["idx"], t["weights"], ctab=t["ctab"], ctl=t["ctl"], t_offset=self.adam_offset)
+            _native.check(lib.ap_parity_learn_tail(L, _native.ptr(loss), int(cfg.target_sync_every), _stream()))
+            self._sync(lib)
+            return
 
         def adam_step():
             _native.check(lib.ap_dqn_adam_tab(_native.ptr(net.flat), _native.ptr(net.grad), _native.ptr(opt.m),
@@ -149,6 +155,10 @@ class DeviceSearch:
 
         loss = update_on_indices(net, agent.target, agent.buffer, cfg, t["idx"], t["weights"], agent._batch, adam_step)
         _native.check(lib.ap_parity_learn_tail(L, _native.ptr(loss), int(cfg.target_sync_every), _stream()))
+        self._sync(lib)
+
+    def _sync(self, lib):
+        t = self.t
         segs = self._sync_segments()
         _native.check(lib.ap_parity_target_sync(_native.ptr(t["ctl"]), len(segs),
                                                 (ctypes.c_void_p * len(segs))(*[s for s, _, _ in segs]),
@@ -170,9 +180,12 @@ class DeviceSearch:
         exist before the capture; touches only outputs and gradients, no search state."""
         import torch
 
-        from .agent import _Batch
+        from .agent import FusedLearnState, _Batch
 
         agent, cfg = self.agent, self.agent.config
+        if agent.learner == "fused" and agent._fused is None:
+            agent._fused = FusedLearnState(agent.net, agent.target, agent.buffer, cfg, agent.optimizer)
+        agent.net._fused_scratch(256, True)
         if agent._batch is None:
             agent._batch = _Batch(cfg.batch_size, agent.net.state_dim, agent.net.num_actions)
         b = agent._batch

@@ -26,7 +26,7 @@ def declared_functions() -> set[str]:
     for h in HEADERS:
         text = h.read_text()
         text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-        names |= set(re.findall(r"^\s*(?:int|const char\*|void)\s+(ap_\w+)\s*\(", text, flags=re.M))
+        names |= set(re.findall(r"^\s*(?:int|int64_t|const char\*|void)\s+(ap_\w+)\s*\(", text, flags=re.M))
     return names
 
 
