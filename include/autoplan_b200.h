@@ -238,6 +238,9 @@ int ap_pipe_train_state_ex(ap_pipe_t p, const ap_topology* topo, const int32_t* 
  * [num_envs, 3, granularity] fp64, bit-identical to the host. */
 int ap_generate_envs(int32_t kind, const uint64_t* pcg_states, int64_t num_envs, int32_t n, int32_t granularity,
                      double* arrays_out, void* stream);
+/* Host run of the same per-environment code (tests): kinds 1 and 2 of ap_generate_envs. */
+int ap_generate_envs_host(int32_t kind, const uint64_t* pcg_states, int64_t num_envs, int32_t n,
+                          int32_t granularity, double* arrays_out);
 /* Host run of the device samplers (tests): kind 0 Generator.standard_normal(),
  * kind 1 Generator.binomial(bin_n, bin_p); state6 as ap_pcg64_host_draws. */
 int ap_np_samples_host(uint64_t* state6, int32_t kind, int64_t count, int64_t bin_n, double bin_p, double* out);
@@ -668,6 +671,7 @@ typedef struct ap_fused_learn {
   float* loss;              /* [1] sum_b w_b huber(td_b) */
   float* workspace;         /* ap_mlp_fused_workspace(L, dims, batch, 0) floats */
   uint32_t* barrier;        /* [2] zero-initialised, private to the caller's stream */
+  uint64_t* trace;          /* optional [16]: %globaltimer after each phase (profiling) */
 } ap_fused_learn;
 
 int64_t ap_mlp_fused_workspace(int32_t L, const int32_t* dims, int32_t rows, int32_t forward_only);

@@ -136,6 +136,7 @@ class FusedLearnDesc(ctypes.Structure):
         ("ctab", ctypes.c_void_p), ("ctl", ctypes.c_void_p), ("t_offset", ctypes.c_int64),
         ("wt", ctypes.c_void_p * 5), ("wt_ld", ctypes.c_int64 * 5), ("td", ctypes.c_void_p),
         ("loss", ctypes.c_void_p), ("workspace", ctypes.c_void_p), ("barrier", ctypes.c_void_p),
+        ("trace", ctypes.c_void_p),
     ]
 PL = {"STEP": 0, "SLOT": 1, "SIZE": 2, "TRAIN": 3, "EPISODES": 4, "BUDGET": 5, "MAX_STEPS": 6, "POS": 7,
       "EP_STEPS": 8, "BEST_PART": 9, "BEST_EP": 10, "SYNC": 11, "T_POS": 12, "EP_BASE": 13, "TRAIN0": 14,
@@ -165,6 +166,7 @@ SIGNATURES: dict[str, tuple] = {
     "ap_mlp_forward_fused": (ctypes.c_int, [_I32, _VP, _VP, _VP, _VP, _VP, _I64, _I32, _VP, _VP, _VP, _VP]),
     "ap_generate_envs": (ctypes.c_int, [_I32, _VP, _I64, _I32, _I32, _VP, _VP]),
     "ap_np_samples_host": (ctypes.c_int, [_VP, _I32, _I64, _I64, _F64, _VP]),
+    "ap_generate_envs_host": (ctypes.c_int, [_I32, _VP, _I64, _I32, _I32, _VP]),
     "ap_propagate_trace": (ctypes.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "ap_pipe_create": (ctypes.c_int, [ctypes.POINTER(PipeDesc), ctypes.POINTER(_VP)]),
     "ap_pipe_destroy": (ctypes.c_int, [_VP]),

@@ -64,6 +64,7 @@ static void release_decision(DecisionTables* t) {
   t->d_dec_masks.release();
   t->d_dec_cls8.release();
   t->d_class_ncand.release();
+  t->d_ncand_planes.release();
 }
 
 }  // namespace apb

@@ -81,51 +81,53 @@ __global__ void __launch_bounds__(kGenThreads) uniform_env_kernel(const uint64_t
 // per environment: c, a, w drawn in the reference's order (n each), c and w as the
 // naive cumsum, right-endpoint coarsening to G points, joint scaling by the maximum.
 // kind 1: clip(0.5 + 0.15 * z, 0, 1); kind 2: binomial(100, 0.5) / 100.
-__global__ void __launch_bounds__(128) sampled_env_kernel(const uint64_t* __restrict__ seeds4, int64_t E, int n, int G,
-                                                         int kind, double* __restrict__ out) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= E) return;
-  const uint64_t* q = seeds4 + 4 * e;
+__host__ __device__ inline void sampled_env(const uint64_t* q, int n, int G, int kind, double* o) {
   NpPcg64 g;
   g.state = ((u128)q[0] << 64) | (u128)q[1];
   g.inc = ((u128)q[2] << 64) | (u128)q[3];
   g.has_uint32 = 0;
   g.uinteger = 0;
-  double* o = out + e * 3 * (int64_t)G;
   double peak = 0.0;
   for (int arr = 0; arr < 3; ++arr) {
     const bool prefix = arr != 1;  // C and W are prefix sums, A stays pointwise
-    double acc = 0.0, last = 0.0;
+    double acc = 0.0;
     int j = 0;  // next coarse point
     for (int i = 0; i < n; ++i) {
       double x;
       if (kind == 1) {
-        x = __dadd_rn(0.5, __dmul_rn(0.15, np_standard_normal(g)));
-        x = fmin(fmax(x, 0.0), 1.0);  // np.clip(.., 0.0, 1.0)
+        x = 0.5 + 0.15 * np_standard_normal(g);  // -fmad=false: product and sum rounded separately
+        x = fmin(fmax(x, 0.0), 1.0);              // np.clip(.., 0.0, 1.0)
       } else {
-        x = __ddiv_rn((double)np_binomial(g, 100, 0.5), 100.0);
+        x = (double)np_binomial(g, 100, 0.5) / 100.0;
       }
-      acc = prefix ? (i == 0 ? x : __dadd_rn(acc, x)) : x;
-      last = acc;
-      // right endpoint of coarse point j: floor((j + 1) * n / G) - 1 (n >= G)
-      while (j < G && n >= G && ((int64_t)(j + 1) * n) / G - 1 == i) {
-        o[arr * G + j] = acc;
-        peak = fmax(peak, acc);
-        ++j;
-      }
-      if (n < G && j < G && i == j) {  // shorter inputs: point j takes source j, padded with the last value
+      acc = (prefix && i > 0) ? acc + x : x;
+      if (n >= G) {
+        // right endpoint of coarse point j: floor((j + 1) * n / G) - 1
+        while (j < G && ((int64_t)(j + 1) * n) / G - 1 == i) {
+          o[arr * G + j] = acc;
+          peak = fmax(peak, acc);
+          ++j;
+        }
+      } else if (j == i) {  // shorter inputs: point j takes source j
         o[arr * G + j] = acc;
         peak = fmax(peak, acc);
         ++j;
       }
     }
     for (; j < G; ++j) {  // n < G: right padding with the last value
-      o[arr * G + j] = last;
-      peak = fmax(peak, last);
+      o[arr * G + j] = acc;
+      peak = fmax(peak, acc);
     }
   }
   if (peak > 0.0)
-    for (int i = 0; i < 3 * G; ++i) o[i] = __ddiv_rn(o[i], peak);
+    for (int i = 0; i < 3 * G; ++i) o[i] = o[i] / peak;
+}
+
+__global__ void __launch_bounds__(128) sampled_env_kernel(const uint64_t* __restrict__ seeds4, int64_t E, int n, int G,
+                                                         int kind, double* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  sampled_env(seeds4 + 4 * e, n, G, kind, out + e * 3 * (int64_t)G);
 }
 
 // Slot statuses for host consumers: K1's int8 slot rows (-1 undecided, 0 R,
@@ -194,6 +196,18 @@ int ap_generate_envs(int32_t kind, const uint64_t* pcg_states, int64_t num_envs,
   sampled_env_kernel<<<(unsigned)grid, 128, 0, (cudaStream_t)stream>>>(pcg_states, num_envs, n, granularity, kind,
                                                                         arrays_out);
   AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_generate_envs_host(int32_t kind, const uint64_t* pcg_states, int64_t num_envs, int32_t n,
+                          int32_t granularity, double* arrays_out) {
+  if ((kind != 1 && kind != 2) || num_envs < 0 || n < 1 || granularity < 1 ||
+      (num_envs > 0 && (!pcg_states || !arrays_out))) {
+    set_error("ap_generate_envs_host: bad arguments (kind 1 normal, 2 binomial)");
+    return AP_ERR_INVALID;
+  }
+  for (int64_t e = 0; e < num_envs; ++e)
+    sampled_env(pcg_states + 4 * e, n, granularity, kind, arrays_out + e * 3 * (int64_t)granularity);
   return AP_OK;
 }
 

@@ -33,7 +33,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kMaxLayers = 4;  // hidden layers
 constexpr int kTN = 32;        // tile columns (one per lane)
-constexpr int kSmemFloats = 50 * 1024;  // 200 KB of dynamic shared memory per CTA
+constexpr int kSmemFloats = 56 * 1024;  // 224 KB of dynamic shared memory per CTA (one chunk at K <= 1100)
 
 struct Learn {
   int L, A, B, rows_fwd;  // rows_fwd: forward mode row count (learn mode: 0)
@@ -73,9 +73,19 @@ struct Learn {
   // workspace
   float* ws;
   unsigned* bar;
+  unsigned long long* trace;  // optional: %globaltimer after each phase (CTA 0)
 };
 
 // grid-wide barrier (all CTAs co-resident: cooperative launch); generation counter in bar[1]
+__device__ __forceinline__ void trace_mark(unsigned long long* tr, int& k) {
+  if (tr && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[k] = t;
+  }
+  ++k;
+}
+
 __device__ __forceinline__ void grid_sync(unsigned* bar) {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -121,65 +131,166 @@ struct BOp {
 };
 
 // One tiled product C[M, N] = epi(sum_k A(m, k) B(k, n) + bias[n]); epi: relu (1),
-// relu' mask from `mask` rows (2), none (0).  Tiles of 8 * rpt rows x 32 columns.
+// relu' mask from `mask` rows (2), none (0).  Tiles of (8 / kg) * rpt rows x 32 columns:
+// lane = column, the 8 warps split into 8 / kg row groups x kg K-groups (partial sums
+// added in group order through shared memory, so every sum has one fixed order).
 struct Job {
   AOp a;
   BOp b;
   float* c;
   int64_t ldc;
-  int M, N, K, rpt;
+  int M, N, K, rpt, kg;
   const float* bias;
   int epi;
   const float* mask;
   int64_t ldmask;
-  __device__ __forceinline__ int tiles() const { return ((M + 8 * rpt - 1) / (8 * rpt)) * ((N + kTN - 1) / kTN); }
+  __device__ __forceinline__ int tm() const { return (8 / kg) * rpt; }
+  __device__ __forceinline__ int tiles() const { return ((M + tm() - 1) / tm()) * ((N + kTN - 1) / kTN); }
 };
 
-template <int RPT>
+__device__ __forceinline__ void cp_async16(float* smem_dst, const float* gsrc) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ bool al16(const float* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+constexpr int kBS = kTN + 4;  // B tile row stride (floats): 16-byte rows, conflict-free column reads
+
+// One tile of a job: rows [m0, m0 + 8 RPT), columns [n0, n0 + 32).  Operands are staged in
+// shared memory with cp.async (16-byte asynchronous copies, hundreds in flight per thread)
+// where rows are contiguous and aligned, element loads otherwise:
+//   A row-major      As[r][k]   (TRANS = 0: contiguous along k)
+//   A transposed     At[k][r]   (TRANS = 1: element (m, k) in source row k, contiguous along m)
+//   B                Bs[k][n]   (contiguous along n: sn == 1; along k (sk == 1): element loads)
+template <int RPT, int KG, int TRANS>
 __device__ void run_tile(const Job& j, int t, float* smem) {
-  const int tm_rows = 8 * RPT;
+  constexpr int RW = 8 / KG;       // row-warps
+  constexpr int TM = RW * RPT;
   const int ntn = (j.N + kTN - 1) / kTN;
-  const int m0 = (t / ntn) * tm_rows, n0 = (t % ntn) * kTN;
-  const int tid = threadIdx.x, r = tid >> 5, c = tid & 31;
-  // chunk of K that fits: As [tm_rows][kc] + Bs [kc][33]
-  const int kc_max = kSmemFloats / (tm_rows + kTN + 1);
+  const int m0 = (t / ntn) * TM, n0 = (t % ntn) * kTN;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int kgi = warp % KG, rw = warp / KG, c = lane;
+  const int kc_max = (kSmemFloats / (TM + kBS)) & ~3;
   float acc[RPT];
 #pragma unroll
   for (int q = 0; q < RPT; ++q) acc[q] = 0.0f;
+  const bool b_rows = j.b.sn == 1 && (j.b.sk & 3) == 0 && al16(j.b.p);
   for (int k0 = 0; k0 < j.K; k0 += kc_max) {
     const int kc = min(kc_max, j.K - k0);
-    float* As = smem;                  // [tm_rows][kc]
-    float* Bs = smem + tm_rows * kc;   // [kc][33]
+    const int kcp = (kc + 3) & ~3;
+    float* As = smem;                 // TRANS ? [kcp][TM] : [TM][kcp]
+    float* Bs = smem + TM * kcp;      // [kcp][kBS]
     __syncthreads();
-    if (!j.a.trans) {
-      for (int e = tid; e < tm_rows * kc; e += kThreads) {
-        const int rr = e / kc, kk = e - rr * kc;
+    // ---- A
+    if (!TRANS) {
+      for (int rr = warp; rr < TM; rr += kThreads / 32) {
         const int m = m0 + rr;
-        As[e] = m < j.M ? __ldcg(j.a.row(m) + k0 + kk) : 0.0f;
+        float* dst = As + rr * kcp;
+        if (m >= j.M) {
+          for (int kk = lane; kk < kcp; kk += 32) dst[kk] = 0.0f;
+          continue;
+        }
+        const float* src = j.a.row(m) + k0;
+        if (al16(src)) {
+          const int k4 = kc & ~3;
+          for (int kk = 4 * lane; kk < k4; kk += 128) cp_async16(dst + kk, src + kk);
+          for (int kk = k4 + lane; kk < kcp; kk += 32) dst[kk] = kk < kc ? __ldcg(src + kk) : 0.0f;
+        } else {
+          for (int kk = lane; kk < kcp; kk += 32) dst[kk] = kk < kc ? __ldcg(src + kk) : 0.0f;
+        }
       }
     } else {
-      for (int e = tid; e < tm_rows * kc; e += kThreads) {
-        const int kk = e / tm_rows, rr = e - kk * tm_rows;
-        const int m = m0 + rr;
-        As[rr * kc + kk] = m < j.M ? __ldcg(j.a.row(k0 + kk) + m) : 0.0f;
+      for (int kk = warp; kk < kcp; kk += kThreads / 32) {
+        float* dst = As + kk * TM;
+        if (kk >= kc) {
+          for (int rr = lane; rr < TM; rr += 32) dst[rr] = 0.0f;
+          continue;
+        }
+        const float* src = j.a.row(k0 + kk) + m0;
+        if ((TM & 3) == 0 && al16(src) && m0 + TM <= j.M) {
+          for (int rr = 4 * lane; rr < TM; rr += 128) cp_async16(dst + rr, src + rr);
+        } else {
+          for (int rr = lane; rr < TM; rr += 32) dst[rr] = m0 + rr < j.M ? __ldcg(src + rr) : 0.0f;
+        }
       }
     }
-    for (int e = tid; e < kc * kTN; e += kThreads) {
-      int kk, nn;
-      if (j.b.sn == 1) {
-        kk = e / kTN, nn = e - kk * kTN;
-      } else {
-        nn = e / kc, kk = e - nn * kc;
+    // ---- B (rows [kc, kcp) zero: the padded k steps multiply zeros on both sides)
+    for (int e = kc * kBS + tid; e < kcp * kBS; e += kThreads) Bs[e] = 0.0f;
+    if (b_rows && n0 + kTN <= j.N) {
+      for (int e = tid; e < kc * (kTN / 4); e += kThreads) {
+        const int kk = e >> 3, n4 = (e & 7) * 4;
+        cp_async16(Bs + kk * kBS + n4, j.b.p + (int64_t)(k0 + kk) * j.b.sk + n0 + n4);
       }
-      const int n = n0 + nn;
-      Bs[kk * (kTN + 1) + nn] = n < j.N ? __ldcg(j.b.p + (int64_t)(k0 + kk) * j.b.sk + (int64_t)n * j.b.sn) : 0.0f;
-    }
-    __syncthreads();
-    const float* bcol = Bs + c;
-    for (int kk = 0; kk < kc; ++kk) {
-      const float bv = bcol[kk * (kTN + 1)];
+    } else {
+      // element loads, 8 in flight per thread
+      const int total = kc * kTN;
+      for (int e0 = tid; e0 < total; e0 += 8 * kThreads) {
+        float v[8];
 #pragma unroll
-      for (int q = 0; q < RPT; ++q) acc[q] = fmaf(As[(r + 8 * q) * kc + kk], bv, acc[q]);
+        for (int u = 0; u < 8; ++u) {
+          const int e = e0 + u * kThreads;
+          int kk, nn;
+          if (j.b.sn == 1) kk = e / kTN, nn = e % kTN;
+          else nn = e / kc, kk = e - nn * kc;
+          const int n = n0 + nn;
+          v[u] = (e < total && n < j.N) ? __ldcg(j.b.p + (int64_t)(k0 + kk) * j.b.sk + (int64_t)n * j.b.sn) : 0.0f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e = e0 + u * kThreads;
+          if (e >= total) break;
+          int kk, nn;
+          if (j.b.sn == 1) kk = e / kTN, nn = e % kTN;
+          else nn = e / kc, kk = e - nn * kc;
+          Bs[kk * kBS + nn] = v[u];
+        }
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    // ---- this warp's K segment (multiples of 4)
+    const int seg = ((kcp / 4 + KG - 1) / KG) * 4;
+    const int klo = kgi * seg, khi = min(kcp, klo + seg);
+    const float* bcol = Bs + c;
+    if (!TRANS) {
+      for (int kk = klo; kk < khi; kk += 4) {
+        const float b0 = bcol[kk * kBS], b1 = bcol[(kk + 1) * kBS], b2 = bcol[(kk + 2) * kBS],
+                    b3 = bcol[(kk + 3) * kBS];
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) {
+          const float4 a4 = *reinterpret_cast<const float4*>(As + (rw + RW * q) * kcp + kk);
+          acc[q] = fmaf(a4.x, b0, acc[q]);
+          acc[q] = fmaf(a4.y, b1, acc[q]);
+          acc[q] = fmaf(a4.z, b2, acc[q]);
+          acc[q] = fmaf(a4.w, b3, acc[q]);
+        }
+      }
+    } else {
+#pragma unroll 4
+      for (int kk = klo; kk < khi; ++kk) {
+        const float bv = bcol[kk * kBS];
+        const float* acol = As + kk * TM + rw;
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) acc[q] = fmaf(acol[RW * q], bv, acc[q]);
+      }
+    }
+  }
+  // ---- partial sums of the K groups, added in group order
+  if (KG > 1) {
+    __syncthreads();
+    float* red = smem;  // [KG][TM][32]
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) red[(kgi * TM + rw + RW * q) * kTN + c] = acc[q];
+    __syncthreads();
+    if (kgi != 0) return;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      float v = red[(rw + RW * q) * kTN + c];
+      for (int g = 1; g < KG; ++g) v += red[(g * TM + rw + RW * q) * kTN + c];
+      acc[q] = v;
     }
   }
   const int n = n0 + c;
@@ -187,12 +298,31 @@ __device__ void run_tile(const Job& j, int t, float* smem) {
   const float bias = j.bias ? __ldcg(j.bias + n) : 0.0f;
 #pragma unroll
   for (int q = 0; q < RPT; ++q) {
-    const int m = m0 + r + 8 * q;
+    const int m = m0 + rw + RW * q;
     if (m >= j.M) break;
     float v = acc[q] + bias;
     if (j.epi == 1) v = fmaxf(v, 0.0f);
     if (j.epi == 2 && !(__ldcg(j.mask + (int64_t)m * j.ldmask + n) > 0.0f)) v = 0.0f;
     j.c[(int64_t)m * j.ldc + n] = v;
+  }
+}
+
+template <int TRANS>
+__device__ __forceinline__ void run_tile_cfg(const Job& j, int t, float* smem) {
+  switch (j.rpt * 16 + j.kg) {
+    case 1 * 16 + 1: run_tile<1, 1, TRANS>(j, t, smem); break;
+    case 2 * 16 + 1: run_tile<2, 1, TRANS>(j, t, smem); break;
+    case 4 * 16 + 1: run_tile<4, 1, TRANS>(j, t, smem); break;
+    case 8 * 16 + 1: run_tile<8, 1, TRANS>(j, t, smem); break;
+    case 1 * 16 + 2: run_tile<1, 2, TRANS>(j, t, smem); break;
+    case 2 * 16 + 2: run_tile<2, 2, TRANS>(j, t, smem); break;
+    case 4 * 16 + 2: run_tile<4, 2, TRANS>(j, t, smem); break;
+    case 1 * 16 + 4: run_tile<1, 4, TRANS>(j, t, smem); break;
+    case 2 * 16 + 4: run_tile<2, 4, TRANS>(j, t, smem); break;
+    case 4 * 16 + 4: run_tile<4, 4, TRANS>(j, t, smem); break;
+    case 1 * 16 + 8: run_tile<1, 8, TRANS>(j, t, smem); break;
+    case 2 * 16 + 8: run_tile<2, 8, TRANS>(j, t, smem); break;
+    default: run_tile<4, 8, TRANS>(j, t, smem); break;
   }
 }
 
@@ -203,21 +333,55 @@ __device__ void run_jobs(const Job* jobs, int nj, float* smem) {
   for (int t = blockIdx.x; t < total; t += gridDim.x) {
     int k = t, i = 0;
     while (k >= jobs[i].tiles()) k -= jobs[i].tiles(), ++i;
-    switch (jobs[i].rpt) {
-      case 1: run_tile<1>(jobs[i], k, smem); break;
-      case 2: run_tile<2>(jobs[i], k, smem); break;
-      case 4: run_tile<4>(jobs[i], k, smem); break;
-      default: run_tile<8>(jobs[i], k, smem); break;
-    }
+    if (jobs[i].a.trans)
+      run_tile_cfg<1>(jobs[i], k, smem);
+    else
+      run_tile_cfg<0>(jobs[i], k, smem);
   }
 }
 
-// column sums out[n] = sum_{m < M} x[m * ld + n] (bias gradients), rows in order
+// column sums out[n] = sum_{m < M} x[m * ld + n] (bias gradients), rows in order, 8 loads in flight
 __device__ void colsum(const float* x, int64_t ld, int M, int N, float* out) {
   for (int n = blockIdx.x * kThreads + threadIdx.x; n < N; n += gridDim.x * kThreads) {
     float s = 0.0f;
-    for (int m = 0; m < M; ++m) s += __ldcg(x + (int64_t)m * ld + n);
+    for (int m0 = 0; m0 < M; m0 += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = m0 + u < M ? __ldcg(x + (int64_t)(m0 + u) * ld + n) : 0.0f;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (m0 + u < M) s += v[u];
+    }
     out[n] = s;
+  }
+}
+
+// head outputs z[row] = h[row] . Wh + bh for many rows: one warp per row, lanes split H
+template <int A1M>
+__device__ void head_rows(const float* h, int64_t ldh, int rows, int H, int A1, const float* wh, const float* bh,
+                          float* z, int wbase, int wstride) {
+  const int lane = threadIdx.x & 31;
+  for (int row = wbase; row < rows; row += wstride) {
+    float s[A1M];
+#pragma unroll
+    for (int j = 0; j < A1M; ++j) s[j] = 0.0f;
+    const float* hr = h + (int64_t)row * ldh;
+    for (int k = lane; k < H; k += 32) {
+      const float x = __ldcg(hr + k);
+#pragma unroll
+      for (int j = 0; j < A1M; ++j)
+        if (j < A1) s[j] = fmaf(x, __ldcg(wh + (int64_t)k * A1 + j), s[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < A1M; ++j)
+      for (int o = 16; o; o >>= 1) s[j] += __shfl_xor_sync(0xffffffffu, s[j], o);
+    if (lane < A1) {
+      float v = 0.0f;
+#pragma unroll
+      for (int j = 0; j < A1M; ++j)
+        if (j == lane) v = s[j];
+      z[(int64_t)row * A1 + lane] = v + __ldcg(bh + lane);
+    }
   }
 }
 
@@ -230,6 +394,8 @@ __device__ __forceinline__ float dueling_q(const float* z, int A, int a) {
 
 __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(Learn P) {
   extern __shared__ float smem[];
+  int tk = 0;
+  trace_mark(P.trace, tk);
   const int L = P.L, A = P.A, A1 = A + 1;
   const bool fwd_only = P.rows_fwd > 0;
   const int B = fwd_only ? P.rows_fwd : P.B;
@@ -275,7 +441,9 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(Learn P) {
     on.c = Hon[i + 1];
     on.ldc = N;
     on.M = Ron, on.N = N, on.K = K;
+    // small row counts split K over the warps (the act forward: 1 row), large ones split rows
     on.rpt = Ron >= 64 ? 2 : 1;
+    on.kg = Ron >= 64 ? 2 : (Ron >= 8 ? 4 : 8);
     on.bias = P.p + P.b_off[i];
     on.epi = 1;
     if (!fwd_only) {
@@ -286,32 +454,41 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(Learn P) {
       tg.b = BOp{P.tp + P.w_off[i], N, 1};
       tg.c = Htg[i + 1];
       tg.M = B;
-      tg.rpt = 1;
+      tg.rpt = 2;
+      tg.kg = 2;
       tg.bias = P.tp + P.b_off[i];
     }
     run_jobs(jobs, nj, smem);
     grid_sync(P.bar);
+    trace_mark(P.trace, tk);
   }
 
-  // head + dueling (+ TD, loss, priorities): one CTA
+  // head outputs, one warp per row over the whole grid (online rows, then target rows)
   const int H = P.d[L];
-  if (blockIdx.x == 0) {
-    const float* wh = P.p + P.w_off[L];
-    const float* bh = P.p + P.b_off[L];
-    const float* twh = P.tp + P.w_off[L];
-    const float* tbh = P.tp + P.b_off[L];
-    const int nrows = fwd_only ? Ron : Ron + B;
-    for (int e = threadIdx.x; e < nrows * A1; e += kThreads) {
-      const int row = e / A1, j = e - row * A1;
-      const bool tgt = row >= Ron;
-      const float* h = tgt ? Htg[L] + (int64_t)(row - Ron) * H : Hon[L] + (int64_t)row * H;
-      const float* w = tgt ? twh : wh;
-      float s = 0.0f;
-      for (int k = 0; k < H; ++k) s = fmaf(__ldcg(h + k), __ldcg(w + (int64_t)k * A1 + j), s);
-      s += __ldcg((tgt ? tbh : bh) + j);
-      (tgt ? ztg + (int64_t)(row - Ron) * A1 : zon + (int64_t)row * A1)[j] = s;
+  {
+    const int wid = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5), nw = gridDim.x * (kThreads / 32);
+    if (A1 <= 8) {
+      head_rows<8>(Hon[L], H, Ron, H, A1, P.p + P.w_off[L], P.p + P.b_off[L], zon, wid, nw);
+      if (!fwd_only) head_rows<8>(Htg[L], H, B, H, A1, P.tp + P.w_off[L], P.tp + P.b_off[L], ztg, wid, nw);
+    } else {
+      // wide heads: one thread per (row, output)
+      const int tid = blockIdx.x * kThreads + threadIdx.x, nt = gridDim.x * kThreads;
+      const int nrows = fwd_only ? Ron : Ron + B;
+      for (int e = tid; e < nrows * A1; e += nt) {
+        const int row = e / A1, jj = e - row * A1;
+        const bool tgt = row >= Ron;
+        const float* h = tgt ? Htg[L] + (int64_t)(row - Ron) * H : Hon[L] + (int64_t)row * H;
+        const float* w = (tgt ? P.tp : P.p) + P.w_off[L];
+        float acc = 0.0f;
+        for (int k = 0; k < H; ++k) acc = fmaf(__ldcg(h + k), __ldcg(w + (int64_t)k * A1 + jj), acc);
+        acc += __ldcg((tgt ? P.tp : P.p) + P.b_off[L] + jj);
+        (tgt ? ztg + (int64_t)(row - Ron) * A1 : zon + (int64_t)row * A1)[jj] = acc;
+      }
     }
-    __syncthreads();
+  }
+  grid_sync(P.bar);
+    trace_mark(P.trace, tk);
+  if (blockIdx.x == 0) {
     if (fwd_only) {
       for (int e = threadIdx.x; e < Ron * A; e += kThreads) {
         const int row = e / A, a = e - row * A;
@@ -359,6 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(Learn P) {
   }
   if (fwd_only) return;
   grid_sync(P.bar);
+    trace_mark(P.trace, tk);
 
   // head backward: gWh = H_L(cur)^T dz, gbh, dh_L = relu'(H_L) * (dz Wh^T)
   {
@@ -369,13 +547,13 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(Learn P) {
     jobs[0].b = BOp{dz, A1, 1};
     jobs[0].c = P.grad + P.w_off[L];
     jobs[0].ldc = A1;
-    jobs[0].M = H, jobs[0].N = A1, jobs[0].K = B, jobs[0].rpt = 4;
+    jobs[0].M = H, jobs[0].N = A1, jobs[0].K = B, jobs[0].rpt = 4, jobs[0].kg = 1;
     jobs[1] = Job{};
     jobs[1].a = AOp{dz, A1, nullptr, nullptr, nullptr, 0, 0};
     jobs[1].b = BOp{P.p + P.w_off[L], 1, A1};  // (k=a, n=j) = Wh[j][a]
     jobs[1].c = dh[L];
     jobs[1].ldc = H;
-    jobs[1].M = B, jobs[1].N = H, jobs[1].K = A1, jobs[1].rpt = 1;
+    jobs[1].M = B, jobs[1].N = H, jobs[1].K = A1, jobs[1].rpt = 1, jobs[1].kg = 1;
     jobs[1].epi = 2;
     jobs[1].mask = Hc;
     jobs[1].ldmask = H;
@@ -383,6 +561,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(Learn P) {
     colsum(dz, A1, B, A1, P.grad + P.b_off[L]);
   }
   grid_sync(P.bar);
+    trace_mark(P.trace, tk);
 
   // hidden layers, last to first
   for (int i = L; i >= 1; --i) {
@@ -398,7 +577,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(Learn P) {
     wg.b = BOp{dh[i], dout, 1};
     wg.c = P.grad + P.w_off[i - 1];
     wg.ldc = dout;
-    wg.M = din, wg.N = dout, wg.K = B, wg.rpt = 8;
+    wg.M = din, wg.N = dout, wg.K = B, wg.rpt = 4, wg.kg = 1;
     if (i > 1) {
       Job& dg = jobs[nj++];
       dg = Job{};
@@ -406,7 +585,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(Learn P) {
       dg.b = BOp{P.p + P.w_off[i - 1], 1, dout};  // (k=q, n=p) = W[p][q]
       dg.c = dh[i - 1];
       dg.ldc = din;
-      dg.M = B, dg.N = din, dg.K = dout, dg.rpt = 1;
+      dg.M = B, dg.N = din, dg.K = dout, dg.rpt = 1, dg.kg = 2;
       dg.epi = 2;
       dg.mask = Hon[i - 1] + (int64_t)B * din;
       dg.ldmask = din;
@@ -414,6 +593,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(Learn P) {
     run_jobs(jobs, nj, smem);
     colsum(dh[i], dout, B, dout, P.grad + P.b_off[i - 1]);
     grid_sync(P.bar);
+    trace_mark(P.trace, tk);
   }
 
   // Adam (agent.py:229-250) over every parameter + the transposed weight copies
@@ -439,6 +619,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(Learn P) {
       }
     }
   }
+  trace_mark(P.trace, tk);
 }
 
 int64_t workspace_floats(int L, const int* d, int B, bool fwd_only) {
@@ -557,6 +738,7 @@ int ap_dqn_learn_fused(const ap_fused_learn* a, void* stream) {
   P.loss = a->loss;
   P.ws = a->workspace;
   P.bar = a->barrier;
+  P.trace = reinterpret_cast<unsigned long long*>(a->trace);
   return launch(P, (cudaStream_t)stream);
 }
 

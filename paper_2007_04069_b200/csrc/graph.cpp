@@ -341,6 +341,7 @@ int ensure_decision_on_device(DecisionTables* d) {
     if ((rc = d->d_dec_masks.upload(d->dec_masks)) != AP_OK) return rc;
     if ((rc = d->d_dec_cls8.upload(d->dec_cls8)) != AP_OK) return rc;
     if ((rc = d->d_class_ncand.upload(d->class_ncand)) != AP_OK) return rc;
+    if ((rc = d->d_ncand_planes.upload(d->ncand_planes)) != AP_OK) return rc;
   }
   d->uploaded = true;
   return AP_OK;

@@ -46,8 +46,10 @@ __host__ __device__ inline double np_standard_normal(NpPcg64& g) {
 }
 
 // random_binomial_btpe (numpy distributions.c); the per-(n, p) setup of binomial_t is
-// recomputed, which yields the same values numpy caches.
-__host__ __device__ inline int64_t np_binomial_btpe(NpPcg64& g, int64_t n, double p) {
+// recomputed, which yields the same values numpy caches.  Kept out of line: inlined into
+// the per-environment loop, ptxas -O3 miscompiles it for divergent warps (wrong draws for
+// every thread once lanes take different rejection paths; -O0, -G and a call are exact).
+__host__ __device__ __noinline__ int64_t np_binomial_btpe(NpPcg64& g, int64_t n, double p) {
   const double r = fmin(p, 1.0 - p);
   const double q = 1.0 - r;
   const double fm = n * r + r;

@@ -47,6 +47,8 @@ constexpr int kThreadsF = kWarpsF * 32;
 constexpr unsigned kFullMask = 0xffffffffu;
 constexpr uint32_t kOnes = 0x01010101u;
 constexpr int kScratchPerWarp = 1024;  // flagP[256] flagR[256] table[256] codes[256]
+constexpr int kLaneMaxDecChunks = 8;    // K1-lane limits: |D| <= 128
+constexpr int kLaneMaxSlotChunks = 64;  //                 |S| <= 1024
 
 // 16-bit position mask bit of chunk position t = 4*i + b (word i, byte b)
 inline int perm_bit(int t) { return 4 * (t & 3) + (t >> 2); }
@@ -169,6 +171,10 @@ void build_fast_decision(const GraphTables* g, DecisionTables* d) {
       d->ncand++;
     }
   }
+  d->ncand_planes.assign(16, 0);
+  for (int c = 0; c < std::min(g->num_classes, 64); ++c)
+    for (int k = 0; k < 16; ++k)
+      if ((d->class_ncand[c] >> k) & 1) d->ncand_planes[k] |= 1ull << c;
   std::vector<int> uniq;
   int local[16];
   for (int q = 0; q < nq; ++q) {
@@ -223,6 +229,8 @@ struct FastParams {
   int64_t packed_stride;    // in 32-bit words
   const uint4* slot_desc_t; // transposed-selector descriptors (packed output)
   int bulk;                 // int8 slot rows staged in shared memory, stored by TMA bulk copies
+  const uint64_t* ncand_planes;  // lane kernel: [16] classes whose candidate count has bit k
+  int nplanes;
   int64_t stage_bytes;      // per-warp staging row (16 * nq_s)
   int off_slot_desc, off_slot_cls8, off_dec_desc, off_dec_masks, off_dec_cls8, off_ncand, off_imp_bits, off_scratch;
   int off_stage;
@@ -663,6 +671,243 @@ __global__ void __launch_bounds__(kThreadsF, AP_K1_MIN_BLOCKS) propagate_fast_ke
   if (p.bulk && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+
+// ---------------------------------------------------------------------------
+// K1-lane: one THREAD per plan for small graphs (<= 64 link classes, |D| <= 128,
+// |S| <= 1024: MLP2, VGG-19, the zoo blocks).  A warp per plan spends most of its
+// ~400 instructions on per-plan fixed costs (ballots, reductions, flag tables) when
+// a plan has only a few chunks; here the class bitsets live in one thread's
+// registers (<= 2 words), so the same closure costs a few dozen instructions:
+// seed chunks -> P / R class bits through the decision descriptors, forced classes,
+// OR of the implication rows of the P classes, conflict = P & R, decided counts as
+// popcounts against per-bit planes of the candidate-per-class counts, and slot
+// chunks emitted from the same descriptors as the warp kernel (status of class c =
+// bit c of P / R).  Same outputs bit for bit (tests/test_bench_batches_gpu.py).
+template <int NW>
+__device__ __forceinline__ uint32_t lane_status(const uint32_t* Pw, const uint32_t* Rw, uint32_t c, bool codes) {
+  const uint32_t pw = (NW == 1 || c < 32) ? Pw[0] : Pw[NW - 1];
+  const uint32_t rw = (NW == 1 || c < 32) ? Rw[0] : Rw[NW - 1];
+  const uint32_t sh = c & 31u;
+  const uint32_t pb = (pw >> sh) & 1u, rb = (rw >> sh) & 1u;
+  if (codes) return pb ? 2u : (rb ? 1u : 0u);
+  return pb ? 1u : (rb ? 0u : 0xFFu);
+}
+
+template <int NW>
+__device__ __forceinline__ uint32_t lane_word4(const uint32_t* Pw, const uint32_t* Rw, uint32_t cls4, bool codes) {
+  const uint32_t s0 = lane_status<NW>(Pw, Rw, cls4 & 0xFF, codes);
+  const uint32_t s1 = lane_status<NW>(Pw, Rw, (cls4 >> 8) & 0xFF, codes);
+  const uint32_t s2 = lane_status<NW>(Pw, Rw, (cls4 >> 16) & 0xFF, codes);
+  const uint32_t s3 = lane_status<NW>(Pw, Rw, cls4 >> 24, codes);
+  return s0 | (s1 << 8) | (s2 << 16) | (s3 << 24);
+}
+
+template <int NW>
+__device__ __forceinline__ void lane_set(uint32_t* w, uint32_t c) {
+  const uint32_t bit = 1u << (c & 31u);
+  if (NW == 1 || c < 32) w[0] |= bit;
+  else w[NW - 1] |= bit;
+}
+
+// local classes of a decision chunk (<= 4 in `cls4`, position masks in two words)
+template <int NW>
+__device__ __forceinline__ void lane_mark(uint32_t cls4, uint32_t m01, uint32_t m23, uint32_t xp, uint32_t xr,
+                                          uint32_t* Pw, uint32_t* Rw) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t c = (cls4 >> (8 * j)) & 0xFF;
+    const uint32_t m = (j & 1) ? ((j < 2 ? m01 : m23) >> 16) : ((j < 2 ? m01 : m23) & 0xFFFF);
+    if (c == 0xFF) continue;
+    if (xp & m) lane_set<NW>(Pw, c);
+    if (xr & m) lane_set<NW>(Rw, c);
+  }
+}
+
+template <int NW>
+__global__ void __launch_bounds__(256) propagate_lane_kernel(FastParams p) {
+  pdl_entry();
+  extern __shared__ __align__(16) uint8_t smem[];
+  auto stage = [&](int off, const void* src, int64_t bytes) {
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    uint4* d = reinterpret_cast<uint4*>(smem + off);
+    const int64_t n16 = bytes / 16;
+    for (int64_t i = threadIdx.x; i < n16; i += blockDim.x) d[i] = s[i];
+    const uint8_t* sb = reinterpret_cast<const uint8_t*>(src);
+    for (int64_t i = n16 * 16 + threadIdx.x; i < bytes; i += blockDim.x) smem[off + i] = sb[i];
+  };
+  stage(p.off_slot_desc, p.packed_out ? p.slot_desc_t : p.slot_desc, (int64_t)p.nq_s * 16);
+  if (p.any_slot_fallback) stage(p.off_slot_cls8, p.slot_cls8, (int64_t)p.nq_s * 16);
+  stage(p.off_dec_desc, p.dec_desc, (int64_t)p.nq_d * 32);
+  stage(p.off_dec_masks, p.dec_masks, (int64_t)p.nq_d * 4);
+  stage(p.off_dec_cls8, p.dec_cls8, (int64_t)p.nq_d * 16);
+  stage(p.off_ncand, p.ncand_planes, 128);
+  stage(p.off_imp_bits, p.imp_bits, (int64_t)p.C * 32);
+  __syncthreads();
+  const uint4* slot_desc = reinterpret_cast<const uint4*>(smem + p.off_slot_desc);
+  const uint8_t* slot_cls8 = smem + p.off_slot_cls8;
+  const uint4* dec_desc = reinterpret_cast<const uint4*>(smem + p.off_dec_desc);
+  const uint32_t* dec_masks = reinterpret_cast<const uint32_t*>(smem + p.off_dec_masks);
+  const uint8_t* dec_cls8 = smem + p.off_dec_cls8;
+  const uint32_t* planes = reinterpret_cast<const uint32_t*>(smem + p.off_ncand);  // [16][2]
+  const uint32_t* imp = reinterpret_cast<const uint32_t*>(smem + p.off_imp_bits);  // [C][8]
+  uint32_t forced[NW];
+#pragma unroll
+  for (int k = 0; k < NW; ++k) forced[k] = p.forced_bits[k];
+  const bool codes = p.packed_out != nullptr;
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < p.batch; b += nthreads) {
+    uint32_t Pw[NW], Rw[NW];
+#pragma unroll
+    for (int k = 0; k < NW; ++k) Pw[k] = Rw[k] = 0;
+    int nPs = 0, nRs = 0;
+    uint32_t anyU = 0;
+    const int8_t* srow = p.seeds + b * p.seed_stride;
+    for (int q = 0; q < p.nq_d; ++q) {
+      uint32_t xp, xr, xu;
+      seed_masks(ldg_stream(srow + 16 * q), &xp, &xr, &xu);
+      const uint32_t vm = dec_masks[q];
+      const uint32_t valid = vm & 0xFFFF, cand = vm >> 16;
+      xp &= valid;
+      xr &= valid;
+      anyU |= xu & valid;
+      nPs += __popc(xp & cand);
+      nRs += __popc(xr & cand);
+      const uint4 d0 = dec_desc[2 * q];
+      if ((d0.x & 0xFF) != 0xFF) {
+        lane_mark<NW>(d0.x, d0.z, d0.w, xp, xr, Pw, Rw);
+        if (d0.y != 0xFFFFFFFFu) {
+          const uint4 d1 = dec_desc[2 * q + 1];
+          lane_mark<NW>(d0.y, d1.x, d1.y, xp, xr, Pw, Rw);
+        }
+      } else {
+        for (int t = 0; t < 16; ++t) {
+          const uint32_t bit = 1u << (4 * (t & 3) + (t >> 2));
+          const uint32_t c = dec_cls8[16 * q + t];
+          if (xp & bit) lane_set<NW>(Pw, c);
+          if (xr & bit) lane_set<NW>(Rw, c);
+        }
+      }
+    }
+    // implications of the partitioned classes, conflict
+    uint32_t acc[NW];
+#pragma unroll
+    for (int k = 0; k < NW; ++k) acc[k] = 0;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+      uint32_t t = Pw[k];
+      while (t) {
+        const int c = 32 * k + __ffs(t) - 1;
+        t &= t - 1;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) acc[w] |= imp[8 * c + w];
+      }
+    }
+    uint32_t clash = 0;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) {
+      Rw[k] |= forced[k] | acc[k];
+      clash |= Pw[k] & Rw[k];
+    }
+    bool conflict = clash != 0;
+    int dP = 0, dR = 0;
+    for (int k = 0; k < p.nplanes; ++k) {
+      int cp = 0, cr = 0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        cp += __popc(Pw[w] & planes[2 * k + w]);
+        cr += __popc(Rw[w] & ~Pw[w] & planes[2 * k + w]);
+      }
+      dP += cp << k;
+      dR += cr << k;
+    }
+    int nP = dP - nPs, nR = dR - nRs;
+    if (anyU) {  // UNDECIDED seeds: conflict rule and exact per-position newly counts
+      bool uconf = false;
+      int np = 0, nr = 0;
+      for (int j = 0; j < p.D; ++j) {
+        const int v = srow[j];
+        if (v == 2) {
+          if (p.dec_flags[j] & 2) uconf = true;
+          for (int k = p.first_same[j]; k < j; ++k)
+            if (srow[k] == 1) uconf = true;
+        }
+        if ((p.dec_flags[j] & 1) && v == -1) {
+          const uint32_t st = lane_status<NW>(Pw, Rw, dec_cls8[j], false);
+          np += st == 1;
+          nr += st == 0;
+        }
+      }
+      conflict |= uconf;
+      nP = np;
+      nR = nr;
+    }
+    p.outcome[b] = conflict ? AP_OUTCOME_CONFLICT
+                            : ((dP + dR == p.ncand_total) ? AP_OUTCOME_COMPLETE : AP_OUTCOME_INCOMPLETE);
+    if (p.counts)
+      reinterpret_cast<int4*>(p.counts)[b] = conflict ? make_int4(0, 0, 0, 0) : make_int4(dP, dR, nP, nR);
+    if (p.cand_out) {
+      int8_t* crow = p.cand_out + b * p.cand_stride;
+      for (int q = 0; q < p.nq_d; ++q) {
+        const uint4 d0 = dec_desc[2 * q];
+        uint4 o;
+        if ((d0.x & 0xFF) != 0xFF) {
+          const uint4 d1 = dec_desc[2 * q + 1];
+          const uint32_t lo = lane_word4<NW>(Pw, Rw, d0.x, false);
+          const uint32_t hi = d0.y == 0xFFFFFFFFu ? lo : lane_word4<NW>(Pw, Rw, d0.y, false);
+          o = select16(lo, hi, d1.z, d1.w);
+        } else {
+          uint32_t ow[4] = {0, 0, 0, 0};
+          for (int t = 0; t < 16; ++t) ow[t >> 2] |= lane_status<NW>(Pw, Rw, dec_cls8[16 * q + t], false) << (8 * (t & 3));
+          o = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+        }
+        if (p.cand_vec && 16 * q + 16 <= p.D) {
+          reinterpret_cast<uint4*>(crow)[q] = o;
+        } else {
+          for (int t = 0; 16 * q + t < p.D && t < 16; ++t) {
+            const uint32_t wv = (t >> 2) == 0 ? o.x : ((t >> 2) == 1 ? o.y : ((t >> 2) == 2 ? o.z : o.w));
+            crow[16 * q + t] = (int8_t)(wv >> (8 * (t & 3)));
+          }
+        }
+      }
+    }
+    if (p.slots_out) {
+      int8_t* orow = p.slots_out + b * p.slots_stride;
+      for (int q = 0; q < p.nq_s; ++q) {
+        const uint4 d = slot_desc[q];
+        uint4 o;
+        if ((d.x & 0xFF) != 0xFF) {
+          const uint32_t lo = lane_word4<NW>(Pw, Rw, d.x, false);
+          const uint32_t hi = d.y == 0xFFFFFFFFu ? lo : lane_word4<NW>(Pw, Rw, d.y, false);
+          o = select16(lo, hi, d.z, d.w);
+        } else {
+          uint32_t ow[4] = {0, 0, 0, 0};
+          for (int t = 0; t < 16; ++t) ow[t >> 2] |= lane_status<NW>(Pw, Rw, slot_cls8[16 * q + t], false) << (8 * (t & 3));
+          o = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+        }
+        stg_stream(orow + 16 * q, o);
+      }
+    } else if (codes) {
+      uint32_t* prow = p.packed_out + b * p.packed_stride;
+      for (int q = 0; q < p.nq_s; ++q) {
+        const uint4 d = slot_desc[q];  // transposed selectors
+        uint32_t word = 0;
+        if ((d.x & 0xFF) != 0xFF) {
+          const uint32_t lo = lane_word4<NW>(Pw, Rw, d.x, true);
+          const uint32_t hi = d.y == 0xFFFFFFFFu ? 0u : lane_word4<NW>(Pw, Rw, d.y, true);
+          word = prmt(lo, hi, d.z) | (prmt(lo, hi, d.z >> 16) << 2) | (prmt(lo, hi, d.w) << 4) |
+                 (prmt(lo, hi, d.w >> 16) << 6);
+          const int64_t rem = p.S - 16 * (int64_t)q;
+          if (rem < 16) word &= (1u << (2 * rem)) - 1u;
+        } else {
+          for (int t = 0; t < 16 && 16 * q + t < p.S; ++t)
+            word |= lane_status<NW>(Pw, Rw, slot_cls8[16 * q + t], true) << (2 * t);
+        }
+        __stcs(prow + q, word);
+      }
+    }
+  }
+}
+
 template <int MAXCH, int NW>
 int launch_fast_t(const FastParams& p, int64_t smem, cudaStream_t stream) {
   int num_sms = 0;
@@ -769,6 +1014,31 @@ int launch_propagate_fast(const GraphTables* g, const DecisionTables* d, const i
   }
   const int64_t smem = off;
   if (smem > 200 * 1024) return AP_ERR_UNSUPPORTED;
+  // K1-lane (one thread per plan) for small graphs; AP_K1_LANE=0 forces the warp kernel
+  const char* lane_env = std::getenv("AP_K1_LANE");
+  const bool lane_ok = p.C <= 64 && nq_d <= kLaneMaxDecChunks && nq_s <= kLaneMaxSlotChunks && !p.bulk;
+  if (lane_ok && !(lane_env && lane_env[0] == '0')) {
+    p.ncand_planes = d->d_ncand_planes.ptr;
+    int maxc = 0;
+    for (int c = 0; c < p.C; ++c) maxc = std::max<int>(maxc, d->class_ncand[c]);
+    p.nplanes = 0;
+    while ((1 << p.nplanes) <= maxc) ++p.nplanes;
+    const int64_t lsmem = p.off_scratch;  // descriptor tables only, no per-warp scratch
+    int sms = 0;
+    if (int rc = current_sm_count(&sms)) return rc;
+    const int64_t want = (batch + 255) / 256;
+    if (p.C <= 32) {
+      auto k = propagate_lane_kernel<1>;
+      AP_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsmem));
+      launch_pdl(k, dim3((unsigned)std::min<int64_t>(want, (int64_t)sms * 8)), dim3(256), (size_t)lsmem, stream, p);
+    } else {
+      auto k = propagate_lane_kernel<2>;
+      AP_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsmem));
+      launch_pdl(k, dim3((unsigned)std::min<int64_t>(want, (int64_t)sms * 8)), dim3(256), (size_t)lsmem, stream, p);
+    }
+    AP_CUDA_CHECK(cudaGetLastError());
+    return AP_OK;
+  }
   const int chunks = (nq_d + 31) / 32;
   const int nw = (p.C + 31) / 32;
   if (chunks <= 1) return dispatch_nw<1>(nw, p, smem, stream);

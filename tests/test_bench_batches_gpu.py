@@ -159,3 +159,44 @@ def test_launch_rejects_wrong_seed_width(cuda):
         eng.launch(bad, torch.empty(4, dtype=torch.uint8, device="cuda"))
     with pytest.raises(ValueError):
         eng.run_batch_host(torch.full((4, len(dims) + 1), -1, dtype=torch.int8))
+
+
+@pytest.mark.parametrize("name", ["mlp2", "vgg19", "attention_block", "t5_block"])
+@pytest.mark.parametrize("mode", ["full", "packed"])
+def test_lane_kernel_matches_warp_kernel(cuda, monkeypatch, name, mode):
+    """K1-lane (one thread per plan, small graphs) == the warp-per-plan kernel, every output,
+    including UNDECIDED seeds, all-unseeded rows and conflict rows."""
+    from goldens import load_prop
+
+    g = graphs.generate(name) if name in ("mlp2", "vgg19") else load_prop(name).graph
+    dims = decision_dims(g, g.trainable_variables)
+    n = len(dims)
+    eng = PropagationEngine(g, dims)
+    rng = np.random.default_rng(9)
+    rows = np.concatenate([
+        rng.integers(-1, 2, size=(3000, n)),                 # P / R / unseeded
+        rng.integers(-1, 3, size=(500, n)),                  # with UNDECIDED seeds
+        np.full((1, n), -1), np.zeros((1, n)),
+    ]).astype(np.int8)
+    seeds = padded(torch.from_numpy(rows).cuda())
+    B = seeds.shape[0]
+
+    def run():
+        o = {"outcome": torch.empty(B, dtype=torch.uint8, device="cuda"),
+             "counts": torch.empty((B, 4), dtype=torch.int32, device="cuda"),
+             "statuses": torch.empty((B, max(16, (n + 15) // 16 * 16)), dtype=torch.int8, device="cuda")}
+        if mode == "packed":
+            o["packed"] = torch.zeros((B, eng.packed_slots_stride), dtype=torch.uint8, device="cuda")
+            eng.launch(seeds, o["outcome"], o["counts"], None, o["statuses"], packed=o["packed"])
+        else:
+            o["slots"] = torch.zeros((B, eng.slots_stride), dtype=torch.int8, device="cuda")
+            eng.launch(seeds, o["outcome"], o["counts"], o["slots"], o["statuses"])
+        o["statuses"] = o["statuses"][:, :n]
+        return o
+
+    monkeypatch.setenv("AP_K1_LANE", "0")
+    warp = run()
+    monkeypatch.setenv("AP_K1_LANE", "1")
+    lane = run()
+    for k in warp:
+        assert torch.equal(warp[k], lane[k]), k
