@@ -183,12 +183,12 @@ struct DecisionTables {
   std::vector<uint32_t> dec_masks;    // [nq_d] valid | candidate << 16 (permuted bit order)
   std::vector<uint8_t> dec_cls8;      // [nq_d * 16]
   std::vector<uint16_t> class_ncand;  // [C] candidate positions per class
-  std::vector<uint64_t> ncand_planes; // [16] lane kernel (<= 64 classes): classes whose ncand has bit k
+  std::vector<uint32_t> ncand_planes; // [16][4] lane kernel (<= 128 classes): classes whose ncand has bit k
   DevBuf<uint32_t> d_dec_desc;
   DevBuf<uint32_t> d_dec_masks;
   DevBuf<uint8_t> d_dec_cls8;
   DevBuf<uint16_t> d_class_ncand;
-  DevBuf<uint64_t> d_ncand_planes;
+  DevBuf<uint32_t> d_ncand_planes;
   DevBuf<int32_t> d_dec_class;
   DevBuf<uint8_t> d_dec_flags;
   DevBuf<int32_t> d_first_same;

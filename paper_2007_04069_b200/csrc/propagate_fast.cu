@@ -47,8 +47,8 @@ constexpr int kThreadsF = kWarpsF * 32;
 constexpr unsigned kFullMask = 0xffffffffu;
 constexpr uint32_t kOnes = 0x01010101u;
 constexpr int kScratchPerWarp = 1024;  // flagP[256] flagR[256] table[256] codes[256]
-constexpr int kLaneMaxDecChunks = 8;    // K1-lane limits: |D| <= 128
-constexpr int kLaneMaxSlotChunks = 64;  //                 |S| <= 1024
+constexpr int kLaneMaxDecChunks = 32;   // K1-lane limits: |D| <= 512
+constexpr int kLaneMaxSlotChunks = 32;  //                 |S| <= 512 (measured: BERT-base's 1,421 slots run faster warp-per-plan)
 
 // 16-bit position mask bit of chunk position t = 4*i + b (word i, byte b)
 inline int perm_bit(int t) { return 4 * (t & 3) + (t >> 2); }
@@ -171,10 +171,10 @@ void build_fast_decision(const GraphTables* g, DecisionTables* d) {
       d->ncand++;
     }
   }
-  d->ncand_planes.assign(16, 0);
-  for (int c = 0; c < std::min(g->num_classes, 64); ++c)
+  d->ncand_planes.assign(16 * 4, 0);
+  for (int c = 0; c < std::min(g->num_classes, 128); ++c)
     for (int k = 0; k < 16; ++k)
-      if ((d->class_ncand[c] >> k) & 1) d->ncand_planes[k] |= 1ull << c;
+      if ((d->class_ncand[c] >> k) & 1) d->ncand_planes[4 * k + (c >> 5)] |= 1u << (c & 31);
   std::vector<int> uniq;
   int local[16];
   for (int q = 0; q < nq; ++q) {
@@ -229,8 +229,10 @@ struct FastParams {
   int64_t packed_stride;    // in 32-bit words
   const uint4* slot_desc_t; // transposed-selector descriptors (packed output)
   int bulk;                 // int8 slot rows staged in shared memory, stored by TMA bulk copies
-  const uint64_t* ncand_planes;  // lane kernel: [16] classes whose candidate count has bit k
+  const uint32_t* ncand_planes;  // lane kernel: [16][4] classes whose candidate count has bit k
   int nplanes;
+  int lane_pitch;   // lane kernel: per-row pitch of the warp's shared-memory output block (0: direct stores)
+  int off_lane_stage;
   int64_t stage_bytes;      // per-warp staging row (16 * nq_s)
   int off_slot_desc, off_slot_cls8, off_dec_desc, off_dec_masks, off_dec_cls8, off_ncand, off_imp_bits, off_scratch;
   int off_stage;
@@ -673,8 +675,8 @@ __global__ void __launch_bounds__(kThreadsF, AP_K1_MIN_BLOCKS) propagate_fast_ke
 
 
 // ---------------------------------------------------------------------------
-// K1-lane: one THREAD per plan for small graphs (<= 64 link classes, |D| <= 128,
-// |S| <= 1024: MLP2, VGG-19, the zoo blocks).  A warp per plan spends most of its
+// K1-lane: one THREAD per plan for small graphs (<= 128 link classes, |D| <= 512,
+// |S| <= 512: MLP2, VGG-19, the zoo blocks).  A warp per plan spends most of its
 // ~400 instructions on per-plan fixed costs (ballots, reductions, flag tables) when
 // a plan has only a few chunks; here the class bitsets live in one thread's
 // registers (<= 2 words), so the same closure costs a few dozen instructions:
@@ -683,10 +685,19 @@ __global__ void __launch_bounds__(kThreadsF, AP_K1_MIN_BLOCKS) propagate_fast_ke
 // popcounts against per-bit planes of the candidate-per-class counts, and slot
 // chunks emitted from the same descriptors as the warp kernel (status of class c =
 // bit c of P / R).  Same outputs bit for bit (tests/test_bench_batches_gpu.py).
+// word c >> 5 of a register bitset (NW <= 4) without dynamic indexing
+template <int NW>
+__device__ __forceinline__ uint32_t lane_word(const uint32_t* w, uint32_t c) {
+  uint32_t v = w[0];
+#pragma unroll
+  for (int k = 1; k < NW; ++k) v = (c >> 5) == (uint32_t)k ? w[k] : v;
+  return v;
+}
+
 template <int NW>
 __device__ __forceinline__ uint32_t lane_status(const uint32_t* Pw, const uint32_t* Rw, uint32_t c, bool codes) {
-  const uint32_t pw = (NW == 1 || c < 32) ? Pw[0] : Pw[NW - 1];
-  const uint32_t rw = (NW == 1 || c < 32) ? Rw[0] : Rw[NW - 1];
+  const uint32_t pw = lane_word<NW>(Pw, c);
+  const uint32_t rw = lane_word<NW>(Rw, c);
   const uint32_t sh = c & 31u;
   const uint32_t pb = (pw >> sh) & 1u, rb = (rw >> sh) & 1u;
   if (codes) return pb ? 2u : (rb ? 1u : 0u);
@@ -705,8 +716,8 @@ __device__ __forceinline__ uint32_t lane_word4(const uint32_t* Pw, const uint32_
 template <int NW>
 __device__ __forceinline__ void lane_set(uint32_t* w, uint32_t c) {
   const uint32_t bit = 1u << (c & 31u);
-  if (NW == 1 || c < 32) w[0] |= bit;
-  else w[NW - 1] |= bit;
+#pragma unroll
+  for (int k = 0; k < NW; ++k) w[k] |= (c >> 5) == (uint32_t)k ? bit : 0u;
 }
 
 // local classes of a decision chunk (<= 4 in `cls4`, position masks in two words)
@@ -740,7 +751,7 @@ __global__ void __launch_bounds__(256) propagate_lane_kernel(FastParams p) {
   stage(p.off_dec_desc, p.dec_desc, (int64_t)p.nq_d * 32);
   stage(p.off_dec_masks, p.dec_masks, (int64_t)p.nq_d * 4);
   stage(p.off_dec_cls8, p.dec_cls8, (int64_t)p.nq_d * 16);
-  stage(p.off_ncand, p.ncand_planes, 128);
+  stage(p.off_ncand, p.ncand_planes, 256);
   stage(p.off_imp_bits, p.imp_bits, (int64_t)p.C * 32);
   __syncthreads();
   const uint4* slot_desc = reinterpret_cast<const uint4*>(smem + p.off_slot_desc);
@@ -748,14 +759,22 @@ __global__ void __launch_bounds__(256) propagate_lane_kernel(FastParams p) {
   const uint4* dec_desc = reinterpret_cast<const uint4*>(smem + p.off_dec_desc);
   const uint32_t* dec_masks = reinterpret_cast<const uint32_t*>(smem + p.off_dec_masks);
   const uint8_t* dec_cls8 = smem + p.off_dec_cls8;
-  const uint32_t* planes = reinterpret_cast<const uint32_t*>(smem + p.off_ncand);  // [16][2]
+  const uint32_t* planes = reinterpret_cast<const uint32_t*>(smem + p.off_ncand);  // [16][4]
   const uint32_t* imp = reinterpret_cast<const uint32_t*>(smem + p.off_imp_bits);  // [C][8]
   uint32_t forced[NW];
 #pragma unroll
   for (int k = 0; k < NW; ++k) forced[k] = p.forced_bits[k];
   const bool codes = p.packed_out != nullptr;
-  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < p.batch; b += nthreads) {
+  const int lane = threadIdx.x & 31;
+  // 32 consecutive plans per warp: their output rows form one contiguous block, staged in
+  // shared memory (row pitch an odd number of 16-byte units: conflict-free 16-byte stores)
+  // and written back with coalesced stores instead of 32 scattered row stores
+  uint8_t* ostage = p.lane_pitch ? smem + p.off_lane_stage + (threadIdx.x >> 5) * 32 * p.lane_pitch : nullptr;
+  const int64_t nwarps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t base = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < p.batch;
+       base += nwarps_total * 32) {
+   const int64_t b = base + lane;
+   if (b < p.batch) {
     uint32_t Pw[NW], Rw[NW];
 #pragma unroll
     for (int k = 0; k < NW; ++k) Pw[k] = Rw[k] = 0;
@@ -814,8 +833,8 @@ __global__ void __launch_bounds__(256) propagate_lane_kernel(FastParams p) {
       int cp = 0, cr = 0;
 #pragma unroll
       for (int w = 0; w < NW; ++w) {
-        cp += __popc(Pw[w] & planes[2 * k + w]);
-        cr += __popc(Rw[w] & ~Pw[w] & planes[2 * k + w]);
+        cp += __popc(Pw[w] & planes[4 * k + w]);
+        cr += __popc(Rw[w] & ~Pw[w] & planes[4 * k + w]);
       }
       dP += cp << k;
       dR += cr << k;
@@ -871,7 +890,7 @@ __global__ void __launch_bounds__(256) propagate_lane_kernel(FastParams p) {
       }
     }
     if (p.slots_out) {
-      int8_t* orow = p.slots_out + b * p.slots_stride;
+      int8_t* orow = ostage ? reinterpret_cast<int8_t*>(ostage + lane * p.lane_pitch) : p.slots_out + b * p.slots_stride;
       for (int q = 0; q < p.nq_s; ++q) {
         const uint4 d = slot_desc[q];
         uint4 o;
@@ -884,10 +903,13 @@ __global__ void __launch_bounds__(256) propagate_lane_kernel(FastParams p) {
           for (int t = 0; t < 16; ++t) ow[t >> 2] |= lane_status<NW>(Pw, Rw, slot_cls8[16 * q + t], false) << (8 * (t & 3));
           o = make_uint4(ow[0], ow[1], ow[2], ow[3]);
         }
-        stg_stream(orow + 16 * q, o);
+        if (ostage)
+          *reinterpret_cast<uint4*>(orow + 16 * q) = o;
+        else
+          stg_stream(orow + 16 * q, o);
       }
     } else if (codes) {
-      uint32_t* prow = p.packed_out + b * p.packed_stride;
+      uint32_t* prow = ostage ? reinterpret_cast<uint32_t*>(ostage + lane * p.lane_pitch) : p.packed_out + b * p.packed_stride;
       for (int q = 0; q < p.nq_s; ++q) {
         const uint4 d = slot_desc[q];  // transposed selectors
         uint32_t word = 0;
@@ -902,8 +924,33 @@ __global__ void __launch_bounds__(256) propagate_lane_kernel(FastParams p) {
           for (int t = 0; t < 16 && 16 * q + t < p.S; ++t)
             word |= lane_status<NW>(Pw, Rw, slot_cls8[16 * q + t], true) << (2 * t);
         }
-        __stcs(prow + q, word);
+        if (ostage)
+          prow[q] = word;
+        else
+          __stcs(prow + q, word);
       }
+    }
+   }
+    if (ostage) {  // the warp's block of rows [base, base + rows) -> global, coalesced
+      __syncwarp();
+      const int rows = p.batch - base < 32 ? (int)(p.batch - base) : 32;
+      // only each row's nq_s data units: the caller's row stride may leave bytes it owns
+      const int nq = p.nq_s;
+      if (p.slots_out) {
+        const int64_t ld16 = p.slots_stride / 16;
+        uint4* dst = reinterpret_cast<uint4*>(p.slots_out + base * p.slots_stride);
+        for (int i = lane; i < rows * nq; i += 32) {
+          const int r = i / nq, c = i - r * nq;
+          __stcs(dst + r * ld16 + c, *reinterpret_cast<const uint4*>(ostage + r * p.lane_pitch + 16 * c));
+        }
+      } else {
+        uint32_t* dst = p.packed_out + base * p.packed_stride;
+        for (int i = lane; i < rows * nq; i += 32) {
+          const int r = i / nq, c = i - r * nq;
+          __stcs(dst + r * p.packed_stride + c, *reinterpret_cast<const uint32_t*>(ostage + r * p.lane_pitch + 4 * c));
+        }
+      }
+      __syncwarp();
     }
   }
 }
@@ -1016,26 +1063,36 @@ int launch_propagate_fast(const GraphTables* g, const DecisionTables* d, const i
   if (smem > 200 * 1024) return AP_ERR_UNSUPPORTED;
   // K1-lane (one thread per plan) for small graphs; AP_K1_LANE=0 forces the warp kernel
   const char* lane_env = std::getenv("AP_K1_LANE");
-  const bool lane_ok = p.C <= 64 && nq_d <= kLaneMaxDecChunks && nq_s <= kLaneMaxSlotChunks && !p.bulk;
+  const bool lane_ok = p.C <= 128 && nq_d <= kLaneMaxDecChunks && nq_s <= kLaneMaxSlotChunks && !p.bulk;
   if (lane_ok && !(lane_env && lane_env[0] == '0')) {
     p.ncand_planes = d->d_ncand_planes.ptr;
     int maxc = 0;
     for (int c = 0; c < p.C; ++c) maxc = std::max<int>(maxc, d->class_ncand[c]);
     p.nplanes = 0;
     while ((1 << p.nplanes) <= maxc) ++p.nplanes;
-    const int64_t lsmem = p.off_scratch;  // descriptor tables only, no per-warp scratch
+    // per-warp output staging when a warp's 32 rows fit (pitch: odd count of 16-byte units)
+    const int64_t row_bytes = slots_out ? slots_stride : (packed_out ? packed_stride : 0);
+    int64_t pitch = (row_bytes + 15) / 16;
+    if (pitch % 2 == 0) ++pitch;
+    pitch *= 16;
+    p.lane_pitch = 0;
+    p.off_lane_stage = (int)a16(p.off_scratch);
+    const char* st_env = std::getenv("AP_K1_LANE_STAGE");
+    if (row_bytes > 16 && pitch <= 400 && !(st_env && st_env[0] == '0')) p.lane_pitch = (int)pitch;
+    const int64_t lsmem = p.lane_pitch ? p.off_lane_stage + 8 * 32 * pitch : p.off_scratch;
     int sms = 0;
     if (int rc = current_sm_count(&sms)) return rc;
     const int64_t want = (batch + 255) / 256;
-    if (p.C <= 32) {
-      auto k = propagate_lane_kernel<1>;
-      AP_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsmem));
-      launch_pdl(k, dim3((unsigned)std::min<int64_t>(want, (int64_t)sms * 8)), dim3(256), (size_t)lsmem, stream, p);
-    } else {
-      auto k = propagate_lane_kernel<2>;
-      AP_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsmem));
-      launch_pdl(k, dim3((unsigned)std::min<int64_t>(want, (int64_t)sms * 8)), dim3(256), (size_t)lsmem, stream, p);
-    }
+    auto go = [&](auto kern) -> int {
+      AP_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsmem));
+      launch_pdl(kern, dim3((unsigned)std::min<int64_t>(want, (int64_t)sms * 8)), dim3(256), (size_t)lsmem, stream, p);
+      return AP_OK;
+    };
+    const int lnw = (p.C + 31) / 32;
+    if (lnw <= 1) go(propagate_lane_kernel<1>);
+    else if (lnw == 2) go(propagate_lane_kernel<2>);
+    else if (lnw == 3) go(propagate_lane_kernel<3>);
+    else go(propagate_lane_kernel<4>);
     AP_CUDA_CHECK(cudaGetLastError());
     return AP_OK;
   }
