@@ -761,13 +761,16 @@ __global__ void per_sample_kernel(const double* prio, int n, double alpha, doubl
   __shared__ double s_total, s_last, s_wmax;
   for (int i = threadIdx.x; i < n; i += blockDim.x) scaled[i] = pow(prio[i], alpha);
   __syncthreads();
+  if (threadIdx.x == 0) s_total = pairwise_sum(scaled, n);
+  __syncthreads();
+  // probs = scaled / total (independent divisions, in parallel); cdf = probs.cumsum() (one
+  // sequential chain of adds, numpy's order); cdf /= cdf[-1]
+  for (int i = threadIdx.x; i < n; i += blockDim.x) cdf[i] = scaled[i] / s_total;
+  __syncthreads();
   if (threadIdx.x == 0) {
-    const double total = pairwise_sum(scaled, n);
-    s_total = total;
-    // probs = scaled / total; cdf = probs.cumsum(); cdf /= cdf[-1]
-    double acc = 0.0;
-    for (int i = 0; i < n; ++i) {
-      acc = (i == 0) ? scaled[0] / total : acc + scaled[i] / total;
+    double acc = cdf[0];
+    for (int i = 1; i < n; ++i) {
+      acc = acc + cdf[i];
       cdf[i] = acc;
     }
     s_last = acc;

@@ -31,6 +31,7 @@ namespace apb {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
 constexpr int kMaxLayers = 4;  // hidden layers
 constexpr int kTN = 32;        // tile columns (one per lane)
 constexpr int kSmemFloats = 56 * 1024;  // 224 KB of dynamic shared memory per CTA (one chunk at K <= 1100)
@@ -76,7 +77,6 @@ struct Learn {
   unsigned long long* trace;  // optional: %globaltimer after each phase (CTA 0)
 };
 
-// grid-wide barrier (all CTAs co-resident: cooperative launch); generation counter in bar[1]
 __device__ __forceinline__ void trace_mark(unsigned long long* tr, int& k) {
   if (tr && blockIdx.x == 0 && threadIdx.x == 0) {
     unsigned long long t;
@@ -86,23 +86,20 @@ __device__ __forceinline__ void trace_mark(unsigned long long* tr, int& k) {
   ++k;
 }
 
+// grid-wide barrier (all CTAs co-resident: cooperative launch).  bar[0] counts arrivals
+// monotonically (it stays a multiple of the grid size between launches): one release add per
+// CTA, then acquire loads until the count reaches the next multiple.  The CTA barrier before
+// the add orders every thread's writes before thread 0's release (cumulativity).
 __device__ __forceinline__ void grid_sync(unsigned* bar) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned gen;
-    asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(gen) : "l"(bar + 1) : "memory");
-    __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-      bar[0] = 0;
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      unsigned cur;
-      do {
-        asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 1) : "memory");
-      } while (cur == gen);
-    }
-    __threadfence();
+    unsigned old;
+    asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+    const unsigned target = (old / gridDim.x + 1) * gridDim.x;
+    unsigned cur;
+    do {
+      asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
+    } while ((int)(cur - target) < 0);
   }
   __syncthreads();
 }
@@ -144,7 +141,7 @@ struct Job {
   int epi;
   const float* mask;
   int64_t ldmask;
-  __device__ __forceinline__ int tm() const { return (8 / kg) * rpt; }
+  __device__ __forceinline__ int tm() const { return (kWarps / kg) * rpt; }
   __device__ __forceinline__ int tiles() const { return ((M + tm() - 1) / tm()) * ((N + kTN - 1) / kTN); }
 };
 
@@ -167,7 +164,7 @@ constexpr int kBS = kTN + 4;  // B tile row stride (floats): 16-byte rows, confl
 //   B                Bs[k][n]   (contiguous along n: sn == 1; along k (sk == 1): element loads)
 template <int RPT, int KG, int TRANS>
 __device__ void run_tile(const Job& j, int t, float* smem) {
-  constexpr int RW = 8 / KG;       // row-warps
+  constexpr int RW = kWarps / KG;  // row-warps
   constexpr int TM = RW * RPT;
   const int ntn = (j.N + kTN - 1) / kTN;
   const int m0 = (t / ntn) * TM, n0 = (t % ntn) * kTN;
@@ -322,7 +319,7 @@ __device__ __forceinline__ void run_tile_cfg(const Job& j, int t, float* smem) {
     case 4 * 16 + 4: run_tile<4, 4, TRANS>(j, t, smem); break;
     case 1 * 16 + 8: run_tile<1, 8, TRANS>(j, t, smem); break;
     case 2 * 16 + 8: run_tile<2, 8, TRANS>(j, t, smem); break;
-    default: run_tile<4, 8, TRANS>(j, t, smem); break;
+    default: run_tile<1, 8, TRANS>(j, t, smem); break;
   }
 }
 
