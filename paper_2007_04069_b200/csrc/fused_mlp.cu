@@ -115,6 +115,7 @@ struct AOp {
   const int32_t* idx;
   int split;
   int trans;
+  int ones_at;  // trans only: row m == ones_at reads 1.0 (bias gradient as one more output row), -1 none
   __device__ __forceinline__ const float* row(int r) const {
     if (!idx) return p + (int64_t)r * sr;
     return r < split ? p0 + (int64_t)idx[r] * sr : p1 + (int64_t)idx[r - split] * sr;
@@ -207,10 +208,14 @@ __device__ void run_tile(const Job& j, int t, float* smem) {
           continue;
         }
         const float* src = j.a.row(k0 + kk) + m0;
-        if ((TM & 3) == 0 && al16(src) && m0 + TM <= j.M) {
+        const int mdata = j.a.ones_at >= 0 ? j.a.ones_at : j.M;
+        if ((TM & 3) == 0 && al16(src) && m0 + TM <= mdata) {
           for (int rr = 4 * lane; rr < TM; rr += 128) cp_async16(dst + rr, src + rr);
         } else {
-          for (int rr = lane; rr < TM; rr += 32) dst[rr] = m0 + rr < j.M ? __ldcg(src + rr) : 0.0f;
+          for (int rr = lane; rr < TM; rr += 32) {
+            const int m = m0 + rr;
+            dst[rr] = m < mdata ? __ldcg(src + rr) : (m == j.a.ones_at ? 1.0f : 0.0f);
+          }
         }
       }
     }
@@ -337,22 +342,6 @@ __device__ void run_jobs(const Job* jobs, int nj, float* smem) {
   }
 }
 
-// column sums out[n] = sum_{m < M} x[m * ld + n] (bias gradients), rows in order, 8 loads in flight
-__device__ void colsum(const float* x, int64_t ld, int M, int N, float* out) {
-  for (int n = blockIdx.x * kThreads + threadIdx.x; n < N; n += gridDim.x * kThreads) {
-    float s = 0.0f;
-    for (int m0 = 0; m0 < M; m0 += 8) {
-      float v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = m0 + u < M ? __ldcg(x + (int64_t)(m0 + u) * ld + n) : 0.0f;
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (m0 + u < M) s += v[u];
-    }
-    out[n] = s;
-  }
-}
-
 // head outputs z[row] = h[row] . Wh + bh for many rows: one warp per row, lanes split H
 template <int A1M>
 __device__ void head_rows(const float* h, int64_t ldh, int rows, int H, int A1, const float* wh, const float* bh,
@@ -427,12 +416,12 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(Learn P) {
     on = Job{};
     if (i == 0) {
       if (fwd_only) {
-        on.a = AOp{P.x_in, P.x_ld, nullptr, nullptr, nullptr, 0, 0};
+        on.a = AOp{P.x_in, P.x_ld, nullptr, nullptr, nullptr, 0, 0, -1};
       } else {
-        on.a = AOp{nullptr, P.r_ld, P.r_next, P.r_states, P.idx, B, 0};
+        on.a = AOp{nullptr, P.r_ld, P.r_next, P.r_states, P.idx, B, 0, -1};
       }
     } else {
-      on.a = AOp{Hon[i], P.d[i], nullptr, nullptr, nullptr, 0, 0};
+      on.a = AOp{Hon[i], P.d[i], nullptr, nullptr, nullptr, 0, 0, -1};
     }
     on.b = BOp{P.p + P.w_off[i], N, 1};
     on.c = Hon[i + 1];
@@ -446,8 +435,8 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(Learn P) {
     if (!fwd_only) {
       Job& tg = jobs[nj++];
       tg = on;
-      tg.a = i == 0 ? AOp{nullptr, P.r_ld, P.r_next, P.r_next, P.idx, B, 0} : AOp{Htg[i], P.d[i], nullptr, nullptr,
-                                                                                    nullptr, 0, 0};
+      tg.a = i == 0 ? AOp{nullptr, P.r_ld, P.r_next, P.r_next, P.idx, B, 0, -1} : AOp{Htg[i], P.d[i], nullptr, nullptr,
+                                                                                    nullptr, 0, 0, -1};
       tg.b = BOp{P.tp + P.w_off[i], N, 1};
       tg.c = Htg[i + 1];
       tg.M = B;
@@ -521,13 +510,16 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(Learn P) {
         for (int j = 0; j <= A; ++j) dz[(int64_t)b * A1 + j] = j == 0 ? g : ((j - 1) == a ? g : 0.0f) - g / (float)A;
         P.td[b] = tdv;
         lrow[b] = w * hub;
+        // priorities[idx] = |td| + 1e-6; among duplicate indices the last write wins (agent.py:226)
+        bool last = true;
+        for (int k = b + 1; k < B; ++k) last &= P.idx[k] != row;
+        if (last) P.r_prio[row] = fabs((double)tdv) + 1e-6;
       }
       __syncthreads();
       if (threadIdx.x == 0) {
         float s = 0.0f;
         for (int b = 0; b < B; ++b) s += lrow[b];
         *P.loss = s;
-        for (int b = 0; b < B; ++b) P.r_prio[P.idx[b]] = fabs((double)P.td[b]) + 1e-6;  // last duplicate wins
       }
     }
   }
@@ -540,14 +532,16 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(Learn P) {
     const float* Hc = Hon[L] + (int64_t)B * H;  // current-state rows
     Job jobs[2];
     jobs[0] = Job{};
-    jobs[0].a = AOp{Hc, H, nullptr, nullptr, nullptr, 0, 1};  // (m=j, k=b) = Hc[b][j]
+    // (m=j, k=b) = Hc[b][j]; row H of ones: the bias gradient lands right after gWh (bh follows wh)
+    jobs[0].a = AOp{Hc, H, nullptr, nullptr, nullptr, 0, 1, H};
     jobs[0].b = BOp{dz, A1, 1};
     jobs[0].c = P.grad + P.w_off[L];
     jobs[0].ldc = A1;
-    jobs[0].M = H, jobs[0].N = A1, jobs[0].K = B, jobs[0].rpt = 4, jobs[0].kg = 1;
+    jobs[0].M = H + 1, jobs[0].N = A1, jobs[0].K = B, jobs[0].rpt = 4, jobs[0].kg = 1;
     jobs[1] = Job{};
-    jobs[1].a = AOp{dz, A1, nullptr, nullptr, nullptr, 0, 0};
-    jobs[1].b = BOp{P.p + P.w_off[L], 1, A1};  // (k=a, n=j) = Wh[j][a]
+    jobs[1].a = AOp{dz, A1, nullptr, nullptr, nullptr, 0, 0, -1};
+    // (k=a, n=j) = Wh[j][a]: rows of the transposed copy when present (16-byte staging)
+    jobs[1].b = P.wt[L] ? BOp{P.wt[L], P.wt_ld[L], 1} : BOp{P.p + P.w_off[L], 1, A1};
     jobs[1].c = dh[L];
     jobs[1].ldc = H;
     jobs[1].M = B, jobs[1].N = H, jobs[1].K = A1, jobs[1].rpt = 1, jobs[1].kg = 1;
@@ -555,7 +549,6 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(Learn P) {
     jobs[1].mask = Hc;
     jobs[1].ldmask = H;
     run_jobs(jobs, 2, smem);
-    colsum(dz, A1, B, A1, P.grad + P.b_off[L]);
   }
   grid_sync(P.bar);
     trace_mark(P.trace, tk);
@@ -567,19 +560,21 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(Learn P) {
     int nj = 0;
     Job& wg = jobs[nj++];
     wg = Job{};
+    // (m=p, k=b) = input row b, column p; row din of ones gives gb right after gW (b_i follows w_i)
     if (i == 1)
-      wg.a = AOp{nullptr, P.r_ld, P.r_states, P.r_states, P.idx, B, 1};  // (m=p, k=b) = state row idx[b], col p
+      wg.a = AOp{nullptr, P.r_ld, P.r_states, P.r_states, P.idx, B, 1, din};
     else
-      wg.a = AOp{Hon[i - 1] + (int64_t)B * din, din, nullptr, nullptr, nullptr, 0, 1};
+      wg.a = AOp{Hon[i - 1] + (int64_t)B * din, din, nullptr, nullptr, nullptr, 0, 1, din};
     wg.b = BOp{dh[i], dout, 1};
     wg.c = P.grad + P.w_off[i - 1];
     wg.ldc = dout;
-    wg.M = din, wg.N = dout, wg.K = B, wg.rpt = 4, wg.kg = 1;
+    wg.M = din + 1, wg.N = dout, wg.K = B, wg.rpt = 4, wg.kg = 1;
     if (i > 1) {
       Job& dg = jobs[nj++];
       dg = Job{};
-      dg.a = AOp{dh[i], dout, nullptr, nullptr, nullptr, 0, 0};
-      dg.b = BOp{P.p + P.w_off[i - 1], 1, dout};  // (k=q, n=p) = W[p][q]
+      dg.a = AOp{dh[i], dout, nullptr, nullptr, nullptr, 0, 0, -1};
+      // (k=q, n=p) = W[p][q] = row q of the transposed copy
+      dg.b = P.wt[i - 1] ? BOp{P.wt[i - 1], P.wt_ld[i - 1], 1} : BOp{P.p + P.w_off[i - 1], 1, dout};
       dg.c = dh[i - 1];
       dg.ldc = din;
       dg.M = B, dg.N = din, dg.K = dout, dg.rpt = 1, dg.kg = 2;
@@ -588,7 +583,6 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(Learn P) {
       dg.ldmask = din;
     }
     run_jobs(jobs, nj, smem);
-    colsum(dh[i], dout, B, dout, P.grad + P.b_off[i - 1]);
     grid_sync(P.bar);
     trace_mark(P.trace, tk);
   }

@@ -233,6 +233,7 @@ struct FastParams {
   int nplanes;
   int lane_pitch;   // lane kernel: per-row pitch of the warp's shared-memory output block (0: direct stores)
   int off_lane_stage;
+  int off_lane_tab, lane_tab_stride;  // lane kernel: per-thread class status (or code) table
   int64_t stage_bytes;      // per-warp staging row (16 * nq_s)
   int off_slot_desc, off_slot_cls8, off_dec_desc, off_dec_masks, off_dec_cls8, off_ncand, off_imp_bits, off_scratch;
   int off_stage;
@@ -734,6 +735,37 @@ __device__ __forceinline__ void lane_mark(uint32_t cls4, uint32_t m01, uint32_t 
   }
 }
 
+// the thread's class table: byte c = status of class c (codes: status + 1), four classes per
+// 32-bit store, straight from the register bitsets
+template <int NW>
+__device__ __forceinline__ void lane_write_table(uint32_t* tab, const uint32_t* Pw, const uint32_t* Rw, int C,
+                                                 bool codes) {
+#pragma unroll
+  for (int k = 0; k < NW; ++k) {
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      const int c4 = 8 * k + n;
+      if (4 * c4 >= C) break;
+      const uint32_t p4 = (Pw[k] >> (4 * n)) & 0xFu, r4 = (Rw[k] >> (4 * n)) & 0xFu;
+      uint32_t w = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t pb = (p4 >> j) & 1u, rb = (r4 >> j) & 1u;
+        const uint32_t v = codes ? (pb ? 2u : (rb ? 1u : 0u)) : (pb ? 1u : (rb ? 0u : 0xFFu));
+        w |= v << (8 * j);
+      }
+      tab[c4] = w;
+    }
+  }
+}
+
+// status word of 4 classes (bytes of `cls4`) from the thread's table
+__device__ __forceinline__ uint32_t lane_tab4(const uint8_t* tab, uint32_t cls4) {
+  const uint32_t s0 = tab[cls4 & 0xFF], s1 = tab[(cls4 >> 8) & 0xFF], s2 = tab[(cls4 >> 16) & 0xFF],
+                 s3 = tab[cls4 >> 24];
+  return prmt(prmt(s0, s1, 0x0040), prmt(s2, s3, 0x0040), 0x5410);
+}
+
 template <int NW>
 __global__ void __launch_bounds__(256) propagate_lane_kernel(FastParams p) {
   pdl_entry();
@@ -864,6 +896,10 @@ __global__ void __launch_bounds__(256) propagate_lane_kernel(FastParams p) {
                             : ((dP + dR == p.ncand_total) ? AP_OUTCOME_COMPLETE : AP_OUTCOME_INCOMPLETE);
     if (p.counts)
       reinterpret_cast<int4*>(p.counts)[b] = conflict ? make_int4(0, 0, 0, 0) : make_int4(dP, dR, nP, nR);
+    uint8_t* tab = smem + p.off_lane_tab + threadIdx.x * p.lane_tab_stride;
+    // statuses (slots / candidates) or codes (packed rows); the packed mode's candidate statuses
+    // come from the bitsets directly
+    lane_write_table<NW>(reinterpret_cast<uint32_t*>(tab), Pw, Rw, p.C, codes);
     if (p.cand_out) {
       int8_t* crow = p.cand_out + b * p.cand_stride;
       for (int q = 0; q < p.nq_d; ++q) {
@@ -871,8 +907,9 @@ __global__ void __launch_bounds__(256) propagate_lane_kernel(FastParams p) {
         uint4 o;
         if ((d0.x & 0xFF) != 0xFF) {
           const uint4 d1 = dec_desc[2 * q + 1];
-          const uint32_t lo = lane_word4<NW>(Pw, Rw, d0.x, false);
-          const uint32_t hi = d0.y == 0xFFFFFFFFu ? lo : lane_word4<NW>(Pw, Rw, d0.y, false);
+          const uint32_t lo = codes ? lane_word4<NW>(Pw, Rw, d0.x, false) : lane_tab4(tab, d0.x);
+          const uint32_t hi = d0.y == 0xFFFFFFFFu ? lo : (codes ? lane_word4<NW>(Pw, Rw, d0.y, false)
+                                                                : lane_tab4(tab, d0.y));
           o = select16(lo, hi, d1.z, d1.w);
         } else {
           uint32_t ow[4] = {0, 0, 0, 0};
@@ -895,12 +932,12 @@ __global__ void __launch_bounds__(256) propagate_lane_kernel(FastParams p) {
         const uint4 d = slot_desc[q];
         uint4 o;
         if ((d.x & 0xFF) != 0xFF) {
-          const uint32_t lo = lane_word4<NW>(Pw, Rw, d.x, false);
-          const uint32_t hi = d.y == 0xFFFFFFFFu ? lo : lane_word4<NW>(Pw, Rw, d.y, false);
+          const uint32_t lo = lane_tab4(tab, d.x);
+          const uint32_t hi = d.y == 0xFFFFFFFFu ? lo : lane_tab4(tab, d.y);
           o = select16(lo, hi, d.z, d.w);
         } else {
           uint32_t ow[4] = {0, 0, 0, 0};
-          for (int t = 0; t < 16; ++t) ow[t >> 2] |= lane_status<NW>(Pw, Rw, slot_cls8[16 * q + t], false) << (8 * (t & 3));
+          for (int t = 0; t < 16; ++t) ow[t >> 2] |= (uint32_t)tab[slot_cls8[16 * q + t]] << (8 * (t & 3));
           o = make_uint4(ow[0], ow[1], ow[2], ow[3]);
         }
         if (ostage)
@@ -914,15 +951,14 @@ __global__ void __launch_bounds__(256) propagate_lane_kernel(FastParams p) {
         const uint4 d = slot_desc[q];  // transposed selectors
         uint32_t word = 0;
         if ((d.x & 0xFF) != 0xFF) {
-          const uint32_t lo = lane_word4<NW>(Pw, Rw, d.x, true);
-          const uint32_t hi = d.y == 0xFFFFFFFFu ? 0u : lane_word4<NW>(Pw, Rw, d.y, true);
+          const uint32_t lo = lane_tab4(tab, d.x);
+          const uint32_t hi = d.y == 0xFFFFFFFFu ? 0u : lane_tab4(tab, d.y);
           word = prmt(lo, hi, d.z) | (prmt(lo, hi, d.z >> 16) << 2) | (prmt(lo, hi, d.w) << 4) |
                  (prmt(lo, hi, d.w >> 16) << 6);
           const int64_t rem = p.S - 16 * (int64_t)q;
           if (rem < 16) word &= (1u << (2 * rem)) - 1u;
         } else {
-          for (int t = 0; t < 16 && 16 * q + t < p.S; ++t)
-            word |= lane_status<NW>(Pw, Rw, slot_cls8[16 * q + t], true) << (2 * t);
+          for (int t = 0; t < 16 && 16 * q + t < p.S; ++t) word |= (uint32_t)tab[slot_cls8[16 * q + t]] << (2 * t);
         }
         if (ostage)
           prow[q] = word;
@@ -939,15 +975,21 @@ __global__ void __launch_bounds__(256) propagate_lane_kernel(FastParams p) {
       if (p.slots_out) {
         const int64_t ld16 = p.slots_stride / 16;
         uint4* dst = reinterpret_cast<uint4*>(p.slots_out + base * p.slots_stride);
+        int r = lane / nq, c = lane - r * nq;
+        const int dr = 32 / nq, dc = 32 - dr * nq;
         for (int i = lane; i < rows * nq; i += 32) {
-          const int r = i / nq, c = i - r * nq;
           __stcs(dst + r * ld16 + c, *reinterpret_cast<const uint4*>(ostage + r * p.lane_pitch + 16 * c));
+          r += dr, c += dc;
+          if (c >= nq) c -= nq, ++r;
         }
       } else {
         uint32_t* dst = p.packed_out + base * p.packed_stride;
+        int r = lane / nq, c = lane - r * nq;
+        const int dr = 32 / nq, dc = 32 - dr * nq;
         for (int i = lane; i < rows * nq; i += 32) {
-          const int r = i / nq, c = i - r * nq;
           __stcs(dst + r * p.packed_stride + c, *reinterpret_cast<const uint32_t*>(ostage + r * p.lane_pitch + 4 * c));
+          r += dr, c += dc;
+          if (c >= nq) c -= nq, ++r;
         }
       }
       __syncwarp();
@@ -1079,7 +1121,14 @@ int launch_propagate_fast(const GraphTables* g, const DecisionTables* d, const i
     p.off_lane_stage = (int)a16(p.off_scratch);
     const char* st_env = std::getenv("AP_K1_LANE_STAGE");
     if (row_bytes > 16 && pitch <= 400 && !(st_env && st_env[0] == '0')) p.lane_pitch = (int)pitch;
-    const int64_t lsmem = p.lane_pitch ? p.off_lane_stage + 8 * 32 * pitch : p.off_scratch;
+    int64_t lsmem = p.lane_pitch ? p.off_lane_stage + 8 * 32 * pitch : p.off_scratch;
+    int tw = (p.C + 3) / 4;  // 32-bit words per thread table, odd: conflict-free byte lookups
+    if (tw % 2 == 0) ++tw;
+    p.lane_tab_stride = 4 * tw;
+    p.off_lane_tab = (int)a16(lsmem);
+    // + 256: unused local-class bytes (0xFF) of a descriptor index past the thread's row; the
+    // selectors never pick those bytes, the loads only have to stay inside the allocation
+    lsmem = p.off_lane_tab + 256 * (int64_t)p.lane_tab_stride + 256;
     int sms = 0;
     if (int rc = current_sm_count(&sms)) return rc;
     const int64_t want = (batch + 255) / 256;

@@ -231,8 +231,12 @@ class DeviceSearch:
 
     def __del__(self):
         h = getattr(self, "loop", None)
-        if h is not None and _native._lib is not None:
-            _native._lib.ap_loop_graph_destroy(h)
+        lib = getattr(_native, "_lib", None) if _native is not None else None
+        if h is not None and lib is not None:
+            try:
+                lib.ap_loop_graph_destroy(h)
+            except Exception:  # interpreter shutdown: the library may be half torn down
+                pass
 
     # -- one launch -------------------------------------------------------------------------
 
