@@ -86,6 +86,36 @@ __device__ __forceinline__ void trace_mark(unsigned long long* tr, int& k) {
   ++k;
 }
 
+#ifdef AP_FUSED_TILE_TRACE  // dev-only: stamps of CTA 0's tiles into trace[4096 + 8 n + k]
+__device__ unsigned long long* g_tile_trace;
+__device__ int g_tile_n;
+#define TT(k)                                                                     \
+  do {                                                                            \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && g_tile_trace && g_tile_n < 64) {    \
+      unsigned long long t_;                                                      \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                      \
+      g_tile_trace[4096 + 8 * g_tile_n + k] = t_;                                 \
+      if (k == 5) ++g_tile_n;                                                     \
+    }                                                                             \
+  } while (0)
+#else
+#define TT(k) \
+  do {        \
+  } while (0)
+#endif
+
+// trace mode: each CTA's arrival time at the end of phase k (its work done), after the
+// per-phase marks of CTA 0 (tr[64 + k * grid + cta])
+__device__ __forceinline__ void trace_arrive(unsigned long long* tr, int k) {
+  if (!tr) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[64 + k * gridDim.x + blockIdx.x] = t;
+  }
+}
+
 // grid-wide barrier (all CTAs co-resident: cooperative launch).  bar[0] counts arrivals
 // monotonically (it stays a multiple of the grid size between launches): one release add per
 // CTA, then acquire loads until the count reaches the next multiple.  The CTA barrier before
@@ -97,8 +127,11 @@ __device__ __forceinline__ void grid_sync(unsigned* bar) {
     asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
     const unsigned target = (old / gridDim.x + 1) * gridDim.x;
     unsigned cur;
+    // relaxed polls: an acquire load invalidates the SM's L1 on every poll (CCTL.IVALL), which
+    // also evicts the CTA's stack; every cross-CTA operand of this kernel is read at L2
+    // (ld.global.cg / cp.async.cg), where the releasing CTAs' writes already are
     do {
-      asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
+      asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
     } while ((int)(cur - target) < 0);
   }
   __syncthreads();
@@ -142,6 +175,15 @@ struct Job {
   int epi;
   const float* mask;
   int64_t ldmask;
+  // Adam epilogue (weight-gradient jobs, which sum the whole batch inside one tile): C is
+  // the gradient block of the parameters at flat offset `eoff`; the tile also applies Adam
+  // to them and, with `wt`, writes rows < wt_rows of the transposed copy
+  const Learn* lp;
+  int64_t eoff;
+  float c1, c2;
+  float* wt;
+  int64_t wt_ld;
+  int wt_rows;
   __device__ __forceinline__ int tm() const { return (kWarps / kg) * rpt; }
   __device__ __forceinline__ int tiles() const { return ((M + tm() - 1) / tm()) * ((N + kTN - 1) / kTN); }
 };
@@ -163,8 +205,12 @@ constexpr int kBS = kTN + 4;  // B tile row stride (floats): 16-byte rows, confl
 //   A row-major      As[r][k]   (TRANS = 0: contiguous along k)
 //   A transposed     At[k][r]   (TRANS = 1: element (m, k) in source row k, contiguous along m)
 //   B                Bs[k][n]   (contiguous along n: sn == 1; along k (sk == 1): element loads)
+// (out of line, like run_jobs: one copy of each variant instead of one per phase keeps the
+// kernel's code small enough for the instruction caches)
 template <int RPT, int KG, int TRANS>
-__device__ void run_tile(const Job& j, int t, float* smem) {
+__device__ __noinline__ void run_tile(const Job& jref, int t, float* smem) {
+  TT(0);
+  const Job& j = jref;  // in shared memory (Frame)
   constexpr int RW = kWarps / KG;  // row-warps
   constexpr int TM = RW * RPT;
   const int ntn = (j.N + kTN - 1) / kTN;
@@ -251,8 +297,10 @@ __device__ void run_tile(const Job& j, int t, float* smem) {
         }
       }
     }
+    TT(1);
     cp_async_wait_all();
     __syncthreads();
+    TT(2);
     // ---- this warp's K segment (multiples of 4)
     const int seg = ((kcp / 4 + KG - 1) / KG) * 4;
     const int klo = kgi * seg, khi = min(kcp, klo + seg);
@@ -280,6 +328,7 @@ __device__ void run_tile(const Job& j, int t, float* smem) {
       }
     }
   }
+  TT(3);
   // ---- partial sums of the K groups, added in group order
   if (KG > 1) {
     __syncthreads();
@@ -295,18 +344,60 @@ __device__ void run_tile(const Job& j, int t, float* smem) {
       acc[q] = v;
     }
   }
+  TT(4);
   const int n = n0 + c;
   if (n >= j.N) return;
   const float bias = j.bias ? __ldcg(j.bias + n) : 0.0f;
+  // operands of the epilogue loaded up front (one round trip, not one per row)
+  float mk[RPT];
+  if (j.epi == 2) {
 #pragma unroll
-  for (int q = 0; q < RPT; ++q) {
-    const int m = m0 + rw + RW * q;
-    if (m >= j.M) break;
-    float v = acc[q] + bias;
-    if (j.epi == 1) v = fmaxf(v, 0.0f);
-    if (j.epi == 2 && !(__ldcg(j.mask + (int64_t)m * j.ldmask + n) > 0.0f)) v = 0.0f;
-    j.c[(int64_t)m * j.ldc + n] = v;
+    for (int q = 0; q < RPT; ++q) {
+      const int m = m0 + rw + RW * q;
+      mk[q] = m < j.M ? __ldcg(j.mask + (int64_t)m * j.ldmask + n) : 0.0f;
+    }
   }
+  if (!j.lp) {
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int m = m0 + rw + RW * q;
+      if (m >= j.M) break;
+      float v = acc[q] + bias;
+      if (j.epi == 1) v = fmaxf(v, 0.0f);
+      if (j.epi == 2 && !(mk[q] > 0.0f)) v = 0.0f;
+      j.c[(int64_t)m * j.ldc + n] = v;
+    }
+  } else {  // Adam (agent.py:229-250) on the finished gradient
+    const Learn& P = *j.lp;
+    float* const pm = P.m + j.eoff;
+    float* const pv = P.v + j.eoff;
+    float* const pp = P.p + j.eoff;
+    const float b1 = P.b1, b2 = P.b2, lr = P.lr, eps = P.eps, c1 = j.c1, c2 = j.c2;
+    float om[RPT], ov[RPT], op[RPT];
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int m = m0 + rw + RW * q;
+      const int64_t e = (int64_t)m * j.ldc + n;
+      om[q] = ov[q] = op[q] = 0.0f;
+      if (m < j.M) om[q] = __ldcg(pm + e), ov[q] = __ldcg(pv + e), op[q] = __ldcg(pp + e);
+    }
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int m = m0 + rw + RW * q;
+      if (m >= j.M) break;
+      const float v = acc[q] + bias;
+      const int64_t e = (int64_t)m * j.ldc + n;
+      j.c[e] = v;
+      const float mi = b1 * om[q] + (1.0f - b1) * v;
+      const float vi = b2 * ov[q] + (1.0f - b2) * v * v;
+      pm[e] = mi;
+      pv[e] = vi;
+      const float pi = op[q] - lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+      pp[e] = pi;
+      if (j.wt && m < j.wt_rows) j.wt[(int64_t)n * j.wt_ld + m] = pi;
+    }
+  }
+  TT(5);
 }
 
 template <int TRANS>
@@ -329,7 +420,7 @@ __device__ __forceinline__ void run_tile_cfg(const Job& j, int t, float* smem) {
 }
 
 // all tiles of up to 3 independent jobs, spread over the grid
-__device__ void run_jobs(const Job* jobs, int nj, float* smem) {
+__device__ __noinline__ void run_jobs(const Job* jobs, int nj, float* smem) {
   int total = 0;
   for (int i = 0; i < nj; ++i) total += jobs[i].tiles();
   for (int t = blockIdx.x; t < total; t += gridDim.x) {
@@ -342,274 +433,514 @@ __device__ void run_jobs(const Job* jobs, int nj, float* smem) {
   }
 }
 
-// head outputs z[row] = h[row] . Wh + bh for many rows: one warp per row, lanes split H
-template <int A1M>
-__device__ void head_rows(const float* h, int64_t ldh, int rows, int H, int A1, const float* wh, const float* bh,
-                          float* z, int wbase, int wstride) {
-  const int lane = threadIdx.x & 31;
-  for (int row = wbase; row < rows; row += wstride) {
-    float s[A1M];
-#pragma unroll
-    for (int j = 0; j < A1M; ++j) s[j] = 0.0f;
-    const float* hr = h + (int64_t)row * ldh;
-    for (int k = lane; k < H; k += 32) {
-      const float x = __ldcg(hr + k);
-#pragma unroll
-      for (int j = 0; j < A1M; ++j)
-        if (j < A1) s[j] = fmaf(x, __ldcg(wh + (int64_t)k * A1 + j), s[j]);
+// Tile shapes of one phase: the smallest row count per tile whose tiles fit one wave of a
+// reference 148-SM grid, then row-warps x K-groups for that height (K-groups when K is long).
+// A fixed reference grid keeps every summation order a function of the problem alone.
+__device__ void plan_tiles(Job* jobs, int nj) {
+  constexpr int kRefGrid = 148;
+  int lvl = 0;
+  for (; lvl < 6; ++lvl) {
+    int total = 0;
+    for (int i = 0; i < nj; ++i) {
+      int tm = 1 << lvl;
+      while (tm > 1 && tm / 2 >= jobs[i].M) tm /= 2;
+      total += ((jobs[i].M + tm - 1) / tm) * ((jobs[i].N + kTN - 1) / kTN);
     }
-#pragma unroll
-    for (int j = 0; j < A1M; ++j)
-      for (int o = 16; o; o >>= 1) s[j] += __shfl_xor_sync(0xffffffffu, s[j], o);
-    if (lane < A1) {
-      float v = 0.0f;
-#pragma unroll
-      for (int j = 0; j < A1M; ++j)
-        if (j == lane) v = s[j];
-      z[(int64_t)row * A1 + lane] = v + __ldcg(bh + lane);
+    if (total <= kRefGrid) break;
+  }
+  for (int i = 0; i < nj; ++i) {
+    Job& j = jobs[i];
+    int tm = 1 << lvl;
+    while (tm > 1 && tm / 2 >= j.M) tm /= 2;
+    const int K = j.K;
+    switch (tm) {
+      case 1: j.rpt = 1, j.kg = 8; break;
+      case 2: j.rpt = K >= 256 ? 2 : 1, j.kg = K >= 256 ? 8 : 4; break;
+      case 4: j.rpt = K >= 256 ? 2 : 1, j.kg = K >= 256 ? 4 : 2; break;
+      case 8: j.rpt = K >= 512 ? 4 : (K >= 128 ? 2 : 1), j.kg = K >= 512 ? 4 : (K >= 128 ? 2 : 1); break;
+      case 16: j.rpt = K >= 128 ? 4 : 2, j.kg = K >= 128 ? 2 : 1; break;
+      case 32: j.rpt = 4, j.kg = 1; break;
+      default: j.rpt = 8, j.kg = 1; break;
     }
   }
 }
 
-__device__ __forceinline__ float dueling_q(const float* z, int A, int a) {
-  float mean = 0.0f;
-  for (int j = 1; j <= A; ++j) mean += z[j];
-  mean /= (float)A;
-  return z[0] + z[1 + a] - mean;
+// warp sum of per-lane partials (fixed xor tree: every lane gets the same value)
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
 }
 
-__global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(Learn P) {
+// mean of the advantages z[1..A]: lane-strided partial sums, then the xor tree
+__device__ __forceinline__ float adv_mean(const float* z, int A) {
+  float s = 0.0f;
+  for (int j = 1 + (threadIdx.x & 31); j <= A; j += 32) s += __ldcg(z + j);
+  return warp_sum(s) / (float)A;
+}
+
+// head outputs of R rows (rows hr[r], weights wh[r] / bh[r]) into registers of every lane,
+// in head_row's summation order; the loads of 4 k-steps are issued together
+template <int A1M, int R>
+__device__ __forceinline__ void head_regs_(const float* const* hr, int H, int A1, const float* const* wh,
+                                          const float* const* bh, float (*z)[A1M]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int j = 0; j < A1M; ++j) z[r][j] = 0.0f;
+  constexpr int U = 4;
+  for (int k0 = 0; k0 < H; k0 += U * 32) {
+    float x[R][U], w[R][U][A1M];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k = k0 + u * 32 + lane;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        x[r][u] = k < H ? __ldcg(hr[r] + k) : 0.0f;
+#pragma unroll
+        for (int j = 0; j < A1M; ++j) w[r][u][j] = (k < H && j < A1) ? __ldcg(wh[r] + (int64_t)k * A1 + j) : 0.0f;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int j = 0; j < A1M; ++j) z[r][j] = fmaf(x[r][u], w[r][u][j], z[r][j]);
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int j = 0; j < A1M; ++j) z[r][j] = warp_sum(z[r][j]) + (j < A1 ? __ldcg(bh[r] + j) : 0.0f);
+}
+
+// one head row z = h . Wh + bh by one warp (lanes split H), for heads of <= A1M outputs
+template <int A1M>
+__device__ __forceinline__ void head_row(const float* hr, int H, int A1, const float* wh, const float* bh, float* z) {
+  const int lane = threadIdx.x & 31;
+  float s[A1M];
+#pragma unroll
+  for (int j = 0; j < A1M; ++j) s[j] = 0.0f;
+  for (int k = lane; k < H; k += 32) {
+    const float x = __ldcg(hr + k);
+#pragma unroll
+    for (int j = 0; j < A1M; ++j)
+      if (j < A1) s[j] = fmaf(x, __ldcg(wh + (int64_t)k * A1 + j), s[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < A1M; ++j) s[j] = warp_sum(s[j]);
+  if (lane < A1) {
+    float v = 0.0f;
+#pragma unroll
+    for (int j = 0; j < A1M; ++j)
+      if (j == lane) v = s[j];
+    z[lane] = v + __ldcg(bh + lane);
+  }
+}
+
+// One row of the small-head step (1 + A <= A1M outputs) with the head outputs kept in
+// registers: forward mode writes Q; learn mode runs the double-DQN TD of sample b.
+template <int A1M>
+__device__ __noinline__ void small_head_row(const Learn& P, int r, int B, const float* HonL, const float* HtgL,
+                                            float* dz, float* lrow, bool fwd_only) {
+  const int lane = threadIdx.x & 31;
+  const int L = P.L, A = P.A, A1 = A + 1, H = P.d[L];
+  const float* w_on = P.p + P.w_off[L];
+  const float* b_on = P.p + P.b_off[L];
+  if (fwd_only) {
+    const float* hr[1] = {HonL + (int64_t)r * H};
+    const float* wh[1] = {w_on};
+    const float* bh[1] = {b_on};
+    float z[1][A1M];
+    head_regs_<A1M, 1>(hr, H, A1, wh, bh, z);
+    float mean = 0.0f;
+#pragma unroll
+    for (int j = 1; j < A1M; ++j)
+      if (j <= A) mean += z[0][j];
+    mean /= (float)A;
+#pragma unroll
+    for (int a = 0; a + 1 < A1M; ++a)
+      if (a < A && lane == a) P.q_out[(int64_t)r * A + a] = z[0][0] + z[0][1 + a] - mean;
+    return;
+  }
+  const int b = r;
+  const int64_t row = P.idx[b];
+  const float rew = P.r_rewards[row];
+  const int a = P.r_actions[row];
+  const bool done = P.r_done[row] != 0;
+  const float w = P.isw[b];
+  uint32_t mbits = 0;
+#pragma unroll
+  for (int j = 0; j + 1 < A1M; ++j)
+    if (j < A && P.r_mask[row * A + j]) mbits |= 1u << j;
+  bool later = false;
+  for (int k = b + 1 + lane; k < B; k += 32) later |= P.idx[k] == row;
+  const float* hr[3] = {HonL + (int64_t)b * H, HonL + (int64_t)(B + b) * H, HtgL + (int64_t)b * H};
+  const float* wh[3] = {w_on, w_on, P.tp + P.w_off[L]};
+  const float* bh[3] = {b_on, b_on, P.tp + P.b_off[L]};
+  float z[3][A1M];  // online next, online cur, target next
+  head_regs_<A1M, 3>(hr, H, A1, wh, bh, z);
+  float mn = 0.0f, mc = 0.0f, mt = 0.0f;
+#pragma unroll
+  for (int j = 1; j < A1M; ++j)
+    if (j <= A) mn += z[0][j], mc += z[1][j], mt += z[2][j];
+  mn /= (float)A, mc /= (float)A, mt /= (float)A;
+  // masked argmax, first index among equal maxima (agent.py masked_argmax)
+  float best = -INFINITY;
+  int bj = -1;
+  float qa = 0.0f, tn = 0.0f;
+#pragma unroll
+  for (int j = 0; j + 1 < A1M; ++j) {
+    if (j >= A) break;
+    const float qv = z[0][0] + z[0][1 + j] - mn;
+    if (((mbits >> j) & 1u) && (bj < 0 || qv > best)) best = qv, bj = j;
+    if (j == a) qa = z[1][0] + z[1][1 + j] - mc;
+  }
+  const bool any = bj >= 0;
+  const int a_next = any ? bj : 0;
+#pragma unroll
+  for (int j = 0; j + 1 < A1M; ++j)
+    if (j == a_next) tn = z[2][0] + z[2][1 + j] - mt;
+  const float d = (done || !any) ? 1.0f : 0.0f;
+  const float target = rew + P.gamma * (1.0f - d) * tn;
+  const float tdv = qa - target;
+  const float ad = fabsf(tdv);
+  const float hub = ad <= P.delta ? 0.5f * tdv * tdv : P.delta * (ad - 0.5f * P.delta);
+  const float g = w * fminf(fmaxf(tdv, -P.delta), P.delta) / (float)B;
+  if (lane <= A) dz[(int64_t)b * A1 + lane] = lane == 0 ? g : ((lane - 1) == a ? g : 0.0f) - g / (float)A;
+  later = __any_sync(0xffffffffu, later);
+  if (lane == 0) {
+    P.td[b] = tdv;
+    lrow[b] = w * hub;
+    if (!later) P.r_prio[row] = fabs((double)tdv) + 1e-6;
+  }
+}
+
+// Per-CTA control state in shared memory, written by thread 0: the phase's jobs and the
+// workspace pointers.  (As per-thread locals these were 2 KB of stack per thread, 0.5 MB per
+// CTA, far past the L1 left beside 224 KB of shared memory: every phase setup went to L2.)
+struct Frame {
+  Job jobs[2];
+  int nj;
+  float* Hon[kMaxLayers + 1];
+  float* Htg[kMaxLayers + 1];
+  float* dh[kMaxLayers + 1];
+  float *zon, *ztg, *dz, *lrow;
+};
+
+__device__ __forceinline__ AOp rows_of(const float* p, int64_t sr) {
+  return AOp{p, sr, nullptr, nullptr, nullptr, 0, 0, -1};
+}
+
+__global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const __grid_constant__ Learn P) {
   extern __shared__ float smem[];
+  __shared__ Frame F;
   int tk = 0;
+#ifdef AP_FUSED_TILE_TRACE
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_tile_trace = P.trace, g_tile_n = 0;
+#endif
   trace_mark(P.trace, tk);
   const int L = P.L, A = P.A, A1 = A + 1;
   const bool fwd_only = P.rows_fwd > 0;
   const int B = fwd_only ? P.rows_fwd : P.B;
   const int Ron = fwd_only ? B : 2 * B;  // online rows: [next; cur]
-  // workspace: online activations [Ron, d_i], target activations [B, d_i] (i = 1..L),
-  // head outputs, dz, dh_i [B, d_i]
-  float* ws = P.ws;
-  float* Hon[kMaxLayers + 1];
-  float* Htg[kMaxLayers + 1];
-  float* dh[kMaxLayers + 1];
-  for (int i = 1; i <= L; ++i) {
-    Hon[i] = ws;
-    ws += (int64_t)Ron * P.d[i];
-    Htg[i] = ws;
-    ws += (int64_t)B * P.d[i];
-    dh[i] = ws;
-    ws += (int64_t)B * P.d[i];
+  const bool t0 = threadIdx.x == 0;
+  if (t0) {
+    // workspace: online activations [Ron, d_i], target activations [B, d_i] (i = 1..L),
+    // head outputs, dz, dh_i [B, d_i], the per-row loss terms
+    float* ws = P.ws;
+    for (int i = 1; i <= L; ++i) {
+      F.Hon[i] = ws;
+      ws += (int64_t)Ron * P.d[i];
+      F.Htg[i] = ws;
+      ws += (int64_t)B * P.d[i];
+      F.dh[i] = ws;
+      ws += (int64_t)B * P.d[i];
+    }
+    F.zon = ws;
+    ws += (int64_t)Ron * A1;
+    F.ztg = ws;
+    ws += (int64_t)B * A1;
+    F.dz = ws;
+    ws += (int64_t)B * A1;
+    F.lrow = ws;
   }
-  float* zon = ws;
-  ws += (int64_t)Ron * A1;
-  float* ztg = ws;
-  ws += (int64_t)B * A1;
-  float* dz = ws;
-  ws += (int64_t)B * A1;
 
   // forward, layer by layer
   for (int i = 0; i < L; ++i) {
-    const int K = P.d[i], N = P.d[i + 1];
-    Job jobs[2];
-    int nj = 0;
-    Job& on = jobs[nj++];
-    on = Job{};
-    if (i == 0) {
-      if (fwd_only) {
-        on.a = AOp{P.x_in, P.x_ld, nullptr, nullptr, nullptr, 0, 0, -1};
-      } else {
-        on.a = AOp{nullptr, P.r_ld, P.r_next, P.r_states, P.idx, B, 0, -1};
+    if (t0) {
+      const int K = P.d[i], N = P.d[i + 1];
+      F.nj = 0;
+      Job& on = F.jobs[F.nj++];
+      on = Job{};
+      if (i == 0)
+        on.a = fwd_only ? rows_of(P.x_in, P.x_ld) : AOp{nullptr, P.r_ld, P.r_next, P.r_states, P.idx, B, 0, -1};
+      else
+        on.a = rows_of(F.Hon[i], P.d[i]);
+      on.b = BOp{P.p + P.w_off[i], N, 1};
+      on.c = F.Hon[i + 1];
+      on.ldc = N;
+      on.M = Ron, on.N = N, on.K = K;
+      on.bias = P.p + P.b_off[i];
+      on.epi = 1;
+      if (!fwd_only) {
+        Job& tg = F.jobs[F.nj++];
+        tg = on;
+        tg.a = i == 0 ? AOp{nullptr, P.r_ld, P.r_next, P.r_next, P.idx, B, 0, -1} : rows_of(F.Htg[i], P.d[i]);
+        tg.b = BOp{P.tp + P.w_off[i], N, 1};
+        tg.c = F.Htg[i + 1];
+        tg.M = B;
+        tg.bias = P.tp + P.b_off[i];
       }
-    } else {
-      on.a = AOp{Hon[i], P.d[i], nullptr, nullptr, nullptr, 0, 0, -1};
+      plan_tiles(F.jobs, F.nj);
     }
-    on.b = BOp{P.p + P.w_off[i], N, 1};
-    on.c = Hon[i + 1];
-    on.ldc = N;
-    on.M = Ron, on.N = N, on.K = K;
-    // small row counts split K over the warps (the act forward: 1 row), large ones split rows
-    on.rpt = Ron >= 64 ? 2 : 1;
-    on.kg = Ron >= 64 ? 2 : (Ron >= 8 ? 4 : 8);
-    on.bias = P.p + P.b_off[i];
-    on.epi = 1;
-    if (!fwd_only) {
-      Job& tg = jobs[nj++];
-      tg = on;
-      tg.a = i == 0 ? AOp{nullptr, P.r_ld, P.r_next, P.r_next, P.idx, B, 0, -1} : AOp{Htg[i], P.d[i], nullptr, nullptr,
-                                                                                    nullptr, 0, 0, -1};
-      tg.b = BOp{P.tp + P.w_off[i], N, 1};
-      tg.c = Htg[i + 1];
-      tg.M = B;
-      tg.rpt = 2;
-      tg.kg = 2;
-      tg.bias = P.tp + P.b_off[i];
-    }
-    run_jobs(jobs, nj, smem);
+    __syncthreads();
+    run_jobs(F.jobs, F.nj, smem);
+    trace_arrive(P.trace, tk);
     grid_sync(P.bar);
     trace_mark(P.trace, tk);
   }
 
-  // head outputs, one warp per row over the whole grid (online rows, then target rows)
+  // head outputs: wide heads as tiles over the grid (then a barrier), small heads inside the
+  // per-row step below (one warp computes its row's 1 or 3 head rows itself)
   const int H = P.d[L];
-  {
-    const int wid = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5), nw = gridDim.x * (kThreads / 32);
-    if (A1 <= 8) {
-      head_rows<8>(Hon[L], H, Ron, H, A1, P.p + P.w_off[L], P.p + P.b_off[L], zon, wid, nw);
-      if (!fwd_only) head_rows<8>(Htg[L], H, B, H, A1, P.tp + P.w_off[L], P.tp + P.b_off[L], ztg, wid, nw);
-    } else {
-      // wide heads: one thread per (row, output)
-      const int tid = blockIdx.x * kThreads + threadIdx.x, nt = gridDim.x * kThreads;
-      const int nrows = fwd_only ? Ron : Ron + B;
-      for (int e = tid; e < nrows * A1; e += nt) {
-        const int row = e / A1, jj = e - row * A1;
-        const bool tgt = row >= Ron;
-        const float* h = tgt ? Htg[L] + (int64_t)(row - Ron) * H : Hon[L] + (int64_t)row * H;
-        const float* w = (tgt ? P.tp : P.p) + P.w_off[L];
-        float acc = 0.0f;
-        for (int k = 0; k < H; ++k) acc = fmaf(__ldcg(h + k), __ldcg(w + (int64_t)k * A1 + jj), acc);
-        acc += __ldcg((tgt ? P.tp : P.p) + P.b_off[L] + jj);
-        (tgt ? ztg + (int64_t)(row - Ron) * A1 : zon + (int64_t)row * A1)[jj] = acc;
+  const bool small_head = A1 <= 8;
+  if (!small_head) {
+    if (t0) {
+      F.nj = 0;
+      Job& on = F.jobs[F.nj++];
+      on = Job{};
+      on.a = rows_of(F.Hon[L], H);
+      on.b = BOp{P.p + P.w_off[L], A1, 1};
+      on.c = F.zon;
+      on.ldc = A1;
+      on.M = Ron, on.N = A1, on.K = H;
+      on.bias = P.p + P.b_off[L];
+      if (!fwd_only) {
+        Job& tg = F.jobs[F.nj++];
+        tg = on;
+        tg.a = rows_of(F.Htg[L], H);
+        tg.b = BOp{P.tp + P.w_off[L], A1, 1};
+        tg.c = F.ztg;
+        tg.M = B;
+        tg.bias = P.tp + P.b_off[L];
       }
+      plan_tiles(F.jobs, F.nj);
     }
-  }
-  grid_sync(P.bar);
+    __syncthreads();
+    run_jobs(F.jobs, F.nj, smem);
+    trace_arrive(P.trace, tk);
+    grid_sync(P.bar);
     trace_mark(P.trace, tk);
-  if (blockIdx.x == 0) {
-    if (fwd_only) {
-      for (int e = threadIdx.x; e < Ron * A; e += kThreads) {
-        const int row = e / A, a = e - row * A;
-        P.q_out[(int64_t)row * A + a] = dueling_q(zon + (int64_t)row * A1, A, a);
+  }
+  {
+    const int lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * kWarps + (threadIdx.x >> 5), nw = gridDim.x * kWarps;
+    float* const zon = F.zon;
+    float* const ztg = F.ztg;
+    float* const dz = F.dz;
+    const float* const HonL = F.Hon[L];
+    const float* const HtgL = F.Htg[L];
+    for (int r = gw; r < (fwd_only ? Ron : B); r += nw) {
+      if (small_head) {
+        if (A1 <= 3)
+          small_head_row<3>(P, r, B, HonL, HtgL, dz, F.lrow, fwd_only);
+        else
+          small_head_row<8>(P, r, B, HonL, HtgL, dz, F.lrow, fwd_only);
+        continue;
       }
-    } else {
-      // double-DQN TD (agent.py:277-296) for row b: online next -> best action over the next mask,
-      // target next -> its value, online cur -> Q of the taken action
-      float* lrow = smem;  // [B] weighted Huber terms
-      for (int b = threadIdx.x; b < B; b += kThreads) {
-        const int64_t row = P.idx[b];
-        const uint8_t* mk = P.r_mask + row * A;
-        const float* zn = zon + (int64_t)b * A1;
-        bool any = false;
-        float best = -INFINITY;
-        int best_j = 0;
-        for (int j = 0; j < A; ++j) {
-          if (!mk[j]) continue;
-          const float qv = dueling_q(zn, A, j);
-          if (!any || qv > best) best = qv, best_j = j;
-          any = true;
+      if (fwd_only) {
+        if (small_head) {
+          head_row<8>(HonL + (int64_t)r * H, H, A1, P.p + P.w_off[L], P.p + P.b_off[L], zon + (int64_t)r * A1);
+          __syncwarp();
         }
-        const int a_next = any ? best_j : 0;
-        const float d = (P.r_done[row] || !any) ? 1.0f : 0.0f;
-        const float target =
-            P.r_rewards[row] + P.gamma * (1.0f - d) * dueling_q(ztg + (int64_t)b * A1, A, a_next);
-        const int a = P.r_actions[row];
-        const float tdv = dueling_q(zon + (int64_t)(B + b) * A1, A, a) - target;
-        const float w = P.isw[b];
-        const float ad = fabsf(tdv);
-        const float hub = ad <= P.delta ? 0.5f * tdv * tdv : P.delta * (ad - 0.5f * P.delta);
-        const float g = w * fminf(fmaxf(tdv, -P.delta), P.delta) / (float)B;
-        for (int j = 0; j <= A; ++j) dz[(int64_t)b * A1 + j] = j == 0 ? g : ((j - 1) == a ? g : 0.0f) - g / (float)A;
-        P.td[b] = tdv;
-        lrow[b] = w * hub;
-        // priorities[idx] = |td| + 1e-6; among duplicate indices the last write wins (agent.py:226)
-        bool last = true;
-        for (int k = b + 1; k < B; ++k) last &= P.idx[k] != row;
-        if (last) P.r_prio[row] = fabs((double)tdv) + 1e-6;
+        // Q = V + A - mean(A) (agent.py dueling head)
+        const float* z = zon + (int64_t)r * A1;
+        const float mean = adv_mean(z, A), v0 = __ldcg(z);
+        for (int a2 = lane; a2 < A; a2 += 32) P.q_out[(int64_t)r * A + a2] = v0 + __ldcg(z + 1 + a2) - mean;
+        continue;
       }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        float s = 0.0f;
-        for (int b = 0; b < B; ++b) s += lrow[b];
-        *P.loss = s;
+      // double-DQN TD (agent.py:277-296) for row b = r: online next -> best action over the next
+      // mask, target next -> its value, online cur -> Q of the taken action
+      const int b = r;
+      const int64_t row = P.idx[b];
+      // the row's replay fields, loaded before the head math they do not depend on
+      const float rew = P.r_rewards[row];
+      const int a = P.r_actions[row];
+      const bool done = P.r_done[row] != 0;
+      const float w = P.isw[b];
+      const uint8_t* mk = P.r_mask + row * A;
+      bool later = false;
+      for (int k = b + 1 + lane; k < B; k += 32) later |= P.idx[k] == row;
+      if (small_head) {
+        head_row<8>(HonL + (int64_t)b * H, H, A1, P.p + P.w_off[L], P.p + P.b_off[L], zon + (int64_t)b * A1);
+        head_row<8>(HonL + (int64_t)(B + b) * H, H, A1, P.p + P.w_off[L], P.p + P.b_off[L],
+                    zon + (int64_t)(B + b) * A1);
+        head_row<8>(HtgL + (int64_t)b * H, H, A1, P.tp + P.w_off[L], P.tp + P.b_off[L], ztg + (int64_t)b * A1);
+        __syncwarp();
+      }
+      const float* zn = zon + (int64_t)b * A1;
+      const float* zt = ztg + (int64_t)b * A1;
+      const float* zc = zon + (int64_t)(B + b) * A1;
+      const float mn = adv_mean(zn, A), mt = adv_mean(zt, A), mc = adv_mean(zc, A);
+      // masked argmax, the first index among equal maxima (lane-strided, then a tie-aware tree)
+      float best = -INFINITY;
+      int bj = -1;
+      const float zn0 = __ldcg(zn);
+      for (int j2 = lane; j2 < A; j2 += 32) {
+        if (!mk[j2]) continue;
+        const float qv = zn0 + __ldcg(zn + 1 + j2) - mn;
+        if (bj < 0 || qv > best) best = qv, bj = j2;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+        if (oj >= 0 && (bj < 0 || ob > best || (ob == best && oj < bj))) best = ob, bj = oj;
+      }
+      const bool any = bj >= 0;
+      const int a_next = any ? bj : 0;
+      const float d = (done || !any) ? 1.0f : 0.0f;
+      const float target = rew + P.gamma * (1.0f - d) * (__ldcg(zt) + __ldcg(zt + 1 + a_next) - mt);
+      const float tdv = (__ldcg(zc) + __ldcg(zc + 1 + a) - mc) - target;
+      const float ad = fabsf(tdv);
+      const float hub = ad <= P.delta ? 0.5f * tdv * tdv : P.delta * (ad - 0.5f * P.delta);
+      const float g = w * fminf(fmaxf(tdv, -P.delta), P.delta) / (float)B;
+      for (int j2 = lane; j2 <= A; j2 += 32)
+        dz[(int64_t)b * A1 + j2] = j2 == 0 ? g : ((j2 - 1) == a ? g : 0.0f) - g / (float)A;
+      // priorities[idx] = |td| + 1e-6; among duplicate indices the last write wins (agent.py:226)
+      later = __any_sync(0xffffffffu, later);
+      if (lane == 0) {
+        P.td[b] = tdv;
+        F.lrow[b] = w * hub;
+        if (!later) P.r_prio[row] = fabs((double)tdv) + 1e-6;
       }
     }
   }
   if (fwd_only) return;
+  trace_arrive(P.trace, tk);
   grid_sync(P.bar);
-    trace_mark(P.trace, tk);
-
-  // head backward: gWh = H_L(cur)^T dz, gbh, dh_L = relu'(H_L) * (dz Wh^T)
-  {
-    const float* Hc = Hon[L] + (int64_t)B * H;  // current-state rows
-    Job jobs[2];
-    jobs[0] = Job{};
-    // (m=j, k=b) = Hc[b][j]; row H of ones: the bias gradient lands right after gWh (bh follows wh)
-    jobs[0].a = AOp{Hc, H, nullptr, nullptr, nullptr, 0, 1, H};
-    jobs[0].b = BOp{dz, A1, 1};
-    jobs[0].c = P.grad + P.w_off[L];
-    jobs[0].ldc = A1;
-    jobs[0].M = H + 1, jobs[0].N = A1, jobs[0].K = B, jobs[0].rpt = 4, jobs[0].kg = 1;
-    jobs[1] = Job{};
-    jobs[1].a = AOp{dz, A1, nullptr, nullptr, nullptr, 0, 0, -1};
-    // (k=a, n=j) = Wh[j][a]: rows of the transposed copy when present (16-byte staging)
-    jobs[1].b = P.wt[L] ? BOp{P.wt[L], P.wt_ld[L], 1} : BOp{P.p + P.w_off[L], 1, A1};
-    jobs[1].c = dh[L];
-    jobs[1].ldc = H;
-    jobs[1].M = B, jobs[1].N = H, jobs[1].K = A1, jobs[1].rpt = 1, jobs[1].kg = 1;
-    jobs[1].epi = 2;
-    jobs[1].mask = Hc;
-    jobs[1].ldmask = H;
-    run_jobs(jobs, 2, smem);
-  }
-  grid_sync(P.bar);
-    trace_mark(P.trace, tk);
-
-  // hidden layers, last to first
-  for (int i = L; i >= 1; --i) {
-    const int din = P.d[i - 1], dout = P.d[i];
-    Job jobs[2];
-    int nj = 0;
-    Job& wg = jobs[nj++];
-    wg = Job{};
-    // (m=p, k=b) = input row b, column p; row din of ones gives gb right after gW (b_i follows w_i)
-    if (i == 1)
-      wg.a = AOp{nullptr, P.r_ld, P.r_states, P.r_states, P.idx, B, 1, din};
-    else
-      wg.a = AOp{Hon[i - 1] + (int64_t)B * din, din, nullptr, nullptr, nullptr, 0, 1, din};
-    wg.b = BOp{dh[i], dout, 1};
-    wg.c = P.grad + P.w_off[i - 1];
-    wg.ldc = dout;
-    wg.M = din + 1, wg.N = dout, wg.K = B, wg.rpt = 4, wg.kg = 1;
-    if (i > 1) {
-      Job& dg = jobs[nj++];
-      dg = Job{};
-      dg.a = AOp{dh[i], dout, nullptr, nullptr, nullptr, 0, 0, -1};
-      // (k=q, n=p) = W[p][q] = row q of the transposed copy
-      dg.b = P.wt[i - 1] ? BOp{P.wt[i - 1], P.wt_ld[i - 1], 1} : BOp{P.p + P.w_off[i - 1], 1, dout};
-      dg.c = dh[i - 1];
-      dg.ldc = din;
-      dg.M = B, dg.N = din, dg.K = dout, dg.rpt = 1, dg.kg = 2;
-      dg.epi = 2;
-      dg.mask = Hon[i - 1] + (int64_t)B * din;
-      dg.ldmask = din;
+  trace_mark(P.trace, tk);
+  if (blockIdx.x == 0 && threadIdx.x < 32) {  // fixed-order sum; the terms loaded in parallel
+    float* sl = smem + kSmemFloats - 256;       // (past every tile's footprint in this phase)
+    for (int b = threadIdx.x; b < B; b += 32) sl[b] = __ldcg(F.lrow + b);
+    __syncwarp();
+    if (threadIdx.x == 0) {
+      float s = 0.0f;
+      for (int b = 0; b < B; ++b) s += sl[b];
+      *P.loss = s;
     }
-    run_jobs(jobs, nj, smem);
-    grid_sync(P.bar);
-    trace_mark(P.trace, tk);
   }
 
-  // Adam (agent.py:229-250) over every parameter + the transposed weight copies
+  // Adam bias corrections (host values, or the parity loop's table entry for this train step)
   float c1 = P.c1, c2 = P.c2;
   if (P.ctab) {
     const int64_t k = P.ctl[AP_CTL_TRAIN] + P.t_offset - P.ctl[AP_PL_TAB_BASE];
     c1 = P.ctab[2 * k];
     c2 = P.ctab[2 * k + 1];
   }
-  for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < P.nparams; e += (int64_t)gridDim.x * kThreads) {
-    const float gi = __ldcg(P.grad + e);
-    const float mi = P.b1 * P.m[e] + (1.0f - P.b1) * gi;
-    const float vi = P.b2 * P.v[e] + (1.0f - P.b2) * gi * gi;
-    P.m[e] = mi;
-    P.v[e] = vi;
-    const float pi = P.p[e] - P.lr * (mi / c1) / (sqrtf(vi / c2) + P.eps);
-    P.p[e] = pi;
-    for (int s = 0; s <= L; ++s) {
-      const int64_t off = P.w_off[s], rows = P.d[s], cols = P.d[s + 1];
-      if (e >= off && e < off + rows * cols && P.wt[s]) {
-        const int64_t rr = (e - off) / cols, cc = (e - off) - rr * cols;
-        P.wt[s][cc * P.wt_ld[s] + rr] = pi;
+  // Each weight-gradient tile sums the whole batch, so it applies Adam itself; a weight's
+  // transposed copy is refreshed one phase later when a dgrad of its own phase reads it.
+  auto with_adam = [&](Job& j, int s, bool direct_wt) {
+    j.lp = &P;
+    j.eoff = P.w_off[s];
+    j.c1 = c1, j.c2 = c2;
+    j.wt = direct_wt ? P.wt[s] : nullptr;
+    j.wt_ld = P.wt_ld[s];
+    j.wt_rows = P.d[s];
+  };
+  auto refresh_wt = [&](int s) {
+    const int rows = P.d[s], cols = P.d[s + 1];
+    const float* w = P.p + P.w_off[s];
+    float* dst = P.wt[s];
+    const int64_t ld = P.wt_ld[s];
+    for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < (int64_t)rows * cols;
+         e += (int64_t)gridDim.x * kThreads) {
+      const int64_t c = e / rows, r = e - c * rows;
+      dst[c * ld + r] = __ldcg(w + r * cols + c);
+    }
+  };
+
+  // head backward: gWh = H_L(cur)^T dz, gbh, dh_L = relu'(H_L) * (dz Wh^T); Adam on Wh, bh
+  if (t0) {
+    const float* Hc = F.Hon[L] + (int64_t)B * H;  // current-state rows
+    F.nj = 2;
+    Job& wg = F.jobs[0];
+    wg = Job{};
+    // (m=j, k=b) = Hc[b][j]; row H of ones: the bias gradient lands right after gWh (bh follows wh)
+    wg.a = AOp{Hc, H, nullptr, nullptr, nullptr, 0, 1, H};
+    wg.b = BOp{F.dz, A1, 1};
+    wg.c = P.grad + P.w_off[L];
+    wg.ldc = A1;
+    wg.M = H + 1, wg.N = A1, wg.K = B;
+    with_adam(wg, L, false);
+    Job& dg = F.jobs[1];
+    dg = Job{};
+    dg.a = rows_of(F.dz, A1);
+    // (k=a, n=j) = Wh[j][a]: rows of the transposed copy (the pre-update weights)
+    dg.b = BOp{P.wt[L], P.wt_ld[L], 1};
+    dg.c = F.dh[L];
+    dg.ldc = H;
+    dg.M = B, dg.N = H, dg.K = A1;
+    dg.epi = 2;
+    dg.mask = Hc;
+    dg.ldmask = H;
+    plan_tiles(F.jobs, 2);
+  }
+  __syncthreads();
+  run_jobs(F.jobs, F.nj, smem);
+  trace_arrive(P.trace, tk);
+  grid_sync(P.bar);
+  trace_mark(P.trace, tk);
+
+  // hidden layers, last to first: gW_{i-1} (+ Adam), dh_{i-1}; refresh the transposed copy of
+  // the weight updated in the phase before
+  for (int i = L; i >= 1; --i) {
+    if (t0) {
+      const int din = P.d[i - 1], dout = P.d[i];
+      F.nj = 0;
+      Job& wg = F.jobs[F.nj++];
+      wg = Job{};
+      // (m=p, k=b) = input row b, column p; row din of ones gives gb right after gW (b_i follows w_i)
+      if (i == 1)
+        wg.a = AOp{nullptr, P.r_ld, P.r_states, P.r_states, P.idx, B, 1, din};
+      else
+        wg.a = AOp{F.Hon[i - 1] + (int64_t)B * din, din, nullptr, nullptr, nullptr, 0, 1, din};
+      wg.b = BOp{F.dh[i], dout, 1};
+      wg.c = P.grad + P.w_off[i - 1];
+      wg.ldc = dout;
+      wg.M = din + 1, wg.N = dout, wg.K = B;
+      with_adam(wg, i - 1, i == 1);  // no dgrad reads w_0's copy: written directly
+      if (i > 1) {
+        Job& dg = F.jobs[F.nj++];
+        dg = Job{};
+        dg.a = rows_of(F.dh[i], dout);
+        // (k=q, n=p) = W[p][q] = row q of the transposed copy (pre-update)
+        dg.b = BOp{P.wt[i - 1], P.wt_ld[i - 1], 1};
+        dg.c = F.dh[i - 1];
+        dg.ldc = din;
+        dg.M = B, dg.N = din, dg.K = dout;
+        dg.epi = 2;
+        dg.mask = F.Hon[i - 1] + (int64_t)B * din;
+        dg.ldmask = din;
       }
+      plan_tiles(F.jobs, F.nj);
+    }
+    __syncthreads();
+    run_jobs(F.jobs, F.nj, smem);
+#ifdef AP_FUSED_TILE_TRACE_TWICE  // dev-only timing probe: the same tiles again (warm code and data)
+    __syncthreads();
+    run_jobs(F.jobs, F.nj, smem);
+#endif
+    refresh_wt(i);  // i == L: the head; else w_i (updated in the phase of layer i + 1)
+    if (i > 1) {
+      trace_arrive(P.trace, tk);
+      grid_sync(P.bar);
+      trace_mark(P.trace, tk);
     }
   }
+  trace_arrive(P.trace, tk);
   trace_mark(P.trace, tk);
 }
 
@@ -618,7 +949,7 @@ int64_t workspace_floats(int L, const int* d, int B, bool fwd_only) {
   int64_t n = 0;
   for (int i = 1; i <= L; ++i) n += (Ron + 2 * (int64_t)B) * d[i];
   const int64_t A1 = d[L + 1];
-  return n + (Ron + 2 * (int64_t)B) * A1 + 64;
+  return n + (Ron + 2 * (int64_t)B) * A1 + B + 64;
 }
 
 int launch(const Learn& P, cudaStream_t stream) {
@@ -693,6 +1024,11 @@ int ap_dqn_learn_fused(const ap_fused_learn* a, void* stream) {
     set_error("ap_dqn_learn_fused: bad arguments");
     return AP_ERR_INVALID;
   }
+  for (int i = 0; i <= a->L; ++i)
+    if (!a->wt[i] || a->wt_ld[i] < a->dims[i]) {
+      set_error("ap_dqn_learn_fused: every weight needs its transposed copy (wt[i], wt_ld[i] >= dims[i])");
+      return AP_ERR_INVALID;
+    }
   P.B = a->batch;
   P.p = a->params;
   P.tp = a->target;
