@@ -599,6 +599,8 @@ typedef struct ap_parity_loop {
   double* ep_return;
   float* loss_log;          /* [loss_cap] summed batch loss per train step */
   int64_t loss_cap;
+  int64_t learn_gate;       /* > 0: the learn-body kernels do nothing while the ring holds fewer
+                               rows (a loop graph without the IF node); 0: ungated */
 } ap_parity_loop;
 
 /* agent.act: eps-greedy with numpy's draws (random(), integers(A)) over Q of the
@@ -672,6 +674,7 @@ typedef struct ap_fused_learn {
   float* workspace;         /* ap_mlp_fused_workspace(L, dims, batch, 0) floats */
   uint32_t* barrier;        /* [2] zero-initialised, private to the caller's stream */
   uint64_t* trace;          /* optional [16]: %globaltimer after each phase (profiling) */
+  int64_t gate;             /* > 0 (with ctl): no-op while ctl[AP_CTL_SIZE] < gate */
 } ap_fused_learn;
 
 int64_t ap_mlp_fused_workspace(int32_t L, const int32_t* dims, int32_t rows, int32_t forward_only);

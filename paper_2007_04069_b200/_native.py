@@ -114,6 +114,7 @@ class ParityLoopDesc(ctypes.Structure):
         ("log_pos", ctypes.c_void_p), ("log_decided", ctypes.c_void_p), ("ep_conflict", ctypes.c_void_p),
         ("ep_len", ctypes.c_void_p), ("ep_return", ctypes.c_void_p), ("loss_log", ctypes.c_void_p),
         ("loss_cap", ctypes.c_int64),
+        ("learn_gate", ctypes.c_int64),
     ]
 
 
@@ -137,6 +138,7 @@ class FusedLearnDesc(ctypes.Structure):
         ("wt", ctypes.c_void_p * 5), ("wt_ld", ctypes.c_int64 * 5), ("td", ctypes.c_void_p),
         ("loss", ctypes.c_void_p), ("workspace", ctypes.c_void_p), ("barrier", ctypes.c_void_p),
         ("trace", ctypes.c_void_p),
+        ("gate", ctypes.c_int64),
     ]
 PL = {"STEP": 0, "SLOT": 1, "SIZE": 2, "TRAIN": 3, "EPISODES": 4, "BUDGET": 5, "MAX_STEPS": 6, "POS": 7,
       "EP_STEPS": 8, "BEST_PART": 9, "BEST_EP": 10, "SYNC": 11, "T_POS": 12, "EP_BASE": 13, "TRAIN0": 14,

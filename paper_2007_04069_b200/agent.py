@@ -728,7 +728,7 @@ class FusedLearnState:
             beta1=optimizer.beta1, beta2=optimizer.beta2, eps=optimizer.eps, wt=wt, wt_ld=wt_ld, td=P(self.td),
             loss=P(self.loss), workspace=P(self.ws), barrier=P(self.bar))
 
-    def run(self, idx, weights, correct1=1.0, correct2=1.0, ctab=None, ctl=None, t_offset=0):
+    def run(self, idx, weights, correct1=1.0, correct2=1.0, ctab=None, ctl=None, t_offset=0, gate=0):
         import ctypes
 
         d = self.desc
@@ -737,6 +737,7 @@ class FusedLearnState:
         d.ctab = None if ctab is None else ctab.data_ptr()
         d.ctl = None if ctl is None else ctl.data_ptr()
         d.t_offset = int(t_offset)
+        d.gate = int(gate)
         _native.check(_native.require_device().ap_dqn_learn_fused(ctypes.byref(d), _stream()))
         return self.loss
 

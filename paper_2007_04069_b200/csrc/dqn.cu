@@ -758,6 +758,7 @@ __global__ void per_sample_kernel(const double* prio, int n, double alpha, doubl
                                   const int64_t* ctl) {
   pdl_entry();
   if (ctl) n = (int)ctl[AP_CTL_SIZE];  // device-held ring size (parity loop)
+  if (ctl && n < B) return;            // no learn step yet (self-gated loop body)
   __shared__ double s_total, s_last, s_wmax;
   for (int i = threadIdx.x; i < n; i += blockDim.x) scaled[i] = pow(prio[i], alpha);
   __syncthreads();

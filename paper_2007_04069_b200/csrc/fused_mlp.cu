@@ -7,21 +7,27 @@
 // dueling MLP and Adam.  As separate tensor-core GEMMs that is ~40 dependent
 // launches of 4-11 us each; here every phase is a set of register-tiled fp32
 // tiles spread over all SMs, with grid-wide barriers between dependent phases
-// (2L + 3 for L hidden layers), so one launch does the whole step:
+// (2L + 2 for L hidden layers, one more for heads wider than 8), so one launch does
+// the whole step:
 //
 //   fwd layer i   H_i = relu(H_{i-1} W_i + b_i)   online rows [next; cur], target rows next
 //                 (layer 0 reads the replay-ring rows through the sampled indices)
 //   head + TD     z = H_L Wh + bh, Q = V + A - mean(A), double-DQN target, Huber,
-//                 dz = dLoss/dz, td, loss, priorities |td| + 1e-6 (last duplicate wins)
+//                 dz = dLoss/dz, td, loss terms, priorities |td| + 1e-6 (last duplicate
+//                 wins); one warp per sample, small heads computed in its registers
 //   head bwd      gWh = H_L^T dz, gbh = colsum dz, dh_L = relu'(H_L) (dz Wh^T)
 //   layer i bwd   gW_i = H_{i-1}^T dh_i, gb_i = colsum dh_i, dh_{i-1} = relu'(H_{i-1}) (dh_i W_i^T)
-//   Adam          every parameter, plus the transposed weight copies the tensor-core
-//                 forward path reads
+//   Adam          in the epilogue of each weight-gradient tile (a tile sums the whole
+//                 batch, so its gradient is final); the transposed copies the dgrads and
+//                 the tensor-core forward read are refreshed one phase later
 //
-// Every sum runs in a fixed order (k ascending inside a tile, tiles never split K),
-// so results are deterministic and independent of the grid size.  fp32 products
-// and sums (FMA) track the fp64 reference to ~1e-6 relative (tests/test_fused_mlp_gpu.py).
-// The same kernel in forward mode gives Q for a few rows (the act of the search loop).
+// Tile shapes are planned per phase against a fixed 148-SM reference grid, every sum
+// runs in a fixed order (k ascending inside a K-group, groups added in order, tiles
+// never split K across CTAs), so results are deterministic and independent of the
+// launch grid.  fp32 products and sums (FMA) track the fp64 reference to ~1e-6
+// relative (tests/test_fused_mlp_gpu.py).  Control state (jobs, workspace pointers)
+// lives in shared memory, not in per-thread stacks.  The same kernel in forward mode
+// gives Q for a few rows (the act of the search loop).
 #include <algorithm>
 #include <cstdint>
 
@@ -75,6 +81,7 @@ struct Learn {
   float* ws;
   unsigned* bar;
   unsigned long long* trace;  // optional: %globaltimer after each phase (CTA 0)
+  int64_t gate;               // > 0: no-op while ctl[AP_CTL_SIZE] < gate (self-gated loop body)
 };
 
 __device__ __forceinline__ void trace_mark(unsigned long long* tr, int& k) {
@@ -636,6 +643,7 @@ __device__ __forceinline__ AOp rows_of(const float* p, int64_t sr) {
 __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const __grid_constant__ Learn P) {
   extern __shared__ float smem[];
   __shared__ Frame F;
+  if (P.gate > 0 && P.ctl[AP_CTL_SIZE] < P.gate) return;  // every CTA alike: no barrier is entered
   int tk = 0;
 #ifdef AP_FUSED_TILE_TRACE
   if (blockIdx.x == 0 && threadIdx.x == 0) g_tile_trace = P.trace, g_tile_n = 0;
@@ -1066,6 +1074,7 @@ int ap_dqn_learn_fused(const ap_fused_learn* a, void* stream) {
   P.ws = a->workspace;
   P.bar = a->barrier;
   P.trace = reinterpret_cast<unsigned long long*>(a->trace);
+  P.gate = a->ctl ? a->gate : 0;
   return launch(P, (cudaStream_t)stream);
 }
 

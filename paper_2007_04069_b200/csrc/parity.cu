@@ -196,6 +196,7 @@ __global__ void __launch_bounds__(kPostThreads) parity_post_kernel(ap_parity_loo
       L.dctl[AP_PLD_TOTAL] = 0.0;
     }
     L.ctl[AP_PL_STEP] = step + 1;
+    L.ctl[AP_PL_SYNC] = 0;  // raised by this step's learn tail when a target sync is due
     L.ctl[AP_CTL_SLOT] = (slot + 1) % L.cap;
     L.ctl[AP_CTL_SIZE] = size + 1 < L.cap ? size + 1 : L.cap;
   }
@@ -223,9 +224,13 @@ __global__ void __launch_bounds__(kPostThreads) parity_post_kernel(ap_parity_loo
 }
 
 // B random() draws for rng.choice's uniforms (agent.py:220)
+__device__ __forceinline__ bool learn_gated_off(const ap_parity_loop& L) {
+  return L.learn_gate > 0 && L.ctl[AP_CTL_SIZE] < L.learn_gate;
+}
+
 __global__ void parity_uniforms_kernel(ap_parity_loop L, int B, double* __restrict__ out) {
   pdl_entry();
-  if (threadIdx.x) return;
+  if (threadIdx.x || learn_gated_off(L)) return;
   NpPcg64 g = NpPcg64::load(L.rng);
   for (int b = 0; b < B; ++b) out[b] = g.next_double();
   g.store(L.rng);
@@ -234,7 +239,7 @@ __global__ void parity_uniforms_kernel(ap_parity_loop L, int B, double* __restri
 // loss log, train-step counter, target-sync flag (agent.py:325-337)
 __global__ void parity_learn_tail_kernel(ap_parity_loop L, const float* __restrict__ loss, int sync_every) {
   pdl_entry();
-  if (threadIdx.x) return;
+  if (threadIdx.x || learn_gated_off(L)) return;
   const int64_t t = L.ctl[AP_CTL_TRAIN];
   const int64_t k = t - L.ctl[AP_PL_TRAIN0];
   const float v = *loss;
@@ -365,7 +370,7 @@ int ap_pcg64_host_draws(uint64_t* state6, const int64_t* ops, int32_t n, double*
 }
 
 int ap_loop_graph_create(void* step_graph, void* learn_graph, const int64_t* ctl, int64_t batch, ap_loop_t* out) {
-  if (!step_graph || !learn_graph || !ctl || !out || batch < 1) {
+  if (!step_graph || !ctl || !out || batch < 1) {
     set_error("ap_loop_graph_create: bad arguments");
     return AP_ERR_INVALID;
   }
@@ -384,7 +389,8 @@ int ap_loop_graph_create(void* step_graph, void* learn_graph, const int64_t* ctl
   cudaGraphConditionalHandle h_loop, h_learn;
   if ((e = cudaGraphConditionalHandleCreate(&h_loop, lp->graph, 1, cudaGraphCondAssignDefault)) != cudaSuccess)
     return fail(e, "cudaGraphConditionalHandleCreate(loop)");
-  if ((e = cudaGraphConditionalHandleCreate(&h_learn, lp->graph, 0, cudaGraphCondAssignDefault)) != cudaSuccess)
+  if (learn_graph &&
+      (e = cudaGraphConditionalHandleCreate(&h_learn, lp->graph, 0, cudaGraphCondAssignDefault)) != cudaSuccess)
     return fail(e, "cudaGraphConditionalHandleCreate(learn)");
   cudaGraphNodeParams wp = {};
   wp.type = cudaGraphNodeTypeConditional;
@@ -397,27 +403,30 @@ int ap_loop_graph_create(void* step_graph, void* learn_graph, const int64_t* ctl
   cudaGraphNode_t n_step, n_lcond, n_if, n_cont;
   if ((e = cudaGraphAddChildGraphNode(&n_step, body, nullptr, 0, (cudaGraph_t)step_graph)) != cudaSuccess)
     return fail(e, "add step child graph");
-  {
-    cudaKernelNodeParams kp = {};
-    int64_t b = batch;
-    void* args[] = {&h_learn, (void*)&ctl, &b};
-    kp.func = (void*)loop_learn_cond_kernel;
-    kp.gridDim = dim3(1);
-    kp.blockDim = dim3(1);
-    kp.kernelParams = args;
-    if ((e = cudaGraphAddKernelNode(&n_lcond, body, &n_step, 1, &kp)) != cudaSuccess)
-      return fail(e, "add learn-condition kernel");
+  n_if = n_step;  // no learn graph: the step graph holds a self-gated learn body (learn_gate)
+  if (learn_graph) {
+    {
+      cudaKernelNodeParams kp = {};
+      int64_t b = batch;
+      void* args[] = {&h_learn, (void*)&ctl, &b};
+      kp.func = (void*)loop_learn_cond_kernel;
+      kp.gridDim = dim3(1);
+      kp.blockDim = dim3(1);
+      kp.kernelParams = args;
+      if ((e = cudaGraphAddKernelNode(&n_lcond, body, &n_step, 1, &kp)) != cudaSuccess)
+        return fail(e, "add learn-condition kernel");
+    }
+    cudaGraphNodeParams ip = {};
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = h_learn;
+    ip.conditional.type = cudaGraphCondTypeIf;
+    ip.conditional.size = 1;
+    if ((e = cudaGraphAddNode(&n_if, body, &n_lcond, 1, &ip)) != cudaSuccess) return fail(e, "add IF node");
+    cudaGraphNode_t n_learn;
+    if ((e = cudaGraphAddChildGraphNode(&n_learn, ip.conditional.phGraph_out[0], nullptr, 0,
+                                        (cudaGraph_t)learn_graph)) != cudaSuccess)
+      return fail(e, "add learn child graph");
   }
-  cudaGraphNodeParams ip = {};
-  ip.type = cudaGraphNodeTypeConditional;
-  ip.conditional.handle = h_learn;
-  ip.conditional.type = cudaGraphCondTypeIf;
-  ip.conditional.size = 1;
-  if ((e = cudaGraphAddNode(&n_if, body, &n_lcond, 1, &ip)) != cudaSuccess) return fail(e, "add IF node");
-  cudaGraphNode_t n_learn;
-  if ((e = cudaGraphAddChildGraphNode(&n_learn, ip.conditional.phGraph_out[0], nullptr, 0,
-                                      (cudaGraph_t)learn_graph)) != cudaSuccess)
-    return fail(e, "add learn child graph");
   {
     cudaKernelNodeParams kp = {};
     void* args[] = {&h_loop, (void*)&ctl};

@@ -19,7 +19,10 @@ runs on the GPU without returning to the host:
 
 The step and learn sequences are captured once as CUDA graphs and wrapped by
 `ap_loop_graph_create` in a graph with device-side control flow: WHILE
-(episodes < budget) { step; IF (ring holds a batch) { learn } }.  One graph
+(episodes < budget) { step; learn }, where the learn kernels (fused learner)
+skip themselves while the ring holds fewer than a batch (`learn_gate`), so the
+body is one graph with programmatic-dependent-launch edges; the GEMM learner
+keeps an IF (ring holds a batch) node around its learn graph instead.  One graph
 launch runs a whole block of episodes.  Afterwards the agent (RNG state, train
 steps, Adam step, ring) and the env are left exactly as the host loop leaves
 them, so host and device loops can be mixed (the finetune stage continues the
@@ -114,6 +117,10 @@ class DeviceSearch:
             ep_len=P(t["ep_len"]), ep_return=P(t["ep_return"]), loss_log=P(t["loss_log"]),
             loss_cap=steps_per_launch)
         self.adam_offset = agent.optimizer.t - agent.train_steps  # invariant: both advance per learn step
+        # the fused learner and the parity kernels gate themselves on the ring size; the GEMM
+        # learner runs under the loop graph's IF node
+        self.gated = agent.learner == "fused"
+        self.desc.learn_gate = cfg.batch_size if self.gated else 0
         self._capture()
 
     # -- capture ---------------------------------------------------------------------------
@@ -141,7 +148,8 @@ class DeviceSearch:
                                               _native.ptr(t["idx"]), _native.ptr(t["weights"]), _stream()))
         opt, net = agent.optimizer, agent.net
         if agent.learner == "fused":
-            loss = agent._fused.run(t["idx"], t["weights"], ctab=t["ctab"], ctl=t["ctl"], t_offset=self.adam_offset)
+            loss = agent._fused.run(t["idx"], t["weights"], ctab=t["ctab"], ctl=t["ctl"], t_offset=self.adam_offset,
+                                    gate=B if self.gated else 0)
             _native.check(lib.ap_parity_learn_tail(L, _native.ptr(loss), int(cfg.target_sync_every), _stream()))
             self._sync(lib)
             return
@@ -206,17 +214,26 @@ class DeviceSearch:
         import os
 
         pdl = os.environ.get("AP_NO_PDL")
-        os.environ["AP_NO_PDL"] = "1"  # plain edges inside the conditional bodies
+        if not self.gated:
+            os.environ["AP_NO_PDL"] = "1"  # plain edges inside the IF node's body
         try:
             with torch.cuda.stream(self.stream):
                 self._warm()
                 torch.cuda.current_stream().synchronize()
                 self.g_step = torch.cuda.CUDAGraph(keep_graph=True)
-                with torch.cuda.graph(self.g_step, stream=self.stream):
-                    self._step_body()
-                self.g_learn = torch.cuda.CUDAGraph(keep_graph=True)
-                with torch.cuda.graph(self.g_learn, stream=self.stream):
-                    self._learn_body()
+                if self.gated:
+                    # one body: the step, then the learn kernels, which skip themselves while the
+                    # ring holds fewer than a batch (no IF node, no condition kernel per step)
+                    with torch.cuda.graph(self.g_step, stream=self.stream):
+                        self._step_body()
+                        self._learn_body()
+                    self.g_learn = None
+                else:
+                    with torch.cuda.graph(self.g_step, stream=self.stream):
+                        self._step_body()
+                    self.g_learn = torch.cuda.CUDAGraph(keep_graph=True)
+                    with torch.cuda.graph(self.g_learn, stream=self.stream):
+                        self._learn_body()
         finally:
             if pdl is None:
                 os.environ.pop("AP_NO_PDL", None)
@@ -225,7 +242,8 @@ class DeviceSearch:
         torch.cuda.current_stream().wait_stream(self.stream)
         h = ctypes.c_void_p()
         _native.check(_native.require_device().ap_loop_graph_create(
-            ctypes.c_void_p(self.g_step.raw_cuda_graph()), ctypes.c_void_p(self.g_learn.raw_cuda_graph()),
+            ctypes.c_void_p(self.g_step.raw_cuda_graph()),
+            ctypes.c_void_p(None if self.g_learn is None else self.g_learn.raw_cuda_graph()),
             _native.ptr(self.t["ctl"]), int(self.agent.config.batch_size), ctypes.byref(h)))
         self.loop = h
 
