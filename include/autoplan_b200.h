@@ -560,6 +560,11 @@ enum {
   AP_PL_TRAIN0 = 14,    /* train steps before the run (loss log base) */
   AP_PL_LOSS_BAD = 15,  /* first run-relative train step with a non-finite loss, or -1 */
   AP_PL_TAB_BASE = 16,  /* Adam step t of bias-correction table entry 0, minus 1 */
+  AP_PL_ACTIVE = 17,    /* set by the act of each step: 0 once the budget is spent (the loop body's
+                           later kernels then do nothing: several steps per WHILE iteration) */
+  AP_PL_GEN = 18,       /* env steps ever taken by this loop state (advanced by env.step) */
+  AP_PL_ACK = 19,       /* GEN + 1 once the step's early PER sample has read the ring and stream */
+  AP_PL_FAULT = 20,     /* nonzero: a device-side wait gave up (the loop's results are void) */
   AP_PL_WORDS = 32
 };
 enum { AP_PLD_TOTAL = 0, AP_PLD_BEST_REWARD = 1, AP_PLD_WORDS = 2 };
@@ -601,6 +606,13 @@ typedef struct ap_parity_loop {
   int64_t loss_cap;
   int64_t learn_gate;       /* > 0: the learn-body kernels do nothing while the ring holds fewer
                                rows (a loop graph without the IF node); 0: ungated */
+  double* r_scaled;         /* early_sample: [cap] priorities ** per_alpha, kept current by env.step
+                               and the fused learn step (the early PER sample reads it) */
+  double* pstat;            /* early_sample: [2] the ring's max priority and its ** per_alpha */
+  double per_alpha;
+  int64_t early_sample;     /* 1: each step's PER sample runs beside its act / env kernels
+                               (ap_parity_sample early mode); the act then waits for its ack
+                               before it advances the random stream */
 } ap_parity_loop;
 
 /* agent.act: eps-greedy with numpy's draws (random(), integers(A)) over Q of the
@@ -609,18 +621,26 @@ int ap_parity_act(const ap_parity_loop* L, const float* q_dev, int32_t* action_d
 /* env.step after K1 + episode bookkeeping + agent.observe (ring push at the
  * current max priority) + reset to the template after a finished episode. */
 int ap_parity_post(const ap_parity_loop* L, const int32_t* action_dev, void* stream);
-/* B random() draws (the uniforms of rng.choice in PER sampling). */
-int ap_parity_uniforms(const ap_parity_loop* L, int32_t B, double* out_dev, void* stream);
+/* agent.learn's B random() draws (the uniforms of rng.choice) and the PER sample of the ring
+ * (agent.py:207-223), one kernel: indices [B], importance weights [B]; scratch holds 2 * cap + B
+ * doubles; uniforms_out optional.  No-op while the loop's learn gate is closed.  1 <= B <= 1024.
+ * Late mode (early == 0, after env.step): the pushed ring, the act's random stream, which it
+ * advances.  Early mode (launched with the act of the step, L->early_sample): the ring and stream
+ * as the step starts -- it replays the act's draws (random(), integers(A) when exploring),
+ * counts the step's pending push (max priority at the current slot), acknowledges its read in
+ * ctl[AP_PL_ACK] and leaves the final stream state in rng_next (6 words) for the learn step to
+ * commit (ap_fused_learn.rng_from). */
+int ap_parity_sample(const ap_parity_loop* L, int32_t B, double alpha, double beta, double* scratch,
+                     int32_t* indices, float* weights, double* uniforms_out, uint64_t* rng_next, int32_t early,
+                     void* stream);
 /* loss log, train-step counter, target-sync flag. */
 int ap_parity_learn_tail(const ap_parity_loop* L, const float* loss_dev, int32_t sync_every, void* stream);
+/* scaled[i] = priorities[i] ** alpha for i < n (the PER sample's cache, CUDA pow as everywhere)
+ * and, with pstat, pstat = {max priority (1.0 for n == 0), its ** alpha}. */
+int ap_per_scaled(const double* priorities, int64_t n, double alpha, double* scaled, double* pstat, void* stream);
 /* dst[k][:count[k]] = src[k][...] when ctl[AP_PL_SYNC] (n <= 8 segments). */
 int ap_parity_target_sync(const int64_t* ctl, int32_t n, const float* const* src, float* const* dst,
                           const int64_t* count, void* stream);
-/* ap_per_sample over the first ctl[AP_CTL_SIZE] priorities (device-held ring
- * size); scratch holds 2 * capacity + B doubles. */
-int ap_per_sample_n_ctl(const double* priorities, const int64_t* ctl, int64_t capacity, double alpha, double beta,
-                        const double* uniforms, int32_t B, double* scratch, int32_t* indices, float* weights,
-                        void* stream);
 /* ap_dqn_adam with the bias corrections of step t = ctl[AP_CTL_TRAIN] + t_offset + 1
  * read from a host-computed table: ctab[2 * k + {0, 1}] = fp32(1 - beta{1,2}^t)
  * for k = t - 1 - ctl[AP_PL_TAB_BASE] (the host's `1.0 - beta ** t`, agent.py:241-242). */
@@ -675,6 +695,24 @@ typedef struct ap_fused_learn {
   uint32_t* barrier;        /* [2] zero-initialised, private to the caller's stream */
   uint64_t* trace;          /* optional [16]: %globaltimer after each phase (profiling) */
   int64_t gate;             /* > 0 (with ctl): no-op while ctl[AP_CTL_SIZE] < gate */
+  /* optional parity-loop tail (replaces ap_parity_learn_tail + ap_parity_target_sync):
+   * with tail_ctl, after the update the kernel logs the loss at loss_log[t - ctl[AP_PL_TRAIN0]]
+   * (t = ctl[AP_CTL_TRAIN]), records the first non-finite loss in ctl[AP_PL_LOSS_BAD],
+   * advances ctl[AP_CTL_TRAIN], and when (t + 1) % sync_every == 0 copies
+   * sync_src[k][:sync_count[k]] -> sync_dst[k] (the target sync, agent.py:142-144, 335-337) */
+  int64_t* tail_ctl;
+  float* loss_log;
+  int64_t loss_cap;
+  int32_t sync_every;
+  int32_t sync_n;           /* <= 6 segments */
+  const float* sync_src[6];
+  float* sync_dst[6];
+  int64_t sync_count[6];
+  double* r_scaled;         /* optional [cap]: r_scaled[idx] = (|td| + 1e-6) ** per_alpha with each priority */
+  double* pstat;            /* with r_scaled: [2] the ring's max priority after the update, its ** per_alpha */
+  double per_alpha;
+  const uint64_t* rng_from; /* optional (tail mode): copied to rng_to (6 words) when the step learns */
+  uint64_t* rng_to;
 } ap_fused_learn;
 
 int64_t ap_mlp_fused_workspace(int32_t L, const int32_t* dims, int32_t rows, int32_t forward_only);
@@ -684,6 +722,13 @@ int ap_dqn_learn_fused(const ap_fused_learn* args, void* stream);
 int ap_mlp_forward_fused(int32_t L, const int32_t* dims, const int64_t* w_off, const int64_t* b_off,
                          const float* params, const float* x, int64_t ldx, int32_t rows, float* q,
                          float* workspace, uint32_t* barrier, void* stream);
+
+/* agent.act of the parity loop in one launch: Q of the loop's state row (the fused forward,
+ * which for <= 4 rows and <= 7 actions splits every layer's K over the grid) and the
+ * epsilon-greedy decision of ap_parity_act on it (params: the online network). */
+int ap_parity_act_fused(const ap_parity_loop* L, int32_t hidden_layers, const int32_t* dims, const int64_t* w_off,
+                        const int64_t* b_off, const float* params, float* q_dev, float* workspace,
+                        uint32_t* barrier, int32_t* action_dev, void* stream);
 
 typedef struct ap_loop* ap_loop_t;
 /* Outer graph: WHILE(episodes < budget && steps < max_steps) { step_graph;

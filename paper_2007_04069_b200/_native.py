@@ -114,7 +114,9 @@ class ParityLoopDesc(ctypes.Structure):
         ("log_pos", ctypes.c_void_p), ("log_decided", ctypes.c_void_p), ("ep_conflict", ctypes.c_void_p),
         ("ep_len", ctypes.c_void_p), ("ep_return", ctypes.c_void_p), ("loss_log", ctypes.c_void_p),
         ("loss_cap", ctypes.c_int64),
-        ("learn_gate", ctypes.c_int64),
+        ("learn_gate", ctypes.c_int64), ("r_scaled", ctypes.c_void_p), ("pstat", ctypes.c_void_p),
+        ("per_alpha", ctypes.c_double),
+        ("early_sample", ctypes.c_int64),
     ]
 
 
@@ -139,10 +141,15 @@ class FusedLearnDesc(ctypes.Structure):
         ("loss", ctypes.c_void_p), ("workspace", ctypes.c_void_p), ("barrier", ctypes.c_void_p),
         ("trace", ctypes.c_void_p),
         ("gate", ctypes.c_int64),
+        ("tail_ctl", ctypes.c_void_p), ("loss_log", ctypes.c_void_p), ("loss_cap", ctypes.c_int64),
+        ("sync_every", ctypes.c_int32), ("sync_n", ctypes.c_int32), ("sync_src", ctypes.c_void_p * 6),
+        ("sync_dst", ctypes.c_void_p * 6), ("sync_count", ctypes.c_int64 * 6),
+        ("r_scaled", ctypes.c_void_p), ("pstat", ctypes.c_void_p), ("per_alpha", ctypes.c_double),
+        ("rng_from", ctypes.c_void_p), ("rng_to", ctypes.c_void_p),
     ]
 PL = {"STEP": 0, "SLOT": 1, "SIZE": 2, "TRAIN": 3, "EPISODES": 4, "BUDGET": 5, "MAX_STEPS": 6, "POS": 7,
       "EP_STEPS": 8, "BEST_PART": 9, "BEST_EP": 10, "SYNC": 11, "T_POS": 12, "EP_BASE": 13, "TRAIN0": 14,
-      "LOSS_BAD": 15, "TAB_BASE": 16, "WORDS": 32}
+      "LOSS_BAD": 15, "TAB_BASE": 16, "ACTIVE": 17, "GEN": 18, "ACK": 19, "FAULT": 20, "WORDS": 32}
 SIGNATURES: dict[str, tuple] = {
     "ap_graph_create": (ctypes.c_int, [ctypes.POINTER(GraphDesc), ctypes.POINTER(_VP)]),
     "ap_graph_destroy": (ctypes.c_int, [_VP]),
@@ -154,10 +161,11 @@ SIGNATURES: dict[str, tuple] = {
     "ap_propagate_batch_packed": (ctypes.c_int, [_VP, _VP, _VP, _I64, _I64, _VP, _I64, _VP, _I64, _VP, _VP, _VP]),
     "ap_parity_act": (ctypes.c_int, [_PL, _VP, _VP, _VP]),
     "ap_parity_post": (ctypes.c_int, [_PL, _VP, _VP]),
-    "ap_parity_uniforms": (ctypes.c_int, [_PL, _I32, _VP, _VP]),
+    "ap_parity_act_fused": (ctypes.c_int, [_PL, _I32, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "ap_parity_sample": (ctypes.c_int, [_PL, _I32, _F64, _F64, _VP, _VP, _VP, _VP, _VP, _I32, _VP]),
     "ap_parity_learn_tail": (ctypes.c_int, [_PL, _VP, _I32, _VP]),
+    "ap_per_scaled": (ctypes.c_int, [_VP, _I64, _F64, _VP, _VP, _VP]),
     "ap_parity_target_sync": (ctypes.c_int, [_VP, _I32, _VP, _VP, _VP, _VP]),
-    "ap_per_sample_n_ctl": (ctypes.c_int, [_VP, _VP, _I64, _F64, _F64, _VP, _I32, _VP, _VP, _VP, _VP]),
     "ap_dqn_adam_tab": (ctypes.c_int, [_VP, _VP, _VP, _VP, _I64, _F32, _F32, _F32, _F32, _VP, _VP, _I64, _VP]),
     "ap_loop_graph_create": (ctypes.c_int, [_VP, _VP, _VP, _I64, ctypes.POINTER(_VP)]),
     "ap_loop_graph_launch": (ctypes.c_int, [_VP, _VP]),
@@ -248,9 +256,11 @@ _lib = None
 _lock = threading.Lock()
 
 
-def load_library(path: Path | str = LIB_PATH):
-    """Load the engine library and bind its C-ABI signatures (no GPU needed)."""
+def load_library(path: Path | str | None = None):
+    """Load the engine library and bind its C-ABI signatures (no GPU needed).  AP_LIB_PATH
+    names another build of the same library (profiling variants)."""
     global _lib
+    path = path or os.environ.get("AP_LIB_PATH") or LIB_PATH
     with _lock:
         if _lib is None:
             if not Path(path).exists():

@@ -728,7 +728,11 @@ class FusedLearnState:
             beta1=optimizer.beta1, beta2=optimizer.beta2, eps=optimizer.eps, wt=wt, wt_ld=wt_ld, td=P(self.td),
             loss=P(self.loss), workspace=P(self.ws), barrier=P(self.bar))
 
-    def run(self, idx, weights, correct1=1.0, correct2=1.0, ctab=None, ctl=None, t_offset=0, gate=0):
+    def run(self, idx, weights, correct1=1.0, correct2=1.0, ctab=None, ctl=None, t_offset=0, gate=0, tail=None,
+            scaled=None, pstat=None, alpha=0.0):
+        """One learn step.  `tail` (parity loop): (loss_log, loss_cap, sync_every, [(src, dst, count)]
+        [, (rng_from, rng_to)]) -- the kernel also logs the loss, advances ctl's train counter,
+        syncs the target and commits the early PER sample's random-stream state."""
         import ctypes
 
         d = self.desc
@@ -738,6 +742,21 @@ class FusedLearnState:
         d.ctl = None if ctl is None else ctl.data_ptr()
         d.t_offset = int(t_offset)
         d.gate = int(gate)
+        # optional priorities ** alpha cache kept current with each new priority (the device loop's PER sample)
+        d.r_scaled, d.per_alpha = (None, 0.0) if scaled is None else (scaled.data_ptr(), float(alpha))
+        d.pstat = None if pstat is None else pstat.data_ptr()
+        if tail is None:
+            d.tail_ctl = None
+        else:
+            loss_log, loss_cap, sync_every, segs = tail[:4]
+            rng = tail[4] if len(tail) > 4 else None
+            d.rng_from, d.rng_to = (None, None) if rng is None else (rng[0].data_ptr(), rng[1].data_ptr())
+            if len(segs) > 6:
+                raise ValueError("at most 6 target-sync segments")
+            d.tail_ctl = d.ctl
+            d.loss_log, d.loss_cap, d.sync_every, d.sync_n = loss_log.data_ptr(), int(loss_cap), int(sync_every), len(segs)
+            for k, (src, dst, cnt) in enumerate(segs):
+                d.sync_src[k], d.sync_dst[k], d.sync_count[k] = src, dst, cnt
         _native.check(_native.require_device().ap_dqn_learn_fused(ctypes.byref(d), _stream()))
         return self.loss
 

@@ -18,6 +18,7 @@
 #include <cstdlib>
 
 #include "engine.h"
+#include "per_sample.cuh"
 
 namespace apb {
 
@@ -696,118 +697,15 @@ __global__ void adam_t_kernel(float* p, const float* g, float* m, float* v, int6
   }
 }
 
-// numpy pairwise summation of a block of <= 128 doubles
-// (numpy/_core/src/umath/loops_utils.h.src, PW_BLOCKSIZE = 128)
-__device__ double pairwise_leaf(const double* x, int64_t m) {
-  if (m < 8) {
-    double v = -0.0;  // numpy starts from -0.0 to preserve -0.0 sums
-    for (int64_t i = 0; i < m; ++i) v += x[i];
-    return v;
-  }
-  double r[8];
-  for (int k = 0; k < 8; ++k) r[k] = x[k];
-  int64_t i;
-  for (i = 8; i < m - (m % 8); i += 8)
-    for (int k = 0; k < 8; ++k) r[k] += x[i + k];
-  double v = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-  for (; i < m; ++i) v += x[i];
-  return v;
-}
-
-// the recursion sum(a, n) = sum(a, n2) + sum(a + n2, n - n2), n2 = n/2 rounded
-// down to a multiple of 8, evaluated with an explicit post-order stack
-__device__ double pairwise_sum(const double* a, int64_t n) {
-  struct Frame {
-    int64_t off, n;
-    int state;
-    double left;
-  };
-  Frame fr[64];
-  int top = 0;
-  fr[0] = {0, n, 0, 0.0};
-  double ret = 0.0;
-  while (top >= 0) {
-    Frame& f = fr[top];
-    if (f.n <= 128) {
-      ret = pairwise_leaf(a + f.off, f.n);
-      --top;
-      continue;
-    }
-    int64_t n2 = f.n / 2;
-    n2 -= n2 % 8;
-    if (f.state == 0) {
-      f.state = 1;
-      fr[top + 1] = {f.off, n2, 0, 0.0};
-      ++top;
-    } else if (f.state == 1) {
-      f.left = ret;
-      f.state = 2;
-      fr[top + 1] = {f.off + n2, f.n - n2, 0, 0.0};
-      ++top;
-    } else {
-      ret = f.left + ret;
-      --top;
-    }
-  }
-  return ret;
-}
-
-// one CTA: PER sample (agent.py:207-223) for B uniforms drawn by the caller
-__global__ void per_sample_kernel(const double* prio, int n, double alpha, double beta, const double* uniforms, int B,
-                                  double* scaled, double* cdf, int32_t* idx_out, float* w_out,
-                                  const int64_t* ctl) {
+// one CTA: PER sample (agent.py:207-223) for B uniforms drawn by the caller (per_sample.cuh)
+__global__ void __launch_bounds__(512) per_sample_kernel(const double* prio, int n, double alpha, double beta,
+                                                         const double* uniforms, int B, double* scaled, double* cdf,
+                                                         int32_t* idx_out, float* w_out, const int64_t* ctl) {
   pdl_entry();
   if (ctl) n = (int)ctl[AP_CTL_SIZE];  // device-held ring size (parity loop)
   if (ctl && n < B) return;            // no learn step yet (self-gated loop body)
-  __shared__ double s_total, s_last, s_wmax;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) scaled[i] = pow(prio[i], alpha);
-  __syncthreads();
-  if (threadIdx.x == 0) s_total = pairwise_sum(scaled, n);
-  __syncthreads();
-  // probs = scaled / total (independent divisions, in parallel); cdf = probs.cumsum() (one
-  // sequential chain of adds, numpy's order); cdf /= cdf[-1]
-  for (int i = threadIdx.x; i < n; i += blockDim.x) cdf[i] = scaled[i] / s_total;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double acc = cdf[0];
-    for (int i = 1; i < n; ++i) {
-      acc = acc + cdf[i];
-      cdf[i] = acc;
-    }
-    s_last = acc;
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) cdf[i] = cdf[i] / s_last;
-  __syncthreads();
-  double wloc = 0.0;
-  for (int b = threadIdx.x; b < B; b += blockDim.x) {
-    const double u = uniforms[b];
-    int lo = 0, hi = n;  // first index with cdf > u (searchsorted side='right')
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (cdf[mid] <= u)
-        lo = mid + 1;
-      else
-        hi = mid;
-    }
-    idx_out[b] = lo;
-    const double p = scaled[lo] / s_total;
-    const double w = pow((double)n * p, -beta);
-    cdf[n + b] = w;
-    wloc = fmax(wloc, w);
-  }
-  // max over B weights
-  __shared__ double s_w[32];
-  for (int o = 16; o; o >>= 1) wloc = fmax(wloc, __shfl_xor_sync(kFull, wloc, o));
-  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = wloc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double m = 0.0;
-    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) m = fmax(m, s_w[k]);
-    s_wmax = m;
-  }
-  __syncthreads();
-  for (int b = threadIdx.x; b < B; b += blockDim.x) w_out[b] = (float)(cdf[n + b] / s_wmax);
+  __shared__ PerShared S;
+  per_sample_block(prio, n, alpha, beta, uniforms, B, scaled, cdf, idx_out, w_out, S);
 }
 
 // priorities[idx] = |td| + 1e-6, duplicates: the last occurrence wins (agent.py:226)
@@ -1157,22 +1055,8 @@ int ap_per_sample(const double* priorities, int32_t n, double alpha, double beta
     return AP_ERR_INVALID;
   }
   // scratch: [n] scaled + [n + B] cdf / weights
-  launch_pdl(per_sample_kernel, dim3(1), dim3(256), 0, (cudaStream_t)stream, priorities, n, alpha, beta, uniforms, B, scratch,
+  launch_pdl(per_sample_kernel, dim3(1), dim3(512), 0, (cudaStream_t)stream, priorities, n, alpha, beta, uniforms, B, scratch,
                                                          scratch + n, indices, weights, (const int64_t*)nullptr);
-  AP_CUDA_CHECK(cudaGetLastError());
-  return AP_OK;
-}
-
-int ap_per_sample_n_ctl(const double* priorities, const int64_t* ctl, int64_t capacity, double alpha, double beta,
-                        const double* uniforms, int32_t B, double* scratch, int32_t* indices, float* weights,
-                        void* stream) {
-  if (!priorities || !ctl || !uniforms || !scratch || !indices || !weights || B < 1 || capacity < 1) {
-    set_error("ap_per_sample_n_ctl: bad arguments");
-    return AP_ERR_INVALID;
-  }
-  // scratch: [capacity] scaled priorities, then [capacity + B] cdf / weights
-  launch_pdl(per_sample_kernel, dim3(1), dim3(256), 0, (cudaStream_t)stream, priorities, 0, alpha, beta, uniforms, B,
-             scratch, scratch + capacity, indices, weights, (const int64_t*)ctl);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }

@@ -32,6 +32,7 @@
 #include <cstdint>
 
 #include "engine.h"
+#include "parity_act.cuh"
 
 namespace apb {
 namespace {
@@ -82,6 +83,23 @@ struct Learn {
   unsigned* bar;
   unsigned long long* trace;  // optional: %globaltimer after each phase (CTA 0)
   int64_t gate;               // > 0: no-op while ctl[AP_CTL_SIZE] < gate (self-gated loop body)
+  // forward mode, parity loop: the epsilon-greedy act on row 0's Q (parity_act.cuh)
+  int act;
+  ap_parity_loop pl;
+  int32_t* action;
+  // parity-loop tail: loss log, train counter, target sync (see ap_fused_learn)
+  int64_t* tail_ctl;
+  float* loss_log;
+  int64_t loss_cap;
+  int sync_every, sync_n;
+  const float* sync_src[6];
+  float* sync_dst[6];
+  int64_t sync_count[6];
+  double* r_scaled;          // optional: priorities ** alpha, updated with each priority
+  double* pstat;             // with r_scaled: the ring's max priority after the update, its ** alpha
+  double alpha;
+  const uint64_t* rng_from;  // parity loop, early PER sample: the stream state to commit
+  uint64_t* rng_to;
 };
 
 __device__ __forceinline__ void trace_mark(unsigned long long* tr, int& k) {
@@ -550,7 +568,7 @@ __device__ __forceinline__ void head_row(const float* hr, int H, int A1, const f
 // registers: forward mode writes Q; learn mode runs the double-DQN TD of sample b.
 template <int A1M>
 __device__ __noinline__ void small_head_row(const Learn& P, int r, int B, const float* HonL, const float* HtgL,
-                                            float* dz, float* lrow, bool fwd_only) {
+                                            float* dz, float* lrow, float* dhL, bool fwd_only) {
   const int lane = threadIdx.x & 31;
   const int L = P.L, A = P.A, A1 = A + 1, H = P.d[L];
   const float* w_on = P.p + P.w_off[L];
@@ -616,11 +634,146 @@ __device__ __noinline__ void small_head_row(const Learn& P, int r, int B, const 
   const float hub = ad <= P.delta ? 0.5f * tdv * tdv : P.delta * (ad - 0.5f * P.delta);
   const float g = w * fminf(fmaxf(tdv, -P.delta), P.delta) / (float)B;
   if (lane <= A) dz[(int64_t)b * A1 + lane] = lane == 0 ? g : ((lane - 1) == a ? g : 0.0f) - g / (float)A;
+  // the head's dgrad for this row, dh_L[b] = relu'(H_L(cur)[b]) * (dz[b] Wh^T): K = 1 + A is tiny,
+  // so the row's warp does it here (one fma chain per output, k ascending) instead of a phase
+  // of its own; Wh is still the pre-update head (its Adam runs in the next phase)
+  {
+    float dzk[A1M];
+#pragma unroll
+    for (int k = 0; k < A1M; ++k) dzk[k] = k == 0 ? g : ((k - 1) == a ? g : 0.0f) - g / (float)A;
+    const float* hc = HonL + (int64_t)(B + b) * H;
+    float* out = dhL + (int64_t)b * H;
+    for (int n = lane; n < H; n += 32) {
+      const float* wrow = w_on + (int64_t)n * A1;
+      float acc = 0.0f;
+#pragma unroll
+      for (int k = 0; k < A1M; ++k)
+        if (k < A1) acc = fmaf(dzk[k], __ldcg(wrow + k), acc);
+      const float v = acc + 0.0f;
+      out[n] = __ldcg(hc + n) > 0.0f ? v : 0.0f;
+    }
+  }
   later = __any_sync(0xffffffffu, later);
   if (lane == 0) {
     P.td[b] = tdv;
     lrow[b] = w * hub;
-    if (!later) P.r_prio[row] = fabs((double)tdv) + 1e-6;
+    if (!later) {
+      const double pr = fabs((double)tdv) + 1e-6;
+      P.r_prio[row] = pr;
+      if (P.r_scaled) P.r_scaled[row] = pow(pr, P.alpha);
+    }
+  }
+}
+
+// ---- forward of a few rows (the act of the search loop) --------------------------------
+// One row x [1060] through 256-wide layers is ~0.3 MFLOP: the cost is latency.  Every layer's
+// K is split over the grid so each CTA reads a few KB of weights: work item (column tile of
+// 32, K-chunk) sums its chunk (8 warps split it, fma chains k ascending, warps added in order)
+// into a partial row of the workspace; the consumer of the layer's output adds the chunks in
+// chunk order, then bias and relu.  The split is planned against a 144-CTA reference grid,
+// so every sum's order is a function of the network alone.  The head (<= 8 outputs) runs in
+// one warp per row as in the learn step.
+constexpr int kSmallRows = 4;
+
+struct Split {
+  int nt, ks, kc;  // column tiles, K-chunks, chunk length
+};
+
+__host__ __device__ __forceinline__ Split split_of(int K, int N) {
+  constexpr int kRefGrid = 144;  // <= the SMs a launch that leaves one free for the sampler has
+  Split sp;
+  sp.nt = (N + kTN - 1) / kTN;
+  int ks = max(1, kRefGrid / sp.nt);
+  ks = min(ks, (K + 7) / 8);  // chunks of >= 8
+  sp.kc = (K + ks - 1) / ks;
+  sp.ks = (K + sp.kc - 1) / sp.kc;
+  return sp;
+}
+
+// element (r, k) of layer i's input: the state row (i = 0), else relu(sum of layer i-1's
+// chunk partials in chunk order + bias)
+__device__ __forceinline__ float small_input(const Learn& P, int i, const float* part_prev, int ks_prev, int R, int r,
+                                             int k) {
+  if (i == 0) return __ldcg(P.x_in + (int64_t)r * P.x_ld + k);
+  const int N = P.d[i];
+  float v = __ldcg(part_prev + (int64_t)r * N + k);
+  for (int q = 1; q < ks_prev; ++q) v += __ldcg(part_prev + ((int64_t)q * R + r) * N + k);
+  return fmaxf(v + __ldcg(P.p + P.b_off[i - 1] + k), 0.0f);
+}
+
+template <int R>
+__device__ __noinline__ void small_forward(const Learn& P, float* smem) {
+  const int L = P.L, A1 = P.A + 1;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  float* red = smem;  // [kWarps][R][32]
+  if (P.act && blockIdx.x == gridDim.x - 1) parity_act_rows(P.pl);  // ordered before the decision by the barriers
+  const float* part_prev = nullptr;
+  int ks_prev = 0;
+  int64_t off = 0;
+  for (int i = 0; i < L; ++i) {
+    const int K = P.d[i], N = P.d[i + 1];
+    const Split sp = split_of(K, N);
+    float* part = P.ws + off;  // [ks][R][N]
+    const float* W = P.p + P.w_off[i];
+    for (int item = blockIdx.x; item < sp.nt * sp.ks; item += gridDim.x) {
+      const int ct = item % sp.nt, kq = item / sp.nt;
+      const int n = ct * kTN + lane;
+      const int k0 = kq * sp.kc, k1 = min(K, k0 + sp.kc);
+      const int kw = (k1 - k0 + kWarps - 1) / kWarps;
+      const int wk0 = min(k1, k0 + warp * kw), wk1 = min(k1, wk0 + kw);
+      float acc[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] = 0.0f;
+      for (int kb = wk0; kb < wk1; kb += 32) {
+        const int cnt = min(32, wk1 - kb);
+        float x[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) x[r] = lane < cnt ? small_input(P, i, part_prev, ks_prev, R, r, kb + lane) : 0.0f;
+        float w[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) w[u] = (u < cnt && n < N) ? __ldcg(W + (int64_t)(kb + u) * N + n) : 0.0f;
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+          if (u >= cnt) break;
+#pragma unroll
+          for (int r = 0; r < R; ++r) acc[r] = fmaf(__shfl_sync(0xffffffffu, x[r], u), w[u], acc[r]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) red[(warp * R + r) * kTN + lane] = acc[r];
+      __syncthreads();
+      if (warp == 0 && n < N) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          float v = red[r * kTN + lane];
+          for (int w2 = 1; w2 < kWarps; ++w2) v += red[(w2 * R + r) * kTN + lane];
+          part[((int64_t)kq * R + r) * N + n] = v;
+        }
+      }
+      __syncthreads();
+    }
+    grid_sync(P.bar);
+    part_prev = part;
+    ks_prev = sp.ks;
+    off += (int64_t)sp.ks * R * N;
+  }
+  if (blockIdx.x != 0) return;
+  // the last hidden layer's rows, then the head and Q (one warp per row)
+  const int H = P.d[L];
+  float* hl = P.ws + off;  // [R][H]
+  for (int e = tid; e < R * H; e += kThreads) hl[e] = small_input(P, L, part_prev, ks_prev, R, e / H, e % H);
+  __syncthreads();
+  if (warp < R) {
+    if (A1 <= 3)
+      small_head_row<3>(P, warp, R, hl, nullptr, nullptr, nullptr, nullptr, true);
+    else
+      small_head_row<8>(P, warp, R, hl, nullptr, nullptr, nullptr, nullptr, true);
+  }
+  if (!P.act) return;
+  __syncthreads();
+  if (tid == 0) {
+    parity_step_begin(P.pl, false, true);  // active; slot / size before the push
+    parity_act_decide(P.pl, P.q_out, P.action);
   }
 }
 
@@ -628,7 +781,7 @@ __device__ __noinline__ void small_head_row(const Learn& P, int r, int B, const 
 // workspace pointers.  (As per-thread locals these were 2 KB of stack per thread, 0.5 MB per
 // CTA, far past the L1 left beside 224 KB of shared memory: every phase setup went to L2.)
 struct Frame {
-  Job jobs[2];
+  Job jobs[3];
   int nj;
   float* Hon[kMaxLayers + 1];
   float* Htg[kMaxLayers + 1];
@@ -643,7 +796,22 @@ __device__ __forceinline__ AOp rows_of(const float* p, int64_t sr) {
 __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const __grid_constant__ Learn P) {
   extern __shared__ float smem[];
   __shared__ Frame F;
-  if (P.gate > 0 && P.ctl[AP_CTL_SIZE] < P.gate) return;  // every CTA alike: no barrier is entered
+  // every CTA alike (no barrier is entered): the self-gated loop body's learn waits for a full
+  // batch in the ring and stops with the loop (act of the step saw the budget spent)
+  if (P.gate > 0 && (P.ctl[AP_CTL_SIZE] < P.gate || !P.ctl[AP_PL_ACTIVE])) return;
+  if (P.act) {
+    // every CTA decides alike from words nobody writes during the act; CTA 0 records it
+    // after the first grid barrier (all reads are done by then)
+    const bool active = parity_step_begin(P.pl, true, false);
+    if (!active) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) P.pl.ctl[AP_PL_ACTIVE] = 0;
+      return;
+    }
+  }
+  // this learn step's train counter, read by every CTA before the first grid barrier (CTA 0
+  // advances it at the end, in parity-tail mode)
+  const int64_t t_train = P.ctl ? P.ctl[AP_CTL_TRAIN] : 0;
+  if (P.rng_from && blockIdx.x == 0 && threadIdx.x < 6) P.rng_to[threadIdx.x] = P.rng_from[threadIdx.x];
   int tk = 0;
 #ifdef AP_FUSED_TILE_TRACE
   if (blockIdx.x == 0 && threadIdx.x == 0) g_tile_trace = P.trace, g_tile_n = 0;
@@ -654,6 +822,15 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const __grid_con
   const int B = fwd_only ? P.rows_fwd : P.B;
   const int Ron = fwd_only ? B : 2 * B;  // online rows: [next; cur]
   const bool t0 = threadIdx.x == 0;
+  if (fwd_only && B <= kSmallRows && A1 <= 8) {
+    switch (B) {
+      case 1: small_forward<1>(P, smem); break;
+      case 2: small_forward<2>(P, smem); break;
+      case 3: small_forward<3>(P, smem); break;
+      default: small_forward<4>(P, smem); break;
+    }
+    return;
+  }
   if (t0) {
     // workspace: online activations [Ron, d_i], target activations [B, d_i] (i = 1..L),
     // head outputs, dz, dh_i [B, d_i], the per-row loss terms
@@ -753,9 +930,9 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const __grid_con
     for (int r = gw; r < (fwd_only ? Ron : B); r += nw) {
       if (small_head) {
         if (A1 <= 3)
-          small_head_row<3>(P, r, B, HonL, HtgL, dz, F.lrow, fwd_only);
+          small_head_row<3>(P, r, B, HonL, HtgL, dz, F.lrow, F.dh[L], fwd_only);
         else
-          small_head_row<8>(P, r, B, HonL, HtgL, dz, F.lrow, fwd_only);
+          small_head_row<8>(P, r, B, HonL, HtgL, dz, F.lrow, F.dh[L], fwd_only);
         continue;
       }
       if (fwd_only) {
@@ -822,7 +999,11 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const __grid_con
       if (lane == 0) {
         P.td[b] = tdv;
         F.lrow[b] = w * hub;
-        if (!later) P.r_prio[row] = fabs((double)tdv) + 1e-6;
+        if (!later) {
+      const double pr = fabs((double)tdv) + 1e-6;
+      P.r_prio[row] = pr;
+      if (P.r_scaled) P.r_scaled[row] = pow(pr, P.alpha);
+    }
       }
     }
   }
@@ -830,6 +1011,25 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const __grid_con
   trace_arrive(P.trace, tk);
   grid_sync(P.bar);
   trace_mark(P.trace, tk);
+  if (P.pstat && blockIdx.x == gridDim.x - 1) {
+    // the ring's max priority after this step's updates (the next push writes it; agent.py:199),
+    // by the last CTA, which the following phases load least
+    const int64_t size = P.ctl[AP_CTL_SIZE];
+    float* red = smem + kSmemFloats - 512;
+    double m = 0.0;
+    for (int64_t i = threadIdx.x; i < size; i += kThreads) m = fmax(m, __ldcg(P.r_prio + i));
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    double* dred = reinterpret_cast<double*>(red);
+    if ((threadIdx.x & 31) == 0) dred[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int k = 1; k < kWarps; ++k) m = fmax(m, dred[k]);
+      m = fmax(m, dred[0]);
+      P.pstat[0] = size ? m : 1.0;
+      P.pstat[1] = pow(P.pstat[0], P.alpha);
+    }
+    __syncthreads();
+  }
   if (blockIdx.x == 0 && threadIdx.x < 32) {  // fixed-order sum; the terms loaded in parallel
     float* sl = smem + kSmemFloats - 256;       // (past every tile's footprint in this phase)
     for (int b = threadIdx.x; b < B; b += 32) sl[b] = __ldcg(F.lrow + b);
@@ -844,7 +1044,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const __grid_con
   // Adam bias corrections (host values, or the parity loop's table entry for this train step)
   float c1 = P.c1, c2 = P.c2;
   if (P.ctab) {
-    const int64_t k = P.ctl[AP_CTL_TRAIN] + P.t_offset - P.ctl[AP_PL_TAB_BASE];
+    const int64_t k = t_train + P.t_offset - P.ctl[AP_PL_TAB_BASE];
     c1 = P.ctab[2 * k];
     c2 = P.ctab[2 * k + 1];
   }
@@ -870,7 +1070,10 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const __grid_con
     }
   };
 
-  // head backward: gWh = H_L(cur)^T dz, gbh, dh_L = relu'(H_L) * (dz Wh^T); Adam on Wh, bh
+  // head backward: gWh = H_L(cur)^T dz, gbh, dh_L = relu'(H_L) * (dz Wh^T); Adam on Wh, bh.
+  // Small heads: dh_L came with the TD rows and gWh joins the next phase (one barrier less).
+  const bool fold_head = small_head;
+  if (!fold_head) {
   if (t0) {
     const float* Hc = F.Hon[L] + (int64_t)B * H;  // current-state rows
     F.nj = 2;
@@ -901,6 +1104,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const __grid_con
   trace_arrive(P.trace, tk);
   grid_sync(P.bar);
   trace_mark(P.trace, tk);
+  }
 
   // hidden layers, last to first: gW_{i-1} (+ Adam), dh_{i-1}; refresh the transposed copy of
   // the weight updated in the phase before
@@ -933,6 +1137,18 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const __grid_con
         dg.mask = F.Hon[i - 1] + (int64_t)B * din;
         dg.ldmask = din;
       }
+      if (i == L && fold_head) {
+        // gWh = H_L(cur)^T dz + Adam; no job of this phase reads the head's transposed
+        // copy, so the epilogue writes it directly
+        Job& hg = F.jobs[F.nj++];
+        hg = Job{};
+        hg.a = AOp{F.Hon[L] + (int64_t)B * H, H, nullptr, nullptr, nullptr, 0, 1, H};
+        hg.b = BOp{F.dz, A1, 1};
+        hg.c = P.grad + P.w_off[L];
+        hg.ldc = A1;
+        hg.M = H + 1, hg.N = A1, hg.K = B;
+        with_adam(hg, L, true);
+      }
       plan_tiles(F.jobs, F.nj);
     }
     __syncthreads();
@@ -941,7 +1157,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const __grid_con
     __syncthreads();
     run_jobs(F.jobs, F.nj, smem);
 #endif
-    refresh_wt(i);  // i == L: the head; else w_i (updated in the phase of layer i + 1)
+    if (i < L || !fold_head) refresh_wt(i);  // i == L: the head; else w_i (updated in the phase of layer i + 1)
     if (i > 1) {
       trace_arrive(P.trace, tk);
       grid_sync(P.bar);
@@ -950,6 +1166,30 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const __grid_con
   }
   trace_arrive(P.trace, tk);
   trace_mark(P.trace, tk);
+  if (!P.tail_ctl) return;
+  // parity-loop tail (agent.py:325-337): every CTA read the train counter before the first
+  // barrier, so CTA 0 may advance it now
+  if (blockIdx.x == 0 && t0) {
+    const int64_t k = t_train - P.tail_ctl[AP_PL_TRAIN0];
+    const float v = *P.loss;
+    if (k >= 0 && k < P.loss_cap) P.loss_log[k] = v;
+    if (!isfinite(v) && P.tail_ctl[AP_PL_LOSS_BAD] < 0) P.tail_ctl[AP_PL_LOSS_BAD] = k;
+    P.tail_ctl[AP_CTL_TRAIN] = t_train + 1;
+  }
+  if ((t_train + 1) % P.sync_every != 0) return;
+  // hard target sync: online parameters and transposed copies -> the target's, once every
+  // CTA's Adam updates and copy refreshes are done
+  grid_sync(P.bar);
+  for (int k = 0; k < P.sync_n; ++k) {
+    const float4* src = reinterpret_cast<const float4*>(P.sync_src[k]);
+    float4* dst = reinterpret_cast<float4*>(P.sync_dst[k]);
+    const int64_t n4 = P.sync_count[k] / 4;
+    for (int64_t e = (int64_t)blockIdx.x * kThreads + threadIdx.x; e < n4; e += (int64_t)gridDim.x * kThreads)
+      dst[e] = __ldcg(src + e);
+    for (int64_t e = 4 * n4 + (int64_t)blockIdx.x * kThreads + threadIdx.x; e < P.sync_count[k];
+         e += (int64_t)gridDim.x * kThreads)
+      P.sync_dst[k][e] = __ldcg(P.sync_src[k] + e);
+  }
 }
 
 int64_t workspace_floats(int L, const int* d, int B, bool fwd_only) {
@@ -957,12 +1197,19 @@ int64_t workspace_floats(int L, const int* d, int B, bool fwd_only) {
   int64_t n = 0;
   for (int i = 1; i <= L; ++i) n += (Ron + 2 * (int64_t)B) * d[i];
   const int64_t A1 = d[L + 1];
-  return n + (Ron + 2 * (int64_t)B) * A1 + B + 64;
+  n += (Ron + 2 * (int64_t)B) * A1 + B + 64;
+  if (fwd_only && B <= kSmallRows && A1 <= 8) {  // small_forward: chunk partials + the last hidden rows
+    int64_t s = (int64_t)B * d[L];
+    for (int i = 0; i < L; ++i) s += (int64_t)split_of(d[i], d[i + 1]).ks * B * d[i + 1];
+    n = std::max(n, s);
+  }
+  return n;
 }
 
-int launch(const Learn& P, cudaStream_t stream) {
+int launch(const Learn& P, cudaStream_t stream, int reserve_sms = 0) {
   int sms = 0;
   if (int rc = current_sm_count(&sms)) return rc;
+  sms = std::max(1, sms - reserve_sms);
   static PerDeviceMax configured;
   const int smem = kSmemFloats * 4 + 64;
   if (configured.need(current_device(), smem))
@@ -1025,6 +1272,30 @@ int ap_mlp_forward_fused(int32_t L, const int32_t* dims, const int64_t* w_off, c
   return launch(P, (cudaStream_t)stream);
 }
 
+int ap_parity_act_fused(const ap_parity_loop* pl, int32_t L, const int32_t* dims, const int64_t* w_off,
+                        const int64_t* b_off, const float* params, float* q, float* workspace, uint32_t* barrier,
+                        int32_t* action, void* stream) {
+  Learn P = {};
+  if (!pl || !pl->ctl || !pl->rng || !pl->state || !fill_net(&P, L, dims, w_off, b_off) || !params || !q ||
+      !workspace || !barrier || !action || P.A + 1 > 8 || P.A != pl->num_actions) {
+    set_error("ap_parity_act_fused: bad arguments (1..4 hidden layers, 1 <= A <= 7 actions matching the loop)");
+    return AP_ERR_INVALID;
+  }
+  P.rows_fwd = 1;
+  P.p = const_cast<float*>(params);
+  P.tp = params;
+  P.x_in = pl->state;
+  P.x_ld = dims[0];
+  P.q_out = q;
+  P.ws = workspace;
+  P.bar = barrier;
+  P.act = 1;
+  P.pl = *pl;
+  P.action = action;
+  // early PER sample: one SM stays free for the sampler the act's decision waits for
+  return launch(P, (cudaStream_t)stream, pl->early_sample ? 1 : 0);
+}
+
 int ap_dqn_learn_fused(const ap_fused_learn* a, void* stream) {
   Learn P = {};
   if (!a || !fill_net(&P, a->L, a->dims, a->w_off, a->b_off) || a->batch < 1 || a->batch > 256 || !a->params ||
@@ -1075,6 +1346,29 @@ int ap_dqn_learn_fused(const ap_fused_learn* a, void* stream) {
   P.bar = a->barrier;
   P.trace = reinterpret_cast<unsigned long long*>(a->trace);
   P.gate = a->ctl ? a->gate : 0;
+  if (a->tail_ctl) {
+    if (!a->ctl || a->tail_ctl != a->ctl || !a->loss_log || a->sync_every < 1 || a->sync_n < 0 || a->sync_n > 6) {
+      set_error("ap_dqn_learn_fused: the tail needs ctl == tail_ctl, loss_log, sync_every >= 1, <= 6 sync segments");
+      return AP_ERR_INVALID;
+    }
+    for (int k = 0; k < a->sync_n; ++k)
+      if (!a->sync_src[k] || !a->sync_dst[k] || a->sync_count[k] < 0 || (reinterpret_cast<uintptr_t>(a->sync_src[k]) & 15) ||
+          (reinterpret_cast<uintptr_t>(a->sync_dst[k]) & 15)) {
+        set_error("ap_dqn_learn_fused: sync segments need 16-byte aligned non-null pointers");
+        return AP_ERR_INVALID;
+      }
+    P.tail_ctl = a->tail_ctl;
+    P.loss_log = a->loss_log;
+    P.loss_cap = a->loss_cap;
+    P.sync_every = a->sync_every;
+    P.sync_n = a->sync_n;
+    for (int k = 0; k < a->sync_n; ++k)
+      P.sync_src[k] = a->sync_src[k], P.sync_dst[k] = a->sync_dst[k], P.sync_count[k] = a->sync_count[k];
+    if (a->rng_from && a->rng_to) P.rng_from = a->rng_from, P.rng_to = a->rng_to;
+  }
+  P.r_scaled = a->r_scaled;
+  P.pstat = a->r_scaled ? a->pstat : nullptr;
+  P.alpha = a->per_alpha;
   return launch(P, (cudaStream_t)stream);
 }
 

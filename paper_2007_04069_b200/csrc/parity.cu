@@ -21,25 +21,37 @@
 // stream is numpy's own (pcg64.cuh), so draws, actions, rewards, states and the
 // chosen plan are those of the host-driven loop bit for bit
 // (tests/test_devloop_gpu.py).
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <new>
 
 #include "engine.h"
+
+#ifdef AP_SAMPLE_TRACE  // dev-only: SM clock at the sampler's stages (thread 0; one CTA, one SM)
+__device__ unsigned long long g_sample_trace[16];
+extern "C" int ap_debug_sample_trace(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_sample_trace, sizeof(g_sample_trace));
+}
+#define ST(k)                                                          \
+  do {                                                                 \
+    if (threadIdx.x == 0) {                                            \
+      unsigned long long t_;                                           \
+      t_ = clock64();                                                  \
+      g_sample_trace[k] = t_;                                          \
+    }                                                                  \
+  } while (0)
+#endif
+
+#include "parity_act.cuh"
 #include "pcg64.cuh"
+#include "per_sample.cuh"
 
 namespace apb {
 namespace {
 
 constexpr int kPostThreads = 256;
-
-__device__ __forceinline__ double epsilon_at(int64_t it, double start, double final_eps, int64_t decay) {
-  // agent.py:50-55: start + (final - start) * min(1, max(0, it / decay)), every op rounded
-  if (decay <= 0) return final_eps;
-  double frac = __ddiv_rn((double)it, (double)decay);
-  frac = fmin(1.0, fmax(0.0, frac));
-  return __dadd_rn(start, __dmul_rn(__dsub_rn(final_eps, start), frac));
-}
+constexpr int kSampleMaxB = 1024;
 
 // state row entry of the decision position: flat index / |D| in fp64, stored as fp32
 // (the host agent converts the fp64 state to fp32 the same way); 1.0 when no position
@@ -50,32 +62,11 @@ __device__ __forceinline__ float position_feature(int64_t pos, int n) {
 __global__ void __launch_bounds__(kPostThreads) parity_act_kernel(ap_parity_loop L, const float* __restrict__ q,
                                                                   int32_t* __restrict__ action) {
   pdl_entry();
-  const int64_t step = L.ctl[AP_PL_STEP];
-  const int64_t pos = L.ctl[AP_PL_POS];
-  for (int j = threadIdx.x; j < L.ld; j += blockDim.x) {
-    L.seeds_try[j] = L.seeds[j];
-    if (L.log_decided) L.log_decided[step * L.ld + j] = L.decided[j];
-  }
+  __syncthreads();  // every thread has read the control block before thread 0 writes to it
+  parity_step_begin(L, false, threadIdx.x == 0);
+  parity_act_rows(L);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    NpPcg64 g = NpPcg64::load(L.rng);
-    const double eps = epsilon_at(L.ctl[AP_CTL_TRAIN], L.eps_start, L.eps_final, L.eps_decay);
-    int a;
-    if (g.next_double() < eps) {
-      // every action is allowed while the episode runs (envs.py:175-179)
-      a = (int)g.integers(L.num_actions);
-    } else {  // masked argmax, ties to the lowest index (agent.py:147-152)
-      a = 0;
-      float best = q[0];
-      for (int k = 1; k < L.num_actions; ++k)
-        if (q[k] > best) best = q[k], a = k;
-    }
-    g.store(L.rng);
-    *action = a;
-    L.seeds_try[pos] = a == 0 ? 1 : 0;  // ACTION_PARTITION seeds P, ACTION_REPLICATE seeds R
-    L.log_action[step] = a;
-    L.log_pos[step] = (int32_t)pos;
-  }
+  if (threadIdx.x == 0) parity_act_decide(L, q, action);
 }
 
 __device__ __forceinline__ int block_sum(int v, int* s_red) {
@@ -101,6 +92,7 @@ __device__ __forceinline__ int block_min(int v, int* s_red) {
 // env.step post-processing + episode bookkeeping + agent.observe, one CTA
 __global__ void __launch_bounds__(kPostThreads) parity_post_kernel(ap_parity_loop L, const int32_t* __restrict__ action) {
   pdl_entry();
+  if (!L.ctl[AP_PL_ACTIVE]) return;  // the budget ran out earlier in this WHILE iteration
   __shared__ int s_red[kPostThreads / 32];
   __shared__ double s_prio[kPostThreads / 32];
   const int n = L.n;
@@ -111,9 +103,11 @@ __global__ void __launch_bounds__(kPostThreads) parity_post_kernel(ap_parity_loo
   const int64_t step = L.ctl[AP_PL_STEP];
   const int64_t slot = L.ctl[AP_CTL_SLOT], size = L.ctl[AP_CTL_SIZE];
   const int a = *action;
-  // max priority over the filled ring, read before this push (agent.py:199)
+  // max priority over the filled ring, read before this push (agent.py:199): kept in pstat by
+  // the learn step when the loop has it (a push of the maximum leaves the maximum unchanged)
   double pm = 0.0;
-  for (int64_t i = tid; i < size; i += blockDim.x) pm = fmax(pm, L.r_prio[i]);
+  if (!L.pstat)
+    for (int64_t i = tid; i < size; i += blockDim.x) pm = fmax(pm, L.r_prio[i]);
   for (int o = 16; o; o >>= 1) pm = fmax(pm, __shfl_xor_sync(0xffffffffu, pm, o));
   if ((tid & 31) == 0) s_prio[tid >> 5] = pm;
   // the transition's state: the current row, before it changes
@@ -160,7 +154,13 @@ __global__ void __launch_bounds__(kPostThreads) parity_post_kernel(ap_parity_loo
     L.r_done[slot] = done;
     double pmax = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) pmax = fmax(pmax, s_prio[w]);
-    L.r_prio[slot] = size ? pmax : 1.0;
+    if (L.pstat) {
+      if (!size) L.pstat[0] = L.pstat[1] = 1.0;  // 1.0 ** alpha == 1.0
+      L.r_prio[slot] = L.pstat[0];
+      L.r_scaled[slot] = L.pstat[1];
+    } else {
+      L.r_prio[slot] = size ? pmax : 1.0;
+    }
     L.log_reward[step] = reward;
   }
   for (int k = tid; k < L.num_actions; k += blockDim.x) L.r_mask[slot * L.num_actions + k] = done ? 0 : 1;
@@ -196,6 +196,7 @@ __global__ void __launch_bounds__(kPostThreads) parity_post_kernel(ap_parity_loo
       L.dctl[AP_PLD_TOTAL] = 0.0;
     }
     L.ctl[AP_PL_STEP] = step + 1;
+    L.ctl[AP_PL_GEN] += 1;
     L.ctl[AP_PL_SYNC] = 0;  // raised by this step's learn tail when a target sync is due
     L.ctl[AP_CTL_SLOT] = (slot + 1) % L.cap;
     L.ctl[AP_CTL_SIZE] = size + 1 < L.cap ? size + 1 : L.cap;
@@ -228,12 +229,118 @@ __device__ __forceinline__ bool learn_gated_off(const ap_parity_loop& L) {
   return L.learn_gate > 0 && L.ctl[AP_CTL_SIZE] < L.learn_gate;
 }
 
-__global__ void parity_uniforms_kernel(ap_parity_loop L, int B, double* __restrict__ out) {
+// agent.learn's draws and PER sample in one CTA: B random() draws (rng.choice's uniforms,
+// agent.py:220), each thread jumping the PCG64 stream ahead to its own draw, then the PER
+// sample (per_sample.cuh) with the priorities and cdf staged in shared memory when they fit.
+// Early mode (see ap_parity_sample): the ring and stream as the step starts, the act's draws
+// replayed, the pending push counted, the read acknowledged, the final stream in rng_next.
+constexpr int kSampleThreads = 1024;
+
+constexpr int kSampleSmemBytes = 190 * 1024;  // + ~30 KB static <= 227 KB
+
+__global__ void __launch_bounds__(kSampleThreads) parity_sample_kernel(ap_parity_loop L, int B, double alpha,
+                                                                       double beta, double* scratch, int32_t* idx,
+                                                                       float* w, double* u_out, uint64_t* rng_next,
+                                                                       int early, int smem_doubles) {
   pdl_entry();
-  if (threadIdx.x || learn_gated_off(L)) return;
-  NpPcg64 g = NpPcg64::load(L.rng);
-  for (int b = 0; b < B; ++b) out[b] = g.next_double();
-  g.store(L.rng);
+  extern __shared__ double dyn[];
+  __shared__ PerShared S;
+  __shared__ double su[kSampleMaxB];
+  __shared__ uint64_t s_rng[6];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  ST(0);
+  // every thread reads the control words it needs, then a barrier: in early mode nothing is
+  // read from the control block after the acknowledgement (env.step advances slot / size)
+  const int64_t* c = L.ctl;
+  bool go;
+  int64_t slot, size;
+  if (early) {
+    go = c[AP_PL_EPISODES] < c[AP_PL_BUDGET] && c[AP_PL_STEP] < c[AP_PL_MAX_STEPS];
+    slot = c[AP_CTL_SLOT];
+    size = c[AP_CTL_SIZE];
+  } else {
+    go = c[AP_PL_ACTIVE] != 0;
+    slot = -1;
+    size = c[AP_CTL_SIZE] - 1;  // the ring before this step's push (n below is the pushed size)
+  }
+  const int n = (int)(size + 1 < L.cap ? size + 1 : L.cap);
+  const int64_t gen = early ? c[AP_PL_GEN] : 0, train = early ? c[AP_CTL_TRAIN] : 0;
+  const bool active = go;  // the step runs (the act waits for this kernel's acknowledgement)
+  go = go && !(L.learn_gate > 0 && n < L.learn_gate) && n >= B;
+  __syncthreads();
+  if (tid == 0) {
+    NpPcg64 g = NpPcg64::load(L.rng);
+    if (early && go) {
+      // the act's draws (agent.py:161-166): they depend on the step count, not on Q
+      const double eps = epsilon_at(train, L.eps_start, L.eps_final, L.eps_decay);
+      if (g.next_double() < eps) (void)g.integers(L.num_actions);
+    }
+    g.store(s_rng);
+    // every read of the stream / control block is done: the act may advance the stream
+    if (early && active)
+      asm volatile("st.release.gpu.u64 [%0], %1;" ::"l"(L.ctl + AP_PL_ACK), "l"(gen + 1) : "memory");
+  }
+  if (!go) return;
+  const bool staged = 2 * (int64_t)n + B <= smem_doubles;
+  if (tid == 32) per_tree(n, S);
+  // scaled = priorities ** alpha: early mode from the cache (+ the pending push: the ring's max
+  // priority and its power, kept by env.step / the learn step), late mode computed
+  const double sub = early ? L.pstat[1] : 0.0;
+  for (int i = tid; i < n; i += nt) {
+    const double v = early ? (i == slot ? sub : __ldcg(L.r_scaled + i)) : pow(L.r_prio[i], alpha);
+    if (staged)
+      dyn[i] = v;
+    else
+      scratch[i] = v;
+  }
+  __syncthreads();
+  ST(1);
+  // the B uniforms by the last threads (the first ones sum the pairwise blocks next)
+  const u128 s0 = ((u128)s_rng[0] << 64) | (u128)s_rng[1], inc = ((u128)s_rng[2] << 64) | (u128)s_rng[3];
+  for (int b = nt - 1 - tid; b >= 0 && b < B; b -= nt) {
+    u128 st = pcg_advance(s0, inc, (uint64_t)b);
+    const double v = pcg_next_double(st, inc);  // draw b: the state after b + 1 steps
+    su[b] = v;
+    if (u_out) u_out[b] = v;
+    if (b == B - 1) {  // random() leaves the 32-bit buffer alone
+      uint64_t* dst = early ? rng_next : L.rng;
+      dst[0] = (uint64_t)(st >> 64);
+      dst[1] = (uint64_t)st;
+      if (early) dst[2] = s_rng[2], dst[3] = s_rng[3], dst[4] = s_rng[4], dst[5] = s_rng[5];
+    }
+  }
+  // (two inlined copies: with the shared-memory arrays the compiler knows their space)
+  if (staged) {
+    per_total(dyn, S);
+    ST(2);
+    per_draw(dyn, n, beta, su, B, dyn + n, idx, w, S);
+  } else {
+    per_total(scratch, S);
+    ST(2);
+    per_draw(scratch, n, beta, su, B, scratch + L.cap, idx, w, S);
+  }
+  ST(3);
+}
+
+__global__ void per_scaled_kernel(const double* __restrict__ prio, int64_t n, double alpha, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = pow(prio[i], alpha);
+}
+
+// pstat = {max priority over the ring (1.0 when empty), its ** alpha}: one CTA
+__global__ void per_pstat_kernel(const double* __restrict__ prio, int64_t n, double alpha, double* __restrict__ pstat) {
+  __shared__ double red[32];
+  double m = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, prio[i]);
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) m = fmax(m, red[k]);
+    m = fmax(m, red[0]);
+    pstat[0] = n ? m : 1.0;
+    pstat[1] = pow(pstat[0], alpha);
+  }
 }
 
 // loss log, train-step counter, target-sync flag (agent.py:325-337)
@@ -307,12 +414,35 @@ int ap_parity_post(const ap_parity_loop* L, const int32_t* action, void* stream)
   return AP_OK;
 }
 
-int ap_parity_uniforms(const ap_parity_loop* L, int32_t B, double* out, void* stream) {
-  if (!L || !out || B < 1) {
-    set_error("ap_parity_uniforms: bad arguments");
+int ap_parity_sample(const ap_parity_loop* L, int32_t B, double alpha, double beta, double* scratch,
+                     int32_t* indices, float* weights, double* uniforms_out, uint64_t* rng_next, int32_t early,
+                     void* stream) {
+  if (!L || !L->ctl || !L->rng || !L->r_prio || !scratch || !indices || !weights || B < 1 || B > kSampleMaxB ||
+      (early && !rng_next)) {
+    set_error("ap_parity_sample: bad arguments (1 <= B <= 1024; early mode needs rng_next)");
     return AP_ERR_INVALID;
   }
-  launch_pdl(parity_uniforms_kernel, dim3(1), dim3(32), 0, (cudaStream_t)stream, *L, (int)B, out);
+  static PerDeviceMax configured;
+  const int64_t want = (2 * L->cap + B) * (int64_t)sizeof(double);
+  const int smem = want <= kSampleSmemBytes ? (int)want : 0;
+  if (smem && configured.need(current_device(), smem))
+    AP_CUDA_CHECK(cudaFuncSetAttribute(parity_sample_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  launch_pdl(parity_sample_kernel, dim3(1), dim3(kSampleThreads), (size_t)smem, (cudaStream_t)stream, *L, (int)B,
+             alpha, beta, scratch, indices, weights, uniforms_out, rng_next, (int)(early != 0),
+             smem / (int)sizeof(double));
+  AP_CUDA_CHECK(cudaGetLastError());
+  return AP_OK;
+}
+
+int ap_per_scaled(const double* priorities, int64_t n, double alpha, double* scaled, double* pstat, void* stream) {
+  if (n < 0 || (n && (!priorities || !scaled))) {
+    set_error("ap_per_scaled: bad arguments");
+    return AP_ERR_INVALID;
+  }
+  if (pstat) per_pstat_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(priorities, n, alpha, pstat);
+  if (!n) return AP_OK;
+  per_scaled_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, (cudaStream_t)stream>>>(priorities, n,
+                                                                                                   alpha, scaled);
   AP_CUDA_CHECK(cudaGetLastError());
   return AP_OK;
 }

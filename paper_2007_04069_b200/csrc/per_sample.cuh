@@ -1,0 +1,249 @@
+// Prioritized-replay sampling in numpy's exact arithmetic, one CTA (agent.py:207-223):
+//
+//   scaled = priorities[:n] ** alpha
+//   probs  = scaled / scaled.sum()                  (numpy pairwise summation)
+//   idx    = rng.choice(n, B, p=probs)              (cdf = probs.cumsum(); cdf /= cdf[-1];
+//                                                    searchsorted(uniforms, side='right'))
+//   w      = (n * probs[idx]) ** -beta;  w /= w.max()
+//
+// Everything but the cumsum runs across the CTA.  numpy's pairwise sum is a fixed binary
+// recursion over blocks of <= 128 elements (PW_BLOCKSIZE): thread 0 lists the blocks, the
+// block sums run in parallel (8 interleaved accumulators each, numpy's unrolled loop), and
+// thread 0 adds them back up in the recursion's order.  The cumsum is numpy's sequential
+// chain of adds on one thread, its operands prefetched 16 at a time.
+#pragma once
+
+#include <cstdint>
+
+#ifndef ST
+#define ST(k) \
+  do {        \
+  } while (0)
+#endif
+
+namespace apb {
+namespace {  // internal linkage: included by several translation units
+
+constexpr int kPerMaxNodes = 1024;  // nodes of the pairwise recursion handled in parallel (24 KB)
+
+// numpy pairwise summation of one block of <= 128 doubles
+// (numpy/_core/src/umath/loops_utils.h.src)
+__device__ __forceinline__ double np_pairwise_leaf(const double* x, int64_t m) {
+  if (m < 8) {
+    double v = -0.0;  // numpy starts from -0.0 to preserve -0.0 sums
+    for (int64_t i = 0; i < m; ++i) v += x[i];
+    return v;
+  }
+  double r[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) r[k] = x[k];
+  int64_t i;
+  for (i = 8; i < m - (m % 8); i += 8)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[k] += x[i + k];
+  double v = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (; i < m; ++i) v += x[i];
+  return v;
+}
+
+// Walk of the recursion sum(a, n) = sum(a, n2) + sum(a + n2, n - n2), n2 = n/2 rounded down to
+// a multiple of 8, with an explicit post-order stack.  LEAF(off, len) gives a block's sum.
+template <typename Leaf>
+__device__ double np_pairwise_walk(int64_t n, Leaf leaf) {
+  struct Frame {
+    int64_t off, n;
+    int state;
+    double left;
+  };
+  Frame fr[64];
+  int top = 0;
+  fr[0] = {0, n, 0, 0.0};
+  double ret = 0.0;
+  while (top >= 0) {
+    Frame& f = fr[top];
+    if (f.n <= 128) {
+      ret = leaf(f.off, f.n);
+      --top;
+      continue;
+    }
+    int64_t n2 = f.n / 2;
+    n2 -= n2 % 8;
+    if (f.state == 0) {
+      f.state = 1;
+      fr[top + 1] = {f.off, n2, 0, 0.0};
+      ++top;
+    } else if (f.state == 1) {
+      f.left = ret;
+      f.state = 2;
+      fr[top + 1] = {f.off + n2, f.n - n2, 0, 0.0};
+      ++top;
+    } else {
+      ret = f.left + ret;
+      --top;
+    }
+  }
+  return ret;
+}
+
+struct PerShared {
+  int64_t node_off[kPerMaxNodes];
+  int32_t node_len[kPerMaxNodes];
+  int32_t node_child[kPerMaxNodes];  // left child (right = left + 1), -1 a block, -2 summed serially
+  double node_sum[kPerMaxNodes];
+  int nnodes;
+  double total, last, wmax;
+  double wred[32];
+};
+
+// The recursion's nodes for n elements, breadth first (children after their parent).  One thread.
+__device__ __forceinline__ void per_tree(int n, PerShared& S) {
+  int cnt = 1;
+  S.node_off[0] = 0, S.node_len[0] = n;
+  for (int i = 0; i < cnt; ++i) {
+    const int len = S.node_len[i];
+    if (len <= 128 || cnt + 2 > kPerMaxNodes) {
+      S.node_child[i] = len <= 128 ? -1 : -2;
+      continue;
+    }
+    int n2 = len / 2;
+    n2 -= n2 % 8;
+    S.node_child[i] = cnt;
+    S.node_off[cnt] = S.node_off[i], S.node_len[cnt] = n2;
+    S.node_off[cnt + 1] = S.node_off[i] + n2, S.node_len[cnt + 1] = len - n2;
+    cnt += 2;
+  }
+  S.nnodes = cnt;
+}
+
+// numpy's pairwise block of 8 <= m <= 128 (shared memory): 8 accumulators, 16 loads in flight
+__device__ __forceinline__ double np_pairwise_block(const double* x, int m) {
+  if (m < 8) return np_pairwise_leaf(x, m);
+  double r[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) r[k] = x[k];
+  const int m8 = m - (m % 8);
+  int i = 8;
+  for (; i + 16 <= m8; i += 16) {
+    double v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = x[i + k];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[k] += v[k];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[k] += v[8 + k];
+  }
+  for (; i < m8; i += 8)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[k] += x[i + k];
+  double v = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (; i < m; ++i) v += x[i];
+  return v;
+}
+
+// total = numpy's pairwise sum of scaled[0, n) over the tree of per_tree (every thread; the
+// block sums in parallel, then thread 0 adds the nodes children first).  Ends with a barrier.
+__device__ __forceinline__ void per_total(const double* scaled, PerShared& S) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int nn = S.nnodes;
+  for (int i = tid; i < nn; i += nt) {
+    const int c = S.node_child[i];
+    if (c == -1)
+      S.node_sum[i] = np_pairwise_block(scaled + S.node_off[i], S.node_len[i]);
+    else if (c == -2)
+      S.node_sum[i] = np_pairwise_walk(S.node_len[i], [&](int64_t off, int64_t len) {
+        return np_pairwise_leaf(scaled + S.node_off[i] + off, len);
+      });
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int i = nn - 1; i >= 0; --i) {
+      const int c = S.node_child[i];
+      if (c >= 0) S.node_sum[i] = S.node_sum[c] + S.node_sum[c + 1];
+    }
+    S.total = S.node_sum[0];
+  }
+  __syncthreads();
+}
+
+// From scaled[0, n) and S.total: probs, numpy's cdf (sequential cumsum), the B searchsorted
+// draws and the normalised importance weights (every thread).  probs: n + B doubles.  The
+// cumsum overwrites scaled (p = probs[i] is all the weights need afterwards).
+__device__ __forceinline__ void per_draw(double* __restrict__ scaled, int n, double beta, const double* u, int B,
+                                         double* __restrict__ probs, int32_t* __restrict__ idx_out,
+                                         float* __restrict__ w_out, PerShared& S) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  // probs = scaled / total (independent divisions)
+  const double total = S.total;
+  for (int i = tid; i < n; i += nt) probs[i] = scaled[i] / total;
+  __syncthreads();
+  ST(6);
+  if (tid == 0) {
+    // cdf = probs.cumsum(): one chain of adds, the critical path; operands 16 ahead in registers
+    double* __restrict__ cdf = scaled;
+    double acc = probs[0];
+    cdf[0] = acc;
+    int i = 1;
+    for (; i + 16 <= n; i += 16) {
+      double x[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) x[k] = probs[i + k];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        acc = acc + x[k];
+        cdf[i + k] = acc;
+      }
+    }
+    for (; i < n; ++i) {
+      acc = acc + probs[i];
+      cdf[i] = acc;
+    }
+    S.last = acc;
+  }
+  __syncthreads();
+  ST(7);
+  // cdf /= cdf[-1]; searchsorted(side='right'): the first i with cdf[i] / last > u, each
+  // probe's quotient computed where it is needed (the same rounded value)
+  const double* cdf = scaled;
+  const double last = S.last;
+  double wloc = 0.0;
+  for (int b = tid; b < B; b += nt) {
+    const double ub = u[b];
+    int lo = 0, hi = n;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (cdf[mid] / last <= ub)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    idx_out[b] = lo;
+    const double w = pow((double)n * probs[lo], -beta);
+    probs[n + b] = w;
+    wloc = fmax(wloc, w);
+  }
+  for (int o = 16; o; o >>= 1) wloc = fmax(wloc, __shfl_xor_sync(0xffffffffu, wloc, o));
+  if ((tid & 31) == 0) S.wred[tid >> 5] = wloc;
+  __syncthreads();
+  if (tid < 32) {
+    double m = tid < (nt >> 5) ? S.wred[tid] : 0.0;
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (tid == 0) S.wmax = m;
+  }
+  __syncthreads();
+  for (int b = tid; b < B; b += nt) w_out[b] = (float)(probs[n + b] / S.wmax);
+}
+
+// The whole sample with scaled = priorities ** alpha computed here (every thread).
+__device__ __noinline__ void per_sample_block(const double* __restrict__ prio, int n, double alpha, double beta,
+                                              const double* u, int B, double* scaled, double* cdf,
+                                              int32_t* __restrict__ idx_out, float* __restrict__ w_out,
+                                              PerShared& S) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) scaled[i] = pow(prio[i], alpha);
+  if (threadIdx.x == 0) per_tree(n, S);
+  __syncthreads();
+  per_total(scaled, S);
+  per_draw(scaled, n, beta, u, B, cdf, idx_out, w_out, S);  // (cdf: n + B doubles)
+}
+
+}  // namespace
+}  // namespace apb

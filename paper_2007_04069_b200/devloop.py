@@ -34,6 +34,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 
 import numpy as np
 
@@ -45,6 +46,8 @@ from .search import PartitionOutcome, state_digest
 from .sharding import DimStatus, pad16
 
 _LOG_BYTES = 256 << 20  # state-row log budget per launch (trace digests)
+# steps per WHILE iteration of the self-gated loop graph (a WHILE iteration costs ~30 us)
+_STEPS_PER_ITER = int(os.environ.get("AP_LOOP_STEPS_PER_ITER", "8"))
 # device time / env steps / launches of the last train_partition_device call (bench.py reads it)
 last_stats: dict = {}
 
@@ -76,6 +79,9 @@ class DeviceSearch:
             "ctl": torch.zeros(_native.PL["WORDS"], dtype=i64, device=dev),
             "dctl": torch.zeros(2, dtype=f64, device=dev),
             "rng": torch.zeros(6, dtype=i64, device=dev),
+            "rng_next": torch.zeros(6, dtype=i64, device=dev),
+            "scaled": torch.zeros(buf.capacity, dtype=f64, device=dev),
+            "pstat": torch.ones(2, dtype=f64, device=dev),
             "seeds": torch.full((self.ld,), -1, dtype=i8, device=dev),
             "seeds_try": torch.full((1, self.ld), -1, dtype=i8, device=dev),
             "decided": torch.full((self.ld,), -1, dtype=i8, device=dev),
@@ -87,6 +93,7 @@ class DeviceSearch:
             # contiguous [1, S], the shape the host agent's act feeds the Q-network (same GEMM path)
             "state": torch.zeros((1, env.state_dim), dtype=f32, device=dev),
             "action": torch.zeros(1, dtype=i32, device=dev),
+            "q": torch.zeros((1, A), dtype=f32, device=dev),
             "best_row": torch.full((self.ld,), -1, dtype=i8, device=dev),
             "log_action": torch.zeros(steps_per_launch, dtype=i32, device=dev),
             "log_reward": torch.zeros(steps_per_launch, dtype=f64, device=dev),
@@ -97,7 +104,6 @@ class DeviceSearch:
             "ep_return": torch.zeros(steps_per_launch, dtype=f64, device=dev),
             "loss_log": torch.zeros(steps_per_launch, dtype=f32, device=dev),
             "ctab": torch.zeros(2 * steps_per_launch, dtype=f32, device=dev),
-            "uniforms": torch.zeros(cfg.batch_size, dtype=f64, device=dev),
             "idx": torch.zeros(cfg.batch_size, dtype=i32, device=dev),
             "weights": torch.zeros(cfg.batch_size, dtype=f32, device=dev),
         }
@@ -119,39 +125,85 @@ class DeviceSearch:
         self.adam_offset = agent.optimizer.t - agent.train_steps  # invariant: both advance per learn step
         # the fused learner and the parity kernels gate themselves on the ring size; the GEMM
         # learner runs under the loop graph's IF node
-        self.gated = agent.learner == "fused"
+        self.gated = agent.learner == "fused" and getattr(agent.net, "fused_act", False) and A + 1 <= 8
         self.desc.learn_gate = cfg.batch_size if self.gated else 0
+        self.desc.early_sample = 1 if self.gated else 0
+        if self.gated:  # the early sampler reads priorities ** alpha from a cache env.step / learn keep current
+            self.desc.r_scaled = t["scaled"].data_ptr()
+            self.desc.pstat = t["pstat"].data_ptr()
+            self.desc.per_alpha = float(cfg.per_alpha)
         self._capture()
 
     # -- capture ---------------------------------------------------------------------------
 
-    def _step_body(self):
+    def _act(self):
         lib = _native.require_device()
         t, L = self.t, ctypes.byref(self.desc)
         net = self.agent.net
-        q = net.forward_fused(t["state"]) if getattr(net, "fused_act", False) else net.forward_device(t["state"])
-        _native.check(lib.ap_parity_act(L, _native.ptr(q), _native.ptr(t["action"]), _stream()))
+        if self.gated:
+            # forward + epsilon-greedy decision in one launch (the host act's forward arithmetic);
+            # it also closes the step once the budget is spent (the body runs several steps)
+            Lh, dims, w_off, b_off = net.fused_layout()[:4]
+            ws, bar = net._fused_scratch(256, True)
+            _native.check(lib.ap_parity_act_fused(L, Lh, dims, w_off, b_off, _native.ptr(net.flat),
+                                                  _native.ptr(t["q"]), _native.ptr(ws), _native.ptr(bar),
+                                                  _native.ptr(t["action"]), _stream()))
+        else:
+            q = net.forward_fused(t["state"]) if getattr(net, "fused_act", False) else net.forward_device(t["state"])
+            _native.check(lib.ap_parity_act(L, _native.ptr(q), _native.ptr(t["action"]), _stream()))
+            self._keep_q = q
+
+    def _env_step(self):
+        lib = _native.require_device()
+        t, L = self.t, ctypes.byref(self.desc)
         self.env._engine.launch(t["seeds_try"][:, : self.n], t["outcome"], None, None, t["status"])
         _native.check(lib.ap_parity_post(L, _native.ptr(t["action"]), _stream()))
-        self._keep_q = q
 
-    def _learn_body(self):
+    def _sample(self, early: bool = False):
+        lib = _native.require_device()
+        cfg, t = self.agent.config, self.t
+        st = self.agent.buffer.store
+        _native.check(lib.ap_parity_sample(ctypes.byref(self.desc), cfg.batch_size, float(cfg.per_alpha),
+                                           float(cfg.per_beta), _native.ptr(st["scratch"]), _native.ptr(t["idx"]),
+                                           _native.ptr(t["weights"]), None,
+                                           _native.ptr(t["rng_next"]) if early else None, int(early), _stream()))
+
+    def _step_body(self):
+        self._act()
+        self._env_step()
+
+    def _gated_body(self):
+        """One step of the self-gated loop body: the PER sample of the step (early mode: the ring
+        and random stream as the step starts, the act's draws replayed, the pending push counted)
+        on a side branch beside act -> K1 -> env.step, then the learn step, which commits the
+        sampler's stream state."""
+        import torch
+
+        cur = torch.cuda.current_stream()
+        self.side.wait_stream(cur)
+        with torch.cuda.stream(self.side):
+            self._sample(early=True)
+        self._act()
+        self._env_step()
+        cur.wait_stream(self.side)
+        self._learn_body(sample=False)
+
+    def _learn_body(self, sample: bool = True):
         lib = _native.require_device()
         agent, cfg, t = self.agent, self.agent.config, self.t
         L = ctypes.byref(self.desc)
         B = cfg.batch_size
-        st = agent.buffer.store
-        _native.check(lib.ap_parity_uniforms(L, B, _native.ptr(t["uniforms"]), _stream()))
-        _native.check(lib.ap_per_sample_n_ctl(_native.ptr(st["priorities"]), _native.ptr(t["ctl"]),
-                                              agent.buffer.capacity, float(cfg.per_alpha), float(cfg.per_beta),
-                                              _native.ptr(t["uniforms"]), B, _native.ptr(st["scratch"]),
-                                              _native.ptr(t["idx"]), _native.ptr(t["weights"]), _stream()))
+        if sample:
+            self._sample()
         opt, net = agent.optimizer, agent.net
         if agent.learner == "fused":
-            loss = agent._fused.run(t["idx"], t["weights"], ctab=t["ctab"], ctl=t["ctl"], t_offset=self.adam_offset,
-                                    gate=B if self.gated else 0)
-            _native.check(lib.ap_parity_learn_tail(L, _native.ptr(loss), int(cfg.target_sync_every), _stream()))
-            self._sync(lib)
+            # the learn tail (loss log, train counter) and the target sync run inside the kernel
+            agent._fused.run(t["idx"], t["weights"], ctab=t["ctab"], ctl=t["ctl"], t_offset=self.adam_offset,
+                             gate=B if self.gated else 0,
+                             tail=(t["loss_log"], self.steps_cap, int(cfg.target_sync_every), self._sync_segments(),
+                                   (t["rng_next"], t["rng"]) if self.gated else None),
+                             scaled=t["scaled"] if self.gated else None, pstat=t["pstat"] if self.gated else None,
+                             alpha=cfg.per_alpha)
             return
 
         def adam_step():
@@ -222,11 +274,13 @@ class DeviceSearch:
                 torch.cuda.current_stream().synchronize()
                 self.g_step = torch.cuda.CUDAGraph(keep_graph=True)
                 if self.gated:
-                    # one body: the step, then the learn kernels, which skip themselves while the
-                    # ring holds fewer than a batch (no IF node, no condition kernel per step)
+                    # one body of _STEPS_PER_ITER steps; the learn kernels skip themselves while the
+                    # ring holds fewer than a batch and every kernel after the act skips once the
+                    # act found the budget spent (no IF node, one condition kernel per iteration)
+                    self.side = torch.cuda.Stream()
                     with torch.cuda.graph(self.g_step, stream=self.stream):
-                        self._step_body()
-                        self._learn_body()
+                        for _ in range(_STEPS_PER_ITER):
+                            self._gated_body()
                     self.g_learn = None
                 else:
                     with torch.cuda.graph(self.g_step, stream=self.stream):
@@ -264,6 +318,11 @@ class DeviceSearch:
 
         self.t["ctl"].copy_(torch.from_numpy(ctl_host))
         self.t["ctab"][: ctab.size].copy_(torch.from_numpy(ctab))
+        if self.gated:  # the PER cache from the priorities as the host left them
+            _native.check(_native.require_device().ap_per_scaled(
+                _native.ptr(self.agent.buffer.store["priorities"]), int(ctl_host[_native.PL["SIZE"]]),
+                float(self.agent.config.per_alpha), _native.ptr(self.t["scaled"]), _native.ptr(self.t["pstat"]),
+                _native.stream_handle()))
         self.stream.wait_stream(torch.cuda.current_stream())
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record(self.stream)
@@ -359,6 +418,8 @@ def train_partition_device(env: PartitionSearchEnv, agent: DqnAgent, episodes: i
         last_stats["steps"] += int(ctl[W["STEP"]])
         last_stats["launches"] += 1
         last_stats["train_steps"] += int(ctl[W["TRAIN"]]) - train0
+        if ctl[W["FAULT"]]:
+            raise RuntimeError("device loop: the act gave up waiting for the step's PER sample")
         if ctl[W["LOSS_BAD"]] >= 0:
             raise DivergenceError("training loss diverged on the device loop")
         steps = int(ctl[W["STEP"]])
