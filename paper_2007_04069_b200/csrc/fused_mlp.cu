@@ -30,6 +30,8 @@
 // gives Q for a few rows (the act of the search loop).
 #include <algorithm>
 #include <cstdint>
+#include <mutex>
+#include <unordered_map>
 
 #include "engine.h"
 #include "parity_act.cuh"
@@ -43,64 +45,8 @@ constexpr int kMaxLayers = 4;  // hidden layers
 constexpr int kTN = 32;        // tile columns (one per lane)
 constexpr int kSmemFloats = 56 * 1024;  // 224 KB of dynamic shared memory per CTA (one chunk at K <= 1100)
 
-struct Learn {
-  int L, A, B, rows_fwd;  // rows_fwd: forward mode row count (learn mode: 0)
-  int d[kMaxLayers + 2];  // d[0] state dim, d[1..L] hidden widths, d[L+1] = 1 + A
-  float* p;               // online flat parameters (updated in place)
-  const float* tp;        // target flat parameters
-  int64_t w_off[kMaxLayers + 1], b_off[kMaxLayers + 1];
-  // replay ring and PER sample
-  const float* r_states;
-  const float* r_next;
-  int64_t r_ld;
-  const int32_t* r_actions;
-  const float* r_rewards;
-  const uint8_t* r_done;
-  const uint8_t* r_mask;
-  double* r_prio;
-  const int32_t* idx;
-  const float* isw;
-  float gamma, delta;
-  // Adam
-  float* grad;
-  float* m;
-  float* v;
-  int64_t nparams;
-  float lr, b1, b2, eps, c1, c2;
-  const float* ctab;  // optional bias-correction table (parity loop), see ap_dqn_adam_tab
-  const int64_t* ctl;
-  int64_t t_offset;
-  float* wt[kMaxLayers + 1];  // transposed copies [d_{i+1}, ld] of w_i (and the head)
-  int64_t wt_ld[kMaxLayers + 1];
-  // outputs
-  float* td;
-  float* loss;  // sum_b w_b * huber_b
-  float* q_out;  // forward mode: [rows, A]
-  const float* x_in;  // forward mode: [rows, x_ld]
-  int64_t x_ld;
-  // workspace
-  float* ws;
-  unsigned* bar;
-  unsigned long long* trace;  // optional: %globaltimer after each phase (CTA 0)
-  int64_t gate;               // > 0: no-op while ctl[AP_CTL_SIZE] < gate (self-gated loop body)
-  // forward mode, parity loop: the epsilon-greedy act on row 0's Q (parity_act.cuh)
-  int act;
-  ap_parity_loop pl;
-  int32_t* action;
-  // parity-loop tail: loss log, train counter, target sync (see ap_fused_learn)
-  int64_t* tail_ctl;
-  float* loss_log;
-  int64_t loss_cap;
-  int sync_every, sync_n;
-  const float* sync_src[6];
-  float* sync_dst[6];
-  int64_t sync_count[6];
-  double* r_scaled;          // optional: priorities ** alpha, updated with each priority
-  double* pstat;             // with r_scaled: the ring's max priority after the update, its ** alpha
-  double alpha;
-  const uint64_t* rng_from;  // parity loop, early PER sample: the stream state to commit
-  uint64_t* rng_to;
-};
+struct Learn;
+
 
 __device__ __forceinline__ void trace_mark(unsigned long long* tr, int& k) {
   if (tr && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -142,9 +88,10 @@ __device__ __forceinline__ void trace_arrive(unsigned long long* tr, int k) {
 }
 
 // grid-wide barrier (all CTAs co-resident: cooperative launch).  bar[0] counts arrivals
-// monotonically (it stays a multiple of the grid size between launches): one release add per
-// CTA, then acquire loads until the count reaches the next multiple.  The CTA barrier before
-// the add orders every thread's writes before thread 0's release (cumulativity).
+// monotonically (it stays a multiple of the grid size between launches, so one barrier buffer
+// must always see the same grid size: launch() enforces it): one release add per CTA, then
+// relaxed loads until the count reaches the next multiple.  The CTA barrier before the add
+// orders every thread's writes before thread 0's release (cumulativity).
 __device__ __forceinline__ void grid_sync(unsigned* bar) {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -174,7 +121,7 @@ struct AOp {
   int split;
   int trans;
   int ones_at;  // trans only: row m == ones_at reads 1.0 (bias gradient as one more output row), -1 none
-  __device__ __forceinline__ const float* row(int r) const {
+  __host__ __device__ __forceinline__ const float* row(int r) const {
     if (!idx) return p + (int64_t)r * sr;
     return r < split ? p0 + (int64_t)idx[r] * sr : p1 + (int64_t)idx[r - split] * sr;
   }
@@ -203,14 +150,87 @@ struct Job {
   // Adam epilogue (weight-gradient jobs, which sum the whole batch inside one tile): C is
   // the gradient block of the parameters at flat offset `eoff`; the tile also applies Adam
   // to them and, with `wt`, writes rows < wt_rows of the transposed copy
-  const Learn* lp;
+  int adam;
   int64_t eoff;
-  float c1, c2;
   float* wt;
   int64_t wt_ld;
   int wt_rows;
-  __device__ __forceinline__ int tm() const { return (kWarps / kg) * rpt; }
-  __device__ __forceinline__ int tiles() const { return ((M + tm() - 1) / tm()) * ((N + kTN - 1) / kTN); }
+  __host__ __device__ __forceinline__ int tm() const { return (kWarps / kg) * rpt; }
+  __host__ __device__ __forceinline__ int tiles() const { return ((M + tm() - 1) / tm()) * ((N + kTN - 1) / kTN); }
+};
+
+static_assert(sizeof(Job) % 4 == 0, "jobs are copied as 32-bit words");
+constexpr int kMaxPhases = 2 * kMaxLayers + 2;  // L forwards, wide head, head backward, L backwards
+
+struct Phase {
+  Job jobs[3];
+  int nj;
+};
+
+struct Learn {
+  int L, A, B, rows_fwd;  // rows_fwd: forward mode row count (learn mode: 0)
+  int d[kMaxLayers + 2];  // d[0] state dim, d[1..L] hidden widths, d[L+1] = 1 + A
+  float* p;               // online flat parameters (updated in place)
+  const float* tp;        // target flat parameters
+  int64_t w_off[kMaxLayers + 1], b_off[kMaxLayers + 1];
+  // replay ring and PER sample
+  const float* r_states;
+  const float* r_next;
+  int64_t r_ld;
+  const int32_t* r_actions;
+  const float* r_rewards;
+  const uint8_t* r_done;
+  const uint8_t* r_mask;
+  double* r_prio;
+  const int32_t* idx;
+  const float* isw;
+  float gamma, delta;
+  // Adam
+  float* grad;
+  float* m;
+  float* v;
+  int64_t nparams;
+  float lr, b1, b2, eps, c1, c2;
+  const float* ctab;  // optional bias-correction table (parity loop), see ap_dqn_adam_tab
+  const int64_t* ctl;
+  int64_t t_offset;
+  float* wt[kMaxLayers + 1];  // transposed copies [d_{i+1}, ld] of w_i (and the head)
+  int64_t wt_ld[kMaxLayers + 1];
+  // outputs
+  float* td;
+  float* loss;  // sum_b w_b * huber_b
+  float* q_out;  // forward mode: [rows, A]
+  const float* x_in;  // forward mode: [rows, x_ld]
+  int64_t x_ld;
+  // workspace
+  float* ws;
+  unsigned* bar;
+  unsigned long long* trace;  // optional: %globaltimer after each phase (CTA 0)
+  // planned on the host (plan_phases): every phase's tile jobs and the workspace carve-up
+  Phase ph[kMaxPhases];
+  int nph;
+  float* Hon[kMaxLayers + 1];
+  float* Htg[kMaxLayers + 1];
+  float* dh[kMaxLayers + 1];
+  float *zon, *ztg, *dz, *lrow;
+  int64_t gate;               // > 0: no-op while ctl[AP_CTL_SIZE] < gate (self-gated loop body)
+  // forward mode, parity loop: the epsilon-greedy act on row 0's Q (parity_act.cuh)
+  int act;
+  ap_parity_loop pl;
+  int32_t* action;
+  // parity-loop tail: loss log, train counter, target sync (see ap_fused_learn)
+  int64_t* tail_ctl;
+  float* loss_log;
+  int64_t loss_cap;
+  int sync_every, sync_n;
+  const float* sync_src[6];
+  float* sync_dst[6];
+  int64_t sync_count[6];
+  double* r_scaled;          // optional: priorities ** alpha, updated with each priority
+  double* pstat;             // with r_scaled: the ring's max priority after the update, its ** alpha
+  double alpha;
+  const uint64_t* rng_from;  // parity loop, early PER sample: the stream state to commit
+  uint64_t* rng_to;
 };
 
 __device__ __forceinline__ void cp_async16(float* smem_dst, const float* gsrc) {
@@ -233,9 +253,9 @@ constexpr int kBS = kTN + 4;  // B tile row stride (floats): 16-byte rows, confl
 // (out of line, like run_jobs: one copy of each variant instead of one per phase keeps the
 // kernel's code small enough for the instruction caches)
 template <int RPT, int KG, int TRANS>
-__device__ __noinline__ void run_tile(const Job& jref, int t, float* smem) {
+__device__ __noinline__ void run_tile(const Job& jref, int t, float* smem, const Learn& P, float c1, float c2) {
   TT(0);
-  const Job& j = jref;  // in shared memory (Frame)
+  const Job& j = jref;  // in shared memory (run_jobs)
   constexpr int RW = kWarps / KG;  // row-warps
   constexpr int TM = RW * RPT;
   const int ntn = (j.N + kTN - 1) / kTN;
@@ -255,14 +275,25 @@ __device__ __noinline__ void run_tile(const Job& jref, int t, float* smem) {
     __syncthreads();
     // ---- A
     if (!TRANS) {
-      for (int rr = warp; rr < TM; rr += kThreads / 32) {
-        const int m = m0 + rr;
+      // this warp's row pointers first: gathered rows read their ring index from global
+      // memory, so all of them are in flight together instead of one round trip per row
+      constexpr int RPW = (TM + kWarps - 1) / kWarps;
+      const float* rows[RPW];
+#pragma unroll
+      for (int q = 0; q < RPW; ++q) {
+        const int rr = warp + q * kWarps, m = m0 + rr;
+        rows[q] = (rr < TM && m < j.M) ? j.a.row(m) : nullptr;
+      }
+#pragma unroll
+      for (int q = 0; q < RPW; ++q) {
+        const int rr = warp + q * kWarps;
+        if (rr >= TM) break;
         float* dst = As + rr * kcp;
-        if (m >= j.M) {
+        if (!rows[q]) {
           for (int kk = lane; kk < kcp; kk += 32) dst[kk] = 0.0f;
           continue;
         }
-        const float* src = j.a.row(m) + k0;
+        const float* src = rows[q] + k0;
         if (al16(src)) {
           const int k4 = kc & ~3;
           for (int kk = 4 * lane; kk < k4; kk += 128) cp_async16(dst + kk, src + kk);
@@ -331,6 +362,7 @@ __device__ __noinline__ void run_tile(const Job& jref, int t, float* smem) {
     const int klo = kgi * seg, khi = min(kcp, klo + seg);
     const float* bcol = Bs + c;
     if (!TRANS) {
+#pragma unroll 2
       for (int kk = klo; kk < khi; kk += 4) {
         const float b0 = bcol[kk * kBS], b1 = bcol[(kk + 1) * kBS], b2 = bcol[(kk + 2) * kBS],
                     b3 = bcol[(kk + 3) * kBS];
@@ -382,7 +414,7 @@ __device__ __noinline__ void run_tile(const Job& jref, int t, float* smem) {
       mk[q] = m < j.M ? __ldcg(j.mask + (int64_t)m * j.ldmask + n) : 0.0f;
     }
   }
-  if (!j.lp) {
+  if (!j.adam) {
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
       const int m = m0 + rw + RW * q;
@@ -393,11 +425,10 @@ __device__ __noinline__ void run_tile(const Job& jref, int t, float* smem) {
       j.c[(int64_t)m * j.ldc + n] = v;
     }
   } else {  // Adam (agent.py:229-250) on the finished gradient
-    const Learn& P = *j.lp;
     float* const pm = P.m + j.eoff;
     float* const pv = P.v + j.eoff;
     float* const pp = P.p + j.eoff;
-    const float b1 = P.b1, b2 = P.b2, lr = P.lr, eps = P.eps, c1 = j.c1, c2 = j.c2;
+    const float b1 = P.b1, b2 = P.b2, lr = P.lr, eps = P.eps;
     float om[RPT], ov[RPT], op[RPT];
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
@@ -426,42 +457,52 @@ __device__ __noinline__ void run_tile(const Job& jref, int t, float* smem) {
 }
 
 template <int TRANS>
-__device__ __forceinline__ void run_tile_cfg(const Job& j, int t, float* smem) {
+__device__ __forceinline__ void run_tile_cfg(const Job& j, int t, float* smem, const Learn& P, float c1, float c2) {
   switch (j.rpt * 16 + j.kg) {
-    case 1 * 16 + 1: run_tile<1, 1, TRANS>(j, t, smem); break;
-    case 2 * 16 + 1: run_tile<2, 1, TRANS>(j, t, smem); break;
-    case 4 * 16 + 1: run_tile<4, 1, TRANS>(j, t, smem); break;
-    case 8 * 16 + 1: run_tile<8, 1, TRANS>(j, t, smem); break;
-    case 1 * 16 + 2: run_tile<1, 2, TRANS>(j, t, smem); break;
-    case 2 * 16 + 2: run_tile<2, 2, TRANS>(j, t, smem); break;
-    case 4 * 16 + 2: run_tile<4, 2, TRANS>(j, t, smem); break;
-    case 1 * 16 + 4: run_tile<1, 4, TRANS>(j, t, smem); break;
-    case 2 * 16 + 4: run_tile<2, 4, TRANS>(j, t, smem); break;
-    case 4 * 16 + 4: run_tile<4, 4, TRANS>(j, t, smem); break;
-    case 1 * 16 + 8: run_tile<1, 8, TRANS>(j, t, smem); break;
-    case 2 * 16 + 8: run_tile<2, 8, TRANS>(j, t, smem); break;
-    default: run_tile<1, 8, TRANS>(j, t, smem); break;
+    case 1 * 16 + 1: run_tile<1, 1, TRANS>(j, t, smem, P, c1, c2); break;
+    case 2 * 16 + 1: run_tile<2, 1, TRANS>(j, t, smem, P, c1, c2); break;
+    case 4 * 16 + 1: run_tile<4, 1, TRANS>(j, t, smem, P, c1, c2); break;
+    case 8 * 16 + 1: run_tile<8, 1, TRANS>(j, t, smem, P, c1, c2); break;
+    case 1 * 16 + 2: run_tile<1, 2, TRANS>(j, t, smem, P, c1, c2); break;
+    case 2 * 16 + 2: run_tile<2, 2, TRANS>(j, t, smem, P, c1, c2); break;
+    case 4 * 16 + 2: run_tile<4, 2, TRANS>(j, t, smem, P, c1, c2); break;
+    case 1 * 16 + 4: run_tile<1, 4, TRANS>(j, t, smem, P, c1, c2); break;
+    case 2 * 16 + 4: run_tile<2, 4, TRANS>(j, t, smem, P, c1, c2); break;
+    case 4 * 16 + 4: run_tile<4, 4, TRANS>(j, t, smem, P, c1, c2); break;
+    case 1 * 16 + 8: run_tile<1, 8, TRANS>(j, t, smem, P, c1, c2); break;
+    case 2 * 16 + 8: run_tile<2, 8, TRANS>(j, t, smem, P, c1, c2); break;
+    default: run_tile<1, 8, TRANS>(j, t, smem, P, c1, c2); break;
   }
 }
 
 // all tiles of up to 3 independent jobs, spread over the grid
-__device__ __noinline__ void run_jobs(const Job* jobs, int nj, float* smem) {
+__device__ __noinline__ void run_jobs(const Job* pjobs, int nj, float* smem, const Learn& P, float c1 = 1.0f,
+                                      float c2 = 1.0f) {
+  // the phase's jobs from the kernel parameters into shared memory (the tile loops reread job
+  // fields around their asynchronous copies; shared-memory reads are the cheap ones)
+  __shared__ Job jobs[3];
+  {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(pjobs);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(jobs);
+    for (int e = threadIdx.x; e < nj * (int)(sizeof(Job) / 4); e += blockDim.x) dst[e] = src[e];
+  }
+  __syncthreads();
   int total = 0;
   for (int i = 0; i < nj; ++i) total += jobs[i].tiles();
   for (int t = blockIdx.x; t < total; t += gridDim.x) {
     int k = t, i = 0;
     while (k >= jobs[i].tiles()) k -= jobs[i].tiles(), ++i;
     if (jobs[i].a.trans)
-      run_tile_cfg<1>(jobs[i], k, smem);
+      run_tile_cfg<1>(jobs[i], k, smem, P, c1, c2);
     else
-      run_tile_cfg<0>(jobs[i], k, smem);
+      run_tile_cfg<0>(jobs[i], k, smem, P, c1, c2);
   }
 }
 
 // Tile shapes of one phase: the smallest row count per tile whose tiles fit one wave of a
 // reference 148-SM grid, then row-warps x K-groups for that height (K-groups when K is long).
 // A fixed reference grid keeps every summation order a function of the problem alone.
-__device__ void plan_tiles(Job* jobs, int nj) {
+__host__ __device__ void plan_tiles(Job* jobs, int nj) {
   constexpr int kRefGrid = 148;
   int lvl = 0;
   for (; lvl < 6; ++lvl) {
@@ -777,25 +818,176 @@ __device__ __noinline__ void small_forward(const Learn& P, float* smem) {
   }
 }
 
-// Per-CTA control state in shared memory, written by thread 0: the phase's jobs and the
-// workspace pointers.  (As per-thread locals these were 2 KB of stack per thread, 0.5 MB per
-// CTA, far past the L1 left beside 224 KB of shared memory: every phase setup went to L2.)
-struct Frame {
-  Job jobs[3];
-  int nj;
-  float* Hon[kMaxLayers + 1];
-  float* Htg[kMaxLayers + 1];
-  float* dh[kMaxLayers + 1];
-  float *zon, *ztg, *dz, *lrow;
-};
-
-__device__ __forceinline__ AOp rows_of(const float* p, int64_t sr) {
+__host__ __device__ __forceinline__ AOp rows_of(const float* p, int64_t sr) {
   return AOp{p, sr, nullptr, nullptr, nullptr, 0, 0, -1};
+}
+
+// Every phase's jobs and the workspace carve-up, planned once on the host (they depend on the
+// network, the batch and the buffers only) and read by the kernel from its parameters: no
+// per-phase setup on the critical path.  Phase order: the L forward layers, the wide head's
+// forward (heads of > 7 actions), the head backward (wide heads), the L backward layers.
+void plan_phases(Learn& P) {
+  const int L = P.L, A1 = P.A + 1;
+  const bool fwd_only = P.rows_fwd > 0;
+  const int B = fwd_only ? P.rows_fwd : P.B;
+  const int Ron = fwd_only ? B : 2 * B;  // online rows: [next; cur]
+  // workspace: online activations [Ron, d_i], target activations [B, d_i] (i = 1..L),
+  // head outputs, dz, dh_i [B, d_i], the per-row loss terms
+  float* ws = P.ws;
+  for (int i = 1; i <= L; ++i) {
+    P.Hon[i] = ws;
+    ws += (int64_t)Ron * P.d[i];
+    P.Htg[i] = ws;
+    ws += (int64_t)B * P.d[i];
+    P.dh[i] = ws;
+    ws += (int64_t)B * P.d[i];
+  }
+  P.zon = ws;
+  ws += (int64_t)Ron * A1;
+  P.ztg = ws;
+  ws += (int64_t)B * A1;
+  P.dz = ws;
+  ws += (int64_t)B * A1;
+  P.lrow = ws;
+  P.nph = 0;
+  // forward, layer by layer
+  for (int i = 0; i < L; ++i) {
+    Phase& ph = P.ph[P.nph++];
+    const int K = P.d[i], N = P.d[i + 1];
+    ph.nj = 0;
+    Job& on = ph.jobs[ph.nj++];
+    on = Job{};
+    if (i == 0)
+      on.a = fwd_only ? rows_of(P.x_in, P.x_ld) : AOp{nullptr, P.r_ld, P.r_next, P.r_states, P.idx, B, 0, -1};
+    else
+      on.a = rows_of(P.Hon[i], P.d[i]);
+    on.b = BOp{P.p + P.w_off[i], N, 1};
+    on.c = P.Hon[i + 1];
+    on.ldc = N;
+    on.M = Ron, on.N = N, on.K = K;
+    on.bias = P.p + P.b_off[i];
+    on.epi = 1;
+    if (!fwd_only) {
+      Job& tg = ph.jobs[ph.nj++];
+      tg = on;
+      tg.a = i == 0 ? AOp{nullptr, P.r_ld, P.r_next, P.r_next, P.idx, B, 0, -1} : rows_of(P.Htg[i], P.d[i]);
+      tg.b = BOp{P.tp + P.w_off[i], N, 1};
+      tg.c = P.Htg[i + 1];
+      tg.M = B;
+      tg.bias = P.tp + P.b_off[i];
+    }
+    plan_tiles(ph.jobs, ph.nj);
+  }
+  const int H = P.d[L];
+  const bool small_head = A1 <= 8;
+  if (!small_head) {  // head outputs as tiles over the grid
+    Phase& ph = P.ph[P.nph++];
+    ph.nj = 0;
+    Job& on = ph.jobs[ph.nj++];
+    on = Job{};
+    on.a = rows_of(P.Hon[L], H);
+    on.b = BOp{P.p + P.w_off[L], A1, 1};
+    on.c = P.zon;
+    on.ldc = A1;
+    on.M = Ron, on.N = A1, on.K = H;
+    on.bias = P.p + P.b_off[L];
+    if (!fwd_only) {
+      Job& tg = ph.jobs[ph.nj++];
+      tg = on;
+      tg.a = rows_of(P.Htg[L], H);
+      tg.b = BOp{P.tp + P.w_off[L], A1, 1};
+      tg.c = P.ztg;
+      tg.M = B;
+      tg.bias = P.tp + P.b_off[L];
+    }
+    plan_tiles(ph.jobs, ph.nj);
+  }
+  if (fwd_only) return;
+  // Each weight-gradient tile sums the whole batch, so it applies Adam itself; a weight's
+  // transposed copy is refreshed one phase later when a dgrad of its own phase reads it.
+  auto with_adam = [&](Job& j, int s, bool direct_wt) {
+    j.adam = 1;
+    j.eoff = P.w_off[s];
+    j.wt = direct_wt ? P.wt[s] : nullptr;
+    j.wt_ld = P.wt_ld[s];
+    j.wt_rows = P.d[s];
+  };
+  const float* Hc = P.Hon[L] + (int64_t)B * H;  // current-state rows of the last hidden layer
+  if (!small_head) {
+    // head backward: gWh = H_L(cur)^T dz, gbh, dh_L = relu'(H_L) * (dz Wh^T); Adam on Wh, bh.
+    // (Small heads: dh_L comes with the TD rows and gWh joins the next phase.)
+    Phase& ph = P.ph[P.nph++];
+    ph.nj = 2;
+    Job& wg = ph.jobs[0];
+    wg = Job{};
+    // (m=j, k=b) = Hc[b][j]; row H of ones: the bias gradient lands right after gWh (bh follows wh)
+    wg.a = AOp{Hc, H, nullptr, nullptr, nullptr, 0, 1, H};
+    wg.b = BOp{P.dz, A1, 1};
+    wg.c = P.grad + P.w_off[L];
+    wg.ldc = A1;
+    wg.M = H + 1, wg.N = A1, wg.K = B;
+    with_adam(wg, L, false);
+    Job& dg = ph.jobs[1];
+    dg = Job{};
+    dg.a = rows_of(P.dz, A1);
+    // (k=a, n=j) = Wh[j][a]: rows of the transposed copy (the pre-update weights)
+    dg.b = BOp{P.wt[L], P.wt_ld[L], 1};
+    dg.c = P.dh[L];
+    dg.ldc = H;
+    dg.M = B, dg.N = H, dg.K = A1;
+    dg.epi = 2;
+    dg.mask = Hc;
+    dg.ldmask = H;
+    plan_tiles(ph.jobs, 2);
+  }
+  // hidden layers, last to first: gW_{i-1} (+ Adam), dh_{i-1}
+  for (int i = L; i >= 1; --i) {
+    Phase& ph = P.ph[P.nph++];
+    const int din = P.d[i - 1], dout = P.d[i];
+    ph.nj = 0;
+    Job& wg = ph.jobs[ph.nj++];
+    wg = Job{};
+    // (m=p, k=b) = input row b, column p; row din of ones gives gb right after gW (b_i follows w_i)
+    if (i == 1)
+      wg.a = AOp{nullptr, P.r_ld, P.r_states, P.r_states, P.idx, B, 1, din};
+    else
+      wg.a = AOp{P.Hon[i - 1] + (int64_t)B * din, din, nullptr, nullptr, nullptr, 0, 1, din};
+    wg.b = BOp{P.dh[i], dout, 1};
+    wg.c = P.grad + P.w_off[i - 1];
+    wg.ldc = dout;
+    wg.M = din + 1, wg.N = dout, wg.K = B;
+    with_adam(wg, i - 1, i == 1);  // no dgrad reads w_0's copy: written directly
+    if (i > 1) {
+      Job& dg = ph.jobs[ph.nj++];
+      dg = Job{};
+      dg.a = rows_of(P.dh[i], dout);
+      // (k=q, n=p) = W[p][q] = row q of the transposed copy (pre-update)
+      dg.b = BOp{P.wt[i - 1], P.wt_ld[i - 1], 1};
+      dg.c = P.dh[i - 1];
+      dg.ldc = din;
+      dg.M = B, dg.N = din, dg.K = dout;
+      dg.epi = 2;
+      dg.mask = P.Hon[i - 1] + (int64_t)B * din;
+      dg.ldmask = din;
+    }
+    if (i == L && small_head) {
+      // gWh = H_L(cur)^T dz + Adam; no job of this phase reads the head's transposed copy, so
+      // the epilogue writes it directly
+      Job& hg = ph.jobs[ph.nj++];
+      hg = Job{};
+      hg.a = AOp{Hc, H, nullptr, nullptr, nullptr, 0, 1, H};
+      hg.b = BOp{P.dz, A1, 1};
+      hg.c = P.grad + P.w_off[L];
+      hg.ldc = A1;
+      hg.M = H + 1, hg.N = A1, hg.K = B;
+      with_adam(hg, L, true);
+    }
+    plan_tiles(ph.jobs, ph.nj);
+  }
 }
 
 __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const __grid_constant__ Learn P) {
   extern __shared__ float smem[];
-  __shared__ Frame F;
   // every CTA alike (no barrier is entered): the self-gated loop body's learn waits for a full
   // batch in the ring and stops with the loop (act of the step saw the budget spent)
   if (P.gate > 0 && (P.ctl[AP_CTL_SIZE] < P.gate || !P.ctl[AP_PL_ACTIVE])) return;
@@ -831,90 +1023,21 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const __grid_con
     }
     return;
   }
-  if (t0) {
-    // workspace: online activations [Ron, d_i], target activations [B, d_i] (i = 1..L),
-    // head outputs, dz, dh_i [B, d_i], the per-row loss terms
-    float* ws = P.ws;
-    for (int i = 1; i <= L; ++i) {
-      F.Hon[i] = ws;
-      ws += (int64_t)Ron * P.d[i];
-      F.Htg[i] = ws;
-      ws += (int64_t)B * P.d[i];
-      F.dh[i] = ws;
-      ws += (int64_t)B * P.d[i];
-    }
-    F.zon = ws;
-    ws += (int64_t)Ron * A1;
-    F.ztg = ws;
-    ws += (int64_t)B * A1;
-    F.dz = ws;
-    ws += (int64_t)B * A1;
-    F.lrow = ws;
-  }
-
+  int ph = 0;
   // forward, layer by layer
-  for (int i = 0; i < L; ++i) {
-    if (t0) {
-      const int K = P.d[i], N = P.d[i + 1];
-      F.nj = 0;
-      Job& on = F.jobs[F.nj++];
-      on = Job{};
-      if (i == 0)
-        on.a = fwd_only ? rows_of(P.x_in, P.x_ld) : AOp{nullptr, P.r_ld, P.r_next, P.r_states, P.idx, B, 0, -1};
-      else
-        on.a = rows_of(F.Hon[i], P.d[i]);
-      on.b = BOp{P.p + P.w_off[i], N, 1};
-      on.c = F.Hon[i + 1];
-      on.ldc = N;
-      on.M = Ron, on.N = N, on.K = K;
-      on.bias = P.p + P.b_off[i];
-      on.epi = 1;
-      if (!fwd_only) {
-        Job& tg = F.jobs[F.nj++];
-        tg = on;
-        tg.a = i == 0 ? AOp{nullptr, P.r_ld, P.r_next, P.r_next, P.idx, B, 0, -1} : rows_of(F.Htg[i], P.d[i]);
-        tg.b = BOp{P.tp + P.w_off[i], N, 1};
-        tg.c = F.Htg[i + 1];
-        tg.M = B;
-        tg.bias = P.tp + P.b_off[i];
-      }
-      plan_tiles(F.jobs, F.nj);
-    }
-    __syncthreads();
-    run_jobs(F.jobs, F.nj, smem);
+  for (int i = 0; i < L; ++i, ++ph) {
+    run_jobs(P.ph[ph].jobs, P.ph[ph].nj, smem, P);
     trace_arrive(P.trace, tk);
     grid_sync(P.bar);
     trace_mark(P.trace, tk);
   }
-
   // head outputs: wide heads as tiles over the grid (then a barrier), small heads inside the
   // per-row step below (one warp computes its row's 1 or 3 head rows itself)
   const int H = P.d[L];
   const bool small_head = A1 <= 8;
   if (!small_head) {
-    if (t0) {
-      F.nj = 0;
-      Job& on = F.jobs[F.nj++];
-      on = Job{};
-      on.a = rows_of(F.Hon[L], H);
-      on.b = BOp{P.p + P.w_off[L], A1, 1};
-      on.c = F.zon;
-      on.ldc = A1;
-      on.M = Ron, on.N = A1, on.K = H;
-      on.bias = P.p + P.b_off[L];
-      if (!fwd_only) {
-        Job& tg = F.jobs[F.nj++];
-        tg = on;
-        tg.a = rows_of(F.Htg[L], H);
-        tg.b = BOp{P.tp + P.w_off[L], A1, 1};
-        tg.c = F.ztg;
-        tg.M = B;
-        tg.bias = P.tp + P.b_off[L];
-      }
-      plan_tiles(F.jobs, F.nj);
-    }
-    __syncthreads();
-    run_jobs(F.jobs, F.nj, smem);
+    run_jobs(P.ph[ph].jobs, P.ph[ph].nj, smem, P);
+    ++ph;
     trace_arrive(P.trace, tk);
     grid_sync(P.bar);
     trace_mark(P.trace, tk);
@@ -922,17 +1045,17 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const __grid_con
   {
     const int lane = threadIdx.x & 31;
     const int gw = blockIdx.x * kWarps + (threadIdx.x >> 5), nw = gridDim.x * kWarps;
-    float* const zon = F.zon;
-    float* const ztg = F.ztg;
-    float* const dz = F.dz;
-    const float* const HonL = F.Hon[L];
-    const float* const HtgL = F.Htg[L];
+    float* const zon = P.zon;
+    float* const ztg = P.ztg;
+    float* const dz = P.dz;
+    const float* const HonL = P.Hon[L];
+    const float* const HtgL = P.Htg[L];
     for (int r = gw; r < (fwd_only ? Ron : B); r += nw) {
       if (small_head) {
         if (A1 <= 3)
-          small_head_row<3>(P, r, B, HonL, HtgL, dz, F.lrow, F.dh[L], fwd_only);
+          small_head_row<3>(P, r, B, HonL, HtgL, dz, P.lrow, P.dh[L], fwd_only);
         else
-          small_head_row<8>(P, r, B, HonL, HtgL, dz, F.lrow, F.dh[L], fwd_only);
+          small_head_row<8>(P, r, B, HonL, HtgL, dz, P.lrow, P.dh[L], fwd_only);
         continue;
       }
       if (fwd_only) {
@@ -998,7 +1121,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const __grid_con
       later = __any_sync(0xffffffffu, later);
       if (lane == 0) {
         P.td[b] = tdv;
-        F.lrow[b] = w * hub;
+        P.lrow[b] = w * hub;
         if (!later) {
       const double pr = fabs((double)tdv) + 1e-6;
       P.r_prio[row] = pr;
@@ -1032,7 +1155,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const __grid_con
   }
   if (blockIdx.x == 0 && threadIdx.x < 32) {  // fixed-order sum; the terms loaded in parallel
     float* sl = smem + kSmemFloats - 256;       // (past every tile's footprint in this phase)
-    for (int b = threadIdx.x; b < B; b += 32) sl[b] = __ldcg(F.lrow + b);
+    for (int b = threadIdx.x; b < B; b += 32) sl[b] = __ldcg(P.lrow + b);
     __syncwarp();
     if (threadIdx.x == 0) {
       float s = 0.0f;
@@ -1048,16 +1171,6 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const __grid_con
     c1 = P.ctab[2 * k];
     c2 = P.ctab[2 * k + 1];
   }
-  // Each weight-gradient tile sums the whole batch, so it applies Adam itself; a weight's
-  // transposed copy is refreshed one phase later when a dgrad of its own phase reads it.
-  auto with_adam = [&](Job& j, int s, bool direct_wt) {
-    j.lp = &P;
-    j.eoff = P.w_off[s];
-    j.c1 = c1, j.c2 = c2;
-    j.wt = direct_wt ? P.wt[s] : nullptr;
-    j.wt_ld = P.wt_ld[s];
-    j.wt_rows = P.d[s];
-  };
   auto refresh_wt = [&](int s) {
     const int rows = P.d[s], cols = P.d[s + 1];
     const float* w = P.p + P.w_off[s];
@@ -1070,94 +1183,18 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const __grid_con
     }
   };
 
-  // head backward: gWh = H_L(cur)^T dz, gbh, dh_L = relu'(H_L) * (dz Wh^T); Adam on Wh, bh.
-  // Small heads: dh_L came with the TD rows and gWh joins the next phase (one barrier less).
-  const bool fold_head = small_head;
-  if (!fold_head) {
-  if (t0) {
-    const float* Hc = F.Hon[L] + (int64_t)B * H;  // current-state rows
-    F.nj = 2;
-    Job& wg = F.jobs[0];
-    wg = Job{};
-    // (m=j, k=b) = Hc[b][j]; row H of ones: the bias gradient lands right after gWh (bh follows wh)
-    wg.a = AOp{Hc, H, nullptr, nullptr, nullptr, 0, 1, H};
-    wg.b = BOp{F.dz, A1, 1};
-    wg.c = P.grad + P.w_off[L];
-    wg.ldc = A1;
-    wg.M = H + 1, wg.N = A1, wg.K = B;
-    with_adam(wg, L, false);
-    Job& dg = F.jobs[1];
-    dg = Job{};
-    dg.a = rows_of(F.dz, A1);
-    // (k=a, n=j) = Wh[j][a]: rows of the transposed copy (the pre-update weights)
-    dg.b = BOp{P.wt[L], P.wt_ld[L], 1};
-    dg.c = F.dh[L];
-    dg.ldc = H;
-    dg.M = B, dg.N = H, dg.K = A1;
-    dg.epi = 2;
-    dg.mask = Hc;
-    dg.ldmask = H;
-    plan_tiles(F.jobs, 2);
+  if (!small_head) {
+    run_jobs(P.ph[ph].jobs, P.ph[ph].nj, smem, P, c1, c2);
+    ++ph;
+    trace_arrive(P.trace, tk);
+    grid_sync(P.bar);
+    trace_mark(P.trace, tk);
   }
-  __syncthreads();
-  run_jobs(F.jobs, F.nj, smem);
-  trace_arrive(P.trace, tk);
-  grid_sync(P.bar);
-  trace_mark(P.trace, tk);
-  }
-
   // hidden layers, last to first: gW_{i-1} (+ Adam), dh_{i-1}; refresh the transposed copy of
   // the weight updated in the phase before
-  for (int i = L; i >= 1; --i) {
-    if (t0) {
-      const int din = P.d[i - 1], dout = P.d[i];
-      F.nj = 0;
-      Job& wg = F.jobs[F.nj++];
-      wg = Job{};
-      // (m=p, k=b) = input row b, column p; row din of ones gives gb right after gW (b_i follows w_i)
-      if (i == 1)
-        wg.a = AOp{nullptr, P.r_ld, P.r_states, P.r_states, P.idx, B, 1, din};
-      else
-        wg.a = AOp{F.Hon[i - 1] + (int64_t)B * din, din, nullptr, nullptr, nullptr, 0, 1, din};
-      wg.b = BOp{F.dh[i], dout, 1};
-      wg.c = P.grad + P.w_off[i - 1];
-      wg.ldc = dout;
-      wg.M = din + 1, wg.N = dout, wg.K = B;
-      with_adam(wg, i - 1, i == 1);  // no dgrad reads w_0's copy: written directly
-      if (i > 1) {
-        Job& dg = F.jobs[F.nj++];
-        dg = Job{};
-        dg.a = rows_of(F.dh[i], dout);
-        // (k=q, n=p) = W[p][q] = row q of the transposed copy (pre-update)
-        dg.b = BOp{P.wt[i - 1], P.wt_ld[i - 1], 1};
-        dg.c = F.dh[i - 1];
-        dg.ldc = din;
-        dg.M = B, dg.N = din, dg.K = dout;
-        dg.epi = 2;
-        dg.mask = F.Hon[i - 1] + (int64_t)B * din;
-        dg.ldmask = din;
-      }
-      if (i == L && fold_head) {
-        // gWh = H_L(cur)^T dz + Adam; no job of this phase reads the head's transposed
-        // copy, so the epilogue writes it directly
-        Job& hg = F.jobs[F.nj++];
-        hg = Job{};
-        hg.a = AOp{F.Hon[L] + (int64_t)B * H, H, nullptr, nullptr, nullptr, 0, 1, H};
-        hg.b = BOp{F.dz, A1, 1};
-        hg.c = P.grad + P.w_off[L];
-        hg.ldc = A1;
-        hg.M = H + 1, hg.N = A1, hg.K = B;
-        with_adam(hg, L, true);
-      }
-      plan_tiles(F.jobs, F.nj);
-    }
-    __syncthreads();
-    run_jobs(F.jobs, F.nj, smem);
-#ifdef AP_FUSED_TILE_TRACE_TWICE  // dev-only timing probe: the same tiles again (warm code and data)
-    __syncthreads();
-    run_jobs(F.jobs, F.nj, smem);
-#endif
-    if (i < L || !fold_head) refresh_wt(i);  // i == L: the head; else w_i (updated in the phase of layer i + 1)
+  for (int i = L; i >= 1; --i, ++ph) {
+    run_jobs(P.ph[ph].jobs, P.ph[ph].nj, smem, P, c1, c2);
+    if (i < L || !small_head) refresh_wt(i);  // i == L: the head; else w_i (updated in the phase of layer i + 1)
     if (i > 1) {
       trace_arrive(P.trace, tk);
       grid_sync(P.bar);
@@ -1206,10 +1243,25 @@ int64_t workspace_floats(int L, const int* d, int B, bool fwd_only) {
   return n;
 }
 
+// grid size each barrier buffer has been used with (grid_sync's counter assumes one size)
+std::mutex g_bar_mu;
+std::unordered_map<const void*, int> g_bar_grid;
+
 int launch(const Learn& P, cudaStream_t stream, int reserve_sms = 0) {
   int sms = 0;
   if (int rc = current_sm_count(&sms)) return rc;
   sms = std::max(1, sms - reserve_sms);
+  {
+    std::lock_guard<std::mutex> lk(g_bar_mu);
+    auto it = g_bar_grid.find(P.bar);
+    if (it == g_bar_grid.end()) {
+      g_bar_grid.emplace(P.bar, sms);
+    } else if (it->second != sms) {
+      set_error("fused kernels: this barrier buffer was used with another grid size (the act of a "
+                "loop with an early PER sample leaves one SM free: give it its own barrier)");
+      return AP_ERR_INVALID;
+    }
+  }
   static PerDeviceMax configured;
   const int smem = kSmemFloats * 4 + 64;
   if (configured.need(current_device(), smem))
@@ -1269,6 +1321,7 @@ int ap_mlp_forward_fused(int32_t L, const int32_t* dims, const int64_t* w_off, c
   P.q_out = q;
   P.ws = workspace;
   P.bar = barrier;
+  plan_phases(P);
   return launch(P, (cudaStream_t)stream);
 }
 
@@ -1369,6 +1422,7 @@ int ap_dqn_learn_fused(const ap_fused_learn* a, void* stream) {
   P.r_scaled = a->r_scaled;
   P.pstat = a->r_scaled ? a->pstat : nullptr;
   P.alpha = a->per_alpha;
+  plan_phases(P);
   return launch(P, (cudaStream_t)stream);
 }
 

@@ -94,6 +94,7 @@ class DeviceSearch:
             "state": torch.zeros((1, env.state_dim), dtype=f32, device=dev),
             "action": torch.zeros(1, dtype=i32, device=dev),
             "q": torch.zeros((1, A), dtype=f32, device=dev),
+            "act_bar": torch.zeros(2, dtype=i32, device=dev),
             "best_row": torch.full((self.ld,), -1, dtype=i8, device=dev),
             "log_action": torch.zeros(steps_per_launch, dtype=i32, device=dev),
             "log_reward": torch.zeros(steps_per_launch, dtype=f64, device=dev),
@@ -144,9 +145,11 @@ class DeviceSearch:
             # forward + epsilon-greedy decision in one launch (the host act's forward arithmetic);
             # it also closes the step once the budget is spent (the body runs several steps)
             Lh, dims, w_off, b_off = net.fused_layout()[:4]
-            ws, bar = net._fused_scratch(256, True)
+            ws = net._fused_scratch(256, True)[0]
+            # own grid barrier: this launch leaves an SM to the sampler (a smaller grid than the
+            # host act's forward, which must not share a barrier counter with it)
             _native.check(lib.ap_parity_act_fused(L, Lh, dims, w_off, b_off, _native.ptr(net.flat),
-                                                  _native.ptr(t["q"]), _native.ptr(ws), _native.ptr(bar),
+                                                  _native.ptr(t["q"]), _native.ptr(ws), _native.ptr(t["act_bar"]),
                                                   _native.ptr(t["action"]), _stream()))
         else:
             q = net.forward_fused(t["state"]) if getattr(net, "fused_act", False) else net.forward_device(t["state"])

@@ -105,9 +105,11 @@ def pieces(reps: int = 20, fill: int = 15):
         B = cfg.batch_size
         S = lambda: _native.stream_handle(self.stream)  # noqa: E731
 
-        def act():
+        def act():  # (without the early sampler: the act would wait for its acknowledgement)
+            self.desc.early_sample = 0  # full grid: the forward's own barrier
             _native.check(lib.ap_parity_act_fused(L, Lh, dmz, w_off, b_off, _native.ptr(net.flat), _native.ptr(t["q"]),
                                                   _native.ptr(ws), _native.ptr(bar), _native.ptr(t["action"]), S()))
+            self.desc.early_sample = 1
 
         def k1():
             self.env._engine.launch(t["seeds_try"][:, : self.n], t["outcome"], None, None, t["status"],

@@ -36,7 +36,7 @@ def main():
     idx = torch.randint(0, len(agent.buffer), (B,), generator=gen, dtype=torch.int32).cuda()
     w = torch.ones(B, dtype=torch.float32, device="cuda")
     grid = torch.cuda.get_device_properties(0).multi_processor_count
-    tr = torch.zeros(64 + 16 * grid, dtype=torch.int64, device="cuda")
+    tr = torch.zeros(max(64 + 16 * grid, 4096 + 8 * 64), dtype=torch.int64, device="cuda")
     fused.desc.trace = tr.data_ptr()
     rows = []
     for r in range(reps + 3):
@@ -59,6 +59,16 @@ def main():
         v = np.median([[x for x in r[1][p]] for r in rows], axis=0) / 1e3
         print(f"phase {p}: {v[0]:7.2f} us   first CTA done {v[1]:6.2f}   last CTA done {v[2]:6.2f}   "
               f"barrier {v[0] - v[2]:5.2f}")
+    # AP_FUSED_TILE_TRACE builds (build_trace_lib.sh): CTA 0's tiles of the last launch, stage
+    # stamps relative to the tile start (loads issued, landed, k-loop done, k-groups added, stored)
+    t = tr.cpu().numpy()
+    tiles = t[4096:4096 + 8 * 64].reshape(64, 8)
+    marks0 = t[0]
+    for i, row in enumerate(tiles):
+        if row[0] == 0:
+            break
+        print(f"tile {i}: start +{(row[0] - marks0) / 1e3:7.2f} us, stages " +
+              " ".join(f"{(row[k] - row[0]) / 1e3:6.2f}" for k in range(1, 6)))
     fused.desc.trace = None
 
 
