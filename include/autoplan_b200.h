@@ -711,6 +711,8 @@ typedef struct ap_fused_learn {
   double* r_scaled;         /* optional [cap]: r_scaled[idx] = (|td| + 1e-6) ** per_alpha with each priority */
   double* pstat;            /* with r_scaled: [2] the ring's max priority after the update, its ** per_alpha */
   double per_alpha;
+  int32_t lazy_wt0;         /* 1: leave the first layer's transposed copy stale (no fused kernel reads
+                               it; the caller refreshes it, e.g. after a device-loop launch) */
   const uint64_t* rng_from; /* optional (tail mode): copied to rng_to (6 words) when the step learns */
   uint64_t* rng_to;
 } ap_fused_learn;

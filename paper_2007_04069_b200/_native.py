@@ -145,7 +145,7 @@ class FusedLearnDesc(ctypes.Structure):
         ("sync_every", ctypes.c_int32), ("sync_n", ctypes.c_int32), ("sync_src", ctypes.c_void_p * 6),
         ("sync_dst", ctypes.c_void_p * 6), ("sync_count", ctypes.c_int64 * 6),
         ("r_scaled", ctypes.c_void_p), ("pstat", ctypes.c_void_p), ("per_alpha", ctypes.c_double),
-        ("rng_from", ctypes.c_void_p), ("rng_to", ctypes.c_void_p),
+        ("lazy_wt0", ctypes.c_int32), ("rng_from", ctypes.c_void_p), ("rng_to", ctypes.c_void_p),
     ]
 PL = {"STEP": 0, "SLOT": 1, "SIZE": 2, "TRAIN": 3, "EPISODES": 4, "BUDGET": 5, "MAX_STEPS": 6, "POS": 7,
       "EP_STEPS": 8, "BEST_PART": 9, "BEST_EP": 10, "SYNC": 11, "T_POS": 12, "EP_BASE": 13, "TRAIN0": 14,

@@ -729,7 +729,7 @@ class FusedLearnState:
             loss=P(self.loss), workspace=P(self.ws), barrier=P(self.bar))
 
     def run(self, idx, weights, correct1=1.0, correct2=1.0, ctab=None, ctl=None, t_offset=0, gate=0, tail=None,
-            scaled=None, pstat=None, alpha=0.0):
+            scaled=None, pstat=None, alpha=0.0, lazy_wt0=False):
         """One learn step.  `tail` (parity loop): (loss_log, loss_cap, sync_every, [(src, dst, count)]
         [, (rng_from, rng_to)]) -- the kernel also logs the loss, advances ctl's train counter,
         syncs the target and commits the early PER sample's random-stream state."""
@@ -745,6 +745,7 @@ class FusedLearnState:
         # optional priorities ** alpha cache kept current with each new priority (the device loop's PER sample)
         d.r_scaled, d.per_alpha = (None, 0.0) if scaled is None else (scaled.data_ptr(), float(alpha))
         d.pstat = None if pstat is None else pstat.data_ptr()
+        d.lazy_wt0 = int(lazy_wt0)
         if tail is None:
             d.tail_ctl = None
         else:

@@ -226,6 +226,7 @@ struct Learn {
   const float* sync_src[6];
   float* sync_dst[6];
   int64_t sync_count[6];
+  int lazy_wt0;              // the first layer's transposed copy is refreshed by the caller
   double* r_scaled;          // optional: priorities ** alpha, updated with each priority
   double* pstat;             // with r_scaled: the ring's max priority after the update, its ** alpha
   double alpha;
@@ -303,13 +304,25 @@ __device__ __noinline__ void run_tile(const Job& jref, int t, float* smem, const
         }
       }
     } else {
-      for (int kk = warp; kk < kcp; kk += kThreads / 32) {
+      // source rows of this warp's k steps, one per lane, fetched together (gathered rows read
+      // their ring index from global memory) and handed out by shuffles
+      const float* lrow = nullptr;
+      {
+        const int kk = warp + kWarps * lane;
+        if (kk < kc) lrow = j.a.row(k0 + kk);
+      }
+      int it = 0;
+      for (int kk = warp; kk < kcp; kk += kThreads / 32, ++it) {
         float* dst = As + kk * TM;
         if (kk >= kc) {
           for (int rr = lane; rr < TM; rr += 32) dst[rr] = 0.0f;
           continue;
         }
-        const float* src = j.a.row(k0 + kk) + m0;
+        const float* rowp =
+            it < 32 ? reinterpret_cast<const float*>(__shfl_sync(
+                          0xffffffffu, static_cast<unsigned long long>(reinterpret_cast<uintptr_t>(lrow)), it))
+                    : j.a.row(k0 + kk);
+        const float* src = rowp + m0;
         const int mdata = j.a.ones_at >= 0 ? j.a.ones_at : j.M;
         if ((TM & 3) == 0 && al16(src) && m0 + TM <= mdata) {
           for (int rr = 4 * lane; rr < TM; rr += 128) cp_async16(dst + rr, src + rr);
@@ -415,42 +428,51 @@ __device__ __noinline__ void run_tile(const Job& jref, int t, float* smem, const
     }
   }
   if (!j.adam) {
+    float* __restrict__ const out = j.c;
+    const int64_t ldc = j.ldc;
+    const int M = j.M, epi = j.epi;
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
       const int m = m0 + rw + RW * q;
-      if (m >= j.M) break;
+      if (m >= M) break;
       float v = acc[q] + bias;
-      if (j.epi == 1) v = fmaxf(v, 0.0f);
-      if (j.epi == 2 && !(mk[q] > 0.0f)) v = 0.0f;
-      j.c[(int64_t)m * j.ldc + n] = v;
+      if (epi == 1) v = fmaxf(v, 0.0f);
+      if (epi == 2 && !(mk[q] > 0.0f)) v = 0.0f;
+      out[(int64_t)m * ldc + n] = v;
     }
   } else {  // Adam (agent.py:229-250) on the finished gradient
-    float* const pm = P.m + j.eoff;
-    float* const pv = P.v + j.eoff;
-    float* const pp = P.p + j.eoff;
+    // the job's fields in registers first: the stores below go through generic pointers the
+    // compiler cannot tell apart from the job in shared memory
+    float* __restrict__ const pm = P.m + j.eoff;
+    float* __restrict__ const pv = P.v + j.eoff;
+    float* __restrict__ const pp = P.p + j.eoff;
+    float* __restrict__ const pg = j.c;
+    float* __restrict__ const wt = j.wt;
+    const int64_t ldc = j.ldc, wt_ld = j.wt_ld;
+    const int M = j.M, wt_rows = wt ? j.wt_rows : 0;
     const float b1 = P.b1, b2 = P.b2, lr = P.lr, eps = P.eps;
     float om[RPT], ov[RPT], op[RPT];
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
       const int m = m0 + rw + RW * q;
-      const int64_t e = (int64_t)m * j.ldc + n;
+      const int64_t e = (int64_t)m * ldc + n;
       om[q] = ov[q] = op[q] = 0.0f;
-      if (m < j.M) om[q] = __ldcg(pm + e), ov[q] = __ldcg(pv + e), op[q] = __ldcg(pp + e);
+      if (m < M) om[q] = __ldcg(pm + e), ov[q] = __ldcg(pv + e), op[q] = __ldcg(pp + e);
     }
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
       const int m = m0 + rw + RW * q;
-      if (m >= j.M) break;
+      if (m >= M) break;
       const float v = acc[q] + bias;
-      const int64_t e = (int64_t)m * j.ldc + n;
-      j.c[e] = v;
+      const int64_t e = (int64_t)m * ldc + n;
+      pg[e] = v;
       const float mi = b1 * om[q] + (1.0f - b1) * v;
       const float vi = b2 * ov[q] + (1.0f - b2) * v * v;
       pm[e] = mi;
       pv[e] = vi;
       const float pi = op[q] - lr * (mi / c1) / (sqrtf(vi / c2) + eps);
       pp[e] = pi;
-      if (j.wt && m < j.wt_rows) j.wt[(int64_t)n * j.wt_ld + m] = pi;
+      if (m < wt_rows) wt[(int64_t)n * wt_ld + m] = pi;
     }
   }
   TT(5);
@@ -684,25 +706,35 @@ __device__ __noinline__ void small_head_row(const Learn& P, int r, int B, const 
     for (int k = 0; k < A1M; ++k) dzk[k] = k == 0 ? g : ((k - 1) == a ? g : 0.0f) - g / (float)A;
     const float* hc = HonL + (int64_t)(B + b) * H;
     float* out = dhL + (int64_t)b * H;
-    for (int n = lane; n < H; n += 32) {
-      const float* wrow = w_on + (int64_t)n * A1;
-      float acc = 0.0f;
+    // 8 columns per lane at a time, every load of the block issued before its first use (the
+    // stores of one block could alias the next block's loads for the compiler)
+    constexpr int U = 8;
+    for (int n0 = 0; n0 < H; n0 += 32 * U) {
+      float wv[U][A1M], hv[U];
 #pragma unroll
-      for (int k = 0; k < A1M; ++k)
-        if (k < A1) acc = fmaf(dzk[k], __ldcg(wrow + k), acc);
-      const float v = acc + 0.0f;
-      out[n] = __ldcg(hc + n) > 0.0f ? v : 0.0f;
+      for (int u = 0; u < U; ++u) {
+        const int n = n0 + u * 32 + lane;
+        hv[u] = n < H ? __ldcg(hc + n) : 0.0f;
+#pragma unroll
+        for (int k = 0; k < A1M; ++k) wv[u][k] = (n < H && k < A1) ? __ldcg(w_on + (int64_t)n * A1 + k) : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int n = n0 + u * 32 + lane;
+        float acc = 0.0f;
+#pragma unroll
+        for (int k = 0; k < A1M; ++k)
+          if (k < A1) acc = fmaf(dzk[k], wv[u][k], acc);
+        const float v = acc + 0.0f;
+        if (n < H) out[n] = hv[u] > 0.0f ? v : 0.0f;
+      }
     }
   }
   later = __any_sync(0xffffffffu, later);
   if (lane == 0) {
     P.td[b] = tdv;
     lrow[b] = w * hub;
-    if (!later) {
-      const double pr = fabs((double)tdv) + 1e-6;
-      P.r_prio[row] = pr;
-      if (P.r_scaled) P.r_scaled[row] = pow(pr, P.alpha);
-    }
+    if (!later) P.r_prio[row] = fabs((double)tdv) + 1e-6;
   }
 }
 
@@ -956,7 +988,7 @@ void plan_phases(Learn& P) {
     wg.c = P.grad + P.w_off[i - 1];
     wg.ldc = dout;
     wg.M = din + 1, wg.N = dout, wg.K = B;
-    with_adam(wg, i - 1, i == 1);  // no dgrad reads w_0's copy: written directly
+    with_adam(wg, i - 1, i == 1 && !P.lazy_wt0);  // no dgrad reads w_0's copy: written directly (or left)
     if (i > 1) {
       Job& dg = ph.jobs[ph.nj++];
       dg = Job{};
@@ -1122,11 +1154,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const __grid_con
       if (lane == 0) {
         P.td[b] = tdv;
         P.lrow[b] = w * hub;
-        if (!later) {
-      const double pr = fabs((double)tdv) + 1e-6;
-      P.r_prio[row] = pr;
-      if (P.r_scaled) P.r_scaled[row] = pow(pr, P.alpha);
-    }
+        if (!later) P.r_prio[row] = fabs((double)tdv) + 1e-6;
       }
     }
   }
@@ -1135,8 +1163,13 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const __grid_con
   grid_sync(P.bar);
   trace_mark(P.trace, tk);
   if (P.pstat && blockIdx.x == gridDim.x - 1) {
-    // the ring's max priority after this step's updates (the next push writes it; agent.py:199),
-    // by the last CTA, which the following phases load least
+    // the ring's max priority after this step's updates (the next push writes it; agent.py:199)
+    // and the cached powers of the updated priorities, by the last CTA, which the following
+    // phases load least (duplicate indices write the same final value)
+    for (int b = threadIdx.x; b < B; b += kThreads) {
+      const int64_t row = P.idx[b];
+      P.r_scaled[row] = pow(__ldcg(P.r_prio + row), P.alpha);
+    }
     const int64_t size = P.ctl[AP_CTL_SIZE];
     float* red = smem + kSmemFloats - 512;
     double m = 0.0;
@@ -1420,8 +1453,13 @@ int ap_dqn_learn_fused(const ap_fused_learn* a, void* stream) {
     if (a->rng_from && a->rng_to) P.rng_from = a->rng_from, P.rng_to = a->rng_to;
   }
   P.r_scaled = a->r_scaled;
+  if (a->r_scaled && !a->pstat) {
+    set_error("ap_dqn_learn_fused: the priority-power cache needs pstat");
+    return AP_ERR_INVALID;
+  }
   P.pstat = a->r_scaled ? a->pstat : nullptr;
   P.alpha = a->per_alpha;
+  P.lazy_wt0 = a->lazy_wt0;
   plan_phases(P);
   return launch(P, (cudaStream_t)stream);
 }

