@@ -1302,7 +1302,9 @@ int launch(const Learn& P, cudaStream_t stream, int reserve_sms = 0) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(sms);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem;
+  // the few-row forward (small_forward) needs only its warp-reduction buffer
+  const bool small = P.rows_fwd > 0 && P.rows_fwd <= kSmallRows && P.A + 1 <= 8;
+  cfg.dynamicSmemBytes = small ? kWarps * kSmallRows * kTN * 4 : smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;  // every CTA resident: the grid barriers cannot deadlock

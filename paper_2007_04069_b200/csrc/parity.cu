@@ -234,7 +234,33 @@ __device__ __forceinline__ bool learn_gated_off(const ap_parity_loop& L) {
 // sample (per_sample.cuh) with the priorities and cdf staged in shared memory when they fit.
 // Early mode (see ap_parity_sample): the ring and stream as the step starts, the act's draws
 // replayed, the pending push counted, the read acknowledged, the final stream in rng_next.
-constexpr int kSampleThreads = 1024;
+constexpr int kSampleThreads = 512;  // (128 registers per thread: the cumsum keeps 32 operands in flight)
+
+// PCG64 jump-ahead by k <= kSampleMaxB steps without the square-and-multiply loop:
+// state_k = M^k state_0 + S_k inc with S_k = 1 + M + ... + M^(k-1) (mod 2^128), both tabulated at
+// compile time (w[k] = {M^k hi, lo, S_k hi, lo}).
+struct JumpTable {
+  uint64_t w[kSampleMaxB + 1][4];
+};
+constexpr JumpTable make_jump_table() {
+  JumpTable t{};
+  const u128 mult = ((u128)0x2360ED051FC65DA4ULL << 64) | (u128)0x4385DF649FCCF645ULL;  // pcg_mult()
+  u128 m = 1, sum = 0;
+  for (int k = 0; k <= kSampleMaxB; ++k) {
+    t.w[k][0] = (uint64_t)(m >> 64), t.w[k][1] = (uint64_t)m;
+    t.w[k][2] = (uint64_t)(sum >> 64), t.w[k][3] = (uint64_t)sum;
+    sum = sum * mult + 1;
+    m = m * mult;
+  }
+  return t;
+}
+__constant__ JumpTable g_jump = make_jump_table();
+
+__device__ __forceinline__ u128 pcg_jump(u128 state, u128 inc, int k) {
+  const u128 m = ((u128)g_jump.w[k][0] << 64) | (u128)g_jump.w[k][1];
+  const u128 sum = ((u128)g_jump.w[k][2] << 64) | (u128)g_jump.w[k][3];
+  return m * state + sum * inc;
+}
 
 constexpr int kSampleSmemBytes = 190 * 1024;  // + ~30 KB static <= 227 KB
 
@@ -295,10 +321,20 @@ __global__ void __launch_bounds__(kSampleThreads) parity_sample_kernel(ap_parity
   }
   __syncthreads();
   ST(1);
-  // the B uniforms by the last threads (the first ones sum the pairwise blocks next)
+  // (two inlined copies: with the shared-memory arrays the compiler knows their space)
+  if (staged) {
+    per_total(dyn, S);
+    ST(2);
+    per_cdf(dyn, n, dyn + n, S);
+  } else {
+    per_total(scratch, S);
+    ST(2);
+    per_cdf(scratch, n, scratch + L.cap, S);
+  }
+  // the B uniforms, by the threads the cdf chain leaves idle
   const u128 s0 = ((u128)s_rng[0] << 64) | (u128)s_rng[1], inc = ((u128)s_rng[2] << 64) | (u128)s_rng[3];
-  for (int b = nt - 1 - tid; b >= 0 && b < B; b -= nt) {
-    u128 st = pcg_advance(s0, inc, (uint64_t)b);
+  for (int b = nt - 1 - tid; tid != 0 && b < B; b += nt - 1) {
+    u128 st = pcg_jump(s0, inc, b);
     const double v = pcg_next_double(st, inc);  // draw b: the state after b + 1 steps
     su[b] = v;
     if (u_out) u_out[b] = v;
@@ -309,16 +345,11 @@ __global__ void __launch_bounds__(kSampleThreads) parity_sample_kernel(ap_parity
       if (early) dst[2] = s_rng[2], dst[3] = s_rng[3], dst[4] = s_rng[4], dst[5] = s_rng[5];
     }
   }
-  // (two inlined copies: with the shared-memory arrays the compiler knows their space)
-  if (staged) {
-    per_total(dyn, S);
-    ST(2);
-    per_draw(dyn, n, beta, su, B, dyn + n, idx, w, S);
-  } else {
-    per_total(scratch, S);
-    ST(2);
-    per_draw(scratch, n, beta, su, B, scratch + L.cap, idx, w, S);
-  }
+  __syncthreads();
+  if (staged)
+    per_pick(dyn, n, beta, su, B, dyn + n, idx, w, S);
+  else
+    per_pick(scratch, n, beta, su, B, scratch + L.cap, idx, w, S);
   ST(3);
 }
 

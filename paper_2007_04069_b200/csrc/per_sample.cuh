@@ -140,6 +140,12 @@ __device__ __forceinline__ double np_pairwise_block(const double* x, int m) {
   return v;
 }
 
+// a subtree past the node table's capacity, summed serially (out of line: its stack of
+// recursion frames stays out of the common path)
+__device__ __noinline__ double np_pairwise_serial(const double* x, int64_t n) {
+  return np_pairwise_walk(n, [&](int64_t off, int64_t len) { return np_pairwise_leaf(x + off, len); });
+}
+
 // total = numpy's pairwise sum of scaled[0, n) over the tree of per_tree (every thread; the
 // block sums in parallel, then thread 0 adds the nodes children first).  Ends with a barrier.
 __device__ __forceinline__ void per_total(const double* scaled, PerShared& S) {
@@ -150,11 +156,10 @@ __device__ __forceinline__ void per_total(const double* scaled, PerShared& S) {
     if (c == -1)
       S.node_sum[i] = np_pairwise_block(scaled + S.node_off[i], S.node_len[i]);
     else if (c == -2)
-      S.node_sum[i] = np_pairwise_walk(S.node_len[i], [&](int64_t off, int64_t len) {
-        return np_pairwise_leaf(scaled + S.node_off[i] + off, len);
-      });
+      S.node_sum[i] = np_pairwise_serial(scaled + S.node_off[i], S.node_len[i]);
   }
   __syncthreads();
+  ST(4);
   if (tid == 0) {
     for (int i = nn - 1; i >= 0; --i) {
       const int c = S.node_child[i];
@@ -166,11 +171,12 @@ __device__ __forceinline__ void per_total(const double* scaled, PerShared& S) {
 }
 
 // From scaled[0, n) and S.total: probs, numpy's cdf (sequential cumsum), the B searchsorted
-// draws and the normalised importance weights (every thread).  probs: n + B doubles.  The
-// cumsum overwrites scaled (p = probs[i] is all the weights need afterwards).
-__device__ __forceinline__ void per_draw(double* __restrict__ scaled, int n, double beta, const double* u, int B,
-                                         double* __restrict__ probs, int32_t* __restrict__ idx_out,
-                                         float* __restrict__ w_out, PerShared& S) {
+// draws and the normalised importance weights, in two calls (every thread).  probs: n + B
+// doubles.  The cumsum overwrites scaled (p = probs[i] is all the weights need afterwards).
+// (1) probs and the cdf chain: every thread divides, then thread 0 runs the chain while the
+// others are free (the caller syncs before per_pick)
+__device__ __forceinline__ void per_cdf(double* __restrict__ scaled, int n, double* __restrict__ probs,
+                                        PerShared& S) {
   const int tid = threadIdx.x, nt = blockDim.x;
   // probs = scaled / total (independent divisions)
   const double total = S.total;
@@ -199,7 +205,13 @@ __device__ __forceinline__ void per_draw(double* __restrict__ scaled, int n, dou
     }
     S.last = acc;
   }
-  __syncthreads();
+}
+
+// (2) after a barrier: searchsorted on cdf / cdf[-1] and the normalised importance weights
+__device__ __forceinline__ void per_pick(const double* __restrict__ scaled, int n, double beta, const double* u,
+                                         int B, double* __restrict__ probs, int32_t* __restrict__ idx_out,
+                                         float* __restrict__ w_out, PerShared& S) {
+  const int tid = threadIdx.x, nt = blockDim.x;
   ST(7);
   // cdf /= cdf[-1]; searchsorted(side='right'): the first i with cdf[i] / last > u, each
   // probe's quotient computed where it is needed (the same rounded value)
@@ -242,7 +254,9 @@ __device__ __noinline__ void per_sample_block(const double* __restrict__ prio, i
   if (threadIdx.x == 0) per_tree(n, S);
   __syncthreads();
   per_total(scaled, S);
-  per_draw(scaled, n, beta, u, B, cdf, idx_out, w_out, S);  // (cdf: n + B doubles)
+  per_cdf(scaled, n, cdf, S);  // (cdf: n + B doubles)
+  __syncthreads();
+  per_pick(scaled, n, beta, u, B, cdf, idx_out, w_out, S);
 }
 
 }  // namespace

@@ -163,7 +163,7 @@ def pieces(reps: int = 20, fill: int = 15):
         if hasattr(lib, "ap_debug_sample_trace"):  # AP_LIB_PATH build with -DAP_SAMPLE_TRACE
             tr = (ctypes.c_ulonglong * 16)()
             lib.ap_debug_sample_trace(tr)
-            seq = [0, 1, 2, 6, 7, 3]  # start, staged, total, probs, cumsum, draws+weights
+            seq = [0, 1, 4, 2, 6, 7, 3]  # start, staged, blocks, total, probs, cumsum, draws+weights
             out["sample_stage_cycles"] = [int(tr[seq[k + 1]] - tr[seq[k]]) for k in range(len(seq) - 1)]
         print(json.dumps({"us_per_launch_in_graph": out}))
         raise SystemExit(0)
