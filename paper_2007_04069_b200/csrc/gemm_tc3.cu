@@ -616,10 +616,13 @@ static int launch_v3_impl(const float* A, int64_t lda, int transA, const float* 
   if (!adam && splits == 1 && bn == 64 && nt % 4 == 0 && use_mc) {
     CUtensorMap maq;
     if (!make_map(&maq, A, M, K, lda, BM3 / 4)) return AP_ERR_UNSUPPORTED;
-    constexpr int SMEM = (BM3 + 64) * BK3 * 4 * 6 + 1024;
-    auto k = gemm_v3_mc_kernel<64, 6, 4>;
+    // stages in flight: the kernel is bound by the L2 -> shared-memory ingest of its operand
+    // tiles (24 KB per k slice); AP_GEMM_MC_STAGES = 6 | 8 (sweep knob)
+    const int mc_stages = std::getenv("AP_GEMM_MC_STAGES") ? std::atoi(std::getenv("AP_GEMM_MC_STAGES")) : 6;
+    const int SMEM = (BM3 + 64) * BK3 * 4 * (mc_stages == 8 ? 8 : 6) + 1024;
+    auto k = mc_stages == 8 ? gemm_v3_mc_kernel<64, 8, 4> : gemm_v3_mc_kernel<64, 6, 4>;
     static PerDeviceMax mc_configured;
-    if (mc_configured.need(current_device(), 1))
+    if (mc_configured.need(current_device(), SMEM))
       AP_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
