@@ -169,3 +169,125 @@ def test_device_loop_curve_and_chunking(cuda):
     b2 = train_partition_device(e3[1], a3[1], 30, None, None)
     assert _plan(b1) == _plan(b2)
     _assert_agents_equal(a3[0], a3[1])
+
+
+def _sample_desc(t, cap, A, eps_decay):
+    d = _native.ParityLoopDesc()
+    d.ctl, d.rng, d.r_prio, d.cap, d.num_actions = t["ctl"].data_ptr(), t["rng"].data_ptr(), t["prio"].data_ptr(), cap, A
+    d.eps_start, d.eps_final, d.eps_decay = 1.0, 0.05, eps_decay
+    d.r_scaled, d.pstat, d.per_alpha = t["scaled"].data_ptr(), t["pstat"].data_ptr(), 0.6
+    return d
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("size,train", [(64, 0), (700, 150), (1999, 1999), (2000, 400), (2000, 5000)])
+def test_early_per_sample_equals_sampling_after_the_push(cuda, size, train):
+    """ap_parity_sample in early mode (launched beside the step's act / env.step: the ring and the
+    random stream as the step starts, the act's draws replayed, the pending push counted) gives
+    the indices, weights and final stream of numpy sampling after the act's draws and the push
+    (agent.py:155-170, 197-223), and acknowledges its read; late mode (after the push) agrees."""
+    import ctypes
+
+    import torch
+
+    cap, A, B, alpha, beta = 2000, 2, 64, 0.6, 0.4
+    rng = np.random.default_rng(size + train)
+    prio = np.zeros(cap)
+    prio[:size] = rng.random(size) * 3 + 1e-6
+    slot = size % cap
+    gen = 41
+    lib = _native.require_device()
+    np_rng = np.random.default_rng(train + 1)
+    np_rng.random(3)
+    words = _rng_words(np_rng.bit_generator.state)
+    W = _native.PL
+
+    def run(early):
+        ctl = np.zeros(W["WORDS"], dtype=np.int64)
+        ctl[W["SLOT"]], ctl[W["TRAIN"]], ctl[W["GEN"]] = slot, train, gen
+        ctl[W["BUDGET"]], ctl[W["MAX_STEPS"]], ctl[W["ACTIVE"]] = 1, 10, 1
+        p = prio.copy()
+        if early:
+            ctl[W["SIZE"]] = size
+            r = words.copy()
+        else:  # the act's draws and the push already happened
+            ctl[W["SIZE"]] = min(size + 1, cap)
+            p[slot] = prio[:size].max() if size else 1.0
+            g = np.random.default_rng()
+            g.bit_generator.state = _rng_state(words.copy())
+            eps = 1.0 + (0.05 - 1.0) * min(1.0, max(0.0, train / 2000))
+            if g.random() < eps:
+                g.integers(A)
+            r = _rng_words(g.bit_generator.state)
+        t = {"ctl": torch.from_numpy(ctl).cuda(), "rng": torch.from_numpy(r).cuda(),
+             "prio": torch.from_numpy(p).cuda(), "scaled": torch.zeros(cap, dtype=torch.float64, device="cuda"),
+             "pstat": torch.zeros(2, dtype=torch.float64, device="cuda")}
+        _native.check(lib.ap_per_scaled(_native.ptr(t["prio"]), size, alpha, _native.ptr(t["scaled"]),
+                                        _native.ptr(t["pstat"]), None))
+        d = _sample_desc(t, cap, A, 2000)
+        d.early_sample = int(early)
+        scratch = torch.zeros(2 * cap + 1024, dtype=torch.float64, device="cuda")
+        idx = torch.zeros(B, dtype=torch.int32, device="cuda")
+        w = torch.zeros(B, dtype=torch.float32, device="cuda")
+        u = torch.zeros(B, dtype=torch.float64, device="cuda")
+        rng_next = torch.zeros(6, dtype=torch.int64, device="cuda")
+        _native.check(lib.ap_parity_sample(ctypes.byref(d), B, alpha, beta, _native.ptr(scratch), _native.ptr(idx),
+                                           _native.ptr(w), _native.ptr(u), _native.ptr(rng_next), int(early), None))
+        torch.cuda.synchronize()
+        final = rng_next if early else t["rng"]
+        return (idx.cpu().numpy(), w.cpu().numpy(), u.cpu().numpy(), final.cpu().numpy(),
+                t["ctl"].cpu().numpy(), p)
+
+    n = min(size + 1, cap)
+    early, late = run(True), run(False)
+    p = late[5]
+    # numpy: the act's draws, the push, then rng.choice's uniforms and searchsorted
+    g = np.random.default_rng()
+    g.bit_generator.state = _rng_state(words.copy())
+    eps = 1.0 + (0.05 - 1.0) * min(1.0, max(0.0, train / 2000))
+    if g.random() < eps:
+        g.integers(A)
+    uu = g.random(B)
+    scaled = p[:n] ** alpha
+    probs = scaled / scaled.sum()
+    cdf = probs.cumsum()
+    cdf /= cdf[-1]
+    ref_idx = cdf.searchsorted(uu, side="right")
+    ref_w = (n * probs[ref_idx]) ** (-beta)
+    ref_w /= ref_w.max()
+    for idx, w, u, final, ctl, _ in (early, late):
+        np.testing.assert_array_equal(u, uu)
+        np.testing.assert_array_equal(idx, ref_idx)
+        assert np.max(np.abs(w - ref_w) / ref_w) < 1e-6
+        assert _rng_state(final.view(np.int64)) == g.bit_generator.state
+    np.testing.assert_array_equal(early[0], late[0])
+    np.testing.assert_array_equal(early[1], late[1])
+    assert early[4][W["ACK"]] == gen + 1 and late[4][W["ACK"]] == 0
+
+
+@pytest.mark.gpu
+def test_fused_barrier_keeps_one_grid_size(cuda):
+    """A grid barrier buffer of the fused kernels counts arrivals in multiples of its grid: the
+    loop's act (which leaves an SM to the sampler) may not share one with the full-grid forward."""
+    import ctypes
+
+    import torch
+
+    from paper_2007_04069_b200.agent import QNetwork
+
+    net = QNetwork(9, 2, (32, 32), np.random.default_rng(0))
+    x = torch.zeros((1, 9), dtype=torch.float32, device="cuda")
+    net.forward_fused(x)  # full grid on the network's forward barrier
+    ws, bar = net._fused_scratch(256, True)
+    Lh, dims, w_off, b_off = net.fused_layout()[:4]
+    t = {"ctl": torch.zeros(_native.PL["WORDS"], dtype=torch.int64, device="cuda"),
+         "rng": torch.zeros(6, dtype=torch.int64, device="cuda")}
+    t["ctl"][_native.PL["BUDGET"]] = 1
+    d = _native.ParityLoopDesc()
+    d.ctl, d.rng, d.state, d.num_actions, d.early_sample = t["ctl"].data_ptr(), t["rng"].data_ptr(), x.data_ptr(), 2, 1
+    q = torch.zeros((1, 2), dtype=torch.float32, device="cuda")
+    a = torch.zeros(1, dtype=torch.int32, device="cuda")
+    lib = _native.require_device()
+    rc = lib.ap_parity_act_fused(ctypes.byref(d), Lh, dims, w_off, b_off, _native.ptr(net.flat), _native.ptr(q),
+                                 _native.ptr(ws), _native.ptr(bar), _native.ptr(a), None)
+    assert rc != 0 and "grid size" in lib.ap_last_error().decode()
