@@ -115,31 +115,6 @@ __device__ __forceinline__ void per_tree(int n, PerShared& S) {
   S.nnodes = cnt;
 }
 
-// numpy's pairwise block of 8 <= m <= 128 (shared memory): 8 accumulators, 16 loads in flight
-__device__ __forceinline__ double np_pairwise_block(const double* x, int m) {
-  if (m < 8) return np_pairwise_leaf(x, m);
-  double r[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) r[k] = x[k];
-  const int m8 = m - (m % 8);
-  int i = 8;
-  for (; i + 16 <= m8; i += 16) {
-    double v[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) v[k] = x[i + k];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) r[k] += v[k];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) r[k] += v[8 + k];
-  }
-  for (; i < m8; i += 8)
-#pragma unroll
-    for (int k = 0; k < 8; ++k) r[k] += x[i + k];
-  double v = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-  for (; i < m; ++i) v += x[i];
-  return v;
-}
-
 // a subtree past the node table's capacity, summed serially (out of line: its stack of
 // recursion frames stays out of the common path)
 __device__ __noinline__ double np_pairwise_serial(const double* x, int64_t n) {
@@ -151,12 +126,40 @@ __device__ __noinline__ double np_pairwise_serial(const double* x, int64_t n) {
 __device__ __forceinline__ void per_total(const double* scaled, PerShared& S) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int nn = S.nnodes;
-  for (int i = tid; i < nn; i += nt) {
-    const int c = S.node_child[i];
-    if (c == -1)
-      S.node_sum[i] = np_pairwise_block(scaled + S.node_off[i], S.node_len[i]);
-    else if (c == -2)
-      S.node_sum[i] = np_pairwise_serial(scaled + S.node_off[i], S.node_len[i]);
+  // Blocks of >= 8 elements: 8 lanes per block, lane k runs numpy's accumulator r[k] (x[k],
+  // x[k + 8], ... in order), then the fixed tree ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7))
+  // over shuffles and the m % 8 tail on lane 0.  (Block offsets are multiples of 8, so one lane
+  // per block would put every lane's loads on the same two banks.)
+  const int grp = tid >> 3, k = tid & 7, ngrp = nt >> 3;
+  for (int i0 = 0; i0 < nn; i0 += ngrp) {
+    const int i = i0 + grp;
+    const int c = i < nn ? S.node_child[i] : 0;
+    const int m = c == -1 ? S.node_len[i] : 0;
+    const bool big = c == -1 && m >= 8;
+    double r = 0.0;
+    const double* x = big ? scaled + S.node_off[i] : nullptr;
+    const int m8 = m - (m % 8);
+    if (big) {
+      r = x[k];
+      for (int j = 8 + k; j < m8; j += 8) r += x[j];
+    }
+    // the tree over the 8 lanes of the group (every lane of the warp takes part in the shuffles)
+    const double r1 = __shfl_xor_sync(0xffffffffu, r, 1);
+    const double p01 = (k & 1) ? r1 + r : r + r1;  // lanes 2q hold r[2q] + r[2q + 1]
+    const double p23 = __shfl_xor_sync(0xffffffffu, p01, 2);
+    const double q = (k & 2) ? p23 + p01 : p01 + p23;  // lanes 0, 4: (r0 + r1) + (r2 + r3), (r4 + r5) + (r6 + r7)
+    const double q4 = __shfl_xor_sync(0xffffffffu, q, 4);
+    if (big && k == 0) {
+      double v = q + q4;
+      for (int j = m8; j < m; ++j) v += x[j];
+      S.node_sum[i] = v;
+    }
+    if (i < nn && k == 0) {
+      if (c == -1 && m < 8)
+        S.node_sum[i] = np_pairwise_leaf(scaled + S.node_off[i], m);
+      else if (c == -2)
+        S.node_sum[i] = np_pairwise_serial(scaled + S.node_off[i], S.node_len[i]);
+    }
   }
   __syncthreads();
   ST(4);
