@@ -90,15 +90,16 @@ struct PerShared {
   int32_t node_len[kPerMaxNodes];
   int32_t node_child[kPerMaxNodes];  // left child (right = left + 1), -1 a block, -2 summed serially
   double node_sum[kPerMaxNodes];
-  int nnodes;
+  uint8_t node_depth[kPerMaxNodes];
+  int nnodes, max_depth;
   double total, last, wmax;
   double wred[32];
 };
 
 // The recursion's nodes for n elements, breadth first (children after their parent).  One thread.
 __device__ __forceinline__ void per_tree(int n, PerShared& S) {
-  int cnt = 1;
-  S.node_off[0] = 0, S.node_len[0] = n;
+  int cnt = 1, dmax = 0;
+  S.node_off[0] = 0, S.node_len[0] = n, S.node_depth[0] = 0;
   for (int i = 0; i < cnt; ++i) {
     const int len = S.node_len[i];
     if (len <= 128 || cnt + 2 > kPerMaxNodes) {
@@ -107,12 +108,15 @@ __device__ __forceinline__ void per_tree(int n, PerShared& S) {
     }
     int n2 = len / 2;
     n2 -= n2 % 8;
+    const int d = S.node_depth[i] + 1;
+    dmax = d > dmax ? d : dmax;
     S.node_child[i] = cnt;
-    S.node_off[cnt] = S.node_off[i], S.node_len[cnt] = n2;
-    S.node_off[cnt + 1] = S.node_off[i] + n2, S.node_len[cnt + 1] = len - n2;
+    S.node_off[cnt] = S.node_off[i], S.node_len[cnt] = n2, S.node_depth[cnt] = (uint8_t)d;
+    S.node_off[cnt + 1] = S.node_off[i] + n2, S.node_len[cnt + 1] = len - n2, S.node_depth[cnt + 1] = (uint8_t)d;
     cnt += 2;
   }
   S.nnodes = cnt;
+  S.max_depth = dmax;
 }
 
 // a subtree past the node table's capacity, summed serially (out of line: its stack of
@@ -122,7 +126,7 @@ __device__ __noinline__ double np_pairwise_serial(const double* x, int64_t n) {
 }
 
 // total = numpy's pairwise sum of scaled[0, n) over the tree of per_tree (every thread; the
-// block sums in parallel, then thread 0 adds the nodes children first).  Ends with a barrier.
+// block sums in parallel, then the internal nodes level by level).  Ends with a barrier.
 __device__ __forceinline__ void per_total(const double* scaled, PerShared& S) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int nn = S.nnodes;
@@ -163,13 +167,15 @@ __device__ __forceinline__ void per_total(const double* scaled, PerShared& S) {
   }
   __syncthreads();
   ST(4);
-  if (tid == 0) {
-    for (int i = nn - 1; i >= 0; --i) {
+  // internal nodes level by level, deepest first (one thread per node; ~log2(n / 64) levels)
+  for (int d = S.max_depth - 1; d >= 0; --d) {
+    for (int i = tid; i < nn; i += nt) {
       const int c = S.node_child[i];
-      if (c >= 0) S.node_sum[i] = S.node_sum[c] + S.node_sum[c + 1];
+      if (c >= 0 && S.node_depth[i] == d) S.node_sum[i] = S.node_sum[c] + S.node_sum[c + 1];
     }
-    S.total = S.node_sum[0];
+    __syncthreads();
   }
+  if (tid == 0) S.total = S.node_sum[0];
   __syncthreads();
 }
 
@@ -223,10 +229,15 @@ __device__ __forceinline__ void per_pick(const double* __restrict__ scaled, int 
   double wloc = 0.0;
   for (int b = tid; b < B; b += nt) {
     const double ub = u[b];
+    // fl(c / last) <= u is decided by c against u * last with a 2^-48 relative margin (far wider
+    // than the 2^-53 rounding of either side); only a c inside the margin pays the division
+    const double ul = ub * last, mg = ul * 0x1p-48, lo_t = ul - mg, hi_t = ul + mg;
     int lo = 0, hi = n;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if (cdf[mid] / last <= ub)
+      const double c = cdf[mid];
+      const bool le = c <= lo_t ? true : (c >= hi_t ? false : c / last <= ub);
+      if (le)
         lo = mid + 1;
       else
         hi = mid;
