@@ -569,7 +569,7 @@ __device__ __forceinline__ float adv_mean(const float* z, int A) {
 
 // head outputs of R rows (rows hr[r], weights wh[r] / bh[r]) into registers of every lane,
 // in head_row's summation order; the loads of 4 k-steps are issued together
-template <int A1M, int R>
+template <int A1M, int R, int U = 4>
 __device__ __forceinline__ void head_regs_(const float* const* hr, int H, int A1, const float* const* wh,
                                           const float* const* bh, float (*z)[A1M]) {
   const int lane = threadIdx.x & 31;
@@ -577,7 +577,6 @@ __device__ __forceinline__ void head_regs_(const float* const* hr, int H, int A1
   for (int r = 0; r < R; ++r)
 #pragma unroll
     for (int j = 0; j < A1M; ++j) z[r][j] = 0.0f;
-  constexpr int U = 4;
   for (int k0 = 0; k0 < H; k0 += U * 32) {
     float x[R][U], w[R][U][A1M];
 #pragma unroll
@@ -667,6 +666,21 @@ __device__ __noinline__ void small_head_row(const Learn& P, int r, int B, const 
   const float* hr[3] = {HonL + (int64_t)b * H, HonL + (int64_t)(B + b) * H, HtgL + (int64_t)b * H};
   const float* wh[3] = {w_on, w_on, P.tp + P.w_off[L]};
   const float* bh[3] = {b_on, b_on, P.tp + P.b_off[L]};
+  // the head dgrad's operands (below) for H <= 256, loaded before the head math: they do not
+  // depend on it, and issued here their round trip overlaps the head's
+  constexpr int DU = 8;
+  const bool dh_pre = A1M <= 3 && H <= 32 * DU;
+  const float* hc = HonL + (int64_t)(B + b) * H;
+  float dwv[DU][A1M], dhv[DU];
+  if (dh_pre) {
+#pragma unroll
+    for (int u = 0; u < DU; ++u) {
+      const int n = u * 32 + lane;
+      dhv[u] = n < H ? __ldcg(hc + n) : 0.0f;
+#pragma unroll
+      for (int k = 0; k < A1M; ++k) dwv[u][k] = (n < H && k < A1) ? __ldcg(w_on + (int64_t)n * A1 + k) : 0.0f;
+    }
+  }
   float z[3][A1M];  // online next, online cur, target next
   head_regs_<A1M, 3>(hr, H, A1, wh, bh, z);
   float mn = 0.0f, mc = 0.0f, mt = 0.0f;
@@ -704,12 +718,23 @@ __device__ __noinline__ void small_head_row(const Learn& P, int r, int B, const 
     float dzk[A1M];
 #pragma unroll
     for (int k = 0; k < A1M; ++k) dzk[k] = k == 0 ? g : ((k - 1) == a ? g : 0.0f) - g / (float)A;
-    const float* hc = HonL + (int64_t)(B + b) * H;
     float* out = dhL + (int64_t)b * H;
+    if (dh_pre) {
+#pragma unroll
+      for (int u = 0; u < DU; ++u) {
+        const int n = u * 32 + lane;
+        float acc = 0.0f;
+#pragma unroll
+        for (int k = 0; k < A1M; ++k)
+          if (k < A1) acc = fmaf(dzk[k], dwv[u][k], acc);
+        const float v = acc + 0.0f;
+        if (n < H) out[n] = dhv[u] > 0.0f ? v : 0.0f;
+      }
+    }
     // 8 columns per lane at a time, every load of the block issued before its first use (the
     // stores of one block could alias the next block's loads for the compiler)
     constexpr int U = 8;
-    for (int n0 = 0; n0 < H; n0 += 32 * U) {
+    for (int n0 = 0; n0 < (dh_pre ? 0 : H); n0 += 32 * U) {
       float wv[U][A1M], hv[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
