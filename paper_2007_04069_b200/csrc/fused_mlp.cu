@@ -1056,6 +1056,22 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_fused_kernel(const __grid_con
       if (blockIdx.x == 0 && threadIdx.x == 0) P.pl.ctl[AP_PL_ACTIVE] = 0;
       return;
     }
+    // an exploring step needs no Q (agent.py:166-168: the random() draw decides first), so every
+    // CTA replays that draw and, when it explores, only CTA 0 stays to take the step's action
+    uint64_t w6[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) w6[k] = P.pl.rng[k];
+    NpPcg64 g = NpPcg64::load(w6);
+    if (g.next_double() < epsilon_at(P.pl.ctl[AP_CTL_TRAIN], P.pl.eps_start, P.pl.eps_final, P.pl.eps_decay)) {
+      if (blockIdx.x != 0) return;
+      parity_act_rows(P.pl);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        parity_step_begin(P.pl, false, true);
+        parity_act_decide(P.pl, P.q_out, P.action);
+      }
+      return;
+    }
   }
   // this learn step's train counter, read by every CTA before the first grid barrier (CTA 0
   // advances it at the end, in parity-tail mode)
