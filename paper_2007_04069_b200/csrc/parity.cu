@@ -7,16 +7,18 @@
 // -1 on CONFLICT, next position in the linkage order), agent.observe (push with
 // the current max priority, agent.py:197-205) and agent.learn (PER sample from
 // 64 more random() draws, double-DQN update, Adam, priorities, target sync every
-// 100 train steps, agent.py:207-337).  Here every one of those runs on the GPU:
+// 100 train steps, agent.py:207-337).  Here every one of those runs on the GPU.  With the
+// fused learner (devloop.py) one step of the loop body is
 //
-//   step graph   forward(state) -> parity_act -> K1 (one row) -> parity_post
-//   learn graph  uniforms -> PER sample -> gathers -> 3 forwards -> TD ->
-//                backward -> Adam (bias corrections from a host table) ->
-//                transposed copies -> priorities -> learn_tail -> target sync
+//   ap_parity_sample (early mode) ----------------------------------------.
+//   ap_parity_act_fused -> K1 (one row) -> ap_parity_post ----------------+-> ap_dqn_learn_fused
 //
-// and a CUDA graph with device-side control flow loops over them: a WHILE node
-// (episodes done < budget) whose body is the step graph, a kernel that sets an
-// IF condition (ring size >= batch) and the IF node holding the learn graph.
+// (the sampler replays the act's draws and counts the pending push, so it runs beside the env
+// kernels; the act skips its forward on exploring steps; the learn kernel keeps the loss log,
+// train counter, target sync and the PER caches), 8 such steps form the body of a WHILE node
+// (episodes done < budget).  With the tensor-core GEMM learner the body is the step graph
+// forward -> ap_parity_act -> K1 -> ap_parity_post and an IF (ring >= batch) node holding
+// sample (late mode) -> learn GEMMs -> ap_parity_learn_tail -> ap_parity_target_sync.
 // Nothing returns to the host until the episode budget is spent.  The random
 // stream is numpy's own (pcg64.cuh), so draws, actions, rewards, states and the
 // chosen plan are those of the host-driven loop bit for bit
