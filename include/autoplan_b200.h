@@ -692,7 +692,7 @@ typedef struct ap_fused_learn {
   float* td;                /* [batch] */
   float* loss;              /* [1] sum_b w_b huber(td_b) */
   float* workspace;         /* ap_mlp_fused_workspace(L, dims, batch, 0) floats */
-  uint32_t* barrier;        /* [2] zero-initialised, private to the caller's stream */
+  uint32_t* barrier;        /* [4] zero-initialised, private to the caller's stream */
   uint64_t* trace;          /* optional [16]: %globaltimer after each phase (profiling) */
   int64_t gate;             /* > 0 (with ctl): no-op while ctl[AP_CTL_SIZE] < gate */
   /* optional parity-loop tail (replaces ap_parity_learn_tail + ap_parity_target_sync):

@@ -296,7 +296,7 @@ class QNetwork:
         key = "_fws_f" if forward_only else "_fws_l"
         ws = self.__dict__.get(key)
         if ws is None or ws[0].numel() < need:
-            ws = (torch.empty(need, dtype=torch.float32, device="cuda"), torch.zeros(2, dtype=torch.int32, device="cuda"))
+            ws = (torch.empty(need, dtype=torch.float32, device="cuda"), torch.zeros(4, dtype=torch.int32, device="cuda"))
             self.__dict__[key] = ws
         return ws
 

@@ -30,8 +30,6 @@
 // gives Q for a few rows (the act of the search loop).
 #include <algorithm>
 #include <cstdint>
-#include <mutex>
-#include <unordered_map>
 
 #include "engine.h"
 #include "parity_act.cuh"
@@ -88,8 +86,8 @@ __device__ __forceinline__ void trace_arrive(unsigned long long* tr, int k) {
 }
 
 // grid-wide barrier (all CTAs co-resident: cooperative launch).  bar[0] counts arrivals
-// monotonically (it stays a multiple of the grid size between launches, so one barrier buffer
-// must always see the same grid size: launch() enforces it): one release add per CTA, then
+// monotonically (it stays a multiple of the grid size between launches: the phases using it
+// always run on the full grid; see grid_sync_any for the few-row forward): one release add per CTA, then
 // relaxed loads until the count reaches the next multiple.  The CTA barrier before the add
 // orders every thread's writes before thread 0's release (cumulativity).
 __device__ __forceinline__ void grid_sync(unsigned* bar) {
@@ -105,6 +103,33 @@ __device__ __forceinline__ void grid_sync(unsigned* bar) {
     do {
       asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
     } while ((int)(cur - target) < 0);
+  }
+  __syncthreads();
+}
+
+// Grid barrier for launches whose grid size may change from one launch to the next (the few-row
+// forward: the act of the search loop leaves an SM to the PER sampler, the host act does not),
+// on words 2-3 of the barrier buffer: bar[2] counts this round's arrivals, bar[3] is the round's
+// generation.  Thread 0 reads the generation, arrives (acq_rel: its CTA's writes are released,
+// the generation read stays before the arrival); the last arriver resets the count and releases
+// the next generation, the others poll for it.
+__device__ __forceinline__ void grid_sync_any(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned* cnt = bar + 2;
+    unsigned* gen = bar + 3;
+    unsigned g, old;
+    asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(g) : "l"(gen) : "memory");
+    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
+    if (old == gridDim.x - 1) {
+      asm volatile("st.relaxed.gpu.u32 [%0], %1;" ::"l"(cnt), "r"(0u) : "memory");
+      asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(gen), "r"(g + 1) : "memory");
+    } else {
+      unsigned cur;
+      do {
+        asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(gen) : "memory");
+      } while (cur == g);
+    }
   }
   __syncthreads();
 }
@@ -850,7 +875,7 @@ __device__ __noinline__ void small_forward(const Learn& P, float* smem) {
       }
       __syncthreads();
     }
-    grid_sync(P.bar);
+    grid_sync_any(P.bar);
     part_prev = part;
     ks_prev = sp.ks;
     off += (int64_t)sp.ks * R * N;
@@ -1317,25 +1342,10 @@ int64_t workspace_floats(int L, const int* d, int B, bool fwd_only) {
   return n;
 }
 
-// grid size each barrier buffer has been used with (grid_sync's counter assumes one size)
-std::mutex g_bar_mu;
-std::unordered_map<const void*, int> g_bar_grid;
-
 int launch(const Learn& P, cudaStream_t stream, int reserve_sms = 0) {
   int sms = 0;
   if (int rc = current_sm_count(&sms)) return rc;
   sms = std::max(1, sms - reserve_sms);
-  {
-    std::lock_guard<std::mutex> lk(g_bar_mu);
-    auto it = g_bar_grid.find(P.bar);
-    if (it == g_bar_grid.end()) {
-      g_bar_grid.emplace(P.bar, sms);
-    } else if (it->second != sms) {
-      set_error("fused kernels: this barrier buffer was used with another grid size (the act of a "
-                "loop with an early PER sample leaves one SM free: give it its own barrier)");
-      return AP_ERR_INVALID;
-    }
-  }
   static PerDeviceMax configured;
   const int smem = kSmemFloats * 4 + 64;
   if (configured.need(current_device(), smem))

@@ -94,7 +94,7 @@ class DeviceSearch:
             "state": torch.zeros((1, env.state_dim), dtype=f32, device=dev),
             "action": torch.zeros(1, dtype=i32, device=dev),
             "q": torch.zeros((1, A), dtype=f32, device=dev),
-            "act_bar": torch.zeros(2, dtype=i32, device=dev),
+            "act_bar": torch.zeros(4, dtype=i32, device=dev),
             "best_row": torch.full((self.ld,), -1, dtype=i8, device=dev),
             "log_action": torch.zeros(steps_per_launch, dtype=i32, device=dev),
             "log_reward": torch.zeros(steps_per_launch, dtype=f64, device=dev),
@@ -146,8 +146,7 @@ class DeviceSearch:
             # it also closes the step once the budget is spent (the body runs several steps)
             Lh, dims, w_off, b_off = net.fused_layout()[:4]
             ws = net._fused_scratch(256, True)[0]
-            # own grid barrier: this launch leaves an SM to the sampler (a smaller grid than the
-            # host act's forward, which must not share a barrier counter with it)
+            # (its grid leaves an SM to the sampler; the few-row forward's barrier allows any grid)
             _native.check(lib.ap_parity_act_fused(L, Lh, dims, w_off, b_off, _native.ptr(net.flat),
                                                   _native.ptr(t["q"]), _native.ptr(ws), _native.ptr(t["act_bar"]),
                                                   _native.ptr(t["action"]), _stream()))
@@ -275,6 +274,13 @@ class DeviceSearch:
         pdl = os.environ.get("AP_NO_PDL")
         if not self.gated:
             os.environ["AP_NO_PDL"] = "1"  # plain edges inside the IF node's body
+        import gc
+
+        # no garbage collection inside the captures: a collected DeviceSearch of an earlier call
+        # would destroy its CUDA graphs in the middle of this stream capture
+        gc.collect()
+        gc_was = gc.isenabled()
+        gc.disable()
         try:
             with torch.cuda.stream(self.stream):
                 self._warm()
@@ -296,6 +302,8 @@ class DeviceSearch:
                     with torch.cuda.graph(self.g_learn, stream=self.stream):
                         self._learn_body()
         finally:
+            if gc_was:
+                gc.enable()
             if pdl is None:
                 os.environ.pop("AP_NO_PDL", None)
             else:

@@ -171,6 +171,21 @@ def test_device_loop_curve_and_chunking(cuda):
     _assert_agents_equal(a3[0], a3[1])
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("per_iter", [1, 3])
+def test_device_loop_steps_per_iteration(cuda, monkeypatch, per_iter):
+    """A WHILE iteration of 1 or 3 steps (the act closes the steps past the budget, the later
+    kernels of the body skip) gives the default body's results."""
+    from paper_2007_04069_b200 import devloop
+
+    (e1, e2), (a1, a2) = _agent_pair(_env_factory("mlp2", "opp"), 3, 0.0005, 300)
+    b_default = devloop.train_partition_device(e1, a1, 60, None, None)
+    monkeypatch.setattr(devloop, "_STEPS_PER_ITER", per_iter)
+    b_other = devloop.train_partition_device(e2, a2, 60, None, None)
+    assert _plan(b_default) == _plan(b_other)
+    _assert_agents_equal(a1, a2)
+
+
 def _sample_desc(t, cap, A, eps_decay):
     d = _native.ParityLoopDesc()
     d.ctl, d.rng, d.r_prio, d.cap, d.num_actions = t["ctl"].data_ptr(), t["rng"].data_ptr(), t["prio"].data_ptr(), cap, A
@@ -266,9 +281,10 @@ def test_early_per_sample_equals_sampling_after_the_push(cuda, size, train):
 
 
 @pytest.mark.gpu
-def test_fused_barrier_keeps_one_grid_size(cuda):
-    """A grid barrier buffer of the fused kernels counts arrivals in multiples of its grid: the
-    loop's act (which leaves an SM to the sampler) may not share one with the full-grid forward."""
+def test_act_forward_any_grid_on_one_barrier(cuda):
+    """The few-row forward's grid barrier allows a different grid from launch to launch on the
+    same buffer: the full-grid host forward, then the loop's act (one SM left to the sampler),
+    then the host forward again give the same Q."""
     import ctypes
 
     import torch
@@ -276,18 +292,34 @@ def test_fused_barrier_keeps_one_grid_size(cuda):
     from paper_2007_04069_b200.agent import QNetwork
 
     net = QNetwork(9, 2, (32, 32), np.random.default_rng(0))
-    x = torch.zeros((1, 9), dtype=torch.float32, device="cuda")
-    net.forward_fused(x)  # full grid on the network's forward barrier
+    x = torch.randn((1, 9), dtype=torch.float32, device="cuda")
+    q0 = net.forward_fused(x).clone()  # full grid on the network's forward barrier
     ws, bar = net._fused_scratch(256, True)
     Lh, dims, w_off, b_off = net.fused_layout()[:4]
     t = {"ctl": torch.zeros(_native.PL["WORDS"], dtype=torch.int64, device="cuda"),
          "rng": torch.zeros(6, dtype=torch.int64, device="cuda")}
     t["ctl"][_native.PL["BUDGET"]] = 1
+    t["ctl"][_native.PL["MAX_STEPS"]] = 1
+    t["ctl"][_native.PL["TRAIN"]] = 10 ** 6  # past the decay: epsilon 0.05, a greedy draw below
+    t["ctl"][_native.PL["ACK"]] = 1  # as if the step's sampler had read the stream (GEN 0)
+    g = np.random.default_rng(5)
+    t["rng"].copy_(torch.from_numpy(_rng_words(g.bit_generator.state)))
+    seeds = torch.full((16,), -1, dtype=torch.int8, device="cuda")
+    seeds_try = seeds.clone()
+    log = torch.zeros(4, dtype=torch.int32, device="cuda")
     d = _native.ParityLoopDesc()
-    d.ctl, d.rng, d.state, d.num_actions, d.early_sample = t["ctl"].data_ptr(), t["rng"].data_ptr(), x.data_ptr(), 2, 1
+    d.ctl, d.rng, d.state, d.num_actions, d.ld = t["ctl"].data_ptr(), t["rng"].data_ptr(), x.data_ptr(), 2, 16
+    d.seeds, d.seeds_try, d.decided = seeds.data_ptr(), seeds_try.data_ptr(), seeds.data_ptr()
+    d.log_action, d.log_pos = log.data_ptr(), log.data_ptr()
+    d.eps_start, d.eps_final, d.eps_decay = 1.0, 0.05, 100
+    d.early_sample = 1  # the loop's act: one SM left free, a smaller grid
     q = torch.zeros((1, 2), dtype=torch.float32, device="cuda")
     a = torch.zeros(1, dtype=torch.int32, device="cuda")
     lib = _native.require_device()
-    rc = lib.ap_parity_act_fused(ctypes.byref(d), Lh, dims, w_off, b_off, _native.ptr(net.flat), _native.ptr(q),
-                                 _native.ptr(ws), _native.ptr(bar), _native.ptr(a), None)
-    assert rc != 0 and "grid size" in lib.ap_last_error().decode()
+    _native.check(lib.ap_parity_act_fused(ctypes.byref(d), Lh, dims, w_off, b_off, _native.ptr(net.flat),
+                                          _native.ptr(q), _native.ptr(ws), _native.ptr(bar), _native.ptr(a), None))
+    q2 = net.forward_fused(x)
+    torch.cuda.synchronize()
+    if g.random() >= 0.05:  # the act exploited: it computed Q on the smaller grid
+        assert torch.equal(q, q0)
+    assert torch.equal(q2, q0)
