@@ -85,9 +85,10 @@ __device__ __forceinline__ void trace_arrive(unsigned long long* tr, int k) {
   }
 }
 
-// grid-wide barrier (all CTAs co-resident: cooperative launch).  bar[0] counts arrivals
-// monotonically (it stays a multiple of the grid size between launches: the phases using it
-// always run on the full grid; see grid_sync_any for the few-row forward): one release add per CTA, then
+// grid-wide barrier (all CTAs co-resident: cooperative launch).  The counter word counts arrivals
+// monotonically (it stays a multiple of the grid size between launches, so each word of the
+// barrier buffer serves one grid size: word 0 the full-grid phases, words 2 / 3 the few-row
+// forward on the full grid / with one SM left free): one release add per CTA, then
 // relaxed loads until the count reaches the next multiple.  The CTA barrier before the add
 // orders every thread's writes before thread 0's release (cumulativity).
 __device__ __forceinline__ void grid_sync(unsigned* bar) {
@@ -103,33 +104,6 @@ __device__ __forceinline__ void grid_sync(unsigned* bar) {
     do {
       asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
     } while ((int)(cur - target) < 0);
-  }
-  __syncthreads();
-}
-
-// Grid barrier for launches whose grid size may change from one launch to the next (the few-row
-// forward: the act of the search loop leaves an SM to the PER sampler, the host act does not),
-// on words 2-3 of the barrier buffer: bar[2] counts this round's arrivals, bar[3] is the round's
-// generation.  Thread 0 reads the generation, arrives (acq_rel: its CTA's writes are released,
-// the generation read stays before the arrival); the last arriver resets the count and releases
-// the next generation, the others poll for it.
-__device__ __forceinline__ void grid_sync_any(unsigned* bar) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned* cnt = bar + 2;
-    unsigned* gen = bar + 3;
-    unsigned g, old;
-    asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(g) : "l"(gen) : "memory");
-    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
-    if (old == gridDim.x - 1) {
-      asm volatile("st.relaxed.gpu.u32 [%0], %1;" ::"l"(cnt), "r"(0u) : "memory");
-      asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(gen), "r"(g + 1) : "memory");
-    } else {
-      unsigned cur;
-      do {
-        asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(cur) : "l"(gen) : "memory");
-      } while (cur == g);
-    }
   }
   __syncthreads();
 }
@@ -252,6 +226,7 @@ struct Learn {
   float* sync_dst[6];
   int64_t sync_count[6];
   int lazy_wt0;              // the first layer's transposed copy is refreshed by the caller
+  int reserve;               // SMs the launch leaves free (the few-row forward's barrier word)
   double* r_scaled;          // optional: priorities ** alpha, updated with each priority
   double* pstat;             // with r_scaled: the ring's max priority after the update, its ** alpha
   double alpha;
@@ -875,7 +850,7 @@ __device__ __noinline__ void small_forward(const Learn& P, float* smem) {
       }
       __syncthreads();
     }
-    grid_sync_any(P.bar);
+    grid_sync(P.bar + 2 + P.reserve);  // one counter word per grid size
     part_prev = part;
     ks_prev = sp.ks;
     off += (int64_t)sp.ks * R * N;
@@ -1432,7 +1407,8 @@ int ap_parity_act_fused(const ap_parity_loop* pl, int32_t L, const int32_t* dims
   P.pl = *pl;
   P.action = action;
   // early PER sample: one SM stays free for the sampler the act's decision waits for
-  return launch(P, (cudaStream_t)stream, pl->early_sample ? 1 : 0);
+  P.reserve = pl->early_sample ? 1 : 0;
+  return launch(P, (cudaStream_t)stream, P.reserve);
 }
 
 int ap_dqn_learn_fused(const ap_fused_learn* a, void* stream) {
