@@ -116,6 +116,8 @@ def bench_config(name, g, dims, order_src, plan_batch="prefix"):
         "candidate_dims": len(dims),
         "plan_batch": desc,
         "decision_order": order_src,
+        "conflict_rows": "outcome + counts as the reference; slot rows hold the closure with P winning "
+                         "(the reference's mid-sweep snapshot of a CONFLICT comes from ap_propagate_trace)",
         "l2": "inputs larger than L2 (seeds + slot outputs per step >> 126 MB)",
     }
 
